@@ -1,0 +1,223 @@
+/*
+ * fde.h -- C-ABI of the B200-native hot path of arXiv 1808.02937
+ * ("H-matrix preconditioned SEM solver for the 1-D two-sided Riemann-Liouville
+ * fractional diffusion equation").  Library: paper_1808_02937_b200/libfde.so.
+ *
+ * Problem (Eq. (Model)):
+ *   -D^2( theta aI_x^{2-alpha} u + (1-theta) xI_b^{2-alpha} u ) + rho u = f on (a,b),
+ *   u(a) = c1, u(b) = c2,  1 < alpha < 2, 0 <= theta <= 1, rho >= 0.
+ * Discretisation: spectral elements on the partition
+ * a = x_0 < ... < x_N = b with N-1 nodal hats and P-1 modal functions
+ * psi_p = L_{p-1} - L_{p+1} per element; n = N*P - 1 unknowns.
+ *
+ * Conventions shared by every entry point
+ *  - Vectors at this boundary are in the paper's X ordering:
+ *      [u^1_1..u^{P-1}_1; ...; u^1_N..u^{P-1}_N; u~_1..u~_{N-1}].
+ *    Multi-RHS blocks are column-major with leading dimension `ld` (>= n).
+ *  - Vector pointers are DEVICE pointers owned by the caller (e.g. torch
+ *    tensors); the library never frees them.  Host pointers are marked (host).
+ *  - Every call is ordered on the handle's CUDA stream; nothing synchronises
+ *    the host except solve (returns after convergence) and calls that
+ *    return host data.
+ *  - Opaque objects are created by the library and released with the
+ *    matching fde_free_* call.  Mesh nodes are copied.
+ *  - Return value: FDE_OK (0) or a negative FDE_E* code; fde_last_error()
+ *    gives the message.  No entry point falls back to the CPU: without a
+ *    usable CUDA device fde_create returns FDE_ECUDA.
+ */
+#ifndef FDE_H
+#define FDE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ------------------------------------------------------------ error codes */
+enum {
+    FDE_OK = 0,
+    FDE_EINVAL_DOMAIN = -1,      /* a >= b                                          */
+    FDE_EINVAL_SIZE = -2,        /* N < 1, nrhs < 1, ld < n                          */
+    FDE_EINVAL_PARAM = -3,       /* alpha not in (1,2), theta not in [0,1], rho < 0,
+                                    R < 1, lambda <= 0, n_min < 1, tol < 0           */
+    FDE_EINVAL_MESH = -4,        /* nodes not strictly increasing / ends != a,b      */
+    FDE_EDEGREE = -5,            /* P < 1 or P > FDE_MAX_P                           */
+    FDE_EUNSUPPORTED_MESH = -6,  /* Toeplitz path requested on a non-uniform mesh    */
+    FDE_EDIM = -7,               /* objects of different problems mixed              */
+    FDE_ESINGULAR_PIVOT = -8,    /* zero/NaN pivot in an H-LU leaf                   */
+    FDE_EBREAKDOWN = -9,         /* Krylov breakdown                                 */
+    FDE_EMAXITER = -10,          /* Krylov did not converge within maxiter           */
+    FDE_ECUDA = -11,
+    FDE_ENCCL = -12,
+    FDE_ENOMEM = -13,
+    FDE_ERANK = -14              /* a low-rank block exceeded its rank capacity      */
+};
+
+#define FDE_MAX_P 32
+
+/* ------------------------------------------------------------- problem */
+typedef struct {
+    double a, b;          /* interval                       */
+    double alpha;         /* 1 < alpha < 2                                 */
+    double theta;         /* 0 <= theta <= 1                               */
+    double rho;           /* reaction coefficient >= 0                     */
+    double c1, c2;        /* Dirichlet data u(a)=c1, u(b)=c2               */
+} fde_problem;
+
+enum { FDE_MESH_CUSTOM = 0, FDE_MESH_UNIFORM = 1 };
+
+typedef struct {
+    int32_t N;              /* elements                                      */
+    const double* nodes;    /* (host) N+1 strictly increasing, [0]=a, [N]=b  */
+    int32_t P;              /* uniform polynomial degree, 1 <= P <= FDE_MAX_P */
+    int32_t kind;           /* FDE_MESH_*; UNIFORM is verified, not trusted  */
+} fde_mesh;
+
+/* Forcing f(x) = sum_k leg[k] L_k(2(x-a)/(b-a)-1)
+ *             + sum_t coef[t] (x-a)^power[t]  (side[t]==0)
+ *             + sum_t coef[t] (b-x)^power[t]  (side[t]==1).   All host arrays. */
+typedef struct {
+    int32_t nleg;  const double* leg;
+    int32_t nterm; const int32_t* side; const double* power; const double* coef;
+} fde_forcing;
+
+typedef struct fde_ctx* fde_handle;
+typedef struct fde_op* fde_operator;
+typedef struct fde_hm* fde_hmatrix;
+typedef struct fde_lu* fde_hlu;
+
+/* ------------------------------------------------------------- context */
+/* device: CUDA ordinal; cuda_stream: cudaStream_t to order work on (NULL =
+ * a library-owned stream); nccl_unique_id: 128-byte ncclUniqueId shared by all
+ * ranks (NULL => world must be 1); rank/world: this process in the job. */
+int fde_create(fde_handle* out, int device, void* cuda_stream, const void* nccl_unique_id,
+               int rank, int world);
+void fde_destroy(fde_handle h);
+const char* fde_last_error(fde_handle h);
+int fde_sync(fde_handle h);                   /* cudaStreamSynchronize(stream)    */
+int fde_nccl_unique_id(void* out128);          /* ncclGetUniqueId, for rank 0     */
+
+/* --------------------------------------------------------- sem_assemble */
+enum { FDE_OP_DENSE = 1, FDE_OP_TOEPLITZ = 2 };
+
+/* Builds the operator A = rho M + theta S_l + (1-theta) S_l^T of Eq. (lsys)
+ * on the device.  FDE_OP_DENSE stores this rank's row shard
+ * of the dense fp64 matrix (element-interleaved internal order, row-major);
+ * FDE_OP_TOEPLITZ (uniform meshes only) stores the P x P block-Toeplitz lag
+ * symbols and their 2N-point circulant spectra.  Both may be
+ * requested together.  Entries are computed by Gauss quadrature of the pair
+ * moments K_ij[m][n] = gamma0 int int L_m L_n (t-s)_+^{1-alpha} with
+ * Gauss-Jacobi / Duffy treatment of the diagonal and touching pairs and graded
+ * composite rules on near pairs. */
+int sem_assemble(fde_handle h, const fde_problem* prob, const fde_mesh* mesh, int flags,
+                 fde_operator* out);
+
+typedef struct {
+    int64_t n;            /* unknowns NP-1                                      */
+    int32_t N, P;
+    int64_t row_begin, row_end;   /* this rank's rows (internal order)          */
+    int64_t lda;          /* leading dimension of the dense shard               */
+    int32_t flags;
+    int32_t uniform;      /* mesh verified uniform                               */
+    double assemble_ms;   /* device time of the last assembly                    */
+} fde_operator_info;
+int fde_operator_get_info(fde_operator op, fde_operator_info* info);
+
+/* Copy the dense operator rows [r0,r1) x all columns, PAPER order, into the
+ * device buffer out (row-major, ldo >= n).  World==1 only (test helper). */
+int fde_operator_dense_paper(fde_handle h, fde_operator op, double* out, int64_t ldo);
+/* Columns of the boundary hats (node 0, node N) of the full operator, length n
+ * each, paper order, into device buffer out[2*n] (used for the lifting). */
+int fde_operator_boundary_columns(fde_handle h, fde_operator op, double* out);
+
+/* -------------------------------------------------------------- sem_rhs */
+/* G[:, r] = (f_r, phi_I) - A[:, {0,N}] [c1, c2]  (lifting
+ * by the boundary hats).  f: host array of nrhs forcings; G device, paper
+ * order, column-major ld. */
+int sem_rhs(fde_handle h, fde_operator op, const fde_forcing* f, int nrhs, double* G, int64_t ld);
+
+/* ----------------------------------------------------- stiffness_matvec */
+enum { FDE_PATH_AUTO = 0, FDE_PATH_DENSE = 1, FDE_PATH_TOEPLITZ = 2 };
+/* y = A x for nrhs columns (PAPER.md:629 dense O(N_d^2); PAPER.md:632-735 FFT on
+ * uniform meshes).  x, y device, paper order, full length n on every rank;
+ * with world > 1 the dense path multiplies the local row shard and all-gathers
+ * y over NCCL. */
+int stiffness_matvec(fde_handle h, fde_operator op, const double* x, double* y, int nrhs,
+                     int64_t ld, int path);
+
+/* -------------------------------------------------------- hmatrix_build */
+/* H-matrix H ~ S_l on the element-cluster block tree with admissibility
+ * max(diam) <= lambda dist (Eq. (admis)), Taylor factors of rank
+ * R (Lemma 3.2; Q,W, Qbar, Wbar of PAPER.md:365-388) on
+ * admissible leaves, exact entries on inadmissible leaves,
+ * and the preconditioner operator A~ = rho M + theta H + (1-theta) H^T
+ * (Eq. (approxsys), reading A2).  Replicated on every rank. */
+int hmatrix_build(fde_handle h, fde_operator op, int R, double lambda, int n_min, fde_hmatrix* out);
+
+typedef struct {
+    int32_t nblocks_dense, nblocks_lr, depth, nclusters;
+    int64_t dense_entries, lr_entries;   /* stored fp64 words              */
+    double build_ms;
+} fde_hmatrix_info;
+int fde_hmatrix_get_info(fde_hmatrix hm, fde_hmatrix_info* info);
+/* Expand A~ into a dense n x n matrix, paper order, column-major with ldo >= n,
+ * device buffer (test / diagnostics helper; O(n^2) memory). */
+int fde_hmatrix_dense_paper(fde_handle h, fde_hmatrix hm, double* out, int64_t ldo);
+
+/* ----------------------------------------------------------- hlu_factor */
+/* A~ ~= L_H U_H, L_H unit lower, both in H format on the same block tree
+ * (Fig. fig:HLU); formatted arithmetic with per-block
+ * truncation sigma_i <= tol sigma_1 (reading A12); tol = 0 keeps every rank
+ * (exact up to rounding; rank capacity permitting).  No pivoting
+ * (coercivity, Theorem 2.1).  Does not modify hm. */
+int hlu_factor(fde_handle h, fde_hmatrix hm, double tol, fde_hlu* out);
+
+typedef struct {
+    int32_t max_rank;
+    int64_t stored_entries;
+    double factor_ms;
+    int32_t nops;          /* device operations issued                      */
+} fde_hlu_info;
+int fde_hlu_get_info(fde_hlu lu, fde_hlu_info* info);
+
+/* -------------------------------------------------------- precond_apply */
+/* z = U_H^{-1} L_H^{-1} r: hierarchical forward and backward substitution
+ * (PAPER.md:605).  r, z device, paper order; r may equal z. */
+int precond_apply(fde_handle h, fde_hlu lu, const double* r, double* z, int nrhs, int64_t ld);
+
+/* ---------------------------------------------------------------- solve */
+enum { FDE_GMRES = 0, FDE_BICGSTAB = 1 };
+typedef struct {
+    int32_t method;       /* FDE_GMRES (BASELINE) | FDE_BICGSTAB */
+    double tol;           /* relative residual of the preconditioned system     */
+    int32_t maxiter;      /* total iterations                                    */
+    int32_t restart;      /* GMRES(m)                                            */
+    int32_t path;         /* FDE_PATH_* for the matvec                           */
+} fde_solve_opts;
+
+typedef struct {
+    int32_t iterations;   /* max over RHS                                       */
+    int32_t matvecs;      /* operator applications per RHS column               */
+    int32_t converged;    /* number of converged RHS columns                    */
+    double relres;        /* max final preconditioned relative residual          */
+    double solve_ms;
+} fde_solve_report;
+
+/* Solve A~^{-1} A X = A~^{-1} G (Eq. (precondsys)) from
+ * X0 = 0; lu may be NULL (unpreconditioned).  G, X device, paper order. */
+int solve(fde_handle h, fde_operator op, fde_hlu lu, const double* G, double* X, int nrhs,
+          int64_t ld, const fde_solve_opts* opts, fde_solve_report* rep);
+/* same entry point under a prefixed name */
+int fde_solve(fde_handle h, fde_operator op, fde_hlu lu, const double* G, double* X, int nrhs,
+              int64_t ld, const fde_solve_opts* opts, fde_solve_report* rep);
+
+/* ------------------------------------------------------------- cleanup */
+void fde_free_operator(fde_operator op);
+void fde_free_hmatrix(fde_hmatrix hm);
+void fde_free_hlu(fde_hlu lu);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FDE_H */

@@ -1,0 +1,371 @@
+// C-ABI entry points of libfde (include/fde.h).  Host orchestration only:
+// validation, sharding bookkeeping, buffer management and kernel launches.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <exception>
+
+#include "fde_internal.h"
+#include "hlu.h"
+#include "hmatrix.h"
+
+void comm_unique_id(void* out128);
+void comm_init(fde_ctx* h, const void* uid128);
+void comm_destroy(fde_ctx* h);
+void krylov_gmres(fde_ctx* h, fde_op* op, fde_lu* lu, const double* G, double* X, int nrhs, long long ldv,
+                  const fde_solve_opts* o, fde_solve_report* rep);
+void krylov_bicgstab(fde_ctx* h, fde_op* op, fde_lu* lu, const double* G, double* X, int nrhs, long long ldv,
+                     const fde_solve_opts* o, fde_solve_report* rep);
+void dense_to_paper(fde_ctx* h, fde_op* op, double* out, int64_t ldo);
+void bnd_to_paper(fde_ctx* h, fde_op* op, double* out);
+void internal_dense_to_paper(fde_ctx* h, int N, int P, const double* in, int64_t ldi, double* out, int64_t ldo);
+
+static thread_local std::string g_noctx_err;
+
+#define API_BEGIN try {
+#define API_END(h)                                                   \
+    }                                                                \
+    catch (FdeError & e) {                                           \
+        if (h) (h)->err = e.msg; else g_noctx_err = e.msg;           \
+        return e.code;                                               \
+    }                                                                \
+    catch (std::exception & e) {                                     \
+        if (h) (h)->err = e.what(); else g_noctx_err = e.what();     \
+        return FDE_ECUDA;                                            \
+    }                                                                \
+    return FDE_OK;
+
+extern "C" {
+
+int fde_create(fde_handle* out, int device, void* cuda_stream, const void* nccl_unique_id, int rank, int world)
+{
+    fde_ctx* h = nullptr;
+    API_BEGIN
+    if (!out) fde_fail(FDE_EINVAL_PARAM, "fde_create: out is NULL");
+    if (world < 1 || rank < 0 || rank >= world) fde_fail(FDE_EINVAL_PARAM, "fde_create: bad rank/world");
+    if (world > 1 && !nccl_unique_id) fde_fail(FDE_EINVAL_PARAM, "fde_create: world > 1 needs an NCCL unique id");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) fde_fail(FDE_ECUDA, "no CUDA device");
+    h = new fde_ctx();
+    h->device = device;
+    h->rank = rank;
+    h->world = world;
+    FDE_CUDA(cudaSetDevice(device));
+    if (cuda_stream) {
+        h->stream = (cudaStream_t)cuda_stream;
+    } else {
+        FDE_CUDA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+        h->own_stream = true;
+    }
+    FDE_CUDA(cudaEventCreate(&h->ev0));
+    FDE_CUDA(cudaEventCreate(&h->ev1));
+    FDE_CUDA(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, device));
+    if (world > 1) comm_init(h, nccl_unique_id);
+    *out = h;
+    }
+    catch (FdeError& e) {
+        g_noctx_err = e.msg;
+        delete h;
+        return e.code;
+    }
+    return FDE_OK;
+}
+
+void fde_destroy(fde_handle h)
+{
+    if (!h) return;
+    comm_destroy(h);
+    if (h->ev0) cudaEventDestroy(h->ev0);
+    if (h->ev1) cudaEventDestroy(h->ev1);
+    if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
+    delete h;
+}
+
+const char* fde_last_error(fde_handle h) { return h ? h->err.c_str() : g_noctx_err.c_str(); }
+
+int fde_sync(fde_handle h)
+{
+    API_BEGIN
+    FDE_CUDA(cudaStreamSynchronize(h->stream));
+    API_END(h)
+}
+
+int fde_nccl_unique_id(void* out128)
+{
+    fde_ctx* h = nullptr;
+    API_BEGIN
+    comm_unique_id(out128);
+    API_END(h)
+}
+
+// ------------------------------------------------------------ validation
+static void validate(const fde_problem* p, const fde_mesh* m)
+{
+    if (!p || !m || !m->nodes) fde_fail(FDE_EINVAL_PARAM, "NULL problem/mesh");
+    if (!(p->a < p->b)) fde_fail(FDE_EINVAL_DOMAIN, "invalid domain: a >= b");
+    if (m->N < 1) fde_fail(FDE_EINVAL_SIZE, "invalid size: N < 1");
+    if (!(p->alpha > 1.0 && p->alpha < 2.0)) fde_fail(FDE_EINVAL_PARAM, "alpha must lie in (1,2)");
+    if (!(p->theta >= 0.0 && p->theta <= 1.0)) fde_fail(FDE_EINVAL_PARAM, "theta must lie in [0,1]");
+    if (!(p->rho >= 0.0)) fde_fail(FDE_EINVAL_PARAM, "rho must be >= 0");
+    if (m->P < 1 || m->P > FDE_MAX_P) fde_fail(FDE_EDEGREE, "P must lie in [1, FDE_MAX_P]");
+    if (m->nodes[0] != p->a || m->nodes[m->N] != p->b) fde_fail(FDE_EINVAL_MESH, "mesh ends must equal a and b");
+    for (int i = 0; i < m->N; ++i)
+        if (!(m->nodes[i + 1] > m->nodes[i])) fde_fail(FDE_EINVAL_MESH, "mesh nodes must be strictly increasing");
+}
+
+int sem_assemble(fde_handle h, const fde_problem* prob, const fde_mesh* mesh, int flags, fde_operator* out)
+{
+    fde_op* op = nullptr;
+    API_BEGIN
+    validate(prob, mesh);
+    if (!(flags & (FDE_OP_DENSE | FDE_OP_TOEPLITZ))) fde_fail(FDE_EINVAL_PARAM, "flags: DENSE and/or TOEPLITZ");
+    FDE_CUDA(cudaSetDevice(h->device));
+    op = new fde_op();
+    op->prob = *prob;
+    op->N = mesh->N;
+    op->P = mesh->P;
+    op->n = (int64_t)mesh->N * mesh->P - 1;
+    op->flags = flags;
+    op->world = h->world;
+    op->g0 = 1.0 / std::tgamma(2.0 - prob->alpha);
+    op->nodes_h.assign(mesh->nodes, mesh->nodes + mesh->N + 1);
+    {
+        const double h0 = op->nodes_h[1] - op->nodes_h[0];
+        bool uni = true;
+        for (int i = 0; i < op->N; ++i)
+            if (std::fabs((op->nodes_h[i + 1] - op->nodes_h[i]) - h0) > 1e-12 * h0) uni = false;
+        op->uniform = uni;
+    }
+    if ((flags & FDE_OP_TOEPLITZ) && !op->uniform)
+        fde_fail(FDE_EUNSUPPORTED_MESH, "unsupported mesh: the Toeplitz path needs a uniform mesh");
+    if (op->n < 1) fde_fail(FDE_EINVAL_SIZE, "no unknowns (N*P - 1 < 1)");
+    // element partition over ranks
+    const int G = h->world, N = op->N, P = op->P;
+    op->rank_r0.resize(G + 1);
+    int64_t rmax = 0;
+    for (int g = 0; g <= G; ++g) {
+        int e = (int)((int64_t)N * g / G);
+        op->rank_r0[g] = std::min((int64_t)e * P, op->n);
+    }
+    for (int g = 0; g < G; ++g) rmax = std::max(rmax, op->rank_r0[g + 1] - op->rank_r0[g]);
+    op->rows_max = std::max<int64_t>(rmax, 1);
+    op->e_lo = (int)((int64_t)N * h->rank / G);
+    op->e_hi = (int)((int64_t)N * (h->rank + 1) / G);
+    op->r0 = op->rank_r0[h->rank];
+    op->r1 = op->rank_r0[h->rank + 1];
+    op->lda = round_up(op->n, 32);
+
+    FDE_CUDA(cudaEventRecord(h->ev0, h->stream));
+    asm_prepare_tables(h, op);
+    if (flags & FDE_OP_DENSE) {
+        const int b0 = op->e_lo, b1 = std::min(op->e_hi, N - 1);
+        const int64_t P2 = (int64_t)P * P;
+        DBuf<double> Krow, Kcol;
+        const int64_t nrow = (int64_t)(b1 + 1) * (b1 + 2) / 2 - (int64_t)b0 * (b0 + 1) / 2;
+        const int64_t ncol = (int64_t)(N - 1 - b1) * (b1 - b0 + 1);
+        Krow.alloc((size_t)std::max<int64_t>(nrow, 1) * P2);
+        if (ncol > 0) Kcol.alloc((size_t)ncol * P2);
+        asm_k_triangle(h, op, b0, b1 + 1, Krow.p);
+        if (ncol > 0) asm_k_rect(h, op, b1 + 1, N, b0, b1 + 1, Kcol.p);
+        op->A.alloc((size_t)std::max<int64_t>(op->r1 - op->r0, 1) * op->lda);
+        asm_expand_dense(h, op, Krow.p, Kcol.p);
+        FDE_CUDA(cudaStreamSynchronize(h->stream));   // K tables are released here
+    }
+    asm_boundary_columns(h, op);
+    if (flags & FDE_OP_TOEPLITZ) toeplitz_prepare(h, op);
+    op->xw_cols = 0;
+    FDE_CUDA(cudaEventRecord(h->ev1, h->stream));
+    FDE_CUDA(cudaEventSynchronize(h->ev1));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, h->ev0, h->ev1);
+    op->assemble_ms = ms;
+    *out = op;
+    op = nullptr;
+    }
+    catch (FdeError& e) {
+        h->err = e.msg;
+        delete op;
+        return e.code;
+    }
+    return FDE_OK;
+}
+
+int fde_operator_get_info(fde_operator op, fde_operator_info* info)
+{
+    if (!op || !info) return FDE_EINVAL_PARAM;
+    info->n = op->n;
+    info->N = op->N;
+    info->P = op->P;
+    info->row_begin = op->r0;
+    info->row_end = op->r1;
+    info->lda = op->lda;
+    info->flags = op->flags;
+    info->uniform = op->uniform ? 1 : 0;
+    info->assemble_ms = op->assemble_ms;
+    return FDE_OK;
+}
+
+int fde_operator_dense_paper(fde_handle h, fde_operator op, double* out, int64_t ldo)
+{
+    API_BEGIN
+    if (h->world != 1) fde_fail(FDE_EINVAL_PARAM, "dense export needs world == 1");
+    if (!(op->flags & FDE_OP_DENSE)) fde_fail(FDE_EINVAL_PARAM, "operator has no dense form");
+    if (ldo < op->n) fde_fail(FDE_EINVAL_SIZE, "ldo < n");
+    dense_to_paper(h, op, out, ldo);
+    API_END(h)
+}
+
+int fde_operator_boundary_columns(fde_handle h, fde_operator op, double* out)
+{
+    API_BEGIN
+    bnd_to_paper(h, op, out);
+    API_END(h)
+}
+
+// ------------------------------------------------------------------ work
+static void ensure_work(fde_op* op, int nrhs)
+{
+    if (op->xw_cols < (size_t)nrhs) {
+        op->xw.alloc((size_t)nrhs * op->lda);
+        op->yw.alloc((size_t)nrhs * op->lda);
+        op->gw.alloc((size_t)nrhs * op->lda);
+        op->xw_cols = nrhs;
+    }
+}
+
+int sem_rhs(fde_handle h, fde_operator op, const fde_forcing* f, int nrhs, double* G, int64_t ld)
+{
+    API_BEGIN
+    if (nrhs < 1 || ld < op->n) fde_fail(FDE_EINVAL_SIZE, "sem_rhs: nrhs >= 1 and ld >= n required");
+    if (!f) fde_fail(FDE_EINVAL_PARAM, "sem_rhs: forcing is NULL");
+    ensure_work(op, nrhs);
+    asm_rhs(h, op, f, nrhs, op->gw.p, op->lda);
+    perm_internal_to_paper(h, op->N, op->P, op->gw.p, op->lda, G, ld, nrhs);
+    API_END(h)
+}
+
+int stiffness_matvec(fde_handle h, fde_operator op, const double* x, double* y, int nrhs, int64_t ld, int path)
+{
+    API_BEGIN
+    if (nrhs < 1 || ld < op->n) fde_fail(FDE_EINVAL_SIZE, "stiffness_matvec: nrhs >= 1 and ld >= n required");
+    if (path == FDE_PATH_TOEPLITZ && !(op->flags & FDE_OP_TOEPLITZ))
+        fde_fail(FDE_EUNSUPPORTED_MESH, "unsupported mesh: operator was assembled without the Toeplitz form");
+    ensure_work(op, nrhs);
+    perm_paper_to_internal(h, op->N, op->P, x, ld, op->xw.p, op->lda, nrhs);
+    op_apply_internal(h, op, op->xw.p, op->lda, op->yw.p, op->lda, nrhs, path);
+    perm_internal_to_paper(h, op->N, op->P, op->yw.p, op->lda, y, ld, nrhs);
+    API_END(h)
+}
+
+// ------------------------------------------------------------- H-matrix
+int hmatrix_build(fde_handle h, fde_operator op, int R, double lambda, int n_min, fde_hmatrix* out)
+{
+    API_BEGIN
+    *out = hm_build(h, op, R, lambda, n_min);
+    API_END(h)
+}
+
+int fde_hmatrix_get_info(fde_hmatrix hm, fde_hmatrix_info* info)
+{
+    if (!hm || !info) return FDE_EINVAL_PARAM;
+    info->nblocks_dense = hm->n_dense;
+    info->nblocks_lr = hm->n_lr;
+    info->depth = hm->S.depth;
+    info->nclusters = (int)hm->S.cl.size();
+    info->dense_entries = hm->dense_words;
+    info->lr_entries = hm->lr_words;
+    info->build_ms = hm->build_ms;
+    return FDE_OK;
+}
+
+int fde_hmatrix_dense_paper(fde_handle h, fde_hmatrix hm, double* out, int64_t ldo)
+{
+    API_BEGIN
+    const int64_t n = hm->S.n;
+    if (ldo < n) fde_fail(FDE_EINVAL_SIZE, "ldo < n");
+    DBuf<double> tmp;
+    tmp.alloc((size_t)n * n);
+    hm_to_dense_internal(h, hm, tmp.p, n);
+    internal_dense_to_paper(h, hm->S.N, hm->S.P, tmp.p, n, out, ldo);
+    FDE_CUDA(cudaStreamSynchronize(h->stream));
+    API_END(h)
+}
+
+// ----------------------------------------------------------------- H-LU
+int hlu_factor(fde_handle h, fde_hmatrix hm, double tol, fde_hlu* out)
+{
+    API_BEGIN
+    if (!(tol >= 0.0)) fde_fail(FDE_EINVAL_PARAM, "hlu_factor: tol must be >= 0");
+    *out = hlu_build(h, hm, tol);
+    API_END(h)
+}
+
+int fde_hlu_get_info(fde_hlu lu, fde_hlu_info* info)
+{
+    if (!lu || !info) return FDE_EINVAL_PARAM;
+    hlu_info(lu, info);
+    return FDE_OK;
+}
+
+int precond_apply(fde_handle h, fde_hlu lu, const double* r, double* z, int nrhs, int64_t ld)
+{
+    API_BEGIN
+    fde_op* op = hlu_operator(lu);
+    if (nrhs < 1 || ld < op->n) fde_fail(FDE_EINVAL_SIZE, "precond_apply: nrhs >= 1 and ld >= n required");
+    ensure_work(op, nrhs);
+    perm_paper_to_internal(h, op->N, op->P, r, ld, op->xw.p, op->lda, nrhs);
+    precond_apply_internal(h, lu, op->xw.p, op->lda, op->yw.p, op->lda, nrhs);
+    perm_internal_to_paper(h, op->N, op->P, op->yw.p, op->lda, z, ld, nrhs);
+    API_END(h)
+}
+
+// ---------------------------------------------------------------- solve
+int solve(fde_handle h, fde_operator op, fde_hlu lu, const double* G, double* X, int nrhs, int64_t ld,
+          const fde_solve_opts* opts, fde_solve_report* rep)
+{
+    API_BEGIN
+    if (nrhs < 1 || ld < op->n) fde_fail(FDE_EINVAL_SIZE, "solve: nrhs >= 1 and ld >= n required");
+    if (lu && hlu_operator(lu)->n != op->n) fde_fail(FDE_EDIM, "solve: preconditioner of another problem");
+    fde_solve_opts o{};
+    o.method = FDE_GMRES;
+    o.tol = 1e-12;
+    o.maxiter = 500;
+    o.restart = 50;
+    o.path = FDE_PATH_AUTO;
+    if (opts) o = *opts;
+    fde_solve_report r{};
+    ensure_work(op, nrhs);
+    perm_paper_to_internal(h, op->N, op->P, G, ld, op->gw.p, op->lda, nrhs);
+    FDE_CUDA(cudaEventRecord(h->ev0, h->stream));
+    if (o.method == FDE_BICGSTAB)
+        krylov_bicgstab(h, op, lu, op->gw.p, op->xw.p, nrhs, op->lda, &o, &r);
+    else
+        krylov_gmres(h, op, lu, op->gw.p, op->xw.p, nrhs, op->lda, &o, &r);
+    FDE_CUDA(cudaEventRecord(h->ev1, h->stream));
+    perm_internal_to_paper(h, op->N, op->P, op->xw.p, op->lda, X, ld, nrhs);
+    FDE_CUDA(cudaEventSynchronize(h->ev1));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, h->ev0, h->ev1);
+    r.solve_ms = ms;
+    if (rep) *rep = r;
+    FDE_CUDA(cudaStreamSynchronize(h->stream));
+    if (r.converged < nrhs) {
+        char b[160];
+        snprintf(b, sizeof(b), "solve: %d of %d columns did not converge (relres %.3e)", nrhs - r.converged, nrhs,
+                 r.relres);
+        fde_fail(FDE_EMAXITER, b);
+    }
+    API_END(h)
+}
+
+int fde_solve(fde_handle h, fde_operator op, fde_hlu lu, const double* G, double* X, int nrhs, int64_t ld,
+              const fde_solve_opts* opts, fde_solve_report* rep)
+{
+    return solve(h, op, lu, G, X, nrhs, ld, opts, rep);
+}
+
+void fde_free_operator(fde_operator op) { delete op; }
+void fde_free_hmatrix(fde_hmatrix hm) { delete hm; }
+void fde_free_hlu(fde_hlu lu) { hlu_destroy(lu); }
+
+}  // extern "C"

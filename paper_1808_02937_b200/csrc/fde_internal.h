@@ -1,0 +1,182 @@
+// Internal declarations of libfde (B200 hot path of arXiv 1808.02937).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "../../include/fde.h"
+
+// ---------------------------------------------------------------- errors
+struct FdeError {
+    int code;
+    std::string msg;
+};
+
+#define FDE_CUDA(call)                                                                        \
+    do {                                                                                      \
+        cudaError_t _e = (call);                                                              \
+        if (_e != cudaSuccess) {                                                              \
+            char _b[512];                                                                     \
+            snprintf(_b, sizeof(_b), "%s:%d %s: %s", __FILE__, __LINE__, #call,               \
+                     cudaGetErrorString(_e));                                                 \
+            throw FdeError{FDE_ECUDA, _b};                                                    \
+        }                                                                                     \
+    } while (0)
+
+#define FDE_CHECK_LAUNCH() FDE_CUDA(cudaGetLastError())
+
+inline void fde_fail(int code, const std::string& m) { throw FdeError{code, m}; }
+
+// ----------------------------------------------------------- device buffer
+template <typename T>
+struct DBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    DBuf() = default;
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    ~DBuf() { release(); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    void alloc(size_t count) {
+        release();
+        if (count == 0) return;
+        cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+        if (e != cudaSuccess) {
+            p = nullptr;
+            throw FdeError{FDE_ENOMEM, std::string("cudaMalloc failed: ") + cudaGetErrorString(e)};
+        }
+        n = count;
+    }
+    void upload(const T* h, size_t count, cudaStream_t s) {
+        if (count > n) alloc(count);
+        if (count) FDE_CUDA(cudaMemcpyAsync(p, h, count * sizeof(T), cudaMemcpyHostToDevice, s));
+    }
+    void zero(cudaStream_t s) {
+        if (n) FDE_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), s));
+    }
+};
+
+// ------------------------------------------------------------------ context
+struct fde_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    int rank = 0, world = 1;
+    void* nccl = nullptr;   // ncclComm_t
+    std::string err;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    int num_sms = 148;
+};
+
+// ------------------------------------------------------- quadrature tables
+// Host-side generation (long double), Sturm-sequence bisection for the nodes
+// of the Jacobi matrix and Christoffel numbers for the weights.
+namespace fdeq {
+// Gauss-Legendre on [-1,1]
+void gauss_legendre(int n, std::vector<double>& x, std::vector<double>& w);
+// Gauss-Jacobi for the weight (1-x)^a (1+x)^b on [-1,1]
+void gauss_jacobi(int n, double a, double b, std::vector<double>& x, std::vector<double>& w);
+}  // namespace fdeq
+
+// Maximum points of one tensor-rule direction on the device.
+#define FDE_QMAX 32
+// Packed Gauss-Legendre rules for Q = 1..FDE_QMAX: offset(Q) = Q(Q-1)/2.
+#define FDE_GL_TOTAL (FDE_QMAX * (FDE_QMAX + 1) / 2)
+
+// ----------------------------------------------------------------- operator
+struct AsmTables {
+    // device copies
+    DBuf<double> nodes;        // N+1
+    DBuf<double> gjr_x, gjr_w; // Gauss-Jacobi (0, 2-alpha): radial Duffy / self outer
+    DBuf<double> gji_x, gji_w; // Gauss-Jacobi (0, 1-alpha): self inner
+    DBuf<double> kself;        // P*P reference self moment
+    DBuf<double> mref;         // (P+1)^2 reference mass
+    int qr = 0, qi = 0;
+};
+
+struct fde_op {
+    fde_problem prob{};
+    int N = 0, P = 0;
+    int64_t n = 0;
+    int flags = 0;
+    bool uniform = false;
+    double g0 = 0;                  // 1/Gamma(2-alpha)
+    std::vector<double> nodes_h;
+    AsmTables tab;
+    // sharding (element ranges; rows in internal order)
+    int e_lo = 0, e_hi = 0;         // owned elements [e_lo, e_hi)
+    int64_t r0 = 0, r1 = 0;         // owned rows [r0, r1)
+    int64_t rows_max = 0;           // max rows over ranks (allgather padding)
+    std::vector<int64_t> rank_r0;   // row starts of every rank
+    // dense shard
+    int64_t lda = 0;
+    DBuf<double> A;                 // (r1-r0) x lda row-major, internal order
+    DBuf<double> bnd;               // 2 x n internal order: columns of hats 0 and N
+    // Toeplitz
+    int L = 0;                      // FFT length
+    DBuf<double> sym;               // N x P*P lag moments K_{k,0}
+    DBuf<double> spec;              // L x P x P complex (interleaved re,im): theta K^ + (1-theta) K^H
+    DBuf<double> twid;              // L/2 complex twiddles
+    // scratch
+    DBuf<double> xw, yw, gw;        // internal-order work vectors
+    size_t xw_cols = 0;
+    double assemble_ms = 0;
+    int world = 1;
+};
+
+// ------------------------------------------------------------- kernels API
+// (implemented in assemble.cu / matvec.cu / toeplitz.cu)
+struct PairList {
+    // explicit element pairs (i >= j) and output slots
+    DBuf<int> i, j;
+    DBuf<long long> slot;
+    int64_t count = 0;
+};
+
+void asm_prepare_tables(fde_ctx* h, fde_op* op);
+// K blocks for rows i in [i0, i1) x j in [0, i] (packed lower triangle rows) -> out
+void asm_k_triangle(fde_ctx* h, fde_op* op, int i0, int i1, double* out);
+// K blocks K_{i,j} for i in [i0,i1) x j in [j0, j1), all with i > j, dense rect
+void asm_k_rect(fde_ctx* h, fde_op* op, int i0, int i1, int j0, int j1, double* out);
+// explicit list
+void asm_k_list(fde_ctx* h, fde_op* op, const int* di, const int* dj, const long long* dslot,
+                int64_t count, double* out);
+// expand dense shard rows [r0,r1) from the band K storage
+void asm_expand_dense(fde_ctx* h, fde_op* op, const double* Krow, const double* Kcol);
+void asm_boundary_columns(fde_ctx* h, fde_op* op);
+void asm_rhs(fde_ctx* h, fde_op* op, const fde_forcing* f, int nrhs, double* G_internal, int64_t ld);
+
+// generic entry expansion from a K lookup described by a "KIndex" (see kindex.cuh)
+struct KIndexDev;
+
+// permutations
+void perm_paper_to_internal(fde_ctx* h, int N, int P, const double* src, int64_t lds, double* dst,
+                            int64_t ldd, int nrhs);
+void perm_internal_to_paper(fde_ctx* h, int N, int P, const double* src, int64_t lds, double* dst,
+                            int64_t ldd, int nrhs);
+
+// dense matvec on the shard: y[r0..r1) = A x (internal order, padded lda)
+void dense_gemv(fde_ctx* h, fde_op* op, const double* x, int64_t ldx, double* y, int64_t ldy, int nrhs);
+
+// Toeplitz
+void toeplitz_prepare(fde_ctx* h, fde_op* op);
+void toeplitz_matvec(fde_ctx* h, fde_op* op, const double* x, int64_t ldx, double* y, int64_t ldy, int nrhs);
+
+// full operator application in internal order (dense/fft + allgather)
+void op_apply_internal(fde_ctx* h, fde_op* op, const double* x, int64_t ldx, double* y, int64_t ldy,
+                       int nrhs, int path);
+
+// communication
+void comm_allgather_rows(fde_ctx* h, fde_op* op, const double* local, double* full, int64_t ldfull, int nrhs);
+
+// -------------------------------------------------------------- utilities
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }

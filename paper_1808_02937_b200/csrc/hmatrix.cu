@@ -1,0 +1,406 @@
+// hmatrix_build: H-matrix approximation A~ = rho M + theta H + (1-theta) H^T of
+// the SEM stiffness (Eq. (approxmat)/(approxsys); reading A2).
+//
+//  * cluster tree: binary median split of element ranges down to n_min elements
+//    (reading A9); a cluster carries the modal dofs of its elements and the hats
+//    of their right nodes (element-interleaved order => contiguous dof range);
+//    its support is the union of the supports, [x_e0, x_{e1+1}].
+//  * partition: a block is an admissible leaf if max(diam) <= lambda dist
+//    (Eq. (admis)), a dense leaf if not and one cluster is a leaf,
+//    otherwise it is subdivided 2 x 2.
+//  * admissible leaves carry the Taylor factors of Lemma 3.2:
+//    Q = gamma0 int h_nu phi', W = int g_nu phi',
+//    expanded in s about the column-cluster midpoint, or in t about the row
+//    midpoint when the column cluster is larger (Remark).
+//    Lower blocks (row cluster right of column cluster) store
+//    U = theta Q, V = W; upper blocks U = (1-theta) W, V = Q of the mirrored pair.
+//  * inadmissible leaves hold exact entries of A, computed from
+//    the pair moments K_ij of assemble.cu for the element pairs of the leaf.
+//  All arithmetic runs on the device; the host only builds the tree.
+#include <algorithm>
+#include <cmath>
+
+#include "hmatrix.h"
+
+
+// ------------------------------------------------------------ structure
+static int build_cluster(HStruct& S, const std::vector<double>& x, int e0, int e1, int n_min)
+{
+    HCluster c;
+    c.e0 = e0;
+    c.e1 = e1;
+    c.r0 = (int64_t)e0 * S.P;
+    c.r1 = std::min((int64_t)e1 * S.P, S.n);
+    c.child[0] = c.child[1] = -1;
+    c.lo = x[e0];
+    c.hi = x[std::min(e1 + 1, S.N)];
+    int id = (int)S.cl.size();
+    S.cl.push_back(c);
+    if (e1 - e0 > n_min) {
+        int mid = (e0 + e1) / 2;
+        int a = build_cluster(S, x, e0, mid, n_min);
+        int b = build_cluster(S, x, mid, e1, n_min);
+        S.cl[id].child[0] = a;
+        S.cl[id].child[1] = b;
+    }
+    return id;
+}
+
+static bool admissible(const HCluster& t, const HCluster& s, double lam)
+{
+    const double diam = std::max(t.hi - t.lo, s.hi - s.lo);
+    const double dist = std::max(std::max(s.lo - t.hi, t.lo - s.hi), 0.0);
+    return dist > 0.0 && diam <= lam * dist;
+}
+
+static int build_block(HStruct& S, int t, int s, double lam, int level)
+{
+    HBlock b;
+    b.tau = t;
+    b.sig = s;
+    b.m = S.cl[t].r1 - S.cl[t].r0;
+    b.n = S.cl[s].r1 - S.cl[s].r0;
+    for (int k = 0; k < 4; ++k) b.child[k] = -1;
+    b.off = 0;
+    b.kcap = 0;
+    b.lower = 0;
+    S.depth = std::max(S.depth, level);
+    const HCluster &T = S.cl[t], &Sg = S.cl[s];
+    if (admissible(T, Sg, lam)) {
+        b.type = HB_LR;
+        b.lower = (T.e0 >= Sg.e1) ? 1 : 0;   // row cluster right of column cluster
+    } else if (T.child[0] < 0 || Sg.child[0] < 0) {
+        b.type = HB_DENSE;
+    } else {
+        b.type = HB_HIER;
+    }
+    int id = (int)S.bl.size();
+    S.bl.push_back(b);
+    if (b.type == HB_HIER) {
+        int k = 0;
+        for (int a = 0; a < 2; ++a)
+            for (int c = 0; c < 2; ++c) {
+                int ch = build_block(S, T.child[a], Sg.child[c], lam, level + 1);
+                S.bl[id].child[k++] = ch;
+            }
+    }
+    return id;
+}
+
+void hstruct_build(HStruct& S, const std::vector<double>& nodes, int P, int n_min, double lam)
+{
+    S.N = (int)nodes.size() - 1;
+    S.P = P;
+    S.n = (int64_t)S.N * P - 1;
+    S.cl.clear();
+    S.bl.clear();
+    S.depth = 0;
+    int root = build_cluster(S, nodes, 0, S.N, std::max(1, n_min));
+    S.root = build_block(S, root, root, lam, 0);
+}
+
+// ------------------------------------------------------------- device side
+struct FDesc {
+    int e0;            // first element of the cluster
+    int rows;          // dof rows
+    int64_t out;       // arena offset of the factor (rows x kcap col-major, ld rows)
+    int kind;          // 0: power  pref * alt^nu * c_nu * z^{1-alpha-nu},  1: polynomial pref * (x-x0)^nu
+    int sgn;           // power: z = sgn * (x - x0)
+    int alt;           // power: multiply by (-1)^nu
+    double pref;
+    int ea;            // x0 = x_ea + oa  (anchor node + offset, avoids cancellation)
+    double oa;
+};
+
+__global__ void k_factors(const FDesc* fd, const double* nodes, int N, int P, int R, double alpha, double g0,
+                          double* arena)
+{
+    __shared__ double red[8][32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const FDesc D = fd[blockIdx.y];
+    const int row = blockIdx.x * 8 + wid;
+    if (row >= D.rows) return;
+    const int e = D.e0 + row / P, q = row - (row / P) * P;
+    double acc[32];
+    for (int nu = 0; nu < R; ++nu) acc[nu] = 0.0;
+    // 32-point Gauss-Legendre, one point per lane, over the 1 or 2 elements of the dof
+    const int npass = (q < P - 1) ? 1 : 2;
+    for (int pass = 0; pass < npass; ++pass) {
+        const int el = (q < P - 1) ? e : (pass == 0 ? e : e + 1);
+        if (el >= N) continue;
+        const double xl = nodes[el], h = nodes[el + 1] - nodes[el];
+        // Gauss-Legendre 32 from constant memory (assemble.cu)
+        const int Q = 32;
+        const double xi = c_glx[Q * (Q - 1) / 2 + lane];
+        const double wq = c_glw[Q * (Q - 1) / 2 + lane];
+        double dphi;
+        if (q < P - 1) {
+            const int p = q + 1;
+            double p0 = 1.0, p1 = xi, Lp = (p == 0) ? 1.0 : xi;
+            for (int k = 1; k < p; ++k) {
+                double p2 = ((2 * k + 1) * xi * p1 - k * p0) / (k + 1);
+                p0 = p1;
+                p1 = p2;
+                Lp = p2;
+            }
+            dphi = (2.0 / h) * (-(2.0 * p + 1.0)) * Lp;
+        } else {
+            dphi = (pass == 0) ? 1.0 / h : -1.0 / h;
+        }
+        // x - x0 from node differences
+        const double dx = (xl - nodes[D.ea]) + 0.5 * h * (xi + 1.0) - D.oa;
+        const double w = wq * 0.5 * h * dphi;
+        if (D.kind == 0) {
+            const double z = D.sgn * dx;
+            const double lz = log(z);
+            double c = 1.0;
+            for (int nu = 0; nu < R; ++nu) {
+                double term = c * exp((1.0 - alpha - nu) * lz);
+                if (D.alt && (nu & 1)) term = -term;
+                acc[nu] = fma(w, term, acc[nu]);
+                c *= (alpha - 1.0 + nu) / (nu + 1.0);
+            }
+        } else {
+            double pw = 1.0;
+            for (int nu = 0; nu < R; ++nu) {
+                acc[nu] = fma(w, pw, acc[nu]);
+                pw *= dx;
+            }
+        }
+    }
+    for (int nu = 0; nu < R; ++nu) {
+        double v = acc[nu];
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) red[wid][nu] = v;
+    }
+    __syncwarp();
+    if (lane < R) arena[D.out + (int64_t)lane * D.rows + row] = D.pref * red[wid][lane];
+    (void)g0;
+}
+
+
+struct DenseDesc {
+    int type;
+    int64_t r0, c0;
+    int m, n;
+    int64_t off;
+    int kcap;
+    int blk;
+};
+
+__global__ void k_blocks_to_dense(const DenseDesc* dd, const double* dense, const double* lr, const int* rank,
+                                  double* out, int64_t ldo)
+{
+    const DenseDesc D = dd[blockIdx.y];
+    const int64_t tot = (int64_t)D.m * D.n;
+    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < tot; idx += (int64_t)gridDim.x * blockDim.x) {
+        const int i = (int)(idx % D.m), j = (int)(idx / D.m);
+        double v;
+        if (D.type == HB_DENSE) {
+            v = dense[D.off + (int64_t)j * D.m + i];
+        } else {
+            const int k = rank[D.blk];
+            const double* U = lr + D.off;
+            const double* V = U + (int64_t)D.m * D.kcap;
+            v = 0.0;
+            for (int t = 0; t < k; ++t) v = fma(U[(int64_t)t * D.m + i], V[(int64_t)t * D.n + j], v);
+        }
+        out[(D.c0 + j) * ldo + D.r0 + i] = v;
+    }
+}
+
+// ------------------------------------------------------------------ host
+void hm_leaves(const HStruct& S, int b, std::vector<int>& out)
+{
+    const HBlock& B = S.bl[b];
+    if (B.type == HB_HIER) {
+        for (int k = 0; k < 4; ++k) hm_leaves(S, B.child[k], out);
+    } else {
+        out.push_back(b);
+    }
+}
+
+fde_hm* hm_build(fde_ctx* h, fde_op* op, int R, double lam, int n_min)
+{
+    if (R < 1 || R > 32) fde_fail(FDE_EINVAL_PARAM, "hmatrix_build: R must be in [1, 32]");
+    if (!(lam > 0)) fde_fail(FDE_EINVAL_PARAM, "hmatrix_build: lambda must be > 0");
+    if (n_min < 1) fde_fail(FDE_EINVAL_PARAM, "hmatrix_build: n_min must be >= 1");
+    FDE_CUDA(cudaEventRecord(h->ev0, h->stream));
+    fde_hm* hm = new fde_hm();
+    try {
+        hm->op = op;
+        hm->R = R;
+        hm->lam = lam;
+        hm->n_min = n_min;
+        HStruct& S = hm->S;
+        hstruct_build(S, op->nodes_h, op->P, n_min, lam);
+        const int N = op->N, P = op->P;
+        const std::vector<double>& x = op->nodes_h;
+        std::vector<int> lv;
+        hm_leaves(S, S.root, lv);
+        // arenas
+        int64_t doff = 0, loff = 0;
+        for (int b : lv) {
+            HBlock& B = S.bl[b];
+            if (B.type == HB_DENSE) {
+                B.off = doff;
+                doff += B.m * B.n;
+                hm->n_dense++;
+            } else {
+                B.kcap = R;
+                B.off = loff;
+                loff += (B.m + B.n) * R;
+                hm->n_lr++;
+            }
+        }
+        hm->dense_words = doff;
+        hm->lr_words = loff;
+        hm->dense.alloc(std::max<int64_t>(doff, 1));
+        hm->lr.alloc(std::max<int64_t>(loff, 1));
+        std::vector<int> rank_h(S.bl.size(), 0);
+        // ---- low-rank factors
+        std::vector<FDesc> fd;
+        const double theta = op->prob.theta, g0 = op->g0;
+        for (int b : lv) {
+            HBlock& B = S.bl[b];
+            if (B.type != HB_LR) continue;
+            rank_h[b] = R;
+            // expansion pair: test cluster T (right), trial cluster Sg (left)
+            const int tcl = B.lower ? B.tau : B.sig;
+            const int scl = B.lower ? B.sig : B.tau;
+            const HCluster &T = S.cl[tcl], &Sg = S.cl[scl];
+            const bool s_exp = (Sg.hi - Sg.lo) <= (T.hi - T.lo);
+            FDesc q{}, w{};
+            // Q on the test cluster, W on the trial cluster
+            q.e0 = T.e0;
+            q.rows = (int)(T.r1 - T.r0);
+            w.e0 = Sg.e0;
+            w.rows = (int)(Sg.r1 - Sg.r0);
+            const double scale = B.lower ? theta : (1.0 - theta);
+            if (s_exp) {
+                // s0 = mid(Sg): anchor at x_{Sg.e0}
+                const int ea = Sg.e0;
+                const double oa = 0.5 * (x[std::min(Sg.e1 + 1, N)] - x[Sg.e0]);
+                q.kind = 0; q.sgn = 1; q.alt = 0; q.pref = g0; q.ea = ea; q.oa = oa;
+                w.kind = 1; w.sgn = 1; w.alt = 0; w.pref = 1.0; w.ea = ea; w.oa = oa;
+            } else {
+                const int ea = T.e0;
+                const double oa = 0.5 * (x[std::min(T.e1 + 1, N)] - x[T.e0]);
+                q.kind = 1; q.sgn = 1; q.alt = 0; q.pref = g0; q.ea = ea; q.oa = oa;
+                w.kind = 0; w.sgn = -1; w.alt = 1; w.pref = 1.0; w.ea = ea; w.oa = oa;
+            }
+            // lower: U = theta Q (rows tau = T), V = W (rows sigma = Sg)
+            // upper: U = (1-theta) W (rows tau = Sg), V = Q (rows sigma = T)
+            const int64_t Uoff = B.off, Voff = B.off + B.m * R;
+            if (B.lower) {
+                q.pref *= scale;
+                q.out = Uoff;
+                w.out = Voff;
+            } else {
+                w.pref *= scale;
+                w.out = Uoff;
+                q.out = Voff;
+            }
+            fd.push_back(q);
+            fd.push_back(w);
+        }
+        DBuf<FDesc> dfd;
+        if (!fd.empty()) {
+            dfd.upload(fd.data(), fd.size(), h->stream);
+            int maxrows = 0;
+            for (auto& f : fd) maxrows = std::max(maxrows, f.rows);
+            // grid.y limit 65535: chunk the descriptor list
+            for (size_t base = 0; base < fd.size(); base += 65535) {
+                unsigned cnt = (unsigned)std::min<size_t>(65535, fd.size() - base);
+                k_factors<<<dim3((unsigned)ceil_div(maxrows, 8), cnt), 256, 0, h->stream>>>(
+                    dfd.p + base, op->tab.nodes.p, N, P, R, op->prob.alpha, g0, hm->lr.p);
+                FDE_CHECK_LAUNCH();
+            }
+        }
+        // ---- dense leaves: K tables + expansion
+        std::vector<LeafDesc> ld;
+        std::vector<int> li, lj;
+        std::vector<long long> ls;
+        int64_t kslot = 0;
+        int maxent = 0;
+        for (int b : lv) {
+            HBlock& B = S.bl[b];
+            if (B.type != HB_DENSE) continue;
+            const HCluster &T = S.cl[B.tau], &Sg = S.cl[B.sig];
+            LeafDesc L;
+            L.ra = T.r0;
+            L.ca = Sg.r0;
+            L.m = (int)B.m;
+            L.nc = (int)B.n;
+            L.i0 = T.e0;
+            L.ni = std::min(T.e1 + 1, N) - T.e0;
+            L.j0 = Sg.e0;
+            L.nj = std::min(Sg.e1 + 1, N) - Sg.e0;
+            L.ktab = kslot;
+            L.out = B.off;
+            for (int a = 0; a < L.ni; ++a)
+                for (int c = 0; c < L.nj; ++c) {
+                    int i = L.i0 + a, j = L.j0 + c;
+                    li.push_back(std::max(i, j));
+                    lj.push_back(std::min(i, j));
+                    ls.push_back(kslot + (int64_t)a * L.nj + c);
+                }
+            kslot += (int64_t)L.ni * L.nj;
+            maxent = std::max(maxent, L.m * L.nc);
+            ld.push_back(L);
+        }
+        if (!ld.empty()) {
+            DBuf<int> di, dj;
+            DBuf<long long> dsl;
+            DBuf<double> ktab;
+            DBuf<LeafDesc> dld;
+            di.upload(li.data(), li.size(), h->stream);
+            dj.upload(lj.data(), lj.size(), h->stream);
+            dsl.upload(ls.data(), ls.size(), h->stream);
+            ktab.alloc((size_t)kslot * P * P);
+            asm_k_list(h, op, di.p, dj.p, dsl.p, (int64_t)li.size(), ktab.p);
+            dld.upload(ld.data(), ld.size(), h->stream);
+            asm_expand_leaves(h, op, ktab.p, dld.p, (int)ld.size(), maxent, hm->dense.p);
+            FDE_CUDA(cudaStreamSynchronize(h->stream));
+        }
+        hm->rank.upload(rank_h.data(), rank_h.size(), h->stream);
+        FDE_CUDA(cudaEventRecord(h->ev1, h->stream));
+        FDE_CUDA(cudaEventSynchronize(h->ev1));
+        float ms = 0;
+        cudaEventElapsedTime(&ms, h->ev0, h->ev1);
+        hm->build_ms = ms;
+    } catch (...) {
+        delete hm;
+        throw;
+    }
+    return hm;
+}
+
+void hm_to_dense_internal(fde_ctx* h, fde_hm* hm, double* out, int64_t ldo)
+{
+    std::vector<int> lv;
+    hm_leaves(hm->S, hm->S.root, lv);
+    std::vector<DenseDesc> dd;
+    for (int b : lv) {
+        const HBlock& B = hm->S.bl[b];
+        DenseDesc d;
+        d.type = B.type;
+        d.r0 = hm->S.cl[B.tau].r0;
+        d.c0 = hm->S.cl[B.sig].r0;
+        d.m = (int)B.m;
+        d.n = (int)B.n;
+        d.off = B.off;
+        d.kcap = B.kcap;
+        d.blk = b;
+        dd.push_back(d);
+    }
+    DBuf<DenseDesc> ddd;
+    ddd.upload(dd.data(), dd.size(), h->stream);
+    for (size_t base = 0; base < dd.size(); base += 65535) {
+        unsigned cnt = (unsigned)std::min<size_t>(65535, dd.size() - base);
+        k_blocks_to_dense<<<dim3(64, cnt), 256, 0, h->stream>>>(ddd.p + base, hm->dense.p, hm->lr.p, hm->rank.p, out,
+                                                               ldo);
+        FDE_CHECK_LAUNCH();
+    }
+    FDE_CUDA(cudaStreamSynchronize(h->stream));
+}

@@ -1,0 +1,66 @@
+// H-matrix structures shared by hmatrix.cu and hlu.cu.
+#pragma once
+
+#include "fde_internal.h"
+
+enum { HB_DENSE = 0, HB_LR = 1, HB_HIER = 2 };
+
+struct HCluster {
+    int e0, e1;          // element range [e0, e1)
+    int64_t r0, r1;      // dof range (internal order)
+    int child[2];        // -1 for leaves
+    double lo, hi;       // support [x_e0, x_min(e1+1,N)]
+};
+
+struct HBlock {
+    int tau, sig;        // row / column cluster
+    int type;
+    int child[4];        // hier: (t0,s0) (t0,s1) (t1,s0) (t1,s1)
+    int64_t m, n;        // rows, cols
+    int64_t off;         // dense: offset of the m x n col-major block (ld = m)
+                         // lr: offset of U (m x kcap col-major), V follows (n x kcap)
+    int kcap;            // rank capacity (lr)
+    int lower;           // lr: tau right of sigma
+};
+
+struct HStruct {
+    int N = 0, P = 0;
+    int64_t n = 0;
+    std::vector<HCluster> cl;
+    std::vector<HBlock> bl;
+    int root = 0;
+    int depth = 0;
+};
+
+struct fde_hm {
+    fde_op* op = nullptr;
+    int R = 0;
+    double lam = 1.0;
+    int n_min = 16;
+    HStruct S;
+    DBuf<double> dense;      // dense leaf arena
+    DBuf<double> lr;         // low-rank arena (kcap = R)
+    DBuf<int> rank;          // per block (device), R for LR blocks of A~
+    int64_t dense_words = 0, lr_words = 0;
+    int n_dense = 0, n_lr = 0;
+    double build_ms = 0;
+};
+
+struct LeafDesc {
+    int64_t ra, ca;    // first row / column dof
+    int m, nc;
+    int i0, ni, j0, nj;
+    int64_t ktab;      // first K block of the leaf table
+    int64_t out;       // dense arena offset
+};
+
+void hm_leaves(const HStruct& S, int b, std::vector<int>& out);
+// exact entries of the dense leaves from their K tables (assemble.cu)
+void asm_expand_leaves(fde_ctx* h, fde_op* op, const double* Ktab, const LeafDesc* d, int nleaves, int maxentries,
+                       double* arena);
+
+// build the cluster tree and block partition (host, structure only)
+void hstruct_build(HStruct& S, const std::vector<double>& nodes, int P, int n_min, double lam);
+
+fde_hm* hm_build(fde_ctx* h, fde_op* op, int R, double lam, int n_min);
+void hm_to_dense_internal(fde_ctx* h, fde_hm* hm, double* out, int64_t ldo);   // out col-major n x n

@@ -1,0 +1,321 @@
+// stiffness_matvec, dense path: y = A x with the dense fp64 row shard
+// (O(N_d^2) per Krylov iteration).  HBM-bound GEMV: one warp per
+// row, 128-bit streaming loads of A (L1 no-allocate), x from L1/L2, fixed-order
+// warp-shuffle reduction (deterministic, no atomics).  Multi-RHS blocks reuse
+// each A row for up to 4 right-hand sides per pass.
+//
+// Also: paper <-> element-interleaved permutations and the NCCL all-gather of
+// row shards (world > 1).
+#include <dlfcn.h>
+
+#include <cstring>
+
+#include "fde_internal.h"
+
+// ------------------------------------------------------------- permutation
+__device__ inline long long paper_of_internal(long long r, int N, int P)
+{
+    int e = (int)(r / P), q = (int)(r - (long long)e * P);
+    if (q < P - 1) return (long long)e * (P - 1) + q;
+    return (long long)N * (P - 1) + e;
+}
+
+__global__ void k_perm_p2i(int N, int P, long long n, const double* src, long long lds, double* dst, long long ldd)
+{
+    const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const int c = blockIdx.y;
+    if (r >= ldd) return;
+    dst[c * ldd + r] = (r < n) ? src[c * lds + paper_of_internal(r, N, P)] : 0.0;
+}
+
+__global__ void k_perm_i2p(int N, int P, long long n, const double* src, long long lds, double* dst, long long ldd)
+{
+    const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const int c = blockIdx.y;
+    if (r >= n) return;
+    dst[c * ldd + paper_of_internal(r, N, P)] = src[c * lds + r];
+}
+
+void perm_paper_to_internal(fde_ctx* h, int N, int P, const double* src, int64_t lds, double* dst, int64_t ldd,
+                            int nrhs)
+{
+    const long long n = (long long)N * P - 1;
+    dim3 g((unsigned)ceil_div(ldd, 256), (unsigned)nrhs);
+    k_perm_p2i<<<g, 256, 0, h->stream>>>(N, P, n, src, lds, dst, ldd);
+    FDE_CHECK_LAUNCH();
+}
+
+void perm_internal_to_paper(fde_ctx* h, int N, int P, const double* src, int64_t lds, double* dst, int64_t ldd,
+                            int nrhs)
+{
+    const long long n = (long long)N * P - 1;
+    dim3 g((unsigned)ceil_div(n, 256), (unsigned)nrhs);
+    k_perm_i2p<<<g, 256, 0, h->stream>>>(N, P, n, src, lds, dst, ldd);
+    FDE_CHECK_LAUNCH();
+}
+
+// ------------------------------------------------------------------- GEMV
+__device__ __forceinline__ double2 ld_stream(const double2* p)
+{
+    double2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+    return v;
+}
+
+#define GEMV_WARPS 8
+#define GEMV_UNROLL 4
+
+// y[row + c*ldy] = sum_k A[row*lda + k] x[k + c*ldx], c < NR ; lda % 2 == 0, x padded with zeros to lda
+template <int NR>
+__global__ void __launch_bounds__(32 * GEMV_WARPS) k_gemv(const double* __restrict__ A, long long lda,
+                                                         long long rows, const double* __restrict__ x,
+                                                         long long ldx, double* __restrict__ y, long long ldy)
+{
+    const int lane = threadIdx.x & 31;
+    const long long row = (long long)blockIdx.x * GEMV_WARPS + (threadIdx.x >> 5);
+    if (row >= rows) return;
+    const double2* a2 = reinterpret_cast<const double2*>(A + row * lda);
+    const long long n2 = lda >> 1;
+    double acc[NR][2];
+#pragma unroll
+    for (int c = 0; c < NR; ++c) acc[c][0] = acc[c][1] = 0.0;
+    long long k = lane;
+    for (; k + 32 * (GEMV_UNROLL - 1) < n2; k += 32 * GEMV_UNROLL) {
+        double2 a[GEMV_UNROLL];
+#pragma unroll
+        for (int u = 0; u < GEMV_UNROLL; ++u) a[u] = ld_stream(a2 + k + 32 * u);
+#pragma unroll
+        for (int u = 0; u < GEMV_UNROLL; ++u) {
+#pragma unroll
+            for (int c = 0; c < NR; ++c) {
+                const double2 xv = __ldg(reinterpret_cast<const double2*>(x + c * ldx) + k + 32 * u);
+                acc[c][u & 1] = fma(a[u].x, xv.x, acc[c][u & 1]);
+                acc[c][u & 1] = fma(a[u].y, xv.y, acc[c][u & 1]);
+            }
+        }
+    }
+    for (; k < n2; k += 32) {
+        double2 a = ld_stream(a2 + k);
+#pragma unroll
+        for (int c = 0; c < NR; ++c) {
+            const double2 xv = __ldg(reinterpret_cast<const double2*>(x + c * ldx) + k);
+            acc[c][0] = fma(a.x, xv.x, acc[c][0]);
+            acc[c][0] = fma(a.y, xv.y, acc[c][0]);
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < NR; ++c) {
+        double v = acc[c][0] + acc[c][1];
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+        if (lane == 0) y[row + c * ldy] = v;
+    }
+}
+
+void dense_gemv_raw(cudaStream_t s, const double* A, long long lda, long long rows, const double* x, long long ldx,
+                    double* y, long long ldy, int nrhs)
+{
+    const unsigned blocks = (unsigned)ceil_div(rows, GEMV_WARPS);
+    int c = 0;
+    while (c < nrhs) {
+        int r = nrhs - c;
+        if (r >= 4) {
+            k_gemv<4><<<blocks, 32 * GEMV_WARPS, 0, s>>>(A, lda, rows, x + c * ldx, ldx, y + c * ldy, ldy);
+            c += 4;
+        } else if (r == 3) {
+            k_gemv<3><<<blocks, 32 * GEMV_WARPS, 0, s>>>(A, lda, rows, x + c * ldx, ldx, y + c * ldy, ldy);
+            c += 3;
+        } else if (r == 2) {
+            k_gemv<2><<<blocks, 32 * GEMV_WARPS, 0, s>>>(A, lda, rows, x + c * ldx, ldx, y + c * ldy, ldy);
+            c += 2;
+        } else {
+            k_gemv<1><<<blocks, 32 * GEMV_WARPS, 0, s>>>(A, lda, rows, x + c * ldx, ldx, y + c * ldy, ldy);
+            c += 1;
+        }
+        FDE_CHECK_LAUNCH();
+    }
+}
+
+void dense_gemv(fde_ctx* h, fde_op* op, const double* x, int64_t ldx, double* y, int64_t ldy, int nrhs)
+{
+    dense_gemv_raw(h->stream, op->A.p, op->lda, op->r1 - op->r0, x, ldx, y, ldy, nrhs);
+}
+
+// ------------------------------------------------------------------ NCCL
+// NCCL is resolved at run time (dlopen) so that the library uses the
+// libnccl.so.2 already loaded by the host process (torch) when there is one.
+typedef struct { char internal[128]; } nccl_uid_t;
+typedef int (*nccl_getuid_fn)(nccl_uid_t*);
+typedef int (*nccl_init_fn)(void**, int, nccl_uid_t, int);
+typedef int (*nccl_allgather_fn)(const void*, void*, size_t, int, void*, cudaStream_t);
+typedef int (*nccl_destroy_fn)(void*);
+typedef const char* (*nccl_errstr_fn)(int);
+
+struct NcclApi {
+    void* lib = nullptr;
+    nccl_getuid_fn getuid = nullptr;
+    nccl_init_fn init = nullptr;
+    nccl_allgather_fn allgather = nullptr;
+    nccl_destroy_fn destroy = nullptr;
+    nccl_errstr_fn errstr = nullptr;
+};
+
+static NcclApi& nccl_api()
+{
+    static NcclApi api;
+    if (!api.lib) {
+        void* l = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD | RTLD_GLOBAL);
+        if (!l) l = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!l) l = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!l) fde_fail(FDE_ENCCL, "cannot dlopen libnccl.so.2");
+        api.lib = l;
+        api.getuid = (nccl_getuid_fn)dlsym(l, "ncclGetUniqueId");
+        api.init = (nccl_init_fn)dlsym(l, "ncclCommInitRank");
+        api.allgather = (nccl_allgather_fn)dlsym(l, "ncclAllGather");
+        api.destroy = (nccl_destroy_fn)dlsym(l, "ncclCommDestroy");
+        api.errstr = (nccl_errstr_fn)dlsym(l, "ncclGetErrorString");
+        if (!api.getuid || !api.init || !api.allgather || !api.destroy)
+            fde_fail(FDE_ENCCL, "libnccl.so.2 lacks required symbols");
+    }
+    return api;
+}
+
+void comm_unique_id(void* out128)
+{
+    nccl_uid_t id;
+    int r = nccl_api().getuid(&id);
+    if (r != 0) fde_fail(FDE_ENCCL, "ncclGetUniqueId failed");
+    memcpy(out128, &id, 128);
+}
+
+void comm_init(fde_ctx* h, const void* uid128)
+{
+    nccl_uid_t id;
+    memcpy(&id, uid128, 128);
+    void* comm = nullptr;
+    int r = nccl_api().init(&comm, h->world, id, h->rank);
+    if (r != 0) fde_fail(FDE_ENCCL, std::string("ncclCommInitRank failed: ") + (nccl_api().errstr ? nccl_api().errstr(r) : ""));
+    h->nccl = comm;
+}
+
+void comm_destroy(fde_ctx* h)
+{
+    if (h->nccl) nccl_api().destroy(h->nccl);
+    h->nccl = nullptr;
+}
+
+// gathered buffer holds world blocks of rows_max rows per RHS column -> compact
+__global__ void k_compact_gather(const double* gath, long long rows_max, int world, const int64_t* rstart,
+                                 long long n, double* full, long long ldfull, int nrhs)
+{
+    const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const int c = blockIdx.y;
+    if (r >= n) return;
+    // find owning rank (world <= 64, linear scan)
+    int g = 0;
+    while (g + 1 < world && rstart[g + 1] <= r) ++g;
+    const long long loc = r - rstart[g];
+    full[c * ldfull + r] = gath[((long long)g * nrhs + c) * rows_max + loc];
+}
+
+struct GatherScratch {
+    DBuf<double> send, recv;
+    DBuf<int64_t> rstart;
+};
+static GatherScratch& gscratch()
+{
+    static GatherScratch g;
+    return g;
+}
+
+// local: (r1-r0) rows per column with ld = rows_max ; full: n rows with ldfull
+void comm_allgather_rows(fde_ctx* h, fde_op* op, const double* local, double* full, int64_t ldfull, int nrhs)
+{
+    GatherScratch& G = gscratch();
+    const size_t chunk = (size_t)op->rows_max * nrhs;
+    if (G.recv.n < chunk * h->world) G.recv.alloc(chunk * h->world);
+    if (G.rstart.n < (size_t)h->world) {
+        G.rstart.alloc(h->world);
+    }
+    G.rstart.upload(op->rank_r0.data(), h->world, h->stream);
+    int r = nccl_api().allgather(local, G.recv.p, chunk, /*ncclFloat64*/ 8, h->nccl, h->stream);
+    if (r != 0) fde_fail(FDE_ENCCL, "ncclAllGather failed");
+    dim3 g((unsigned)ceil_div(op->n, 256), (unsigned)nrhs);
+    k_compact_gather<<<g, 256, 0, h->stream>>>(G.recv.p, op->rows_max, h->world, G.rstart.p, op->n, full, ldfull,
+                                                nrhs);
+    FDE_CHECK_LAUNCH();
+}
+
+// --------------------------------------------------- operator application
+// x: internal order (padded, ld ldx >= lda); y: internal order, full n rows.
+struct ApplyScratch {
+    DBuf<double> loc;
+};
+static ApplyScratch& ascratch()
+{
+    static ApplyScratch a;
+    return a;
+}
+
+void op_apply_internal(fde_ctx* h, fde_op* op, const double* x, int64_t ldx, double* y, int64_t ldy, int nrhs,
+                       int path)
+{
+    if (path == FDE_PATH_AUTO) path = (op->flags & FDE_OP_DENSE) ? FDE_PATH_DENSE : FDE_PATH_TOEPLITZ;
+    if (path == FDE_PATH_TOEPLITZ) {
+        if (!(op->flags & FDE_OP_TOEPLITZ)) fde_fail(FDE_EUNSUPPORTED_MESH, "operator has no Toeplitz form");
+        toeplitz_matvec(h, op, x, ldx, y, ldy, nrhs);
+        return;
+    }
+    if (!(op->flags & FDE_OP_DENSE)) fde_fail(FDE_EINVAL_PARAM, "operator has no dense form");
+    if (h->world == 1) {
+        dense_gemv(h, op, x, ldx, y, ldy, nrhs);
+        return;
+    }
+    ApplyScratch& S = ascratch();
+    const size_t need = (size_t)op->rows_max * nrhs;
+    if (S.loc.n < need) S.loc.alloc(need);
+    dense_gemv(h, op, x, ldx, S.loc.p, op->rows_max, nrhs);
+    comm_allgather_rows(h, op, S.loc.p, y, ldy, nrhs);
+}
+
+// ------------------------------------------------- dense exports (tests)
+__device__ inline long long paper_idx(long long r, int N, int P) { return paper_of_internal(r, N, P); }
+
+// out (paper order, row-major ldo) <- A (internal order, row-major lda), world == 1
+__global__ void k_dense_to_paper(const double* A, long long lda, long long n, int N, int P, double* out, long long ldo)
+{
+    const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long r = blockIdx.y;
+    if (c >= n) return;
+    out[paper_idx(r, N, P) * ldo + paper_idx(c, N, P)] = A[r * lda + c];
+}
+
+void dense_to_paper(fde_ctx* h, fde_op* op, double* out, int64_t ldo)
+{
+    dim3 g((unsigned)ceil_div(op->n, 256), (unsigned)op->n);
+    k_dense_to_paper<<<g, 256, 0, h->stream>>>(op->A.p, op->lda, op->n, op->N, op->P, out, ldo);
+    FDE_CHECK_LAUNCH();
+}
+
+// out col-major (paper order, ldo) <- in col-major (internal order, ldi)
+__global__ void k_idense_to_paper(const double* in, long long ldi, long long n, int N, int P, double* out,
+                                  long long ldo)
+{
+    const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long c = blockIdx.y;
+    if (r >= n) return;
+    out[paper_idx(c, N, P) * ldo + paper_idx(r, N, P)] = in[c * ldi + r];
+}
+
+void internal_dense_to_paper(fde_ctx* h, int N, int P, const double* in, int64_t ldi, double* out, int64_t ldo)
+{
+    const long long n = (long long)N * P - 1;
+    dim3 g((unsigned)ceil_div(n, 256), (unsigned)n);
+    k_idense_to_paper<<<g, 256, 0, h->stream>>>(in, ldi, n, N, P, out, ldo);
+    FDE_CHECK_LAUNCH();
+}
+
+void bnd_to_paper(fde_ctx* h, fde_op* op, double* out)
+{
+    perm_internal_to_paper(h, op->N, op->P, op->bnd.p, op->n, out, op->n, 2);
+}

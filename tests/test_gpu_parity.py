@@ -1,0 +1,183 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle.
+
+Metrics:
+  M-A  max |dA_IJ| / sqrt(A_II A_JJ)            <= 1e-10 (assembly, A~)
+  M-B  max |dy_I| / (|A| |x|)_I                 <= 1e-10 (matvec)
+  M-D  ||X - X_ora||_D / ||X_ora||_D, D=diag(A) <= 1e-10 (solve)
+"""
+import numpy as np
+import pytest
+
+import fde_inputs as fi
+import oracle as O
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-10
+
+
+@pytest.fixture(scope="module")
+def fde():
+    from paper_1808_02937_b200 import fde as F
+    return F
+
+
+@pytest.fixture(scope="module")
+def h(fde):
+    return fde.Handle(0)
+
+
+def metric_A(Ag, Ao):
+    d = np.sqrt(np.abs(np.diag(Ao)))
+    return np.max(np.abs(Ag - Ao) / (d[:, None] * d[None, :]))
+
+
+def graded_mirrored(N):
+    p = fi.config4(N=N, P=8)
+    return p
+
+
+def problems_small():
+    out = [fi.config1()]
+    for a in (1.2, 1.5, 1.8):
+        out.append(fi.config2(a, N=24, P=8))
+    out.append(fi.config3(P=4))
+    out.append(fi.config3(P=9))
+    out.append(fi.config4(N=40, P=6))
+    rng = np.random.default_rng(7)
+    x = np.sort(rng.uniform(0.0, 3.0, 17))
+    nodes = np.concatenate([[0.0], x, [3.0]])
+    out.append(fi.Problem("random", 0.0, 3.0, 1.65, 0.25, 0.5, 0.3, -0.7, nodes, 5, 6, n_min=3,
+                          forcings=[fi.random_legendre_forcing(3)]))
+    out.append(fi.Problem("P1", 0.0, 1.0, 1.3, 0.6, 1.0, 0.0, 0.0, fi.uniform_mesh(0, 1, 12), 1, 4, n_min=2,
+                          forcings=[fi.random_legendre_forcing(4)]))
+    return out
+
+
+_ORA = {}
+
+
+def oracle_system(p):
+    if p.name not in _ORA:
+        _ORA[p.name] = O.assemble_system(p)
+    return _ORA[p.name]
+
+
+@pytest.mark.parametrize("p", problems_small(), ids=lambda p: p.name)
+def test_assembly_matches_oracle(fde, h, p):
+    op = fde.assemble_problem(h, p)
+    Ag = fde.operator_dense_paper(h, op).cpu().numpy()
+    so = oracle_system(p)
+    assert metric_A(Ag, so.A) <= TOL
+    B = fde.operator_boundary_columns(h, op).cpu().numpy()
+    d = np.sqrt(np.abs(np.diag(so.A)))
+    for k in range(2):
+        Ab = so.Abnd[:, k]
+        # scale by sqrt(A_II * A_bb); boundary hat diagonal from the extended matrix
+        nb = p.n + k
+        Abb = p.rho * so.M_ext[nb, nb] + so.Sl_ext[nb, nb]
+        assert np.max(np.abs(B[k] - Ab) / (d * np.sqrt(abs(Abb)))) <= TOL
+    op.free()
+
+
+@pytest.mark.parametrize("p", problems_small(), ids=lambda p: p.name)
+def test_rhs_matches_oracle(fde, h, p):
+    if not p.forcings:
+        pytest.skip("no forcing")
+    op = fde.assemble_problem(h, p)
+    Gg = fde.sem_rhs(h, op, p.forcings).cpu().numpy()[0]
+    so = oracle_system(p)
+    Go = O.rhs(p, so, p.forcings[0])
+    scale = np.abs(Go).max() + 1e-300
+    assert np.max(np.abs(Gg - Go)) <= 1e-12 * scale + 1e-13
+    op.free()
+
+
+@pytest.mark.parametrize("p", problems_small(), ids=lambda p: p.name)
+def test_dense_matvec_matches_oracle(fde, h, p):
+    op = fde.assemble_problem(h, p)
+    so = oracle_system(p)
+    rng = np.random.default_rng(1)
+    X = rng.standard_normal((3, p.n))
+    Y = fde.stiffness_matvec(h, op, torch.tensor(X, device="cuda"), path=fde.PATH_DENSE).cpu().numpy()
+    Yo = (so.A.astype(np.longdouble) @ X.T.astype(np.longdouble)).T.astype(np.float64)
+    den = (np.abs(so.A) @ np.abs(X.T)).T
+    assert np.max(np.abs(Y - Yo) / den) <= TOL
+    op.free()
+
+
+@pytest.mark.parametrize("alpha", [1.2, 1.5, 1.8])
+@pytest.mark.parametrize("N", [24, 100])
+def test_toeplitz_fft_matvec_matches_oracle(fde, h, alpha, N):
+    p = fi.config2(alpha, N=N, P=8)
+    op = fde.assemble_problem(h, p, flags=fde.OP_DENSE | fde.OP_TOEPLITZ)
+    rng = np.random.default_rng(2)
+    X = torch.tensor(rng.standard_normal((2, p.n)), device="cuda")
+    Yf = fde.stiffness_matvec(h, op, X, path=fde.PATH_TOEPLITZ).cpu().numpy()
+    Yd = fde.stiffness_matvec(h, op, X, path=fde.PATH_DENSE).cpu().numpy()
+    Ag = fde.operator_dense_paper(h, op).cpu().numpy()
+    den = (np.abs(Ag) @ np.abs(X.cpu().numpy().T)).T
+    assert np.max(np.abs(Yf - Yd) / den) <= TOL
+    if N == 24:
+        so = oracle_system(p)
+        Yo = (so.A @ X.cpu().numpy().T).T
+        assert np.max(np.abs(Yf - Yo) / den) <= TOL
+    op.free()
+
+
+def test_toeplitz_rejects_nonuniform(fde, h):
+    p = fi.config4(N=16, P=4)
+    with pytest.raises(fde.FdeError) as e:
+        fde.assemble_problem(h, p, flags=fde.OP_TOEPLITZ)
+    assert e.value.name == "FDE_EUNSUPPORTED_MESH"
+
+
+@pytest.mark.parametrize("p", [fi.config1(), fi.config2(1.5, N=24, P=8), fi.config3(P=6)], ids=lambda p: p.name)
+def test_unpreconditioned_gmres_matches_oracle(fde, h, p):
+    op = fde.assemble_problem(h, p)
+    G = fde.sem_rhs(h, op, p.forcings)
+    X, rep = fde.solve(h, op, None, G, tol=1e-13, maxiter=4000, restart=200)
+    so = oracle_system(p)
+    Go = O.rhs(p, so, p.forcings[0])
+    Xo = O.solve_dense(so.A, Go)
+    x = X.cpu().numpy()[0]
+    D = np.abs(np.diag(so.A))
+    err = np.sqrt(np.sum(D * (x - Xo) ** 2) / np.sum(D * Xo ** 2))
+    assert err <= 1e-9, (err, rep.iterations)
+    op.free()
+
+
+@pytest.mark.parametrize("p", [fi.config1(), fi.config2(1.5, N=48, P=4), fi.config4(N=64, P=4)],
+                         ids=lambda p: p.name)
+@pytest.mark.parametrize("R", [3, 6])
+def test_hmatrix_matches_oracle(fde, h, p, R):
+    n_min = 2 if p.N <= 8 else 4
+    op = fde.assemble_problem(h, p)
+    hm = fde.hmatrix_build(h, op, R, 1.0, n_min)
+    Ag = fde.hmatrix_dense_paper(h, hm).cpu().numpy()
+    so = oracle_system(p)
+    At, part = O.hmatrix_dense(p, so, R=R, lam=1.0, n_min=n_min)
+    assert hm.info.nblocks_lr == sum(1 for _, _, k in part if k == "lr")
+    assert hm.info.nblocks_dense == sum(1 for _, _, k in part if k == "dense")
+    assert metric_A(Ag, At) <= TOL
+    hm.free()
+    op.free()
+
+
+def test_invalid_inputs_raise(fde, h):
+    p = fi.config1()
+    with pytest.raises(fde.FdeError) as e:
+        fde.sem_assemble(h, 0.0, 1.0, 2.5, 0.5, 1.0, 0, 0, p.nodes, 4)
+    assert e.value.name == "FDE_EINVAL_PARAM"
+    with pytest.raises(fde.FdeError) as e:
+        fde.sem_assemble(h, 1.0, 0.0, 1.5, 0.5, 1.0, 0, 0, p.nodes, 4)
+    assert e.value.name == "FDE_EINVAL_DOMAIN"
+    bad = p.nodes.copy()
+    bad[3] = bad[2]
+    with pytest.raises(fde.FdeError) as e:
+        fde.sem_assemble(h, 0.0, 1.0, 1.5, 0.5, 1.0, 0, 0, bad, 4)
+    assert e.value.name == "FDE_EINVAL_MESH"
+    with pytest.raises(fde.FdeError) as e:
+        fde.sem_assemble(h, 0.0, 1.0, 1.5, 0.5, 1.0, 0, 0, p.nodes, 0)
+    assert e.value.name == "FDE_EDEGREE"
