@@ -179,7 +179,7 @@ def config1_exact(x: np.ndarray) -> np.ndarray:
 def config2(alpha: float = 1.5, seed: Optional[int] = None, N: int = 256, P: int = 8) -> Problem:
     if seed is None:
         seed = {1.2: 0, 1.5: 1, 1.8: 2}.get(alpha, 0)
-    return Problem(f"c2-a{alpha}", 0.0, 1.0, alpha, 0.3, 1.0, 0.5, -1.0, uniform_mesh(0, 1, N), P, 8,
+    return Problem(f"c2-a{alpha}-N{N}-P{P}", 0.0, 1.0, alpha, 0.3, 1.0, 0.5, -1.0, uniform_mesh(0, 1, N), P, 8,
                    forcings=[random_legendre_forcing(seed)], mesh_kind="uniform")
 
 
@@ -202,12 +202,12 @@ def config4(N: int = 1024, P: int = 8) -> Problem:
             x[j] = 0.5 * (2.0 * j / N) ** 2
         else:
             x[j] = 1.0 - 0.5 * (2.0 * (N - j) / N) ** 2
-    return Problem("c4", 0.0, 1.0, 1.4, 0.7, 2.0, 0.0, 0.0, x, P, 12,
+    return Problem(f"c4-N{N}-P{P}", 0.0, 1.0, 1.4, 0.7, 2.0, 0.0, 0.0, x, P, 12,
                    forcings=[random_legendre_forcing(0)], mesh_kind="graded")
 
 
 def config5(N: int = 4096, P: int = 8, nrhs: int = 64) -> Problem:
-    return Problem("c5", 0.0, 1.0, 1.6, 0.4, 1.0, 0.0, 0.0, uniform_mesh(0, 1, N), P, 16,
+    return Problem(f"c5-N{N}-P{P}", 0.0, 1.0, 1.6, 0.4, 1.0, 0.0, 0.0, uniform_mesh(0, 1, N), P, 16,
                    forcings=[random_legendre_forcing(s) for s in range(nrhs)], mesh_kind="uniform")
 
 

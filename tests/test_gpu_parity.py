@@ -59,9 +59,10 @@ _ORA = {}
 
 
 def oracle_system(p):
-    if p.name not in _ORA:
-        _ORA[p.name] = O.assemble_system(p)
-    return _ORA[p.name]
+    key = (p.name, p.N, p.P, p.alpha, p.theta, p.rho, float(p.nodes.sum()))
+    if key not in _ORA:
+        _ORA[key] = O.assemble_system(p)
+    return _ORA[key]
 
 
 @pytest.mark.parametrize("p", problems_small(), ids=lambda p: p.name)
