@@ -89,7 +89,7 @@ typedef struct fde_lu* fde_hlu;
 
 /* ------------------------------------------------------------- context */
 /* device: CUDA ordinal; cuda_stream: cudaStream_t to order work on (NULL =
- * a library-owned stream); nccl_unique_id: 128-byte ncclUniqueId shared by all
+ * the legacy default stream, as in the CUDA runtime); nccl_unique_id: 128-byte ncclUniqueId shared by all
  * ranks (NULL => world must be 1); rank/world: this process in the job. */
 int fde_create(fde_handle* out, int device, void* cuda_stream, const void* nccl_unique_id,
                int rank, int world);
@@ -180,6 +180,12 @@ typedef struct {
     int32_t nops;          /* device operations issued                      */
 } fde_hlu_info;
 int fde_hlu_get_info(fde_hlu lu, fde_hlu_info* info);
+
+/* Test helper: the packed factors (strict lower part L_H, upper part U_H) as a
+ * dense n x n column-major device matrix in the INTERNAL element-interleaved
+ * order (dof r: element r/P; r%P < P-1 modal psi_{r%P+1}, r%P = P-1 hat of
+ * node r/P+1). */
+int fde_hlu_dense_internal(fde_handle h, fde_hlu lu, double* out, int64_t ldo);
 
 /* -------------------------------------------------------- precond_apply */
 /* z = U_H^{-1} L_H^{-1} r: hierarchical forward and backward substitution

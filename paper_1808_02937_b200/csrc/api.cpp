@@ -51,12 +51,10 @@ int fde_create(fde_handle* out, int device, void* cuda_stream, const void* nccl_
     h->rank = rank;
     h->world = world;
     FDE_CUDA(cudaSetDevice(device));
-    if (cuda_stream) {
-        h->stream = (cudaStream_t)cuda_stream;
-    } else {
-        FDE_CUDA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
-        h->own_stream = true;
-    }
+    // NULL is the legacy default stream (stream 0), as everywhere in CUDA;
+    // work is always ordered on the caller's stream.
+    h->stream = (cudaStream_t)cuda_stream;
+    h->own_stream = false;
     FDE_CUDA(cudaEventCreate(&h->ev0));
     FDE_CUDA(cudaEventCreate(&h->ev1));
     FDE_CUDA(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, device));
@@ -305,6 +303,20 @@ int fde_hlu_get_info(fde_hlu lu, fde_hlu_info* info)
     if (!lu || !info) return FDE_EINVAL_PARAM;
     hlu_info(lu, info);
     return FDE_OK;
+}
+
+int fde_hlu_dense_internal(fde_handle h, fde_hlu lu, double* out, int64_t ldo)
+{
+    API_BEGIN
+    hlu_dense_internal(h, lu, out, ldo);
+    API_END(h)
+}
+
+int fde_hlu_solve_debug(fde_handle h, fde_hlu lu, double* X, int64_t ldx, int nrhs, int which)
+{
+    API_BEGIN
+    hlu_solve_debug(h, lu, X, ldx, nrhs, which);
+    API_END(h)
 }
 
 int precond_apply(fde_handle h, fde_hlu lu, const double* r, double* z, int nrhs, int64_t ld)

@@ -37,7 +37,7 @@ EXPORTED = [
     "fde_create", "fde_destroy", "fde_last_error", "fde_sync", "fde_nccl_unique_id",
     "sem_assemble", "fde_operator_get_info", "fde_operator_dense_paper", "fde_operator_boundary_columns",
     "sem_rhs", "stiffness_matvec", "hmatrix_build", "fde_hmatrix_get_info", "fde_hmatrix_dense_paper",
-    "hlu_factor", "fde_hlu_get_info", "precond_apply", "solve", "fde_solve",
+    "hlu_factor", "fde_hlu_get_info", "fde_hlu_dense_internal", "precond_apply", "solve", "fde_solve",
     "fde_free_operator", "fde_free_hmatrix", "fde_free_hlu",
 ]
 
@@ -124,6 +124,7 @@ def lib():
         L.hlu_factor.argtypes = [vp, vp, dbl, ctypes.POINTER(vp)]
         L.fde_hlu_get_info.argtypes = [vp, ctypes.POINTER(HluInfo)]
         L.precond_apply.argtypes = [vp, vp, vp, vp, i32, i64]
+        L.fde_hlu_dense_internal.argtypes = [vp, vp, vp, i64]
         L.solve.argtypes = [vp, vp, vp, vp, vp, i32, i64, ctypes.POINTER(SolveOpts), ctypes.POINTER(SolveReport)]
         L.fde_free_operator.argtypes = [vp]
         L.fde_free_operator.restype = None
@@ -313,6 +314,21 @@ def hlu_factor(handle: Handle, hm: HMatrix, tol: float = 1e-3) -> HLU:
     out = ctypes.c_void_p()
     _check(lib().hlu_factor(handle.h, hm.ptr, tol, ctypes.byref(out)), handle.h)
     return HLU(handle, out, hm.n)
+
+
+def hlu_dense_internal(handle: Handle, lu: HLU):
+    import torch
+    F = torch.zeros((lu.n, lu.n), dtype=torch.float64, device=f"cuda:{handle.device}")
+    _check(lib().fde_hlu_dense_internal(handle.h, lu.ptr, _ptr(F), lu.n), handle.h)
+    return F.t()   # column-major buffer -> [I, J]
+
+
+def internal_to_paper_index(N: int, P: int):
+    """paper index of every internal (element-interleaved) dof (fde.h convention)."""
+    import numpy as np
+    r = np.arange(N * P - 1)
+    e, q = r // P, r % P
+    return np.where(q < P - 1, e * (P - 1) + q, N * (P - 1) + e)
 
 
 def precond_apply(handle: Handle, lu: HLU, r, out=None):

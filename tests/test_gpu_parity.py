@@ -182,3 +182,60 @@ def test_invalid_inputs_raise(fde, h):
     with pytest.raises(fde.FdeError) as e:
         fde.sem_assemble(h, 0.0, 1.0, 1.5, 0.5, 1.0, 0, 0, p.nodes, 0)
     assert e.value.name == "FDE_EDEGREE"
+
+
+# ------------------------------------------------------------------ H-LU
+HLU_CASES = [
+    (fi.config1(), 2),
+    (fi.config2(1.5, N=48, P=4), 4),
+    (fi.config4(N=64, P=4), 4),
+    (fi.config3(P=4), 4),
+]
+
+
+@pytest.mark.parametrize("case", HLU_CASES, ids=lambda c: c[0].name)
+def test_hlu_exact_mode_equals_dense_solve_of_Atilde(fde, h, case):
+    """tol = 0: the formatted H-LU is the exact LU of A~ (up to rounding), so
+    precond_apply must equal a dense solve with the oracle's A~ (metric M-C)."""
+    p, n_min = case
+    op = fde.assemble_problem(h, p)
+    hm = fde.hmatrix_build(h, op, p.R, 1.0, n_min)
+    lu = fde.hlu_factor(h, hm, 0.0)
+    so = oracle_system(p)
+    At, _ = O.hmatrix_dense(p, so, R=p.R, lam=1.0, n_min=n_min)
+    rng = np.random.default_rng(5)
+    r = rng.standard_normal((2, p.n))
+    z = fde.precond_apply(h, lu, torch.tensor(r, device="cuda")).cpu().numpy()
+    zo = np.linalg.solve(At, r.T).T
+    err = np.linalg.norm(z - zo) / np.linalg.norm(zo)
+    assert err <= TOL, err
+    for o in (lu, hm, op):
+        o.free()
+
+
+@pytest.mark.parametrize("case", HLU_CASES, ids=lambda c: c[0].name)
+def test_hlu_preconditioned_gmres_matches_oracle(fde, h, case):
+    """tol = 1e-3: A~^{-1} is only approximate (parity unpinned
+    for the factor itself), but the preconditioned solve must reach the oracle's
+    X (metric M-D) and need fewer iterations than the unpreconditioned one."""
+    p, n_min = case
+    op = fde.assemble_problem(h, p)
+    hm = fde.hmatrix_build(h, op, p.R, 1.0, n_min)
+    lu = fde.hlu_factor(h, hm, 1e-3)
+    G = fde.sem_rhs(h, op, p.forcings)
+    X, rep = fde.solve(h, op, lu, G, tol=1e-13)
+    X0, rep0 = fde.solve(h, op, None, G, tol=1e-13, maxiter=5000, restart=200)
+    so = oracle_system(p)
+    Xo = O.solve_dense(so.A, O.rhs(p, so, p.forcings[0]))
+    x = X.cpu().numpy()[0]
+    D = np.abs(np.diag(so.A))
+    err = np.sqrt(np.sum(D * (x - Xo) ** 2) / np.sum(D * Xo ** 2))
+    assert err <= 1e-9, err
+    assert rep.iterations < rep0.iterations
+    # the factor approximates A~: ||A~ z - r|| small relative to ||r||
+    At, _ = O.hmatrix_dense(p, so, R=p.R, lam=1.0, n_min=n_min)
+    r = np.random.default_rng(6).standard_normal(p.n)
+    z = fde.precond_apply(h, lu, torch.tensor(r, device="cuda")).cpu().numpy()[0]
+    assert np.linalg.norm(At @ z - r) / np.linalg.norm(r) < 5e-2
+    for o in (lu, hm, op):
+        o.free()
