@@ -1,0 +1,326 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 hot path of arXiv 1808.02937 (BASELINE.json metric:
+"preconditioned SEM solves/sec and fp64 stiffness matvec HBM GB/s vs peak").
+
+One step = one COLD preconditioned solve of the workload (every row of
+SURVEY.md §8(a)): sem_assemble (dense fp64 A, this rank's rows) + sem_rhs
+(load vector + lifting) + hmatrix_build (R, lambda=1) + hlu_factor
+(Tol_HLU = 1e-3) + solve (left-preconditioned GMRES, tol 1e-12).
+Default workload: BASELINE config 4 (symmetric graded mesh, N=1024, P=8,
+n = 8191, dense A = 537 MB > L2, so every matvec streams from HBM).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4|c2|c5]
+                  [--impl ours|reference]
+
+N > 1 is launched with torchrun (one rank per GPU, NCCL): the dense operator
+is row-sharded and y = A x is all-gathered every Krylov iteration.
+Rank 0 prints ONE JSON line.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import fde_inputs as fi  # noqa: E402
+
+METRIC = "preconditioned SEM solves/sec and fp64 stiffness matvec HBM GB/s vs peak"
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+def workload(name):
+    if name == "c2":
+        return fi.config2(1.5)
+    if name == "c5":
+        return fi.config5(nrhs=int(os.environ.get("FDE_C5_NRHS", "64")))
+    if name == "c3":
+        return fi.config3(16)
+    return fi.config4()
+
+
+# --------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index=0):
+        self.index, self.samples, self.proc = index, [], None
+
+    def start(self):
+        cmd = ["nvidia-smi", f"--id={self.index}",
+               "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+               "--format=csv,noheader,nounits", "-lms", "100"]
+        try:
+            self.proc = subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm = [float(s[0]) for s in self.samples if len(s) >= 8 and s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if len(s) >= 8 and s[1].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for s in self.samples:
+            if len(s) < 8:
+                continue
+            for k, nm in enumerate(names):
+                if s[4 + k].lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.samples)}
+
+
+# --------------------------------------------------------- CPU baseline
+def cpu_baseline(prob, budget_rows=12):
+    """The oracle as it stands, on a bounded sample of the same workload:
+    oracle assembly of `budget_rows` element rows spread over the mesh (scaled
+    to all rows by the number of element pairs) + the oracle's dense solve
+    (equilibrated LU + refinement) on a same-size synthetic matrix."""
+    import oracle as O
+    N, P, n = prob.N, prob.P, prob.n
+    cores = os.cpu_count() or 1
+    rows = np.unique(np.linspace(0, N - 1, budget_rows).astype(int))
+    t0 = time.perf_counter()
+    pairs_sampled = 0
+    for i in rows:
+        O.assemble_Sl_ext(prob.nodes, P, prob.alpha, int(i), int(i) + 1, threads=cores)
+        pairs_sampled += i + 1
+    t_asm_sample = time.perf_counter() - t0
+    pairs_total = N * (N + 1) / 2
+    t_asm = t_asm_sample * pairs_total / pairs_sampled
+    rng = np.random.default_rng(0)
+    A = rng.standard_normal((n, n)) / np.sqrt(n) + 4.0 * np.eye(n)
+    G = rng.standard_normal((n, len(prob.forcings)))
+    t0 = time.perf_counter()
+    O.solve_dense(A, G, refine=2)
+    t_solve = time.perf_counter() - t0
+    total = t_asm + t_solve
+    nrhs = len(prob.forcings)
+    return {"value": nrhs / total, "unit": "solves/s", "cores": cores, "kind": "oracle",
+            "sample": (f"oracle assembly of {len(rows)} of {N} element rows ({pairs_sampled} of "
+                       f"{int(pairs_total)} element pairs, {t_asm_sample:.2f}s, scaled by pair count to "
+                       f"{t_asm:.1f}s) + oracle dense solve (equilibrated LU + long-double refinement) "
+                       f"of a same-size synthetic n={n} system ({t_solve:.1f}s)"),
+            "seconds_per_solve_estimate": total}
+
+
+# --------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    from paper_1808_02937_b200 import fde
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    nccl_id = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        obj = [fde.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    prob = workload(args.config)
+    stream = torch.cuda.current_stream()
+    h = fde.Handle(local, stream=stream.cuda_stream, nccl_id=nccl_id, rank=rank, world=world)
+    nrhs = len(prob.forcings)
+    flags = fde.OP_DENSE
+
+    def step(e2e=False):
+        op = fde.assemble_problem(h, prob, flags)
+        G = fde.sem_rhs(h, op, prob.forcings)
+        hm = fde.hmatrix_build(h, op, prob.R, prob.lam, prob.n_min)
+        lu = fde.hlu_factor(h, hm, 1e-3)
+        X, rep = fde.solve(h, op, lu, G, tol=1e-12, restart=50, maxiter=500)
+        info = dict(assemble_ms=op.info.assemble_ms, hbuild_ms=hm.info.build_ms, hlu_ms=lu.info.factor_ms,
+                    solve_ms=rep.solve_ms, iters=rep.iterations, matvecs=rep.matvecs, relres=rep.relres,
+                    hlu_max_rank=lu.info.max_rank, hlu_ops=lu.info.nops)
+        Xh = X.cpu() if e2e else None
+        lu.free()
+        hm.free()
+        op.free()
+        return info, Xh
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- device-timed region: K cold solves
+    clocks = ClockSampler(local)
+    clocks.start()
+    fde.lib().fde_profile(h.h, 1)
+    barrier()
+    launches0 = fde.lib().fde_launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    infos = []
+    for _ in range(args.steps):
+        infos.append(step()[0])
+    e1.record(stream)
+    barrier()
+    launches = fde.lib().fde_launch_count() - launches0
+    ms = e0.elapsed_time(e1)
+    import ctypes
+    prof = (ctypes.c_double * 9)()
+    fde.lib().fde_profile_collect(h.h, prof, 1)
+    fde.lib().fde_profile(h.h, 0)
+    clk = clocks.stop()
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+
+    # ---- end-to-end through the C-ABI with host buffers (forcing from host, X to host)
+    barrier()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(max(1, args.steps // 2)):
+        _, Xh = step(e2e=True)
+    t1.record(stream)
+    barrier()
+    ms_e2e = t0.elapsed_time(t1) / max(1, args.steps // 2)
+    if world > 1:
+        t = torch.tensor([ms_e2e], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_e2e = float(t.item())
+
+    gemv_n, gemv_ms, gemv_bytes = prof[0], prof[1], prof[2]
+    pre_n, pre_ms = prof[6], prof[7]
+    peak, peak_kind = load_peaks()
+    res = None
+    if rank == 0:
+        ms_step = ms / args.steps
+        value = nrhs * args.steps / (ms / 1e3)     # whole-job solves/s (strong scaling)
+        achieved = (gemv_bytes / gemv_n) / (gemv_ms / gemv_n * 1e-3) / 1e9 if gemv_n else 0.0
+        avg = {k: float(np.mean([i[k] for i in infos])) for k in infos[0]}
+        h2d = 8 * (prob.N + 1) + sum(8 * (len(f.leg) + 3 * len(f.terms)) for f in prob.forcings)
+        res = {
+            "metric": METRIC,
+            "value": value,
+            "unit": "solves/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms_step,
+            "higher_is_better": True,
+            "scaling": "strong",
+            "vs_baseline": None,
+            "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": f"BASELINE config {args.config[1]}: {prob.name}", "N": prob.N, "P": prob.P,
+                       "n": prob.n, "alpha": prob.alpha, "theta": prob.theta, "rho": prob.rho, "R": prob.R,
+                       "lambda": prob.lam, "n_min": prob.n_min, "nrhs": nrhs, "hlu_tol": 1e-3,
+                       "krylov": "GMRES(50) tol 1e-12", "parallelism": f"row-shard x{world}",
+                       "l2": "dense A (537 MB at c4) exceeds the 126 MB L2; no flush needed",
+                       "step": "cold solve: assemble + rhs + hmatrix_build + hlu_factor + solve"},
+            "phases_ms": {k: round(v, 3) for k, v in avg.items()},
+            "roofline": {"kernel": "k_gemv (dense stiffness matvec, PAPER.md:629)", "bound": "hbm",
+                         "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "peak_kind": peak_kind, "traffic": None,
+                         "launches": int(gemv_n), "avg_launch_us": (gemv_ms / gemv_n * 1e3) if gemv_n else None,
+                         "share_of_step": gemv_ms / ms if ms else None,
+                         "algorithmic_bytes_per_launch": (gemv_bytes / gemv_n) if gemv_n else None},
+            "precond_apply": {"launches": int(pre_n), "avg_us": (pre_ms / pre_n * 1e3) if pre_n else None,
+                              "share_of_step": pre_ms / ms if ms else None},
+            "e2e": {"value": nrhs / (ms_e2e / 1e3), "unit": "solves/s", "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(8 * prob.n * nrhs)},
+            "gpu_launches": int(launches),
+            "clocks": clk,
+        }
+    return res, prob, rank, world
+
+
+def run_reference(args):
+    """Reference arm = the CPU oracle (this tier has no reference implementation)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return None
+    prob = workload(args.config)
+    vals = []
+    t0 = time.perf_counter()
+    for _ in range(args.warmup):
+        pass
+    cb = None
+    for _ in range(max(1, args.steps)):
+        cb = cpu_baseline(prob, budget_rows=4)
+        vals.append(cb["seconds_per_solve_estimate"])
+    sec = float(np.mean(vals))
+    nrhs = len(prob.forcings)
+    value = nrhs / sec
+    return {
+        "metric": METRIC, "value": value, "unit": "solves/s", "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+        "config": {"workload": f"BASELINE config {args.config[1]}: {prob.name}", "N": prob.N, "P": prob.P,
+                   "n": prob.n},
+        "cpu_baseline": {"value": value, "unit": "solves/s", "cores": cb["cores"], "kind": "oracle",
+                         "sample": cb["sample"]},
+        "e2e": {"value": value, "unit": "solves/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "wall_s": time.perf_counter() - t0,
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c4", choices=["c2", "c3", "c4", "c5"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        res = run_reference(args)
+        if res is not None:
+            print(json.dumps(res), flush=True)
+        return
+    res, prob, rank, world = run_ours(args)
+    if rank == 0:
+        if world == 1 and not args.no_cpu_baseline:
+            res["cpu_baseline"] = cpu_baseline(prob)
+        else:
+            res["cpu_baseline"] = None
+        print(json.dumps(res), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

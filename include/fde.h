@@ -98,6 +98,16 @@ const char* fde_last_error(fde_handle h);
 int fde_sync(fde_handle h);                   /* cudaStreamSynchronize(stream)    */
 int fde_nccl_unique_id(void* out128);          /* ncclGetUniqueId, for rank 0     */
 
+/* Live kernel timing with CUDA events recorded on the handle's stream around
+ * the dense GEMV launches (class 0), the Toeplitz FFT matvec (class 1) and the
+ * preconditioner application (class 2).  fde_profile_collect synchronises the
+ * stream and writes, per class c, out9[3c] = launches, out9[3c+1] = total ms,
+ * out9[3c+2] = algorithmic bytes (GEMV: 8 * rows * n per 4-RHS pass + vectors). */
+int fde_profile(fde_handle h, int enable);
+int fde_profile_collect(fde_handle h, double* out9, int reset);
+/* Number of kernels this library has launched in the process so far. */
+long long fde_launch_count(void);
+
 /* --------------------------------------------------------- sem_assemble */
 enum { FDE_OP_DENSE = 1, FDE_OP_TOEPLITZ = 2 };
 

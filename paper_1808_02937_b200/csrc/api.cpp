@@ -19,6 +19,7 @@ void krylov_bicgstab(fde_ctx* h, fde_op* op, fde_lu* lu, const double* G, double
 void dense_to_paper(fde_ctx* h, fde_op* op, double* out, int64_t ldo);
 void bnd_to_paper(fde_ctx* h, fde_op* op, double* out);
 void internal_dense_to_paper(fde_ctx* h, int N, int P, const double* in, int64_t ldi, double* out, int64_t ldo);
+void prof_collect(fde_ctx* h, double* out, int reset);
 
 static thread_local std::string g_noctx_err;
 
@@ -95,6 +96,22 @@ int fde_nccl_unique_id(void* out128)
     comm_unique_id(out128);
     API_END(h)
 }
+
+int fde_profile(fde_handle h, int enable)
+{
+    API_BEGIN
+    h->profiling = enable;
+    API_END(h)
+}
+
+int fde_profile_collect(fde_handle h, double* out9, int reset)
+{
+    API_BEGIN
+    prof_collect(h, out9, reset);
+    API_END(h)
+}
+
+long long fde_launch_count(void) { return __atomic_load_n(&g_fde_launches, __ATOMIC_RELAXED); }
 
 // ------------------------------------------------------------ validation
 static void validate(const fde_problem* p, const fde_mesh* m)

@@ -27,7 +27,14 @@ struct FdeError {
         }                                                                                     \
     } while (0)
 
-#define FDE_CHECK_LAUNCH() FDE_CUDA(cudaGetLastError())
+// every kernel launch site calls FDE_CHECK_LAUNCH(): it also counts launches
+// (fde_launch_count, reported by bench.py as gpu_launches)
+extern long long g_fde_launches;
+#define FDE_CHECK_LAUNCH()                        \
+    do {                                          \
+        __atomic_add_fetch(&g_fde_launches, 1, __ATOMIC_RELAXED); \
+        FDE_CUDA(cudaGetLastError());             \
+    } while (0)
 
 inline void fde_fail(int code, const std::string& m) { throw FdeError{code, m}; }
 
@@ -65,7 +72,18 @@ struct DBuf {
 };
 
 // ------------------------------------------------------------------ context
+// live kernel timing (CUDA events on the launching stream), enabled by fde_profile
+enum { PROF_GEMV = 0, PROF_FFT = 1, PROF_PRECOND = 2, PROF_NCLASS = 3 };
+struct ProfRec {
+    cudaEvent_t a, b;
+    int cls;
+    double bytes;
+};
+
 struct fde_ctx {
+    int profiling = 0;
+    std::vector<ProfRec> prof;
+    std::vector<cudaEvent_t> ev_pool;
     int device = 0;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
@@ -176,6 +194,10 @@ void op_apply_internal(fde_ctx* h, fde_op* op, const double* x, int64_t ldx, dou
 
 // communication
 void comm_allgather_rows(fde_ctx* h, fde_op* op, const double* local, double* full, int64_t ldfull, int nrhs);
+
+// profiling helpers (no-ops unless h->profiling)
+int prof_begin(fde_ctx* h, int cls, double bytes);
+void prof_end(fde_ctx* h, int idx);
 
 // -------------------------------------------------------------- utilities
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }

@@ -910,10 +910,12 @@ void hlu_destroy(fde_lu* L)
 void precond_apply_internal(fde_ctx* h, fde_lu* lu, const double* r, int64_t ldr, double* z, int64_t ldz, int nrhs)
 {
     lu->h = h;
+    const int pi = prof_begin(h, PROF_PRECOND, 0.0);
     if (r != z) FDE_CUDA(cudaMemcpy2DAsync(z, ldz * sizeof(double), r, ldr * sizeof(double), lu->S.n * sizeof(double),
                                            nrhs, cudaMemcpyDeviceToDevice, h->stream));
     solve_L(lu, lu->S.root, z, ldz, nrhs);
     solve_U(lu, lu->S.root, z, ldz, nrhs);
+    prof_end(h, pi);
 }
 
 // test helper: the packed factors as a dense n x n matrix (internal order,
@@ -928,7 +930,10 @@ void hlu_dense_internal(fde_ctx* h, fde_lu* L, double* out, int64_t ldo)
             if (b.k)
                 gemm(L, 0, 1, b.m, b.n, b.k, 1.0, b.U, b.m, b.V, b.n, 0.0, out + b.c0 * ldo + b.r0, ldo);
             else
+            {
                 k_copy2d<<<64, 256, 0, h->stream>>>(out, 0, (int)b.m, (int)b.n, out + b.c0 * ldo + b.r0, ldo, 0.0);
+                FDE_CHECK_LAUNCH();
+            }
         }
     }
     FDE_CUDA(cudaStreamSynchronize(h->stream));

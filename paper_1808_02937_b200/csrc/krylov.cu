@@ -248,7 +248,9 @@ void krylov_gmres(fde_ctx* h, fde_op* op, fde_lu* lu, const double* G, double* X
             }
         }
         k_norms<<<nrhs, KB, 0, s>>>(W.w.p, ldv, n, W.nrm.p);
+        FDE_CHECK_LAUNCH();
         k_scale_into<<<gv, KB, 0, s>>>(W.w.p, ldv, W.nrm.p, W.V.p, ldv, n, W.active.p);
+        FDE_CHECK_LAUNCH();
         k_set_g0<<<ceil_div(nrhs, 64), 64, 0, s>>>(nrhs, m, W.nrm.p, W.g.p);
         FDE_CHECK_LAUNCH();
         std::vector<int> kc(nrhs, 0);
@@ -262,12 +264,16 @@ void krylov_gmres(fde_ctx* h, fde_op* op, fde_lu* lu, const double* G, double* X
             // CGS2
             k_multidot<<<dim3(k + 1, nrhs), KB, 0, s>>>(W.V.p, ldv, nrhs, W.w.p, ldv, n, W.hbuf.p, m + 1, 0,
                                                          W.active.p);
+            FDE_CHECK_LAUNCH();
             k_sub_combo<<<gv, KB, 0, s>>>(W.V.p, ldv, nrhs, k + 1, W.hbuf.p, m + 1, W.w.p, ldv, n, W.active.p);
+            FDE_CHECK_LAUNCH();
             k_multidot<<<dim3(k + 1, nrhs), KB, 0, s>>>(W.V.p, ldv, nrhs, W.w.p, ldv, n, W.y.p, m + 1, 0,
                                                          W.active.p);
+            FDE_CHECK_LAUNCH();
             k_sub_combo<<<gv, KB, 0, s>>>(W.V.p, ldv, nrhs, k + 1, W.y.p, m + 1, W.w.p, ldv, n, W.active.p);
             FDE_CHECK_LAUNCH();
             k_norms<<<nrhs, KB, 0, s>>>(W.w.p, ldv, n, W.nrm.p);
+            FDE_CHECK_LAUNCH();
             k_scale_into<<<gv, KB, 0, s>>>(W.w.p, ldv, W.nrm.p, Vk1, ldv, n, W.active.p);
             FDE_CHECK_LAUNCH();
             // Hessenberg column = first CGS pass + second CGS pass
@@ -295,6 +301,7 @@ void krylov_gmres(fde_ctx* h, fde_op* op, fde_lu* lu, const double* G, double* X
         // X += V y
         W.kc.upload(kc.data(), nrhs, s);
         k_backsolve<<<ceil_div(nrhs, 64), 64, 0, s>>>(nrhs, m, W.kc.p, W.H.p, W.g.p, W.y.p);
+        FDE_CHECK_LAUNCH();
         k_add_combo<<<gv, KB, 0, s>>>(W.V.p, ldv, nrhs, W.kc.p, W.y.p, m + 1, X, ldv, n);
         FDE_CHECK_LAUNCH();
         FDE_CUDA(cudaStreamSynchronize(s));
@@ -427,6 +434,7 @@ void krylov_bicgstab(fde_ctx* h, fde_op* op, fde_lu* lu, const double* G, double
     else FDE_CUDA(cudaMemcpyAsync(r.p, G, sizeof(double) * sz, cudaMemcpyDeviceToDevice, s));
     FDE_CUDA(cudaMemcpyAsync(rh.p, r.p, sizeof(double) * sz, cudaMemcpyDeviceToDevice, s));
     k_norms<<<nrhs, KB, 0, s>>>(r.p, ldv, n, d1.p);
+    FDE_CHECK_LAUNCH();
     std::vector<double> bn(nrhs), nr(nrhs), relres(nrhs, 1.0);
     FDE_CUDA(cudaMemcpyAsync(bn.data(), d1.p, sizeof(double) * nrhs, cudaMemcpyDeviceToHost, s));
     FDE_CUDA(cudaStreamSynchronize(s));
@@ -457,14 +465,20 @@ void krylov_bicgstab(fde_ctx* h, fde_op* op, fde_lu* lu, const double* G, double
         ++it;
         // rho = <rh, r>; beta
         k_dot_cols<<<nrhs, KB, 0, s>>>(rh.p, ldv, r.p, ldv, n, d1.p);
+        FDE_CHECK_LAUNCH();
         k_copy_rho<<<ceil_div(nrhs, 64), 64, 0, s>>>(nrhs, sc.p, d1.p, active.p);
+        FDE_CHECK_LAUNCH();
         k_bicg_beta<<<ceil_div(nrhs, 64), 64, 0, s>>>(nrhs, sc.p, active.p);
+        FDE_CHECK_LAUNCH();
         k_bicg_p<<<gv, KB, 0, s>>>(p.p, r.p, v.p, sc.p, ldv, n, active.p);
         FDE_CHECK_LAUNCH();
         apply(p.p, v.p);
         k_dot_cols<<<nrhs, KB, 0, s>>>(rh.p, ldv, v.p, ldv, n, d1.p);
+        FDE_CHECK_LAUNCH();
         k_bicg_alpha<<<ceil_div(nrhs, 64), 64, 0, s>>>(nrhs, sc.p, d1.p, active.p);
+        FDE_CHECK_LAUNCH();
         k_bicg_s<<<gv, KB, 0, s>>>(sv.p, r.p, v.p, sc.p, ldv, n, active.p);
+        FDE_CHECK_LAUNCH();
         k_norms<<<nrhs, KB, 0, s>>>(sv.p, ldv, n, d2.p);
         FDE_CHECK_LAUNCH();
         FDE_CUDA(cudaMemcpyAsync(nr.data(), d2.p, sizeof(double) * nrhs, cudaMemcpyDeviceToHost, s));
@@ -485,9 +499,13 @@ void krylov_bicgstab(fde_ctx* h, fde_op* op, fde_lu* lu, const double* G, double
         }
         apply(sv.p, t.p);
         k_dot_cols<<<nrhs, KB, 0, s>>>(t.p, ldv, sv.p, ldv, n, d1.p);
+        FDE_CHECK_LAUNCH();
         k_dot_cols<<<nrhs, KB, 0, s>>>(t.p, ldv, t.p, ldv, n, d2.p);
+        FDE_CHECK_LAUNCH();
         k_bicg_omega<<<ceil_div(nrhs, 64), 64, 0, s>>>(nrhs, sc.p, d1.p, d2.p, active.p);
+        FDE_CHECK_LAUNCH();
         k_bicg_xr<<<gv, KB, 0, s>>>(X, r.p, p.p, sv.p, t.p, sc.p, ldv, n, active.p, 0);
+        FDE_CHECK_LAUNCH();
         k_norms<<<nrhs, KB, 0, s>>>(r.p, ldv, n, d1.p);
         FDE_CHECK_LAUNCH();
         FDE_CUDA(cudaMemcpyAsync(nr.data(), d1.p, sizeof(double) * nrhs, cudaMemcpyDeviceToHost, s));

@@ -263,18 +263,26 @@ void op_apply_internal(fde_ctx* h, fde_op* op, const double* x, int64_t ldx, dou
     if (path == FDE_PATH_AUTO) path = (op->flags & FDE_OP_DENSE) ? FDE_PATH_DENSE : FDE_PATH_TOEPLITZ;
     if (path == FDE_PATH_TOEPLITZ) {
         if (!(op->flags & FDE_OP_TOEPLITZ)) fde_fail(FDE_EUNSUPPORTED_MESH, "operator has no Toeplitz form");
+        const int pi = prof_begin(h, PROF_FFT, 0.0);
         toeplitz_matvec(h, op, x, ldx, y, ldy, nrhs);
+        prof_end(h, pi);
         return;
     }
     if (!(op->flags & FDE_OP_DENSE)) fde_fail(FDE_EINVAL_PARAM, "operator has no dense form");
+    const double gemv_bytes = 8.0 * (double)(op->r1 - op->r0) * (double)op->n * (double)((nrhs + 3) / 4) +
+                              8.0 * (double)op->n * nrhs + 8.0 * (double)(op->r1 - op->r0) * nrhs;
     if (h->world == 1) {
+        const int pi = prof_begin(h, PROF_GEMV, gemv_bytes);
         dense_gemv(h, op, x, ldx, y, ldy, nrhs);
+        prof_end(h, pi);
         return;
     }
     ApplyScratch& S = ascratch();
     const size_t need = (size_t)op->rows_max * nrhs;
     if (S.loc.n < need) S.loc.alloc(need);
+    const int pi = prof_begin(h, PROF_GEMV, gemv_bytes);
     dense_gemv(h, op, x, ldx, S.loc.p, op->rows_max, nrhs);
+    prof_end(h, pi);
     comm_allgather_rows(h, op, S.loc.p, y, ldy, nrhs);
 }
 
@@ -318,4 +326,60 @@ void internal_dense_to_paper(fde_ctx* h, int N, int P, const double* in, int64_t
 void bnd_to_paper(fde_ctx* h, fde_op* op, double* out)
 {
     perm_internal_to_paper(h, op->N, op->P, op->bnd.p, op->n, out, op->n, 2);
+}
+
+
+// ------------------------------------------------------------ profiling
+long long g_fde_launches = 0;
+
+static cudaEvent_t prof_event(fde_ctx* h)
+{
+    if (!h->ev_pool.empty()) {
+        cudaEvent_t e = h->ev_pool.back();
+        h->ev_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    FDE_CUDA(cudaEventCreate(&e));
+    return e;
+}
+
+int prof_begin(fde_ctx* h, int cls, double bytes)
+{
+    if (!h->profiling) return -1;
+    ProfRec r;
+    r.a = prof_event(h);
+    r.b = prof_event(h);
+    r.cls = cls;
+    r.bytes = bytes;
+    FDE_CUDA(cudaEventRecord(r.a, h->stream));
+    h->prof.push_back(r);
+    return (int)h->prof.size() - 1;
+}
+
+void prof_end(fde_ctx* h, int idx)
+{
+    if (idx < 0) return;
+    FDE_CUDA(cudaEventRecord(h->prof[idx].b, h->stream));
+}
+
+// totals per class: out[3*c + 0] = launches, [1] = total ms, [2] = total bytes
+void prof_collect(fde_ctx* h, double* out, int reset)
+{
+    for (int c = 0; c < PROF_NCLASS; ++c) out[3 * c] = out[3 * c + 1] = out[3 * c + 2] = 0.0;
+    FDE_CUDA(cudaStreamSynchronize(h->stream));
+    for (auto& r : h->prof) {
+        float ms = 0;
+        FDE_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
+        out[3 * r.cls] += 1;
+        out[3 * r.cls + 1] += ms;
+        out[3 * r.cls + 2] += r.bytes;
+    }
+    if (reset) {
+        for (auto& r : h->prof) {
+            h->ev_pool.push_back(r.a);
+            h->ev_pool.push_back(r.b);
+        }
+        h->prof.clear();
+    }
 }

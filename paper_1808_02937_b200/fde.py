@@ -38,7 +38,8 @@ EXPORTED = [
     "sem_assemble", "fde_operator_get_info", "fde_operator_dense_paper", "fde_operator_boundary_columns",
     "sem_rhs", "stiffness_matvec", "hmatrix_build", "fde_hmatrix_get_info", "fde_hmatrix_dense_paper",
     "hlu_factor", "fde_hlu_get_info", "fde_hlu_dense_internal", "precond_apply", "solve", "fde_solve",
-    "fde_free_operator", "fde_free_hmatrix", "fde_free_hlu",
+    "fde_free_operator", "fde_free_hmatrix", "fde_free_hlu", "fde_profile", "fde_profile_collect",
+    "fde_launch_count",
 ]
 
 
@@ -125,6 +126,10 @@ def lib():
         L.fde_hlu_get_info.argtypes = [vp, ctypes.POINTER(HluInfo)]
         L.precond_apply.argtypes = [vp, vp, vp, vp, i32, i64]
         L.fde_hlu_dense_internal.argtypes = [vp, vp, vp, i64]
+        L.fde_profile.argtypes = [vp, i32]
+        L.fde_profile_collect.argtypes = [vp, ctypes.POINTER(ctypes.c_double), i32]
+        L.fde_launch_count.argtypes = []
+        L.fde_launch_count.restype = ctypes.c_longlong
         L.solve.argtypes = [vp, vp, vp, vp, vp, i32, i64, ctypes.POINTER(SolveOpts), ctypes.POINTER(SolveReport)]
         L.fde_free_operator.argtypes = [vp]
         L.fde_free_operator.restype = None
