@@ -20,6 +20,7 @@ void dense_to_paper(fde_ctx* h, fde_op* op, double* out, int64_t ldo);
 void bnd_to_paper(fde_ctx* h, fde_op* op, double* out);
 void internal_dense_to_paper(fde_ctx* h, int N, int P, const double* in, int64_t ldi, double* out, int64_t ldo);
 void prof_collect(fde_ctx* h, double* out, int reset);
+void hlu_trunc_stats(unsigned long long* out4);
 
 static thread_local std::string g_noctx_err;
 
@@ -59,6 +60,15 @@ int fde_create(fde_handle* out, int device, void* cuda_stream, const void* nccl_
     FDE_CUDA(cudaEventCreate(&h->ev0));
     FDE_CUDA(cudaEventCreate(&h->ev1));
     FDE_CUDA(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, device));
+    {
+        // keep freed stream-ordered allocations in the pool (the H-LU allocates
+        // and frees many small temporaries; returning them to the OS at every
+        // synchronisation costs tens of microseconds per allocation)
+        cudaMemPool_t pool;
+        FDE_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+        uint64_t thr = UINT64_MAX;
+        FDE_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    }
     if (world > 1) comm_init(h, nccl_unique_id);
     *out = h;
     }
@@ -108,6 +118,14 @@ int fde_profile_collect(fde_handle h, double* out9, int reset)
 {
     API_BEGIN
     prof_collect(h, out9, reset);
+    API_END(h)
+}
+
+int fde_debug_trunc_stats(unsigned long long* out4)
+{
+    fde_ctx* h = nullptr;
+    API_BEGIN
+    hlu_trunc_stats(out4);
     API_END(h)
 }
 

@@ -14,6 +14,7 @@
 // (dense LU of the leaves, triangular solves, GEMMs, Gram matrices, the small
 // Jacobi eigen-solves of the truncation) is a CUDA kernel.  The truncated rank
 // is the only value read back (one pinned word per truncation).
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 
@@ -76,6 +77,92 @@ __global__ void __launch_bounds__(256) k_gemm(int m, int n, int k, double alpha,
         }
 }
 
+// split-K partial: W[z][m x n] = op(A)[:, kz] op(B)[kz, :]
+__global__ void __launch_bounds__(256) k_gemm_splitk(int m, int n, int k, int chunk, const double* __restrict__ A,
+                                                    long long lda, int ta, const double* __restrict__ B, long long ldb,
+                                                    int tb, double* __restrict__ W)
+{
+    __shared__ double sA[GK][GT + 1];
+    __shared__ double sB[GK][GT + 1];
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    const int m0 = blockIdx.x * GT, n0 = blockIdx.y * GT;
+    const int kb = blockIdx.z * chunk, ke = min(k, kb + chunk);
+    double acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+    for (int k0 = kb; k0 < ke; k0 += GK) {
+        for (int t = threadIdx.x; t < GK * GT; t += 256) {
+            const int kk = t / GT, mm = t - kk * GT;
+            const int gi = m0 + mm, gk = k0 + kk;
+            double va = 0.0;
+            if (gi < m && gk < ke) va = ta ? A[(long long)gi * lda + gk] : A[(long long)gk * lda + gi];
+            sA[kk][mm] = va;
+            const int gj = n0 + mm;
+            double vb = 0.0;
+            if (gj < n && gk < ke) vb = tb ? B[(long long)gk * ldb + gj] : B[(long long)gj * ldb + gk];
+            sB[kk][mm] = vb;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < GK; ++kk) {
+            double a[4], b[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) a[i] = sA[kk][tx + 16 * i];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) b[j] = sB[kk][ty + 16 * j];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+        }
+        __syncthreads();
+    }
+    double* Wz = W + (long long)blockIdx.z * m * n;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int gi = m0 + tx + 16 * i, gj = n0 + ty + 16 * j;
+            if (gi < m && gj < n) Wz[(long long)gj * m + gi] = acc[i][j];
+        }
+}
+
+__global__ void k_splitk_reduce(int m, int n, int ns, const double* W, double alpha, double beta, double* C, long long ldc)
+{
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= (long long)m * n) return;
+    double s = 0.0;
+    for (int z = 0; z < ns; ++z) s += W[(long long)z * m * n + t];
+    const int i = (int)(t % m), j = (int)(t / m);
+    double* c = C + (long long)j * ldc + i;
+    *c = alpha * s + (beta == 0.0 ? 0.0 : beta * *c);
+}
+
+// in-place LU without pivoting of an m x m column-major block, staged in shared
+// memory (one CTA, m*m*8 bytes of dynamic smem)
+__global__ void __launch_bounds__(1024) k_dense_lu_smem(double* D, int m, long long ld, int* bad)
+{
+    extern __shared__ double S[];
+    for (int t = threadIdx.x; t < m * m; t += blockDim.x) S[t] = D[(long long)(t / m) * ld + (t % m)];
+    __syncthreads();
+    for (int kk = 0; kk < m; ++kk) {
+        const double p = S[kk * m + kk];
+        if (threadIdx.x == 0 && (!(fabs(p) > 0.0) || !isfinite(p))) *bad = 1;
+        const double ip = 1.0 / p;
+        const int rem = m - kk - 1;
+        for (int i = kk + 1 + threadIdx.x; i < m; i += blockDim.x) S[kk * m + i] *= ip;
+        __syncthreads();
+        for (int t = threadIdx.x; t < rem * rem; t += blockDim.x) {
+            const int j = kk + 1 + t / rem, i = kk + 1 + t % rem;
+            S[j * m + i] = fma(-S[kk * m + i], S[j * m + kk], S[j * m + i]);
+        }
+        __syncthreads();
+    }
+    for (int t = threadIdx.x; t < m * m; t += blockDim.x) D[(long long)(t / m) * ld + (t % m)] = S[t];
+}
+
 // in-place LU without pivoting of an m x m column-major block (one CTA)
 __global__ void k_dense_lu(double* D, int m, long long ld, int* bad)
 {
@@ -99,9 +186,9 @@ __global__ void k_dense_lu(double* D, int m, long long ld, int* bad)
 }
 
 // triangular solves of a dense leaf factor, one warp per right-hand-side column;
-// rows are distributed round-robin over the lanes (m <= 32*TR)
-#define TR 24
+// rows are distributed round-robin over the lanes (m <= 32*TRN registers per lane)
 // mode 0: X <- L^{-1} X (unit lower of D) ; 1: X <- U^{-1} X (upper of D) ; 2: X <- U^{-T} X
+template <int TRN>
 __global__ void k_leaf_trsm(const double* __restrict__ D, int m, long long ld, double* X, long long ldx, int ncols,
                             int mode)
 {
@@ -109,57 +196,36 @@ __global__ void k_leaf_trsm(const double* __restrict__ D, int m, long long ld, d
     const int col = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (col >= ncols) return;
     double* x = X + (long long)col * ldx;
-    double r[TR];
-    const int nr = (m + 31) / 32;
+    double r[TRN];
 #pragma unroll
-    for (int t = 0; t < TR; ++t) r[t] = (t < nr && t * 32 + lane < m) ? x[t * 32 + lane] : 0.0;
-    if (mode == 0 || mode == 2) {
-        for (int i = 0; i < m; ++i) {
-            const int ti = i >> 5, li = i & 31;
-            double xi = 0.0;
+    for (int t = 0; t < TRN; ++t) r[t] = (t * 32 + lane < m) ? x[t * 32 + lane] : 0.0;
+    const bool fwd = (mode != 1);
+    for (int s = 0; s < m; ++s) {
+        const int i = fwd ? s : m - 1 - s;
+        const int ti = i >> 5, li = i & 31;
+        double xi = 0.0;
 #pragma unroll
-            for (int t = 0; t < TR; ++t)
-                if (t == ti) xi = r[t];
-            xi = __shfl_sync(0xffffffffu, xi, li);
-            if (mode == 2) xi /= D[(long long)i * ld + i];
-            if (lane == li) {
+        for (int t = 0; t < TRN; ++t)
+            if (t == ti) xi = r[t];
+        xi = __shfl_sync(0xffffffffu, xi, li);
+        if (mode != 0) xi /= D[(long long)i * ld + i];
+        if (lane == li) {
 #pragma unroll
-                for (int t = 0; t < TR; ++t)
-                    if (t == ti) r[t] = xi;
-            }
-#pragma unroll
-            for (int t = 0; t < TR; ++t) {
-                const int row = t * 32 + lane;
-                if (t < nr && row > i && row < m) {
-                    const double l = (mode == 0) ? D[(long long)i * ld + row] : D[(long long)row * ld + i];
-                    r[t] = fma(-l, xi, r[t]);
-                }
-            }
+            for (int t = 0; t < TRN; ++t)
+                if (t == ti) r[t] = xi;
         }
-    } else {
-        for (int i = m - 1; i >= 0; --i) {
-            const int ti = i >> 5, li = i & 31;
-            double xi = 0.0;
 #pragma unroll
-            for (int t = 0; t < TR; ++t)
-                if (t == ti) xi = r[t];
-            xi = __shfl_sync(0xffffffffu, xi, li);
-            xi /= D[(long long)i * ld + i];
-            if (lane == li) {
-#pragma unroll
-                for (int t = 0; t < TR; ++t)
-                    if (t == ti) r[t] = xi;
-            }
-#pragma unroll
-            for (int t = 0; t < TR; ++t) {
-                const int row = t * 32 + lane;
-                if (t < nr && row < i) r[t] = fma(-D[(long long)i * ld + row], xi, r[t]);
+        for (int t = 0; t < TRN; ++t) {
+            const int row = t * 32 + lane;
+            if (row < m && (fwd ? row > i : row < i)) {
+                const double l = (mode == 2) ? D[(long long)row * ld + i] : D[(long long)i * ld + row];
+                r[t] = fma(-l, xi, r[t]);
             }
         }
     }
 #pragma unroll
-    for (int t = 0; t < TR; ++t)
-        if (t < nr && t * 32 + lane < m) x[t * 32 + lane] = r[t];
+    for (int t = 0; t < TRN; ++t)
+        if (t * 32 + lane < m) x[t * 32 + lane] = r[t];
 }
 
 // B (n x m) = A^T (A: m x n), column-major
@@ -198,13 +264,20 @@ __global__ void k_eye(double* B, long long ldb, int m)
 
 // ---- truncation core: parallel cyclic Jacobi on symmetric matrices in smem
 // A (n x n, ld n) -> eigenvalues on the diagonal, V eigenvectors (columns).
-__device__ void cta_jacobi(double* A, double* V, int n, int* pairs)
+__device__ int cta_jacobi(double* A, double* V, int n, int* pairs)
 {
     // n even (caller pads)
     for (int t = threadIdx.x; t < n * n; t += blockDim.x) V[t] = ((t % n) == (t / n)) ? 1.0 : 0.0;
     __shared__ double cs[128], sn[128];
     __shared__ int conv;
+    __shared__ double afro;
     const int half = n / 2;
+    if (threadIdx.x == 0) {
+        double f = 0.0;
+        for (int t = 0; t < n * n; ++t) f += A[t] * A[t];
+        afro = sqrt(f);
+    }
+    __syncthreads();
     for (int sweep = 0; sweep < 30; ++sweep) {
         if (threadIdx.x == 0) conv = 1;
         __syncthreads();
@@ -218,7 +291,7 @@ __device__ void cta_jacobi(double* A, double* V, int n, int* pairs)
                 pairs[2 * k + 1] = q;
                 const double app = A[p * n + p], aqq = A[q * n + q], apq = A[q * n + p];
                 double c = 1.0, s = 0.0;
-                if (fabs(apq) > 1e-300 && fabs(apq) > 1e-17 * sqrt(fabs(app * aqq))) {
+                if (fabs(apq) > 1e-15 * sqrt(fabs(app * aqq)) + 1e-17 * afro + 1e-300) {
                     conv = 0;
                     const double tau = (aqq - app) / (2.0 * apq);
                     const double tt = (tau >= 0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
@@ -253,76 +326,83 @@ __device__ void cta_jacobi(double* A, double* V, int n, int* pairs)
             }
             __syncthreads();
         }
-        if (conv) break;
+        if (conv) return sweep + 1;
     }
+    return 30;
 }
 
-// Given Gram matrices Gu = U^T U and Gv = V^T V (k x k), produce transforms
-// Tu, Tv (k x r) with U Tu (V Tv)^T the rank-r truncation of U V^T,
-// r = #{sigma_i > tol sigma_1} (capped by rmax).  Works in smem, one CTA.
-__global__ void __launch_bounds__(256) k_trunc_core(const double* Gu, const double* Gv, int k, double tol, int rmax,
-                                                   double* Tu, double* Tv, int* rank_out, double* scratch)
+__device__ unsigned long long g_trunc_stats[4];   // calls, sum ke, sum sweeps, max ke
+
+// Truncation core (one CTA).  Input: Gram matrices Gu = U^T U, Gv = V^T V of a
+// low-rank sum U V^T with k columns (zero columns allowed: they are the unused
+// capacity and are compacted away using diag(Gu)).  With Gu = Eu Lu Eu^T and
+// Ru = Lu^{1/2} Eu^T (U = Qu Ru), M = Ru Gv Ru^T = X S^2 X^T gives the SVD
+// U V^T = (Qu X) S (V Ru^T X S^{-1})^T.  Output transforms (k x kc, zero padded):
+//   Tu = Eu Lu^{-1/2} X_r S_r      Tv = Eu Lu^{1/2} X_r S_r^{-1}
+// with r = #{s_i > tol s_1}; r > kc raises the overflow flag (FDE_ERANK).
+__global__ void __launch_bounds__(256) k_trunc_core(const double* Gu, const double* Gv, int k, double tol, int kc,
+                                                   double* Tu, double* Tv, int* flag, double* scratch)
 {
-    double* sm = scratch;
-    const int n = (k + 1) & ~1;   // even
-    double* A = sm;
-    double* Eu = A + n * n;
-    double* Ev = Eu + n * n;
-    double* C = Ev + n * n;
-    double* X = C + n * n;
-    double* lu = X + n * n;       // n
-    double* lv = lu + n;          // n
-    int* pairs = (int*)(lv + n);  // n
-    // eigen(Gu)
-    for (int t = threadIdx.x; t < n * n; t += blockDim.x) {
-        const int i = t % n, j = t / n;
-        A[t] = (i < k && j < k) ? Gu[j * k + i] : (i == j ? 0.0 : 0.0);
-    }
-    __syncthreads();
-    cta_jacobi(A, Eu, n, pairs);
-    for (int t = threadIdx.x; t < n; t += blockDim.x) lu[t] = A[t * n + t];
-    __syncthreads();
-    for (int t = threadIdx.x; t < n * n; t += blockDim.x) {
-        const int i = t % n, j = t / n;
-        A[t] = (i < k && j < k) ? Gv[j * k + i] : 0.0;
-    }
-    __syncthreads();
-    cta_jacobi(A, Ev, n, pairs);
-    for (int t = threadIdx.x; t < n; t += blockDim.x) lv[t] = A[t * n + t];
-    __syncthreads();
-    // sqrt of the retained eigenvalues (drop <= 1e-14 max: below the Gram precision)
-    __shared__ double mu, mv;
+    __shared__ int idx[256];
+    __shared__ int ke_sh;
     if (threadIdx.x == 0) {
-        double a = 0, b = 0;
-        for (int i = 0; i < n; ++i) { a = fmax(a, lu[i]); b = fmax(b, lv[i]); }
+        int c = 0;
+        for (int j = 0; j < k; ++j)
+            if (Gu[j * k + j] > 0.0) idx[c++] = j;
+        ke_sh = c;
+    }
+    __syncthreads();
+    const int ke = ke_sh;
+    for (int t = threadIdx.x; t < k * kc; t += blockDim.x) { Tu[t] = 0.0; Tv[t] = 0.0; }
+    if (ke == 0) return;
+    const int n = (ke + 1) & ~1;
+    double* A = scratch;
+    double* Eu = A + n * n;
+    double* X = Eu + n * n;
+    double* lu = X + n * n;
+    int* pairs = (int*)(lu + n);
+    for (int t = threadIdx.x; t < n * n; t += blockDim.x) {
+        const int i = t % n, j = t / n;
+        A[t] = (i < ke && j < ke) ? Gu[idx[j] * k + idx[i]] : 0.0;
+    }
+    __syncthreads();
+    const int sw1 = cta_jacobi(A, Eu, n, pairs);
+    __shared__ double mu;
+    if (threadIdx.x == 0) {
+        double a = 0.0;
+        for (int i = 0; i < n; ++i) a = fmax(a, A[i * n + i]);
         mu = a;
-        mv = b;
     }
     __syncthreads();
     for (int t = threadIdx.x; t < n; t += blockDim.x) {
-        lu[t] = (lu[t] > 1e-14 * mu) ? sqrt(lu[t]) : 0.0;
-        lv[t] = (lv[t] > 1e-14 * mv) ? sqrt(lv[t]) : 0.0;
+        const double l = A[t * n + t];
+        lu[t] = (l > 1e-14 * mu) ? sqrt(l) : 0.0;
     }
     __syncthreads();
-    // C = Ru Rv^T, Ru = diag(lu) Eu^T, Rv = diag(lv) Ev^T -> C_ij = lu_i lv_j (Eu^T Ev)_ij
+    // M = Ru Gv Ru^T, Ru = diag(lu) Eu^T ; first X <- Gv_c Eu (temp), then A <- Ru (Gv Eu diag(lu))
     for (int t = threadIdx.x; t < n * n; t += blockDim.x) {
-        const int i = t % n, j = t / n;
+        const int i = t % n, j = t / n;   // (Gv Eu)_ij
         double s = 0.0;
-        for (int q = 0; q < n; ++q) s = fma(Eu[i * n + q], Ev[j * n + q], s);
-        C[j * n + i] = lu[i] * lv[j] * s;
+        if (i < ke)
+            for (int q = 0; q < ke; ++q) s = fma(Gv[idx[q] * k + idx[i]], Eu[j * n + q], s);
+        X[t] = s;
     }
     __syncthreads();
-    // M = C C^T -> eigen -> X (left singular vectors), sigma^2
     for (int t = threadIdx.x; t < n * n; t += blockDim.x) {
-        const int i = t % n, j = t / n;
+        const int i = t % n, j = t / n;   // M_ij = lu_i lu_j (Eu^T Gv Eu)_ij
         double s = 0.0;
-        for (int q = 0; q < n; ++q) s = fma(C[q * n + i], C[q * n + j], s);
-        A[j * n + i] = s;
+        for (int q = 0; q < n; ++q) s = fma(Eu[i * n + q], X[j * n + q], s);
+        A[t] = lu[i] * lu[j] * s;
     }
     __syncthreads();
-    cta_jacobi(A, X, n, pairs);
+    const int sw2 = cta_jacobi(A, X, n, pairs);
     __syncthreads();
-    // order singular values descending (selection, one thread)
+    if (threadIdx.x == 0) {
+        atomicAdd(&g_trunc_stats[0], 1ull);
+        atomicAdd(&g_trunc_stats[1], (unsigned long long)ke);
+        atomicAdd(&g_trunc_stats[2], (unsigned long long)(sw1 + sw2));
+        atomicMax(&g_trunc_stats[3], (unsigned long long)ke);
+    }
     __shared__ int ord[256];
     __shared__ int r_sh;
     if (threadIdx.x == 0) {
@@ -331,7 +411,7 @@ __global__ void __launch_bounds__(256) k_trunc_core(const double* Gu, const doub
             int b = i;
             for (int j = i + 1; j < n; ++j)
                 if (A[ord[j] * n + ord[j]] > A[ord[b] * n + ord[b]]) b = j;
-            int tmp = ord[i]; ord[i] = ord[b]; ord[b] = tmp;
+            const int tmp = ord[i]; ord[i] = ord[b]; ord[b] = tmp;
         }
         const double s1 = sqrt(fmax(A[ord[0] * n + ord[0]], 0.0));
         int r = 0;
@@ -339,29 +419,25 @@ __global__ void __launch_bounds__(256) k_trunc_core(const double* Gu, const doub
             const double si = sqrt(fmax(A[ord[i] * n + ord[i]], 0.0));
             if (s1 > 0.0 && si > tol * s1 && si > 1e-15 * s1) ++r;
         }
-        if (r > rmax) r = rmax;
+        if (r > kc) { r = kc; *flag = 1; }
         r_sh = r;
-        *rank_out = r;
     }
     __syncthreads();
     const int r = r_sh;
-    // Tu = Eu diag(1/lu) X_r Sigma_r  ;  Tv = Ev diag(1/lv) C^T X_r Sigma_r^{-1}
-    for (int t = threadIdx.x; t < k * r; t += blockDim.x) {
-        const int i = t % k, c = t / k;
+    for (int t = threadIdx.x; t < ke * r; t += blockDim.x) {
+        const int i = t % ke, c = t / ke;
         const int col = ord[c];
         const double sig = sqrt(fmax(A[col * n + col], 0.0));
         double su = 0.0, sv = 0.0;
         for (int q = 0; q < n; ++q) {
-            // (diag(1/lu) X)_qc
-            const double xq = X[col * n + q];
-            if (lu[q] > 0.0) su = fma(Eu[q * n + i], xq / lu[q] * sig, su);
-            // (C^T X)_qc
-            double ctx = 0.0;
-            for (int p = 0; p < n; ++p) ctx = fma(C[q * n + p], X[col * n + p], ctx);
-            if (lv[q] > 0.0 && sig > 0.0) sv = fma(Ev[q * n + i], ctx / (lv[q] * sig), sv);
+            const double e = Eu[q * n + i] * X[col * n + q];
+            if (lu[q] > 0.0) {
+                su = fma(e, sig / lu[q], su);
+                sv = fma(e, lu[q] / sig, sv);
+            }
         }
-        Tu[c * k + i] = su;
-        Tv[c * k + i] = sv;
+        Tu[c * k + idx[i]] = su;
+        Tv[c * k + idx[i]] = sv;
     }
 }
 
@@ -374,6 +450,8 @@ struct LBlk {
     double* U = nullptr;   // lr: m x k, ld m
     double* V = nullptr;   // lr: n x k, ld n
     int k = 0;
+    double* Li = nullptr;  // diagonal leaves (tol > 0): inverse of the unit-lower factor
+    double* Ui = nullptr;  //                            inverse of the upper factor
 };
 
 struct fde_lu {
@@ -390,7 +468,14 @@ struct fde_lu {
     int* pinned = nullptr;
     DBuf<int> dflag;
     std::vector<double*> live;   // allocations to free
+    // flattened substitution schedule (built after the factorisation)
+    struct ApplySched* ap = nullptr;
 };
+
+struct ApplySched;
+static void apply_sched_free(ApplySched* a);
+static ApplySched* apply_sched_build(fde_lu* L);
+static void apply_sched_run(fde_ctx* h, fde_lu* L, double* x, int64_t ldx, int nrhs);
 
 struct Mat {   // owned temporary (column-major)
     double* p = nullptr;
@@ -414,6 +499,22 @@ static void gemm(fde_lu* L, int ta, int tb, int64_t m, int64_t n, int64_t k, dou
 {
     if (m <= 0 || n <= 0) return;
     if (k <= 0 && beta == 1.0) return;
+    const int64_t tiles = ceil_div(m, GT) * ceil_div(n, GT);
+    if (tiles <= 8 && k >= 384) {
+        // deterministic split-K: partial products over k-chunks, then a fixed-order sum
+        const int64_t chunk = 512;
+        const int64_t ns = ceil_div(k, chunk);
+        double* W = lu_alloc(L, (size_t)ns * m * n);
+        dim3 g((unsigned)ceil_div(m, GT), (unsigned)ceil_div(n, GT), (unsigned)ns);
+        k_gemm_splitk<<<g, 256, 0, L->h->stream>>>((int)m, (int)n, (int)k, (int)chunk, A, lda, ta, B, ldb, tb, W);
+        FDE_CHECK_LAUNCH();
+        k_splitk_reduce<<<(unsigned)ceil_div(m * n, 256), 256, 0, L->h->stream>>>((int)m, (int)n, (int)ns, W, alpha,
+                                                                                  beta, C, ldc);
+        FDE_CHECK_LAUNCH();
+        lu_free(L, W);
+        L->nops += 2;
+        return;
+    }
     dim3 g((unsigned)ceil_div(m, GT), (unsigned)ceil_div(n, GT));
     k_gemm<<<g, 256, 0, L->h->stream>>>((int)m, (int)n, (int)std::max<int64_t>(k, 0), alpha, A, lda, ta, B, ldb, tb,
                                         beta, C, ldc);
@@ -437,15 +538,35 @@ static void transpose(fde_lu* L, const double* A, int64_t lda, int64_t m, int64_
     FDE_CHECK_LAUNCH();
 }
 
+static void leaf_trsm_raw(fde_lu* L, const LBlk& D, double* X, int64_t ldx, int64_t ncols, int mode)
+{
+    if (ncols <= 0 || D.m == 0) return;
+    if (D.m > 32 * 24) fde_fail(FDE_EINVAL_PARAM, "H-LU: leaf larger than 768 dofs (reduce n_min)");
+    const int wpb = 4;
+    const unsigned g = (unsigned)ceil_div(ncols, wpb);
+    cudaStream_t st = L->h->stream;
+    const int nr = (int)ceil_div(D.m, 32);
+    if (nr <= 1) k_leaf_trsm<1><<<g, 32 * wpb, 0, st>>>(D.D, (int)D.m, D.m, X, ldx, (int)ncols, mode);
+    else if (nr <= 2) k_leaf_trsm<2><<<g, 32 * wpb, 0, st>>>(D.D, (int)D.m, D.m, X, ldx, (int)ncols, mode);
+    else if (nr <= 4) k_leaf_trsm<4><<<g, 32 * wpb, 0, st>>>(D.D, (int)D.m, D.m, X, ldx, (int)ncols, mode);
+    else if (nr <= 8) k_leaf_trsm<8><<<g, 32 * wpb, 0, st>>>(D.D, (int)D.m, D.m, X, ldx, (int)ncols, mode);
+    else if (nr <= 12) k_leaf_trsm<12><<<g, 32 * wpb, 0, st>>>(D.D, (int)D.m, D.m, X, ldx, (int)ncols, mode);
+    else k_leaf_trsm<24><<<g, 32 * wpb, 0, st>>>(D.D, (int)D.m, D.m, X, ldx, (int)ncols, mode);
+    FDE_CHECK_LAUNCH();
+    L->nops++;
+}
+
+// leaf solve: with stored inverses a GEMM into a temporary, else the warp trsm
 static void leaf_trsm(fde_lu* L, const LBlk& D, double* X, int64_t ldx, int64_t ncols, int mode)
 {
     if (ncols <= 0 || D.m == 0) return;
-    if (D.m > 32 * TR) fde_fail(FDE_EINVAL_PARAM, "H-LU: leaf larger than 768 dofs (reduce n_min)");
-    const int wpb = 4;
-    k_leaf_trsm<<<(unsigned)ceil_div(ncols, wpb), 32 * wpb, 0, L->h->stream>>>(D.D, (int)D.m, D.m, X, ldx, (int)ncols,
-                                                                                mode);
-    FDE_CHECK_LAUNCH();
-    L->nops++;
+    const double* Inv = (mode == 0) ? D.Li : (mode == 1 ? D.Ui : D.Ui);
+    if (!Inv) return leaf_trsm_raw(L, D, X, ldx, ncols, mode);
+    double* T = lu_alloc(L, (size_t)D.m * ncols);
+    // mode 2 (U^{-T} X) uses Ui^T
+    gemm(L, mode == 2 ? 1 : 0, 0, D.m, ncols, D.m, 1.0, Inv, D.m, X, ldx, 0.0, T, D.m);
+    copy2d(L, T, D.m, D.m, ncols, X, ldx, 1.0);
+    lu_free(L, T);
 }
 
 // Y += alpha op(A) X  (X: cols(op A) x nc, Y: rows(op A) x nc)
@@ -522,35 +643,31 @@ static void solve_UT(fde_lu* L, int b, double* X, int64_t ldx, int64_t nc)
     solve_UT(L, A.child[3], X + m0, ldx, nc);
 }
 
-// truncate [U (m x k), V (n x k)] -> new (U', V', r); consumes U,V
+// truncate [U (m x k), V (n x k)] -> (U', V') of capacity kcap (zero padded
+// beyond the numerical rank); consumes U, V.  No host synchronisation: the rank
+// stays implicit in the zero columns.  tol = 0: exact arithmetic, no truncation.
 static void truncate(fde_lu* L, double*& U, double*& V, int64_t m, int64_t n, int& k)
 {
     if (k == 0) return;
-    if (L->tol == 0.0) {   // exact formatted arithmetic: keep every column
+    if (L->tol == 0.0) {
         L->max_rank = std::max(L->max_rank, k);
         return;
     }
     if (k > 254) fde_fail(FDE_ERANK, "H-LU: low-rank sum wider than 254 columns before truncation");
-    const int kk = k;
+    const int kk = k, kc = L->rmax;
     double* G = lu_alloc(L, (size_t)2 * kk * kk);
-    double* T = lu_alloc(L, (size_t)2 * kk * kk);
+    double* T = lu_alloc(L, (size_t)2 * kk * kc);
     gemm(L, 1, 0, kk, kk, m, 1.0, U, m, U, m, 0.0, G, kk);
     gemm(L, 1, 0, kk, kk, n, 1.0, V, n, V, n, 0.0, G + kk * kk, kk);
     const int ne = (kk + 1) & ~1;
-    double* scr = lu_alloc(L, (size_t)(5 * ne * ne + 3 * ne + 8));
-    k_trunc_core<<<1, 256, 0, L->h->stream>>>(G, G + kk * kk, kk, L->tol, L->rmax, T, T + kk * kk, L->dflag.p + 1,
-                                              scr);
+    double* scr = lu_alloc(L, (size_t)(3 * ne * ne + 2 * ne + 8));
+    k_trunc_core<<<1, 256, 0, L->h->stream>>>(G, G + kk * kk, kk, L->tol, kc, T, T + kk * kc, L->dflag.p + 1, scr);
     FDE_CHECK_LAUNCH();
     L->nops++;
-    FDE_CUDA(cudaMemcpyAsync(L->pinned, L->dflag.p + 1, sizeof(int), cudaMemcpyDeviceToHost, L->h->stream));
-    FDE_CUDA(cudaStreamSynchronize(L->h->stream));
-    const int r = *L->pinned;
-    double* U2 = lu_alloc(L, (size_t)m * std::max(r, 1));
-    double* V2 = lu_alloc(L, (size_t)n * std::max(r, 1));
-    if (r > 0) {
-        gemm(L, 0, 0, m, r, kk, 1.0, U, m, T, kk, 0.0, U2, m);
-        gemm(L, 0, 0, n, r, kk, 1.0, V, n, T + kk * kk, kk, 0.0, V2, n);
-    }
+    double* U2 = lu_alloc(L, (size_t)m * kc);
+    double* V2 = lu_alloc(L, (size_t)n * kc);
+    gemm(L, 0, 0, m, kc, kk, 1.0, U, m, T, kk, 0.0, U2, m);
+    gemm(L, 0, 0, n, kc, kk, 1.0, V, n, T + kk * kc, kk, 0.0, V2, n);
     lu_free(L, U);
     lu_free(L, V);
     lu_free(L, G);
@@ -558,8 +675,8 @@ static void truncate(fde_lu* L, double*& U, double*& V, int64_t m, int64_t n, in
     lu_free(L, scr);
     U = U2;
     V = V2;
-    k = r;
-    L->max_rank = std::max(L->max_rank, k);
+    k = kc;
+    L->max_rank = std::max(L->max_rank, kc);
 }
 
 // C += U V^T (formatted); U: m x k (ldu), V: n x k (ldv); U, V not consumed
@@ -810,9 +927,26 @@ static void hlu_rec(fde_lu* L, int a)
     LBlk& A = L->B[a];
     if (A.type == HB_DENSE) {
         if (A.m == 0) return;
-        k_dense_lu<<<1, 512, 0, L->h->stream>>>(A.D, (int)A.m, A.m, L->dflag.p);
+        const size_t sm = (size_t)A.m * A.m * sizeof(double);
+        if (sm <= 200 * 1024) {
+            FDE_CUDA(cudaFuncSetAttribute(k_dense_lu_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            k_dense_lu_smem<<<1, 1024, sm, L->h->stream>>>(A.D, (int)A.m, A.m, L->dflag.p);
+        } else {
+            k_dense_lu<<<1, 512, 0, L->h->stream>>>(A.D, (int)A.m, A.m, L->dflag.p);
+        }
         FDE_CHECK_LAUNCH();
         L->nops++;
+        if (L->tol > 0.0) {
+            // explicit inverses of the leaf factors: every later leaf solve is a GEMM
+            A.Li = lu_alloc(L, (size_t)A.m * A.m);
+            A.Ui = lu_alloc(L, (size_t)A.m * A.m);
+            k_eye<<<64, 256, 0, L->h->stream>>>(A.Li, A.m, (int)A.m);
+            FDE_CHECK_LAUNCH();
+            k_eye<<<64, 256, 0, L->h->stream>>>(A.Ui, A.m, (int)A.m);
+            FDE_CHECK_LAUNCH();
+            leaf_trsm_raw(L, A, A.Li, A.m, A.m, 0);
+            leaf_trsm_raw(L, A, A.Ui, A.m, A.m, 1);
+        }
         return;
     }
     if (A.type != HB_HIER) fde_fail(FDE_EINVAL_PARAM, "H-LU: diagonal block is low rank");
@@ -831,7 +965,7 @@ fde_lu* hlu_build(fde_ctx* h, fde_hm* hm, double tol)
         L->h = h;
         L->S = hm->S;
         L->tol = tol;
-        L->rmax = 254;
+        L->rmax = std::max(16, hm->R);   // rank capacity of the truncated blocks
         FDE_CUDA(cudaMallocHost(&L->pinned, sizeof(int) * 4));
         L->dflag.alloc(4);
         L->dflag.zero(h->stream);
@@ -863,10 +997,14 @@ fde_lu* hlu_build(fde_ctx* h, fde_hm* hm, double tol)
             }
         }
         hlu_rec(L, L->S.root);
-        FDE_CUDA(cudaMemcpyAsync(L->pinned, L->dflag.p, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+        FDE_CUDA(cudaMemcpyAsync(L->pinned, L->dflag.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, h->stream));
         FDE_CUDA(cudaEventRecord(h->ev1, h->stream));
         FDE_CUDA(cudaEventSynchronize(h->ev1));
-        if (*L->pinned) fde_fail(FDE_ESINGULAR_PIVOT, "H-LU: zero or non-finite pivot in a leaf factorisation");
+        if (L->pinned[0]) fde_fail(FDE_ESINGULAR_PIVOT, "H-LU: zero or non-finite pivot in a leaf factorisation");
+        if (L->pinned[1]) fde_fail(FDE_ERANK, "H-LU: truncated rank exceeded the block capacity");
+        L->ap = apply_sched_build(L);
+        FDE_CUDA(cudaEventRecord(h->ev1, h->stream));
+        FDE_CUDA(cudaEventSynchronize(h->ev1));
         float ms = 0;
         cudaEventElapsedTime(&ms, h->ev0, h->ev1);
         L->factor_ms = ms;
@@ -900,9 +1038,12 @@ void hlu_destroy(fde_lu* L)
         if (b.D) cudaFreeAsync(b.D, s);
         if (b.U) cudaFreeAsync(b.U, s);
         if (b.V) cudaFreeAsync(b.V, s);
+        if (b.Li) cudaFreeAsync(b.Li, s);
+        if (b.Ui) cudaFreeAsync(b.Ui, s);
     }
     if (s) cudaStreamSynchronize(s);
     if (L->pinned) cudaFreeHost(L->pinned);
+    apply_sched_free(L->ap);
     delete L;
 }
 
@@ -913,8 +1054,7 @@ void precond_apply_internal(fde_ctx* h, fde_lu* lu, const double* r, int64_t ldr
     const int pi = prof_begin(h, PROF_PRECOND, 0.0);
     if (r != z) FDE_CUDA(cudaMemcpy2DAsync(z, ldz * sizeof(double), r, ldr * sizeof(double), lu->S.n * sizeof(double),
                                            nrhs, cudaMemcpyDeviceToDevice, h->stream));
-    solve_L(lu, lu->S.root, z, ldz, nrhs);
-    solve_U(lu, lu->S.root, z, ldz, nrhs);
+    apply_sched_run(h, lu, z, ldz, nrhs);
     prof_end(h, pi);
 }
 
@@ -947,4 +1087,385 @@ void hlu_solve_debug(fde_ctx* h, fde_lu* L, double* X, int64_t ldx, int nrhs, in
     if (which == 1) solve_U(L, L->S.root, X, ldx, nrhs);
     if (which == 2) solve_UT(L, L->S.root, X, ldx, nrhs);
     FDE_CUDA(cudaStreamSynchronize(h->stream));
+}
+
+// ===================================================================== apply
+// precond_apply as ONE kernel: the hierarchical substitutions L_H y = r and
+// U_H z = y are flattened into a left-looking sweep over the
+// leaf clusters (forward), then a right-looking one (backward).  For leaf k:
+//   z_k = x_k - sum_{dense near-field blocks (k,j)} D x_j
+//             - sum_{low-rank blocks B with row cluster containing k} U_B[k rows] t_B
+//   x_k = Inv_k z_k          (Inv_k: explicit inverse of the leaf's L or U factor)
+// and t_B = V_B^T x_sigma is projected as soon as the column cluster sigma of B
+// is complete (the admissibility gap guarantees a step in between).
+// One thread-block cluster of APPLY_CTAS CTAs runs both sweeps; the steps are
+// separated by cluster barriers (release/acquire); mutable data is read with
+// L2-coherent loads (ld.global.cg).
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
+
+#define APPLY_CTAS 8
+#define APPLY_THREADS 512
+#define PROJ_CHUNK 1024
+#define APPLY_TSM 2048
+
+struct SLeaf {
+    long long r0;
+    int m;
+    const double* inv;      // m x m column-major
+    int d_lo, d_hi;         // dense blocks in this leaf row
+    int l_lo, l_hi;         // low-rank row contributions
+    int p_lo, p_hi;         // projections enabled after this leaf
+};
+struct SDense {
+    const double* D;        // leaf rows x nc, column-major, ld = ldd
+    long long ldd;
+    long long roff;         // row offset of the leaf inside D's block rows
+    long long c0;
+    int nc;
+};
+struct SLRRow {
+    const double* U;        // tau rows x kc, ld = ldu
+    long long ldu;
+    long long roff;         // offset of the leaf rows inside tau
+    int kc;
+    int tslot;              // base slot of t (kc * nchunks entries per column)
+    int nchunk;
+};
+struct SProj {
+    const double* V;        // sigma rows x kc, ld = ldv
+    long long ldv;
+    long long c0;
+    int n;
+    int kc;
+    int tslot;
+    int nchunk;
+};
+
+struct SweepDev {
+    const SLeaf* leaf;
+    int nleaf;
+    const SDense* dense;
+    const SLRRow* lrr;
+    const SProj* proj;
+};
+
+__device__ __forceinline__ double ldcg(const double* p) { return __ldcg(p); }
+
+// y[i] = sum_j M[j*ldm + roff + i] x[c0 + j] for the rows [r_lo, r_hi) owned by this CTA:
+// thread t -> row r_lo + t % nr, column phase t / nr (coalesced along rows),
+// partial sums reduced in shared memory in a fixed order.
+__device__ __forceinline__ void cta_rows_dot(const double* M, long long ldm, long long roff, int ncol, const double* xv,
+                                             int r_lo, int nr, double* part)
+{
+    const int nph = APPLY_THREADS / nr;
+    const int t = threadIdx.x;
+    const int i = t % nr, ph = t / nr;
+    double acc = 0.0;
+    if (ph < nph)
+        for (int j = ph; j < ncol; j += nph) acc = fma(M[(long long)j * ldm + roff + r_lo + i], ldcg(xv + j), acc);
+    part[t] = (ph < nph) ? acc : 0.0;
+}
+
+__device__ void run_sweep(const SweepDev& S, int backward, double* x, long long ldx, int nrhs, double* z, double* t,
+                          int tstride, cg::cluster_group& cl)
+{
+    __shared__ double part[APPLY_THREADS];
+    const int nwarps = APPLY_CTAS * (APPLY_THREADS / 32);
+    const int cta = (int)cl.block_rank();
+    const int gw = cta * (APPLY_THREADS / 32) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    int prev = -1;
+    for (int s = 0; s < S.nleaf; ++s) {
+        const int k = backward ? S.nleaf - 1 - s : s;
+        const SLeaf L = S.leaf[k];
+        const int rows_per = (L.m + APPLY_CTAS - 1) / APPLY_CTAS;
+        const int r_lo = cta * rows_per;
+        const int nr = max(0, min(L.m - r_lo, rows_per));
+        // ---- phase A1: rows of leaf k (this CTA's row slice).  Thread t owns row
+        // r_lo + t % nr and every nph-th column / low-rank term; partial sums are
+        // reduced in shared memory in a fixed order (deterministic).
+        __shared__ double tsm[APPLY_TSM];
+        const int nlr = L.l_hi - L.l_lo;
+        bool lr_smem = nlr * 64 <= APPLY_TSM;
+        for (int l = L.l_lo; l < L.l_hi && lr_smem; ++l) lr_smem = S.lrr[l].kc <= 64;
+        for (int c = 0; c < nrhs; ++c) {
+            const double* xc = x + (long long)c * ldx;
+            const double* tc = t + (long long)c * tstride;
+            if (nr == 0) continue;
+            if (lr_smem) {
+                for (int e = threadIdx.x; e < nlr * 64; e += APPLY_THREADS) {
+                    const int l = L.l_lo + e / 64, q = e % 64;
+                    const SLRRow R = S.lrr[l];
+                    double tv = 0.0;
+                    if (q < R.kc)
+                        for (int ch = 0; ch < R.nchunk; ++ch) tv += ldcg(tc + R.tslot + q * R.nchunk + ch);
+                    tsm[e] = tv;
+                }
+                __syncthreads();
+            }
+            const int nph = APPLY_THREADS / nr;
+            const int i = threadIdx.x % nr, ph = threadIdx.x / nr;
+            double acc = 0.0;
+            if (ph < nph) {
+                const int row = r_lo + i;
+                for (int d = L.d_lo; d < L.d_hi; ++d) {
+                    const SDense D = S.dense[d];
+                    for (int j = ph; j < D.nc; j += nph)
+                        acc = fma(D.D[(long long)j * D.ldd + D.roff + row], ldcg(xc + D.c0 + j), acc);
+                }
+                for (int l = L.l_lo + ph; l < L.l_hi; l += nph) {
+                    const SLRRow R = S.lrr[l];
+                    for (int q = 0; q < R.kc; ++q) {
+                        double tv;
+                        if (lr_smem) {
+                            tv = tsm[(l - L.l_lo) * 64 + q];
+                        } else {
+                            tv = 0.0;
+                            for (int ch = 0; ch < R.nchunk; ++ch) tv += ldcg(tc + R.tslot + q * R.nchunk + ch);
+                        }
+                        acc = fma(R.U[(long long)q * R.ldu + R.roff + row], tv, acc);
+                    }
+                }
+            }
+            part[threadIdx.x] = acc;
+            __syncthreads();
+            if (threadIdx.x < nr) {
+                double s2 = 0.0;
+                for (int q = threadIdx.x; q < nph * nr; q += nr) s2 += part[q];
+                z[(long long)c * L.m + r_lo + threadIdx.x] = ldcg(xc + L.r0 + r_lo + threadIdx.x) - s2;
+            }
+            __syncthreads();
+        }
+        // ---- phase A2: projections enabled by the previous leaf (warp per (block, column, chunk))
+        if (prev >= 0) {
+            const SLeaf Pv = S.leaf[prev];
+            int ntask = 0;
+            for (int p = Pv.p_lo; p < Pv.p_hi; ++p) ntask += S.proj[p].kc * S.proj[p].nchunk;
+            for (int task = gw; task < ntask; task += nwarps) {
+                int q = task, p = Pv.p_lo;
+                while (q >= S.proj[p].kc * S.proj[p].nchunk) {
+                    q -= S.proj[p].kc * S.proj[p].nchunk;
+                    ++p;
+                }
+                const SProj Pj = S.proj[p];
+                const int col = q / Pj.nchunk, ch = q - col * Pj.nchunk;
+                const int i0 = ch * PROJ_CHUNK, i1 = min(Pj.n, i0 + PROJ_CHUNK);
+                for (int c = 0; c < nrhs; ++c) {
+                    const double* xc = x + (long long)c * ldx;
+                    double acc = 0.0;
+                    for (int i = i0 + lane; i < i1; i += 32)
+                        acc = fma(Pj.V[(long long)col * Pj.ldv + i], ldcg(xc + Pj.c0 + i), acc);
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+                    if (lane == 0) t[(long long)c * tstride + Pj.tslot + col * Pj.nchunk + ch] = acc;
+                }
+            }
+        }
+        __threadfence();
+        cl.sync();
+        // ---- phase B: x_k = Inv_k z_k (this CTA's row slice)
+        for (int c = 0; c < nrhs; ++c) {
+            if (nr > 0) {
+                cta_rows_dot(L.inv, L.m, 0, L.m, z + (long long)c * L.m, r_lo, nr, part);
+                __syncthreads();
+                if (threadIdx.x < nr) {
+                    double s2 = 0.0;
+                    for (int q = threadIdx.x; q < APPLY_THREADS; q += nr) s2 += part[q];
+                    x[(long long)c * ldx + L.r0 + r_lo + threadIdx.x] = s2;
+                }
+                __syncthreads();
+            }
+        }
+        __threadfence();
+        cl.sync();
+        prev = k;
+    }
+}
+
+__global__ void __cluster_dims__(APPLY_CTAS, 1, 1) __launch_bounds__(APPLY_THREADS)
+    k_apply(SweepDev fwd, SweepDev bwd, double* x, long long ldx, int nrhs, double* z, double* t, int tstride)
+{
+    cg::cluster_group cl = cg::this_cluster();
+    run_sweep(fwd, 0, x, ldx, nrhs, z, t, tstride, cl);
+    run_sweep(bwd, 1, x, ldx, nrhs, z, t, tstride, cl);
+}
+
+
+// --------------------------------------------------------- schedule (host)
+struct ApplySched {
+    DBuf<SLeaf> leaf_f, leaf_b;
+    DBuf<SDense> dense_f, dense_b;
+    DBuf<SLRRow> lrr_f, lrr_b;
+    DBuf<SProj> proj_f, proj_b;
+    DBuf<double> inv;       // leaf inverses
+    DBuf<double> z, t;
+    int nleaf = 0, zmax = 0, tslots = 0;
+    size_t zcap = 0, tcap = 0;
+};
+
+static void apply_sched_free(ApplySched* a) { delete a; }
+
+static ApplySched* apply_sched_build(fde_lu* L)
+{
+    ApplySched* A = new ApplySched();
+    const HStruct& S = L->S;
+    // leaves in order
+    std::vector<int> leafcl;
+    for (size_t c = 0; c < S.cl.size(); ++c)
+        if (S.cl[c].child[0] < 0) leafcl.push_back((int)c);
+    std::sort(leafcl.begin(), leafcl.end(), [&](int a, int b) { return S.cl[a].r0 < S.cl[b].r0; });
+    const int nl = (int)leafcl.size();
+    A->nleaf = nl;
+    auto leaf_range = [&](int cl, int& first, int& last) {   // leaves inside cluster cl
+        first = -1;
+        last = -1;
+        for (int q = 0; q < nl; ++q) {
+            const HCluster& lc = S.cl[leafcl[q]];
+            if (lc.r0 >= S.cl[cl].r0 && lc.r1 <= S.cl[cl].r1 && lc.r1 > lc.r0) {
+                if (first < 0) first = q;
+                last = q;
+            }
+        }
+    };
+    // diagonal leaf blocks -> inverses
+    std::vector<int> diagblk(nl, -1);
+    int64_t invwords = 0;
+    std::vector<int64_t> invoff(nl);
+    for (size_t b = 0; b < L->B.size(); ++b) {
+        const HBlock& hb = S.bl[b];
+        if (hb.type == HB_DENSE && hb.tau == hb.sig)
+            for (int q = 0; q < nl; ++q)
+                if (leafcl[q] == hb.tau) diagblk[q] = (int)b;
+    }
+    for (int q = 0; q < nl; ++q) {
+        const int64_t m = S.cl[leafcl[q]].r1 - S.cl[leafcl[q]].r0;
+        invoff[q] = invwords;
+        invwords += 2 * m * m;
+        A->zmax = std::max<int>(A->zmax, (int)m);
+    }
+    A->inv.alloc(std::max<int64_t>(invwords, 1));
+    for (int q = 0; q < nl; ++q) {
+        const LBlk& D = L->B[diagblk[q]];
+        const int64_t m = D.m;
+        if (m == 0) continue;
+        double* Li = A->inv.p + invoff[q];
+        double* Ui = Li + m * m;
+        k_eye<<<64, 256, 0, L->h->stream>>>(Li, m, (int)m);
+        FDE_CHECK_LAUNCH();
+        k_eye<<<64, 256, 0, L->h->stream>>>(Ui, m, (int)m);
+        FDE_CHECK_LAUNCH();
+        leaf_trsm(L, D, Li, m, m, 0);
+        leaf_trsm(L, D, Ui, m, m, 1);
+    }
+    // per-leaf lists
+    std::vector<std::vector<SDense>> df(nl), db(nl);
+    std::vector<std::vector<SLRRow>> lf(nl), lb(nl);
+    std::vector<std::vector<SProj>> pf(nl), pb(nl);
+    int tslot = 0;
+    for (size_t b = 0; b < L->B.size(); ++b) {
+        const HBlock& hb = S.bl[b];
+        const LBlk& B = L->B[b];
+        if (hb.type == HB_HIER || hb.tau == hb.sig) continue;
+        const HCluster &T = S.cl[hb.tau], &Sg = S.cl[hb.sig];
+        const bool lower = T.r0 > Sg.r0;
+        int t0, t1, s0, s1;
+        leaf_range(hb.tau, t0, t1);
+        leaf_range(hb.sig, s0, s1);
+        if (t0 < 0 || s0 < 0 || B.m == 0 || B.n == 0) continue;
+        if (hb.type == HB_DENSE) {
+            for (int q = t0; q <= t1; ++q) {
+                SDense d;
+                d.D = B.D;
+                d.ldd = B.m;
+                d.roff = S.cl[leafcl[q]].r0 - T.r0;
+                d.c0 = Sg.r0;
+                d.nc = (int)B.n;
+                (lower ? df : db)[q].push_back(d);
+            }
+        } else {
+            if (B.k == 0) continue;
+            const int nchunk = (int)ceil_div(B.n, PROJ_CHUNK);
+            const int slot = tslot;
+            tslot += B.k * nchunk;
+            for (int q = t0; q <= t1; ++q) {
+                SLRRow r;
+                r.U = B.U;
+                r.ldu = B.m;
+                r.roff = S.cl[leafcl[q]].r0 - T.r0;
+                r.kc = B.k;
+                r.tslot = slot;
+                r.nchunk = nchunk;
+                (lower ? lf : lb)[q].push_back(r);
+            }
+            SProj p;
+            p.V = B.V;
+            p.ldv = B.n;
+            p.c0 = Sg.r0;
+            p.n = (int)B.n;
+            p.kc = B.k;
+            p.tslot = slot;
+            p.nchunk = nchunk;
+            if (lower)
+                pf[s1].push_back(p);   // sigma complete after its last leaf (forward)
+            else
+                pb[s0].push_back(p);   // ... after its first leaf (backward)
+        }
+    }
+    A->tslots = std::max(tslot, 1);
+    auto flatten = [&](std::vector<std::vector<SDense>>& d, std::vector<std::vector<SLRRow>>& l,
+                       std::vector<std::vector<SProj>>& p, int which, DBuf<SLeaf>& Lo, DBuf<SDense>& Do,
+                       DBuf<SLRRow>& Ro, DBuf<SProj>& Po) {
+        std::vector<SLeaf> lv(nl);
+        std::vector<SDense> dv;
+        std::vector<SLRRow> rv;
+        std::vector<SProj> pv;
+        for (int q = 0; q < nl; ++q) {
+            SLeaf& s = lv[q];
+            const HCluster& c = S.cl[leafcl[q]];
+            s.r0 = c.r0;
+            s.m = (int)(c.r1 - c.r0);
+            s.inv = A->inv.p + invoff[q] + (which ? (int64_t)s.m * s.m : 0);
+            s.d_lo = (int)dv.size();
+            dv.insert(dv.end(), d[q].begin(), d[q].end());
+            s.d_hi = (int)dv.size();
+            s.l_lo = (int)rv.size();
+            rv.insert(rv.end(), l[q].begin(), l[q].end());
+            s.l_hi = (int)rv.size();
+            s.p_lo = (int)pv.size();
+            pv.insert(pv.end(), p[q].begin(), p[q].end());
+            s.p_hi = (int)pv.size();
+        }
+        Lo.upload(lv.data(), lv.size(), L->h->stream);
+        if (!dv.empty()) Do.upload(dv.data(), dv.size(), L->h->stream); else Do.alloc(1);
+        if (!rv.empty()) Ro.upload(rv.data(), rv.size(), L->h->stream); else Ro.alloc(1);
+        if (!pv.empty()) Po.upload(pv.data(), pv.size(), L->h->stream); else Po.alloc(1);
+        FDE_CUDA(cudaStreamSynchronize(L->h->stream));   // host vectors go out of scope
+    };
+    flatten(df, lf, pf, 0, A->leaf_f, A->dense_f, A->lrr_f, A->proj_f);
+    flatten(db, lb, pb, 1, A->leaf_b, A->dense_b, A->lrr_b, A->proj_b);
+    return A;
+}
+
+static void apply_sched_run(fde_ctx* h, fde_lu* L, double* x, int64_t ldx, int nrhs)
+{
+    ApplySched* A = L->ap;
+    if ((size_t)A->zmax * nrhs > A->zcap) {
+        A->z.alloc((size_t)A->zmax * nrhs);
+        A->zcap = (size_t)A->zmax * nrhs;
+    }
+    if ((size_t)A->tslots * nrhs > A->tcap) {
+        A->t.alloc((size_t)A->tslots * nrhs);
+        A->tcap = (size_t)A->tslots * nrhs;
+    }
+    SweepDev f{A->leaf_f.p, A->nleaf, A->dense_f.p, A->lrr_f.p, A->proj_f.p};
+    SweepDev b{A->leaf_b.p, A->nleaf, A->dense_b.p, A->lrr_b.p, A->proj_b.p};
+    k_apply<<<APPLY_CTAS, APPLY_THREADS, 0, h->stream>>>(f, b, x, ldx, nrhs, A->z.p, A->t.p, A->tslots);
+    FDE_CHECK_LAUNCH();
+}
+
+
+void hlu_trunc_stats(unsigned long long* out4)
+{
+    FDE_CUDA(cudaMemcpyFromSymbol(out4, g_trunc_stats, sizeof(unsigned long long) * 4));
 }
