@@ -107,6 +107,9 @@ int fde_profile(fde_handle h, int enable);
 int fde_profile_collect(fde_handle h, double* out9, int reset);
 /* Number of kernels this library has launched in the process so far. */
 long long fde_launch_count(void);
+/* Diagnostics: H-LU truncation statistics since load: out4 = {calls, sum of
+ * compacted widths, sum of Jacobi sweeps, max width}. */
+int fde_debug_trunc_stats(unsigned long long* out4);
 
 /* --------------------------------------------------------- sem_assemble */
 enum { FDE_OP_DENSE = 1, FDE_OP_TOEPLITZ = 2 };
