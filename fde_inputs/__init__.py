@@ -202,12 +202,12 @@ def config4(N: int = 1024, P: int = 8) -> Problem:
             x[j] = 0.5 * (2.0 * j / N) ** 2
         else:
             x[j] = 1.0 - 0.5 * (2.0 * (N - j) / N) ** 2
-    return Problem(f"c4-N{N}-P{P}", 0.0, 1.0, 1.4, 0.7, 2.0, 0.0, 0.0, x, P, 12,
+    return Problem(f"c4-N{N}-P{P}", 0.0, 1.0, 1.4, 0.7, 2.0, 0.0, 0.0, x, P, 12, n_min=64,
                    forcings=[random_legendre_forcing(0)], mesh_kind="graded")
 
 
 def config5(N: int = 4096, P: int = 8, nrhs: int = 64) -> Problem:
-    return Problem(f"c5-N{N}-P{P}", 0.0, 1.0, 1.6, 0.4, 1.0, 0.0, 0.0, uniform_mesh(0, 1, N), P, 16,
+    return Problem(f"c5-N{N}-P{P}", 0.0, 1.0, 1.6, 0.4, 1.0, 0.0, 0.0, uniform_mesh(0, 1, N), P, 16, n_min=64,
                    forcings=[random_legendre_forcing(s) for s in range(nrhs)], mesh_kind="uniform")
 
 

@@ -77,6 +77,47 @@ __global__ void __launch_bounds__(256) k_gemm(int m, int n, int k, double alpha,
         }
 }
 
+// 32 x 32 tiles (more CTAs for the leaf-sized products of the H-LU)
+__global__ void __launch_bounds__(256) k_gemm32(int m, int n, int k, double alpha, const double* __restrict__ A,
+                                               long long lda, int ta, const double* __restrict__ B, long long ldb,
+                                               int tb, double beta, double* __restrict__ C, long long ldc)
+{
+    __shared__ double sA[32][33];
+    __shared__ double sB[32][33];
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;   // 16 x 16 threads, 2x2 micro tile
+    const int m0 = blockIdx.x * 32, n0 = blockIdx.y * 32;
+    double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+    for (int k0 = 0; k0 < k; k0 += 32) {
+        for (int t = threadIdx.x; t < 32 * 32; t += 256) {
+            const int kk = t >> 5, mm = t & 31;
+            const int gi = m0 + mm, gk = k0 + kk, gj = n0 + mm;
+            sA[kk][mm] = (gi < m && gk < k) ? (ta ? A[(long long)gi * lda + gk] : A[(long long)gk * lda + gi]) : 0.0;
+            sB[kk][mm] = (gj < n && gk < k) ? (tb ? B[(long long)gk * ldb + gj] : B[(long long)gj * ldb + gk]) : 0.0;
+        }
+        __syncthreads();
+#pragma unroll 8
+        for (int kk = 0; kk < 32; ++kk) {
+            const double a0 = sA[kk][tx], a1 = sA[kk][tx + 16];
+            const double b0 = sB[kk][ty], b1 = sB[kk][ty + 16];
+            acc[0][0] = fma(a0, b0, acc[0][0]);
+            acc[0][1] = fma(a0, b1, acc[0][1]);
+            acc[1][0] = fma(a1, b0, acc[1][0]);
+            acc[1][1] = fma(a1, b1, acc[1][1]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const int gi = m0 + tx + 16 * i, gj = n0 + ty + 16 * j;
+            if (gi < m && gj < n) {
+                double* c = C + (long long)gj * ldc + gi;
+                *c = alpha * acc[i][j] + (beta == 0.0 ? 0.0 : beta * *c);
+            }
+        }
+}
+
 // split-K partial: W[z][m x n] = op(A)[:, kz] op(B)[kz, :]
 __global__ void __launch_bounds__(256) k_gemm_splitk(int m, int n, int k, int chunk, const double* __restrict__ A,
                                                     long long lda, int ta, const double* __restrict__ B, long long ldb,
@@ -151,12 +192,12 @@ __global__ void __launch_bounds__(1024) k_dense_lu_smem(double* D, int m, long l
         const double p = S[kk * m + kk];
         if (threadIdx.x == 0 && (!(fabs(p) > 0.0) || !isfinite(p))) *bad = 1;
         const double ip = 1.0 / p;
-        const int rem = m - kk - 1;
         for (int i = kk + 1 + threadIdx.x; i < m; i += blockDim.x) S[kk * m + i] *= ip;
         __syncthreads();
-        for (int t = threadIdx.x; t < rem * rem; t += blockDim.x) {
-            const int j = kk + 1 + t / rem, i = kk + 1 + t % rem;
-            S[j * m + i] = fma(-S[kk * m + i], S[j * m + kk], S[j * m + i]);
+        const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+        for (int j = kk + 1 + w; j < m; j += nw) {
+            const double ujk = S[j * m + kk];
+            for (int i = kk + 1 + lane; i < m; i += 32) S[j * m + i] = fma(-S[kk * m + i], ujk, S[j * m + i]);
         }
         __syncthreads();
     }
@@ -441,6 +482,187 @@ __global__ void __launch_bounds__(256) k_trunc_core(const double* Gu, const doub
     }
 }
 
+// ------------------------------------------------ batched truncation
+// A batch of independent low-rank sums U V^T (widths <= TRUNC_KMAX) is
+// recompressed with three launches: partial Gram matrices per 128-row chunk,
+// one CTA per entry for the core (Gram reduction in a fixed order, Jacobi
+// eigen-solves in shared memory), and the transform products per chunk.
+#define TRUNC_KMAX 64
+#define TRUNC_CHUNK 64
+
+struct TEntry {
+    const double* U;     // m x k (ld m)
+    const double* V;     // n x k (ld n)
+    double* Uo;          // m x kc
+    double* Vo;          // n x kc
+    long long m, n;
+    int k;
+    int c_lo, c_hi;      // chunk range (U chunks then V chunks)
+    long long gofs;      // partial Gram slot base (chunks * k * k)
+    long long tofs;      // transform slot base (2 * k * kc)
+};
+struct TChunk {
+    int e;               // entry
+    int side;            // 0 U, 1 V
+    long long r0;
+    int rows;
+};
+
+__global__ void __launch_bounds__(256) k_bgram(const TEntry* E, const TChunk* C, double* part)
+{
+    __shared__ double tile[TRUNC_CHUNK * TRUNC_KMAX];
+    const TChunk ch = C[blockIdx.x];
+    const TEntry e = E[ch.e];
+    const double* M = ch.side ? e.V : e.U;
+    const long long ld = ch.side ? e.n : e.m;
+    const int k = e.k;
+    for (int t = threadIdx.x; t < ch.rows * k; t += blockDim.x) {
+        const int r = t % ch.rows, j = t / ch.rows;
+        tile[j * TRUNC_CHUNK + r] = M[(long long)j * ld + ch.r0 + r];
+    }
+    __syncthreads();
+    double* out = part + e.gofs + (long long)(blockIdx.x - e.c_lo) * k * k;
+    for (int o = threadIdx.x; o < k * k; o += blockDim.x) {
+        const int i = o % k, j = o / k;
+        double s = 0.0;
+        for (int r = 0; r < ch.rows; ++r) s = fma(tile[i * TRUNC_CHUNK + r], tile[j * TRUNC_CHUNK + r], s);
+        out[o] = s;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_bcore(const TEntry* E, const TChunk* C, const double* part, double tol,
+                                              int kc, double* T, int* flag)
+{
+    extern __shared__ double sm[];
+    const TEntry e = E[blockIdx.x];
+    const int k = e.k;
+    double* Gu = sm;
+    double* Gv = Gu + k * k;
+    // fixed-order reduction of the chunk partials
+    for (int o = threadIdx.x; o < k * k; o += blockDim.x) {
+        double su = 0.0, sv = 0.0;
+        for (int c = e.c_lo; c < e.c_hi; ++c) {
+            const double v = part[e.gofs + (long long)(c - e.c_lo) * k * k + o];
+            if (C[c].side == 0) su += v; else sv += v;
+        }
+        Gu[o] = su;
+        Gv[o] = sv;
+    }
+    __syncthreads();
+    double* Tu = T + e.tofs;
+    double* Tv = Tu + (long long)k * kc;
+    __shared__ int idx[TRUNC_KMAX];
+    __shared__ int ke_sh;
+    if (threadIdx.x == 0) {
+        int c = 0;
+        for (int j = 0; j < k; ++j)
+            if (Gu[j * k + j] > 0.0) idx[c++] = j;
+        ke_sh = c;
+    }
+    __syncthreads();
+    const int ke = ke_sh;
+    for (int t = threadIdx.x; t < k * kc; t += blockDim.x) { Tu[t] = 0.0; Tv[t] = 0.0; }
+    __syncthreads();
+    if (ke == 0) return;
+    const int n = (ke + 1) & ~1;
+    double* A = Gv + k * k;
+    double* Eu = A + n * n;
+    double* X = Eu + n * n;
+    double* lu = X + n * n;
+    int* pairs = (int*)(lu + n);
+    for (int t = threadIdx.x; t < n * n; t += blockDim.x) {
+        const int i = t % n, j = t / n;
+        A[t] = (i < ke && j < ke) ? Gu[idx[j] * k + idx[i]] : 0.0;
+    }
+    __syncthreads();
+    cta_jacobi(A, Eu, n, pairs);
+    __shared__ double mu;
+    if (threadIdx.x == 0) {
+        double a = 0.0;
+        for (int i = 0; i < n; ++i) a = fmax(a, A[i * n + i]);
+        mu = a;
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < n; t += blockDim.x) {
+        const double l = A[t * n + t];
+        lu[t] = (l > 1e-14 * mu) ? sqrt(l) : 0.0;
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < n * n; t += blockDim.x) {
+        const int i = t % n, j = t / n;
+        double s = 0.0;
+        if (i < ke)
+            for (int q = 0; q < ke; ++q) s = fma(Gv[idx[q] * k + idx[i]], Eu[j * n + q], s);
+        X[t] = s;
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < n * n; t += blockDim.x) {
+        const int i = t % n, j = t / n;
+        double s = 0.0;
+        for (int q = 0; q < n; ++q) s = fma(Eu[i * n + q], X[j * n + q], s);
+        A[t] = lu[i] * lu[j] * s;
+    }
+    __syncthreads();
+    cta_jacobi(A, X, n, pairs);
+    __syncthreads();
+    __shared__ int ord[TRUNC_KMAX];
+    __shared__ int r_sh;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < n; ++i) ord[i] = i;
+        for (int i = 0; i < n; ++i) {
+            int b = i;
+            for (int j = i + 1; j < n; ++j)
+                if (A[ord[j] * n + ord[j]] > A[ord[b] * n + ord[b]]) b = j;
+            const int tmp = ord[i]; ord[i] = ord[b]; ord[b] = tmp;
+        }
+        const double s1 = sqrt(fmax(A[ord[0] * n + ord[0]], 0.0));
+        int r = 0;
+        for (int i = 0; i < n; ++i) {
+            const double si = sqrt(fmax(A[ord[i] * n + ord[i]], 0.0));
+            if (s1 > 0.0 && si > tol * s1 && si > 1e-15 * s1) ++r;
+        }
+        if (r > kc) { r = kc; *flag = 1; }
+        r_sh = r;
+    }
+    __syncthreads();
+    const int r = r_sh;
+    for (int t = threadIdx.x; t < ke * r; t += blockDim.x) {
+        const int i = t % ke, c = t / ke;
+        const int col = ord[c];
+        const double sig = sqrt(fmax(A[col * n + col], 0.0));
+        double su = 0.0, sv = 0.0;
+        for (int q = 0; q < n; ++q) {
+            const double ev = Eu[q * n + i] * X[col * n + q];
+            if (lu[q] > 0.0) {
+                su = fma(ev, sig / lu[q], su);
+                sv = fma(ev, lu[q] / sig, sv);
+            }
+        }
+        Tu[c * k + idx[i]] = su;
+        Tv[c * k + idx[i]] = sv;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_bapply(const TEntry* E, const TChunk* C, const double* T, int kc)
+{
+    __shared__ double Ts[TRUNC_KMAX * TRUNC_KMAX];
+    const TChunk ch = C[blockIdx.x];
+    const TEntry e = E[ch.e];
+    const int k = e.k;
+    const double* Tm = T + e.tofs + (ch.side ? (long long)k * kc : 0);
+    for (int t = threadIdx.x; t < k * kc; t += blockDim.x) Ts[t] = Tm[t];
+    __syncthreads();
+    const double* M = ch.side ? e.V : e.U;
+    double* O = ch.side ? e.Vo : e.Uo;
+    const long long ld = ch.side ? e.n : e.m;
+    for (int t = threadIdx.x; t < ch.rows * kc; t += blockDim.x) {
+        const int r = t % ch.rows, c = t / ch.rows;
+        double s = 0.0;
+        for (int q = 0; q < k; ++q) s = fma(M[(long long)q * ld + ch.r0 + r], Ts[c * k + q], s);
+        O[(long long)c * ld + ch.r0 + r] = s;
+    }
+}
+
 // ---------------------------------------------------------------- host side
 struct LBlk {
     int type;
@@ -470,6 +692,11 @@ struct fde_lu {
     std::vector<double*> live;   // allocations to free
     // flattened substitution schedule (built after the factorisation)
     struct ApplySched* ap = nullptr;
+    // deferred truncation
+    std::vector<int> dirty;
+    std::vector<char> is_dirty;
+    int gemm_depth = 0;
+    int nflush = 0;
 };
 
 struct ApplySched;
@@ -500,10 +727,11 @@ static void gemm(fde_lu* L, int ta, int tb, int64_t m, int64_t n, int64_t k, dou
     if (m <= 0 || n <= 0) return;
     if (k <= 0 && beta == 1.0) return;
     const int64_t tiles = ceil_div(m, GT) * ceil_div(n, GT);
-    if (tiles <= 8 && k >= 384) {
+    if (tiles < 148 && k >= 256) {
         // deterministic split-K: partial products over k-chunks, then a fixed-order sum
-        const int64_t chunk = 512;
-        const int64_t ns = ceil_div(k, chunk);
+        int64_t ns = std::min<int64_t>(ceil_div(296, tiles), ceil_div(k, 128));
+        const int64_t chunk = round_up(ceil_div(k, ns), GK);
+        ns = ceil_div(k, chunk);
         double* W = lu_alloc(L, (size_t)ns * m * n);
         dim3 g((unsigned)ceil_div(m, GT), (unsigned)ceil_div(n, GT), (unsigned)ns);
         k_gemm_splitk<<<g, 256, 0, L->h->stream>>>((int)m, (int)n, (int)k, (int)chunk, A, lda, ta, B, ldb, tb, W);
@@ -515,9 +743,15 @@ static void gemm(fde_lu* L, int ta, int tb, int64_t m, int64_t n, int64_t k, dou
         L->nops += 2;
         return;
     }
-    dim3 g((unsigned)ceil_div(m, GT), (unsigned)ceil_div(n, GT));
-    k_gemm<<<g, 256, 0, L->h->stream>>>((int)m, (int)n, (int)std::max<int64_t>(k, 0), alpha, A, lda, ta, B, ldb, tb,
-                                        beta, C, ldc);
+    if (tiles < 96) {
+        dim3 g((unsigned)ceil_div(m, 32), (unsigned)ceil_div(n, 32));
+        k_gemm32<<<g, 256, 0, L->h->stream>>>((int)m, (int)n, (int)std::max<int64_t>(k, 0), alpha, A, lda, ta, B, ldb,
+                                              tb, beta, C, ldc);
+    } else {
+        dim3 g((unsigned)ceil_div(m, GT), (unsigned)ceil_div(n, GT));
+        k_gemm<<<g, 256, 0, L->h->stream>>>((int)m, (int)n, (int)std::max<int64_t>(k, 0), alpha, A, lda, ta, B, ldb, tb,
+                                            beta, C, ldc);
+    }
     FDE_CHECK_LAUNCH();
     L->nops++;
 }
@@ -554,6 +788,89 @@ static void leaf_trsm_raw(fde_lu* L, const LBlk& D, double* X, int64_t ldx, int6
     else k_leaf_trsm<24><<<g, 32 * wpb, 0, st>>>(D.D, (int)D.m, D.m, X, ldx, (int)ncols, mode);
     FDE_CHECK_LAUNCH();
     L->nops++;
+}
+
+// ------------------------------------------------ blocked dense leaf kernels
+static void smem_lu(fde_lu* L, double* D, int64_t m, int64_t ld)
+{
+    const size_t sm = (size_t)m * m * sizeof(double);
+    FDE_CUDA(cudaFuncSetAttribute(k_dense_lu_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    k_dense_lu_smem<<<1, 1024, sm, L->h->stream>>>(D, (int)m, ld, L->dflag.p);
+    FDE_CHECK_LAUNCH();
+    L->nops++;
+}
+
+static void trsm_raw(fde_lu* L, const double* D, int64_t m, int64_t ld, double* X, int64_t ldx, int64_t ncols, int mode)
+{
+    const int wpb = 4;
+    const unsigned g = (unsigned)ceil_div(ncols, wpb);
+    cudaStream_t st = L->h->stream;
+    const int nr = (int)ceil_div(m, 32);
+    if (nr <= 1) k_leaf_trsm<1><<<g, 32 * wpb, 0, st>>>(D, (int)m, ld, X, ldx, (int)ncols, mode);
+    else if (nr <= 2) k_leaf_trsm<2><<<g, 32 * wpb, 0, st>>>(D, (int)m, ld, X, ldx, (int)ncols, mode);
+    else if (nr <= 4) k_leaf_trsm<4><<<g, 32 * wpb, 0, st>>>(D, (int)m, ld, X, ldx, (int)ncols, mode);
+    else if (nr <= 8) k_leaf_trsm<8><<<g, 32 * wpb, 0, st>>>(D, (int)m, ld, X, ldx, (int)ncols, mode);
+    else if (nr <= 12) k_leaf_trsm<12><<<g, 32 * wpb, 0, st>>>(D, (int)m, ld, X, ldx, (int)ncols, mode);
+    else k_leaf_trsm<24><<<g, 32 * wpb, 0, st>>>(D, (int)m, ld, X, ldx, (int)ncols, mode);
+    FDE_CHECK_LAUNCH();
+    L->nops++;
+}
+
+// out (m x m, ld m) = inverse of the unit-lower (upper = 0) or the upper (upper = 1)
+// triangle of the packed LU block D (ld); recursive 2x2 for m > 128
+static void tri_inv(fde_lu* L, const double* D, int64_t m, int64_t ld, int upper, double* out, int64_t ldo)
+{
+    if (m <= 128) {
+        double* I = lu_alloc(L, (size_t)m * m);
+        k_eye<<<64, 256, 0, L->h->stream>>>(I, m, (int)m);
+        FDE_CHECK_LAUNCH();
+        trsm_raw(L, D, m, ld, I, m, m, upper ? 1 : 0);
+        copy2d(L, I, m, m, m, out, ldo);
+        lu_free(L, I);
+        return;
+    }
+    const int64_t m0 = (m / 2 + 31) / 32 * 32, m1 = m - m0;
+    tri_inv(L, D, m0, ld, upper, out, ldo);
+    tri_inv(L, D + m0 * ld + m0, m1, ld, upper, out + m0 * ldo + m0, ldo);
+    double* T = lu_alloc(L, (size_t)m0 * m1);
+    if (!upper) {
+        // X10 = -X11 L10 X00 ;  X01 = 0
+        gemm(L, 0, 0, m1, m0, m0, 1.0, D + m0, ld, out, ldo, 0.0, T, m1);                 // L10 X00 (m1 x m0)
+        gemm(L, 0, 0, m1, m0, m1, -1.0, out + m0 * ldo + m0, ldo, T, m1, 0.0, out + m0, ldo);
+        FDE_CUDA(cudaMemset2DAsync(out + m0 * ldo, ldo * sizeof(double), 0, m0 * sizeof(double), m1, L->h->stream));
+    } else {
+        // X01 = -X00 U01 X11 ;  X10 = 0
+        gemm(L, 0, 0, m0, m1, m1, 1.0, D + m0 * ld, ld, out + m0 * ldo + m0, ldo, 0.0, T, m0);   // U01 X11
+        gemm(L, 0, 0, m0, m1, m0, -1.0, out, ldo, T, m0, 0.0, out + m0 * ldo, ldo);
+        FDE_CUDA(cudaMemset2DAsync(out + m0, ldo * sizeof(double), 0, m1 * sizeof(double), m0, L->h->stream));
+    }
+    lu_free(L, T);
+}
+
+// in-place LU (no pivoting) of an m x m block: shared-memory base case, 2x2
+// recursion with GEMM Schur updates above 128
+static void dense_lu_rec(fde_lu* L, double* D, int64_t m, int64_t ld)
+{
+    if (m <= 128) return smem_lu(L, D, m, ld);
+    const int64_t m0 = (m / 2 + 31) / 32 * 32, m1 = m - m0;
+    dense_lu_rec(L, D, m0, ld);
+    double* Li = lu_alloc(L, (size_t)m0 * m0);
+    double* Ui = lu_alloc(L, (size_t)m0 * m0);
+    tri_inv(L, D, m0, ld, 0, Li, m0);
+    tri_inv(L, D, m0, ld, 1, Ui, m0);
+    double* T = lu_alloc(L, (size_t)m0 * m1);
+    // A01 <- L00^{-1} A01
+    gemm(L, 0, 0, m0, m1, m0, 1.0, Li, m0, D + m0 * ld, ld, 0.0, T, m0);
+    copy2d(L, T, m0, m0, m1, D + m0 * ld, ld);
+    // A10 <- A10 U00^{-1}
+    gemm(L, 0, 0, m1, m0, m0, 1.0, D + m0, ld, Ui, m0, 0.0, T, m1);
+    copy2d(L, T, m1, m1, m0, D + m0, ld);
+    // A11 -= A10 A01
+    gemm(L, 0, 0, m1, m1, m0, -1.0, D + m0, ld, D + m0 * ld, ld, 1.0, D + m0 * ld + m0, ld);
+    lu_free(L, T);
+    lu_free(L, Li);
+    lu_free(L, Ui);
+    dense_lu_rec(L, D + m0 * ld + m0, m1, ld);
 }
 
 // leaf solve: with stored inverses a GEMM into a temporary, else the warp trsm
@@ -679,13 +996,102 @@ static void truncate(fde_lu* L, double*& U, double*& V, int64_t m, int64_t n, in
     L->max_rank = std::max(L->max_rank, kc);
 }
 
-// C += U V^T (formatted); U: m x k (ldu), V: n x k (ldv); U, V not consumed
-static void add_lr(fde_lu* L, int c, const double* U, int64_t ldu, const double* V, int64_t ldv, int k)
+
+// recompress every dirty low-rank block in one batch (tol > 0)
+static void flush_dirty(fde_lu* L)
+{
+    if (L->dirty.empty()) return;
+    std::vector<int> list;
+    list.swap(L->dirty);
+    if (L->tol == 0.0) {
+        for (int b : list) L->is_dirty[b] = 0;
+        return;
+    }
+    const int kc = L->rmax;
+    std::vector<TEntry> E;
+    std::vector<TChunk> C;
+    std::vector<int> blk;
+    long long gofs = 0, tofs = 0;
+    int kmax = 0;
+    for (int b : list) {
+        L->is_dirty[b] = 0;
+        LBlk& B = L->B[b];
+        if (B.k == 0) continue;
+        TEntry e;
+        e.U = B.U;
+        e.V = B.V;
+        e.m = B.m;
+        e.n = B.n;
+        e.k = B.k;
+        e.Uo = lu_alloc(L, (size_t)B.m * kc);
+        e.Vo = lu_alloc(L, (size_t)B.n * kc);
+        e.c_lo = (int)C.size();
+        for (int side = 0; side < 2; ++side) {
+            const long long rows = side ? B.n : B.m;
+            for (long long r0 = 0; r0 < rows; r0 += TRUNC_CHUNK)
+                C.push_back(TChunk{(int)E.size(), side, r0, (int)std::min<long long>(TRUNC_CHUNK, rows - r0)});
+        }
+        e.c_hi = (int)C.size();
+        e.gofs = gofs;
+        gofs += (long long)(e.c_hi - e.c_lo) * B.k * B.k;
+        e.tofs = tofs;
+        tofs += 2LL * B.k * kc;
+        kmax = std::max(kmax, B.k);
+        E.push_back(e);
+        blk.push_back(b);
+    }
+    if (E.empty()) return;
+    // descriptors in stream-ordered memory (pageable copies are staged before the call returns)
+    TEntry* dEp = (TEntry*)lu_alloc(L, (E.size() * sizeof(TEntry) + 7) / 8);
+    TChunk* dCp = (TChunk*)lu_alloc(L, (C.size() * sizeof(TChunk) + 7) / 8);
+    FDE_CUDA(cudaMemcpyAsync(dEp, E.data(), E.size() * sizeof(TEntry), cudaMemcpyHostToDevice, L->h->stream));
+    FDE_CUDA(cudaMemcpyAsync(dCp, C.data(), C.size() * sizeof(TChunk), cudaMemcpyHostToDevice, L->h->stream));
+    struct { TEntry* p; } dE{dEp};
+    struct { TChunk* p; } dC{dCp};
+    double* part = lu_alloc(L, (size_t)std::max<long long>(gofs, 1));
+    double* T = lu_alloc(L, (size_t)std::max<long long>(tofs, 1));
+    k_bgram<<<(unsigned)C.size(), 256, 0, L->h->stream>>>(dE.p, dC.p, part);
+    FDE_CHECK_LAUNCH();
+    const int ne = (kmax + 1) & ~1;
+    const size_t smem = (size_t)(2 * kmax * kmax + 3 * ne * ne + 2 * ne + 8) * sizeof(double);
+    FDE_CUDA(cudaFuncSetAttribute(k_bcore, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_bcore<<<(unsigned)E.size(), 256, smem, L->h->stream>>>(dE.p, dC.p, part, L->tol, kc, T, L->dflag.p + 1);
+    FDE_CHECK_LAUNCH();
+    k_bapply<<<(unsigned)C.size(), 256, 0, L->h->stream>>>(dE.p, dC.p, T, kc);
+    FDE_CHECK_LAUNCH();
+    L->nops += 3;
+    L->nflush++;
+    for (size_t q = 0; q < E.size(); ++q) {
+        LBlk& B = L->B[blk[q]];
+        lu_free(L, B.U);
+        lu_free(L, B.V);
+        B.U = E[q].Uo;
+        B.V = E[q].Vo;
+        B.k = kc;
+    }
+    lu_free(L, part);
+    lu_free(L, T);
+    lu_free(L, (double*)dEp);
+    lu_free(L, (double*)dCp);
+    L->max_rank = std::max(L->max_rank, kc);
+}
+
+static void mark_dirty(fde_lu* L, int b)
+{
+    if (!L->is_dirty[b]) {
+        L->is_dirty[b] = 1;
+        L->dirty.push_back(b);
+    }
+}
+
+// C += alpha U V^T (formatted); U: m x k (ldu), V: n x k (ldv); U, V not consumed
+static void add_lr(fde_lu* L, int c, const double* U, int64_t ldu, const double* V, int64_t ldv, int k,
+                   double alpha = 1.0)
 {
     if (k == 0) return;
     LBlk& C = L->B[c];
     if (C.type == HB_DENSE) {
-        gemm(L, 0, 1, C.m, C.n, k, 1.0, U, ldu, V, ldv, 1.0, C.D, C.m);
+        gemm(L, 0, 1, C.m, C.n, k, alpha, U, ldu, V, ldv, 1.0, C.D, C.m);
         return;
     }
     if (C.type == HB_LR) {
@@ -696,22 +1102,26 @@ static void add_lr(fde_lu* L, int c, const double* U, int64_t ldu, const double*
             copy2d(L, C.U, C.m, C.m, C.k, U2, C.m);
             copy2d(L, C.V, C.n, C.n, C.k, V2, C.n);
         }
-        copy2d(L, U, ldu, C.m, k, U2 + C.m * C.k, C.m);
+        copy2d(L, U, ldu, C.m, k, U2 + C.m * C.k, C.m, alpha);
         copy2d(L, V, ldv, C.n, k, V2 + C.n * C.k, C.n);
         lu_free(L, C.U);
         lu_free(L, C.V);
-        int kk = k2;
-        truncate(L, U2, V2, C.m, C.n, kk);
         C.U = U2;
         C.V = V2;
-        C.k = kk;
+        C.k = k2;
+        if (L->tol > 0.0) {
+            mark_dirty(L, c);
+            if (C.k > TRUNC_KMAX - 16) flush_dirty(L);   // keep pending widths bounded
+        } else {
+            L->max_rank = std::max(L->max_rank, C.k);
+        }
         return;
     }
     const int64_t m0 = L->B[C.child[0]].m, n0 = L->B[C.child[0]].n;
-    add_lr(L, C.child[0], U, ldu, V, ldv, k);
-    add_lr(L, C.child[1], U, ldu, V + n0, ldv, k);
-    add_lr(L, C.child[2], U + m0, ldu, V, ldv, k);
-    add_lr(L, C.child[3], U + m0, ldu, V + n0, ldv, k);
+    add_lr(L, C.child[0], U, ldu, V, ldv, k, alpha);
+    add_lr(L, C.child[1], U, ldu, V + n0, ldv, k, alpha);
+    add_lr(L, C.child[2], U + m0, ldu, V, ldv, k, alpha);
+    add_lr(L, C.child[3], U + m0, ldu, V + n0, ldv, k, alpha);
 }
 
 // A B as a low-rank pair (allocated, caller frees)
@@ -842,14 +1252,23 @@ void lu_axpy2d(fde_lu* L, const double* A, int64_t lda, int64_t m, int64_t n, do
     FDE_CHECK_LAUNCH();
 }
 
-// C <- C - A B
+static void gemm_sub_rec(fde_lu* L, int c, int a, int b);
+
+// C <- C - A B ; pending low-rank updates are recompressed when the outermost call returns
 static void gemm_sub(fde_lu* L, int c, int a, int b)
+{
+    L->gemm_depth++;
+    gemm_sub_rec(L, c, a, b);
+    if (--L->gemm_depth == 0) flush_dirty(L);
+}
+
+static void gemm_sub_rec(fde_lu* L, int c, int a, int b)
 {
     LBlk &C = L->B[c], &A = L->B[a], &B = L->B[b];
     if (A.type == HB_HIER && B.type == HB_HIER && C.type == HB_HIER) {
         for (int i = 0; i < 2; ++i)
             for (int j = 0; j < 2; ++j)
-                for (int k = 0; k < 2; ++k) gemm_sub(L, C.child[2 * i + j], A.child[2 * i + k], B.child[2 * k + j]);
+                for (int k = 0; k < 2; ++k) gemm_sub_rec(L, C.child[2 * i + j], A.child[2 * i + k], B.child[2 * k + j]);
         return;
     }
     if (C.type == HB_DENSE && A.type != HB_LR && B.type != HB_LR) {
@@ -873,11 +1292,28 @@ static void gemm_sub(fde_lu* L, int c, int a, int b)
         }
         return;
     }
+    // low-rank products: reuse the operand's own factor instead of copying it
+    if (A.type == HB_LR && A.k > 0) {
+        double* Vp = lu_alloc(L, (size_t)C.n * A.k);
+        FDE_CUDA(cudaMemsetAsync(Vp, 0, sizeof(double) * C.n * A.k, L->h->stream));
+        hmul(L, b, 1, A.V, A.n, A.k, 1.0, Vp, C.n);   // B^T Va
+        add_lr(L, c, A.U, A.m, Vp, C.n, A.k, -1.0);
+        lu_free(L, Vp);
+        return;
+    }
+    if (B.type == HB_LR && B.k > 0) {
+        double* Up = lu_alloc(L, (size_t)C.m * B.k);
+        FDE_CUDA(cudaMemsetAsync(Up, 0, sizeof(double) * C.m * B.k, L->h->stream));
+        hmul(L, a, 0, B.U, B.m, B.k, 1.0, Up, C.m);   // A Ub
+        add_lr(L, c, Up, C.m, B.V, B.n, B.k, -1.0);
+        lu_free(L, Up);
+        return;
+    }
+    if ((A.type == HB_LR && A.k == 0) || (B.type == HB_LR && B.k == 0)) return;
     double *U, *V;
     int k;
     product_lr(L, a, b, U, V, k);
-    if (k) copy2d(L, U, C.m, C.m, k, U, C.m, -1.0);
-    add_lr(L, c, U, C.m, V, C.n, k);
+    add_lr(L, c, U, C.m, V, C.n, k, -1.0);
     lu_free(L, U);
     lu_free(L, V);
 }
@@ -927,25 +1363,13 @@ static void hlu_rec(fde_lu* L, int a)
     LBlk& A = L->B[a];
     if (A.type == HB_DENSE) {
         if (A.m == 0) return;
-        const size_t sm = (size_t)A.m * A.m * sizeof(double);
-        if (sm <= 200 * 1024) {
-            FDE_CUDA(cudaFuncSetAttribute(k_dense_lu_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-            k_dense_lu_smem<<<1, 1024, sm, L->h->stream>>>(A.D, (int)A.m, A.m, L->dflag.p);
-        } else {
-            k_dense_lu<<<1, 512, 0, L->h->stream>>>(A.D, (int)A.m, A.m, L->dflag.p);
-        }
-        FDE_CHECK_LAUNCH();
-        L->nops++;
+        dense_lu_rec(L, A.D, A.m, A.m);
         if (L->tol > 0.0) {
             // explicit inverses of the leaf factors: every later leaf solve is a GEMM
             A.Li = lu_alloc(L, (size_t)A.m * A.m);
             A.Ui = lu_alloc(L, (size_t)A.m * A.m);
-            k_eye<<<64, 256, 0, L->h->stream>>>(A.Li, A.m, (int)A.m);
-            FDE_CHECK_LAUNCH();
-            k_eye<<<64, 256, 0, L->h->stream>>>(A.Ui, A.m, (int)A.m);
-            FDE_CHECK_LAUNCH();
-            leaf_trsm_raw(L, A, A.Li, A.m, A.m, 0);
-            leaf_trsm_raw(L, A, A.Ui, A.m, A.m, 1);
+            tri_inv(L, A.D, A.m, A.m, 0, A.Li, A.m);
+            tri_inv(L, A.D, A.m, A.m, 1, A.Ui, A.m);
         }
         return;
     }
@@ -990,12 +1414,13 @@ fde_lu* hlu_build(fde_ctx* h, fde_hm* hm, double tol)
                 lb.V = lu_alloc(L, (size_t)hb.n * hm->R);
                 copy2d(L, hm->lr.p + hb.off, hb.m, hb.m, hm->R, lb.U, hb.m);
                 copy2d(L, hm->lr.p + hb.off + hb.m * hb.kcap, hb.n, hb.n, hm->R, lb.V, hb.n);
-                // compress the Taylor factors themselves (W_{.0} = 0, reading A11)
-                int kk = lb.k;
-                truncate(L, lb.U, lb.V, hb.m, hb.n, kk);
-                lb.k = kk;
             }
         }
+        // compress the Taylor factors themselves (W_{.0} = 0, reading A11): one batch
+        L->is_dirty.assign(L->B.size(), 0);
+        for (size_t b = 0; b < L->B.size(); ++b)
+            if (L->B[b].type == HB_LR) mark_dirty(L, (int)b);
+        flush_dirty(L);
         hlu_rec(L, L->S.root);
         FDE_CUDA(cudaMemcpyAsync(L->pinned, L->dflag.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, h->stream));
         FDE_CUDA(cudaEventRecord(h->ev1, h->stream));
@@ -1168,18 +1593,19 @@ __device__ __forceinline__ void cta_rows_dot(const double* M, long long ldm, lon
 }
 
 __device__ void run_sweep(const SweepDev& S, int backward, double* x, long long ldx, int nrhs, double* z, double* t,
-                          int tstride, cg::cluster_group& cl)
+                          int tstride, cg::grid_group& cl)
 {
     __shared__ double part[APPLY_THREADS];
-    const int nwarps = APPLY_CTAS * (APPLY_THREADS / 32);
-    const int cta = (int)cl.block_rank();
+    const int nctas = gridDim.x;
+    const int nwarps = nctas * (APPLY_THREADS / 32);
+    const int cta = blockIdx.x;
     const int gw = cta * (APPLY_THREADS / 32) + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
     int prev = -1;
     for (int s = 0; s < S.nleaf; ++s) {
         const int k = backward ? S.nleaf - 1 - s : s;
         const SLeaf L = S.leaf[k];
-        const int rows_per = (L.m + APPLY_CTAS - 1) / APPLY_CTAS;
+        const int rows_per = max(1, (L.m + nctas - 1) / nctas);
         const int r_lo = cta * rows_per;
         const int nr = max(0, min(L.m - r_lo, rows_per));
         // ---- phase A1: rows of leaf k (this CTA's row slice).  Thread t owns row
@@ -1283,10 +1709,10 @@ __device__ void run_sweep(const SweepDev& S, int backward, double* x, long long 
     }
 }
 
-__global__ void __cluster_dims__(APPLY_CTAS, 1, 1) __launch_bounds__(APPLY_THREADS)
+__global__ void __launch_bounds__(APPLY_THREADS)
     k_apply(SweepDev fwd, SweepDev bwd, double* x, long long ldx, int nrhs, double* z, double* t, int tstride)
 {
-    cg::cluster_group cl = cg::this_cluster();
+    cg::grid_group cl = cg::this_grid();
     run_sweep(fwd, 0, x, ldx, nrhs, z, t, tstride, cl);
     run_sweep(bwd, 1, x, ldx, nrhs, z, t, tstride, cl);
 }
@@ -1351,12 +1777,17 @@ static ApplySched* apply_sched_build(fde_lu* L)
         if (m == 0) continue;
         double* Li = A->inv.p + invoff[q];
         double* Ui = Li + m * m;
+        if (D.Li && D.Ui) {   // computed during the factorisation
+            copy2d(L, D.Li, m, m, m, Li, m);
+            copy2d(L, D.Ui, m, m, m, Ui, m);
+            continue;
+        }
         k_eye<<<64, 256, 0, L->h->stream>>>(Li, m, (int)m);
         FDE_CHECK_LAUNCH();
         k_eye<<<64, 256, 0, L->h->stream>>>(Ui, m, (int)m);
         FDE_CHECK_LAUNCH();
-        leaf_trsm(L, D, Li, m, m, 0);
-        leaf_trsm(L, D, Ui, m, m, 1);
+        leaf_trsm_raw(L, D, Li, m, m, 0);
+        leaf_trsm_raw(L, D, Ui, m, m, 1);
     }
     // per-leaf lists
     std::vector<std::vector<SDense>> df(nl), db(nl);
@@ -1460,7 +1891,14 @@ static void apply_sched_run(fde_ctx* h, fde_lu* L, double* x, int64_t ldx, int n
     }
     SweepDev f{A->leaf_f.p, A->nleaf, A->dense_f.p, A->lrr_f.p, A->proj_f.p};
     SweepDev b{A->leaf_b.p, A->nleaf, A->dense_b.p, A->lrr_b.p, A->proj_b.p};
-    k_apply<<<APPLY_CTAS, APPLY_THREADS, 0, h->stream>>>(f, b, x, ldx, nrhs, A->z.p, A->t.p, A->tslots);
+    // cooperative launch: one CTA per SM (all resident), grid barriers between steps
+    int per_sm = 0;
+    FDE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_apply, APPLY_THREADS, 0));
+    const int nblk = std::max(1, std::min(per_sm, 1)) * h->num_sms;
+    void* args[] = {&f, &b, &x, &ldx, &nrhs, &A->z.p, &A->t.p, &A->tslots};
+    long long ldx_ll = ldx;
+    args[3] = &ldx_ll;
+    FDE_CUDA(cudaLaunchCooperativeKernel((void*)k_apply, nblk, APPLY_THREADS, args, 0, h->stream));
     FDE_CHECK_LAUNCH();
 }
 
