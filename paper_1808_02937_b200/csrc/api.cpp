@@ -23,8 +23,11 @@ void prof_collect(fde_ctx* h, double* out, int reset);
 void hlu_trunc_stats(unsigned long long* out4);
 
 static thread_local std::string g_noctx_err;
+static thread_local cudaStream_t g_alloc_stream = nullptr;
+cudaStream_t fde_alloc_stream() { return g_alloc_stream; }
+void fde_set_alloc_stream(cudaStream_t s) { g_alloc_stream = s; }
 
-#define API_BEGIN try {
+#define API_BEGIN try { if (h) fde_set_alloc_stream(h->stream);
 #define API_END(h)                                                   \
     }                                                                \
     catch (FdeError & e) {                                           \

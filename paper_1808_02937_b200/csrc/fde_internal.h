@@ -39,26 +39,35 @@ extern long long g_fde_launches;
 inline void fde_fail(int code, const std::string& m) { throw FdeError{code, m}; }
 
 // ----------------------------------------------------------- device buffer
+// All library buffers come from the device's stream-ordered memory pool on the
+// stream of the API call in progress (fde_set_alloc_stream); the pool keeps
+// freed memory (release threshold = max), so a cold solve does not pay for
+// cudaMalloc/cudaFree page mapping and implicit device synchronisation.
+cudaStream_t fde_alloc_stream();
+void fde_set_alloc_stream(cudaStream_t s);
+
 template <typename T>
 struct DBuf {
     T* p = nullptr;
     size_t n = 0;
+    cudaStream_t s = nullptr;
     DBuf() = default;
     DBuf(const DBuf&) = delete;
     DBuf& operator=(const DBuf&) = delete;
     ~DBuf() { release(); }
     void release() {
-        if (p) cudaFree(p);
+        if (p) cudaFreeAsync(p, s);
         p = nullptr;
         n = 0;
     }
     void alloc(size_t count) {
         release();
         if (count == 0) return;
-        cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+        s = fde_alloc_stream();
+        cudaError_t e = cudaMallocAsync(&p, count * sizeof(T), s);
         if (e != cudaSuccess) {
             p = nullptr;
-            throw FdeError{FDE_ENOMEM, std::string("cudaMalloc failed: ") + cudaGetErrorString(e)};
+            throw FdeError{FDE_ENOMEM, std::string("cudaMallocAsync failed: ") + cudaGetErrorString(e)};
         }
         n = count;
     }
