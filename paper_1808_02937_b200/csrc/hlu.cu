@@ -269,6 +269,140 @@ __global__ void k_leaf_trsm(const double* __restrict__ D, int m, long long ld, d
         if (t * 32 + lane < m) x[t * 32 + lane] = r[t];
 }
 
+// same triangular solves with the factor staged in shared memory (m <= 128):
+// one CTA, each warp sweeps whole right-hand-side columns (rows spread over lanes)
+template <int TRN>
+__global__ void __launch_bounds__(1024) k_leaf_trsm_smem(const double* __restrict__ D, int m, long long ld, double* X,
+                                                        long long ldx, int ncols, int mode)
+{
+    extern __shared__ double T[];   // m x m, column-major copy of D
+    for (int t = threadIdx.x; t < m * m; t += blockDim.x) T[t] = D[(long long)(t / m) * ld + (t % m)];
+    __syncthreads();
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const bool fwd = (mode != 1);
+    for (int col = blockIdx.x * nw + w; col < ncols; col += gridDim.x * nw) {
+        double* x = X + (long long)col * ldx;
+        double r[TRN];
+#pragma unroll
+        for (int t = 0; t < TRN; ++t) r[t] = (t * 32 + lane < m) ? x[t * 32 + lane] : 0.0;
+        for (int s = 0; s < m; ++s) {
+            const int i = fwd ? s : m - 1 - s;
+            const int ti = i >> 5, li = i & 31;
+            double xi = 0.0;
+#pragma unroll
+            for (int t = 0; t < TRN; ++t)
+                if (t == ti) xi = r[t];
+            xi = __shfl_sync(0xffffffffu, xi, li);
+            if (mode != 0) xi /= T[i * m + i];
+            if (lane == li) {
+#pragma unroll
+                for (int t = 0; t < TRN; ++t)
+                    if (t == ti) r[t] = xi;
+            }
+#pragma unroll
+            for (int t = 0; t < TRN; ++t) {
+                const int row = t * 32 + lane;
+                if (row < m && (fwd ? row > i : row < i)) {
+                    const double l = (mode == 2) ? T[row * m + i] : T[i * m + row];
+                    r[t] = fma(-l, xi, r[t]);
+                }
+            }
+        }
+#pragma unroll
+        for (int t = 0; t < TRN; ++t)
+            if (t * 32 + lane < m) x[t * 32 + lane] = r[t];
+    }
+}
+
+// Blocked triangular inverse for m <= 128 in shared memory (one CTA, 1024 threads).
+// Blocks of 32: the lower triangle of a 4x4 block grid (10 blocks) for the matrix
+// and for the inverse.  upper = 0: inverse of the unit-lower factor of D;
+// upper = 1: inverse of the upper factor, computed as ((U^T)^{-1})^T.
+//   X_ii = L_ii^{-1} (warp per diagonal block, lane per column),
+//   X_ij = -X_ii sum_{k=j}^{i-1} L_ik X_kj   (block diagonals d = i-j = 1..3).
+#define TI_B 32
+__device__ __forceinline__ int ti_pos(int i, int j) { return (i * (i + 1) / 2 + j) * TI_B * TI_B; }
+
+__global__ void __launch_bounds__(1024) k_tri_inv128(const double* __restrict__ D, int m, long long ld, int upper,
+                                                    double* out, long long ldo)
+{
+    extern __shared__ double sm[];
+    double* Lb = sm;                      // 10 blocks
+    double* Xb = Lb + 10 * TI_B * TI_B;   // 10 blocks
+    double* Tb = Xb + 10 * TI_B * TI_B;   // 3 scratch blocks
+    const int nb = (m + TI_B - 1) / TI_B;
+    const int nblk = nb * (nb + 1) / 2;
+    // load (row-major inside a block: [r][c] at r*32 + c); pad with identity
+    for (int t = threadIdx.x; t < nblk * TI_B * TI_B; t += blockDim.x) {
+        const int b = t / (TI_B * TI_B), e = t % (TI_B * TI_B);
+        int i = 0;
+        while ((i + 1) * (i + 2) / 2 <= b) ++i;
+        const int j = b - i * (i + 1) / 2;
+        const int r = e / TI_B, c = e % TI_B;
+        const int gr = i * TI_B + r, gc = j * TI_B + c;
+        double v;
+        if (gr >= m || gc >= m) v = (gr == gc) ? 1.0 : 0.0;
+        else if (!upper) v = (gr == gc) ? 1.0 : (gr > gc ? D[(long long)gc * ld + gr] : 0.0);
+        else v = (gr >= gc) ? D[(long long)gr * ld + gc] : 0.0;   // (U^T)[gr][gc] = U[gc][gr]
+        Lb[t] = v;
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    // diagonal blocks: warp w < nb inverts block (w,w); lane = column
+    if (w < nb) {
+        const double* Lw = Lb + ti_pos(w, w);
+        double* Xw = Xb + ti_pos(w, w);
+        double x[TI_B];
+#pragma unroll
+        for (int r = 0; r < TI_B; ++r) {
+            double s = (r == lane) ? 1.0 : 0.0;
+#pragma unroll
+            for (int k = 0; k < r; ++k) s = fma(-Lw[r * TI_B + k], x[k], s);
+            x[r] = s / Lw[r * TI_B + r];
+        }
+#pragma unroll
+        for (int r = 0; r < TI_B; ++r) Xw[r * TI_B + lane] = x[r];
+    }
+    __syncthreads();
+    for (int d = 1; d < nb; ++d) {
+        const int nbd = nb - d;   // blocks (j + d, j), j < nbd
+        for (int t = threadIdx.x; t < nbd * TI_B * TI_B; t += blockDim.x) {
+            const int j = t / (TI_B * TI_B), e = t % (TI_B * TI_B), i = j + d;
+            const int r = e / TI_B, c = e % TI_B;
+            double s = 0.0;
+            for (int k = j; k < i; ++k) {
+                const double* Lik = Lb + ti_pos(i, k);
+                const double* Xkj = Xb + ti_pos(k, j);
+#pragma unroll 8
+                for (int q = 0; q < TI_B; ++q) s = fma(Lik[r * TI_B + q], Xkj[q * TI_B + c], s);
+            }
+            Tb[j * TI_B * TI_B + e] = s;
+        }
+        __syncthreads();
+        for (int t = threadIdx.x; t < nbd * TI_B * TI_B; t += blockDim.x) {
+            const int j = t / (TI_B * TI_B), e = t % (TI_B * TI_B), i = j + d;
+            const int r = e / TI_B, c = e % TI_B;
+            const double* Xii = Xb + ti_pos(i, i);
+            double s = 0.0;
+#pragma unroll 8
+            for (int q = 0; q < TI_B; ++q) s = fma(Xii[r * TI_B + q], Tb[j * TI_B * TI_B + q * TI_B + c], s);
+            Xb[ti_pos(i, j) + e] = -s;
+        }
+        __syncthreads();
+    }
+    // write out (column-major, ldo); the other triangle is zero
+    for (int t = threadIdx.x; t < m * m; t += blockDim.x) {
+        const int gc = t / m, gr = t % m;          // out[gr][gc]
+        const int lr = upper ? gc : gr, lc = upper ? gr : gc;   // element of X (lower)
+        double v = 0.0;
+        if (lr >= lc) {
+            const int i = lr / TI_B, j = lc / TI_B;
+            v = Xb[ti_pos(i, j) + (lr % TI_B) * TI_B + (lc % TI_B)];
+        }
+        out[(long long)gc * ldo + gr] = v;
+    }
+}
+
 // B (n x m) = A^T (A: m x n), column-major
 __global__ void k_transpose(const double* A, long long lda, int m, int n, double* B, long long ldb)
 {
@@ -795,13 +929,32 @@ static void smem_lu(fde_lu* L, double* D, int64_t m, int64_t ld)
 {
     const size_t sm = (size_t)m * m * sizeof(double);
     FDE_CUDA(cudaFuncSetAttribute(k_dense_lu_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    k_dense_lu_smem<<<1, 1024, sm, L->h->stream>>>(D, (int)m, ld, L->dflag.p);
+    k_dense_lu_smem<<<1, 512, sm, L->h->stream>>>(D, (int)m, ld, L->dflag.p);
     FDE_CHECK_LAUNCH();
     L->nops++;
 }
 
 static void trsm_raw(fde_lu* L, const double* D, int64_t m, int64_t ld, double* X, int64_t ldx, int64_t ncols, int mode)
 {
+    if (m <= 128 && ncols >= 8) {
+        const size_t sm = (size_t)m * m * sizeof(double);
+        const unsigned g = (unsigned)std::min<int64_t>(ceil_div(ncols, 32), 8);
+        cudaStream_t st = L->h->stream;
+        const int nr = (int)ceil_div(m, 32);
+        if (nr <= 1) {
+            FDE_CUDA(cudaFuncSetAttribute(k_leaf_trsm_smem<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            k_leaf_trsm_smem<1><<<g, 1024, sm, st>>>(D, (int)m, ld, X, ldx, (int)ncols, mode);
+        } else if (nr <= 2) {
+            FDE_CUDA(cudaFuncSetAttribute(k_leaf_trsm_smem<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            k_leaf_trsm_smem<2><<<g, 1024, sm, st>>>(D, (int)m, ld, X, ldx, (int)ncols, mode);
+        } else {
+            FDE_CUDA(cudaFuncSetAttribute(k_leaf_trsm_smem<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            k_leaf_trsm_smem<4><<<g, 1024, sm, st>>>(D, (int)m, ld, X, ldx, (int)ncols, mode);
+        }
+        FDE_CHECK_LAUNCH();
+        L->nops++;
+        return;
+    }
     const int wpb = 4;
     const unsigned g = (unsigned)ceil_div(ncols, wpb);
     cudaStream_t st = L->h->stream;
@@ -821,12 +974,11 @@ static void trsm_raw(fde_lu* L, const double* D, int64_t m, int64_t ld, double* 
 static void tri_inv(fde_lu* L, const double* D, int64_t m, int64_t ld, int upper, double* out, int64_t ldo)
 {
     if (m <= 128) {
-        double* I = lu_alloc(L, (size_t)m * m);
-        k_eye<<<64, 256, 0, L->h->stream>>>(I, m, (int)m);
+        const size_t sm = (size_t)23 * TI_B * TI_B * sizeof(double);
+        FDE_CUDA(cudaFuncSetAttribute(k_tri_inv128, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        k_tri_inv128<<<1, 1024, sm, L->h->stream>>>(D, (int)m, ld, upper, out, ldo);
         FDE_CHECK_LAUNCH();
-        trsm_raw(L, D, m, ld, I, m, m, upper ? 1 : 0);
-        copy2d(L, I, m, m, m, out, ldo);
-        lu_free(L, I);
+        L->nops++;
         return;
     }
     const int64_t m0 = (m / 2 + 31) / 32 * 32, m1 = m - m0;
