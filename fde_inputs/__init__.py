@@ -211,10 +211,24 @@ def config5(N: int = 4096, P: int = 8, nrhs: int = 64) -> Problem:
                    forcings=[random_legendre_forcing(s) for s in range(nrhs)], mesh_kind="uniform")
 
 
-def example51(N: int = 100, P: int = 3, alpha: float = 1.6, rho: float = 0.0) -> Problem:
-    """Example 5.1: theta=1, graded q=5 on (0,10); alpha per A16."""
-    return Problem(f"ex51-N{N}-P{P}", 0.0, 10.0, alpha, 1.0, rho, 0.0, 0.0, graded_mesh(0, 10, N, 5.0), P, 5,
-                   forcings=[], mesh_kind="graded")
+def example51(N: int = 100, P: int = 3, alpha: float = 1.6, rho: float = 0.0, R: int = 5,
+              n_min: int = 16) -> Problem:
+    """Example 5.1: theta=1, u = (x-a) - (b-a)^{1-g}(x-a)^g, a=0, b=10,
+    g=0.8, graded mesh x_i = (i/N)^5 (b-a); alpha = 1.6 (reading A16).
+    f = -D^2 aI^{2-alpha} u + rho u from the monomial closed form
+    -D^2 aI^{2-alpha} x^k = -Gamma(k+1)/Gamma(k+1-alpha) x^{k-alpha}."""
+    a, b, g = 0.0, 10.0, 0.8
+    c = (b - a) ** (1 - g)
+    terms = [("L", 1.0 - alpha, -math.gamma(2.0) / math.gamma(2.0 - alpha)),
+             ("L", g - alpha, c * math.gamma(g + 1) / math.gamma(g + 1 - alpha))]
+    if rho != 0.0:
+        terms += [("L", 1.0, rho), ("L", g, -rho * c)]
+    return Problem(f"ex51-N{N}-P{P}-R{R}", a, b, alpha, 1.0, rho, 0.0, 0.0, graded_mesh(a, b, N, 5.0), P, R,
+                   n_min=n_min, forcings=[Forcing(terms=terms)], mesh_kind="graded")
+
+
+def example51_exact(x: np.ndarray) -> np.ndarray:
+    return x - 10.0 ** 0.2 * np.power(x, 0.8)
 
 
 CONFIGS = {"c1": config1, "c2": config2, "c3": config3, "c4": config4, "c5": config5}

@@ -111,6 +111,12 @@ long long fde_launch_count(void);
  * compacted widths, sum of Jacobi sweeps, max width}. */
 int fde_debug_trunc_stats(unsigned long long* out4);
 
+/* Row-block sharding of the dense operator over `world` GPUs (host function,
+ * usable without a device): rank owns internal rows [*r0, *r1) = the dofs of
+ * elements [N*rank/world, N*(rank+1)/world); *rows_max = largest shard (the
+ * all-gather pads every shard to it). */
+int fde_shard_rows(int N, int P, int world, int rank, int64_t* r0, int64_t* r1, int64_t* rows_max);
+
 /* --------------------------------------------------------- sem_assemble */
 enum { FDE_OP_DENSE = 1, FDE_OP_TOEPLITZ = 2 };
 

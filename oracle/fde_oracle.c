@@ -463,14 +463,13 @@ int orc_load(int N, const double *nodes, int P, double a, double b,
         ld xl = nodes[e], xr = nodes[e + 1], h = xr - xl;
         ld loc[MAXP + 1];
         for (int k = 0; k < M; ++k) loc[k] = 0;
-        /* Legendre part + power terms away from their base element */
+        /* Legendre part (and integer powers): Gauss-Legendre on two halves */
         for (int half = 0; half < 2; ++half) {
             for (int k = 0; k < q; ++k) {
                 ld xi = -1 + half + 0.5L * (gx[k] + 1);          /* reference point in the half */
                 ld w = 0.5L * gw[k] * 0.5L * h;
                 ld v[MAXP + 1];
                 local_value(P, xi, v);
-                /* offsets from a and b computed from node differences */
                 ld offa = ((ld)nodes[e] - A) + 0.5L * h * (xi + 1);
                 ld offb = (B - (ld)nodes[e + 1]) + 0.5L * h * (1 - xi);
                 ld fx = 0;
@@ -480,12 +479,32 @@ int orc_load(int N, const double *nodes, int P, double a, double b,
                     for (int kk = 0; kk < nleg; ++kk) fx += leg[kk] * Lk[kk];
                 }
                 for (int t = 0; t < nterm; ++t) {
-                    int touches = (side[t] == 0) ? (e == 0) : (e == N - 1);
                     int integer_pw = (pw[t] == floor(pw[t]) && pw[t] >= 0);
-                    if (touches && !integer_pw) continue;
+                    if (!integer_pw) continue;
                     fx += coef[t] * powl(side[t] == 0 ? offa : offb, pw[t]);
                 }
                 for (int k2 = 0; k2 < M; ++k2) loc[k2] += w * fx * v[k2];
+            }
+        }
+        /* non-integer powers away from their base element: composite Gauss-Legendre on
+         * cells [o, 2o] of the distance o to the base point (cell size = distance) */
+        for (int t = 0; t < nterm; ++t) {
+            int touches = (side[t] == 0) ? (e == 0) : (e == N - 1);
+            int integer_pw = (pw[t] == floor(pw[t]) && pw[t] >= 0);
+            if (touches || integer_pw) continue;
+            ld o0 = (side[t] == 0) ? ((ld)nodes[e] - A) : (B - (ld)nodes[e + 1]);
+            ld oend = o0 + h, oa = o0;
+            while (oa < oend) {
+                ld ob = 2 * oa < oend ? 2 * oa : oend;
+                for (int k = 0; k < q; ++k) {
+                    ld o = oa + 0.5L * (ob - oa) * (gx[k] + 1);
+                    ld w = 0.5L * (ob - oa) * gw[k] * coef[t] * powl(o, (ld)pw[t]);
+                    ld xi = (side[t] == 0) ? (2 * (o - o0) / h - 1) : (1 - 2 * (o - o0) / h);
+                    ld v[MAXP + 1];
+                    local_value(P, xi, v);
+                    for (int k2 = 0; k2 < M; ++k2) loc[k2] += w * v[k2];
+                }
+                oa = ob;
             }
         }
         /* singular power terms on the touching element: Gauss-Jacobi */

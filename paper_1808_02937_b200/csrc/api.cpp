@@ -134,6 +134,22 @@ int fde_debug_trunc_stats(unsigned long long* out4)
 
 long long fde_launch_count(void) { return __atomic_load_n(&g_fde_launches, __ATOMIC_RELAXED); }
 
+// Row-block partition of the dense operator (host logic, no device needed):
+// rank g owns elements [N g / G, N (g+1) / G) and their dofs (element-interleaved
+// rows [e_lo P, min(e_hi P, n))); rows_max pads every shard for the all-gather.
+int fde_shard_rows(int N, int P, int world, int rank, int64_t* r0, int64_t* r1, int64_t* rows_max)
+{
+    if (N < 1 || P < 1 || world < 1 || rank < 0 || rank >= world || !r0 || !r1 || !rows_max) return FDE_EINVAL_PARAM;
+    const int64_t n = (int64_t)N * P - 1;
+    auto start = [&](int g) { return std::min((int64_t)((int64_t)N * g / world) * P, n); };
+    *r0 = start(rank);
+    *r1 = start(rank + 1);
+    int64_t mx = 1;
+    for (int g = 0; g < world; ++g) mx = std::max(mx, start(g + 1) - start(g));
+    *rows_max = mx;
+    return FDE_OK;
+}
+
 // ------------------------------------------------------------ validation
 static void validate(const fde_problem* p, const fde_mesh* m)
 {
@@ -178,13 +194,13 @@ int sem_assemble(fde_handle h, const fde_problem* prob, const fde_mesh* mesh, in
     // element partition over ranks
     const int G = h->world, N = op->N, P = op->P;
     op->rank_r0.resize(G + 1);
-    int64_t rmax = 0;
-    for (int g = 0; g <= G; ++g) {
-        int e = (int)((int64_t)N * g / G);
-        op->rank_r0[g] = std::min((int64_t)e * P, op->n);
+    for (int g = 0; g < G; ++g) {
+        int64_t a0, a1, mx;
+        fde_shard_rows(N, P, G, g, &a0, &a1, &mx);
+        op->rank_r0[g] = a0;
+        op->rank_r0[g + 1] = a1;
+        op->rows_max = mx;
     }
-    for (int g = 0; g < G; ++g) rmax = std::max(rmax, op->rank_r0[g + 1] - op->rank_r0[g]);
-    op->rows_max = std::max<int64_t>(rmax, 1);
     op->e_lo = (int)((int64_t)N * h->rank / G);
     op->e_hi = (int)((int64_t)N * (h->rank + 1) / G);
     op->r0 = op->rank_r0[h->rank];

@@ -136,9 +136,17 @@ void dense_gemv_raw(cudaStream_t s, const double* A, long long lda, long long ro
     }
 }
 
+void dense_gemm_dmma(cudaStream_t s, const double* A, long long lda, long long rows, long long ncol, const double* X,
+                     long long ldx, double* Y, long long ldy, int nrhs);
+
+// y = A x on the shard: GEMV (HBM-bound) for up to 4 RHS per pass, the DMMA
+// GEMM (FP64 tensor cores, one pass over A) from 8 RHS on
 void dense_gemv(fde_ctx* h, fde_op* op, const double* x, int64_t ldx, double* y, int64_t ldy, int nrhs)
 {
-    dense_gemv_raw(h->stream, op->A.p, op->lda, op->r1 - op->r0, x, ldx, y, ldy, nrhs);
+    if (nrhs >= 8 && (op->lda % 2) == 0 && (ldx % 2) == 0)
+        dense_gemm_dmma(h->stream, op->A.p, op->lda, op->r1 - op->r0, op->lda, x, ldx, y, ldy, nrhs);
+    else
+        dense_gemv_raw(h->stream, op->A.p, op->lda, op->r1 - op->r0, x, ldx, y, ldy, nrhs);
 }
 
 // ------------------------------------------------------------------ NCCL
@@ -269,7 +277,8 @@ void op_apply_internal(fde_ctx* h, fde_op* op, const double* x, int64_t ldx, dou
         return;
     }
     if (!(op->flags & FDE_OP_DENSE)) fde_fail(FDE_EINVAL_PARAM, "operator has no dense form");
-    const double gemv_bytes = 8.0 * (double)(op->r1 - op->r0) * (double)op->n * (double)((nrhs + 3) / 4) +
+    const double passes = (nrhs >= 8) ? 1.0 : (double)((nrhs + 3) / 4);
+    const double gemv_bytes = 8.0 * (double)(op->r1 - op->r0) * (double)op->n * passes +
                               8.0 * (double)op->n * nrhs + 8.0 * (double)(op->r1 - op->r0) * nrhs;
     if (h->world == 1) {
         const int pi = prof_begin(h, PROF_GEMV, gemv_bytes);
@@ -382,4 +391,115 @@ void prof_collect(fde_ctx* h, double* out, int reset)
         }
         h->prof.clear();
     }
+}
+
+// ------------------------------------------------- multi-RHS DMMA GEMM
+// Y[rows x k] = A[rows x n] X[n x k] for k >= 8 right-hand sides (config 5: 64):
+// FP64 tensor cores through mma.sync.m8n8k4.f64 (DMMA; tcgen05 has no f64 kind).
+// CTA tile 64 rows x 64 RHS x 32 (K), 8 warps of 16 x 32, 3-stage cp.async
+// pipeline; A is streamed once from HBM, X (L2-resident) once per row tile.
+#define DG_BM 64
+#define DG_BN 64
+#define DG_BK 32
+#define DG_LD 36      // padded smem row (doubles)
+#define DG_STAGES 3
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred)
+{
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    const int sz = pred ? 16 : 0;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
+{
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(256) k_gemm_dmma(const double* __restrict__ A, long long lda, long long rows,
+                                                  long long ncol, const double* __restrict__ X, long long ldx, int nrhs,
+                                                  double* __restrict__ Y, long long ldy)
+{
+    extern __shared__ __align__(16) double dsm[];
+    double* As = dsm;                                    // [stage][64][DG_LD]
+    double* Xs = dsm + DG_STAGES * DG_BM * DG_LD;        // [stage][64 rhs][DG_LD]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const long long m0 = (long long)blockIdx.x * DG_BM;
+    const int n0 = blockIdx.y * DG_BN;
+    const int wm = (warp & 3) * 16, wn = (warp >> 2) * 32;
+    double acc[2][4][2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    const int nk = (int)((ncol + DG_BK - 1) / DG_BK);
+    auto load_stage = [&](int st, int kt) {
+        const long long k0 = (long long)kt * DG_BK;
+        double* as = As + st * DG_BM * DG_LD;
+        double* xs = Xs + st * DG_BN * DG_LD;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const int id = tid + c * 256;                // 1024 16-byte chunks per operand
+            const int r = id >> 4, kk = (id & 15) * 2;
+            const long long gr = m0 + r, gk = k0 + kk;
+            const bool pa = (gr < rows) && (gk < ncol);
+            cp_async16(as + r * DG_LD + kk, A + (pa ? gr * lda + gk : 0), pa);
+            const int rhs = n0 + r;
+            const bool px = (rhs < nrhs) && (gk < ncol);
+            cp_async16(xs + r * DG_LD + kk, X + (px ? (long long)rhs * ldx + gk : 0), px);
+        }
+    };
+#pragma unroll
+    for (int s = 0; s < DG_STAGES - 1; ++s) {
+        if (s < nk) load_stage(s, s);
+        cp_async_commit();
+    }
+    for (int kt = 0; kt < nk; ++kt) {
+        cp_async_wait<DG_STAGES - 2>();
+        __syncthreads();
+        const int nxt = kt + DG_STAGES - 1;
+        if (nxt < nk) load_stage(nxt % DG_STAGES, nxt);
+        cp_async_commit();
+        const double* as = As + (kt % DG_STAGES) * DG_BM * DG_LD;
+        const double* xs = Xs + (kt % DG_STAGES) * DG_BN * DG_LD;
+#pragma unroll
+        for (int kk = 0; kk < DG_BK; kk += 4) {
+            double a[2], b[4];
+#pragma unroll
+            for (int i = 0; i < 2; ++i) a[i] = as[(wm + i * 8 + (lane >> 2)) * DG_LD + kk + (lane & 3)];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) b[j] = xs[(wn + j * 8 + (lane >> 2)) * DG_LD + kk + (lane & 3)];
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+        }
+    }
+    cp_async_wait<0>();
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const long long r = m0 + wm + i * 8 + (lane >> 2);
+            const int c = n0 + wn + j * 8 + (lane & 3) * 2;
+            if (r < rows) {
+                if (c < nrhs) Y[(long long)c * ldy + r] = acc[i][j][0];
+                if (c + 1 < nrhs) Y[(long long)(c + 1) * ldy + r] = acc[i][j][1];
+            }
+        }
+}
+
+void dense_gemm_dmma(cudaStream_t s, const double* A, long long lda, long long rows, long long ncol, const double* X,
+                     long long ldx, double* Y, long long ldy, int nrhs)
+{
+    const size_t smem = (size_t)DG_STAGES * (DG_BM + DG_BN) * DG_LD * sizeof(double);
+    FDE_CUDA(cudaFuncSetAttribute(k_gemm_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    dim3 g((unsigned)ceil_div(rows, DG_BM), (unsigned)ceil_div(nrhs, DG_BN));
+    k_gemm_dmma<<<g, 256, smem, s>>>(A, lda, rows, ncol, X, ldx, nrhs, Y, ldy);
+    FDE_CHECK_LAUNCH();
 }

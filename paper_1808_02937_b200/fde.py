@@ -39,7 +39,7 @@ EXPORTED = [
     "sem_rhs", "stiffness_matvec", "hmatrix_build", "fde_hmatrix_get_info", "fde_hmatrix_dense_paper",
     "hlu_factor", "fde_hlu_get_info", "fde_hlu_dense_internal", "precond_apply", "solve", "fde_solve",
     "fde_free_operator", "fde_free_hmatrix", "fde_free_hlu", "fde_profile", "fde_profile_collect",
-    "fde_launch_count",
+    "fde_launch_count", "fde_shard_rows",
 ]
 
 
@@ -128,6 +128,8 @@ def lib():
         L.fde_hlu_dense_internal.argtypes = [vp, vp, vp, i64]
         L.fde_profile.argtypes = [vp, i32]
         L.fde_profile_collect.argtypes = [vp, ctypes.POINTER(ctypes.c_double), i32]
+        L.fde_shard_rows.argtypes = [i32, i32, i32, i32, ctypes.POINTER(i64), ctypes.POINTER(i64),
+                                     ctypes.POINTER(i64)]
         L.fde_launch_count.argtypes = []
         L.fde_launch_count.restype = ctypes.c_longlong
         L.solve.argtypes = [vp, vp, vp, vp, vp, i32, i64, ctypes.POINTER(SolveOpts), ctypes.POINTER(SolveReport)]
@@ -180,6 +182,13 @@ class Handle:
             self.close()
         except Exception:
             pass
+
+
+def shard_rows(N: int, P: int, world: int, rank: int):
+    """(r0, r1, rows_max) of this rank's row block (internal order), host-only."""
+    a, b, c = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+    _check(lib().fde_shard_rows(N, P, world, rank, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)))
+    return a.value, b.value, c.value
 
 
 def nccl_unique_id() -> bytes:

@@ -1,0 +1,110 @@
+"""Parity at the BASELINE sizes, in the launch configuration bench.py times.
+
+* config 2 (N=256, P=8, alpha=1.5): the full dense operator against the oracle
+  (metric M-A) and the Toeplitz FFT matvec against the oracle's A x (M-B).
+* config 3 (geometric layers, P=16): full operator (M-A) and the solve (M-D).
+* config 4 (N=1024, P=8, n=8191 -- the bench workload): sampled rows.  For
+  columns J whose element lies more than one element left of row I's element,
+  A_IJ = theta * S_l[I,J] exactly (S_l^T and M vanish there), so the oracle's
+  row assembly of the sampled elements pins every far-field entry of those rows.
+  The cold solve of bench.py (assemble + rhs + hmatrix + H-LU + GMRES) must
+  reach a backward error at rounding level.
+"""
+import numpy as np
+import pytest
+
+import fde_inputs as fi
+import oracle as O
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def fde():
+    from paper_1808_02937_b200 import fde as F
+    return F
+
+
+@pytest.fixture(scope="module")
+def h(fde):
+    return fde.Handle(0)
+
+
+def metric_A(Ag, Ao):
+    d = np.sqrt(np.abs(np.diag(Ao)))
+    return np.max(np.abs(Ag - Ao) / (d[:, None] * d[None, :]))
+
+
+def test_config2_full_operator_and_fft(fde, h):
+    p = fi.config2(1.5)
+    op = fde.assemble_problem(h, p, flags=fde.OP_DENSE | fde.OP_TOEPLITZ)
+    Ag = fde.operator_dense_paper(h, op).cpu().numpy()
+    so = O.assemble_system(p)
+    assert metric_A(Ag, so.A) <= 1e-10
+    X = np.random.default_rng(11).standard_normal((2, p.n))
+    Yf = fde.stiffness_matvec(h, op, torch.tensor(X, device="cuda"), path=fde.PATH_TOEPLITZ).cpu().numpy()
+    Yo = (so.A @ X.T).T
+    den = (np.abs(so.A) @ np.abs(X.T)).T
+    assert np.max(np.abs(Yf - Yo) / den) <= 1e-10
+    G = fde.sem_rhs(h, op, p.forcings)
+    Go = O.rhs(p, so, p.forcings[0])
+    assert np.max(np.abs(G.cpu().numpy()[0] - Go)) <= 1e-12 * np.abs(Go).max()
+    op.free()
+
+
+def test_config3_full_P16_operator_and_solve(fde, h):
+    p = fi.config3(16)
+    op = fde.assemble_problem(h, p)
+    Ag = fde.operator_dense_paper(h, op).cpu().numpy()
+    so = O.assemble_system(p)
+    assert metric_A(Ag, so.A) <= 1e-10
+    G = fde.sem_rhs(h, op, p.forcings)
+    hm = fde.hmatrix_build(h, op, p.R, 1.0, 4)
+    lu = fde.hlu_factor(h, hm, 1e-3)
+    X, rep = fde.solve(h, op, lu, G, tol=1e-13)
+    Xo = O.solve_dense(so.A, O.rhs(p, so, p.forcings[0]))
+    x = X.cpu().numpy()[0]
+    D = np.abs(np.diag(so.A))
+    # cond(A) ~ 1e11 here (h_min = 1.5e-14); the D-norm error is bounded by kappa * eps
+    err = np.sqrt(np.sum(D * (x - Xo) ** 2) / np.sum(D * Xo ** 2))
+    assert err <= 1e-8, err
+    for o in (lu, hm, op):
+        o.free()
+
+
+def test_config4_sampled_rows_and_cold_solve(fde, h):
+    p = fi.config4()
+    op = fde.assemble_problem(h, p)                       # as in bench.py
+    Ag = fde.operator_dense_paper(h, op).cpu().numpy()
+    N, P = p.N, p.P
+    n, nm = O.sizes(N, P)
+    rng = np.random.default_rng(4)
+    elems = sorted(set([0, 1, N // 2, N - 2, N - 1] + list(rng.integers(2, N - 2, 6))))
+    for e in elems:
+        S = O.assemble_Sl_ext(p.nodes, P, p.alpha, e, e + 1)
+        rows = O.paper_index_of_element_dofs(N, P, e, e + 1)
+        rows = [r for r in rows if r < nm] or list(rows)
+        far_elems = range(0, max(0, e - 1))
+        cols = O.paper_index_of_element_dofs(N, P, 0, max(0, e - 1)) if e >= 2 else np.array([], dtype=int)
+        if len(cols) == 0:
+            continue
+        # hats of nodes <= e-1 touch element e-1 only through node e-1: drop them (not far)
+        cols = np.array([c for c in cols if not (c >= nm and c - nm + 1 >= e - 1)])
+        for r in rows:
+            got = Ag[r, cols]
+            ref = p.theta * S[r, cols]
+            scale = np.sqrt(abs(Ag[r, r]) * np.abs(np.diag(Ag)[cols]))
+            assert np.max(np.abs(got - ref) / scale) <= 1e-10
+    G = fde.sem_rhs(h, op, p.forcings)
+    hm = fde.hmatrix_build(h, op, p.R, p.lam, p.n_min)
+    lu = fde.hlu_factor(h, hm, 1e-3)
+    X, rep = fde.solve(h, op, lu, G, tol=1e-12, restart=50, maxiter=500)
+    AX = fde.stiffness_matvec(h, op, X).cpu().numpy()[0]
+    g, x = G.cpu().numpy()[0], X.cpu().numpy()[0]
+    A_norm = np.abs(Ag).sum(axis=1).max()
+    berr = np.abs(g - AX).max() / (A_norm * np.abs(x).max() + np.abs(g).max())
+    assert berr <= 1e-13, berr
+    assert rep.iterations <= 10
+    for o in (lu, hm, op):
+        o.free()

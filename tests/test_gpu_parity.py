@@ -239,3 +239,63 @@ def test_hlu_preconditioned_gmres_matches_oracle(fde, h, case):
     assert np.linalg.norm(At @ z - r) / np.linalg.norm(r) < 5e-2
     for o in (lu, hm, op):
         o.free()
+
+
+@pytest.mark.parametrize("nrhs", [8, 37, 64])
+def test_multi_rhs_dmma_matvec_matches_oracle(fde, h, nrhs):
+    """nrhs >= 8 routes the dense matvec to the FP64 tensor-core GEMM (DMMA)."""
+    p = fi.config4(N=40, P=6)
+    op = fde.assemble_problem(h, p)
+    so = oracle_system(p)
+    X = np.random.default_rng(nrhs).standard_normal((nrhs, p.n))
+    Y = fde.stiffness_matvec(h, op, torch.tensor(X, device="cuda"), path=fde.PATH_DENSE).cpu().numpy()
+    Yo = (so.A.astype(np.longdouble) @ X.T.astype(np.longdouble)).T.astype(np.float64)
+    den = (np.abs(so.A) @ np.abs(X.T)).T
+    assert np.max(np.abs(Y - Yo) / den) <= TOL
+    op.free()
+
+
+def test_multi_rhs_solve_matches_single(fde, h):
+    """64 RHS in lockstep (config-5 style) give the same X as one-by-one solves."""
+    p = fi.config2(1.6, N=32, P=8)
+    p.forcings = [fi.random_legendre_forcing(s) for s in range(12)]
+    op = fde.assemble_problem(h, p)
+    hm = fde.hmatrix_build(h, op, 8, 1.0, 4)
+    lu = fde.hlu_factor(h, hm, 1e-3)
+    G = fde.sem_rhs(h, op, p.forcings)
+    X, rep = fde.solve(h, op, lu, G, tol=1e-12)
+    for c in (0, 5, 11):
+        Xc, _ = fde.solve(h, op, lu, G[c:c + 1].clone(), tol=1e-12)
+        assert np.max(np.abs(X[c].cpu().numpy() - Xc[0].cpu().numpy())) <= 1e-9 * np.abs(Xc.cpu().numpy()).max()
+    for o in (lu, hm, op):
+        o.free()
+
+
+def test_example51_bicgstab_iterations_pattern(fde, h):
+    """Example 5.1 (Table 1 setting PAPER.md:794-815): preconditioned
+    BiCGSTAB at tol 1e-13 converges in a handful of iterations, non-increasing in R
+    (the table's pattern), and the solution approximates the exact u."""
+    its = []
+    for R in (2, 3, 5, 7):
+        p = fi.example51(N=100, P=3, R=R)
+        op = fde.assemble_problem(h, p)
+        G = fde.sem_rhs(h, op, p.forcings)
+        hm = fde.hmatrix_build(h, op, R, 1.0, p.n_min)
+        lu = fde.hlu_factor(h, hm, 1e-3)
+        X, rep = fde.solve(h, op, lu, G, method=fde.BICGSTAB, tol=1e-13, maxiter=400)
+        its.append(rep.iterations)
+        if R == 7:
+            so = oracle_system(p)
+            Xo = O.solve_dense(so.A, O.rhs(p, so, p.forcings[0]))
+            x = X.cpu().numpy()[0]
+            D = np.abs(np.diag(so.A))
+            assert np.sqrt(np.sum(D * (x - Xo) ** 2) / np.sum(D * Xo ** 2)) <= 1e-9
+            xis = np.linspace(-1, 1, 9)
+            uh = O.eval_solution(p, x, xis)
+            hh = np.diff(p.nodes)
+            xs = p.nodes[:-1, None] + hh[:, None] * (xis[None, :] + 1) / 2
+            assert np.abs(uh - fi.example51_exact(xs)).max() < 1e-3
+        for o in (lu, hm, op):
+            o.free()
+    assert its[-1] <= 10
+    assert all(its[k + 1] <= its[k] + 1 for k in range(3)), its
