@@ -20,6 +20,18 @@
 
 #include "hlu.h"
 
+#include <map>
+
+// cudaFuncSetAttribute once per (kernel, size) -- it is a host API call per launch otherwise
+static void set_smem_once(const void* fn, int bytes)
+{
+    static std::map<const void*, int> done;
+    auto it = done.find(fn);
+    if (it != done.end() && it->second >= bytes) return;
+    FDE_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    done[fn] = bytes;
+}
+
 // --------------------------------------------------------------- kernels
 #define GT 64   // GEMM tile
 #define GK 16
@@ -200,6 +212,67 @@ __global__ void __launch_bounds__(1024) k_dense_lu_smem(double* D, int m, long l
             for (int i = kk + 1 + lane; i < m; i += 32) S[j * m + i] = fma(-S[kk * m + i], ujk, S[j * m + i]);
         }
         __syncthreads();
+    }
+    for (int t = threadIdx.x; t < m * m; t += blockDim.x) D[(long long)(t / m) * ld + (t % m)] = S[t];
+}
+
+// Blocked in-place LU (no pivoting) of an m x m block (m <= 128) in shared memory:
+// panels of 32 -- warp-level LU of the diagonal block, triangular solves of the
+// row / column panels, GEMM update of the trailing matrix.  4 barriers per panel.
+__global__ void __launch_bounds__(512) k_dense_lu_blk(double* D, int m, long long ld, int* bad)
+{
+    extern __shared__ double S[];   // m x m column-major
+    for (int t = threadIdx.x; t < m * m; t += blockDim.x) S[t] = D[(long long)(t / m) * ld + (t % m)];
+    __syncthreads();
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int k0 = 0; k0 < m; k0 += 32) {
+        const int bs = min(32, m - k0);
+        // (1) diagonal block LU by warp 0: lane = column
+        if (w == 0) {
+            for (int kk = 0; kk < bs; ++kk) {
+                const double p = S[(k0 + kk) * m + k0 + kk];
+                if (lane == 0 && (!(fabs(p) > 0.0) || !isfinite(p))) *bad = 1;
+                // column kk below the pivot: l = a / p  (lanes over rows)
+                const int r = k0 + kk + 1 + lane;
+                if (lane < bs - kk - 1) S[(k0 + kk) * m + r] /= p;
+                __syncwarp();
+                // rank-1 update of the block: lane = column j > kk
+                const int j = k0 + kk + 1 + lane;
+                if (lane < bs - kk - 1) {
+                    const double ukj = S[j * m + k0 + kk];
+                    for (int i = k0 + kk + 1; i < k0 + bs; ++i) S[j * m + i] = fma(-S[(k0 + kk) * m + i], ukj, S[j * m + i]);
+                }
+                __syncwarp();
+            }
+        }
+        __syncthreads();
+        const int rest = m - k0 - bs;
+        if (rest > 0) {
+            // (2) row panel U_kj = L_kk^{-1} A_kj : thread per column j (forward substitution)
+            for (int j = k0 + bs + threadIdx.x; j < m; j += blockDim.x)
+                for (int i = k0 + 1; i < k0 + bs; ++i) {
+                    double s2 = S[j * m + i];
+                    for (int q = k0; q < i; ++q) s2 = fma(-S[q * m + i], S[j * m + q], s2);
+                    S[j * m + i] = s2;
+                }
+            // (3) column panel L_ik = A_ik U_kk^{-1} : thread per row i
+            for (int i = k0 + bs + threadIdx.x; i < m; i += blockDim.x)
+                for (int j = k0; j < k0 + bs; ++j) {
+                    double s2 = S[j * m + i];
+                    for (int q = k0; q < j; ++q) s2 = fma(-S[q * m + i], S[j * m + q], s2);
+                    S[j * m + i] = s2 / S[j * m + j];
+                }
+            __syncthreads();
+            // (4) trailing update A_ij -= sum_q L_iq U_qj
+            for (int j = k0 + bs + w; j < m; j += nw)
+                for (int i = k0 + bs + lane; i < m; i += 32) {
+                    double s2 = S[j * m + i];
+#pragma unroll 8
+                    for (int q = k0; q < k0 + bs; ++q) s2 = fma(-S[q * m + i], S[j * m + q], s2);
+                    S[j * m + i] = s2;
+                }
+            __syncthreads();
+        }
     }
     for (int t = threadIdx.x; t < m * m; t += blockDim.x) D[(long long)(t / m) * ld + (t % m)] = S[t];
 }
@@ -928,8 +1001,8 @@ static void leaf_trsm_raw(fde_lu* L, const LBlk& D, double* X, int64_t ldx, int6
 static void smem_lu(fde_lu* L, double* D, int64_t m, int64_t ld)
 {
     const size_t sm = (size_t)m * m * sizeof(double);
-    FDE_CUDA(cudaFuncSetAttribute(k_dense_lu_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    k_dense_lu_smem<<<1, 512, sm, L->h->stream>>>(D, (int)m, ld, L->dflag.p);
+    set_smem_once((const void*)k_dense_lu_blk, (int)sm);
+    k_dense_lu_blk<<<1, 512, sm, L->h->stream>>>(D, (int)m, ld, L->dflag.p);
     FDE_CHECK_LAUNCH();
     L->nops++;
 }
@@ -942,13 +1015,13 @@ static void trsm_raw(fde_lu* L, const double* D, int64_t m, int64_t ld, double* 
         cudaStream_t st = L->h->stream;
         const int nr = (int)ceil_div(m, 32);
         if (nr <= 1) {
-            FDE_CUDA(cudaFuncSetAttribute(k_leaf_trsm_smem<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            set_smem_once((const void*)k_leaf_trsm_smem<1>, (int)sm);
             k_leaf_trsm_smem<1><<<g, 1024, sm, st>>>(D, (int)m, ld, X, ldx, (int)ncols, mode);
         } else if (nr <= 2) {
-            FDE_CUDA(cudaFuncSetAttribute(k_leaf_trsm_smem<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            set_smem_once((const void*)k_leaf_trsm_smem<2>, (int)sm);
             k_leaf_trsm_smem<2><<<g, 1024, sm, st>>>(D, (int)m, ld, X, ldx, (int)ncols, mode);
         } else {
-            FDE_CUDA(cudaFuncSetAttribute(k_leaf_trsm_smem<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            set_smem_once((const void*)k_leaf_trsm_smem<4>, (int)sm);
             k_leaf_trsm_smem<4><<<g, 1024, sm, st>>>(D, (int)m, ld, X, ldx, (int)ncols, mode);
         }
         FDE_CHECK_LAUNCH();
@@ -975,7 +1048,7 @@ static void tri_inv(fde_lu* L, const double* D, int64_t m, int64_t ld, int upper
 {
     if (m <= 128) {
         const size_t sm = (size_t)23 * TI_B * TI_B * sizeof(double);
-        FDE_CUDA(cudaFuncSetAttribute(k_tri_inv128, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        set_smem_once((const void*)k_tri_inv128, (int)sm);
         k_tri_inv128<<<1, 1024, sm, L->h->stream>>>(D, (int)m, ld, upper, out, ldo);
         FDE_CHECK_LAUNCH();
         L->nops++;
@@ -1206,7 +1279,7 @@ static void flush_dirty(fde_lu* L)
     FDE_CHECK_LAUNCH();
     const int ne = (kmax + 1) & ~1;
     const size_t smem = (size_t)(2 * kmax * kmax + 3 * ne * ne + 2 * ne + 8) * sizeof(double);
-    FDE_CUDA(cudaFuncSetAttribute(k_bcore, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    set_smem_once((const void*)k_bcore, (int)smem);
     k_bcore<<<(unsigned)E.size(), 256, smem, L->h->stream>>>(dE.p, dC.p, part, L->tol, kc, T, L->dflag.p + 1);
     FDE_CHECK_LAUNCH();
     k_bapply<<<(unsigned)C.size(), 256, 0, L->h->stream>>>(dE.p, dC.p, T, kc);
@@ -1684,7 +1757,8 @@ namespace cg = cooperative_groups;
 #define APPLY_CTAS 8
 #define APPLY_THREADS 512
 #define PROJ_CHUNK 1024
-#define APPLY_TSM 2048
+#define APPLY_TSM 4096
+#define APPLY_RC 8      // right-hand sides per register chunk
 
 struct SLeaf {
     long long r0;
@@ -1765,55 +1839,72 @@ __device__ void run_sweep(const SweepDev& S, int backward, double* x, long long 
         // reduced in shared memory in a fixed order (deterministic).
         __shared__ double tsm[APPLY_TSM];
         const int nlr = L.l_hi - L.l_lo;
-        bool lr_smem = nlr * 64 <= APPLY_TSM;
+        bool lr_smem = nlr * 64 <= APPLY_TSM / APPLY_RC;
         for (int l = L.l_lo; l < L.l_hi && lr_smem; ++l) lr_smem = S.lrr[l].kc <= 64;
-        for (int c = 0; c < nrhs; ++c) {
-            const double* xc = x + (long long)c * ldx;
-            const double* tc = t + (long long)c * tstride;
+        for (int c0 = 0; c0 < nrhs; c0 += APPLY_RC) {
+            const int nc = min(APPLY_RC, nrhs - c0);
             if (nr == 0) continue;
             if (lr_smem) {
-                for (int e = threadIdx.x; e < nlr * 64; e += APPLY_THREADS) {
-                    const int l = L.l_lo + e / 64, q = e % 64;
+                for (int e = threadIdx.x; e < nlr * 64 * nc; e += APPLY_THREADS) {
+                    const int cc = e / (nlr * 64), ee = e % (nlr * 64);
+                    const int l = L.l_lo + ee / 64, q = ee % 64;
                     const SLRRow R = S.lrr[l];
+                    const double* tc = t + (long long)(c0 + cc) * tstride;
                     double tv = 0.0;
                     if (q < R.kc)
                         for (int ch = 0; ch < R.nchunk; ++ch) tv += ldcg(tc + R.tslot + q * R.nchunk + ch);
-                    tsm[e] = tv;
+                    tsm[cc * (APPLY_TSM / APPLY_RC) + ee] = tv;
                 }
                 __syncthreads();
             }
             const int nph = APPLY_THREADS / nr;
             const int i = threadIdx.x % nr, ph = threadIdx.x / nr;
-            double acc = 0.0;
+            double acc[APPLY_RC];
+#pragma unroll
+            for (int cc = 0; cc < APPLY_RC; ++cc) acc[cc] = 0.0;
             if (ph < nph) {
                 const int row = r_lo + i;
                 for (int d = L.d_lo; d < L.d_hi; ++d) {
                     const SDense D = S.dense[d];
-                    for (int j = ph; j < D.nc; j += nph)
-                        acc = fma(D.D[(long long)j * D.ldd + D.roff + row], ldcg(xc + D.c0 + j), acc);
+                    for (int j = ph; j < D.nc; j += nph) {
+                        const double a = D.D[(long long)j * D.ldd + D.roff + row];
+#pragma unroll
+                        for (int cc = 0; cc < APPLY_RC; ++cc)
+                            if (cc < nc) acc[cc] = fma(a, ldcg(x + (long long)(c0 + cc) * ldx + D.c0 + j), acc[cc]);
+                    }
                 }
                 for (int l = L.l_lo + ph; l < L.l_hi; l += nph) {
                     const SLRRow R = S.lrr[l];
                     for (int q = 0; q < R.kc; ++q) {
-                        double tv;
-                        if (lr_smem) {
-                            tv = tsm[(l - L.l_lo) * 64 + q];
-                        } else {
-                            tv = 0.0;
-                            for (int ch = 0; ch < R.nchunk; ++ch) tv += ldcg(tc + R.tslot + q * R.nchunk + ch);
+                        const double u = R.U[(long long)q * R.ldu + R.roff + row];
+#pragma unroll
+                        for (int cc = 0; cc < APPLY_RC; ++cc) {
+                            if (cc >= nc) continue;
+                            double tv;
+                            if (lr_smem) {
+                                tv = tsm[cc * (APPLY_TSM / APPLY_RC) + (l - L.l_lo) * 64 + q];
+                            } else {
+                                tv = 0.0;
+                                const double* tc = t + (long long)(c0 + cc) * tstride;
+                                for (int ch = 0; ch < R.nchunk; ++ch) tv += ldcg(tc + R.tslot + q * R.nchunk + ch);
+                            }
+                            acc[cc] = fma(u, tv, acc[cc]);
                         }
-                        acc = fma(R.U[(long long)q * R.ldu + R.roff + row], tv, acc);
                     }
                 }
             }
-            part[threadIdx.x] = acc;
-            __syncthreads();
-            if (threadIdx.x < nr) {
-                double s2 = 0.0;
-                for (int q = threadIdx.x; q < nph * nr; q += nr) s2 += part[q];
-                z[(long long)c * L.m + r_lo + threadIdx.x] = ldcg(xc + L.r0 + r_lo + threadIdx.x) - s2;
+            for (int cc = 0; cc < nc; ++cc) {
+                part[threadIdx.x] = acc[cc];
+                __syncthreads();
+                if (threadIdx.x < nr) {
+                    double s2 = 0.0;
+                    for (int q = threadIdx.x; q < nph * nr; q += nr) s2 += part[q];
+                    const double* xc = x + (long long)(c0 + cc) * ldx;
+                    z[(long long)(c0 + cc) * L.m + r_lo + threadIdx.x] = ldcg(xc + L.r0 + r_lo + threadIdx.x) - s2;
+                }
+                __syncthreads();
             }
-            __syncthreads();
+            if (lr_smem) __syncthreads();
         }
         // ---- phase A2: projections enabled by the previous leaf (warp per (block, column, chunk))
         if (prev >= 0) {
@@ -1840,23 +1931,36 @@ __device__ void run_sweep(const SweepDev& S, int backward, double* x, long long 
                 }
             }
         }
-        __threadfence();
-        cl.sync();
-        // ---- phase B: x_k = Inv_k z_k (this CTA's row slice)
-        for (int c = 0; c < nrhs; ++c) {
-            if (nr > 0) {
-                cta_rows_dot(L.inv, L.m, 0, L.m, z + (long long)c * L.m, r_lo, nr, part);
-                __syncthreads();
-                if (threadIdx.x < nr) {
-                    double s2 = 0.0;
-                    for (int q = threadIdx.x; q < APPLY_THREADS; q += nr) s2 += part[q];
-                    x[(long long)c * ldx + L.r0 + r_lo + threadIdx.x] = s2;
+        cl.sync();   // grid barrier (orders global memory across the grid)
+        // ---- phase B: x_k = Inv_k z_k (this CTA's row slice), RHS in register chunks
+        if (nr > 0) {
+            const int nph = APPLY_THREADS / nr;
+            const int i = threadIdx.x % nr, ph = threadIdx.x / nr;
+            for (int c0 = 0; c0 < nrhs; c0 += APPLY_RC) {
+                const int nc = min(APPLY_RC, nrhs - c0);
+                double acc[APPLY_RC];
+#pragma unroll
+                for (int cc = 0; cc < APPLY_RC; ++cc) acc[cc] = 0.0;
+                if (ph < nph)
+                    for (int j = ph; j < L.m; j += nph) {
+                        const double a = L.inv[(long long)j * L.m + r_lo + i];
+#pragma unroll
+                        for (int cc = 0; cc < APPLY_RC; ++cc)
+                            if (cc < nc) acc[cc] = fma(a, ldcg(z + (long long)(c0 + cc) * L.m + j), acc[cc]);
+                    }
+                for (int cc = 0; cc < nc; ++cc) {
+                    part[threadIdx.x] = (ph < nph) ? acc[cc] : 0.0;
+                    __syncthreads();
+                    if (threadIdx.x < nr) {
+                        double s2 = 0.0;
+                        for (int q = threadIdx.x; q < nph * nr; q += nr) s2 += part[q];
+                        x[(long long)(c0 + cc) * ldx + L.r0 + r_lo + threadIdx.x] = s2;
+                    }
+                    __syncthreads();
                 }
-                __syncthreads();
             }
         }
-        __threadfence();
-        cl.sync();
+        cl.sync();   // grid barrier (orders global memory across the grid)
         prev = k;
     }
 }
