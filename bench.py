@@ -99,6 +99,53 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(self.samples)}
 
 
+class NvmlSampler:
+    """The same clocks / throttle-reason record through NVML from a thread of this
+    process (no nvidia-smi subprocess polling the driver during the timed region)."""
+
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+               "sw_power_cap": 0x4}
+
+    def __init__(self, index=0, period_s=0.1):
+        self.index, self.period, self.samples, self.ok = index, period_s, [], False
+        self.stop_ev = threading.Event()
+
+    def start(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.dev = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.dev, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.ok = False
+            return
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
+
+    def _run(self):
+        nv = self.nv
+        while not self.stop_ev.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self.dev, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.dev)
+                self.samples.append((sm, rs))
+            except Exception:
+                pass
+            self.stop_ev.wait(self.period)
+
+    def stop(self):
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
+        self.stop_ev.set()
+        self.t.join(timeout=2)
+        reasons = sorted({k for _, rs in self.samples for k, bit in self.REASONS.items() if rs & bit})
+        sm = [s for s, _ in self.samples]
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": float(self.max_mhz),
+                "reasons": reasons, "samples": len(self.samples), "source": "nvml"}
+
+
 # --------------------------------------------------------- CPU baseline
 def cpu_baseline(prob, budget_rows=12):
     """The oracle as it stands, on a bounded sample of the same workload:

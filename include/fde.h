@@ -110,6 +110,14 @@ long long fde_launch_count(void);
 /* Diagnostics: H-LU truncation statistics since load: out4 = {calls, sum of
  * compacted widths, sum of Jacobi sweeps, max width}. */
 int fde_debug_trunc_stats(unsigned long long* out4);
+/* Diagnostics: H-LU algorithm selection for later hlu_factor calls (process
+ * wide).  mode 0 (default): the leaf-ordered batched factorisation whenever the
+ * partition allows it (leaves <= 128 dofs), else the recursive one; mode 1: the
+ * recursive formatted H-LU only; mode 2 + s: leaf-ordered, stopped after s leaf
+ * steps (test helper: fde_hlu_dense_internal then shows the partial state; the
+ * factor is not usable for precond_apply).  Both compute the H-LU of
+ * PAPER.md:598-606; FDE_EINVAL_PARAM for negative modes. */
+int fde_debug_hlu_mode(int mode);
 
 /* Row-block sharding of the dense operator over `world` GPUs (host function,
  * usable without a device): rank owns internal rows [*r0, *r1) = the dofs of
@@ -197,6 +205,8 @@ typedef struct {
     int64_t stored_entries;
     double factor_ms;
     int32_t nops;          /* device operations issued                      */
+    int32_t algorithm;     /* 0 recursive formatted H-LU, 1 leaf-ordered    */
+    double plan_ms;        /* host time of the leaf-ordered schedule (ms)   */
 } fde_hlu_info;
 int fde_hlu_get_info(fde_hlu lu, fde_hlu_info* info);
 

@@ -7,7 +7,7 @@ CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libfde.so")
 SOURCES = ["libfde.cu", "api.cpp", "tables.cpp"]
 DEPS = ["assemble.cu", "matvec.cu", "toeplitz.cu", "krylov.cu", "hmatrix.cu", "hlu.cu",
-        "fde_internal.h", "hmatrix.h", "hlu.h"]
+        "fde_internal.h", "hmatrix.h", "hlu.h", "hlu2.cu"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

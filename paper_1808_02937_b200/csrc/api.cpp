@@ -132,6 +132,18 @@ int fde_debug_trunc_stats(unsigned long long* out4)
     API_END(h)
 }
 
+extern int g_hlu_mode;
+extern int g_hlu2_stop;
+int fde_debug_hlu_mode(int mode)
+{
+    fde_ctx* h = nullptr;
+    API_BEGIN
+    if (mode < 0) fde_fail(FDE_EINVAL_PARAM, "fde_debug_hlu_mode: mode must be 0, 1 or 2 + steps");
+    g_hlu_mode = mode >= 2 ? 0 : mode;
+    g_hlu2_stop = mode >= 2 ? mode - 2 : -1;
+    API_END(h)
+}
+
 long long fde_launch_count(void) { return __atomic_load_n(&g_fde_launches, __ATOMIC_RELAXED); }
 
 // Row-block partition of the dense operator (host logic, no device needed):

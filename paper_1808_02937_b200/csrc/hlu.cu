@@ -219,7 +219,7 @@ __global__ void __launch_bounds__(1024) k_dense_lu_smem(double* D, int m, long l
 // Blocked in-place LU (no pivoting) of an m x m block (m <= 128) in shared memory:
 // panels of 32 -- warp-level LU of the diagonal block, triangular solves of the
 // row / column panels, GEMM update of the trailing matrix.  4 barriers per panel.
-__global__ void __launch_bounds__(512) k_dense_lu_blk(double* D, int m, long long ld, int* bad)
+__device__ void dense_lu_blk_body(double* D, int m, long long ld, int* bad)
 {
     extern __shared__ double S[];   // m x m column-major
     for (int t = threadIdx.x; t < m * m; t += blockDim.x) S[t] = D[(long long)(t / m) * ld + (t % m)];
@@ -275,6 +275,11 @@ __global__ void __launch_bounds__(512) k_dense_lu_blk(double* D, int m, long lon
         }
     }
     for (int t = threadIdx.x; t < m * m; t += blockDim.x) D[(long long)(t / m) * ld + (t % m)] = S[t];
+}
+
+__global__ void __launch_bounds__(512) k_dense_lu_blk(double* D, int m, long long ld, int* bad)
+{
+    dense_lu_blk_body(D, m, ld, bad);
 }
 
 // in-place LU without pivoting of an m x m column-major block (one CTA)
@@ -707,6 +712,7 @@ struct TEntry {
     int c_lo, c_hi;      // chunk range (U chunks then V chunks)
     long long gofs;      // partial Gram slot base (chunks * k * k)
     long long tofs;      // transform slot base (2 * k * kc)
+    int zero_tail;       // in place (Uo == U): also zero the columns [kc, k)
 };
 struct TChunk {
     int e;               // entry
@@ -717,7 +723,8 @@ struct TChunk {
 
 __global__ void __launch_bounds__(256) k_bgram(const TEntry* E, const TChunk* C, double* part)
 {
-    __shared__ double tile[TRUNC_CHUNK * TRUNC_KMAX];
+    // tile[r][j] (row-major, padded: the k dot products of one row are conflict free)
+    __shared__ double tile[TRUNC_CHUNK * (TRUNC_KMAX + 1)];
     const TChunk ch = C[blockIdx.x];
     const TEntry e = E[ch.e];
     const double* M = ch.side ? e.V : e.U;
@@ -725,14 +732,14 @@ __global__ void __launch_bounds__(256) k_bgram(const TEntry* E, const TChunk* C,
     const int k = e.k;
     for (int t = threadIdx.x; t < ch.rows * k; t += blockDim.x) {
         const int r = t % ch.rows, j = t / ch.rows;
-        tile[j * TRUNC_CHUNK + r] = M[(long long)j * ld + ch.r0 + r];
+        tile[r * (TRUNC_KMAX + 1) + j] = M[(long long)j * ld + ch.r0 + r];
     }
     __syncthreads();
     double* out = part + e.gofs + (long long)(blockIdx.x - e.c_lo) * k * k;
     for (int o = threadIdx.x; o < k * k; o += blockDim.x) {
         const int i = o % k, j = o / k;
         double s = 0.0;
-        for (int r = 0; r < ch.rows; ++r) s = fma(tile[i * TRUNC_CHUNK + r], tile[j * TRUNC_CHUNK + r], s);
+        for (int r = 0; r < ch.rows; ++r) s = fma(tile[r * (TRUNC_KMAX + 1) + i], tile[r * (TRUNC_KMAX + 1) + j], s);
         out[o] = s;
     }
 }
@@ -850,24 +857,38 @@ __global__ void __launch_bounds__(256) k_bcore(const TEntry* E, const TChunk* C,
     }
 }
 
+// U_out[r, 0:kc] = U[r, 0:k] T (row chunk); the chunk is staged in shared memory
+// first, so the product may be written in place (Uo == U).  dynamic smem:
+// (k * kc + TRUNC_CHUNK * k) doubles
 __global__ void __launch_bounds__(256) k_bapply(const TEntry* E, const TChunk* C, const double* T, int kc)
 {
-    __shared__ double Ts[TRUNC_KMAX * TRUNC_KMAX];
+    extern __shared__ double bsm[];
     const TChunk ch = C[blockIdx.x];
     const TEntry e = E[ch.e];
     const int k = e.k;
+    double* Ts = bsm;
+    double* Ms = bsm + k * kc;
     const double* Tm = T + e.tofs + (ch.side ? (long long)k * kc : 0);
     for (int t = threadIdx.x; t < k * kc; t += blockDim.x) Ts[t] = Tm[t];
-    __syncthreads();
     const double* M = ch.side ? e.V : e.U;
     double* O = ch.side ? e.Vo : e.Uo;
     const long long ld = ch.side ? e.n : e.m;
+    for (int t = threadIdx.x; t < ch.rows * k; t += blockDim.x) {
+        const int r = t % ch.rows, q = t / ch.rows;
+        Ms[q * TRUNC_CHUNK + r] = M[(long long)q * ld + ch.r0 + r];
+    }
+    __syncthreads();
     for (int t = threadIdx.x; t < ch.rows * kc; t += blockDim.x) {
         const int r = t % ch.rows, c = t / ch.rows;
         double s = 0.0;
-        for (int q = 0; q < k; ++q) s = fma(M[(long long)q * ld + ch.r0 + r], Ts[c * k + q], s);
+        for (int q = 0; q < k; ++q) s = fma(Ms[q * TRUNC_CHUNK + r], Ts[c * k + q], s);
         O[(long long)c * ld + ch.r0 + r] = s;
     }
+    if (e.zero_tail)
+        for (int t = threadIdx.x; t < ch.rows * (k - kc); t += blockDim.x) {
+            const int r = t % ch.rows, c = kc + t / ch.rows;
+            O[(long long)c * ld + ch.r0 + r] = 0.0;
+        }
 }
 
 // ---------------------------------------------------------------- host side
@@ -904,7 +925,14 @@ struct fde_lu {
     std::vector<char> is_dirty;
     int gemm_depth = 0;
     int nflush = 0;
+    // leaf-ordered batched factorisation (hlu2.cu): one arena holds every block
+    double* arena = nullptr;
+    struct H2Plan* plan = nullptr;
+    double plan_ms = 0;   // host time of the leaf-ordered plan (structure, descriptors)
 };
+
+static bool hlu2_factor(fde_lu* L, fde_hm* hm);   // hlu2.cu
+static void hlu2_plan_free(struct H2Plan* p);
 
 struct ApplySched;
 static void apply_sched_free(ApplySched* a);
@@ -1248,6 +1276,7 @@ static void flush_dirty(fde_lu* L)
         e.m = B.m;
         e.n = B.n;
         e.k = B.k;
+        e.zero_tail = 0;
         e.Uo = lu_alloc(L, (size_t)B.m * kc);
         e.Vo = lu_alloc(L, (size_t)B.n * kc);
         e.c_lo = (int)C.size();
@@ -1282,7 +1311,9 @@ static void flush_dirty(fde_lu* L)
     set_smem_once((const void*)k_bcore, (int)smem);
     k_bcore<<<(unsigned)E.size(), 256, smem, L->h->stream>>>(dE.p, dC.p, part, L->tol, kc, T, L->dflag.p + 1);
     FDE_CHECK_LAUNCH();
-    k_bapply<<<(unsigned)C.size(), 256, 0, L->h->stream>>>(dE.p, dC.p, T, kc);
+    const size_t asmem = (size_t)(kmax * kc + TRUNC_CHUNK * kmax) * sizeof(double);
+    set_smem_once((const void*)k_bapply, (int)asmem);
+    k_bapply<<<(unsigned)C.size(), 256, asmem, L->h->stream>>>(dE.p, dC.p, T, kc);
     FDE_CHECK_LAUNCH();
     L->nops += 3;
     L->nflush++;
@@ -1606,6 +1637,8 @@ static void hlu_rec(fde_lu* L, int a)
     hlu_rec(L, A.child[3]);
 }
 
+int g_hlu_mode = 0;   // 0: leaf-ordered batched H-LU when the partition allows it, 1: recursive only
+
 fde_lu* hlu_build(fde_ctx* h, fde_hm* hm, double tol)
 {
     fde_lu* L = new fde_lu();
@@ -1619,8 +1652,9 @@ fde_lu* hlu_build(fde_ctx* h, fde_hm* hm, double tol)
         L->dflag.alloc(4);
         L->dflag.zero(h->stream);
         FDE_CUDA(cudaEventRecord(h->ev0, h->stream));
-        // copy the H-matrix into working blocks
         L->B.resize(L->S.bl.size());
+        if (!(g_hlu_mode == 0 && hlu2_factor(L, hm))) {
+        // recursive formatted H-LU (any partition): copy the H-matrix into working blocks
         for (size_t b = 0; b < L->S.bl.size(); ++b) {
             const HBlock& hb = L->S.bl[b];
             LBlk& lb = L->B[b];
@@ -1647,6 +1681,7 @@ fde_lu* hlu_build(fde_ctx* h, fde_hm* hm, double tol)
             if (L->B[b].type == HB_LR) mark_dirty(L, (int)b);
         flush_dirty(L);
         hlu_rec(L, L->S.root);
+        }
         FDE_CUDA(cudaMemcpyAsync(L->pinned, L->dflag.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, h->stream));
         FDE_CUDA(cudaEventRecord(h->ev1, h->stream));
         FDE_CUDA(cudaEventSynchronize(h->ev1));
@@ -1676,6 +1711,8 @@ void hlu_info(fde_lu* lu, fde_hlu_info* info)
     info->stored_entries = lu->stored;
     info->factor_ms = lu->factor_ms;
     info->nops = lu->nops;
+    info->algorithm = lu->arena ? 1 : 0;
+    info->plan_ms = lu->plan_ms;
 }
 
 fde_op* hlu_operator(fde_lu* lu) { return lu->op; }
@@ -1684,6 +1721,11 @@ void hlu_destroy(fde_lu* L)
 {
     if (!L) return;
     cudaStream_t s = L->h ? L->h->stream : nullptr;
+    if (L->arena) {
+        cudaFreeAsync(L->arena, s);
+        for (auto& b : L->B) b.D = b.U = b.V = b.Li = b.Ui = nullptr;
+    }
+    hlu2_plan_free(L->plan);
     for (auto& b : L->B) {
         if (b.D) cudaFreeAsync(b.D, s);
         if (b.U) cudaFreeAsync(b.U, s);
@@ -2052,15 +2094,15 @@ static ApplySched* apply_sched_build(fde_lu* L)
     int tslot = 0;
     for (size_t b = 0; b < L->B.size(); ++b) {
         const HBlock& hb = S.bl[b];
-        const LBlk& B = L->B[b];
-        if (hb.type == HB_HIER || hb.tau == hb.sig) continue;
+        const LBlk& B = L->B[b];   // B.type: a low-rank block may have become dense (hlu2.cu)
+        if (B.type == HB_HIER || hb.tau == hb.sig) continue;
         const HCluster &T = S.cl[hb.tau], &Sg = S.cl[hb.sig];
         const bool lower = T.r0 > Sg.r0;
         int t0, t1, s0, s1;
         leaf_range(hb.tau, t0, t1);
         leaf_range(hb.sig, s0, s1);
         if (t0 < 0 || s0 < 0 || B.m == 0 || B.n == 0) continue;
-        if (hb.type == HB_DENSE) {
+        if (B.type == HB_DENSE) {
             for (int q = t0; q <= t1; ++q) {
                 SDense d;
                 d.D = B.D;

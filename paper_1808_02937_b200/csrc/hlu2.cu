@@ -1,0 +1,1053 @@
+// hlu_factor, leaf-ordered: the formatted H-LU of A~ (Fig.
+// fig:HLU; arithmetic of Boerm et al. §5.2.3 cited at PAPER.md:606, reading A12)
+// executed as a right-looking sweep over the leaf clusters, on the block
+// partition of the H-matrix (blocks keep their H format: one dense array or one
+// low-rank pair U V^T per block of the partition).
+//
+// For leaf k = 0 .. nl-1 (tiles (i, j) are leaf-cluster pairs, the block that
+// owns a tile is its block of the partition):
+//   1. LU of the diagonal tile (k, k) (dense leaf; no pivoting, Theorem 2.1)
+//   2. panels:  A(k, j>k) <- L_kk^{-1} A(k, j)  (dense rows; U factor of a
+//               low-rank block),  A(i>k, k) <- A(i, k) U_kk^{-1}  (dense columns;
+//               V factor: V <- U_kk^{-T} V)
+//   3. Schur complement A(i, j) -= A(i, k) A(k, j) for i, j > k: dense targets
+//      are updated with GEMMs, low-rank targets receive the product as new
+//      columns (low-rank times anything is low rank), grouped per operand
+//   4. truncation of the low-rank sums to sigma_i > tol sigma_1 (formatted
+//      addition), batched, when a block is about to be used as an operand or
+//      its pending width would exceed TRUNC_KMAX.
+// This is the same arithmetic as the recursive algorithm of hlu.cu (the LU of A~
+// is unique: at tol = 0 both give the exact factors up to rounding); the order of
+// the truncations differs.  Every step is a handful of batched launches whose
+// descriptors are built once on the host (no host synchronisation inside).
+//
+// A low-rank block becomes dense (D = U V^T, exact) when a dense x dense product
+// lands in it or when its width would exceed what a truncated block can hold
+// (TRUNC_KMAX; in exact mode, tol = 0, half its smaller dimension).
+// Requirements (else hlu_build uses the recursive algorithm): leaves of at most
+// H2_MMAX dofs and dense diagonal leaf tiles.
+
+#include <chrono>
+#include <cstdlib>
+#include <set>
+
+#define H2_MMAX 128
+#define H2_STRIP 32
+
+struct H2Lu {
+    double* D;
+    long long ld;
+    int m;
+};
+// lower-triangular solve on a strip of vectors:
+//   mode 0: X (m x nvec, columns) <- L^{-1} X   (unit lower L of the packed LU T)
+//   mode 1: X (m x nvec, columns) <- U^{-T} X   (U of the packed LU T)
+//   mode 2: X (nvec x m, rows)    <- X U^{-1}
+struct H2Panel {
+    const double* T;
+    long long ldt;
+    double* X;
+    long long ldx;
+    int m, nvec, mode;
+};
+struct H2Term {
+    const double* A;
+    const double* B;
+    long long lda, ldb;
+    int k, ta, tb;
+    double alpha;
+};
+struct H2Task {
+    double* C;
+    long long ldc;
+    int m, n;
+    double beta;
+    int t_lo, t_hi;
+};
+struct H2Tile {
+    int task, m0, n0;
+};
+struct H2Copy {   // kind 0: dst = alpha src, 1: dst = 0, 2: dst = I
+    const double* src;
+    long long lds;
+    double* dst;
+    long long ldd;
+    int m, n, kind;
+    double alpha;
+};
+
+// ----------------------------------------------------------------- kernels
+// LU without pivoting of an m x m tile (m <= 128) held in registers: thread t owns
+// row i = t % 128 and the columns j = g + 4q (g = t / 128, q = 0..31); per pivot,
+// row k and the multipliers of column k are broadcast through shared memory.
+__global__ void __launch_bounds__(512) k_h2_lu(const H2Lu* tk, int* bad)
+{
+    const H2Lu d = tk[blockIdx.x];
+    __shared__ double sRow[H2_MMAX], sCol[H2_MMAX];
+    const int m = d.m, i = threadIdx.x & 127, g = threadIdx.x >> 7;
+    double a[32];
+#pragma unroll
+    for (int q = 0; q < 32; ++q) {
+        const int j = g + 4 * q;
+        a[q] = (i < m && j < m) ? d.D[(long long)j * d.ld + i] : 0.0;
+    }
+    for (int k = 0; k < m; ++k) {
+        if (i == k) {
+#pragma unroll
+            for (int q = 0; q < 32; ++q)
+                if (g + 4 * q >= k) sRow[g + 4 * q] = a[q];
+        }
+        __syncthreads();
+        const double piv = sRow[k];
+        if (threadIdx.x == 0 && (!(fabs(piv) > 0.0) || !isfinite(piv))) *bad = 1;
+        if (g == (k & 3) && i > k && i < m) {
+            const double ip = 1.0 / piv;
+#pragma unroll
+            for (int q = 0; q < 32; ++q)
+                if (g + 4 * q == k) {
+                    a[q] *= ip;
+                    sCol[i] = a[q];
+                }
+        }
+        __syncthreads();
+        if (i > k && i < m) {
+            const double l = sCol[i];
+#pragma unroll
+            for (int q = 0; q < 32; ++q)
+                if (g + 4 * q > k) a[q] = fma(-l, sRow[g + 4 * q], a[q]);
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < 32; ++q) {
+        const int j = g + 4 * q;
+        if (i < m && j < m) d.D[(long long)j * d.ld + i] = a[q];
+    }
+}
+
+// one CTA per strip of <= 32 vectors; T' (lower, m x m) and the strip in smem
+__global__ void __launch_bounds__(256) k_h2_panel(const H2Panel* P)
+{
+    extern __shared__ double psm[];
+    const H2Panel p = P[blockIdx.x];
+    const int m = p.m, ldT = m + 1, ldB = m + 1;
+    double* Ts = psm;                 // T'[i][j] at Ts[j * ldT + i], i >= j
+    double* Bs = psm + m * ldT;       // vector c, element i at Bs[c * ldB + i]
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const bool unit = (p.mode == 0);
+    const int nv = p.nvec;
+    // loads: 8 independent global loads in flight per thread
+    if (p.mode == 0) {
+        for (int t0 = tid; t0 < m * m; t0 += 256 * 8) {
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int t = t0 + 256 * u, i = t % m, j = t / m;      // L[i][j] = T[i + j ldt]
+                v[u] = (t < m * m && i > j) ? p.T[(long long)j * p.ldt + i] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int t = t0 + 256 * u, i = t % m, j = t / m;
+                if (t < m * m && i > j) Ts[j * ldT + i] = v[u];
+            }
+        }
+    } else {
+        for (int t0 = tid; t0 < m * m; t0 += 256 * 8) {
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int t = t0 + 256 * u, j = t % m, i = t / m;      // T'[i][j] = U[j][i] = T[j + i ldt]
+                v[u] = (t < m * m && i >= j) ? p.T[(long long)i * p.ldt + j] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int t = t0 + 256 * u, j = t % m, i = t / m;
+                if (t < m * m && i >= j) Ts[j * ldT + i] = v[u];
+            }
+        }
+    }
+    for (int t0 = tid; t0 < nv * m; t0 += 256 * 8) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int t = t0 + 256 * u;
+            if (p.mode == 2) {   // rows of X are the vectors
+                const int c = t % nv, i = t / nv;
+                v[u] = (t < nv * m) ? p.X[(long long)i * p.ldx + c] : 0.0;
+            } else {
+                const int i = t % m, c = t / m;
+                v[u] = (t < nv * m) ? p.X[(long long)c * p.ldx + i] : 0.0;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int t = t0 + 256 * u;
+            if (t >= nv * m) continue;
+            if (p.mode == 2) Bs[(t % nv) * ldB + t / nv] = v[u];
+            else Bs[(t / m) * ldB + t % m] = v[u];
+        }
+    }
+    __syncthreads();
+    const int nb = (m + 31) / 32;
+    for (int bi = 0; bi < nb; ++bi) {
+        const int b0 = bi * 32, bs = min(32, m - b0);
+        // diagonal block: warp w solves vectors w + 8u (u = 0..3) together (lane = row)
+        {
+            double v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int c = w + 8 * u;
+                v[u] = (c < nv && lane < bs) ? Bs[c * ldB + b0 + lane] : 0.0;
+            }
+            for (int q = 0; q < bs; ++q) {
+                const double tq = (lane > q && lane < bs) ? Ts[(b0 + q) * ldT + b0 + lane] : 0.0;
+                const double dq = unit ? 1.0 : Ts[(b0 + q) * ldT + b0 + q];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const double y = __shfl_sync(0xffffffffu, v[u], q) / dq;
+                    if (lane == q) v[u] = y;
+                    else v[u] = fma(-tq, y, v[u]);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int c = w + 8 * u;
+                if (c < nv && lane < bs) Bs[c * ldB + b0 + lane] = v[u];
+            }
+        }
+        __syncthreads();
+        // trailing rows: B[i][c] -= sum_q T'[i][b0+q] Y[q][c]
+        const int r0 = b0 + bs;
+        if (r0 < m) {
+            for (int t = tid; t < (m - r0) * nv; t += blockDim.x) {
+                const int i = r0 + t % (m - r0), c = t / (m - r0);
+                double s = Bs[c * ldB + i];
+#pragma unroll 8
+                for (int q = 0; q < bs; ++q) s = fma(-Ts[(b0 + q) * ldT + i], Bs[c * ldB + b0 + q], s);
+                Bs[c * ldB + i] = s;
+            }
+        }
+        __syncthreads();
+    }
+    if (p.mode == 2) {
+        for (int t = tid; t < nv * m; t += blockDim.x) {
+            const int c = t % nv, i = t / nv;
+            p.X[(long long)i * p.ldx + c] = Bs[c * ldB + i];
+        }
+    } else {
+        for (int t = tid; t < nv * m; t += blockDim.x) {
+            const int i = t % m, c = t / m;
+            p.X[(long long)c * p.ldx + i] = Bs[c * ldB + i];
+        }
+    }
+}
+
+// grouped multi-term GEMM: every CTA owns a 64 x 64 tile of one task,
+// C_tile = beta C_tile + sum_terms alpha op(A) op(B); terms in a fixed order.
+// The next 16-deep slice of A and B is loaded into registers while the current
+// one is multiplied from shared memory (one barrier pair per slice).
+__device__ __forceinline__ void h2_load_slice(const H2Term& T, int m0, int n0, int m, int n, int k0, double* ra,
+                                              double* rb)
+{
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const int t = threadIdx.x + 256 * u;
+        int kk, mm;
+        if (T.ta) { mm = t / GK; kk = t % GK; } else { kk = t / GT; mm = t % GT; }
+        const int gi = m0 + mm, gk = k0 + kk;
+        double va = 0.0;
+        if (gi < m && gk < T.k) va = T.ta ? T.A[(long long)gi * T.lda + gk] : T.A[(long long)gk * T.lda + gi];
+        ra[u] = va;
+        int nn;
+        if (T.tb) { kk = t / GT; nn = t % GT; } else { nn = t / GK; kk = t % GK; }
+        const int gj = n0 + nn, gk2 = k0 + kk;
+        double vb = 0.0;
+        if (gj < n && gk2 < T.k) vb = T.tb ? T.B[(long long)gk2 * T.ldb + gj] : T.B[(long long)gj * T.ldb + gk2];
+        rb[u] = vb;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_h2_gemm(const H2Tile* tiles, const H2Task* tasks, const H2Term* terms)
+{
+    __shared__ double sA[GK][GT + 1];
+    __shared__ double sB[GK][GT + 1];
+    const H2Tile tl = tiles[blockIdx.x];
+    const H2Task tk = tasks[tl.task];
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    const int m0 = tl.m0, n0 = tl.n0, m = tk.m, n = tk.n;
+    double acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+    // flatten (term, slice) into one pipelined sequence
+    int q = tk.t_lo, k0 = 0;
+    while (q < tk.t_hi && terms[q].k <= 0) ++q;
+    double ra[4], rb[4];
+    if (q < tk.t_hi) h2_load_slice(terms[q], m0, n0, m, n, 0, ra, rb);
+    while (q < tk.t_hi) {
+        const H2Term T = terms[q];
+        // stage the slice
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int t = threadIdx.x + 256 * u;
+            int kk, mm;
+            if (T.ta) { mm = t / GK; kk = t % GK; } else { kk = t / GT; mm = t % GT; }
+            sA[kk][mm] = T.alpha * ra[u];
+            int nn;
+            if (T.tb) { kk = t / GT; nn = t % GT; } else { nn = t / GK; kk = t % GK; }
+            sB[kk][nn] = rb[u];
+        }
+        __syncthreads();
+        // advance and prefetch the next slice
+        int q2 = q, k2 = k0 + GK;
+        if (k2 >= T.k) {
+            k2 = 0;
+            ++q2;
+            while (q2 < tk.t_hi && terms[q2].k <= 0) ++q2;
+        }
+        if (q2 < tk.t_hi) h2_load_slice(terms[q2], m0, n0, m, n, k2, ra, rb);
+#pragma unroll
+        for (int kk = 0; kk < GK; ++kk) {
+            double a[4], b[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) a[i] = sA[kk][tx + 16 * i];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) b[j] = sB[kk][ty + 16 * j];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+        }
+        __syncthreads();
+        q = q2;
+        k0 = k2;
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int gi = m0 + tx + 16 * i, gj = n0 + ty + 16 * j;
+            if (gi < m && gj < n) {
+                double* c = tk.C + (long long)gj * tk.ldc + gi;
+                *c = acc[i][j] + (tk.beta == 0.0 ? 0.0 : tk.beta * *c);
+            }
+        }
+}
+
+__global__ void __launch_bounds__(256) k_h2_copy(const H2Copy* C)
+{
+    const H2Copy c = C[blockIdx.x];
+    const long long tot = (long long)c.m * c.n;
+    for (long long t = threadIdx.x; t < tot; t += blockDim.x) {
+        const int i = (int)(t % c.m), j = (int)(t / c.m);
+        double v;
+        if (c.kind == 0) v = c.alpha * c.src[(long long)j * c.lds + i];
+        else if (c.kind == 1) v = 0.0;
+        else v = (i == j) ? 1.0 : 0.0;
+        c.dst[(long long)j * c.ldd + i] = v;
+    }
+}
+
+// ------------------------------------------------------------------ plan
+// Pointers are resolved after the arena layout is known: a reference is
+// (space, id, offset): space 0 = dense block id, 1 = U of block id, 2 = V of
+// block id, 3 = step scratch, 4 = leaf inverse id (L^{-1}), 5 = (U^{-1}).
+struct VRef {
+    int sp, id;
+    int64_t off;
+};
+struct VTerm {
+    VRef A, B;
+    int64_t lda, ldb;
+    int k, ta, tb;
+    double alpha;
+};
+struct VTask {
+    VRef C;
+    int64_t ldc;
+    int m, n;
+    double beta;
+    std::vector<VTerm> terms;
+};
+struct VCopy {
+    VRef src, dst;
+    int64_t lds, ldd;
+    int m, n, kind;
+    double alpha;
+};
+struct VPanel {
+    int diag;   // block id of the diagonal tile
+    VRef X;
+    int64_t ldx;
+    int m, nvec, mode;
+};
+struct VTrunc {
+    int blk, k;
+};
+struct VStep {
+    std::vector<VTrunc> trunc;
+    int lu_blk = -1;
+    std::vector<VPanel> panel;
+    std::vector<VTask> g0, g1, g2, g3;   // conversions to dense, cores, products, dense updates
+    std::vector<VCopy> cp;           // low-rank target columns
+    int64_t scratch = 0;
+};
+
+struct H2Launch {      // ranges in the flat device arrays
+    int tr_e0 = 0, tr_ne = 0, tr_c0 = 0, tr_nc = 0, tr_kmax = 0;
+    int lu = -1;
+    int pan0 = 0, npan = 0;
+    int g_tile0[4] = {0, 0, 0, 0}, g_ntile[4] = {0, 0, 0, 0};
+    int cp0 = 0, ncp = 0;
+};
+
+struct H2Plan {
+    int nl = 0;
+    std::vector<H2Launch> steps;
+    H2Launch init, fin;   // initial copies + compression; final inverses
+    DBuf<H2Lu> lu;
+    DBuf<H2Panel> pan;
+    DBuf<H2Term> terms;
+    DBuf<H2Task> tasks;
+    DBuf<H2Tile> tiles;
+    DBuf<H2Copy> cps;
+    DBuf<TEntry> te;
+    DBuf<TChunk> tc;
+    double* tr_part = nullptr;
+    double* tr_T = nullptr;
+    int launches = 0;
+};
+
+static void hlu2_plan_free(H2Plan* p) { delete p; }
+int g_hlu2_stop = -1;   // debug: run only the first g_hlu2_stop leaf steps
+
+static bool hlu2_factor(fde_lu* L, fde_hm* hm)
+{
+    const auto t_plan0 = std::chrono::steady_clock::now();
+    const HStruct& S = L->S;
+    const bool trunc = L->tol > 0.0;
+    const int R = hm->R, rmax = L->rmax;
+    if (trunc && (R > TRUNC_KMAX || rmax > TRUNC_KMAX)) return false;
+    // ---- leaves in dof order
+    std::vector<int> leafcl;
+    for (size_t c = 0; c < S.cl.size(); ++c)
+        if (S.cl[c].child[0] < 0 && S.cl[c].r1 > S.cl[c].r0) leafcl.push_back((int)c);
+    std::sort(leafcl.begin(), leafcl.end(), [&](int a, int b) { return S.cl[a].r0 < S.cl[b].r0; });
+    const int nl = (int)leafcl.size();
+    if (nl == 0) return false;
+    std::vector<int64_t> lr0(nl + 1);
+    for (int q = 0; q < nl; ++q) {
+        lr0[q] = S.cl[leafcl[q]].r0;
+        if (S.cl[leafcl[q]].r1 - lr0[q] > H2_MMAX) return false;
+    }
+    lr0[nl] = S.n;
+    for (int q = 0; q < nl; ++q)
+        if (S.cl[leafcl[q]].r1 != lr0[q + 1]) return false;
+    auto lm = [&](int q) { return (int)(lr0[q + 1] - lr0[q]); };
+    // leaf range of a cluster (clusters are unions of consecutive leaves)
+    auto lrange = [&](int cl, int& a, int& b) {
+        a = (int)(std::lower_bound(lr0.begin(), lr0.end() - 1, S.cl[cl].r0) - lr0.begin());
+        b = (int)(std::lower_bound(lr0.begin(), lr0.end() - 1, S.cl[cl].r1) - lr0.begin()) - 1;
+        if (S.cl[cl].r1 == S.n) b = nl - 1;
+    };
+    const int nb = (int)S.bl.size();
+    std::vector<int> t0(nb, -1), t1(nb, -1), s0(nb, -1), s1(nb, -1);
+    std::vector<int> owner((size_t)nl * nl, -1);
+    for (int b = 0; b < nb; ++b) {
+        const HBlock& hb = S.bl[b];
+        if (hb.type == HB_HIER || hb.m == 0 || hb.n == 0) continue;
+        lrange(hb.tau, t0[b], t1[b]);
+        lrange(hb.sig, s0[b], s1[b]);
+        for (int i = t0[b]; i <= t1[b]; ++i)
+            for (int j = s0[b]; j <= s1[b]; ++j) {
+                if (owner[(size_t)i * nl + j] >= 0) return false;
+                owner[(size_t)i * nl + j] = b;
+            }
+    }
+    for (int q = 0; q < nl; ++q) {
+        const int d = owner[(size_t)q * nl + q];
+        if (d < 0 || S.bl[d].type != HB_DENSE || t0[d] != q || t1[d] != q || s0[d] != q || s1[d] != q) return false;
+    }
+    for (size_t t = 0; t < owner.size(); ++t)
+        if (owner[t] < 0) return false;
+    auto own = [&](int i, int j) { return owner[(size_t)i * nl + j]; };
+    std::vector<char> dyn(nb, 0);   // low-rank blocks converted to dense during the sweep
+    std::vector<int> conv_step(nb, 1 << 30);
+    auto isLR = [&](int b) { return S.bl[b].type == HB_LR && !dyn[b]; };
+    auto row0 = [&](int b) { return S.cl[S.bl[b].tau].r0; };
+    auto col0 = [&](int b) { return S.cl[S.bl[b].sig].r0; };
+
+    // ---- simulation: column counts of the low-rank blocks, per-step op lists
+    std::vector<int> kc(nb, 0), kcap(nb, 0);
+    for (int b = 0; b < nb; ++b)
+        if (S.bl[b].type == HB_LR) kc[b] = kcap[b] = R;
+    std::vector<char> pend(nb, 0);
+    std::vector<VTrunc> init_trunc;
+    if (trunc) {
+        for (int b = 0; b < nb; ++b)
+            if (S.bl[b].type == HB_LR && t0[b] >= 0) {
+                init_trunc.push_back({b, kc[b]});
+                kc[b] = rmax;
+                kcap[b] = std::max(kcap[b], rmax);
+            }
+    }
+    std::vector<VStep> steps(nl);
+    std::vector<int> stamp(nb, 0), tile_stamp((size_t)nl * nl, 0), tile_task((size_t)nl * nl, 0);
+    int stamp_id = 0, tile_stamp_id = 0;
+    for (int k = 0; k < nl; ++k) {
+        VStep& st = steps[k];
+        const int mk = lm(k);
+        const int dk = own(k, k);
+        std::vector<int> Cb, Rc;   // column-panel blocks (rows > k), row-panel blocks (cols > k)
+        for (int i = k + 1; i < nl; ++i) {
+            const int b = own(i, k);
+            if (Cb.empty() || Cb.back() != b) Cb.push_back(b);
+        }
+        for (int j = k + 1; j < nl; ++j) {
+            const int c = own(k, j);
+            if (Rc.empty() || Rc.back() != c) Rc.push_back(c);
+        }
+        for (int b : Cb)
+            if (t0[b] <= k) return false;
+        for (int c : Rc)
+            if (s0[c] <= k) return false;
+        // truncation of panel operands with pending columns
+        std::vector<char> in_tr(nb, 0);
+        auto add_trunc = [&](int b) {
+            if (!trunc || !pend[b] || in_tr[b]) return;
+            in_tr[b] = 1;
+            st.trunc.push_back({b, kc[b]});
+            kc[b] = rmax;
+            pend[b] = 0;
+        };
+        for (int b : Cb)
+            if (isLR(b)) add_trunc(b);
+        for (int c : Rc)
+            if (isLR(c)) add_trunc(c);
+        // panels (after truncation: widths are the current kc of the operands; types
+        // before this step's conversions, which run after the products)
+        st.lu_blk = dk;
+        for (int b : Cb) {
+            const HBlock& B = S.bl[b];
+            if (isLR(b))
+                st.panel.push_back({dk, {2, b, lr0[k] - col0(b)}, B.n, mk, kc[b], 1});
+            else
+                st.panel.push_back({dk, {0, b, (lr0[k] - col0(b)) * B.m}, B.m, mk, (int)B.m, 2});
+        }
+        for (int c : Rc) {
+            const HBlock& C = S.bl[c];
+            if (isLR(c))
+                st.panel.push_back({dk, {1, c, lr0[k] - row0(c)}, C.m, mk, kc[c], 0});
+            else
+                st.panel.push_back({dk, {0, c, lr0[k] - row0(c)}, C.m, mk, (int)C.n, 0});
+        }
+        // products: pair scratch offsets
+        struct Pair { int b, c; int64_t w; int rw; bool bl, cl; };   // bl/cl: operand types at this step   // w: W (n_c x kc_b) or Z (m_b x kc_c) scratch offset
+        std::vector<Pair> pairs;
+        int64_t scr = 0;
+        for (int b : Cb)
+            for (int c : Rc) {
+                Pair pr{b, c, -1, 0, isLR(b), isLR(c)};
+                const HBlock &B = S.bl[b], &C = S.bl[c];
+                if (isLR(b)) {
+                    int64_t core = -1;
+                    if (isLR(c)) {   // core = U_c[k]^T V_b[k]  (kc_c x kc_b)
+                        core = scr;
+                        scr += (int64_t)kc[c] * kc[b];
+                        VTask t{{3, 0, core}, kc[c], kc[c], kc[b], 0.0, {}};
+                        t.terms.push_back({{1, c, lr0[k] - row0(c)}, {2, b, lr0[k] - col0(b)}, C.m, B.n, mk, 1, 0, 1.0});
+                        st.g1.push_back(t);
+                    }
+                    pr.w = scr;
+                    pr.rw = kc[b];
+                    scr += C.n * kc[b];
+                    VTask t{{3, 0, pr.w}, C.n, (int)C.n, kc[b], 0.0, {}};
+                    if (isLR(c))   // W = V_c core
+                        t.terms.push_back({{2, c, 0}, {3, 0, core}, C.n, kc[c], kc[c], 0, 0, 1.0});
+                    else           // W = D_c[k rows, :]^T V_b[k]
+                        t.terms.push_back({{0, c, lr0[k] - row0(c)}, {2, b, lr0[k] - col0(b)}, C.m, B.n, mk, 1, 0, 1.0});
+                    st.g2.push_back(t);
+                } else if (isLR(c)) {   // Z = D_b[:, k cols] U_c[k]   (m_b x kc_c)
+                    pr.w = scr;
+                    pr.rw = kc[c];
+                    scr += B.m * kc[c];
+                    VTask t{{3, 0, pr.w}, B.m, (int)B.m, kc[c], 0.0, {}};
+                    t.terms.push_back({{0, b, (lr0[k] - col0(b)) * B.m}, {1, c, lr0[k] - row0(c)}, B.m, C.m, mk, 0, 0, 1.0});
+                    st.g2.push_back(t);
+                }
+                pairs.push_back(pr);
+            }
+        // targets
+        ++tile_stamp_id;   // dense target tile (i, j) -> g3 task (stamped flat table)
+        struct Grp { int t, key, rank; int64_t slot; };
+        std::map<std::pair<int, int>, int> lgrp;     // (target, key) -> group index
+        std::vector<Grp> grps;
+        std::vector<int> incoming(nb, 0);
+        std::vector<std::pair<int, int>> lterms;     // (pair index, group index)
+        // targets of every pair
+        std::vector<std::vector<int>> ptg(pairs.size());
+        for (size_t pi = 0; pi < pairs.size(); ++pi) {
+            const int b = pairs[pi].b, c = pairs[pi].c;
+            ++stamp_id;
+            for (int i = t0[b]; i <= t1[b];) {
+                int inext = t1[b] + 1;
+                for (int j = s0[c]; j <= s1[c];) {   // jump over the column run of each owner
+                    const int t = own(i, j);
+                    if (stamp[t] != stamp_id) {
+                        stamp[t] = stamp_id;
+                        ptg[pi].push_back(t);
+                    }
+                    inext = std::min(inext, t1[t] + 1);
+                    j = s1[t] + 1;
+                }
+                i = std::max(i + 1, inext);   // rows of the same owners repeat the same targets
+            }
+        }
+        // low-rank targets that must become dense: a dense x dense product lands
+        // in them, or their width would exceed what a low-rank block can hold
+        // (TRUNC_KMAX after truncation; min(m, n) / 2 in exact mode)
+        {
+            std::set<std::pair<int, int>> gseen;
+            std::vector<char> conv(nb, 0);
+            for (size_t pi = 0; pi < pairs.size(); ++pi) {
+                const int b = pairs[pi].b, c = pairs[pi].c;
+                const bool bl = pairs[pi].bl, cl = pairs[pi].cl;
+                for (int t : ptg[pi]) {
+                    if (!isLR(t)) continue;
+                    if (!bl && !cl) { conv[t] = 1; continue; }
+                    const int key = bl ? b : (nb + c);
+                    if (gseen.insert(std::make_pair(t, key)).second) incoming[t] += bl ? kc[b] : kc[c];
+                }
+            }
+            for (int t = 0; t < nb; ++t) {
+                if (!isLR(t) || (!incoming[t] && !conv[t])) continue;
+                const HBlock& T = S.bl[t];
+                const int lim = trunc ? TRUNC_KMAX : (int)std::max<int64_t>(1, std::min(T.m, T.n) / 2);
+                if (!conv[t] && kc[t] + incoming[t] > lim) {
+                    if (trunc && rmax + incoming[t] <= lim) add_trunc(t);
+                    else conv[t] = 1;
+                }
+                if (conv[t]) {   // D_t = U_t V_t^T, then a dense block for good
+                    VTask tk{{0, t, 0}, T.m, (int)T.m, (int)T.n, 0.0, {}};
+                    tk.terms.push_back({{1, t, 0}, {2, t, 0}, T.m, T.n, kc[t], 0, 1, 1.0});
+                    st.g0.push_back(tk);
+                    dyn[t] = 1;
+                    conv_step[t] = k;
+                    pend[t] = 0;
+                    incoming[t] = 0;
+                }
+            }
+        }
+        for (size_t pi = 0; pi < pairs.size(); ++pi) {
+            const Pair& pr = pairs[pi];
+            const int b = pr.b, c = pr.c;
+            for (int t : ptg[pi]) {
+                const HBlock& T = S.bl[t];
+                if (!isLR(t)) {
+                    for (int i = std::max(t0[b], t0[t]); i <= std::min(t1[b], t1[t]); ++i)
+                        for (int j = std::max(s0[c], s0[t]); j <= std::min(s1[c], s1[t]); ++j) {
+                            const size_t key = (size_t)i * nl + j;
+                            int ti;
+                            if (tile_stamp[key] != tile_stamp_id) {
+                                ti = (int)st.g3.size();
+                                tile_stamp[key] = tile_stamp_id;
+                                tile_task[key] = ti;
+                                VTask tk{{0, t, (lr0[j] - col0(t)) * T.m + (lr0[i] - row0(t))}, T.m, lm(i), lm(j), 1.0, {}};
+                                st.g3.push_back(tk);
+                            } else {
+                                ti = tile_task[key];
+                            }
+                            const HBlock &B = S.bl[b], &C = S.bl[c];
+                            VTerm term;
+                            if (!pr.bl && !pr.cl) {
+                                term = {{0, b, (lr0[k] - col0(b)) * B.m + (lr0[i] - row0(b))},
+                                        {0, c, (lr0[j] - col0(c)) * C.m + (lr0[k] - row0(c))}, B.m, C.m, mk, 0, 0, -1.0};
+                            } else if (pr.bl) {   // U_b[i rows] W[j rows]^T
+                                term = {{1, b, lr0[i] - row0(b)}, {3, 0, pr.w + (lr0[j] - col0(c))}, B.m, C.n,
+                                        kc[b], 0, 1, -1.0};
+                            } else {               // Z[i rows] V_c[j rows]^T
+                                term = {{3, 0, pr.w + (lr0[i] - row0(b))}, {2, c, lr0[j] - col0(c)}, B.m, C.n,
+                                        kc[c], 0, 1, -1.0};
+                            }
+                            st.g3[ti].terms.push_back(term);
+                        }
+                } else {
+                    const int key = pr.bl ? b : (nb + c);
+                    auto gk = std::make_pair(t, key);
+                    auto it = lgrp.find(gk);
+                    int gi;
+                    if (it == lgrp.end()) {
+                        gi = (int)grps.size();
+                        lgrp[gk] = gi;
+                        grps.push_back({t, key, pr.bl ? kc[b] : kc[c], -1});
+                    } else {
+                        gi = it->second;
+                    }
+                    lterms.push_back({(int)pi, gi});
+                }
+            }
+        }
+        // slots and copies
+        std::vector<char> u_done(grps.size(), 0);
+        for (size_t g = 0; g < grps.size(); ++g) {
+            const int t = grps[g].t;
+            grps[g].slot = kc[t];
+            kc[t] += grps[g].rank;
+            kcap[t] = std::max(kcap[t], kc[t]);
+            pend[t] = 1;
+        }
+        for (auto& lt : lterms) {
+            const Pair& pr = pairs[lt.first];
+            Grp& g = grps[lt.second];
+            const int t = g.t, b = pr.b, c = pr.c;
+            const HBlock &T = S.bl[t], &B = S.bl[b], &C = S.bl[c];
+            const int ia = std::max(t0[b], t0[t]), ib = std::min(t1[b], t1[t]);
+            const int ja = std::max(s0[c], s0[t]), jb = std::min(s1[c], s1[t]);
+            const int64_t R0 = lr0[ia], R1 = lr0[ib + 1], C0 = lr0[ja], C1 = lr0[jb + 1];
+            const int64_t us = g.slot * T.m + (R0 - row0(t)), vs = g.slot * T.n + (C0 - col0(t));
+            if (pr.bl) {
+                if (!u_done[lt.second]) {   // U slot rows R = U_b rows (once per group)
+                    u_done[lt.second] = 1;
+                    st.cp.push_back({{1, b, R0 - row0(b)}, {1, t, us}, B.m, T.m, (int)(R1 - R0), g.rank, 0, 1.0});
+                }
+                st.cp.push_back({{3, 0, pr.w + (C0 - col0(c))}, {2, t, vs}, C.n, T.n, (int)(C1 - C0), g.rank, 0, -1.0});
+            } else {
+                if (!u_done[lt.second]) {   // V slot rows C = -V_c rows (once per group)
+                    u_done[lt.second] = 1;
+                    st.cp.push_back({{2, c, C0 - col0(c)}, {2, t, vs}, C.n, T.n, (int)(C1 - C0), g.rank, 0, -1.0});
+                }
+                st.cp.push_back({{3, 0, pr.w + (R0 - row0(b))}, {1, t, us}, B.m, T.m, (int)(R1 - R0), g.rank, 0, 1.0});
+            }
+        }
+        st.scratch = scr;
+    }
+    if (trunc)
+        for (int b = 0; b < nb; ++b)
+            if (pend[b]) return false;   // every update precedes a use (see header)
+
+    auto ms_since = [&](std::chrono::steady_clock::time_point t) {
+        return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t).count();
+    };
+    const double ms_sim = ms_since(t_plan0);
+    const auto t_alloc0 = std::chrono::steady_clock::now();
+    // ---- arena layout
+    std::vector<int64_t> offD(nb, -1), offU(nb, -1), offV(nb, -1);
+    int64_t words = 0;
+    for (int b = 0; b < nb; ++b) {
+        const HBlock& hb = S.bl[b];
+        if (hb.type == HB_DENSE || dyn[b]) { offD[b] = words; words += hb.m * hb.n; }
+    }
+    const int64_t lr_lo = words;
+    for (int b = 0; b < nb; ++b) {
+        const HBlock& hb = S.bl[b];
+        if (hb.type == HB_LR) {
+            offU[b] = words; words += hb.m * kcap[b];
+            offV[b] = words; words += hb.n * kcap[b];
+        }
+    }
+    const int64_t lr_hi = words;
+    std::vector<int64_t> offLi(nl), offUi(nl);
+    for (int q = 0; q < nl; ++q) {
+        offLi[q] = words; words += (int64_t)lm(q) * lm(q);
+        offUi[q] = words; words += (int64_t)lm(q) * lm(q);
+    }
+    int64_t scr_max = 1;
+    for (auto& st : steps) scr_max = std::max(scr_max, st.scratch);
+    const int64_t off_scr = words;
+    words += scr_max;
+    // truncation workspace (max over batches)
+    int64_t gmax = 1, tmax = 1;
+    auto tr_size = [&](const std::vector<VTrunc>& v) {
+        int64_t g = 0, tt = 0;
+        for (auto& e : v) {
+            const HBlock& hb = S.bl[e.blk];
+            g += (ceil_div(hb.m, TRUNC_CHUNK) + ceil_div(hb.n, TRUNC_CHUNK)) * e.k * e.k;
+            tt += 2LL * e.k * rmax;
+        }
+        gmax = std::max(gmax, g);
+        tmax = std::max(tmax, tt);
+    };
+    tr_size(init_trunc);
+    for (auto& st : steps) tr_size(st.trunc);
+    const int64_t off_part = words;
+    words += gmax;
+    const int64_t off_T = words;
+    words += tmax;
+
+    H2Plan* P = new H2Plan();
+    L->plan = P;
+    P->nl = nl;
+    cudaStream_t s = L->h->stream;
+    {
+        void* p = nullptr;
+        cudaError_t e = cudaMallocAsync(&p, (size_t)words * sizeof(double), s);
+        if (e != cudaSuccess) throw FdeError{FDE_ENOMEM, "hlu_factor: arena allocation failed"};
+        L->arena = (double*)p;
+    }
+    double* A = L->arena;
+    P->tr_part = A + off_part;
+    P->tr_T = A + off_T;
+    auto res = [&](const VRef& r) -> double* {
+        switch (r.sp) {
+            case 0: return A + offD[r.id] + r.off;
+            case 1: return A + offU[r.id] + r.off;
+            case 2: return A + offV[r.id] + r.off;
+            case 3: return A + off_scr + r.off;
+            case 4: return A + offLi[r.id] + r.off;
+            default: return A + offUi[r.id] + r.off;
+        }
+    };
+
+    const double ms_alloc = ms_since(t_alloc0);
+    const auto t_flat0 = std::chrono::steady_clock::now();
+    // ---- flatten descriptors
+    std::vector<H2Lu> vlu;
+    std::vector<H2Panel> vpan;
+    std::vector<H2Term> vterm;
+    std::vector<H2Task> vtask;
+    std::vector<H2Tile> vtile;
+    std::vector<H2Copy> vcp;
+    std::vector<TEntry> vte;
+    std::vector<TChunk> vtc;
+    auto put_trunc = [&](const std::vector<VTrunc>& v, H2Launch& ln) {
+        ln.tr_e0 = (int)vte.size();
+        ln.tr_c0 = (int)vtc.size();
+        long long gofs = 0, tofs = 0;
+        for (auto& e : v) {
+            const HBlock& hb = S.bl[e.blk];
+            TEntry te;
+            te.U = A + offU[e.blk];
+            te.V = A + offV[e.blk];
+            te.Uo = A + offU[e.blk];
+            te.Vo = A + offV[e.blk];
+            te.m = hb.m;
+            te.n = hb.n;
+            te.k = e.k;
+            te.zero_tail = 1;
+            te.c_lo = (int)vtc.size() - ln.tr_c0;
+            for (int side = 0; side < 2; ++side) {
+                const long long rows = side ? hb.n : hb.m;
+                for (long long r = 0; r < rows; r += TRUNC_CHUNK)
+                    vtc.push_back(TChunk{(int)(vte.size() - ln.tr_e0), side, r,
+                                         (int)std::min<long long>(TRUNC_CHUNK, rows - r)});
+            }
+            te.c_hi = (int)vtc.size() - ln.tr_c0;
+            te.gofs = gofs;
+            gofs += (long long)(te.c_hi - te.c_lo) * e.k * e.k;
+            te.tofs = tofs;
+            tofs += 2LL * e.k * rmax;
+            ln.tr_kmax = std::max(ln.tr_kmax, e.k);
+            vte.push_back(te);
+        }
+        ln.tr_ne = (int)vte.size() - ln.tr_e0;
+        ln.tr_nc = (int)vtc.size() - ln.tr_c0;
+    };
+    auto put_gemm = [&](const std::vector<VTask>& v, H2Launch& ln, int which) {
+        ln.g_tile0[which] = (int)vtile.size();
+        for (auto& t : v) {
+            H2Task d;
+            d.C = res(t.C);
+            d.ldc = t.ldc;
+            d.m = t.m;
+            d.n = t.n;
+            d.beta = t.beta;
+            d.t_lo = (int)vterm.size();
+            for (auto& q : t.terms)
+                vterm.push_back({res(q.A), res(q.B), q.lda, q.ldb, q.k, q.ta, q.tb, q.alpha});
+            d.t_hi = (int)vterm.size();
+            const int ti = (int)vtask.size();
+            vtask.push_back(d);
+            for (int m0 = 0; m0 < t.m; m0 += GT)
+                for (int n0 = 0; n0 < t.n; n0 += GT) vtile.push_back({ti, m0, n0});
+        }
+        ln.g_ntile[which] = (int)vtile.size() - ln.g_tile0[which];
+    };
+    auto put_copy = [&](const std::vector<VCopy>& v, H2Launch& ln) {
+        ln.cp0 = (int)vcp.size();
+        for (auto& c : v)
+            if (c.m > 0 && c.n > 0)
+                vcp.push_back({c.kind == 0 ? res(c.src) : nullptr, c.lds, res(c.dst), c.ldd, c.m, c.n, c.kind, c.alpha});
+        ln.ncp = (int)vcp.size() - ln.cp0;
+    };
+    auto put_panel = [&](const std::vector<VPanel>& v, H2Launch& ln) {
+        ln.pan0 = (int)vpan.size();
+        for (auto& p : v) {
+            const HBlock& D = S.bl[p.diag];
+            for (int c0 = 0; c0 < p.nvec; c0 += H2_STRIP) {
+                H2Panel d;
+                d.T = A + offD[p.diag];
+                d.ldt = D.m;
+                const int nv = std::min(H2_STRIP, p.nvec - c0);
+                d.X = res(p.X) + (p.mode == 2 ? c0 : c0 * p.ldx);
+                d.ldx = p.ldx;
+                d.m = p.m;
+                d.nvec = nv;
+                d.mode = p.mode;
+                vpan.push_back(d);
+            }
+        }
+        ln.npan = (int)vpan.size() - ln.pan0;
+    };
+    // init: dense copies + low-rank factor copies, initial compression
+    {
+        std::vector<VCopy> c;
+        for (int b = 0; b < nb; ++b) {
+            const HBlock& hb = S.bl[b];
+            if (t0[b] < 0) continue;
+            if (hb.type == HB_DENSE) {
+                c.push_back({{0, b, 0}, {0, b, 0}, hb.m, hb.m, (int)hb.m, (int)hb.n, 0, 1.0});
+            } else if (hb.type == HB_LR) {
+                c.push_back({{1, b, 0}, {1, b, 0}, hb.m, hb.m, (int)hb.m, R, 0, 1.0});
+                c.push_back({{2, b, 0}, {2, b, 0}, hb.n, hb.n, (int)hb.n, R, 0, 1.0});
+            }
+        }
+        put_copy(c, P->init);
+        // sources are the H-matrix arenas, not ours: patch
+        int q = P->init.cp0;
+        for (int b = 0; b < nb; ++b) {
+            const HBlock& hb = S.bl[b];
+            if (t0[b] < 0) continue;
+            if (hb.type == HB_DENSE) {
+                if (hb.m > 0 && hb.n > 0) vcp[q++].src = hm->dense.p + hb.off;
+            } else if (hb.type == HB_LR) {
+                if (hb.m > 0 && R > 0) vcp[q++].src = hm->lr.p + hb.off;
+                if (hb.n > 0 && R > 0) vcp[q++].src = hm->lr.p + hb.off + hb.m * hb.kcap;
+            }
+        }
+        put_trunc(init_trunc, P->init);
+    }
+    P->steps.resize(nl);
+    for (int k = 0; k < nl; ++k) {
+        H2Launch& ln = P->steps[k];
+        VStep& st = steps[k];
+        put_trunc(st.trunc, ln);
+        ln.lu = (int)vlu.size();
+        vlu.push_back({A + offD[st.lu_blk], S.bl[st.lu_blk].m, lm(k)});
+        put_panel(st.panel, ln);
+        put_gemm(st.g0, ln, 3);
+        put_gemm(st.g1, ln, 0);
+        put_gemm(st.g2, ln, 1);
+        put_copy(st.cp, ln);
+        put_gemm(st.g3, ln, 2);
+    }
+    // final: explicit inverses of the leaf factors (for the substitutions)
+    {
+        std::vector<VCopy> c;
+        std::vector<VPanel> pv;
+        for (int q = 0; q < nl; ++q) {
+            const int d = own(q, q);
+            c.push_back({{4, q, 0}, {4, q, 0}, lm(q), lm(q), lm(q), lm(q), 2, 1.0});
+            c.push_back({{5, q, 0}, {5, q, 0}, lm(q), lm(q), lm(q), lm(q), 2, 1.0});
+            pv.push_back({d, {4, q, 0}, lm(q), lm(q), lm(q), 0});
+            pv.push_back({d, {5, q, 0}, lm(q), lm(q), lm(q), 2});
+        }
+        put_copy(c, P->fin);
+        put_panel(pv, P->fin);
+    }
+    const double ms_flat = ms_since(t_flat0);
+    P->lu.upload(vlu.data(), vlu.size(), s);
+    if (!vpan.empty()) P->pan.upload(vpan.data(), vpan.size(), s);
+    if (!vterm.empty()) P->terms.upload(vterm.data(), vterm.size(), s);
+    if (!vtask.empty()) P->tasks.upload(vtask.data(), vtask.size(), s);
+    if (!vtile.empty()) P->tiles.upload(vtile.data(), vtile.size(), s);
+    if (!vcp.empty()) P->cps.upload(vcp.data(), vcp.size(), s);
+    if (!vte.empty()) P->te.upload(vte.data(), vte.size(), s);
+    if (!vtc.empty()) P->tc.upload(vtc.data(), vtc.size(), s);
+
+    L->plan_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_plan0).count();
+    if (getenv("FDE_DEBUG_PLAN"))
+        fprintf(stderr, "hlu2 plan: nl %d blocks %d | simulate %.2f ms, layout+alloc %.2f ms, flatten %.2f ms, "
+                        "upload %.2f ms | tiles %zu terms %zu copies %zu panels %zu trunc %zu\n",
+                nl, nb, ms_sim, ms_alloc, ms_flat, L->plan_ms - ms_sim - ms_alloc - ms_flat, vtile.size(),
+                vterm.size(), vcp.size(), vpan.size(), vte.size());
+    // ---- execute
+    const int pan_smem = (H2_MMAX + H2_STRIP) * (H2_MMAX + 1) * (int)sizeof(double);
+    set_smem_once((const void*)k_h2_panel, pan_smem);
+    set_smem_once((const void*)k_h2_lu, H2_MMAX * H2_MMAX * (int)sizeof(double));
+    int nlaunch = 0;
+    auto run_copy = [&](const H2Launch& ln) {
+        if (!ln.ncp) return;
+        k_h2_copy<<<ln.ncp, 256, 0, s>>>(P->cps.p + ln.cp0);
+        FDE_CHECK_LAUNCH();
+        ++nlaunch;
+    };
+    auto run_trunc = [&](const H2Launch& ln) {
+        if (!ln.tr_ne) return;
+        const TEntry* E = P->te.p + ln.tr_e0;
+        const TChunk* C = P->tc.p + ln.tr_c0;
+        k_bgram<<<ln.tr_nc, 256, 0, s>>>(E, C, P->tr_part);
+        FDE_CHECK_LAUNCH();
+        const int kmax = ln.tr_kmax, ne = (kmax + 1) & ~1;
+        const size_t smem = (size_t)(2 * kmax * kmax + 3 * ne * ne + 2 * ne + 8) * sizeof(double);
+        set_smem_once((const void*)k_bcore, (int)smem);
+        k_bcore<<<ln.tr_ne, 256, smem, s>>>(E, C, P->tr_part, L->tol, rmax, P->tr_T, L->dflag.p + 1);
+        FDE_CHECK_LAUNCH();
+        const size_t asmem = (size_t)(kmax * rmax + TRUNC_CHUNK * kmax) * sizeof(double);
+        set_smem_once((const void*)k_bapply, (int)asmem);
+        k_bapply<<<ln.tr_nc, 256, asmem, s>>>(E, C, P->tr_T, rmax);
+        FDE_CHECK_LAUNCH();
+        nlaunch += 3;
+    };
+    auto run_gemm = [&](const H2Launch& ln, int w) {
+        if (!ln.g_ntile[w]) return;
+        k_h2_gemm<<<ln.g_ntile[w], 256, 0, s>>>(P->tiles.p + ln.g_tile0[w], P->tasks.p, P->terms.p);
+        FDE_CHECK_LAUNCH();
+        ++nlaunch;
+    };
+    auto run_panel = [&](const H2Launch& ln) {
+        if (!ln.npan) return;
+        k_h2_panel<<<ln.npan, 256, pan_smem, s>>>(P->pan.p + ln.pan0);
+        FDE_CHECK_LAUNCH();
+        ++nlaunch;
+    };
+    FDE_CUDA(cudaMemsetAsync(A + lr_lo, 0, (size_t)(lr_hi - lr_lo) * sizeof(double), s));
+    run_copy(P->init);
+    run_trunc(P->init);
+    const int kstop = g_hlu2_stop >= 0 ? std::min(g_hlu2_stop, nl) : nl;   // debug: partial sweep
+    for (int k = 0; k < kstop; ++k) {
+        const H2Launch& ln = P->steps[k];
+        run_trunc(ln);
+        k_h2_lu<<<1, 512, lm(k) * lm(k) * sizeof(double), s>>>(P->lu.p + ln.lu, L->dflag.p);
+        FDE_CHECK_LAUNCH();
+        ++nlaunch;
+        run_panel(ln);
+        run_gemm(ln, 0);
+        run_gemm(ln, 1);
+        run_gemm(ln, 3);   // conversions to dense (after the products: a block may be
+                           // an operand (row / column k) and a target (rows > k) at once)
+        run_copy(ln);
+        run_gemm(ln, 2);
+    }
+    if (kstop == nl) {
+        run_copy(P->fin);
+        run_panel(P->fin);
+    }
+    L->nops = nlaunch;
+
+    // ---- the blocks in the format of hlu.cu (substitutions, test helpers)
+    L->max_rank = 0;
+    for (int b = 0; b < nb; ++b) {
+        const HBlock& hb = S.bl[b];
+        LBlk& lb = L->B[b];
+        lb.type = hb.type;
+        lb.m = hb.m;
+        lb.n = hb.n;
+        lb.r0 = S.cl[hb.tau].r0;
+        lb.c0 = S.cl[hb.sig].r0;
+        for (int q = 0; q < 4; ++q) lb.child[q] = hb.child[q];
+        if (dyn[b] && conv_step[b] < kstop) lb.type = HB_DENSE;
+        if (lb.type == HB_DENSE) lb.D = A + offD[b];
+        if (lb.type == HB_LR) {
+            lb.U = A + offU[b];
+            lb.V = A + offV[b];
+            lb.k = kstop == nl ? kc[b] : kcap[b];   // partial sweep: unwritten columns are zero
+            L->max_rank = std::max(L->max_rank, kc[b]);
+        }
+    }
+    for (int q = 0; q < nl; ++q) {
+        LBlk& d = L->B[own(q, q)];
+        d.Li = A + offLi[q];
+        d.Ui = A + offUi[q];
+    }
+    return true;
+}

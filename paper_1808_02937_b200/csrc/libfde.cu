@@ -6,3 +6,4 @@
 #include "krylov.cu"
 #include "hmatrix.cu"
 #include "hlu.cu"
+#include "hlu2.cu"

@@ -39,7 +39,7 @@ EXPORTED = [
     "sem_rhs", "stiffness_matvec", "hmatrix_build", "fde_hmatrix_get_info", "fde_hmatrix_dense_paper",
     "hlu_factor", "fde_hlu_get_info", "fde_hlu_dense_internal", "precond_apply", "solve", "fde_solve",
     "fde_free_operator", "fde_free_hmatrix", "fde_free_hlu", "fde_profile", "fde_profile_collect",
-    "fde_launch_count", "fde_shard_rows",
+    "fde_launch_count", "fde_shard_rows", "fde_debug_hlu_mode",
 ]
 
 
@@ -81,7 +81,8 @@ class HMatrixInfo(ctypes.Structure):
 
 class HluInfo(ctypes.Structure):
     _fields_ = [("max_rank", ctypes.c_int32), ("stored_entries", ctypes.c_int64), ("factor_ms", ctypes.c_double),
-                ("nops", ctypes.c_int32)]
+                ("nops", ctypes.c_int32), ("algorithm", ctypes.c_int32),
+                ("plan_ms", ctypes.c_double)]
 
 
 class SolveOpts(ctypes.Structure):
@@ -130,6 +131,7 @@ def lib():
         L.fde_profile_collect.argtypes = [vp, ctypes.POINTER(ctypes.c_double), i32]
         L.fde_shard_rows.argtypes = [i32, i32, i32, i32, ctypes.POINTER(i64), ctypes.POINTER(i64),
                                      ctypes.POINTER(i64)]
+        L.fde_debug_hlu_mode.argtypes = [i32]
         L.fde_launch_count.argtypes = []
         L.fde_launch_count.restype = ctypes.c_longlong
         L.solve.argtypes = [vp, vp, vp, vp, vp, i32, i64, ctypes.POINTER(SolveOpts), ctypes.POINTER(SolveReport)]
@@ -364,3 +366,8 @@ def solve(handle: Handle, op: Operator, lu: Optional[HLU], G, method: int = GMRE
     _check(lib().solve(handle.h, op.ptr, lu.ptr if lu is not None else None, _ptr(G), _ptr(X), G.shape[0], op.n,
                        ctypes.byref(o), ctypes.byref(rep)), handle.h)
     return X, rep
+
+
+def set_hlu_mode(mode: int) -> None:
+    """0: leaf-ordered batched H-LU when the partition allows it (default), 1: recursive only."""
+    _check(lib().fde_debug_hlu_mode(int(mode)))

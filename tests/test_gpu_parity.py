@@ -193,14 +193,30 @@ HLU_CASES = [
 ]
 
 
-@pytest.mark.parametrize("case", HLU_CASES, ids=lambda c: c[0].name)
-def test_hlu_exact_mode_equals_dense_solve_of_Atilde(fde, h, case):
+HLU2_CASES = HLU_CASES + [
+    (fi.config4(N=96, P=8), 4),          # 24 leaves of 32 dofs: several low-rank levels
+    (fi.config2(1.3, N=64, P=8), 16),    # leaves of exactly 128 dofs (kernel limit)
+    (fi.config4(N=44, P=6), 5),          # leaves at two depths (dense blocks spanning two leaves)
+]
+
+
+@pytest.fixture(params=[0, 1], ids=["leaf-ordered", "recursive"])
+def hlu_mode(fde, request):
+    fde.set_hlu_mode(request.param)
+    yield request.param
+    fde.set_hlu_mode(0)
+
+
+@pytest.mark.parametrize("case", HLU2_CASES, ids=lambda c: f"{c[0].name}-nmin{c[1]}")
+def test_hlu_exact_mode_equals_dense_solve_of_Atilde(fde, h, case, hlu_mode):
     """tol = 0: the formatted H-LU is the exact LU of A~ (up to rounding), so
-    precond_apply must equal a dense solve with the oracle's A~ (metric M-C)."""
+    precond_apply must equal a dense solve with the oracle's A~ (metric M-C).
+    Both algorithms (leaf-ordered batched, recursive) are checked."""
     p, n_min = case
     op = fde.assemble_problem(h, p)
     hm = fde.hmatrix_build(h, op, p.R, 1.0, n_min)
     lu = fde.hlu_factor(h, hm, 0.0)
+    assert lu.info.algorithm == (1 if hlu_mode == 0 else 0)
     so = oracle_system(p)
     At, _ = O.hmatrix_dense(p, so, R=p.R, lam=1.0, n_min=n_min)
     rng = np.random.default_rng(5)
@@ -213,8 +229,8 @@ def test_hlu_exact_mode_equals_dense_solve_of_Atilde(fde, h, case):
         o.free()
 
 
-@pytest.mark.parametrize("case", HLU_CASES, ids=lambda c: c[0].name)
-def test_hlu_preconditioned_gmres_matches_oracle(fde, h, case):
+@pytest.mark.parametrize("case", HLU2_CASES, ids=lambda c: f"{c[0].name}-nmin{c[1]}")
+def test_hlu_preconditioned_gmres_matches_oracle(fde, h, case, hlu_mode):
     """tol = 1e-3: A~^{-1} is only approximate (parity unpinned
     for the factor itself), but the preconditioned solve must reach the oracle's
     X (metric M-D) and need fewer iterations than the unpreconditioned one."""
@@ -299,3 +315,22 @@ def test_example51_bicgstab_iterations_pattern(fde, h):
             o.free()
     assert its[-1] <= 10
     assert all(its[k + 1] <= its[k] + 1 for k in range(3)), its
+
+
+def test_hlu_leaf_ordered_matches_recursive_factors(fde, h):
+    """At tol = 0 both algorithms compute the unique LU of A~ (no pivoting): the
+    packed factors agree entry by entry up to rounding (scaled like M-A)."""
+    p = fi.config4(N=96, P=8)
+    op = fde.assemble_problem(h, p)
+    hm = fde.hmatrix_build(h, op, p.R, 1.0, 4)
+    F = []
+    for mode in (0, 1):
+        fde.set_hlu_mode(mode)
+        lu = fde.hlu_factor(h, hm, 0.0)
+        F.append(fde.hlu_dense_internal(h, lu).cpu().numpy())
+        lu.free()
+    fde.set_hlu_mode(0)
+    d = np.sqrt(np.abs(np.diag(F[1])))
+    assert np.max(np.abs(F[0] - F[1]) / (d[:, None] * d[None, :])) <= 1e-9
+    hm.free()
+    op.free()
