@@ -232,13 +232,15 @@ def run_ours(args):
     fde.lib().fde_profile(h.h, 1)
     barrier()
     launches0 = fde.lib().fde_launch_count()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    evs[0].record(stream)
     infos = []
-    for _ in range(args.steps):
+    for k in range(args.steps):
         infos.append(step()[0])
-    e1.record(stream)
+        evs[k + 1].record(stream)
     barrier()
+    e0, e1 = evs[0], evs[-1]
+    step_ms = [evs[k].elapsed_time(evs[k + 1]) for k in range(args.steps)]
     launches = fde.lib().fde_launch_count() - launches0
     ms = e0.elapsed_time(e1)
     import ctypes
@@ -308,6 +310,7 @@ def run_ours(args):
                        "l2": f"dense A ({8 * prob.n * prob.n / 1e6:.0f} MB) exceeds the 126 MB L2; no flush needed",
                        "step": "cold solve: assemble + rhs + hmatrix_build + hlu_factor + solve"},
             "phases_ms": {k: round(v, 3) for k, v in avg.items()},
+            "step_ms_each": [round(v, 2) for v in step_ms],
             "roofline": roof if nrhs >= 8 else {
                 "kernel": "k_gemv (dense stiffness matvec, PAPER.md:629)", "bound": "hbm",
                 "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,

@@ -89,6 +89,11 @@ void fde_destroy(fde_handle h)
     comm_destroy(h);
     if (h->ev0) cudaEventDestroy(h->ev0);
     if (h->ev1) cudaEventDestroy(h->ev1);
+    if (h->aux) {
+        cudaStreamSynchronize(h->aux);
+        cudaStreamDestroy(h->aux);
+        for (auto e : h->ev_aux) cudaEventDestroy(e);
+    }
     if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
     delete h;
 }

@@ -101,7 +101,20 @@ struct fde_ctx {
     std::string err;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     int num_sms = 148;
+    // auxiliary stream + events for work that overlaps the caller's stream
+    // (created on first use; ordered by events, never by implicit synchronisation)
+    cudaStream_t aux = nullptr;
+    cudaEvent_t ev_aux[3] = {nullptr, nullptr, nullptr};
 };
+
+inline cudaStream_t aux_stream(fde_ctx* h)
+{
+    if (!h->aux) {
+        FDE_CUDA(cudaStreamCreateWithFlags(&h->aux, cudaStreamNonBlocking));
+        for (auto& e : h->ev_aux) FDE_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    return h->aux;
+}
 
 // ------------------------------------------------------- quadrature tables
 // Host-side generation (long double), Sturm-sequence bisection for the nodes

@@ -517,7 +517,7 @@ __global__ void k_eye(double* B, long long ldb, int m)
 
 // ---- truncation core: parallel cyclic Jacobi on symmetric matrices in smem
 // A (n x n, ld n) -> eigenvalues on the diagonal, V eigenvectors (columns).
-__device__ int cta_jacobi(double* A, double* V, int n, int* pairs)
+__device__ int cta_jacobi(double* A, double* V, int n, int* pairs, double eps = 1e-15)
 {
     // n even (caller pads)
     for (int t = threadIdx.x; t < n * n; t += blockDim.x) V[t] = ((t % n) == (t / n)) ? 1.0 : 0.0;
@@ -544,7 +544,7 @@ __device__ int cta_jacobi(double* A, double* V, int n, int* pairs)
                 pairs[2 * k + 1] = q;
                 const double app = A[p * n + p], aqq = A[q * n + q], apq = A[q * n + p];
                 double c = 1.0, s = 0.0;
-                if (fabs(apq) > 1e-15 * sqrt(fabs(app * aqq)) + 1e-17 * afro + 1e-300) {
+                if (fabs(apq) > eps * sqrt(fabs(app * aqq)) + 1e-17 * afro + 1e-300) {
                     conv = 0;
                     const double tau = (aqq - app) / (2.0 * apq);
                     const double tt = (tau >= 0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
@@ -789,7 +789,10 @@ __global__ void __launch_bounds__(256) k_bcore(const TEntry* E, const TChunk* C,
         A[t] = (i < ke && j < ke) ? Gu[idx[j] * k + idx[i]] : 0.0;
     }
     __syncthreads();
-    cta_jacobi(A, Eu, n, pairs);
+    // rotation threshold: converged to 1e-12 relative when truncating to tol >= 1e-6
+    // (far below the truncation error), to rounding otherwise
+    const double jeps = (tol >= 1e-6) ? 1e-12 : 1e-15;
+    cta_jacobi(A, Eu, n, pairs, jeps);
     __shared__ double mu;
     if (threadIdx.x == 0) {
         double a = 0.0;
@@ -817,7 +820,7 @@ __global__ void __launch_bounds__(256) k_bcore(const TEntry* E, const TChunk* C,
         A[t] = lu[i] * lu[j] * s;
     }
     __syncthreads();
-    cta_jacobi(A, X, n, pairs);
+    cta_jacobi(A, X, n, pairs, jeps);
     __syncthreads();
     __shared__ int ord[TRUNC_KMAX];
     __shared__ int r_sh;
@@ -1860,6 +1863,30 @@ __device__ __forceinline__ void cta_rows_dot(const double* M, long long ldm, lon
     part[t] = (ph < nph) ? acc : 0.0;
 }
 
+// Row sums of per-thread partials: thread t holds row t % nrp (nrp a power of two)
+// and phase t / nrp; lanes of one row are combined with shuffles (nrp < 32) or
+// through shared memory, always in the same order (deterministic).  The result
+// is returned to the threads t < nrp.
+__device__ __forceinline__ double apply_row_sum(double v, int nrp, double* part)
+{
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    double s = 0.0;
+    if (nrp < 32) {
+        for (int off = 16; off >= nrp; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+        if (lane < nrp) part[w * nrp + lane] = v;
+        __syncthreads();
+        if (threadIdx.x < nrp)
+            for (int q = 0; q < APPLY_THREADS / 32; ++q) s += part[q * nrp + threadIdx.x];
+    } else {
+        part[threadIdx.x] = v;
+        __syncthreads();
+        if (threadIdx.x < nrp)
+            for (int q = threadIdx.x; q < APPLY_THREADS; q += nrp) s += part[q];
+    }
+    __syncthreads();
+    return s;
+}
+
 __device__ void run_sweep(const SweepDev& S, int backward, double* x, long long ldx, int nrhs, double* z, double* t,
                           int tstride, cg::grid_group& cl)
 {
@@ -1899,12 +1926,14 @@ __device__ void run_sweep(const SweepDev& S, int backward, double* x, long long 
                 }
                 __syncthreads();
             }
-            const int nph = APPLY_THREADS / nr;
-            const int i = threadIdx.x % nr, ph = threadIdx.x / nr;
+            int nrp = 1;
+            while (nrp < nr) nrp <<= 1;
+            const int nph = APPLY_THREADS / nrp;
+            const int i = threadIdx.x % nrp, ph = threadIdx.x / nrp;
             double acc[APPLY_RC];
 #pragma unroll
             for (int cc = 0; cc < APPLY_RC; ++cc) acc[cc] = 0.0;
-            if (ph < nph) {
+            if (ph < nph && i < nr) {
                 const int row = r_lo + i;
                 for (int d = L.d_lo; d < L.d_hi; ++d) {
                     const SDense D = S.dense[d];
@@ -1936,15 +1965,11 @@ __device__ void run_sweep(const SweepDev& S, int backward, double* x, long long 
                 }
             }
             for (int cc = 0; cc < nc; ++cc) {
-                part[threadIdx.x] = acc[cc];
-                __syncthreads();
+                const double s2 = apply_row_sum(acc[cc], nrp, part);
                 if (threadIdx.x < nr) {
-                    double s2 = 0.0;
-                    for (int q = threadIdx.x; q < nph * nr; q += nr) s2 += part[q];
                     const double* xc = x + (long long)(c0 + cc) * ldx;
                     z[(long long)(c0 + cc) * L.m + r_lo + threadIdx.x] = ldcg(xc + L.r0 + r_lo + threadIdx.x) - s2;
                 }
-                __syncthreads();
             }
             if (lr_smem) __syncthreads();
         }
@@ -1976,14 +2001,16 @@ __device__ void run_sweep(const SweepDev& S, int backward, double* x, long long 
         cl.sync();   // grid barrier (orders global memory across the grid)
         // ---- phase B: x_k = Inv_k z_k (this CTA's row slice), RHS in register chunks
         if (nr > 0) {
-            const int nph = APPLY_THREADS / nr;
-            const int i = threadIdx.x % nr, ph = threadIdx.x / nr;
+            int nrp = 1;
+            while (nrp < nr) nrp <<= 1;
+            const int nph = APPLY_THREADS / nrp;
+            const int i = threadIdx.x % nrp, ph = threadIdx.x / nrp;
             for (int c0 = 0; c0 < nrhs; c0 += APPLY_RC) {
                 const int nc = min(APPLY_RC, nrhs - c0);
                 double acc[APPLY_RC];
 #pragma unroll
                 for (int cc = 0; cc < APPLY_RC; ++cc) acc[cc] = 0.0;
-                if (ph < nph)
+                if (ph < nph && i < nr)
                     for (int j = ph; j < L.m; j += nph) {
                         const double a = L.inv[(long long)j * L.m + r_lo + i];
 #pragma unroll
@@ -1991,14 +2018,8 @@ __device__ void run_sweep(const SweepDev& S, int backward, double* x, long long 
                             if (cc < nc) acc[cc] = fma(a, ldcg(z + (long long)(c0 + cc) * L.m + j), acc[cc]);
                     }
                 for (int cc = 0; cc < nc; ++cc) {
-                    part[threadIdx.x] = (ph < nph) ? acc[cc] : 0.0;
-                    __syncthreads();
-                    if (threadIdx.x < nr) {
-                        double s2 = 0.0;
-                        for (int q = threadIdx.x; q < nph * nr; q += nr) s2 += part[q];
-                        x[(long long)(c0 + cc) * ldx + L.r0 + r_lo + threadIdx.x] = s2;
-                    }
-                    __syncthreads();
+                    const double s2 = apply_row_sum(acc[cc], nrp, part);
+                    if (threadIdx.x < nr) x[(long long)(c0 + cc) * ldx + L.r0 + r_lo + threadIdx.x] = s2;
                 }
             }
         }
@@ -2075,11 +2096,7 @@ static ApplySched* apply_sched_build(fde_lu* L)
         if (m == 0) continue;
         double* Li = A->inv.p + invoff[q];
         double* Ui = Li + m * m;
-        if (D.Li && D.Ui) {   // computed during the factorisation
-            copy2d(L, D.Li, m, m, m, Li, m);
-            copy2d(L, D.Ui, m, m, m, Ui, m);
-            continue;
-        }
+        if (D.Li && D.Ui) continue;   // computed during the factorisation: used in place
         k_eye<<<64, 256, 0, L->h->stream>>>(Li, m, (int)m);
         FDE_CHECK_LAUNCH();
         k_eye<<<64, 256, 0, L->h->stream>>>(Ui, m, (int)m);
@@ -2154,7 +2171,8 @@ static ApplySched* apply_sched_build(fde_lu* L)
             const HCluster& c = S.cl[leafcl[q]];
             s.r0 = c.r0;
             s.m = (int)(c.r1 - c.r0);
-            s.inv = A->inv.p + invoff[q] + (which ? (int64_t)s.m * s.m : 0);
+            const LBlk& Dq = L->B[diagblk[q]];
+            s.inv = (Dq.Li && Dq.Ui) ? (which ? Dq.Ui : Dq.Li) : A->inv.p + invoff[q] + (which ? (int64_t)s.m * s.m : 0);
             s.d_lo = (int)dv.size();
             dv.insert(dv.end(), d[q].begin(), d[q].end());
             s.d_hi = (int)dv.size();

@@ -77,115 +77,122 @@ struct H2Copy {   // kind 0: dst = alpha src, 1: dst = 0, 2: dst = I
 };
 
 // ----------------------------------------------------------------- kernels
-// LU without pivoting of an m x m tile (m <= 128) held in registers: thread t owns
-// row i = t % 128 and the columns j = g + 4q (g = t / 128, q = 0..31); per pivot,
-// row k and the multipliers of column k are broadcast through shared memory.
-__global__ void __launch_bounds__(512) k_h2_lu(const H2Lu* tk, int* bad)
+// LU without pivoting of an m x m tile (m <= 128) held in registers: thread t
+// owns row i = t % 128 and the columns j = g + 8q (g = t / 128, q = 0..15).  The
+// pivot row and the pivot column of step k+1 are published (double-buffered
+// shared memory) by their owners right after their step-k update, so every
+// pivot step costs one barrier.  Register indices must be compile-time
+// constants: the column loops start at q0 = k / 8 through a switch.
+template <int Q0>
+__device__ __forceinline__ void h2_lu_update(double (&a)[16], double l, const double* row, int g, int k)
+{
+    // q = Q0 may hold columns <= k (g + 8 Q0 <= k): masked; q > Q0 are all > k
+    a[Q0] = fma((g + 8 * Q0 > k) ? -l : 0.0, row[g + 8 * Q0], a[Q0]);
+#pragma unroll
+    for (int q = Q0 + 1; q < 16; ++q) a[q] = fma(-l, row[g + 8 * q], a[q]);
+}
+
+#define H2_SW16(sel, STMT) \
+    switch (sel) {         \
+        case 0: STMT(0); break;   case 1: STMT(1); break;   case 2: STMT(2); break;   case 3: STMT(3); break;   \
+        case 4: STMT(4); break;   case 5: STMT(5); break;   case 6: STMT(6); break;   case 7: STMT(7); break;   \
+        case 8: STMT(8); break;   case 9: STMT(9); break;   case 10: STMT(10); break; case 11: STMT(11); break; \
+        case 12: STMT(12); break; case 13: STMT(13); break; case 14: STMT(14); break; default: STMT(15); break; \
+    }
+
+__global__ void __launch_bounds__(1024) k_h2_lu(const H2Lu* tk, int* bad)
 {
     const H2Lu d = tk[blockIdx.x];
-    __shared__ double sRow[H2_MMAX], sCol[H2_MMAX];
+    __shared__ double sRow[2][H2_MMAX], sCol[2][H2_MMAX];
     const int m = d.m, i = threadIdx.x & 127, g = threadIdx.x >> 7;
-    double a[32];
+    double a[16];
 #pragma unroll
-    for (int q = 0; q < 32; ++q) {
-        const int j = g + 4 * q;
+    for (int q = 0; q < 16; ++q) {
+        const int j = g + 8 * q;
         a[q] = (i < m && j < m) ? d.D[(long long)j * d.ld + i] : 0.0;
     }
+    if (i == 0)
+#pragma unroll
+        for (int q = 0; q < 16; ++q) sRow[0][g + 8 * q] = a[q];
+    if (g == 0) sCol[0][i] = a[0];
+    __syncthreads();
     for (int k = 0; k < m; ++k) {
-        if (i == k) {
-#pragma unroll
-            for (int q = 0; q < 32; ++q)
-                if (g + 4 * q >= k) sRow[g + 4 * q] = a[q];
-        }
-        __syncthreads();
-        const double piv = sRow[k];
+        const int b = k & 1;
+        const double piv = sRow[b][k];
         if (threadIdx.x == 0 && (!(fabs(piv) > 0.0) || !isfinite(piv))) *bad = 1;
-        if (g == (k & 3) && i > k && i < m) {
-            const double ip = 1.0 / piv;
+        if (i > k && i < m) {
+            const double l = sCol[b][i] / piv;
+            if (g == (k & 7)) {
+#define H2_SETL(Q) a[Q] = l
+                H2_SW16(k >> 3, H2_SETL)
+#undef H2_SETL
+            }
+            const double* row = sRow[b];
 #pragma unroll
-            for (int q = 0; q < 32; ++q)
-                if (g + 4 * q == k) {
-                    a[q] *= ip;
-                    sCol[i] = a[q];
-                }
+            for (int q = 0; q < 16; ++q) {   // branch-free: columns <= k get a zero multiplier
+                const double lq = (g + 8 * q > k) ? -l : 0.0;
+                a[q] = fma(lq, row[g + 8 * q], a[q]);
+            }
+            if (i == k + 1) {   // entries <= k of the published row are never read
+#pragma unroll
+                for (int q = 0; q < 16; ++q) sRow[b ^ 1][g + 8 * q] = a[q];
+            }
+            if (g == ((k + 1) & 7)) {
+#define H2_PUBC(Q) sCol[b ^ 1][i] = a[Q]
+                H2_SW16((k + 1) >> 3, H2_PUBC)
+#undef H2_PUBC
+            }
         }
         __syncthreads();
-        if (i > k && i < m) {
-            const double l = sCol[i];
-#pragma unroll
-            for (int q = 0; q < 32; ++q)
-                if (g + 4 * q > k) a[q] = fma(-l, sRow[g + 4 * q], a[q]);
-        }
     }
 #pragma unroll
-    for (int q = 0; q < 32; ++q) {
-        const int j = g + 4 * q;
+    for (int q = 0; q < 16; ++q) {
+        const int j = g + 8 * q;
         if (i < m && j < m) d.D[(long long)j * d.ld + i] = a[q];
     }
 }
 
-// one CTA per strip of <= 32 vectors; T' (lower, m x m) and the strip in smem
-__global__ void __launch_bounds__(256) k_h2_panel(const H2Panel* P)
+__device__ __forceinline__ void cp_async8(double* sdst, const double* gsrc)
 {
-    extern __shared__ double psm[];
-    const H2Panel p = P[blockIdx.x];
-    const int m = p.m, ldT = m + 1, ldB = m + 1;
-    double* Ts = psm;                 // T'[i][j] at Ts[j * ldT + i], i >= j
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gsrc));
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
+
+// One CTA per strip of <= 32 vectors.  The packed LU tile T (m x m) and the strip
+// are staged in shared memory with asynchronous copies; T' (lower) is read from
+// the staged tile: mode 0: T'[i][j] = L[i][j] = Ts[j ldT + i] (unit diagonal),
+// modes 1, 2: T'[i][j] = U[j][i] = Ts[i ldT + j].
+template <int MODE>
+__device__ __forceinline__ double h2_tp(const double* Ts, int ldT, int i, int j)
+{
+    return MODE == 0 ? Ts[j * ldT + i] : Ts[i * ldT + j];
+}
+
+template <int MODE>
+__device__ void h2_panel_body(const H2Panel& p, double* psm)
+{
+    const int m = p.m, ldT = (m & 1) ? m + 2 : m + 1, ldB = ldT;
+    double* Ts = psm;
     double* Bs = psm + m * ldT;       // vector c, element i at Bs[c * ldB + i]
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    const bool unit = (p.mode == 0);
     const int nv = p.nvec;
-    // loads: 8 independent global loads in flight per thread
-    if (p.mode == 0) {
-        for (int t0 = tid; t0 < m * m; t0 += 256 * 8) {
-            double v[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const int t = t0 + 256 * u, i = t % m, j = t / m;      // L[i][j] = T[i + j ldt]
-                v[u] = (t < m * m && i > j) ? p.T[(long long)j * p.ldt + i] : 0.0;
-            }
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const int t = t0 + 256 * u, i = t % m, j = t / m;
-                if (t < m * m && i > j) Ts[j * ldT + i] = v[u];
-            }
+    for (int t = tid; t < m * m; t += 256) {
+        const int i = t % m, j = t / m;
+        cp_async8(Ts + j * ldT + i, p.T + (long long)j * p.ldt + i);
+    }
+    if (MODE == 2) {   // rows of X are the vectors
+        for (int t = tid; t < nv * m; t += 256) {
+            const int c = t % nv, i = t / nv;
+            cp_async8(Bs + c * ldB + i, p.X + (long long)i * p.ldx + c);
         }
     } else {
-        for (int t0 = tid; t0 < m * m; t0 += 256 * 8) {
-            double v[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const int t = t0 + 256 * u, j = t % m, i = t / m;      // T'[i][j] = U[j][i] = T[j + i ldt]
-                v[u] = (t < m * m && i >= j) ? p.T[(long long)i * p.ldt + j] : 0.0;
-            }
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const int t = t0 + 256 * u, j = t % m, i = t / m;
-                if (t < m * m && i >= j) Ts[j * ldT + i] = v[u];
-            }
+        for (int t = tid; t < nv * m; t += 256) {
+            const int i = t % m, c = t / m;
+            cp_async8(Bs + c * ldB + i, p.X + (long long)c * p.ldx + i);
         }
     }
-    for (int t0 = tid; t0 < nv * m; t0 += 256 * 8) {
-        double v[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            const int t = t0 + 256 * u;
-            if (p.mode == 2) {   // rows of X are the vectors
-                const int c = t % nv, i = t / nv;
-                v[u] = (t < nv * m) ? p.X[(long long)i * p.ldx + c] : 0.0;
-            } else {
-                const int i = t % m, c = t / m;
-                v[u] = (t < nv * m) ? p.X[(long long)c * p.ldx + i] : 0.0;
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            const int t = t0 + 256 * u;
-            if (t >= nv * m) continue;
-            if (p.mode == 2) Bs[(t % nv) * ldB + t / nv] = v[u];
-            else Bs[(t / m) * ldB + t % m] = v[u];
-        }
-    }
+    cp_async_wait_all();
     __syncthreads();
     const int nb = (m + 31) / 32;
     for (int bi = 0; bi < nb; ++bi) {
@@ -199,11 +206,11 @@ __global__ void __launch_bounds__(256) k_h2_panel(const H2Panel* P)
                 v[u] = (c < nv && lane < bs) ? Bs[c * ldB + b0 + lane] : 0.0;
             }
             for (int q = 0; q < bs; ++q) {
-                const double tq = (lane > q && lane < bs) ? Ts[(b0 + q) * ldT + b0 + lane] : 0.0;
-                const double dq = unit ? 1.0 : Ts[(b0 + q) * ldT + b0 + q];
+                const double tq = (lane > q && lane < bs) ? h2_tp<MODE>(Ts, ldT, b0 + lane, b0 + q) : 0.0;
+                const double rq = MODE == 0 ? 1.0 : 1.0 / h2_tp<MODE>(Ts, ldT, b0 + q, b0 + q);
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
-                    const double y = __shfl_sync(0xffffffffu, v[u], q) / dq;
+                    const double y = __shfl_sync(0xffffffffu, v[u], q) * rq;
                     if (lane == q) v[u] = y;
                     else v[u] = fma(-tq, y, v[u]);
                 }
@@ -218,27 +225,36 @@ __global__ void __launch_bounds__(256) k_h2_panel(const H2Panel* P)
         // trailing rows: B[i][c] -= sum_q T'[i][b0+q] Y[q][c]
         const int r0 = b0 + bs;
         if (r0 < m) {
-            for (int t = tid; t < (m - r0) * nv; t += blockDim.x) {
+            for (int t = tid; t < (m - r0) * nv; t += 256) {
                 const int i = r0 + t % (m - r0), c = t / (m - r0);
                 double s = Bs[c * ldB + i];
 #pragma unroll 8
-                for (int q = 0; q < bs; ++q) s = fma(-Ts[(b0 + q) * ldT + i], Bs[c * ldB + b0 + q], s);
+                for (int q = 0; q < bs; ++q) s = fma(-h2_tp<MODE>(Ts, ldT, i, b0 + q), Bs[c * ldB + b0 + q], s);
                 Bs[c * ldB + i] = s;
             }
         }
         __syncthreads();
     }
-    if (p.mode == 2) {
-        for (int t = tid; t < nv * m; t += blockDim.x) {
+    if (MODE == 2) {
+        for (int t = tid; t < nv * m; t += 256) {
             const int c = t % nv, i = t / nv;
             p.X[(long long)i * p.ldx + c] = Bs[c * ldB + i];
         }
     } else {
-        for (int t = tid; t < nv * m; t += blockDim.x) {
+        for (int t = tid; t < nv * m; t += 256) {
             const int i = t % m, c = t / m;
             p.X[(long long)c * p.ldx + i] = Bs[c * ldB + i];
         }
     }
+}
+
+__global__ void __launch_bounds__(256) k_h2_panel(const H2Panel* P)
+{
+    extern __shared__ double psm[];
+    const H2Panel p = P[blockIdx.x];
+    if (p.mode == 0) h2_panel_body<0>(p, psm);
+    else if (p.mode == 1) h2_panel_body<1>(p, psm);
+    else h2_panel_body<2>(p, psm);
 }
 
 // grouped multi-term GEMM: every CTA owns a 64 x 64 tile of one task,
@@ -376,7 +392,8 @@ struct VCopy {
     double alpha;
 };
 struct VPanel {
-    int diag;   // block id of the diagonal tile
+    VRef T;     // packed LU of the diagonal tile (ld ldt)
+    int64_t ldt;
     VRef X;
     int64_t ldx;
     int m, nvec, mode;
@@ -385,16 +402,21 @@ struct VTrunc {
     int blk, k;
 };
 struct VStep {
-    std::vector<VTrunc> trunc;
+    std::vector<VTrunc> trunc;      // panel operands of this step (before the panels)
+    std::vector<VTrunc> trunc_ov;   // targets about to overflow (before this step's new columns)
     int lu_blk = -1;
+    int64_t lu_off = 0;
     std::vector<VPanel> panel;
     std::vector<VTask> g0, g1, g2, g3;   // conversions to dense, cores, products, dense updates
     std::vector<VCopy> cp;           // low-rank target columns
     int64_t scratch = 0;
 };
 
+struct H2Trunc {       // one batched truncation: ranges in the flat entry / chunk arrays
+    int e0 = 0, ne = 0, c0 = 0, nc = 0, kmax = 0;
+};
 struct H2Launch {      // ranges in the flat device arrays
-    int tr_e0 = 0, tr_ne = 0, tr_c0 = 0, tr_nc = 0, tr_kmax = 0;
+    H2Trunc tr, tr_ov;
     int lu = -1;
     int pan0 = 0, npan = 0;
     int g_tile0[4] = {0, 0, 0, 0}, g_ntile[4] = {0, 0, 0, 0};
@@ -403,6 +425,7 @@ struct H2Launch {      // ranges in the flat device arrays
 
 struct H2Plan {
     int nl = 0;
+    std::vector<H2Launch> fin_lv;            // leaf inverses: one level per tile distance
     std::vector<H2Launch> steps;
     H2Launch init, fin;   // initial copies + compression; final inverses
     DBuf<H2Lu> lu;
@@ -428,23 +451,36 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
     const bool trunc = L->tol > 0.0;
     const int R = hm->R, rmax = L->rmax;
     if (trunc && (R > TRUNC_KMAX || rmax > TRUNC_KMAX)) return false;
-    // ---- leaves in dof order
+    // ---- sweep tiles: the leaves of the cluster tree, each split into equal
+    // chunks of at most H2_MMAX dofs (the partition itself is unchanged: a dense
+    // leaf block then spans several tiles)
     std::vector<int> leafcl;
     for (size_t c = 0; c < S.cl.size(); ++c)
         if (S.cl[c].child[0] < 0 && S.cl[c].r1 > S.cl[c].r0) leafcl.push_back((int)c);
     std::sort(leafcl.begin(), leafcl.end(), [&](int a, int b) { return S.cl[a].r0 < S.cl[b].r0; });
-    const int nl = (int)leafcl.size();
-    if (nl == 0) return false;
-    std::vector<int64_t> lr0(nl + 1);
-    for (int q = 0; q < nl; ++q) {
-        lr0[q] = S.cl[leafcl[q]].r0;
-        if (S.cl[leafcl[q]].r1 - lr0[q] > H2_MMAX) return false;
+    if (leafcl.empty()) return false;
+    std::vector<int64_t> lr0;
+    for (size_t q = 0; q < leafcl.size(); ++q) {
+        const int64_t a = S.cl[leafcl[q]].r0, b = S.cl[leafcl[q]].r1;
+        if (q + 1 < leafcl.size() ? S.cl[leafcl[q + 1]].r0 != b : b != S.n) return false;
+        const int64_t nch = ceil_div(b - a, H2_MMAX);
+        for (int64_t c = 0; c < nch; ++c) lr0.push_back(a + (b - a) * c / nch);
     }
-    lr0[nl] = S.n;
-    for (int q = 0; q < nl; ++q)
-        if (S.cl[leafcl[q]].r1 != lr0[q + 1]) return false;
+    lr0.push_back(S.n);
+    const int nl = (int)lr0.size() - 1;
+    // leaves of the partition as tile ranges (the substitutions run over leaves)
+    const int nleaf = (int)leafcl.size();
+    std::vector<int> lq0(nleaf), lq1(nleaf), leaf_of(nl);
+    for (int q = 0, f = 0; f < nleaf; ++f) {
+        lq0[f] = q;
+        while (q < nl && lr0[q + 1] <= S.cl[leafcl[f]].r1) leaf_of[q++] = f;
+        lq1[f] = q - 1;
+    }
+    auto lfm = [&](int f) { return (int64_t)(lr0[lq1[f] + 1] - lr0[lq0[f]]); };
+    // offset of tile (i, j) inside the inverse of leaf f (ld = leaf size)
+    auto ioff = [&](int f, int i, int j) { return (lr0[j] - lr0[lq0[f]]) * lfm(f) + (lr0[i] - lr0[lq0[f]]); };
     auto lm = [&](int q) { return (int)(lr0[q + 1] - lr0[q]); };
-    // leaf range of a cluster (clusters are unions of consecutive leaves)
+    // tile range of a cluster (clusters are unions of consecutive tiles)
     auto lrange = [&](int cl, int& a, int& b) {
         a = (int)(std::lower_bound(lr0.begin(), lr0.end() - 1, S.cl[cl].r0) - lr0.begin());
         b = (int)(std::lower_bound(lr0.begin(), lr0.end() - 1, S.cl[cl].r1) - lr0.begin()) - 1;
@@ -466,7 +502,7 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
     }
     for (int q = 0; q < nl; ++q) {
         const int d = owner[(size_t)q * nl + q];
-        if (d < 0 || S.bl[d].type != HB_DENSE || t0[d] != q || t1[d] != q || s0[d] != q || s1[d] != q) return false;
+        if (d < 0 || S.bl[d].type != HB_DENSE) return false;
     }
     for (size_t t = 0; t < owner.size(); ++t)
         if (owner[t] < 0) return false;
@@ -476,6 +512,8 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
     auto isLR = [&](int b) { return S.bl[b].type == HB_LR && !dyn[b]; };
     auto row0 = [&](int b) { return S.cl[S.bl[b].tau].r0; };
     auto col0 = [&](int b) { return S.cl[S.bl[b].sig].r0; };
+    // offset of tile (i, j) inside dense block b (column-major, ld m_b)
+    auto toff = [&](int b, int i, int j) { return (lr0[j] - col0(b)) * S.bl[b].m + (lr0[i] - row0(b)); };
 
     // ---- simulation: column counts of the low-rank blocks, per-step op lists
     std::vector<int> kc(nb, 0), kcap(nb, 0);
@@ -507,39 +545,46 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
             const int c = own(k, j);
             if (Rc.empty() || Rc.back() != c) Rc.push_back(c);
         }
-        for (int b : Cb)
-            if (t0[b] <= k) return false;
+        for (int b : Cb)   // only dense blocks may straddle tile k (leaf blocks over several tiles)
+            if (t1[b] <= k || (t0[b] <= k && S.bl[b].type != HB_DENSE)) return false;
         for (int c : Rc)
-            if (s0[c] <= k) return false;
+            if (s1[c] <= k || (s0[c] <= k && S.bl[c].type != HB_DENSE)) return false;
         // truncation of panel operands with pending columns
         std::vector<char> in_tr(nb, 0);
-        auto add_trunc = [&](int b) {
+        auto add_trunc = [&](int b, bool overflow) {
             if (!trunc || !pend[b] || in_tr[b]) return;
             in_tr[b] = 1;
-            st.trunc.push_back({b, kc[b]});
+            (overflow ? st.trunc_ov : st.trunc).push_back({b, kc[b]});
             kc[b] = rmax;
             pend[b] = 0;
         };
         for (int b : Cb)
-            if (isLR(b)) add_trunc(b);
+            if (isLR(b)) add_trunc(b, false);
         for (int c : Rc)
-            if (isLR(c)) add_trunc(c);
+            if (isLR(c)) add_trunc(c, false);
         // panels (after truncation: widths are the current kc of the operands; types
         // before this step's conversions, which run after the products)
         st.lu_blk = dk;
+        st.lu_off = toff(dk, k, k);
+        const VRef Tk{0, dk, toff(dk, k, k)};
+        const int64_t ldk = S.bl[dk].m;
         for (int b : Cb) {
             const HBlock& B = S.bl[b];
-            if (isLR(b))
-                st.panel.push_back({dk, {2, b, lr0[k] - col0(b)}, B.n, mk, kc[b], 1});
-            else
-                st.panel.push_back({dk, {0, b, (lr0[k] - col0(b)) * B.m}, B.m, mk, (int)B.m, 2});
+            if (isLR(b)) {
+                st.panel.push_back({Tk, ldk, {2, b, lr0[k] - col0(b)}, B.n, mk, kc[b], 1});
+            } else {   // rows of tiles > k of the column of tile k
+                const int i0 = std::max(t0[b], k + 1);
+                st.panel.push_back({Tk, ldk, {0, b, toff(b, i0, k)}, B.m, mk, (int)(lr0[t1[b] + 1] - lr0[i0]), 2});
+            }
         }
         for (int c : Rc) {
             const HBlock& C = S.bl[c];
-            if (isLR(c))
-                st.panel.push_back({dk, {1, c, lr0[k] - row0(c)}, C.m, mk, kc[c], 0});
-            else
-                st.panel.push_back({dk, {0, c, lr0[k] - row0(c)}, C.m, mk, (int)C.n, 0});
+            if (isLR(c)) {
+                st.panel.push_back({Tk, ldk, {1, c, lr0[k] - row0(c)}, C.m, mk, kc[c], 0});
+            } else {   // columns of tiles > k of the row of tile k
+                const int j0 = std::max(s0[c], k + 1);
+                st.panel.push_back({Tk, ldk, {0, c, toff(c, k, j0)}, C.m, mk, (int)(lr0[s1[c] + 1] - lr0[j0]), 0});
+            }
         }
         // products: pair scratch offsets
         struct Pair { int b, c; int64_t w; int rw; bool bl, cl; };   // bl/cl: operand types at this step   // w: W (n_c x kc_b) or Z (m_b x kc_c) scratch offset
@@ -589,9 +634,9 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         for (size_t pi = 0; pi < pairs.size(); ++pi) {
             const int b = pairs[pi].b, c = pairs[pi].c;
             ++stamp_id;
-            for (int i = t0[b]; i <= t1[b];) {
+            for (int i = std::max(t0[b], k + 1); i <= t1[b];) {
                 int inext = t1[b] + 1;
-                for (int j = s0[c]; j <= s1[c];) {   // jump over the column run of each owner
+                for (int j = std::max(s0[c], k + 1); j <= s1[c];) {   // jump over the column run of each owner
                     const int t = own(i, j);
                     if (stamp[t] != stamp_id) {
                         stamp[t] = stamp_id;
@@ -624,7 +669,7 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
                 const HBlock& T = S.bl[t];
                 const int lim = trunc ? TRUNC_KMAX : (int)std::max<int64_t>(1, std::min(T.m, T.n) / 2);
                 if (!conv[t] && kc[t] + incoming[t] > lim) {
-                    if (trunc && rmax + incoming[t] <= lim) add_trunc(t);
+                    if (trunc && rmax + incoming[t] <= lim) add_trunc(t, true);
                     else conv[t] = 1;
                 }
                 if (conv[t]) {   // D_t = U_t V_t^T, then a dense block for good
@@ -644,8 +689,8 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
             for (int t : ptg[pi]) {
                 const HBlock& T = S.bl[t];
                 if (!isLR(t)) {
-                    for (int i = std::max(t0[b], t0[t]); i <= std::min(t1[b], t1[t]); ++i)
-                        for (int j = std::max(s0[c], s0[t]); j <= std::min(s1[c], s1[t]); ++j) {
+                    for (int i = std::max(std::max(t0[b], t0[t]), k + 1); i <= std::min(t1[b], t1[t]); ++i)
+                        for (int j = std::max(std::max(s0[c], s0[t]), k + 1); j <= std::min(s1[c], s1[t]); ++j) {
                             const size_t key = (size_t)i * nl + j;
                             int ti;
                             if (tile_stamp[key] != tile_stamp_id) {
@@ -701,8 +746,8 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
             Grp& g = grps[lt.second];
             const int t = g.t, b = pr.b, c = pr.c;
             const HBlock &T = S.bl[t], &B = S.bl[b], &C = S.bl[c];
-            const int ia = std::max(t0[b], t0[t]), ib = std::min(t1[b], t1[t]);
-            const int ja = std::max(s0[c], s0[t]), jb = std::min(s1[c], s1[t]);
+            const int ia = std::max(std::max(t0[b], t0[t]), k + 1), ib = std::min(t1[b], t1[t]);
+            const int ja = std::max(std::max(s0[c], s0[t]), k + 1), jb = std::min(s1[c], s1[t]);
             const int64_t R0 = lr0[ia], R1 = lr0[ib + 1], C0 = lr0[ja], C1 = lr0[jb + 1];
             const int64_t us = g.slot * T.m + (R0 - row0(t)), vs = g.slot * T.n + (C0 - col0(t));
             if (pr.bl) {
@@ -746,13 +791,26 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         }
     }
     const int64_t lr_hi = words;
-    std::vector<int64_t> offLi(nl), offUi(nl);
-    for (int q = 0; q < nl; ++q) {
-        offLi[q] = words; words += (int64_t)lm(q) * lm(q);
-        offUi[q] = words; words += (int64_t)lm(q) * lm(q);
+    // inverses of the leaf factors L_f^{-1}, U_f^{-1} (leaf size squared each)
+    std::vector<int64_t> offLi(nleaf), offUi(nleaf);
+    const int64_t inv_lo = words;
+    for (int f = 0; f < nleaf; ++f) {
+        offLi[f] = words; words += lfm(f) * lfm(f);
+        offUi[f] = words; words += lfm(f) * lfm(f);
     }
+    const int64_t inv_hi = words;
     int64_t scr_max = 1;
     for (auto& st : steps) scr_max = std::max(scr_max, st.scratch);
+    int maxnt = 1;
+    for (int f = 0; f < nleaf; ++f) maxnt = std::max(maxnt, lq1[f] - lq0[f] + 1);
+    for (int dd = 1; dd < maxnt; ++dd) {   // scratch of the block-triangular inversion levels
+        int64_t w = 0;
+        for (int f = 0; f < nleaf; ++f)
+            for (int i = lq0[f]; i <= lq1[f]; ++i)
+                for (int j = lq0[f]; j <= lq1[f]; ++j)
+                    if (std::abs(i - j) == dd) w += (int64_t)lm(i) * lm(j);
+        scr_max = std::max(scr_max, w);
+    }
     const int64_t off_scr = words;
     words += scr_max;
     // truncation workspace (max over batches)
@@ -768,7 +826,10 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         tmax = std::max(tmax, tt);
     };
     tr_size(init_trunc);
-    for (auto& st : steps) tr_size(st.trunc);
+    for (auto& st : steps) {
+        tr_size(st.trunc);
+        tr_size(st.trunc_ov);
+    }
     const int64_t off_part = words;
     words += gmax;
     const int64_t off_T = words;
@@ -809,9 +870,9 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
     std::vector<H2Copy> vcp;
     std::vector<TEntry> vte;
     std::vector<TChunk> vtc;
-    auto put_trunc = [&](const std::vector<VTrunc>& v, H2Launch& ln) {
-        ln.tr_e0 = (int)vte.size();
-        ln.tr_c0 = (int)vtc.size();
+    auto put_trunc = [&](const std::vector<VTrunc>& v, H2Trunc& ln) {
+        ln.e0 = (int)vte.size();
+        ln.c0 = (int)vtc.size();
         long long gofs = 0, tofs = 0;
         for (auto& e : v) {
             const HBlock& hb = S.bl[e.blk];
@@ -824,23 +885,23 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
             te.n = hb.n;
             te.k = e.k;
             te.zero_tail = 1;
-            te.c_lo = (int)vtc.size() - ln.tr_c0;
+            te.c_lo = (int)vtc.size() - ln.c0;
             for (int side = 0; side < 2; ++side) {
                 const long long rows = side ? hb.n : hb.m;
                 for (long long r = 0; r < rows; r += TRUNC_CHUNK)
-                    vtc.push_back(TChunk{(int)(vte.size() - ln.tr_e0), side, r,
+                    vtc.push_back(TChunk{(int)(vte.size() - ln.e0), side, r,
                                          (int)std::min<long long>(TRUNC_CHUNK, rows - r)});
             }
-            te.c_hi = (int)vtc.size() - ln.tr_c0;
+            te.c_hi = (int)vtc.size() - ln.c0;
             te.gofs = gofs;
             gofs += (long long)(te.c_hi - te.c_lo) * e.k * e.k;
             te.tofs = tofs;
             tofs += 2LL * e.k * rmax;
-            ln.tr_kmax = std::max(ln.tr_kmax, e.k);
+            ln.kmax = std::max(ln.kmax, e.k);
             vte.push_back(te);
         }
-        ln.tr_ne = (int)vte.size() - ln.tr_e0;
-        ln.tr_nc = (int)vtc.size() - ln.tr_c0;
+        ln.ne = (int)vte.size() - ln.e0;
+        ln.nc = (int)vtc.size() - ln.c0;
     };
     auto put_gemm = [&](const std::vector<VTask>& v, H2Launch& ln, int which) {
         ln.g_tile0[which] = (int)vtile.size();
@@ -872,11 +933,10 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
     auto put_panel = [&](const std::vector<VPanel>& v, H2Launch& ln) {
         ln.pan0 = (int)vpan.size();
         for (auto& p : v) {
-            const HBlock& D = S.bl[p.diag];
             for (int c0 = 0; c0 < p.nvec; c0 += H2_STRIP) {
                 H2Panel d;
-                d.T = A + offD[p.diag];
-                d.ldt = D.m;
+                d.T = res(p.T);
+                d.ldt = p.ldt;
                 const int nv = std::min(H2_STRIP, p.nvec - c0);
                 d.X = res(p.X) + (p.mode == 2 ? c0 : c0 * p.ldx);
                 d.ldx = p.ldx;
@@ -914,15 +974,16 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
                 if (hb.n > 0 && R > 0) vcp[q++].src = hm->lr.p + hb.off + hb.m * hb.kcap;
             }
         }
-        put_trunc(init_trunc, P->init);
+        put_trunc(init_trunc, P->init.tr);
     }
     P->steps.resize(nl);
     for (int k = 0; k < nl; ++k) {
         H2Launch& ln = P->steps[k];
         VStep& st = steps[k];
-        put_trunc(st.trunc, ln);
+        put_trunc(st.trunc, ln.tr);
+        put_trunc(st.trunc_ov, ln.tr_ov);
         ln.lu = (int)vlu.size();
-        vlu.push_back({A + offD[st.lu_blk], S.bl[st.lu_blk].m, lm(k)});
+        vlu.push_back({A + offD[st.lu_blk] + st.lu_off, S.bl[st.lu_blk].m, lm(k)});
         put_panel(st.panel, ln);
         put_gemm(st.g0, ln, 3);
         put_gemm(st.g1, ln, 0);
@@ -930,19 +991,48 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         put_copy(st.cp, ln);
         put_gemm(st.g3, ln, 2);
     }
-    // final: explicit inverses of the leaf factors (for the substitutions)
+    // final: explicit inverses of the leaf factors (for the substitutions).  Tile
+    // inverses on the diagonal, then the off-diagonal tiles level by level:
+    //   L^{-1}(i,j) = -Linv(i,i) sum_{k=j}^{i-1} L(i,k) L^{-1}(k,j)       (i > j)
+    //   U^{-1}(i,j) = -Uinv(i,i) sum_{k=i+1}^{j} U(i,k) U^{-1}(k,j)       (i < j)
     {
         std::vector<VCopy> c;
         std::vector<VPanel> pv;
         for (int q = 0; q < nl; ++q) {
-            const int d = own(q, q);
-            c.push_back({{4, q, 0}, {4, q, 0}, lm(q), lm(q), lm(q), lm(q), 2, 1.0});
-            c.push_back({{5, q, 0}, {5, q, 0}, lm(q), lm(q), lm(q), lm(q), 2, 1.0});
-            pv.push_back({d, {4, q, 0}, lm(q), lm(q), lm(q), 0});
-            pv.push_back({d, {5, q, 0}, lm(q), lm(q), lm(q), 2});
+            const int d = own(q, q), f = leaf_of[q];
+            const VRef Tq{0, d, toff(d, q, q)};
+            c.push_back({{4, f, 0}, {4, f, ioff(f, q, q)}, 0, lfm(f), lm(q), lm(q), 2, 1.0});
+            c.push_back({{5, f, 0}, {5, f, ioff(f, q, q)}, 0, lfm(f), lm(q), lm(q), 2, 1.0});
+            pv.push_back({Tq, S.bl[d].m, {4, f, ioff(f, q, q)}, lfm(f), lm(q), lm(q), 0});
+            pv.push_back({Tq, S.bl[d].m, {5, f, ioff(f, q, q)}, lfm(f), lm(q), lm(q), 2});
         }
         put_copy(c, P->fin);
         put_panel(pv, P->fin);
+        P->fin_lv.resize(std::max(0, maxnt - 1));
+        for (int dd = 1; dd < maxnt; ++dd) {
+            std::vector<VTask> tt, tx;
+            int64_t scr = 0;
+            for (int f = 0; f < nleaf; ++f) {
+                const int d = own(lq0[f], lq0[f]);
+                const int64_t md = S.bl[d].m, mf = lfm(f);
+                for (int i = lq0[f]; i <= lq1[f]; ++i)
+                    for (int j = lq0[f]; j <= lq1[f]; ++j) {
+                        if (std::abs(i - j) != dd) continue;
+                        const bool low = i > j;
+                        const int sp = low ? 4 : 5;
+                        VTask t{{3, 0, scr}, lm(i), lm(i), lm(j), 0.0, {}};
+                        for (int k = low ? j : i + 1; k <= (low ? i - 1 : j); ++k)
+                            t.terms.push_back({{0, d, toff(d, i, k)}, {sp, f, ioff(f, k, j)}, md, mf, lm(k), 0, 0, 1.0});
+                        tt.push_back(t);
+                        VTask x{{sp, f, ioff(f, i, j)}, mf, lm(i), lm(j), 0.0, {}};
+                        x.terms.push_back({{sp, f, ioff(f, i, i)}, {3, 0, scr}, mf, lm(i), lm(i), 0, 0, -1.0});
+                        tx.push_back(x);
+                        scr += (int64_t)lm(i) * lm(j);
+                    }
+            }
+            put_gemm(tt, P->fin_lv[dd - 1], 0);
+            put_gemm(tx, P->fin_lv[dd - 1], 1);
+        }
     }
     const double ms_flat = ms_since(t_flat0);
     P->lu.upload(vlu.data(), vlu.size(), s);
@@ -961,66 +1051,83 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
                 nl, nb, ms_sim, ms_alloc, ms_flat, L->plan_ms - ms_sim - ms_alloc - ms_flat, vtile.size(),
                 vterm.size(), vcp.size(), vpan.size(), vte.size());
     // ---- execute
-    const int pan_smem = (H2_MMAX + H2_STRIP) * (H2_MMAX + 1) * (int)sizeof(double);
+    const int pan_smem = (H2_MMAX + H2_STRIP) * (H2_MMAX + 2) * (int)sizeof(double);
     set_smem_once((const void*)k_h2_panel, pan_smem);
-    set_smem_once((const void*)k_h2_lu, H2_MMAX * H2_MMAX * (int)sizeof(double));
     int nlaunch = 0;
+    // two streams: the truncations of step k (stream sb) overlap the diagonal LU of
+    // step k (stream sa); sa waits for the operand truncations before the panels and
+    // for the overflow truncations before this step's new low-rank columns.
+    cudaStream_t sa = s, sb = aux_stream(L->h);
+    cudaEvent_t evA = L->h->ev_aux[0], evOp = L->h->ev_aux[1], evOv = L->h->ev_aux[2];
     auto run_copy = [&](const H2Launch& ln) {
         if (!ln.ncp) return;
-        k_h2_copy<<<ln.ncp, 256, 0, s>>>(P->cps.p + ln.cp0);
+        k_h2_copy<<<ln.ncp, 256, 0, sa>>>(P->cps.p + ln.cp0);
         FDE_CHECK_LAUNCH();
         ++nlaunch;
     };
-    auto run_trunc = [&](const H2Launch& ln) {
-        if (!ln.tr_ne) return;
-        const TEntry* E = P->te.p + ln.tr_e0;
-        const TChunk* C = P->tc.p + ln.tr_c0;
-        k_bgram<<<ln.tr_nc, 256, 0, s>>>(E, C, P->tr_part);
+    auto run_trunc = [&](const H2Trunc& tr, cudaStream_t st) {
+        if (!tr.ne) return;
+        const TEntry* E = P->te.p + tr.e0;
+        const TChunk* C = P->tc.p + tr.c0;
+        k_bgram<<<tr.nc, 256, 0, st>>>(E, C, P->tr_part);
         FDE_CHECK_LAUNCH();
-        const int kmax = ln.tr_kmax, ne = (kmax + 1) & ~1;
+        const int kmax = tr.kmax, ne = (kmax + 1) & ~1;
         const size_t smem = (size_t)(2 * kmax * kmax + 3 * ne * ne + 2 * ne + 8) * sizeof(double);
         set_smem_once((const void*)k_bcore, (int)smem);
-        k_bcore<<<ln.tr_ne, 256, smem, s>>>(E, C, P->tr_part, L->tol, rmax, P->tr_T, L->dflag.p + 1);
+        k_bcore<<<tr.ne, 256, smem, st>>>(E, C, P->tr_part, L->tol, rmax, P->tr_T, L->dflag.p + 1);
         FDE_CHECK_LAUNCH();
         const size_t asmem = (size_t)(kmax * rmax + TRUNC_CHUNK * kmax) * sizeof(double);
         set_smem_once((const void*)k_bapply, (int)asmem);
-        k_bapply<<<ln.tr_nc, 256, asmem, s>>>(E, C, P->tr_T, rmax);
+        k_bapply<<<tr.nc, 256, asmem, st>>>(E, C, P->tr_T, rmax);
         FDE_CHECK_LAUNCH();
         nlaunch += 3;
     };
     auto run_gemm = [&](const H2Launch& ln, int w) {
         if (!ln.g_ntile[w]) return;
-        k_h2_gemm<<<ln.g_ntile[w], 256, 0, s>>>(P->tiles.p + ln.g_tile0[w], P->tasks.p, P->terms.p);
+        k_h2_gemm<<<ln.g_ntile[w], 256, 0, sa>>>(P->tiles.p + ln.g_tile0[w], P->tasks.p, P->terms.p);
         FDE_CHECK_LAUNCH();
         ++nlaunch;
     };
     auto run_panel = [&](const H2Launch& ln) {
         if (!ln.npan) return;
-        k_h2_panel<<<ln.npan, 256, pan_smem, s>>>(P->pan.p + ln.pan0);
+        k_h2_panel<<<ln.npan, 256, pan_smem, sa>>>(P->pan.p + ln.pan0);
         FDE_CHECK_LAUNCH();
         ++nlaunch;
     };
-    FDE_CUDA(cudaMemsetAsync(A + lr_lo, 0, (size_t)(lr_hi - lr_lo) * sizeof(double), s));
+    FDE_CUDA(cudaMemsetAsync(A + lr_lo, 0, (size_t)(lr_hi - lr_lo) * sizeof(double), sa));
     run_copy(P->init);
-    run_trunc(P->init);
+    run_trunc(P->init.tr, sa);
+    FDE_CUDA(cudaEventRecord(evA, sa));
     const int kstop = g_hlu2_stop >= 0 ? std::min(g_hlu2_stop, nl) : nl;   // debug: partial sweep
     for (int k = 0; k < kstop; ++k) {
         const H2Launch& ln = P->steps[k];
-        run_trunc(ln);
-        k_h2_lu<<<1, 512, lm(k) * lm(k) * sizeof(double), s>>>(P->lu.p + ln.lu, L->dflag.p);
+        FDE_CUDA(cudaStreamWaitEvent(sb, evA, 0));
+        run_trunc(ln.tr, sb);
+        FDE_CUDA(cudaEventRecord(evOp, sb));
+        run_trunc(ln.tr_ov, sb);
+        FDE_CUDA(cudaEventRecord(evOv, sb));
+        k_h2_lu<<<1, 1024, 0, sa>>>(P->lu.p + ln.lu, L->dflag.p);
         FDE_CHECK_LAUNCH();
         ++nlaunch;
+        FDE_CUDA(cudaStreamWaitEvent(sa, evOp, 0));
         run_panel(ln);
         run_gemm(ln, 0);
         run_gemm(ln, 1);
         run_gemm(ln, 3);   // conversions to dense (after the products: a block may be
                            // an operand (row / column k) and a target (rows > k) at once)
+        FDE_CUDA(cudaStreamWaitEvent(sa, evOv, 0));
         run_copy(ln);
         run_gemm(ln, 2);
+        FDE_CUDA(cudaEventRecord(evA, sa));
     }
     if (kstop == nl) {
+        FDE_CUDA(cudaMemsetAsync(A + inv_lo, 0, (size_t)(inv_hi - inv_lo) * sizeof(double), sa));
         run_copy(P->fin);
         run_panel(P->fin);
+        for (auto& lv : P->fin_lv) {
+            run_gemm(lv, 0);
+            run_gemm(lv, 1);
+        }
     }
     L->nops = nlaunch;
 
@@ -1044,10 +1151,12 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
             L->max_rank = std::max(L->max_rank, kc[b]);
         }
     }
-    for (int q = 0; q < nl; ++q) {
-        LBlk& d = L->B[own(q, q)];
-        d.Li = A + offLi[q];
-        d.Ui = A + offUi[q];
+    for (int f = 0; f < nleaf; ++f) {
+        LBlk& d = L->B[own(lq0[f], lq0[f])];   // the dense diagonal block of leaf f
+        d.Li = A + offLi[f];
+        d.Ui = A + offUi[f];
     }
     return true;
 }
+
+

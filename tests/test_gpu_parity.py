@@ -197,6 +197,8 @@ HLU2_CASES = HLU_CASES + [
     (fi.config4(N=96, P=8), 4),          # 24 leaves of 32 dofs: several low-rank levels
     (fi.config2(1.3, N=64, P=8), 16),    # leaves of exactly 128 dofs (kernel limit)
     (fi.config4(N=44, P=6), 5),          # leaves at two depths (dense blocks spanning two leaves)
+    (fi.config4(N=128, P=8), 40),        # 256-dof leaves: two sweep tiles per leaf
+    (fi.config3(P=12), 16),              # geometric layers, 192-dof leaves (two tiles of 96)
 ]
 
 
@@ -239,15 +241,20 @@ def test_hlu_preconditioned_gmres_matches_oracle(fde, h, case, hlu_mode):
     hm = fde.hmatrix_build(h, op, p.R, 1.0, n_min)
     lu = fde.hlu_factor(h, hm, 1e-3)
     G = fde.sem_rhs(h, op, p.forcings)
-    X, rep = fde.solve(h, op, lu, G, tol=1e-13)
-    X0, rep0 = fde.solve(h, op, None, G, tol=1e-13, maxiter=5000, restart=200)
+    X, rep = fde.solve(h, op, lu, G, tol=1e-12)   # BASELINE: GMRES tol 1e-12
+    try:
+        X0, rep0 = fde.solve(h, op, None, G, tol=1e-12, maxiter=3000, restart=200)
+        its0 = rep0.iterations
+    except fde.FdeError as e:   # ill-conditioned cases (c3: kappa ~ 1e11) need the preconditioner
+        assert e.name == "FDE_EMAXITER"
+        its0 = 10 ** 9
     so = oracle_system(p)
     Xo = O.solve_dense(so.A, O.rhs(p, so, p.forcings[0]))
     x = X.cpu().numpy()[0]
     D = np.abs(np.diag(so.A))
     err = np.sqrt(np.sum(D * (x - Xo) ** 2) / np.sum(D * Xo ** 2))
     assert err <= 1e-9, err
-    assert rep.iterations < rep0.iterations
+    assert rep.iterations < its0
     # the factor approximates A~: ||A~ z - r|| small relative to ||r||
     At, _ = O.hmatrix_dense(p, so, R=p.R, lam=1.0, n_min=n_min)
     r = np.random.default_rng(6).standard_normal(p.n)

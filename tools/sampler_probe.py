@@ -38,6 +38,9 @@ def timed(k=4):
 for _ in range(3):
     step()
 print(f"no sampler      {timed():.1f} ms/step")
+fde.lib().fde_profile(h.h, 1)
+print(f"profiling on    {timed():.1f} ms/step")
+fde.lib().fde_profile(h.h, 0)
 s = bench.ClockSampler(0)
 s.start()
 print(f"nvidia-smi      {timed():.1f} ms/step", s.stop())
