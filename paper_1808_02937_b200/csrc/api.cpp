@@ -91,7 +91,9 @@ void fde_destroy(fde_handle h)
     if (h->ev1) cudaEventDestroy(h->ev1);
     if (h->aux) {
         cudaStreamSynchronize(h->aux);
+        cudaStreamSynchronize(h->aux2);
         cudaStreamDestroy(h->aux);
+        cudaStreamDestroy(h->aux2);
         for (auto e : h->ev_aux) cudaEventDestroy(e);
     }
     if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);

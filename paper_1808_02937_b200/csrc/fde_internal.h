@@ -103,17 +103,23 @@ struct fde_ctx {
     int num_sms = 148;
     // auxiliary stream + events for work that overlaps the caller's stream
     // (created on first use; ordered by events, never by implicit synchronisation)
-    cudaStream_t aux = nullptr;
-    cudaEvent_t ev_aux[3] = {nullptr, nullptr, nullptr};
+    cudaStream_t aux = nullptr, aux2 = nullptr;
+    cudaEvent_t ev_aux[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
 };
 
 inline cudaStream_t aux_stream(fde_ctx* h)
 {
     if (!h->aux) {
         FDE_CUDA(cudaStreamCreateWithFlags(&h->aux, cudaStreamNonBlocking));
+        FDE_CUDA(cudaStreamCreateWithFlags(&h->aux2, cudaStreamNonBlocking));
         for (auto& e : h->ev_aux) FDE_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
     return h->aux;
+}
+inline cudaStream_t aux_stream2(fde_ctx* h)
+{
+    aux_stream(h);
+    return h->aux2;
 }
 
 // ------------------------------------------------------- quadrature tables

@@ -77,87 +77,77 @@ struct H2Copy {   // kind 0: dst = alpha src, 1: dst = 0, 2: dst = I
 };
 
 // ----------------------------------------------------------------- kernels
-// LU without pivoting of an m x m tile (m <= 128) held in registers: thread t
-// owns row i = t % 128 and the columns j = g + 8q (g = t / 128, q = 0..15).  The
-// pivot row and the pivot column of step k+1 are published (double-buffered
-// shared memory) by their owners right after their step-k update, so every
-// pivot step costs one barrier.  Register indices must be compile-time
-// constants: the column loops start at q0 = k / 8 through a switch.
-template <int Q0>
-__device__ __forceinline__ void h2_lu_update(double (&a)[16], double l, const double* row, int g, int k)
-{
-    // q = Q0 may hold columns <= k (g + 8 Q0 <= k): masked; q > Q0 are all > k
-    a[Q0] = fma((g + 8 * Q0 > k) ? -l : 0.0, row[g + 8 * Q0], a[Q0]);
-#pragma unroll
-    for (int q = Q0 + 1; q < 16; ++q) a[q] = fma(-l, row[g + 8 * q], a[q]);
-}
-
-#define H2_SW16(sel, STMT) \
-    switch (sel) {         \
-        case 0: STMT(0); break;   case 1: STMT(1); break;   case 2: STMT(2); break;   case 3: STMT(3); break;   \
-        case 4: STMT(4); break;   case 5: STMT(5); break;   case 6: STMT(6); break;   case 7: STMT(7); break;   \
-        case 8: STMT(8); break;   case 9: STMT(9); break;   case 10: STMT(10); break; case 11: STMT(11); break; \
-        case 12: STMT(12); break; case 13: STMT(13); break; case 14: STMT(14); break; default: STMT(15); break; \
-    }
-
-__global__ void __launch_bounds__(1024) k_h2_lu(const H2Lu* tk, int* bad)
-{
-    const H2Lu d = tk[blockIdx.x];
-    __shared__ double sRow[2][H2_MMAX], sCol[2][H2_MMAX];
-    const int m = d.m, i = threadIdx.x & 127, g = threadIdx.x >> 7;
-    double a[16];
-#pragma unroll
-    for (int q = 0; q < 16; ++q) {
-        const int j = g + 8 * q;
-        a[q] = (i < m && j < m) ? d.D[(long long)j * d.ld + i] : 0.0;
-    }
-    if (i == 0)
-#pragma unroll
-        for (int q = 0; q < 16; ++q) sRow[0][g + 8 * q] = a[q];
-    if (g == 0) sCol[0][i] = a[0];
-    __syncthreads();
-    for (int k = 0; k < m; ++k) {
-        const int b = k & 1;
-        const double piv = sRow[b][k];
-        if (threadIdx.x == 0 && (!(fabs(piv) > 0.0) || !isfinite(piv))) *bad = 1;
-        if (i > k && i < m) {
-            const double l = sCol[b][i] / piv;
-            if (g == (k & 7)) {
-#define H2_SETL(Q) a[Q] = l
-                H2_SW16(k >> 3, H2_SETL)
-#undef H2_SETL
-            }
-            const double* row = sRow[b];
-#pragma unroll
-            for (int q = 0; q < 16; ++q) {   // branch-free: columns <= k get a zero multiplier
-                const double lq = (g + 8 * q > k) ? -l : 0.0;
-                a[q] = fma(lq, row[g + 8 * q], a[q]);
-            }
-            if (i == k + 1) {   // entries <= k of the published row are never read
-#pragma unroll
-                for (int q = 0; q < 16; ++q) sRow[b ^ 1][g + 8 * q] = a[q];
-            }
-            if (g == ((k + 1) & 7)) {
-#define H2_PUBC(Q) sCol[b ^ 1][i] = a[Q]
-                H2_SW16((k + 1) >> 3, H2_PUBC)
-#undef H2_PUBC
-            }
-        }
-        __syncthreads();
-    }
-#pragma unroll
-    for (int q = 0; q < 16; ++q) {
-        const int j = g + 8 * q;
-        if (i < m && j < m) d.D[(long long)j * d.ld + i] = a[q];
-    }
-}
-
 __device__ __forceinline__ void cp_async8(double* sdst, const double* gsrc)
 {
     const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gsrc));
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
+
+// LU without pivoting of an m x m tile (m <= 128), right-looking in shared memory
+// with all 512 threads: thread (ti, tj) updates rows k+1+ti+32a and columns
+// k+1+tj+16b of the trailing matrix; the multipliers of column k are scaled one
+// step late (nobody reads the column any more); one barrier per pivot.  The tile is
+// padded to 128 x 128 with the identity (the factors of diag(A, I) are diag(L, I),
+// diag(U, I)), so the leading dimension is a compile-time constant and no
+// element needs a bounds check.  (Measured against blocked / register-resident
+// variants in tools/mb_lu.cu: this one is the fastest, ~130 us for m = 128.)
+__global__ void __launch_bounds__(512) k_h2_lu(const H2Lu* tk, int* bad)
+{
+    constexpr int LD = H2_MMAX + 1, M = H2_MMAX;
+    extern __shared__ double lsm[];
+    const H2Lu d = tk[blockIdx.x];
+    const int m = d.m, tid = threadIdx.x, ti = tid & 31, tj = tid >> 5;
+    double* S = lsm;
+    __shared__ double rp[M];
+    for (int t = tid; t < M * M; t += 512) {
+        const int i = t & (M - 1), j = t / M;
+        if (i < m && j < m) cp_async8(S + j * LD + i, d.D + (long long)j * d.ld + i);
+        else S[j * LD + i] = (i == j) ? 1.0 : 0.0;
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    if (tid == 0) {
+        const double p0 = S[0];
+        if (!(fabs(p0) > 0.0) || !isfinite(p0)) *bad = 1;
+        rp[0] = 1.0 / p0;
+    }
+    __syncthreads();
+    for (int k = 0; k < M - 1; ++k) {
+        const double rpk = rp[k];
+        if (k > 0 && tj == 0)
+            for (int i = k + ti; i < M; i += 32) S[(k - 1) * LD + i] *= rp[k - 1];
+        const int i0 = k + 1 + ti, j0 = k + 1 + tj;
+        double* base = S + j0 * LD + i0;
+        const double* colk = S + k * LD + i0;
+        const double* rowk = S + j0 * LD + k;
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+            if (k + 1 + 32 * a < M) {   // warp-uniform
+                const double l = (i0 + 32 * a < M) ? colk[32 * a] * rpk : 0.0;
+#pragma unroll
+                for (int b = 0; b < 8; ++b) {
+                    if (j0 + 16 * b < M && i0 + 32 * a < M) {
+                        const double u = rowk[16 * b * LD];
+                        base[16 * b * LD + 32 * a] = fma(-l, u, base[16 * b * LD + 32 * a]);
+                    }
+                }
+            }
+        }
+        if (tid == 0) {   // (k+1, k+1) is updated by thread 0
+            const double pn = S[(k + 1) * LD + k + 1];
+            if (k + 1 < m && (!(fabs(pn) > 0.0) || !isfinite(pn))) *bad = 1;
+            rp[k + 1] = 1.0 / pn;
+        }
+        __syncthreads();
+    }
+    if (tid == 0) S[(M - 2) * LD + M - 1] *= rp[M - 2];
+    __syncthreads();
+    for (int t = tid; t < m * m; t += 512) {
+        const int i = t % m, j = t / m;
+        d.D[(long long)j * d.ld + i] = S[j * LD + i];
+    }
+}
 
 // One CTA per strip of <= 32 vectors.  The packed LU tile T (m x m) and the strip
 // are staged in shared memory with asynchronous copies; T' (lower) is read from
@@ -408,6 +398,8 @@ struct VStep {
     int64_t lu_off = 0;
     std::vector<VPanel> panel;
     std::vector<VTask> g0, g1, g2, g3;   // conversions to dense, cores, products, dense updates
+    std::vector<VTask> g3r;              // dense updates of tiles off row / column k+1 (lookahead stream)
+    std::vector<char> g3crit;            // per g3 task: tile in row or column k+1
     std::vector<VCopy> cp;           // low-rank target columns
     int64_t scratch = 0;
 };
@@ -419,7 +411,7 @@ struct H2Launch {      // ranges in the flat device arrays
     H2Trunc tr, tr_ov;
     int lu = -1;
     int pan0 = 0, npan = 0;
-    int g_tile0[4] = {0, 0, 0, 0}, g_ntile[4] = {0, 0, 0, 0};
+    int g_tile0[5] = {0, 0, 0, 0, 0}, g_ntile[5] = {0, 0, 0, 0, 0};
     int cp0 = 0, ncp = 0;
 };
 
@@ -699,6 +691,7 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
                                 tile_task[key] = ti;
                                 VTask tk{{0, t, (lr0[j] - col0(t)) * T.m + (lr0[i] - row0(t))}, T.m, lm(i), lm(j), 1.0, {}};
                                 st.g3.push_back(tk);
+                                st.g3crit.push_back(i == k + 1 || j == k + 1);
                             } else {
                                 ti = tile_task[key];
                             }
@@ -989,7 +982,12 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         put_gemm(st.g1, ln, 0);
         put_gemm(st.g2, ln, 1);
         put_copy(st.cp, ln);
-        put_gemm(st.g3, ln, 2);
+        {   // split the dense updates: row / column k+1 (needed by step k+1) vs the rest
+            std::vector<VTask> crit, rest;
+            for (size_t q = 0; q < st.g3.size(); ++q) (st.g3crit[q] ? crit : rest).push_back(std::move(st.g3[q]));
+            put_gemm(crit, ln, 2);
+            put_gemm(rest, ln, 4);
+        }
     }
     // final: explicit inverses of the leaf factors (for the substitutions).  Tile
     // inverses on the diagonal, then the off-diagonal tiles level by level:
@@ -1053,15 +1051,20 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
     // ---- execute
     const int pan_smem = (H2_MMAX + H2_STRIP) * (H2_MMAX + 2) * (int)sizeof(double);
     set_smem_once((const void*)k_h2_panel, pan_smem);
+    const int lu_smem = H2_MMAX * (H2_MMAX + 1) * (int)sizeof(double);   // padded 128 x 129
+    set_smem_once((const void*)k_h2_lu, lu_smem);
     int nlaunch = 0;
-    // two streams: the truncations of step k (stream sb) overlap the diagonal LU of
-    // step k (stream sa); sa waits for the operand truncations before the panels and
-    // for the overflow truncations before this step's new low-rank columns.
-    cudaStream_t sa = s, sb = aux_stream(L->h);
+    // three streams.  sa: the critical chain LU(k) -> panels -> products ->
+    // conversions -> dense updates of row / column k+1 (needed by step k+1);
+    // sb: truncations (operands before the panels, overflowing targets before the
+    // new columns) and the new low-rank columns; sc: the remaining dense updates of
+    // step k, which overlap LU(k+1) and the panels of step k+1 (lookahead).
+    cudaStream_t sa = s, sb = aux_stream(L->h), sc = aux_stream2(L->h);
     cudaEvent_t evA = L->h->ev_aux[0], evOp = L->h->ev_aux[1], evOv = L->h->ev_aux[2];
-    auto run_copy = [&](const H2Launch& ln) {
+    cudaEvent_t evP = L->h->ev_aux[3], evC = L->h->ev_aux[4], evB = L->h->ev_aux[5];
+    auto run_copy = [&](const H2Launch& ln, cudaStream_t st) {
         if (!ln.ncp) return;
-        k_h2_copy<<<ln.ncp, 256, 0, sa>>>(P->cps.p + ln.cp0);
+        k_h2_copy<<<ln.ncp, 256, 0, st>>>(P->cps.p + ln.cp0);
         FDE_CHECK_LAUNCH();
         ++nlaunch;
     };
@@ -1082,9 +1085,9 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         FDE_CHECK_LAUNCH();
         nlaunch += 3;
     };
-    auto run_gemm = [&](const H2Launch& ln, int w) {
+    auto run_gemm = [&](const H2Launch& ln, int w, cudaStream_t st) {
         if (!ln.g_ntile[w]) return;
-        k_h2_gemm<<<ln.g_ntile[w], 256, 0, sa>>>(P->tiles.p + ln.g_tile0[w], P->tasks.p, P->terms.p);
+        k_h2_gemm<<<ln.g_ntile[w], 256, 0, st>>>(P->tiles.p + ln.g_tile0[w], P->tasks.p, P->terms.p);
         FDE_CHECK_LAUNCH();
         ++nlaunch;
     };
@@ -1095,38 +1098,50 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         ++nlaunch;
     };
     FDE_CUDA(cudaMemsetAsync(A + lr_lo, 0, (size_t)(lr_hi - lr_lo) * sizeof(double), sa));
-    run_copy(P->init);
+    run_copy(P->init, sa);
     run_trunc(P->init.tr, sa);
     FDE_CUDA(cudaEventRecord(evA, sa));
+    FDE_CUDA(cudaStreamWaitEvent(sb, evA, 0));
+    FDE_CUDA(cudaStreamWaitEvent(sc, evA, 0));
+    FDE_CUDA(cudaEventRecord(evC, sc));
     const int kstop = g_hlu2_stop >= 0 ? std::min(g_hlu2_stop, nl) : nl;   // debug: partial sweep
     for (int k = 0; k < kstop; ++k) {
         const H2Launch& ln = P->steps[k];
-        FDE_CUDA(cudaStreamWaitEvent(sb, evA, 0));
+        // sb (after the new columns of step k-1 and the panels of step k-1)
         run_trunc(ln.tr, sb);
         FDE_CUDA(cudaEventRecord(evOp, sb));
         run_trunc(ln.tr_ov, sb);
-        FDE_CUDA(cudaEventRecord(evOv, sb));
-        k_h2_lu<<<1, 1024, 0, sa>>>(P->lu.p + ln.lu, L->dflag.p);
+        // sa: critical chain
+        k_h2_lu<<<1, 512, lu_smem, sa>>>(P->lu.p + ln.lu, L->dflag.p);
         FDE_CHECK_LAUNCH();
         ++nlaunch;
         FDE_CUDA(cudaStreamWaitEvent(sa, evOp, 0));
         run_panel(ln);
-        run_gemm(ln, 0);
-        run_gemm(ln, 1);
-        run_gemm(ln, 3);   // conversions to dense (after the products: a block may be
-                           // an operand (row / column k) and a target (rows > k) at once)
-        FDE_CUDA(cudaStreamWaitEvent(sa, evOv, 0));
-        run_copy(ln);
-        run_gemm(ln, 2);
-        FDE_CUDA(cudaEventRecord(evA, sa));
+        run_gemm(ln, 0, sa);
+        run_gemm(ln, 1, sa);
+        run_gemm(ln, 3, sa);   // conversions to dense (after the products: a block may be
+                               // an operand (row / column k) and a target (rows > k) at once)
+        FDE_CUDA(cudaEventRecord(evP, sa));
+        FDE_CUDA(cudaStreamWaitEvent(sa, evC, 0));   // remaining updates of step k-1
+        run_gemm(ln, 2, sa);                         // row / column k+1
+        // sb: new low-rank columns of step k (after the overflow truncations)
+        FDE_CUDA(cudaStreamWaitEvent(sb, evP, 0));
+        run_copy(ln, sb);
+        // sc: the other dense updates of step k
+        FDE_CUDA(cudaStreamWaitEvent(sc, evP, 0));
+        run_gemm(ln, 4, sc);
+        FDE_CUDA(cudaEventRecord(evC, sc));
     }
+    FDE_CUDA(cudaEventRecord(evB, sb));
+    FDE_CUDA(cudaStreamWaitEvent(sa, evB, 0));
+    FDE_CUDA(cudaStreamWaitEvent(sa, evC, 0));
     if (kstop == nl) {
         FDE_CUDA(cudaMemsetAsync(A + inv_lo, 0, (size_t)(inv_hi - inv_lo) * sizeof(double), sa));
-        run_copy(P->fin);
+        run_copy(P->fin, sa);
         run_panel(P->fin);
         for (auto& lv : P->fin_lv) {
-            run_gemm(lv, 0);
-            run_gemm(lv, 1);
+            run_gemm(lv, 0, sa);
+            run_gemm(lv, 1, sa);
         }
     }
     L->nops = nlaunch;
