@@ -227,7 +227,9 @@ def run_ours(args):
         torch.cuda.synchronize()
 
     # ---- device-timed region: K cold solves
-    clocks = ClockSampler(local)
+    # in-process NVML sampling (an nvidia-smi subprocess polling at 100 ms stalled
+    # some steps of this host-launch-heavy path by ~100 ms); FDE_CLOCKS=smi selects it
+    clocks = ClockSampler(local) if os.environ.get("FDE_CLOCKS") == "smi" else NvmlSampler(local)
     clocks.start()
     fde.lib().fde_profile(h.h, 1)
     barrier()
@@ -255,14 +257,15 @@ def run_ours(args):
 
     # ---- end-to-end through the C-ABI with host buffers (forcing from host, X to host)
     barrier()
-    t0 = torch.cuda.Event(enable_timing=True)
-    t1 = torch.cuda.Event(enable_timing=True)
-    t0.record(stream)
-    for _ in range(max(1, args.steps // 2)):
+    ne = max(1, args.steps // 2)
+    ee = [torch.cuda.Event(enable_timing=True) for _ in range(ne + 1)]
+    ee[0].record(stream)
+    for q in range(ne):
         _, Xh = step(e2e=True)
-    t1.record(stream)
+        ee[q + 1].record(stream)
     barrier()
-    ms_e2e = t0.elapsed_time(t1) / max(1, args.steps // 2)
+    e2e_each = [ee[q].elapsed_time(ee[q + 1]) for q in range(ne)]
+    ms_e2e = ee[0].elapsed_time(ee[-1]) / ne
     if world > 1:
         t = torch.tensor([ms_e2e], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -323,7 +326,7 @@ def run_ours(args):
             "precond_apply": {"launches": int(pre_n), "avg_us": (pre_ms / pre_n * 1e3) if pre_n else None,
                               "share_of_step": pre_ms / ms if ms else None},
             "e2e": {"value": nrhs / (ms_e2e / 1e3), "unit": "solves/s", "h2d_bytes_per_step": int(h2d),
-                    "d2h_bytes_per_step": int(8 * prob.n * nrhs)},
+                    "d2h_bytes_per_step": int(8 * prob.n * nrhs), "step_ms_each": [round(v, 2) for v in e2e_each]},
             "gpu_launches": int(launches),
             "clocks": clk,
         }

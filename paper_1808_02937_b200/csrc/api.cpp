@@ -89,6 +89,7 @@ void fde_destroy(fde_handle h)
     comm_destroy(h);
     if (h->ev0) cudaEventDestroy(h->ev0);
     if (h->ev1) cudaEventDestroy(h->ev1);
+    if (h->pinned) cudaFreeHost(h->pinned);
     if (h->aux) {
         cudaStreamSynchronize(h->aux);
         cudaStreamSynchronize(h->aux2);

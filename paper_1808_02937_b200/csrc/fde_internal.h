@@ -103,9 +103,16 @@ struct fde_ctx {
     int num_sms = 148;
     // auxiliary stream + events for work that overlaps the caller's stream
     // (created on first use; ordered by events, never by implicit synchronisation)
+    int* pinned = nullptr;   // small page-locked read-back buffer (allocated once per handle)
     cudaStream_t aux = nullptr, aux2 = nullptr;
     cudaEvent_t ev_aux[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
 };
+
+inline int* ctx_pinned(fde_ctx* h)
+{
+    if (!h->pinned) FDE_CUDA(cudaMallocHost(&h->pinned, sizeof(int) * 16));
+    return h->pinned;
+}
 
 inline cudaStream_t aux_stream(fde_ctx* h)
 {

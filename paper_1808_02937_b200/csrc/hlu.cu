@@ -1651,7 +1651,7 @@ fde_lu* hlu_build(fde_ctx* h, fde_hm* hm, double tol)
         L->S = hm->S;
         L->tol = tol;
         L->rmax = std::max(16, hm->R);   // rank capacity of the truncated blocks
-        FDE_CUDA(cudaMallocHost(&L->pinned, sizeof(int) * 4));
+        L->pinned = ctx_pinned(h);   // owned by the handle (no page locking per factorisation)
         L->dflag.alloc(4);
         L->dflag.zero(h->stream);
         FDE_CUDA(cudaEventRecord(h->ev0, h->stream));
@@ -1737,7 +1737,6 @@ void hlu_destroy(fde_lu* L)
         if (b.Ui) cudaFreeAsync(b.Ui, s);
     }
     if (s) cudaStreamSynchronize(s);
-    if (L->pinned) cudaFreeHost(L->pinned);
     apply_sched_free(L->ap);
     delete L;
 }
