@@ -90,11 +90,14 @@ void fde_destroy(fde_handle h)
     if (h->ev0) cudaEventDestroy(h->ev0);
     if (h->ev1) cudaEventDestroy(h->ev1);
     if (h->pinned) cudaFreeHost(h->pinned);
+    if (h->stage) cudaFreeHost(h->stage);
     if (h->aux) {
         cudaStreamSynchronize(h->aux);
         cudaStreamSynchronize(h->aux2);
+        cudaStreamSynchronize(h->aux3);
         cudaStreamDestroy(h->aux);
         cudaStreamDestroy(h->aux2);
+        cudaStreamDestroy(h->aux3);
         for (auto e : h->ev_aux) cudaEventDestroy(e);
     }
     if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);

@@ -104,9 +104,28 @@ struct fde_ctx {
     // auxiliary stream + events for work that overlaps the caller's stream
     // (created on first use; ordered by events, never by implicit synchronisation)
     int* pinned = nullptr;   // small page-locked read-back buffer (allocated once per handle)
-    cudaStream_t aux = nullptr, aux2 = nullptr;
-    cudaEvent_t ev_aux[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    cudaStream_t aux = nullptr, aux2 = nullptr, aux3 = nullptr;
+    cudaEvent_t ev_aux[7] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    void* stage = nullptr;   // page-locked staging of descriptor uploads (grow-only)
+    size_t stage_bytes = 0;
 };
+
+// page-locked staging buffer of at least `bytes` (the previous contents are dropped;
+// callers only grow it when no copy from it is pending)
+inline void* ctx_stage(fde_ctx* h, size_t bytes)
+{
+    if (bytes > h->stage_bytes) {
+        if (h->stage) {
+            FDE_CUDA(cudaDeviceSynchronize());
+            FDE_CUDA(cudaFreeHost(h->stage));
+        }
+        h->stage = nullptr;
+        h->stage_bytes = 0;
+        FDE_CUDA(cudaMallocHost(&h->stage, bytes + bytes / 4));
+        h->stage_bytes = bytes + bytes / 4;
+    }
+    return h->stage;
+}
 
 inline int* ctx_pinned(fde_ctx* h)
 {
@@ -119,6 +138,7 @@ inline cudaStream_t aux_stream(fde_ctx* h)
     if (!h->aux) {
         FDE_CUDA(cudaStreamCreateWithFlags(&h->aux, cudaStreamNonBlocking));
         FDE_CUDA(cudaStreamCreateWithFlags(&h->aux2, cudaStreamNonBlocking));
+        FDE_CUDA(cudaStreamCreateWithFlags(&h->aux3, cudaStreamNonBlocking));
         for (auto& e : h->ev_aux) FDE_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
     return h->aux;
@@ -127,6 +147,11 @@ inline cudaStream_t aux_stream2(fde_ctx* h)
 {
     aux_stream(h);
     return h->aux2;
+}
+inline cudaStream_t aux_stream3(fde_ctx* h)
+{
+    aux_stream(h);
+    return h->aux3;
 }
 
 // ------------------------------------------------------- quadrature tables

@@ -848,7 +848,9 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
             case 2: return A + offV[r.id] + r.off;
             case 3: return A + off_scr + r.off;
             case 4: return A + offLi[r.id] + r.off;
-            default: return A + offUi[r.id] + r.off;
+            case 5: return A + offUi[r.id] + r.off;
+            case 6: return hm->dense.p + r.off;   // the H-matrix's own arenas (init copies)
+            default: return hm->lr.p + r.off;
         }
     };
 
@@ -941,127 +943,151 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         }
         ln.npan = (int)vpan.size() - ln.pan0;
     };
-    // init: dense copies + low-rank factor copies, initial compression
-    {
-        std::vector<VCopy> c;
-        for (int b = 0; b < nb; ++b) {
-            const HBlock& hb = S.bl[b];
-            if (t0[b] < 0) continue;
-            if (hb.type == HB_DENSE) {
-                c.push_back({{0, b, 0}, {0, b, 0}, hb.m, hb.m, (int)hb.m, (int)hb.n, 0, 1.0});
-            } else if (hb.type == HB_LR) {
-                c.push_back({{1, b, 0}, {1, b, 0}, hb.m, hb.m, (int)hb.m, R, 0, 1.0});
-                c.push_back({{2, b, 0}, {2, b, 0}, hb.n, hb.n, (int)hb.n, R, 0, 1.0});
-            }
-        }
-        put_copy(c, P->init);
-        // sources are the H-matrix arenas, not ours: patch
-        int q = P->init.cp0;
-        for (int b = 0; b < nb; ++b) {
-            const HBlock& hb = S.bl[b];
-            if (t0[b] < 0) continue;
-            if (hb.type == HB_DENSE) {
-                if (hb.m > 0 && hb.n > 0) vcp[q++].src = hm->dense.p + hb.off;
-            } else if (hb.type == HB_LR) {
-                if (hb.m > 0 && R > 0) vcp[q++].src = hm->lr.p + hb.off;
-                if (hb.n > 0 && R > 0) vcp[q++].src = hm->lr.p + hb.off + hb.m * hb.kcap;
-            }
-        }
-        put_trunc(init_trunc, P->init.tr);
-    }
-    P->steps.resize(nl);
-    for (int k = 0; k < nl; ++k) {
-        H2Launch& ln = P->steps[k];
-        VStep& st = steps[k];
-        put_trunc(st.trunc, ln.tr);
-        put_trunc(st.trunc_ov, ln.tr_ov);
-        ln.lu = (int)vlu.size();
-        vlu.push_back({A + offD[st.lu_blk] + st.lu_off, S.bl[st.lu_blk].m, lm(k)});
-        put_panel(st.panel, ln);
-        put_gemm(st.g0, ln, 3);
-        put_gemm(st.g1, ln, 0);
-        put_gemm(st.g2, ln, 1);
-        put_copy(st.cp, ln);
-        {   // split the dense updates: row / column k+1 (needed by step k+1) vs the rest
-            std::vector<VTask> crit, rest;
-            for (size_t q = 0; q < st.g3.size(); ++q) (st.g3crit[q] ? crit : rest).push_back(std::move(st.g3[q]));
-            put_gemm(crit, ln, 2);
-            put_gemm(rest, ln, 4);
+    // ---- the op lists of the init and final phases
+    std::vector<VCopy> init_cp;   // dense blocks and the R Taylor columns, from the H-matrix arenas
+    for (int b = 0; b < nb; ++b) {
+        const HBlock& hb = S.bl[b];
+        if (t0[b] < 0) continue;
+        if (hb.type == HB_DENSE) {
+            init_cp.push_back({{6, b, hb.off}, {0, b, 0}, hb.m, hb.m, (int)hb.m, (int)hb.n, 0, 1.0});
+        } else if (hb.type == HB_LR) {
+            init_cp.push_back({{7, b, hb.off}, {1, b, 0}, hb.m, hb.m, (int)hb.m, R, 0, 1.0});
+            init_cp.push_back({{7, b, hb.off + hb.m * hb.kcap}, {2, b, 0}, hb.n, hb.n, (int)hb.n, R, 0, 1.0});
         }
     }
     // final: explicit inverses of the leaf factors (for the substitutions).  Tile
     // inverses on the diagonal, then the off-diagonal tiles level by level:
     //   L^{-1}(i,j) = -Linv(i,i) sum_{k=j}^{i-1} L(i,k) L^{-1}(k,j)       (i > j)
     //   U^{-1}(i,j) = -Uinv(i,i) sum_{k=i+1}^{j} U(i,k) U^{-1}(k,j)       (i < j)
-    {
-        std::vector<VCopy> c;
-        std::vector<VPanel> pv;
-        for (int q = 0; q < nl; ++q) {
-            const int d = own(q, q), f = leaf_of[q];
-            const VRef Tq{0, d, toff(d, q, q)};
-            c.push_back({{4, f, 0}, {4, f, ioff(f, q, q)}, 0, lfm(f), lm(q), lm(q), 2, 1.0});
-            c.push_back({{5, f, 0}, {5, f, ioff(f, q, q)}, 0, lfm(f), lm(q), lm(q), 2, 1.0});
-            pv.push_back({Tq, S.bl[d].m, {4, f, ioff(f, q, q)}, lfm(f), lm(q), lm(q), 0});
-            pv.push_back({Tq, S.bl[d].m, {5, f, ioff(f, q, q)}, lfm(f), lm(q), lm(q), 2});
-        }
-        put_copy(c, P->fin);
-        put_panel(pv, P->fin);
-        P->fin_lv.resize(std::max(0, maxnt - 1));
-        for (int dd = 1; dd < maxnt; ++dd) {
-            std::vector<VTask> tt, tx;
-            int64_t scr = 0;
-            for (int f = 0; f < nleaf; ++f) {
-                const int d = own(lq0[f], lq0[f]);
-                const int64_t md = S.bl[d].m, mf = lfm(f);
-                for (int i = lq0[f]; i <= lq1[f]; ++i)
-                    for (int j = lq0[f]; j <= lq1[f]; ++j) {
-                        if (std::abs(i - j) != dd) continue;
-                        const bool low = i > j;
-                        const int sp = low ? 4 : 5;
-                        VTask t{{3, 0, scr}, lm(i), lm(i), lm(j), 0.0, {}};
-                        for (int k = low ? j : i + 1; k <= (low ? i - 1 : j); ++k)
-                            t.terms.push_back({{0, d, toff(d, i, k)}, {sp, f, ioff(f, k, j)}, md, mf, lm(k), 0, 0, 1.0});
-                        tt.push_back(t);
-                        VTask x{{sp, f, ioff(f, i, j)}, mf, lm(i), lm(j), 0.0, {}};
-                        x.terms.push_back({{sp, f, ioff(f, i, i)}, {3, 0, scr}, mf, lm(i), lm(i), 0, 0, -1.0});
-                        tx.push_back(x);
-                        scr += (int64_t)lm(i) * lm(j);
-                    }
-            }
-            put_gemm(tt, P->fin_lv[dd - 1], 0);
-            put_gemm(tx, P->fin_lv[dd - 1], 1);
+    std::vector<VCopy> fin_cp;
+    std::vector<VPanel> fin_pv;
+    std::vector<std::vector<VTask>> fin_tt(std::max(0, maxnt - 1)), fin_tx(std::max(0, maxnt - 1));
+    for (int q = 0; q < nl; ++q) {
+        const int d = own(q, q), f = leaf_of[q];
+        const VRef Tq{0, d, toff(d, q, q)};
+        fin_cp.push_back({{4, f, 0}, {4, f, ioff(f, q, q)}, 0, lfm(f), lm(q), lm(q), 2, 1.0});
+        fin_cp.push_back({{5, f, 0}, {5, f, ioff(f, q, q)}, 0, lfm(f), lm(q), lm(q), 2, 1.0});
+        fin_pv.push_back({Tq, S.bl[d].m, {4, f, ioff(f, q, q)}, lfm(f), lm(q), lm(q), 0});
+        fin_pv.push_back({Tq, S.bl[d].m, {5, f, ioff(f, q, q)}, lfm(f), lm(q), lm(q), 2});
+    }
+    for (int dd = 1; dd < maxnt; ++dd) {
+        int64_t scr = 0;
+        for (int f = 0; f < nleaf; ++f) {
+            const int d = own(lq0[f], lq0[f]);
+            const int64_t md = S.bl[d].m, mf = lfm(f);
+            for (int i = lq0[f]; i <= lq1[f]; ++i)
+                for (int j = lq0[f]; j <= lq1[f]; ++j) {
+                    if (std::abs(i - j) != dd) continue;
+                    const bool low = i > j;
+                    const int sp = low ? 4 : 5;
+                    VTask t{{3, 0, scr}, lm(i), lm(i), lm(j), 0.0, {}};
+                    for (int k = low ? j : i + 1; k <= (low ? i - 1 : j); ++k)
+                        t.terms.push_back({{0, d, toff(d, i, k)}, {sp, f, ioff(f, k, j)}, md, mf, lm(k), 0, 0, 1.0});
+                    fin_tt[dd - 1].push_back(t);
+                    VTask x{{sp, f, ioff(f, i, j)}, mf, lm(i), lm(j), 0.0, {}};
+                    x.terms.push_back({{sp, f, ioff(f, i, i)}, {3, 0, scr}, mf, lm(i), lm(i), 0, 0, -1.0});
+                    fin_tx[dd - 1].push_back(x);
+                    scr += (int64_t)lm(i) * lm(j);
+                }
         }
     }
-    const double ms_flat = ms_since(t_flat0);
-    P->lu.upload(vlu.data(), vlu.size(), s);
-    if (!vpan.empty()) P->pan.upload(vpan.data(), vpan.size(), s);
-    if (!vterm.empty()) P->terms.upload(vterm.data(), vterm.size(), s);
-    if (!vtask.empty()) P->tasks.upload(vtask.data(), vtask.size(), s);
-    if (!vtile.empty()) P->tiles.upload(vtile.data(), vtile.size(), s);
-    if (!vcp.empty()) P->cps.upload(vcp.data(), vcp.size(), s);
-    if (!vte.empty()) P->te.upload(vte.data(), vte.size(), s);
-    if (!vtc.empty()) P->tc.upload(vtc.data(), vtc.size(), s);
-
+    // ---- exact descriptor counts -> device arrays and the pinned staging buffer
+    size_t n_pan = 0, n_task = 0, n_term = 0, n_tile = 0, n_cp = 0, n_te = 0, n_tc = 0;
+    auto cnt_tasks = [&](const std::vector<VTask>& v) {
+        for (auto& t : v) {
+            ++n_task;
+            n_term += t.terms.size();
+            n_tile += (size_t)(ceil_div(t.m, GT) * ceil_div(t.n, GT));
+        }
+    };
+    auto cnt_trunc = [&](const std::vector<VTrunc>& v) {
+        for (auto& e : v) {
+            ++n_te;
+            n_tc += (size_t)(ceil_div(S.bl[e.blk].m, TRUNC_CHUNK) + ceil_div(S.bl[e.blk].n, TRUNC_CHUNK));
+        }
+    };
+    auto cnt_pan = [&](const std::vector<VPanel>& v) {
+        for (auto& q : v) n_pan += (size_t)ceil_div(q.nvec, H2_STRIP);
+    };
+    auto cnt_cp = [&](const std::vector<VCopy>& v) {
+        for (auto& c : v) n_cp += (c.m > 0 && c.n > 0);
+    };
+    cnt_cp(init_cp);
+    cnt_trunc(init_trunc);
+    for (auto& st : steps) {
+        cnt_trunc(st.trunc);
+        cnt_trunc(st.trunc_ov);
+        cnt_pan(st.panel);
+        cnt_tasks(st.g0);
+        cnt_tasks(st.g1);
+        cnt_tasks(st.g2);
+        cnt_tasks(st.g3);
+        cnt_cp(st.cp);
+    }
+    cnt_cp(fin_cp);
+    cnt_pan(fin_pv);
+    for (auto& v : fin_tt) cnt_tasks(v);
+    for (auto& v : fin_tx) cnt_tasks(v);
+    vlu.reserve(nl); vpan.reserve(n_pan); vterm.reserve(n_term); vtask.reserve(n_task);
+    vtile.reserve(n_tile); vcp.reserve(n_cp); vte.reserve(n_te); vtc.reserve(n_tc);
+    P->lu.alloc(std::max<size_t>(nl, 1));
+    P->pan.alloc(std::max<size_t>(n_pan, 1));
+    P->terms.alloc(std::max<size_t>(n_term, 1));
+    P->tasks.alloc(std::max<size_t>(n_task, 1));
+    P->tiles.alloc(std::max<size_t>(n_tile, 1));
+    P->cps.alloc(std::max<size_t>(n_cp, 1));
+    P->te.alloc(std::max<size_t>(n_te, 1));
+    P->tc.alloc(std::max<size_t>(n_tc, 1));
+    // staged uploads: every phase's new descriptors go host -> pinned -> device on a
+    // copy stream, so the host flattens step k+1 while the device runs step k
+    struct Stage {
+        const void* src;   // host vector data (capacity reserved: never reallocated)
+        size_t elem, done;
+        void* dev;
+        size_t pin;        // byte offset in the pinned buffer
+    };
+    auto al16 = [](size_t b) { return (b + 15) & ~(size_t)15; };
+    Stage stg[8] = {{vlu.data(), sizeof(H2Lu), 0, P->lu.p, 0},       {vpan.data(), sizeof(H2Panel), 0, P->pan.p, 0},
+                    {vterm.data(), sizeof(H2Term), 0, P->terms.p, 0}, {vtask.data(), sizeof(H2Task), 0, P->tasks.p, 0},
+                    {vtile.data(), sizeof(H2Tile), 0, P->tiles.p, 0}, {vcp.data(), sizeof(H2Copy), 0, P->cps.p, 0},
+                    {vte.data(), sizeof(TEntry), 0, P->te.p, 0},      {vtc.data(), sizeof(TChunk), 0, P->tc.p, 0}};
+    const size_t cap[8] = {(size_t)nl, n_pan, n_term, n_task, n_tile, n_cp, n_te, n_tc};
+    size_t pin_bytes = 0;
+    for (int a = 0; a < 8; ++a) {
+        stg[a].pin = pin_bytes;
+        pin_bytes += al16(cap[a] * stg[a].elem);
+    }
+    char* pin = (char*)ctx_stage(L->h, pin_bytes);
+    cudaStream_t sa = s, sb = aux_stream(L->h), sc = aux_stream2(L->h), sd = aux_stream3(L->h);
+    cudaEvent_t evA = L->h->ev_aux[0], evOp = L->h->ev_aux[1];
+    cudaEvent_t evP = L->h->ev_aux[3], evC = L->h->ev_aux[4], evB = L->h->ev_aux[5], evD = L->h->ev_aux[6];
+    FDE_CUDA(cudaEventRecord(evA, sa));   // the arena and descriptor arrays are allocated on sa
+    FDE_CUDA(cudaStreamWaitEvent(sd, evA, 0));
+    auto push = [&]() {
+        const size_t now[8] = {vlu.size(), vpan.size(), vterm.size(), vtask.size(),
+                               vtile.size(), vcp.size(), vte.size(), vtc.size()};
+        for (int a = 0; a < 8; ++a) {
+            if (now[a] == stg[a].done) continue;
+            const size_t off = stg[a].done * stg[a].elem, bytes = (now[a] - stg[a].done) * stg[a].elem;
+            memcpy(pin + stg[a].pin + off, (const char*)stg[a].src + off, bytes);
+            FDE_CUDA(cudaMemcpyAsync((char*)stg[a].dev + off, pin + stg[a].pin + off, bytes, cudaMemcpyHostToDevice, sd));
+            stg[a].done = now[a];
+        }
+        FDE_CUDA(cudaEventRecord(evD, sd));
+    };
+    const double ms_flat0 = ms_since(t_flat0);
     L->plan_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_plan0).count();
-    if (getenv("FDE_DEBUG_PLAN"))
-        fprintf(stderr, "hlu2 plan: nl %d blocks %d | simulate %.2f ms, layout+alloc %.2f ms, flatten %.2f ms, "
-                        "upload %.2f ms | tiles %zu terms %zu copies %zu panels %zu trunc %zu\n",
-                nl, nb, ms_sim, ms_alloc, ms_flat, L->plan_ms - ms_sim - ms_alloc - ms_flat, vtile.size(),
-                vterm.size(), vcp.size(), vpan.size(), vte.size());
-    // ---- execute
+
+    // ---- execute.  Three streams.  sa: the critical chain LU(k) -> panels ->
+    // products -> conversions -> dense updates of row / column k+1 (needed by step
+    // k+1); sb: truncations (operands before the panels, overflowing targets before
+    // the new columns) and the new low-rank columns; sc: the remaining dense updates
+    // of step k, which overlap LU(k+1) and the panels of step k+1 (lookahead).
     const int pan_smem = (H2_MMAX + H2_STRIP) * (H2_MMAX + 2) * (int)sizeof(double);
     set_smem_once((const void*)k_h2_panel, pan_smem);
     const int lu_smem = H2_MMAX * (H2_MMAX + 1) * (int)sizeof(double);   // padded 128 x 129
     set_smem_once((const void*)k_h2_lu, lu_smem);
     int nlaunch = 0;
-    // three streams.  sa: the critical chain LU(k) -> panels -> products ->
-    // conversions -> dense updates of row / column k+1 (needed by step k+1);
-    // sb: truncations (operands before the panels, overflowing targets before the
-    // new columns) and the new low-rank columns; sc: the remaining dense updates of
-    // step k, which overlap LU(k+1) and the panels of step k+1 (lookahead).
-    cudaStream_t sa = s, sb = aux_stream(L->h), sc = aux_stream2(L->h);
-    cudaEvent_t evA = L->h->ev_aux[0], evOp = L->h->ev_aux[1], evOv = L->h->ev_aux[2];
-    cudaEvent_t evP = L->h->ev_aux[3], evC = L->h->ev_aux[4], evB = L->h->ev_aux[5];
     auto run_copy = [&](const H2Launch& ln, cudaStream_t st) {
         if (!ln.ncp) return;
         k_h2_copy<<<ln.ncp, 256, 0, st>>>(P->cps.p + ln.cp0);
@@ -1097,7 +1123,12 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         FDE_CHECK_LAUNCH();
         ++nlaunch;
     };
+    // init
+    put_copy(init_cp, P->init);
+    put_trunc(init_trunc, P->init.tr);
+    push();
     FDE_CUDA(cudaMemsetAsync(A + lr_lo, 0, (size_t)(lr_hi - lr_lo) * sizeof(double), sa));
+    FDE_CUDA(cudaStreamWaitEvent(sa, evD, 0));
     run_copy(P->init, sa);
     run_trunc(P->init.tr, sa);
     FDE_CUDA(cudaEventRecord(evA, sa));
@@ -1105,8 +1136,30 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
     FDE_CUDA(cudaStreamWaitEvent(sc, evA, 0));
     FDE_CUDA(cudaEventRecord(evC, sc));
     const int kstop = g_hlu2_stop >= 0 ? std::min(g_hlu2_stop, nl) : nl;   // debug: partial sweep
+    P->steps.resize(nl);
     for (int k = 0; k < kstop; ++k) {
-        const H2Launch& ln = P->steps[k];
+        // flatten step k (the device is still busy with step k-1) and stage it
+        H2Launch& ln = P->steps[k];
+        VStep& st = steps[k];
+        put_trunc(st.trunc, ln.tr);
+        put_trunc(st.trunc_ov, ln.tr_ov);
+        ln.lu = (int)vlu.size();
+        vlu.push_back({A + offD[st.lu_blk] + st.lu_off, S.bl[st.lu_blk].m, lm(k)});
+        put_panel(st.panel, ln);
+        put_gemm(st.g0, ln, 3);
+        put_gemm(st.g1, ln, 0);
+        put_gemm(st.g2, ln, 1);
+        put_copy(st.cp, ln);
+        {   // split the dense updates: row / column k+1 (needed by step k+1) vs the rest
+            std::vector<VTask> crit, rest;
+            for (size_t q = 0; q < st.g3.size(); ++q) (st.g3crit[q] ? crit : rest).push_back(std::move(st.g3[q]));
+            put_gemm(crit, ln, 2);
+            put_gemm(rest, ln, 4);
+        }
+        push();
+        FDE_CUDA(cudaStreamWaitEvent(sa, evD, 0));
+        FDE_CUDA(cudaStreamWaitEvent(sb, evD, 0));
+        FDE_CUDA(cudaStreamWaitEvent(sc, evD, 0));
         // sb (after the new columns of step k-1 and the panels of step k-1)
         run_trunc(ln.tr, sb);
         FDE_CUDA(cudaEventRecord(evOp, sb));
@@ -1136,6 +1189,15 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
     FDE_CUDA(cudaStreamWaitEvent(sa, evB, 0));
     FDE_CUDA(cudaStreamWaitEvent(sa, evC, 0));
     if (kstop == nl) {
+        put_copy(fin_cp, P->fin);
+        put_panel(fin_pv, P->fin);
+        P->fin_lv.resize(fin_tt.size());
+        for (size_t dd = 0; dd < fin_tt.size(); ++dd) {
+            put_gemm(fin_tt[dd], P->fin_lv[dd], 0);
+            put_gemm(fin_tx[dd], P->fin_lv[dd], 1);
+        }
+        push();
+        FDE_CUDA(cudaStreamWaitEvent(sa, evD, 0));
         FDE_CUDA(cudaMemsetAsync(A + inv_lo, 0, (size_t)(inv_hi - inv_lo) * sizeof(double), sa));
         run_copy(P->fin, sa);
         run_panel(P->fin);
@@ -1144,6 +1206,11 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
             run_gemm(lv, 1, sa);
         }
     }
+    if (getenv("FDE_DEBUG_PLAN"))
+        fprintf(stderr, "hlu2 plan: nl %d blocks %d | simulate %.2f ms, layout+alloc %.2f ms, counts %.2f ms, "
+                        "plan+launch total %.2f ms | tiles %zu terms %zu copies %zu panels %zu trunc %zu\n",
+                nl, nb, ms_sim, ms_alloc, ms_flat0, ms_since(t_plan0), vtile.size(), vterm.size(), vcp.size(),
+                vpan.size(), vte.size());
     L->nops = nlaunch;
 
     // ---- the blocks in the format of hlu.cu (substitutions, test helpers)
