@@ -95,6 +95,10 @@ void fde_destroy(fde_handle h)
         cudaStreamSynchronize(h->aux);
         cudaStreamSynchronize(h->aux2);
         cudaStreamSynchronize(h->aux3);
+        cudaStreamSynchronize(h->aux4);
+        cudaStreamDestroy(h->aux4);
+        cudaStreamSynchronize(h->aux5);
+        cudaStreamDestroy(h->aux5);
         cudaStreamDestroy(h->aux);
         cudaStreamDestroy(h->aux2);
         cudaStreamDestroy(h->aux3);

@@ -104,8 +104,8 @@ struct fde_ctx {
     // auxiliary stream + events for work that overlaps the caller's stream
     // (created on first use; ordered by events, never by implicit synchronisation)
     int* pinned = nullptr;   // small page-locked read-back buffer (allocated once per handle)
-    cudaStream_t aux = nullptr, aux2 = nullptr, aux3 = nullptr;
-    cudaEvent_t ev_aux[7] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    cudaStream_t aux = nullptr, aux2 = nullptr, aux3 = nullptr, aux4 = nullptr, aux5 = nullptr;
+    cudaEvent_t ev_aux[10] = {};
     void* stage = nullptr;   // page-locked staging of descriptor uploads (grow-only)
     size_t stage_bytes = 0;
 };
@@ -136,9 +136,15 @@ inline int* ctx_pinned(fde_ctx* h)
 inline cudaStream_t aux_stream(fde_ctx* h)
 {
     if (!h->aux) {
-        FDE_CUDA(cudaStreamCreateWithFlags(&h->aux, cudaStreamNonBlocking));
-        FDE_CUDA(cudaStreamCreateWithFlags(&h->aux2, cudaStreamNonBlocking));
-        FDE_CUDA(cudaStreamCreateWithFlags(&h->aux3, cudaStreamNonBlocking));
+        // priorities: the critical chains (aux: truncations, aux4: diagonal LUs,
+        // aux5: the H-LU critical stream) are served before the bulk updates (aux2)
+        int lo = 0, hi = 0;
+        FDE_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        FDE_CUDA(cudaStreamCreateWithPriority(&h->aux, cudaStreamNonBlocking, hi));
+        FDE_CUDA(cudaStreamCreateWithPriority(&h->aux2, cudaStreamNonBlocking, lo));
+        FDE_CUDA(cudaStreamCreateWithPriority(&h->aux3, cudaStreamNonBlocking, hi));
+        FDE_CUDA(cudaStreamCreateWithPriority(&h->aux4, cudaStreamNonBlocking, hi));
+        FDE_CUDA(cudaStreamCreateWithPriority(&h->aux5, cudaStreamNonBlocking, hi));
         for (auto& e : h->ev_aux) FDE_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
     return h->aux;
@@ -152,6 +158,16 @@ inline cudaStream_t aux_stream3(fde_ctx* h)
 {
     aux_stream(h);
     return h->aux3;
+}
+inline cudaStream_t aux_stream4(fde_ctx* h)
+{
+    aux_stream(h);
+    return h->aux4;
+}
+inline cudaStream_t aux_stream5(fde_ctx* h)
+{
+    aux_stream(h);
+    return h->aux5;
 }
 
 // ------------------------------------------------------- quadrature tables

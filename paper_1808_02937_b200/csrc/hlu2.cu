@@ -249,35 +249,64 @@ __global__ void __launch_bounds__(256) k_h2_panel(const H2Panel* P)
 
 // grouped multi-term GEMM: every CTA owns a 64 x 64 tile of one task,
 // C_tile = beta C_tile + sum_terms alpha op(A) op(B); terms in a fixed order.
-// The next 16-deep slice of A and B is loaded into registers while the current
-// one is multiplied from shared memory (one barrier pair per slice).
-__device__ __forceinline__ void h2_load_slice(const H2Term& T, int m0, int n0, int m, int n, int k0, double* ra,
-                                              double* rb)
+// The (term, 16-deep slice) sequence of the tile runs through a 3-stage
+// asynchronous-copy pipeline in shared memory (8-byte cp.async: any operand
+// layout / transpose), so two slices are in flight while one is multiplied.
+#define H2G_ST 3
+#define H2G_TMAX 48
+#define H2G_SMEM (2 * H2G_ST * GK * (GT + 1) * (int)sizeof(double))
+struct H2Cursor {   // position in the (term, slice) sequence of a tile
+    int q, k0;
+};
+__device__ __forceinline__ void h2_next(const H2Term* terms, int t_hi, H2Cursor& c)
 {
+    c.k0 += GK;
+    if (c.k0 >= terms[c.q].k) {
+        c.k0 = 0;
+        ++c.q;
+        while (c.q < t_hi && terms[c.q].k <= 0) ++c.q;
+    }
+}
+__device__ __forceinline__ void h2_stage(const H2Term& T, int m0, int n0, int m, int n, int k0, double* sA, double* sB)
+{
+    // sA[kk][mm] (ld GT + 1), sB[kk][nn]; zero outside the operands
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
         const int t = threadIdx.x + 256 * u;
         int kk, mm;
         if (T.ta) { mm = t / GK; kk = t % GK; } else { kk = t / GT; mm = t % GT; }
         const int gi = m0 + mm, gk = k0 + kk;
-        double va = 0.0;
-        if (gi < m && gk < T.k) va = T.ta ? T.A[(long long)gi * T.lda + gk] : T.A[(long long)gk * T.lda + gi];
-        ra[u] = va;
+        double* da = sA + kk * (GT + 1) + mm;
+        if (gi < m && gk < T.k) cp_async8(da, T.ta ? T.A + (long long)gi * T.lda + gk : T.A + (long long)gk * T.lda + gi);
+        else *da = 0.0;
         int nn;
         if (T.tb) { kk = t / GT; nn = t % GT; } else { nn = t / GK; kk = t % GK; }
         const int gj = n0 + nn, gk2 = k0 + kk;
-        double vb = 0.0;
-        if (gj < n && gk2 < T.k) vb = T.tb ? T.B[(long long)gk2 * T.ldb + gj] : T.B[(long long)gj * T.ldb + gk2];
-        rb[u] = vb;
+        double* db = sB + kk * (GT + 1) + nn;
+        if (gj < n && gk2 < T.k) cp_async8(db, T.tb ? T.B + (long long)gk2 * T.ldb + gj : T.B + (long long)gj * T.ldb + gk2);
+        else *db = 0.0;
     }
 }
+__device__ __forceinline__ void cp_async_commit_group() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait_group() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 __global__ void __launch_bounds__(256) k_h2_gemm(const H2Tile* tiles, const H2Task* tasks, const H2Term* terms)
 {
-    __shared__ double sA[GK][GT + 1];
-    __shared__ double sB[GK][GT + 1];
+    extern __shared__ double gsm[];   // H2G_SMEM bytes: [stage] A slice, [stage] B slice
+    double (*sA)[GK * (GT + 1)] = reinterpret_cast<double (*)[GK * (GT + 1)]>(gsm);
+    double (*sB)[GK * (GT + 1)] = reinterpret_cast<double (*)[GK * (GT + 1)]>(gsm + H2G_ST * GK * (GT + 1));
+    __shared__ double sAlpha[H2G_ST];
+    __shared__ H2Term sT[H2G_TMAX];   // the task's term descriptors (one global read each)
     const H2Tile tl = tiles[blockIdx.x];
     const H2Task tk = tasks[tl.task];
+    const int nt = tk.t_hi - tk.t_lo;
+    const H2Term* tm = terms + tk.t_lo;
+    if (nt <= H2G_TMAX) {
+        for (int q = threadIdx.x; q < nt; q += blockDim.x) sT[q] = terms[tk.t_lo + q];
+        __syncthreads();
+        tm = sT;
+    }
     const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
     const int m0 = tl.m0, n0 = tl.n0, m = tk.m, n = tk.n;
     double acc[4][4];
@@ -285,49 +314,53 @@ __global__ void __launch_bounds__(256) k_h2_gemm(const H2Tile* tiles, const H2Ta
     for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
-    // flatten (term, slice) into one pipelined sequence
-    int q = tk.t_lo, k0 = 0;
-    while (q < tk.t_hi && terms[q].k <= 0) ++q;
-    double ra[4], rb[4];
-    if (q < tk.t_hi) h2_load_slice(terms[q], m0, n0, m, n, 0, ra, rb);
-    while (q < tk.t_hi) {
-        const H2Term T = terms[q];
-        // stage the slice
+    H2Cursor ld{0, -GK};   // next slice to load
+    while (ld.q < nt && tm[ld.q].k <= 0) ++ld.q;
+    ld.k0 = 0;
+    int nslice = 0;
+    for (int q = 0; q < nt; ++q) nslice += (tm[q].k + GK - 1) / GK;
+    // prologue: stages 0 .. H2G_ST-2
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int t = threadIdx.x + 256 * u;
-            int kk, mm;
-            if (T.ta) { mm = t / GK; kk = t % GK; } else { kk = t / GT; mm = t % GT; }
-            sA[kk][mm] = T.alpha * ra[u];
-            int nn;
-            if (T.tb) { kk = t / GT; nn = t % GT; } else { nn = t / GK; kk = t % GK; }
-            sB[kk][nn] = rb[u];
+    for (int st = 0; st < H2G_ST - 1; ++st) {
+        if (st < nslice) {
+            const H2Term& T = tm[ld.q];
+            h2_stage(T, m0, n0, m, n, ld.k0, sA[st], sB[st]);
+            if (threadIdx.x == 0) sAlpha[st] = T.alpha;
+            h2_next(tm, nt, ld);
         }
+        cp_async_commit_group();
+    }
+    for (int sl = 0; sl < nslice; ++sl) {
+        cp_async_wait_group<H2G_ST - 2>();
         __syncthreads();
-        // advance and prefetch the next slice
-        int q2 = q, k2 = k0 + GK;
-        if (k2 >= T.k) {
-            k2 = 0;
-            ++q2;
-            while (q2 < tk.t_hi && terms[q2].k <= 0) ++q2;
+        // refill the stage consumed H2G_ST-1 slices ago
+        const int nx = sl + H2G_ST - 1;
+        if (nx < nslice) {
+            const int st = nx % H2G_ST;
+            const H2Term& T = tm[ld.q];
+            h2_stage(T, m0, n0, m, n, ld.k0, sA[st], sB[st]);
+            if (threadIdx.x == 0) sAlpha[st] = T.alpha;
+            h2_next(tm, nt, ld);
         }
-        if (q2 < tk.t_hi) h2_load_slice(terms[q2], m0, n0, m, n, k2, ra, rb);
+        cp_async_commit_group();
+        const int cs = sl % H2G_ST;
+        const double* a_s = sA[cs];
+        const double* b_s = sB[cs];
+        const double al = sAlpha[cs];
 #pragma unroll
         for (int kk = 0; kk < GK; ++kk) {
             double a[4], b[4];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) a[i] = sA[kk][tx + 16 * i];
+            for (int i = 0; i < 4; ++i) a[i] = al * a_s[kk * (GT + 1) + tx + 16 * i];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) b[j] = sB[kk][ty + 16 * j];
+            for (int j = 0; j < 4; ++j) b[j] = b_s[kk * (GT + 1) + ty + 16 * j];
 #pragma unroll
             for (int i = 0; i < 4; ++i)
 #pragma unroll
                 for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
         }
-        __syncthreads();
-        q = q2;
-        k0 = k2;
     }
+    cp_async_wait_group<0>();
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -399,7 +432,7 @@ struct VStep {
     std::vector<VPanel> panel;
     std::vector<VTask> g0, g1, g2, g3;   // conversions to dense, cores, products, dense updates
     std::vector<VTask> g3r;              // dense updates of tiles off row / column k+1 (lookahead stream)
-    std::vector<char> g3crit;            // per g3 task: tile in row or column k+1
+    std::vector<char> g3crit;            // per g3 task: 2 tile (k+1, k+1), 1 row / column k+1 or (k+2, k+2), 0 rest
     std::vector<VCopy> cp;           // low-rank target columns
     int64_t scratch = 0;
 };
@@ -411,7 +444,7 @@ struct H2Launch {      // ranges in the flat device arrays
     H2Trunc tr, tr_ov;
     int lu = -1;
     int pan0 = 0, npan = 0;
-    int g_tile0[5] = {0, 0, 0, 0, 0}, g_ntile[5] = {0, 0, 0, 0, 0};
+    int g_tile0[6] = {0, 0, 0, 0, 0, 0}, g_ntile[6] = {0, 0, 0, 0, 0, 0};
     int cp0 = 0, ncp = 0;
 };
 
@@ -691,7 +724,11 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
                                 tile_task[key] = ti;
                                 VTask tk{{0, t, (lr0[j] - col0(t)) * T.m + (lr0[i] - row0(t))}, T.m, lm(i), lm(j), 1.0, {}};
                                 st.g3.push_back(tk);
-                                st.g3crit.push_back(i == k + 1 || j == k + 1);
+                                // 2: the next diagonal tile (input of LU(k+1), right after the panels);
+                                // 1: row / column k+1 and the diagonal tile after it (critical stream);
+                                // 0: the rest (lookahead stream)
+                                st.g3crit.push_back((i == k + 1 && j == k + 1) ? 2
+                                                    : (i == k + 1 || j == k + 1 || (i == k + 2 && j == k + 2)));
                             } else {
                                 ti = tile_task[key];
                             }
@@ -1058,10 +1095,17 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         pin_bytes += al16(cap[a] * stg[a].elem);
     }
     char* pin = (char*)ctx_stage(L->h, pin_bytes);
-    cudaStream_t sa = s, sb = aux_stream(L->h), sc = aux_stream2(L->h), sd = aux_stream3(L->h);
+    // sa: high-priority internal stream ordered after the caller's stream s (and s
+    // after sa at the end): the critical chain must not queue behind bulk updates
+    cudaStream_t sa = aux_stream5(L->h), sb = aux_stream(L->h), sc = aux_stream2(L->h), sd = aux_stream3(L->h);
+    cudaStream_t sl = aux_stream4(L->h);   // the diagonal-tile LUs
+    cudaEvent_t evS = L->h->ev_aux[9];
+    FDE_CUDA(cudaEventRecord(evS, s));
+    FDE_CUDA(cudaStreamWaitEvent(sa, evS, 0));
     cudaEvent_t evA = L->h->ev_aux[0], evOp = L->h->ev_aux[1];
     cudaEvent_t evP = L->h->ev_aux[3], evC = L->h->ev_aux[4], evB = L->h->ev_aux[5], evD = L->h->ev_aux[6];
-    FDE_CUDA(cudaEventRecord(evA, sa));   // the arena and descriptor arrays are allocated on sa
+    cudaEvent_t evLU = L->h->ev_aux[7], evDg = L->h->ev_aux[8];
+    FDE_CUDA(cudaEventRecord(evA, sa));   // (sa is ordered after the arena / descriptor allocations on s)
     FDE_CUDA(cudaStreamWaitEvent(sd, evA, 0));
     auto push = [&]() {
         const size_t now[8] = {vlu.size(), vpan.size(), vterm.size(), vtask.size(),
@@ -1087,6 +1131,7 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
     set_smem_once((const void*)k_h2_panel, pan_smem);
     const int lu_smem = H2_MMAX * (H2_MMAX + 1) * (int)sizeof(double);   // padded 128 x 129
     set_smem_once((const void*)k_h2_lu, lu_smem);
+    set_smem_once((const void*)k_h2_gemm, H2G_SMEM);
     int nlaunch = 0;
     auto run_copy = [&](const H2Launch& ln, cudaStream_t st) {
         if (!ln.ncp) return;
@@ -1113,7 +1158,7 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
     };
     auto run_gemm = [&](const H2Launch& ln, int w, cudaStream_t st) {
         if (!ln.g_ntile[w]) return;
-        k_h2_gemm<<<ln.g_ntile[w], 256, 0, st>>>(P->tiles.p + ln.g_tile0[w], P->tasks.p, P->terms.p);
+        k_h2_gemm<<<ln.g_ntile[w], 256, H2G_SMEM, st>>>(P->tiles.p + ln.g_tile0[w], P->tasks.p, P->terms.p);
         FDE_CHECK_LAUNCH();
         ++nlaunch;
     };
@@ -1123,9 +1168,14 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         FDE_CHECK_LAUNCH();
         ++nlaunch;
     };
-    // init
+    // init (+ every diagonal-tile LU descriptor: LU(k+1) is issued during step k)
     put_copy(init_cp, P->init);
     put_trunc(init_trunc, P->init.tr);
+    P->steps.resize(nl);
+    for (int k = 0; k < nl; ++k) {
+        P->steps[k].lu = (int)vlu.size();
+        vlu.push_back({A + offD[steps[k].lu_blk] + steps[k].lu_off, S.bl[steps[k].lu_blk].m, lm(k)});
+    }
     push();
     FDE_CUDA(cudaMemsetAsync(A + lr_lo, 0, (size_t)(lr_hi - lr_lo) * sizeof(double), sa));
     FDE_CUDA(cudaStreamWaitEvent(sa, evD, 0));
@@ -1134,56 +1184,119 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
     FDE_CUDA(cudaEventRecord(evA, sa));
     FDE_CUDA(cudaStreamWaitEvent(sb, evA, 0));
     FDE_CUDA(cudaStreamWaitEvent(sc, evA, 0));
+    FDE_CUDA(cudaStreamWaitEvent(sl, evA, 0));
     FDE_CUDA(cudaEventRecord(evC, sc));
     const int kstop = g_hlu2_stop >= 0 ? std::min(g_hlu2_stop, nl) : nl;   // debug: partial sweep
-    P->steps.resize(nl);
+    // debug timeline (FDE_DEBUG_TIMELINE): timed events per step and stream
+    const bool tline = getenv("FDE_DEBUG_TIMELINE") != nullptr;
+    enum { T_LU = 0, T_PAN, T_PROD, T_CRIT, T_OP, T_OV, T_CP, T_REST, T_N };
+    std::vector<cudaEvent_t> tev;
+    cudaEvent_t t0ev = nullptr;
+    if (tline) {
+        tev.resize((size_t)kstop * T_N);
+        for (auto& e : tev) FDE_CUDA(cudaEventCreate(&e));
+        FDE_CUDA(cudaEventCreate(&t0ev));
+        FDE_CUDA(cudaEventRecord(t0ev, sa));
+    }
+    auto mark = [&](int k, int w, cudaStream_t st) {
+        if (tline) FDE_CUDA(cudaEventRecord(tev[(size_t)k * T_N + w], st));
+    };
     for (int k = 0; k < kstop; ++k) {
         // flatten step k (the device is still busy with step k-1) and stage it
         H2Launch& ln = P->steps[k];
         VStep& st = steps[k];
         put_trunc(st.trunc, ln.tr);
         put_trunc(st.trunc_ov, ln.tr_ov);
-        ln.lu = (int)vlu.size();
-        vlu.push_back({A + offD[st.lu_blk] + st.lu_off, S.bl[st.lu_blk].m, lm(k)});
         put_panel(st.panel, ln);
         put_gemm(st.g0, ln, 3);
         put_gemm(st.g1, ln, 0);
         put_gemm(st.g2, ln, 1);
         put_copy(st.cp, ln);
         {   // split the dense updates: row / column k+1 (needed by step k+1) vs the rest
-            std::vector<VTask> crit, rest;
-            for (size_t q = 0; q < st.g3.size(); ++q) (st.g3crit[q] ? crit : rest).push_back(std::move(st.g3[q]));
+            std::vector<VTask> diag, crit, rest;
+            for (size_t q = 0; q < st.g3.size(); ++q)
+                (st.g3crit[q] == 2 ? diag : st.g3crit[q] ? crit : rest).push_back(std::move(st.g3[q]));
             put_gemm(crit, ln, 2);
             put_gemm(rest, ln, 4);
+            put_gemm(diag, ln, 5);
         }
         push();
         FDE_CUDA(cudaStreamWaitEvent(sa, evD, 0));
         FDE_CUDA(cudaStreamWaitEvent(sb, evD, 0));
         FDE_CUDA(cudaStreamWaitEvent(sc, evD, 0));
+        FDE_CUDA(cudaStreamWaitEvent(sl, evD, 0));
         // sb (after the new columns of step k-1 and the panels of step k-1)
         run_trunc(ln.tr, sb);
         FDE_CUDA(cudaEventRecord(evOp, sb));
+        mark(k, T_OP, sb);
         run_trunc(ln.tr_ov, sb);
-        // sa: critical chain
-        k_h2_lu<<<1, 512, lu_smem, sa>>>(P->lu.p + ln.lu, L->dflag.p);
-        FDE_CHECK_LAUNCH();
-        ++nlaunch;
+        mark(k, T_OV, sb);
+        // sa: critical chain.  LU(k) ran on sl (k = 0: here), overlapping the
+        // products and updates of step k-1; its only input from step k-1 is the
+        // update of the diagonal tile, issued right after the panels of step k-1.
+        if (k == 0) {
+            k_h2_lu<<<1, 512, lu_smem, sl>>>(P->lu.p + ln.lu, L->dflag.p);
+            FDE_CHECK_LAUNCH();
+            ++nlaunch;
+            FDE_CUDA(cudaEventRecord(evLU, sl));
+        }
+        FDE_CUDA(cudaStreamWaitEvent(sa, evLU, 0));
         FDE_CUDA(cudaStreamWaitEvent(sa, evOp, 0));
         run_panel(ln);
+        mark(k, T_PAN, sa);
+        run_gemm(ln, 5, sa);                         // diagonal tile (k+1, k+1)
+        if (k + 1 < kstop) {
+            FDE_CUDA(cudaEventRecord(evDg, sa));
+            FDE_CUDA(cudaStreamWaitEvent(sl, evDg, 0));
+            k_h2_lu<<<1, 512, lu_smem, sl>>>(P->lu.p + P->steps[k + 1].lu, L->dflag.p);
+            FDE_CHECK_LAUNCH();
+            ++nlaunch;
+            FDE_CUDA(cudaEventRecord(evLU, sl));
+            mark(k, T_LU, sl);
+        }
         run_gemm(ln, 0, sa);
         run_gemm(ln, 1, sa);
         run_gemm(ln, 3, sa);   // conversions to dense (after the products: a block may be
                                // an operand (row / column k) and a target (rows > k) at once)
         FDE_CUDA(cudaEventRecord(evP, sa));
+        mark(k, T_PROD, sa);
         FDE_CUDA(cudaStreamWaitEvent(sa, evC, 0));   // remaining updates of step k-1
         run_gemm(ln, 2, sa);                         // row / column k+1
+        mark(k, T_CRIT, sa);
         // sb: new low-rank columns of step k (after the overflow truncations)
         FDE_CUDA(cudaStreamWaitEvent(sb, evP, 0));
         run_copy(ln, sb);
+        mark(k, T_CP, sb);
         // sc: the other dense updates of step k
         FDE_CUDA(cudaStreamWaitEvent(sc, evP, 0));
         run_gemm(ln, 4, sc);
         FDE_CUDA(cudaEventRecord(evC, sc));
+        mark(k, T_REST, sc);
+    }
+    if (tline) {
+        FDE_CUDA(cudaDeviceSynchronize());
+        const char* nm[T_N] = {"LU(k+1) end", "panel end", "products end", "crit end", "trunc_op end", "trunc_ov end",
+                               "copies end", "rest end"};
+        double prev[T_N] = {0};
+        double sum[T_N] = {0};
+        for (int k = 0; k < kstop; ++k)
+            for (int w = 0; w < T_N; ++w) {
+                float ms = 0;
+                if (cudaEventElapsedTime(&ms, t0ev, tev[(size_t)k * T_N + w]) != cudaSuccess) continue;
+                if (k > 0) sum[w] += ms - prev[w];
+                prev[w] = ms;
+            }
+        fprintf(stderr, "hlu2 timeline (%d steps): per-step period of each mark (us):", kstop);
+        for (int w = 0; w < T_N; ++w) fprintf(stderr, " %s %.1f |", nm[w], 1e3 * sum[w] / std::max(1, kstop - 1));
+        fprintf(stderr, "\n  step 10 marks (ms from start):");
+        for (int w = 0; w < T_N && kstop > 10; ++w) {
+            float ms = 0;
+            cudaEventElapsedTime(&ms, t0ev, tev[(size_t)10 * T_N + w]);
+            fprintf(stderr, " %s %.3f |", nm[w], ms);
+        }
+        fprintf(stderr, "\n");
+        for (auto& e : tev) cudaEventDestroy(e);
+        cudaEventDestroy(t0ev);
     }
     FDE_CUDA(cudaEventRecord(evB, sb));
     FDE_CUDA(cudaStreamWaitEvent(sa, evB, 0));
@@ -1206,6 +1319,8 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
             run_gemm(lv, 1, sa);
         }
     }
+    FDE_CUDA(cudaEventRecord(evS, sa));
+    FDE_CUDA(cudaStreamWaitEvent(s, evS, 0));
     if (getenv("FDE_DEBUG_PLAN"))
         fprintf(stderr, "hlu2 plan: nl %d blocks %d | simulate %.2f ms, layout+alloc %.2f ms, counts %.2f ms, "
                         "plan+launch total %.2f ms | tiles %zu terms %zu copies %zu panels %zu trunc %zu\n",
