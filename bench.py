@@ -215,6 +215,12 @@ def run_ours(args):
         lu.free()
         hm.free()
         op.free()
+        # a cold solve ends when its solution is complete on the device; without this
+        # synchronisation the host ran into the next solve while the previous one's
+        # buffers were still being released and steps jittered by 5-50 ms
+        # (tools/many_steps.py vs this loop).  It only adds idle time to the timed region.
+        if os.environ.get("FDE_BENCH_SYNC", "1") == "1":
+            torch.cuda.synchronize()
         return info, Xh
 
     for _ in range(args.warmup):
@@ -229,9 +235,14 @@ def run_ours(args):
     # ---- device-timed region: K cold solves
     # in-process NVML sampling (an nvidia-smi subprocess polling at 100 ms stalled
     # some steps of this host-launch-heavy path by ~100 ms); FDE_CLOCKS=smi selects it
-    clocks = ClockSampler(local) if os.environ.get("FDE_CLOCKS") == "smi" else NvmlSampler(local)
+    mode = os.environ.get("FDE_CLOCKS", "nvml")
+    clocks = (ClockSampler(local) if mode == "smi" else
+              NvmlSampler(local, period_s=float(os.environ.get("FDE_CLOCKS_PERIOD", "0.1"))))
+    if mode == "none":
+        clocks.start = lambda: None
+        clocks.stop = lambda: {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["not sampled (FDE_CLOCKS=none)"]}
     clocks.start()
-    fde.lib().fde_profile(h.h, 1)
+    fde.lib().fde_profile(h.h, 0 if os.environ.get("FDE_BENCH_PROFILE") == "0" else 1)
     barrier()
     launches0 = fde.lib().fde_launch_count()
     evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
@@ -315,7 +326,7 @@ def run_ours(args):
             "phases_ms": {k: round(v, 3) for k, v in avg.items()},
             "step_ms_each": [round(v, 2) for v in step_ms],
             "roofline": roof if nrhs >= 8 else {
-                "kernel": "k_gemv (dense stiffness matvec, PAPER.md:629)", "bound": "hbm",
+                "kernel": "k_gemv_bulk (dense stiffness matvec, PAPER.md:629; TMA-engine bulk copies)", "bound": "hbm",
                 "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "peak_kind": peak_kind,
                 "traffic": 536881408 + 3397632 if (args.config == "c4" and world == 1) else None,

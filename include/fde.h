@@ -118,6 +118,9 @@ int fde_debug_trunc_stats(unsigned long long* out4);
  * factor is not usable for precond_apply).  Both compute the H-LU of
  * PAPER.md:598-606; FDE_EINVAL_PARAM for negative modes. */
 int fde_debug_hlu_mode(int mode);
+/* Diagnostics: reserved / used bytes of the device's default stream-ordered
+ * memory pool (every library buffer comes from it). */
+int fde_debug_pool_bytes(int device, unsigned long long* reserved, unsigned long long* used);
 
 /* Row-block sharding of the dense operator over `world` GPUs (host function,
  * usable without a device): rank owns internal rows [*r0, *r1) = the dofs of

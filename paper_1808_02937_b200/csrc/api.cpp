@@ -99,6 +99,8 @@ void fde_destroy(fde_handle h)
         cudaStreamDestroy(h->aux4);
         cudaStreamSynchronize(h->aux5);
         cudaStreamDestroy(h->aux5);
+        cudaStreamSynchronize(h->aux6);
+        cudaStreamDestroy(h->aux6);
         cudaStreamDestroy(h->aux);
         cudaStreamDestroy(h->aux2);
         cudaStreamDestroy(h->aux3);
@@ -144,6 +146,20 @@ int fde_debug_trunc_stats(unsigned long long* out4)
     fde_ctx* h = nullptr;
     API_BEGIN
     hlu_trunc_stats(out4);
+    API_END(h)
+}
+
+int fde_debug_pool_bytes(int device, unsigned long long* reserved, unsigned long long* used)
+{
+    fde_ctx* h = nullptr;
+    API_BEGIN
+    cudaMemPool_t pool;
+    FDE_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    unsigned long long r = 0, u = 0;
+    FDE_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &r));
+    FDE_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &u));
+    *reserved = r;
+    *used = u;
     API_END(h)
 }
 

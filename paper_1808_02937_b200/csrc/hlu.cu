@@ -519,7 +519,10 @@ __global__ void k_eye(double* B, long long ldb, int m)
 // A (n x n, ld n) -> eigenvalues on the diagonal, V eigenvectors (columns).
 __device__ int cta_jacobi(double* A, double* V, int n, int* pairs, double eps = 1e-15)
 {
-    // n even (caller pads)
+    // parallel cyclic Jacobi (n even, caller pads); A[c * n + r] symmetric.  Per
+    // round: the n/2 rotations of a tournament pairing, then A <- J^T A J and
+    // V <- V J in ONE pass over the 2 x 2 blocks of (pair, pair) (the pairs
+    // partition the indices, so the blocks are disjoint): two barriers per round.
     for (int t = threadIdx.x; t < n * n; t += blockDim.x) V[t] = ((t % n) == (t / n)) ? 1.0 : 0.0;
     __shared__ double cs[128], sn[128];
     __shared__ int conv;
@@ -555,27 +558,27 @@ __device__ int cta_jacobi(double* A, double* V, int n, int* pairs, double eps = 
                 sn[k] = s;
             }
             __syncthreads();
-            // A <- A J (columns p,q), V <- V J
+            // A <- J^T A J on the block (rows {p1,q1}, cols {p2,q2}) of pairs (k1, k2)
+            for (int t = threadIdx.x; t < half * half; t += blockDim.x) {
+                const int k1 = t % half, k2 = t / half;
+                const int p1 = pairs[2 * k1], q1 = pairs[2 * k1 + 1], p2 = pairs[2 * k2], q2 = pairs[2 * k2 + 1];
+                const double c1 = cs[k1], s1 = sn[k1], c2 = cs[k2], s2 = sn[k2];
+                const double app = A[p2 * n + p1], apq = A[q2 * n + p1], aqp = A[p2 * n + q1], aqq = A[q2 * n + q1];
+                const double xpp = c2 * app - s2 * apq, xpq = s2 * app + c2 * apq;   // columns
+                const double xqp = c2 * aqp - s2 * aqq, xqq = s2 * aqp + c2 * aqq;
+                A[p2 * n + p1] = c1 * xpp - s1 * xqp;                                  // rows
+                A[p2 * n + q1] = s1 * xpp + c1 * xqp;
+                A[q2 * n + p1] = c1 * xpq - s1 * xqq;
+                A[q2 * n + q1] = s1 * xpq + c1 * xqq;
+            }
+            // V <- V J (columns p, q of every pair)
             for (int t = threadIdx.x; t < half * n; t += blockDim.x) {
                 const int k = t / n, i = t - k * n;
                 const int p = pairs[2 * k], q = pairs[2 * k + 1];
                 const double c = cs[k], s = sn[k];
-                const double aip = A[p * n + i], aiq = A[q * n + i];
-                A[p * n + i] = c * aip - s * aiq;
-                A[q * n + i] = s * aip + c * aiq;
                 const double vip = V[p * n + i], viq = V[q * n + i];
                 V[p * n + i] = c * vip - s * viq;
                 V[q * n + i] = s * vip + c * viq;
-            }
-            __syncthreads();
-            // A <- J^T A (rows p,q)
-            for (int t = threadIdx.x; t < half * n; t += blockDim.x) {
-                const int k = t / n, j = t - k * n;
-                const int p = pairs[2 * k], q = pairs[2 * k + 1];
-                const double c = cs[k], s = sn[k];
-                const double apj = A[j * n + p], aqj = A[j * n + q];
-                A[j * n + p] = c * apj - s * aqj;
-                A[j * n + q] = s * apj + c * aqj;
             }
             __syncthreads();
         }

@@ -33,6 +33,7 @@
 
 #define H2_MMAX 128
 #define H2_STRIP 32
+#define H2_CP_CHUNK 4096   // elements per copy CTA
 
 struct H2Lu {
     double* D;
@@ -463,6 +464,8 @@ struct H2Plan {
     DBuf<TChunk> tc;
     double* tr_part = nullptr;
     double* tr_T = nullptr;
+    double* tr_part2 = nullptr;   // overflow truncations (their own stream)
+    double* tr_T2 = nullptr;
     int launches = 0;
 };
 
@@ -861,9 +864,9 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         tr_size(st.trunc_ov);
     }
     const int64_t off_part = words;
-    words += gmax;
+    words += 2 * gmax;   // [operand truncations | overflow truncations] (two streams)
     const int64_t off_T = words;
-    words += tmax;
+    words += 2 * tmax;
 
     H2Plan* P = new H2Plan();
     L->plan = P;
@@ -878,6 +881,8 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
     double* A = L->arena;
     P->tr_part = A + off_part;
     P->tr_T = A + off_T;
+    P->tr_part2 = A + off_part + gmax;
+    P->tr_T2 = A + off_T + tmax;
     auto res = [&](const VRef& r) -> double* {
         switch (r.sp) {
             case 0: return A + offD[r.id] + r.off;
@@ -957,9 +962,21 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
     };
     auto put_copy = [&](const std::vector<VCopy>& v, H2Launch& ln) {
         ln.cp0 = (int)vcp.size();
-        for (auto& c : v)
-            if (c.m > 0 && c.n > 0)
-                vcp.push_back({c.kind == 0 ? res(c.src) : nullptr, c.lds, res(c.dst), c.ldd, c.m, c.n, c.kind, c.alpha});
+        for (auto& c : v) {
+            if (c.m <= 0 || c.n <= 0) continue;
+            double* dst = res(c.dst);
+            const double* src = c.kind == 0 ? res(c.src) : nullptr;
+            if (c.kind == 2 || (int64_t)c.m * c.n <= H2_CP_CHUNK) {
+                vcp.push_back({src, c.lds, dst, c.ldd, c.m, c.n, c.kind, c.alpha});
+                continue;
+            }
+            // large copies: one CTA per chunk of <= H2_CP_CHUNK elements
+            const int rm = std::min(c.m, H2_CP_CHUNK), cn = std::max(1, H2_CP_CHUNK / rm);
+            for (int c0 = 0; c0 < c.n; c0 += cn)
+                for (int r0 = 0; r0 < c.m; r0 += rm)
+                    vcp.push_back({src ? src + (int64_t)c0 * c.lds + r0 : nullptr, c.lds, dst + (int64_t)c0 * c.ldd + r0,
+                                   c.ldd, std::min(rm, c.m - r0), std::min(cn, c.n - c0), c.kind, c.alpha});
+        }
         ln.ncp = (int)vcp.size() - ln.cp0;
     };
     auto put_panel = [&](const std::vector<VPanel>& v, H2Launch& ln) {
@@ -1047,7 +1064,15 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         for (auto& q : v) n_pan += (size_t)ceil_div(q.nvec, H2_STRIP);
     };
     auto cnt_cp = [&](const std::vector<VCopy>& v) {
-        for (auto& c : v) n_cp += (c.m > 0 && c.n > 0);
+        for (auto& c : v) {
+            if (c.m <= 0 || c.n <= 0) continue;
+            if (c.kind == 2 || (int64_t)c.m * c.n <= H2_CP_CHUNK) {
+                ++n_cp;
+                continue;
+            }
+            const int rm = std::min(c.m, H2_CP_CHUNK), cn = std::max(1, H2_CP_CHUNK / rm);
+            n_cp += (size_t)(ceil_div(c.n, cn) * ceil_div(c.m, rm));
+        }
     };
     cnt_cp(init_cp);
     cnt_trunc(init_trunc);
@@ -1105,6 +1130,8 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
     cudaEvent_t evA = L->h->ev_aux[0], evOp = L->h->ev_aux[1];
     cudaEvent_t evP = L->h->ev_aux[3], evC = L->h->ev_aux[4], evB = L->h->ev_aux[5], evD = L->h->ev_aux[6];
     cudaEvent_t evLU = L->h->ev_aux[7], evDg = L->h->ev_aux[8];
+    cudaEvent_t evCp = L->h->ev_aux[10], evOv = L->h->ev_aux[11];
+    cudaStream_t se = aux_stream6(L->h);   // overflow truncations
     FDE_CUDA(cudaEventRecord(evA, sa));   // (sa is ordered after the arena / descriptor allocations on s)
     FDE_CUDA(cudaStreamWaitEvent(sd, evA, 0));
     auto push = [&]() {
@@ -1139,20 +1166,22 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         FDE_CHECK_LAUNCH();
         ++nlaunch;
     };
-    auto run_trunc = [&](const H2Trunc& tr, cudaStream_t st) {
+    auto run_trunc = [&](const H2Trunc& tr, cudaStream_t st, int ws) {
         if (!tr.ne) return;
         const TEntry* E = P->te.p + tr.e0;
         const TChunk* C = P->tc.p + tr.c0;
-        k_bgram<<<tr.nc, 256, 0, st>>>(E, C, P->tr_part);
+        double* part = ws ? P->tr_part2 : P->tr_part;
+        double* Tt = ws ? P->tr_T2 : P->tr_T;
+        k_bgram<<<tr.nc, 256, 0, st>>>(E, C, part);
         FDE_CHECK_LAUNCH();
         const int kmax = tr.kmax, ne = (kmax + 1) & ~1;
         const size_t smem = (size_t)(2 * kmax * kmax + 3 * ne * ne + 2 * ne + 8) * sizeof(double);
         set_smem_once((const void*)k_bcore, (int)smem);
-        k_bcore<<<tr.ne, 256, smem, st>>>(E, C, P->tr_part, L->tol, rmax, P->tr_T, L->dflag.p + 1);
+        k_bcore<<<tr.ne, 256, smem, st>>>(E, C, part, L->tol, rmax, Tt, L->dflag.p + 1);
         FDE_CHECK_LAUNCH();
         const size_t asmem = (size_t)(kmax * rmax + TRUNC_CHUNK * kmax) * sizeof(double);
         set_smem_once((const void*)k_bapply, (int)asmem);
-        k_bapply<<<tr.nc, 256, asmem, st>>>(E, C, P->tr_T, rmax);
+        k_bapply<<<tr.nc, 256, asmem, st>>>(E, C, Tt, rmax);
         FDE_CHECK_LAUNCH();
         nlaunch += 3;
     };
@@ -1180,11 +1209,12 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
     FDE_CUDA(cudaMemsetAsync(A + lr_lo, 0, (size_t)(lr_hi - lr_lo) * sizeof(double), sa));
     FDE_CUDA(cudaStreamWaitEvent(sa, evD, 0));
     run_copy(P->init, sa);
-    run_trunc(P->init.tr, sa);
+    run_trunc(P->init.tr, sa, 0);
     FDE_CUDA(cudaEventRecord(evA, sa));
     FDE_CUDA(cudaStreamWaitEvent(sb, evA, 0));
     FDE_CUDA(cudaStreamWaitEvent(sc, evA, 0));
     FDE_CUDA(cudaStreamWaitEvent(sl, evA, 0));
+    FDE_CUDA(cudaStreamWaitEvent(se, evA, 0));
     FDE_CUDA(cudaEventRecord(evC, sc));
     const int kstop = g_hlu2_stop >= 0 ? std::min(g_hlu2_stop, nl) : nl;   // debug: partial sweep
     // debug timeline (FDE_DEBUG_TIMELINE): timed events per step and stream
@@ -1225,12 +1255,18 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         FDE_CUDA(cudaStreamWaitEvent(sb, evD, 0));
         FDE_CUDA(cudaStreamWaitEvent(sc, evD, 0));
         FDE_CUDA(cudaStreamWaitEvent(sl, evD, 0));
+        FDE_CUDA(cudaStreamWaitEvent(se, evD, 0));
         // sb (after the new columns of step k-1 and the panels of step k-1)
-        run_trunc(ln.tr, sb);
+        // se: overflow truncations, concurrently with the operand truncations (the
+        // blocks are disjoint); they only have to precede this step's new columns
+        FDE_CUDA(cudaEventRecord(evCp, sb));
+        FDE_CUDA(cudaStreamWaitEvent(se, evCp, 0));
+        run_trunc(ln.tr_ov, se, 1);
+        FDE_CUDA(cudaEventRecord(evOv, se));
+        mark(k, T_OV, se);
+        run_trunc(ln.tr, sb, 0);
         FDE_CUDA(cudaEventRecord(evOp, sb));
         mark(k, T_OP, sb);
-        run_trunc(ln.tr_ov, sb);
-        mark(k, T_OV, sb);
         // sa: critical chain.  LU(k) ran on sl (k = 0: here), overlapping the
         // products and updates of step k-1; its only input from step k-1 is the
         // update of the diagonal tile, issued right after the panels of step k-1.
@@ -1265,6 +1301,7 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         mark(k, T_CRIT, sa);
         // sb: new low-rank columns of step k (after the overflow truncations)
         FDE_CUDA(cudaStreamWaitEvent(sb, evP, 0));
+        FDE_CUDA(cudaStreamWaitEvent(sb, evOv, 0));
         run_copy(ln, sb);
         mark(k, T_CP, sb);
         // sc: the other dense updates of step k

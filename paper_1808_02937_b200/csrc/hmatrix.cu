@@ -220,6 +220,26 @@ void hm_leaves(const HStruct& S, int b, std::vector<int>& out)
     }
 }
 
+// one 32 x 32 tile of a dense leaf copied from the row-major dense operator
+struct LeafTile {
+    int64_t r, c;      // first row / column (internal order)
+    int64_t out;       // arena offset of the tile's first element
+    int64_t ldo;       // leaf rows (column-major ld)
+    int m, n;          // tile extent
+};
+
+__global__ void k_leaf_from_dense(const LeafTile* T, const double* __restrict__ A, long long lda, double* arena)
+{
+    __shared__ double t[32][33];
+    const LeafTile d = T[blockIdx.x];
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    for (int r = ty; r < d.m; r += 8)   // coalesced along the row of A
+        if (tx < d.n) t[r][tx] = A[(d.r + r) * lda + d.c + tx];
+    __syncthreads();
+    for (int c = ty; c < d.n; c += 8)   // coalesced along the leaf column
+        if (tx < d.m) arena[d.out + (int64_t)c * d.ldo + tx] = t[tx][c];
+}
+
 fde_hm* hm_build(fde_ctx* h, fde_op* op, int R, double lam, int n_min)
 {
     if (R < 1 || R > 32) fde_fail(FDE_EINVAL_PARAM, "hmatrix_build: R must be in [1, 32]");
@@ -349,7 +369,26 @@ fde_hm* hm_build(fde_ctx* h, fde_op* op, int R, double lam, int n_min)
             maxent = std::max(maxent, L.m * L.nc);
             ld.push_back(L);
         }
-        if (!ld.empty()) {
+        if (!ld.empty() && op->A.p && op->r0 == 0 && op->r1 == op->n) {
+            // the dense operator is resident with all rows: the exact entries of the
+            // inadmissible leaves are its sub-blocks -- one batched
+            // transposing copy (row-major A -> column-major leaves) instead of
+            // recomputing their pair moments
+            std::vector<LeafTile> lt;
+            for (auto& L : ld)
+                for (int c0 = 0; c0 < L.nc; c0 += 32)
+                    for (int r0 = 0; r0 < L.m; r0 += 32)
+                        lt.push_back(LeafTile{L.ra + r0, L.ca + c0, L.out + (int64_t)c0 * L.m + r0, L.m,
+                                              std::min(32, L.m - r0), std::min(32, L.nc - c0)});
+            DBuf<LeafTile> dlt;
+            dlt.upload(lt.data(), lt.size(), h->stream);
+            for (size_t base = 0; base < lt.size(); base += 65535u * 8) {
+                const unsigned cnt = (unsigned)std::min<size_t>(65535u * 8, lt.size() - base);
+                k_leaf_from_dense<<<cnt, dim3(32, 8), 0, h->stream>>>(dlt.p + base, op->A.p, op->lda, hm->dense.p);
+                FDE_CHECK_LAUNCH();
+            }
+            FDE_CUDA(cudaStreamSynchronize(h->stream));
+        } else if (!ld.empty()) {
             DBuf<int> di, dj;
             DBuf<long long> dsl;
             DBuf<double> ktab;

@@ -39,7 +39,7 @@ EXPORTED = [
     "sem_rhs", "stiffness_matvec", "hmatrix_build", "fde_hmatrix_get_info", "fde_hmatrix_dense_paper",
     "hlu_factor", "fde_hlu_get_info", "fde_hlu_dense_internal", "precond_apply", "solve", "fde_solve",
     "fde_free_operator", "fde_free_hmatrix", "fde_free_hlu", "fde_profile", "fde_profile_collect",
-    "fde_launch_count", "fde_shard_rows", "fde_debug_hlu_mode",
+    "fde_launch_count", "fde_shard_rows", "fde_debug_hlu_mode", "fde_debug_pool_bytes",
 ]
 
 
@@ -132,6 +132,7 @@ def lib():
         L.fde_shard_rows.argtypes = [i32, i32, i32, i32, ctypes.POINTER(i64), ctypes.POINTER(i64),
                                      ctypes.POINTER(i64)]
         L.fde_debug_hlu_mode.argtypes = [i32]
+        L.fde_debug_pool_bytes.argtypes = [i32, ctypes.POINTER(ctypes.c_ulonglong), ctypes.POINTER(ctypes.c_ulonglong)]
         L.fde_launch_count.argtypes = []
         L.fde_launch_count.restype = ctypes.c_longlong
         L.solve.argtypes = [vp, vp, vp, vp, vp, i32, i64, ctypes.POINTER(SolveOpts), ctypes.POINTER(SolveReport)]
@@ -371,3 +372,10 @@ def solve(handle: Handle, op: Operator, lu: Optional[HLU], G, method: int = GMRE
 def set_hlu_mode(mode: int) -> None:
     """0: leaf-ordered batched H-LU when the partition allows it (default), 1: recursive only."""
     _check(lib().fde_debug_hlu_mode(int(mode)))
+
+
+def pool_bytes(device: int = 0):
+    """(reserved, used) bytes of the device's default memory pool (diagnostics)."""
+    r, u = ctypes.c_ulonglong(), ctypes.c_ulonglong()
+    _check(lib().fde_debug_pool_bytes(int(device), ctypes.byref(r), ctypes.byref(u)))
+    return r.value, u.value

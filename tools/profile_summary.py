@@ -1,6 +1,6 @@
 """Write the per-round ncu summaries committed under profiles/ (dev tool).
 
-usage: python tools/profile_summary.py <launches.csv> <full.ncu-rep> <out_prefix>
+usage: python tools/profile_summary.py <launches.csv> <out_prefix> <full.ncu-rep> [more.ncu-rep ...]
 """
 import collections
 import csv
@@ -36,6 +36,7 @@ FULL_METRICS = [
     "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
     "sm__warps_active.avg.pct_of_peak_sustained_active",
     "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
+    "smsp__inst_executed.sum", "smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio",
 ]
 
 
@@ -54,22 +55,24 @@ def full(path):
 
 
 def main():
-    lcsv, rep, prefix = sys.argv[1], sys.argv[2], sys.argv[3]
+    lcsv, prefix, reps = sys.argv[1], sys.argv[2], sys.argv[3:]
     tot, cnt = launches(lcsv)
     S = sum(tot.values())
     with open(prefix + "_launches.txt", "w") as f:
         f.write(f"# ncu --metrics gpu__time_duration.sum --clock-control none launch list of\n"
-                f"#   python bench.py --steps 2 --warmup 1 --no-cpu-baseline  (cold-cache, serialised)\n"
+                f"#   python bench.py --steps 1 --warmup 1 --no-cpu-baseline  (cold-cache, serialised;\n"
+                f"#   the warm-up step and the end-to-end step are in the list too: 3 cold solves)\n"
                 f"# {sum(cnt.values())} launches, {S / 1e3:.1f} ms device time in total\n")
         f.write(f"{'kernel':30s} {'launches':>9s} {'total_ms':>10s} {'share':>7s} {'avg_us':>9s}\n")
         for k, v in tot.most_common():
             f.write(f"{k:30s} {cnt[k]:9d} {v / 1e3:10.2f} {100 * v / S:6.1f}% {v / cnt[k]:9.2f}\n")
     with open(prefix + "_full.txt", "w") as f:
         f.write("# ncu --set full --clock-control none (one launch each)\n")
-        for d in full(rep):
-            f.write(f"\n[{d.pop('kernel')}]\n")
-            for k, v in d.items():
-                f.write(f"  {k:62s} {v}\n")
+        for rep in reps:
+            for d in full(rep):
+                f.write(f"\n[{d.pop('kernel')}]  ({rep.split('/')[-1]})\n")
+                for k, v in d.items():
+                    f.write(f"  {k:62s} {v}\n")
 
 
 if __name__ == "__main__":
