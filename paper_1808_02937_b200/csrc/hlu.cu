@@ -582,12 +582,45 @@ __device__ int cta_jacobi(double* A, double* V, int n, int* pairs, double eps = 
             }
             __syncthreads();
         }
-        if (conv) return sweep + 1;
+        // every thread reads the flag before thread 0 resets it for the next sweep
+        // (otherwise threads could leave at different sweeps: divergent barriers)
+        const int done = conv;
+        __syncthreads();
+        if (done) return sweep + 1;
     }
     return 30;
 }
 
-__device__ unsigned long long g_trunc_stats[4];   // calls, sum ke, sum sweeps, max ke
+// debug bounds checking (FDE_H2_CHECK): valid [lo, hi) byte ranges of global data;
+// the first violation is recorded (the access is skipped) and reported by the host
+__device__ int g_h2_check = 0;
+__device__ const char* g_h2_lo[4];
+__device__ const char* g_h2_hi[4];
+struct H2Bad {
+    int tag, a, b;
+    const char* p;
+    long long nbytes;
+};
+__device__ H2Bad g_h2_bad;
+__device__ int g_h2_bad_flag = 0;
+__device__ __forceinline__ bool h2_chk(const void* p, long long nbytes, int tag, int a, int b)
+{
+    if (!g_h2_check) return true;
+    const char* c = (const char*)p;
+    for (int r = 0; r < 4; ++r)
+        if (g_h2_lo[r] && c >= g_h2_lo[r] && c + nbytes <= g_h2_hi[r]) return true;
+    if (atomicExch(&g_h2_bad_flag, 1) == 0) {
+        g_h2_bad.tag = tag;
+        g_h2_bad.a = a;
+        g_h2_bad.b = b;
+        g_h2_bad.p = c;
+        g_h2_bad.nbytes = nbytes;
+    }
+    return false;
+}
+
+__device__ unsigned long long g_trunc_stats[4];
+__device__ int g_trunc_check = 0;   // descriptor checks (FDE_DEBUG_SERIAL)   // calls, sum ke, sum sweeps, max ke
 
 // Truncation core (one CTA).  Input: Gram matrices Gu = U^T U, Gv = V^T V of a
 // low-rank sum U V^T with k columns (zero columns allowed: they are the unused
@@ -733,12 +766,20 @@ __global__ void __launch_bounds__(256) k_bgram(const TEntry* E, const TChunk* C,
     const double* M = ch.side ? e.V : e.U;
     const long long ld = ch.side ? e.n : e.m;
     const int k = e.k;
+    if (g_h2_check && !h2_chk(M + ch.r0, ((long long)(k - 1) * ld + ch.rows) * 8, 40 + ch.side, k, ch.rows)) return;
+    if (g_trunc_check && threadIdx.x == 0 &&
+        (k < 1 || k > TRUNC_KMAX || ch.rows < 1 || ch.rows > TRUNC_CHUNK || ch.e < 0 || !M || ch.r0 + ch.rows > ld)) {
+        printf("k_bgram: bad chunk %d: e %d side %d r0 %lld rows %d k %d ld %lld\n", blockIdx.x, ch.e, ch.side, ch.r0,
+               ch.rows, k, ld);
+        __trap();
+    }
     for (int t = threadIdx.x; t < ch.rows * k; t += blockDim.x) {
         const int r = t % ch.rows, j = t / ch.rows;
         tile[r * (TRUNC_KMAX + 1) + j] = M[(long long)j * ld + ch.r0 + r];
     }
     __syncthreads();
     double* out = part + e.gofs + (long long)(blockIdx.x - e.c_lo) * k * k;
+    if (g_h2_check && !h2_chk(out, (long long)k * k * 8, 42, k, blockIdx.x - e.c_lo)) return;
     for (int o = threadIdx.x; o < k * k; o += blockDim.x) {
         const int i = o % k, j = o / k;
         double s = 0.0;
@@ -753,6 +794,16 @@ __global__ void __launch_bounds__(256) k_bcore(const TEntry* E, const TChunk* C,
     extern __shared__ double sm[];
     const TEntry e = E[blockIdx.x];
     const int k = e.k;
+    if (g_h2_check && (!h2_chk(part + e.gofs, (long long)(e.c_hi - e.c_lo) * k * k * 8, 60, k, e.c_hi - e.c_lo) ||
+                       !h2_chk(T + e.tofs, 2LL * k * kc * 8, 61, k, kc)))
+        return;
+    if (g_trunc_check && threadIdx.x == 0 &&
+        (k < 1 || k > TRUNC_KMAX || e.c_lo < 0 || e.c_hi <= e.c_lo || e.c_hi - e.c_lo > 1 << 16 || e.gofs < 0 ||
+         e.tofs < 0 || kc > TRUNC_KMAX)) {
+        printf("k_bcore: bad entry %d: k %d c %d..%d gofs %lld tofs %lld kc %d\n", blockIdx.x, k, e.c_lo, e.c_hi,
+               e.gofs, e.tofs, kc);
+        __trap();
+    }
     double* Gu = sm;
     double* Gv = Gu + k * k;
     // fixed-order reduction of the chunk partials
@@ -875,10 +926,14 @@ __global__ void __launch_bounds__(256) k_bapply(const TEntry* E, const TChunk* C
     double* Ts = bsm;
     double* Ms = bsm + k * kc;
     const double* Tm = T + e.tofs + (ch.side ? (long long)k * kc : 0);
+    if (g_h2_check && !h2_chk(Tm, (long long)k * kc * 8, 54, k, kc)) return;
     for (int t = threadIdx.x; t < k * kc; t += blockDim.x) Ts[t] = Tm[t];
     const double* M = ch.side ? e.V : e.U;
     double* O = ch.side ? e.Vo : e.Uo;
     const long long ld = ch.side ? e.n : e.m;
+    if (g_h2_check && (!h2_chk(M + ch.r0, ((long long)(k - 1) * ld + ch.rows) * 8, 50 + ch.side, k, ch.rows) ||
+                       !h2_chk(O + ch.r0, ((long long)(max(k, kc) - 1) * ld + ch.rows) * 8, 52 + ch.side, k, kc)))
+        return;
     for (int t = threadIdx.x; t < ch.rows * k; t += blockDim.x) {
         const int r = t % ch.rows, q = t / ch.rows;
         Ms[q * TRUNC_CHUNK + r] = M[(long long)q * ld + ch.r0 + r];

@@ -78,6 +78,7 @@ struct H2Copy {   // kind 0: dst = alpha src, 1: dst = 0, 2: dst = I
 };
 
 // ----------------------------------------------------------------- kernels
+
 __device__ __forceinline__ void cp_async8(double* sdst, const double* gsrc)
 {
     const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
@@ -99,6 +100,7 @@ __global__ void __launch_bounds__(512) k_h2_lu(const H2Lu* tk, int* bad)
     extern __shared__ double lsm[];
     const H2Lu d = tk[blockIdx.x];
     const int m = d.m, tid = threadIdx.x, ti = tid & 31, tj = tid >> 5;
+    if (g_h2_check && !h2_chk(d.D, ((long long)(m - 1) * d.ld + m) * 8, 30, m, 0)) return;
     double* S = lsm;
     __shared__ double rp[M];
     for (int t = tid; t < M * M; t += 512) {
@@ -243,6 +245,11 @@ __global__ void __launch_bounds__(256) k_h2_panel(const H2Panel* P)
 {
     extern __shared__ double psm[];
     const H2Panel p = P[blockIdx.x];
+    if (g_h2_check) {
+        const long long ex = p.mode == 2 ? ((long long)(p.m - 1) * p.ldx + p.nvec) : ((long long)(p.nvec - 1) * p.ldx + p.m);
+        if (!h2_chk(p.T, ((long long)(p.m - 1) * p.ldt + p.m) * 8, 20, p.m, p.mode) || !h2_chk(p.X, ex * 8, 21, p.nvec, p.mode))
+            return;
+    }
     if (p.mode == 0) h2_panel_body<0>(p, psm);
     else if (p.mode == 1) h2_panel_body<1>(p, psm);
     else h2_panel_body<2>(p, psm);
@@ -310,6 +317,27 @@ __global__ void __launch_bounds__(256) k_h2_gemm(const H2Tile* tiles, const H2Ta
     }
     const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
     const int m0 = tl.m0, n0 = tl.n0, m = tk.m, n = tk.n;
+    __shared__ int sbad;
+    if (threadIdx.x == 0) sbad = 0;
+    if (g_h2_check && threadIdx.x == 0) {
+        // C: columns [n0, n0+64) rows [m0, m0+64) clipped
+        const int mm = min(GT, m - m0), nn = min(GT, n - n0);
+        if (mm > 0 && nn > 0) h2_chk(tk.C + (long long)n0 * tk.ldc + m0, ((long long)(nn - 1) * tk.ldc + mm) * 8, 1, m, n);
+        for (int q = 0; q < nt; ++q) {
+            const H2Term T = terms[tk.t_lo + q];
+            if (T.k <= 0) continue;
+            // A: op(A) is m x k; stored (ta ? k x m : m x k) column-major with lda
+            const long long ea = T.ta ? ((long long)(m0 + mm - 1) * T.lda + T.k) : ((long long)(T.k - 1) * T.lda + m0 + mm);
+            const long long sa = T.ta ? (long long)m0 * T.lda : m0;
+            h2_chk(T.A + sa, (ea - sa) * 8, 2, q, T.k);
+            const long long eb = T.tb ? ((long long)(T.k - 1) * T.ldb + n0 + nn) : ((long long)(n0 + nn - 1) * T.ldb + T.k);
+            const long long sb = T.tb ? n0 : (long long)n0 * T.ldb;
+            h2_chk(T.B + sb, (eb - sb) * 8, 3, q, T.k);
+        }
+        sbad = g_h2_bad_flag;
+    }
+    __syncthreads();
+    if (sbad) return;
     double acc[4][4];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
@@ -378,6 +406,11 @@ __global__ void __launch_bounds__(256) k_h2_copy(const H2Copy* C)
 {
     const H2Copy c = C[blockIdx.x];
     const long long tot = (long long)c.m * c.n;
+    if (g_h2_check) {
+        bool ok = h2_chk(c.dst, ((long long)(c.n - 1) * c.ldd + c.m) * 8, 10, c.m, c.n);
+        if (c.kind == 0) ok = ok && h2_chk(c.src, ((long long)(c.n - 1) * c.lds + c.m) * 8, 11, c.m, c.n);
+        if (!ok) return;
+    }
     for (long long t = threadIdx.x; t < tot; t += blockDim.x) {
         const int i = (int)(t % c.m), j = (int)(t / c.m);
         double v;
@@ -434,7 +467,9 @@ struct VStep {
     std::vector<VTask> g0, g1, g2, g3;   // conversions to dense, cores, products, dense updates
     std::vector<VTask> g3r;              // dense updates of tiles off row / column k+1 (lookahead stream)
     std::vector<char> g3crit;            // per g3 task: 2 tile (k+1, k+1), 1 row / column k+1 or (k+2, k+2), 0 rest
-    std::vector<VCopy> cp;           // low-rank target columns
+    std::vector<std::vector<VCopy>> cpr;    // new low-rank target columns, by round
+    std::vector<VCopy> snap;                // operand factor snapshots (after the panels)
+    std::vector<std::vector<VTrunc>> trmid; // truncations between rounds
     int64_t scratch = 0;
 };
 
@@ -443,6 +478,9 @@ struct H2Trunc {       // one batched truncation: ranges in the flat entry / chu
 };
 struct H2Launch {      // ranges in the flat device arrays
     H2Trunc tr, tr_ov;
+    std::vector<std::pair<int, int>> cpr;   // new low-rank columns by round (cp0, ncp)
+    int snap0 = 0, nsnap = 0;               // operand factor snapshots
+    std::vector<H2Trunc> trmid;             // truncations between the rounds
     int lu = -1;
     int pan0 = 0, npan = 0;
     int g_tile0[6] = {0, 0, 0, 0, 0, 0}, g_ntile[6] = {0, 0, 0, 0, 0, 0};
@@ -618,6 +656,22 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         struct Pair { int b, c; int64_t w; int rw; bool bl, cl; };   // bl/cl: operand types at this step   // w: W (n_c x kc_b) or Z (m_b x kc_c) scratch offset
         std::vector<Pair> pairs;
         int64_t scr = 0;
+        // snapshots of the low-rank operand factors read by this step's dense-target
+        // updates (U_b of the column panel, V_c of the row panel): the updates run
+        // concurrently with step k+1, whose truncations / panels rewrite the factors
+        std::map<int, int64_t> snapU, snapV;
+        for (int b : Cb)
+            if (isLR(b)) {
+                snapU[b] = scr;
+                st.snap.push_back({{1, b, 0}, {3, k & 1, scr}, S.bl[b].m, S.bl[b].m, (int)S.bl[b].m, kc[b], 0, 1.0});
+                scr += S.bl[b].m * kc[b];
+            }
+        for (int c : Rc)
+            if (isLR(c)) {
+                snapV[c] = scr;
+                st.snap.push_back({{2, c, 0}, {3, k & 1, scr}, S.bl[c].n, S.bl[c].n, (int)S.bl[c].n, kc[c], 0, 1.0});
+                scr += S.bl[c].n * kc[c];
+            }
         for (int b : Cb)
             for (int c : Rc) {
                 Pair pr{b, c, -1, 0, isLR(b), isLR(c)};
@@ -627,16 +681,16 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
                     if (isLR(c)) {   // core = U_c[k]^T V_b[k]  (kc_c x kc_b)
                         core = scr;
                         scr += (int64_t)kc[c] * kc[b];
-                        VTask t{{3, 0, core}, kc[c], kc[c], kc[b], 0.0, {}};
+                        VTask t{{3, k & 1, core}, kc[c], kc[c], kc[b], 0.0, {}};
                         t.terms.push_back({{1, c, lr0[k] - row0(c)}, {2, b, lr0[k] - col0(b)}, C.m, B.n, mk, 1, 0, 1.0});
                         st.g1.push_back(t);
                     }
                     pr.w = scr;
                     pr.rw = kc[b];
                     scr += C.n * kc[b];
-                    VTask t{{3, 0, pr.w}, C.n, (int)C.n, kc[b], 0.0, {}};
+                    VTask t{{3, k & 1, pr.w}, C.n, (int)C.n, kc[b], 0.0, {}};
                     if (isLR(c))   // W = V_c core
-                        t.terms.push_back({{2, c, 0}, {3, 0, core}, C.n, kc[c], kc[c], 0, 0, 1.0});
+                        t.terms.push_back({{2, c, 0}, {3, k & 1, core}, C.n, kc[c], kc[c], 0, 0, 1.0});
                     else           // W = D_c[k rows, :]^T V_b[k]
                         t.terms.push_back({{0, c, lr0[k] - row0(c)}, {2, b, lr0[k] - col0(b)}, C.m, B.n, mk, 1, 0, 1.0});
                     st.g2.push_back(t);
@@ -644,7 +698,7 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
                     pr.w = scr;
                     pr.rw = kc[c];
                     scr += B.m * kc[c];
-                    VTask t{{3, 0, pr.w}, B.m, (int)B.m, kc[c], 0.0, {}};
+                    VTask t{{3, k & 1, pr.w}, B.m, (int)B.m, kc[c], 0.0, {}};
                     t.terms.push_back({{0, b, (lr0[k] - col0(b)) * B.m}, {1, c, lr0[k] - row0(c)}, B.m, C.m, mk, 0, 0, 1.0});
                     st.g2.push_back(t);
                 }
@@ -652,7 +706,7 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
             }
         // targets
         ++tile_stamp_id;   // dense target tile (i, j) -> g3 task (stamped flat table)
-        struct Grp { int t, key, rank; int64_t slot; };
+        struct Grp { int t, key, rank; int64_t slot; int round; };
         std::map<std::pair<int, int>, int> lgrp;     // (target, key) -> group index
         std::vector<Grp> grps;
         std::vector<int> incoming(nb, 0);
@@ -697,7 +751,11 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
                 const HBlock& T = S.bl[t];
                 const int lim = trunc ? TRUNC_KMAX : (int)std::max<int64_t>(1, std::min(T.m, T.n) / 2);
                 if (!conv[t] && kc[t] + incoming[t] > lim) {
-                    if (trunc && rmax + incoming[t] <= lim) add_trunc(t, true);
+                    // truncated blocks: make room first; more new columns than a block can
+                    // hold are added in rounds with a truncation in between (below).
+                    // Exact mode (tol = 0): a block that would get wider than half its
+                    // smaller dimension is better stored dense.
+                    if (trunc) add_trunc(t, true);
                     else conv[t] = 1;
                 }
                 if (conv[t]) {   // D_t = U_t V_t^T, then a dense block for good
@@ -741,10 +799,10 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
                                 term = {{0, b, (lr0[k] - col0(b)) * B.m + (lr0[i] - row0(b))},
                                         {0, c, (lr0[j] - col0(c)) * C.m + (lr0[k] - row0(c))}, B.m, C.m, mk, 0, 0, -1.0};
                             } else if (pr.bl) {   // U_b[i rows] W[j rows]^T
-                                term = {{1, b, lr0[i] - row0(b)}, {3, 0, pr.w + (lr0[j] - col0(c))}, B.m, C.n,
+                                term = {{3, k & 1, snapU[b] + (lr0[i] - row0(b))}, {3, k & 1, pr.w + (lr0[j] - col0(c))}, B.m, C.n,
                                         kc[b], 0, 1, -1.0};
                             } else {               // Z[i rows] V_c[j rows]^T
-                                term = {{3, 0, pr.w + (lr0[i] - row0(b))}, {2, c, lr0[j] - col0(c)}, B.m, C.n,
+                                term = {{3, k & 1, pr.w + (lr0[i] - row0(b))}, {3, k & 1, snapV[c] + (lr0[j] - col0(c))}, B.m, C.n,
                                         kc[c], 0, 1, -1.0};
                             }
                             st.g3[ti].terms.push_back(term);
@@ -757,7 +815,7 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
                     if (it == lgrp.end()) {
                         gi = (int)grps.size();
                         lgrp[gk] = gi;
-                        grps.push_back({t, key, pr.bl ? kc[b] : kc[c], -1});
+                        grps.push_back({t, key, pr.bl ? kc[b] : kc[c], -1, 0});
                     } else {
                         gi = it->second;
                     }
@@ -765,15 +823,29 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
                 }
             }
         }
-        // slots and copies
+        // slots and copies; a target whose new columns do not fit gets them in rounds,
+        // truncated between rounds (formatted addition of the partial sums)
         std::vector<char> u_done(grps.size(), 0);
+        std::map<int, int> rnd;   // target -> current round
         for (size_t g = 0; g < grps.size(); ++g) {
             const int t = grps[g].t;
+            int& r = rnd[t];
+            if (trunc && kc[t] + grps[g].rank > TRUNC_KMAX) {
+                if (rmax + grps[g].rank > TRUNC_KMAX) return false;   // a single group never exceeds it
+                if ((int)st.trmid.size() <= r) st.trmid.resize(r + 1);
+                st.trmid[r].push_back({t, kc[t]});
+                ++r;
+                kc[t] = rmax;
+            }
+            grps[g].round = r;
             grps[g].slot = kc[t];
             kc[t] += grps[g].rank;
             kcap[t] = std::max(kcap[t], kc[t]);
             pend[t] = 1;
         }
+        int nround = 1;
+        for (auto& g : grps) nround = std::max(nround, g.round + 1);
+        st.cpr.resize(nround);
         for (auto& lt : lterms) {
             const Pair& pr = pairs[lt.first];
             Grp& g = grps[lt.second];
@@ -786,15 +858,15 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
             if (pr.bl) {
                 if (!u_done[lt.second]) {   // U slot rows R = U_b rows (once per group)
                     u_done[lt.second] = 1;
-                    st.cp.push_back({{1, b, R0 - row0(b)}, {1, t, us}, B.m, T.m, (int)(R1 - R0), g.rank, 0, 1.0});
+                    st.cpr[g.round].push_back({{1, b, R0 - row0(b)}, {1, t, us}, B.m, T.m, (int)(R1 - R0), g.rank, 0, 1.0});
                 }
-                st.cp.push_back({{3, 0, pr.w + (C0 - col0(c))}, {2, t, vs}, C.n, T.n, (int)(C1 - C0), g.rank, 0, -1.0});
+                st.cpr[g.round].push_back({{3, k & 1, pr.w + (C0 - col0(c))}, {2, t, vs}, C.n, T.n, (int)(C1 - C0), g.rank, 0, -1.0});
             } else {
                 if (!u_done[lt.second]) {   // V slot rows C = -V_c rows (once per group)
                     u_done[lt.second] = 1;
-                    st.cp.push_back({{2, c, C0 - col0(c)}, {2, t, vs}, C.n, T.n, (int)(C1 - C0), g.rank, 0, -1.0});
+                    st.cpr[g.round].push_back({{2, c, C0 - col0(c)}, {2, t, vs}, C.n, T.n, (int)(C1 - C0), g.rank, 0, -1.0});
                 }
-                st.cp.push_back({{3, 0, pr.w + (R0 - row0(b))}, {1, t, us}, B.m, T.m, (int)(R1 - R0), g.rank, 0, 1.0});
+                st.cpr[g.round].push_back({{3, k & 1, pr.w + (R0 - row0(b))}, {1, t, us}, B.m, T.m, (int)(R1 - R0), g.rank, 0, 1.0});
             }
         }
         st.scratch = scr;
@@ -844,8 +916,11 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
                     if (std::abs(i - j) == dd) w += (int64_t)lm(i) * lm(j);
         scr_max = std::max(scr_max, w);
     }
+    // step scratch (W / Z products, cores), double-buffered: the products of step k
+    // are read by the copies (stream sb) and the bulk updates (stream sc) of step k,
+    // which complete before the critical stream reaches the products of step k+2
     const int64_t off_scr = words;
-    words += scr_max;
+    words += 2 * scr_max;
     // truncation workspace (max over batches)
     int64_t gmax = 1, tmax = 1;
     auto tr_size = [&](const std::vector<VTrunc>& v) {
@@ -862,6 +937,7 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
     for (auto& st : steps) {
         tr_size(st.trunc);
         tr_size(st.trunc_ov);
+        for (auto& v : st.trmid) tr_size(v);
     }
     const int64_t off_part = words;
     words += 2 * gmax;   // [operand truncations | overflow truncations] (two streams)
@@ -888,7 +964,7 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
             case 0: return A + offD[r.id] + r.off;
             case 1: return A + offU[r.id] + r.off;
             case 2: return A + offV[r.id] + r.off;
-            case 3: return A + off_scr + r.off;
+            case 3: return A + off_scr + r.id * scr_max + r.off;
             case 4: return A + offLi[r.id] + r.off;
             case 5: return A + offUi[r.id] + r.off;
             case 6: return hm->dense.p + r.off;   // the H-matrix's own arenas (init copies)
@@ -1084,7 +1160,9 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         cnt_tasks(st.g1);
         cnt_tasks(st.g2);
         cnt_tasks(st.g3);
-        cnt_cp(st.cp);
+        for (auto& v : st.cpr) cnt_cp(v);
+        cnt_cp(st.snap);
+        for (auto& v : st.trmid) cnt_trunc(v);
     }
     cnt_cp(fin_cp);
     cnt_pan(fin_pv);
@@ -1132,11 +1210,23 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
     cudaEvent_t evLU = L->h->ev_aux[7], evDg = L->h->ev_aux[8];
     cudaEvent_t evCp = L->h->ev_aux[10], evOv = L->h->ev_aux[11];
     cudaStream_t se = aux_stream6(L->h);   // overflow truncations
+    // debug: fold auxiliary streams back onto the critical one (race bisection)
+    if (const char* f = getenv("FDE_H2_FOLD")) {
+        const std::string fs(f);
+        if (fs.find('c') != std::string::npos) sc = sa;
+        if (fs.find('e') != std::string::npos) se = sb;
+        if (fs.find('l') != std::string::npos) sl = sa;
+        if (fs.find('b') != std::string::npos) sb = sa;
+        if (fs.find('a') != std::string::npos) { sb = sa; sc = sa; se = sa; sl = sa; }
+    }
     FDE_CUDA(cudaEventRecord(evA, sa));   // (sa is ordered after the arena / descriptor allocations on s)
     FDE_CUDA(cudaStreamWaitEvent(sd, evA, 0));
+    const bool sync_push = getenv("FDE_H2_SYNCPUSH") != nullptr;   // debug
     auto push = [&]() {
         const size_t now[8] = {vlu.size(), vpan.size(), vterm.size(), vtask.size(),
                                vtile.size(), vcp.size(), vte.size(), vtc.size()};
+        for (int a = 0; a < 8; ++a)
+            if (now[a] > cap[a]) fde_fail(FDE_EINVAL_PARAM, "hlu_factor: descriptor count exceeds the plan (internal)");
         for (int a = 0; a < 8; ++a) {
             if (now[a] == stg[a].done) continue;
             const size_t off = stg[a].done * stg[a].elem, bytes = (now[a] - stg[a].done) * stg[a].elem;
@@ -1145,6 +1235,7 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
             stg[a].done = now[a];
         }
         FDE_CUDA(cudaEventRecord(evD, sd));
+        if (sync_push) FDE_CUDA(cudaStreamSynchronize(sd));
     };
     const double ms_flat0 = ms_since(t_flat0);
     L->plan_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_plan0).count();
@@ -1160,11 +1251,36 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
     set_smem_once((const void*)k_h2_lu, lu_smem);
     set_smem_once((const void*)k_h2_gemm, H2G_SMEM);
     int nlaunch = 0;
+    // FDE_DEBUG_SERIAL: synchronise after every launch and name the first failing one
+    const bool dbg_serial = getenv("FDE_DEBUG_SERIAL") != nullptr;
+    {
+        const int on = getenv("FDE_H2_CHECK") ? 1 : 0;
+        const char* lo[4] = {(const char*)A, (const char*)hm->dense.p, (const char*)hm->lr.p, nullptr};
+        const char* hi[4] = {(const char*)(A + words), (const char*)(hm->dense.p + hm->dense.n),
+                             (const char*)(hm->lr.p + hm->lr.n), nullptr};
+        FDE_CUDA(cudaMemcpyToSymbolAsync(g_h2_check, &on, sizeof(int), 0, cudaMemcpyHostToDevice, sa));
+        FDE_CUDA(cudaMemcpyToSymbolAsync(g_h2_lo, lo, sizeof(lo), 0, cudaMemcpyHostToDevice, sa));
+        FDE_CUDA(cudaMemcpyToSymbolAsync(g_h2_hi, hi, sizeof(hi), 0, cudaMemcpyHostToDevice, sa));
+    }
+    {
+        const int chk = dbg_serial ? 1 : 0;
+        FDE_CUDA(cudaMemcpyToSymbolAsync(g_trunc_check, &chk, sizeof(int), 0, cudaMemcpyHostToDevice, sa));
+    }
+    int dbg_step = -1;
+    auto dbg = [&](const char* what) {
+        if (!dbg_serial) return;
+        const cudaError_t e = cudaDeviceSynchronize();
+        if (e != cudaSuccess) {
+            fprintf(stderr, "hlu2 debug: %s at step %d failed: %s\n", what, dbg_step, cudaGetErrorString(e));
+            fde_fail(FDE_ECUDA, std::string("hlu2 debug: ") + what + ": " + cudaGetErrorString(e));
+        }
+    };
     auto run_copy = [&](const H2Launch& ln, cudaStream_t st) {
         if (!ln.ncp) return;
         k_h2_copy<<<ln.ncp, 256, 0, st>>>(P->cps.p + ln.cp0);
         FDE_CHECK_LAUNCH();
         ++nlaunch;
+        dbg("copy");
     };
     auto run_trunc = [&](const H2Trunc& tr, cudaStream_t st, int ws) {
         if (!tr.ne) return;
@@ -1174,15 +1290,18 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         double* Tt = ws ? P->tr_T2 : P->tr_T;
         k_bgram<<<tr.nc, 256, 0, st>>>(E, C, part);
         FDE_CHECK_LAUNCH();
+        dbg("bgram");
         const int kmax = tr.kmax, ne = (kmax + 1) & ~1;
         const size_t smem = (size_t)(2 * kmax * kmax + 3 * ne * ne + 2 * ne + 8) * sizeof(double);
         set_smem_once((const void*)k_bcore, (int)smem);
         k_bcore<<<tr.ne, 256, smem, st>>>(E, C, part, L->tol, rmax, Tt, L->dflag.p + 1);
         FDE_CHECK_LAUNCH();
+        dbg("bcore");
         const size_t asmem = (size_t)(kmax * rmax + TRUNC_CHUNK * kmax) * sizeof(double);
         set_smem_once((const void*)k_bapply, (int)asmem);
         k_bapply<<<tr.nc, 256, asmem, st>>>(E, C, Tt, rmax);
         FDE_CHECK_LAUNCH();
+        dbg("bapply");
         nlaunch += 3;
     };
     auto run_gemm = [&](const H2Launch& ln, int w, cudaStream_t st) {
@@ -1190,12 +1309,16 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         k_h2_gemm<<<ln.g_ntile[w], 256, H2G_SMEM, st>>>(P->tiles.p + ln.g_tile0[w], P->tasks.p, P->terms.p);
         FDE_CHECK_LAUNCH();
         ++nlaunch;
+        static const char* gname[6] = {"gemm cores", "gemm products", "gemm crit", "gemm conversions", "gemm rest",
+                                       "gemm diag"};
+        dbg(gname[w]);
     };
     auto run_panel = [&](const H2Launch& ln) {
         if (!ln.npan) return;
         k_h2_panel<<<ln.npan, 256, pan_smem, sa>>>(P->pan.p + ln.pan0);
         FDE_CHECK_LAUNCH();
         ++nlaunch;
+        dbg("panel");
     };
     // init (+ every diagonal-tile LU descriptor: LU(k+1) is issued during step k)
     put_copy(init_cp, P->init);
@@ -1232,6 +1355,7 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         if (tline) FDE_CUDA(cudaEventRecord(tev[(size_t)k * T_N + w], st));
     };
     for (int k = 0; k < kstop; ++k) {
+        dbg_step = k;
         // flatten step k (the device is still busy with step k-1) and stage it
         H2Launch& ln = P->steps[k];
         VStep& st = steps[k];
@@ -1241,7 +1365,23 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         put_gemm(st.g0, ln, 3);
         put_gemm(st.g1, ln, 0);
         put_gemm(st.g2, ln, 1);
-        put_copy(st.cp, ln);
+        {
+            H2Launch tmp;
+            put_copy(st.snap, tmp);
+            ln.snap0 = tmp.cp0;
+            ln.nsnap = tmp.ncp;
+        }
+        ln.cpr.clear();
+        ln.trmid.clear();
+        for (size_t r = 0; r < st.cpr.size(); ++r) {
+            H2Launch tmp;
+            put_copy(st.cpr[r], tmp);
+            ln.cpr.push_back({tmp.cp0, tmp.ncp});
+            if (r < st.trmid.size()) {
+                ln.trmid.emplace_back();
+                put_trunc(st.trmid[r], ln.trmid.back());
+            }
+        }
         {   // split the dense updates: row / column k+1 (needed by step k+1) vs the rest
             std::vector<VTask> diag, crit, rest;
             for (size_t q = 0; q < st.g3.size(); ++q)
@@ -1251,6 +1391,7 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
             put_gemm(diag, ln, 5);
         }
         push();
+        dbg("push");
         FDE_CUDA(cudaStreamWaitEvent(sa, evD, 0));
         FDE_CUDA(cudaStreamWaitEvent(sb, evD, 0));
         FDE_CUDA(cudaStreamWaitEvent(sc, evD, 0));
@@ -1280,6 +1421,12 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         FDE_CUDA(cudaStreamWaitEvent(sa, evOp, 0));
         run_panel(ln);
         mark(k, T_PAN, sa);
+        if (ln.nsnap) {
+            k_h2_copy<<<ln.nsnap, 256, 0, sa>>>(P->cps.p + ln.snap0);
+            FDE_CHECK_LAUNCH();
+            ++nlaunch;
+            dbg("snapshots");
+        }
         run_gemm(ln, 5, sa);                         // diagonal tile (k+1, k+1)
         if (k + 1 < kstop) {
             FDE_CUDA(cudaEventRecord(evDg, sa));
@@ -1287,6 +1434,7 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
             k_h2_lu<<<1, 512, lu_smem, sl>>>(P->lu.p + P->steps[k + 1].lu, L->dflag.p);
             FDE_CHECK_LAUNCH();
             ++nlaunch;
+            dbg("lu");
             FDE_CUDA(cudaEventRecord(evLU, sl));
             mark(k, T_LU, sl);
         }
@@ -1302,7 +1450,14 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         // sb: new low-rank columns of step k (after the overflow truncations)
         FDE_CUDA(cudaStreamWaitEvent(sb, evP, 0));
         FDE_CUDA(cudaStreamWaitEvent(sb, evOv, 0));
-        run_copy(ln, sb);
+        for (size_t r = 0; r < ln.cpr.size(); ++r) {
+            if (ln.cpr[r].second) {
+                k_h2_copy<<<ln.cpr[r].second, 256, 0, sb>>>(P->cps.p + ln.cpr[r].first);
+                FDE_CHECK_LAUNCH();
+                ++nlaunch;
+            }
+            if (r < ln.trmid.size()) run_trunc(ln.trmid[r], sb, 0);
+        }
         mark(k, T_CP, sb);
         // sc: the other dense updates of step k
         FDE_CUDA(cudaStreamWaitEvent(sc, evP, 0));
@@ -1334,6 +1489,7 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         fprintf(stderr, "\n");
         for (auto& e : tev) cudaEventDestroy(e);
         cudaEventDestroy(t0ev);
+        (void)cudaGetLastError();   // elapsed-time queries of unrecorded marks leave an error behind
     }
     FDE_CUDA(cudaEventRecord(evB, sb));
     FDE_CUDA(cudaStreamWaitEvent(sa, evB, 0));
@@ -1358,6 +1514,28 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
     }
     FDE_CUDA(cudaEventRecord(evS, sa));
     FDE_CUDA(cudaStreamWaitEvent(s, evS, 0));
+    if (getenv("FDE_H2_CHECK")) {
+        FDE_CUDA(cudaDeviceSynchronize());
+        H2Bad bad{};
+        FDE_CUDA(cudaMemcpyFromSymbol(&bad, g_h2_bad, sizeof(H2Bad)));
+        if (bad.tag)
+            fprintf(stderr, "hlu2 bounds: tag %d (%d, %d) ptr %p bytes %lld arena [%p, %p)\n", bad.tag, bad.a, bad.b,
+                    (void*)bad.p, bad.nbytes, (void*)A, (void*)(A + words));
+        const int z = 0;
+        FDE_CUDA(cudaMemcpyToSymbol(g_h2_bad_flag, &z, sizeof(int)));
+        H2Bad zb{};
+        FDE_CUDA(cudaMemcpyToSymbol(g_h2_bad, &zb, sizeof(H2Bad)));
+    }
+    if (getenv("FDE_DEBUG_PLAN")) {
+        int nconv = 0;
+        int64_t wconv = 0;
+        for (int b = 0; b < nb; ++b)
+            if (dyn[b]) {
+                ++nconv;
+                wconv += S.bl[b].m * S.bl[b].n;
+            }
+        fprintf(stderr, "hlu2 plan: %d low-rank blocks converted to dense (%.1f MB)\n", nconv, wconv * 8e-6);
+    }
     if (getenv("FDE_DEBUG_PLAN"))
         fprintf(stderr, "hlu2 plan: nl %d blocks %d | simulate %.2f ms, layout+alloc %.2f ms, counts %.2f ms, "
                         "plan+launch total %.2f ms | tiles %zu terms %zu copies %zu panels %zu trunc %zu\n",
