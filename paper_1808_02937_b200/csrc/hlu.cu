@@ -1858,7 +1858,7 @@ namespace cg = cooperative_groups;
 
 #define APPLY_CTAS 8
 #define APPLY_THREADS 512
-#define PROJ_CHUNK 1024
+#define PROJ_CHUNK 256   // projection rows per warp task (8 loads per lane)
 #define APPLY_TSM 4096
 #define APPLY_RC 8      // right-hand sides per register chunk
 
@@ -1868,6 +1868,7 @@ struct SLeaf {
     const double* inv;      // m x m column-major
     int d_lo, d_hi;         // dense blocks in this leaf row
     int l_lo, l_hi;         // low-rank row contributions
+    int kq;                 // max kc over [l_lo, l_hi)
     int p_lo, p_hi;         // projections enabled after this leaf
 };
 struct SDense {
@@ -1994,16 +1995,30 @@ __device__ void run_sweep(const SweepDev& S, int backward, double* x, long long 
                 const int row = r_lo + i;
                 for (int d = L.d_lo; d < L.d_hi; ++d) {
                     const SDense D = S.dense[d];
-                    for (int j = ph; j < D.nc; j += nph) {
-                        const double a = D.D[(long long)j * D.ldd + D.roff + row];
+                    // four independent column loads in flight per thread
+                    for (int j0 = ph; j0 < D.nc; j0 += 4 * nph) {
+                        double a[4];
 #pragma unroll
-                        for (int cc = 0; cc < APPLY_RC; ++cc)
-                            if (cc < nc) acc[cc] = fma(a, ldcg(x + (long long)(c0 + cc) * ldx + D.c0 + j), acc[cc]);
+                        for (int u = 0; u < 4; ++u) {
+                            const int j = j0 + u * nph;
+                            a[u] = (j < D.nc) ? D.D[(long long)j * D.ldd + D.roff + row] : 0.0;
+                        }
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const int j = j0 + u * nph;
+                            if (j < D.nc)
+#pragma unroll
+                                for (int cc = 0; cc < APPLY_RC; ++cc)
+                                    if (cc < nc) acc[cc] = fma(a[u], ldcg(x + (long long)(c0 + cc) * ldx + D.c0 + j), acc[cc]);
+                        }
                     }
                 }
-                for (int l = L.l_lo + ph; l < L.l_hi; l += nph) {
+                // low-rank row terms: (term, column) pairs spread over all phases
+                for (int lq = ph; lq < (L.l_hi - L.l_lo) * L.kq; lq += nph) {
+                    const int l = L.l_lo + lq / L.kq, q = lq % L.kq;
                     const SLRRow R = S.lrr[l];
-                    for (int q = 0; q < R.kc; ++q) {
+                    if (q >= R.kc) continue;
+                    {
                         const double u = R.U[(long long)q * R.ldu + R.roff + row];
 #pragma unroll
                         for (int cc = 0; cc < APPLY_RC; ++cc) {
@@ -2044,11 +2059,19 @@ __device__ void run_sweep(const SweepDev& S, int backward, double* x, long long 
                 const SProj Pj = S.proj[p];
                 const int col = q / Pj.nchunk, ch = q - col * Pj.nchunk;
                 const int i0 = ch * PROJ_CHUNK, i1 = min(Pj.n, i0 + PROJ_CHUNK);
+                const double* vc = Pj.V + (long long)col * Pj.ldv;
                 for (int c = 0; c < nrhs; ++c) {
-                    const double* xc = x + (long long)c * ldx;
+                    const double* xc = x + (long long)c * ldx + Pj.c0;
+                    // all loads of the lane first (independent), then a fixed-order sum
+                    double a[PROJ_CHUNK / 32];
+#pragma unroll
+                    for (int u = 0; u < PROJ_CHUNK / 32; ++u) {
+                        const int i = i0 + lane + 32 * u;
+                        a[u] = (i < i1) ? vc[i] * ldcg(xc + i) : 0.0;
+                    }
                     double acc = 0.0;
-                    for (int i = i0 + lane; i < i1; i += 32)
-                        acc = fma(Pj.V[(long long)col * Pj.ldv + i], ldcg(xc + Pj.c0 + i), acc);
+#pragma unroll
+                    for (int u = 0; u < PROJ_CHUNK / 32; ++u) acc += a[u];
 #pragma unroll
                     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
                     if (lane == 0) t[(long long)c * tstride + Pj.tslot + col * Pj.nchunk + ch] = acc;
@@ -2068,11 +2091,21 @@ __device__ void run_sweep(const SweepDev& S, int backward, double* x, long long 
 #pragma unroll
                 for (int cc = 0; cc < APPLY_RC; ++cc) acc[cc] = 0.0;
                 if (ph < nph && i < nr)
-                    for (int j = ph; j < L.m; j += nph) {
-                        const double a = L.inv[(long long)j * L.m + r_lo + i];
+                    for (int j0 = ph; j0 < L.m; j0 += 4 * nph) {   // four independent loads in flight
+                        double a[4];
 #pragma unroll
-                        for (int cc = 0; cc < APPLY_RC; ++cc)
-                            if (cc < nc) acc[cc] = fma(a, ldcg(z + (long long)(c0 + cc) * L.m + j), acc[cc]);
+                        for (int u = 0; u < 4; ++u) {
+                            const int j = j0 + u * nph;
+                            a[u] = (j < L.m) ? L.inv[(long long)j * L.m + r_lo + i] : 0.0;
+                        }
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const int j = j0 + u * nph;
+                            if (j < L.m)
+#pragma unroll
+                                for (int cc = 0; cc < APPLY_RC; ++cc)
+                                    if (cc < nc) acc[cc] = fma(a[u], ldcg(z + (long long)(c0 + cc) * L.m + j), acc[cc]);
+                        }
                     }
                 for (int cc = 0; cc < nc; ++cc) {
                     const double s2 = apply_row_sum(acc[cc], nrp, part);
@@ -2236,6 +2269,8 @@ static ApplySched* apply_sched_build(fde_lu* L)
             s.l_lo = (int)rv.size();
             rv.insert(rv.end(), l[q].begin(), l[q].end());
             s.l_hi = (int)rv.size();
+            s.kq = 0;
+            for (const SLRRow& r : l[q]) s.kq = std::max(s.kq, r.kc);
             s.p_lo = (int)pv.size();
             pv.insert(pv.end(), p[q].begin(), p[q].end());
             s.p_hi = (int)pv.size();
