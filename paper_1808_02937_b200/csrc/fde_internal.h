@@ -105,7 +105,7 @@ struct fde_ctx {
     // (created on first use; ordered by events, never by implicit synchronisation)
     int* pinned = nullptr;   // small page-locked read-back buffer (allocated once per handle)
     cudaStream_t aux = nullptr, aux2 = nullptr, aux3 = nullptr, aux4 = nullptr, aux5 = nullptr, aux6 = nullptr;
-    cudaEvent_t ev_aux[12] = {};
+    cudaEvent_t ev_aux[16] = {};
     void* stage = nullptr;   // page-locked staging of descriptor uploads (grow-only)
     size_t stage_bytes = 0;
 };

@@ -517,68 +517,118 @@ __global__ void k_eye(double* B, long long ldb, int m)
 
 // ---- truncation core: parallel cyclic Jacobi on symmetric matrices in smem
 // A (n x n, ld n) -> eigenvalues on the diagonal, V eigenvectors (columns).
-__device__ int cta_jacobi(double* A, double* V, int n, int* pairs, double eps = 1e-15)
+// 1 / x and 1 / sqrt(x) (x > 0, normal): MUFU approximations + two Newton steps
+__device__ __forceinline__ double rcp_nr(double x)
 {
-    // parallel cyclic Jacobi (n even, caller pads); A[c * n + r] symmetric.  Per
-    // round: the n/2 rotations of a tournament pairing, then A <- J^T A J and
-    // V <- V J in ONE pass over the 2 x 2 blocks of (pair, pair) (the pairs
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    r = r * fma(-x, r, 2.0);
+    return r * fma(-x, r, 2.0);
+}
+__device__ __forceinline__ double rsqrt_nr(double x)
+{
+    double r;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    r = r * fma(-0.5 * x * r, r, 1.5);
+    return r * fma(-0.5 * x * r, r, 1.5);
+}
+
+// tournament pairing of round `round` (player 0 fixed, the others rotate), pair k < n/2
+__device__ __forceinline__ void jpair(int k, int round, int n, int& p, int& q)
+{
+    int a = 0;
+    if (k) {
+        a = k - 1 + round;
+        if (a >= n - 1) a -= n - 1;
+        ++a;
+    }
+    int b = n - 2 - k + round;
+    if (b >= n - 1) b -= n - 1;
+    ++b;
+    p = min(a, b);
+    q = max(a, b);
+}
+
+__device__ int cta_jacobi(double* A, double* V, int n, int* /*unused*/, double eps = 1e-15, double arel = 1e-17)
+{
+    // parallel cyclic Jacobi (n even, n <= 256, caller pads); A[c * n + r] symmetric.
+    // Per round: the n/2 rotations of a tournament pairing, then A <- J^T A J
+    // and V <- V J in ONE pass over the 2 x 2 blocks of (pair, pair) (the pairs
     // partition the indices, so the blocks are disjoint): two barriers per round.
     for (int t = threadIdx.x; t < n * n; t += blockDim.x) V[t] = ((t % n) == (t / n)) ? 1.0 : 0.0;
     __shared__ double cs[128], sn[128];
     __shared__ int conv;
     __shared__ double afro;
     const int half = n / 2;
-    if (threadIdx.x == 0) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    if (w == 0) {   // ||A||_F (fixed order)
         double f = 0.0;
-        for (int t = 0; t < n * n; ++t) f += A[t] * A[t];
-        afro = sqrt(f);
+        for (int t = lane; t < n * n; t += 32) f = fma(A[t], A[t], f);
+        for (int o = 16; o; o >>= 1) f += __shfl_xor_sync(0xffffffffu, f, o);
+        if (lane == 0) afro = sqrt(f);
     }
     __syncthreads();
+    const double athr = arel * afro + 1e-300, eps2 = eps * eps;
     for (int sweep = 0; sweep < 30; ++sweep) {
         if (threadIdx.x == 0) conv = 1;
         __syncthreads();
         for (int round = 0; round < n - 1; ++round) {
-            // tournament pairing: player 0 fixed, others rotate
-            for (int k = threadIdx.x; k < half; k += blockDim.x) {
-                int a = (k == 0) ? 0 : 1 + ((k - 1 + round) % (n - 1));
-                int b = 1 + ((n - 2 - k + round) % (n - 1));
-                int p = min(a, b), q = max(a, b);
-                pairs[2 * k] = p;
-                pairs[2 * k + 1] = q;
+            for (int kr = threadIdx.x; kr < half; kr += blockDim.x) {
+                int p, q;
+                jpair(kr, round, n, p, q);
                 const double app = A[p * n + p], aqq = A[q * n + q], apq = A[q * n + p];
                 double c = 1.0, s = 0.0;
-                if (fabs(apq) > eps * sqrt(fabs(app * aqq)) + 1e-17 * afro + 1e-300) {
+                if (fabs(apq) > athr && apq * apq > eps2 * fabs(app * aqq)) {
                     conv = 0;
-                    const double tau = (aqq - app) / (2.0 * apq);
-                    const double tt = (tau >= 0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
-                    c = 1.0 / sqrt(1.0 + tt * tt);
-                    s = tt * c;
+                    // t = sign(tau) / (|tau| + sqrt(1 + tau^2)), tau = (aqq - app) / (2 apq),
+                    // written as sign(d) e / (|d| + sqrt(d^2 + e^2)) (d = aqq - app, e = 2 apq)
+                    // with hardware approximations refined by Newton steps (the
+                    // rotation stays orthogonal: c and s are computed from the same t)
+                    const double d = aqq - app, e = 2.0 * apq;
+                    const double x = fma(d, d, e * e);
+                    double t;
+                    if (x > 1e-290) {
+                        const double h = x * rsqrt_nr(x);
+                        t = (d >= 0.0 ? e : -e) * rcp_nr(fabs(d) + h);
+                    } else {   // tiny entries (squares near underflow)
+                        const double tau = d / e;
+                        t = (tau >= 0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+                    }
+                    c = rsqrt_nr(fma(t, t, 1.0));
+                    s = t * c;
                 }
-                cs[k] = c;
-                sn[k] = s;
+                cs[kr] = c;
+                sn[kr] = s;
             }
             __syncthreads();
-            // A <- J^T A J on the block (rows {p1,q1}, cols {p2,q2}) of pairs (k1, k2)
-            for (int t = threadIdx.x; t < half * half; t += blockDim.x) {
-                const int k1 = t % half, k2 = t / half;
-                const int p1 = pairs[2 * k1], q1 = pairs[2 * k1 + 1], p2 = pairs[2 * k2], q2 = pairs[2 * k2 + 1];
-                const double c1 = cs[k1], s1 = sn[k1], c2 = cs[k2], s2 = sn[k2];
-                const double app = A[p2 * n + p1], apq = A[q2 * n + p1], aqp = A[p2 * n + q1], aqq = A[q2 * n + q1];
-                const double xpp = c2 * app - s2 * apq, xpq = s2 * app + c2 * apq;   // columns
-                const double xqp = c2 * aqp - s2 * aqq, xqq = s2 * aqp + c2 * aqq;
-                A[p2 * n + p1] = c1 * xpp - s1 * xqp;                                  // rows
-                A[p2 * n + q1] = s1 * xpp + c1 * xqp;
-                A[q2 * n + p1] = c1 * xpq - s1 * xqq;
-                A[q2 * n + q1] = s1 * xpq + c1 * xqq;
+            // A <- J^T A J on the block (rows {p1,q1}, cols {p2,q2}) of pairs (k1 = lane, ..., k2)
+            for (int k1 = lane; k1 < half; k1 += 32) {
+                int p1, q1;
+                jpair(k1, round, n, p1, q1);
+                const double c1 = cs[k1], s1 = sn[k1];
+                for (int k2 = w; k2 < half; k2 += nw) {
+                    int p2, q2;
+                    jpair(k2, round, n, p2, q2);
+                    const double c2 = cs[k2], s2 = sn[k2];
+                    const double app = A[p2 * n + p1], apq = A[q2 * n + p1], aqp = A[p2 * n + q1], aqq = A[q2 * n + q1];
+                    const double xpp = c2 * app - s2 * apq, xpq = s2 * app + c2 * apq;   // columns
+                    const double xqp = c2 * aqp - s2 * aqq, xqq = s2 * aqp + c2 * aqq;
+                    A[p2 * n + p1] = c1 * xpp - s1 * xqp;                                  // rows
+                    A[p2 * n + q1] = s1 * xpp + c1 * xqp;
+                    A[q2 * n + p1] = c1 * xpq - s1 * xqq;
+                    A[q2 * n + q1] = s1 * xpq + c1 * xqq;
+                }
             }
-            // V <- V J (columns p, q of every pair)
-            for (int t = threadIdx.x; t < half * n; t += blockDim.x) {
-                const int k = t / n, i = t - k * n;
-                const int p = pairs[2 * k], q = pairs[2 * k + 1];
+            // V <- V J (columns p, q of every pair k = w, w + nw, ...; rows i = lane, lane + 32)
+            for (int k = w; k < half; k += nw) {
+                int p, q;
+                jpair(k, round, n, p, q);
                 const double c = cs[k], s = sn[k];
-                const double vip = V[p * n + i], viq = V[q * n + i];
-                V[p * n + i] = c * vip - s * viq;
-                V[q * n + i] = s * vip + c * viq;
+                for (int i = lane; i < n; i += 32) {
+                    const double vip = V[p * n + i], viq = V[q * n + i];
+                    V[p * n + i] = c * vip - s * viq;
+                    V[q * n + i] = s * vip + c * viq;
+                }
             }
             __syncthreads();
         }
@@ -737,6 +787,7 @@ __global__ void __launch_bounds__(256) k_trunc_core(const double* Gu, const doub
 // eigen-solves in shared memory), and the transform products per chunk.
 #define TRUNC_KMAX 64
 #define TRUNC_CHUNK 64
+#define GRAM_SLOT(k) ((k) * (k) + 1)   // partial Gram of one chunk + its nonzero-column mask
 
 struct TEntry {
     const double* U;     // m x k (ld m)
@@ -761,6 +812,8 @@ __global__ void __launch_bounds__(256) k_bgram(const TEntry* E, const TChunk* C,
 {
     // tile[r][j] (row-major, padded: the k dot products of one row are conflict free)
     __shared__ double tile[TRUNC_CHUNK * (TRUNC_KMAX + 1)];
+    __shared__ unsigned long long msk;
+    __shared__ int cidx[TRUNC_KMAX];
     const TChunk ch = C[blockIdx.x];
     const TEntry e = E[ch.e];
     const double* M = ch.side ? e.V : e.U;
@@ -773,28 +826,51 @@ __global__ void __launch_bounds__(256) k_bgram(const TEntry* E, const TChunk* C,
                ch.rows, k, ld);
         __trap();
     }
+    if (threadIdx.x == 0) msk = 0ull;
+    __syncthreads();
+    // columns with a nonzero entry in this chunk (the unused capacity of a
+    // low-rank block is zero: its Gram entries are skipped here and in k_bcore)
+    unsigned long long lm = 0ull;
     for (int t = threadIdx.x; t < ch.rows * k; t += blockDim.x) {
         const int r = t % ch.rows, j = t / ch.rows;
-        tile[r * (TRUNC_KMAX + 1) + j] = M[(long long)j * ld + ch.r0 + r];
+        const double v = M[(long long)j * ld + ch.r0 + r];
+        tile[r * (TRUNC_KMAX + 1) + j] = v;
+        if (v != 0.0) lm |= 1ull << j;
     }
+    lm = ((unsigned long long)__reduce_or_sync(0xffffffffu, (unsigned)(lm >> 32)) << 32) |
+         __reduce_or_sync(0xffffffffu, (unsigned)lm);
+    if ((threadIdx.x & 31) == 0 && lm) atomicOr(&msk, lm);
     __syncthreads();
-    double* out = part + e.gofs + (long long)(blockIdx.x - e.c_lo) * k * k;
-    if (g_h2_check && !h2_chk(out, (long long)k * k * 8, 42, k, blockIdx.x - e.c_lo)) return;
-    for (int o = threadIdx.x; o < k * k; o += blockDim.x) {
-        const int i = o % k, j = o / k;
+    const unsigned long long m = msk;
+    const int nz = __popcll(m);
+    if (threadIdx.x < k && ((m >> threadIdx.x) & 1ull))
+        cidx[__popcll(m & ((1ull << threadIdx.x) - 1ull))] = threadIdx.x;
+    __syncthreads();
+    double* out = part + e.gofs + (long long)(blockIdx.x - e.c_lo) * GRAM_SLOT(k);
+    if (g_h2_check && !h2_chk(out, (long long)GRAM_SLOT(k) * 8, 42, k, blockIdx.x - e.c_lo)) return;
+    if (threadIdx.x == 0) out[k * k] = __longlong_as_double((long long)m);
+    // entries of the nonzero columns only (the others are never read)
+    for (int o = threadIdx.x; o < nz * nz; o += blockDim.x) {
+        const int i = cidx[o % nz], j = cidx[o / nz];
         double s = 0.0;
         for (int r = 0; r < ch.rows; ++r) s = fma(tile[r * (TRUNC_KMAX + 1) + i], tile[r * (TRUNC_KMAX + 1) + j], s);
-        out[o] = s;
+        out[j * k + i] = s;
     }
 }
 
+// Core work arrays: compact Gram matrices (nm x nm, nm = nonzero columns of U)
+// and the n x n eigen-solve arrays; in static shared memory when nm <= BCORE_KS
+// (the common case: small footprint, the CTA fits beside the bulk GEMMs), else
+// in the entry's slot of the global scratch gscr (BCORE_GSCR doubles per entry).
+#define BCORE_KS 32
+#define BCORE_GSCR (5 * TRUNC_KMAX * TRUNC_KMAX + TRUNC_KMAX)
 __global__ void __launch_bounds__(256) k_bcore(const TEntry* E, const TChunk* C, const double* part, double tol,
-                                              int kc, double* T, int* flag)
+                                              int kc, double* T, int* flag, double* gscr)
 {
-    extern __shared__ double sm[];
+    __shared__ double ssm[5 * BCORE_KS * BCORE_KS + BCORE_KS];
     const TEntry e = E[blockIdx.x];
     const int k = e.k;
-    if (g_h2_check && (!h2_chk(part + e.gofs, (long long)(e.c_hi - e.c_lo) * k * k * 8, 60, k, e.c_hi - e.c_lo) ||
+    if (g_h2_check && (!h2_chk(part + e.gofs, (long long)(e.c_hi - e.c_lo) * GRAM_SLOT(k) * 8, 60, k, e.c_hi - e.c_lo) ||
                        !h2_chk(T + e.tofs, 2LL * k * kc * 8, 61, k, kc)))
         return;
     if (g_trunc_check && threadIdx.x == 0 &&
@@ -804,27 +880,58 @@ __global__ void __launch_bounds__(256) k_bcore(const TEntry* E, const TChunk* C,
                e.gofs, e.tofs, kc);
         __trap();
     }
-    double* Gu = sm;
-    double* Gv = Gu + k * k;
-    // fixed-order reduction of the chunk partials
-    for (int o = threadIdx.x; o < k * k; o += blockDim.x) {
-        double su = 0.0, sv = 0.0;
-        for (int c = e.c_lo; c < e.c_hi; ++c) {
-            const double v = part[e.gofs + (long long)(c - e.c_lo) * k * k + o];
-            if (C[c].side == 0) su += v; else sv += v;
+    __shared__ unsigned long long gmask;
+    __shared__ int cm[TRUNC_KMAX];
+    if (threadIdx.x == 0) gmask = 0ull;
+    __syncthreads();
+    // columns of U with a nonzero entry (the only ones with Gu_jj > 0; Gv is read
+    // on the same columns)
+    const double* slot0 = part + e.gofs;
+    const int sl = GRAM_SLOT(k);
+    {
+        unsigned long long lm = 0ull;
+        for (int c = e.c_lo + threadIdx.x; c < e.c_hi; c += blockDim.x)
+            if (C[c].side == 0) lm |= (unsigned long long)__double_as_longlong(slot0[(long long)(c - e.c_lo) * sl + k * k]);
+        lm = ((unsigned long long)__reduce_or_sync(0xffffffffu, (unsigned)(lm >> 32)) << 32) |
+             __reduce_or_sync(0xffffffffu, (unsigned)lm);
+        if ((threadIdx.x & 31) == 0 && lm) atomicOr(&gmask, lm);
+    }
+    __syncthreads();
+    const unsigned long long gm = gmask;
+    const int nm = __popcll(gm);
+    if (threadIdx.x < k && ((gm >> threadIdx.x) & 1ull)) cm[__popcll(gm & ((1ull << threadIdx.x) - 1ull))] = threadIdx.x;
+    double* W = (nm <= BCORE_KS) ? ssm : gscr + (long long)blockIdx.x * BCORE_GSCR;
+    double* Gu = W;              // Gu[b * nm + a] = (U^T U)(cm[a], cm[b])
+    double* Gv = Gu + nm * nm;
+    __syncthreads();
+    // fixed-order reduction of the chunk partials on those columns (chunks in which
+    // column i or j is zero contribute exact zeros and are skipped)
+    for (int p = threadIdx.x; p < 2 * nm * nm; p += blockDim.x) {
+        const int side = p / (nm * nm), q = p % (nm * nm);
+        const int i = cm[q % nm], j = cm[q / nm];
+        // U chunks first, then V chunks (both planners); unwritten entries of a
+        // slot are loaded but not used (select, so the loads can be batched)
+        const int cmid = (int)((e.m + TRUNC_CHUNK - 1) / TRUNC_CHUNK);
+        const int ca = side ? cmid : 0, cb = side ? e.c_hi - e.c_lo : cmid;
+        double s = 0.0;
+#pragma unroll 8
+        for (int c = ca; c < cb; ++c) {
+            const double* sp = slot0 + (long long)c * sl;
+            const unsigned long long cmk = (unsigned long long)__double_as_longlong(__ldg(sp + k * k));
+            const double v = __ldg(sp + j * k + i);
+            s += ((cmk >> i) & (cmk >> j) & 1ull) ? v : 0.0;
         }
-        Gu[o] = su;
-        Gv[o] = sv;
+        (side ? Gv : Gu)[q] = s;
     }
     __syncthreads();
     double* Tu = T + e.tofs;
     double* Tv = Tu + (long long)k * kc;
-    __shared__ int idx[TRUNC_KMAX];
+    __shared__ int idx[TRUNC_KMAX];   // compact positions of the columns with Gu_jj > 0
     __shared__ int ke_sh;
     if (threadIdx.x == 0) {
         int c = 0;
-        for (int j = 0; j < k; ++j)
-            if (Gu[j * k + j] > 0.0) idx[c++] = j;
+        for (int a = 0; a < nm; ++a)
+            if (Gu[a * nm + a] > 0.0) idx[c++] = a;
         ke_sh = c;
     }
     __syncthreads();
@@ -833,20 +940,22 @@ __global__ void __launch_bounds__(256) k_bcore(const TEntry* E, const TChunk* C,
     __syncthreads();
     if (ke == 0) return;
     const int n = (ke + 1) & ~1;
-    double* A = Gv + k * k;
+    double* A = Gv + nm * nm;
     double* Eu = A + n * n;
     double* X = Eu + n * n;
     double* lu = X + n * n;
-    int* pairs = (int*)(lu + n);
     for (int t = threadIdx.x; t < n * n; t += blockDim.x) {
         const int i = t % n, j = t / n;
-        A[t] = (i < ke && j < ke) ? Gu[idx[j] * k + idx[i]] : 0.0;
+        A[t] = (i < ke && j < ke) ? Gu[idx[j] * nm + idx[i]] : 0.0;
     }
     __syncthreads();
     // rotation threshold: converged to 1e-12 relative when truncating to tol >= 1e-6
     // (far below the truncation error), to rounding otherwise
-    const double jeps = (tol >= 1e-6) ? 1e-12 : 1e-15;
-    cta_jacobi(A, Eu, n, pairs, jeps);
+    // (and, then, off-diagonal entries below 1e-14 ||A||_F, the rounding noise
+    // the rotations themselves leave behind, are not rotated: with a wide
+    // eigenvalue range the relative test alone never stops)
+    const double jeps = (tol >= 1e-6) ? 1e-12 : 1e-15, jarel = (tol >= 1e-6) ? 1e-14 : 1e-17;
+    const int sw1 = cta_jacobi(A, Eu, n, nullptr, jeps, jarel);
     __shared__ double mu;
     if (threadIdx.x == 0) {
         double a = 0.0;
@@ -863,7 +972,7 @@ __global__ void __launch_bounds__(256) k_bcore(const TEntry* E, const TChunk* C,
         const int i = t % n, j = t / n;
         double s = 0.0;
         if (i < ke)
-            for (int q = 0; q < ke; ++q) s = fma(Gv[idx[q] * k + idx[i]], Eu[j * n + q], s);
+            for (int q = 0; q < ke; ++q) s = fma(Gv[idx[q] * nm + idx[i]], Eu[j * n + q], s);
         X[t] = s;
     }
     __syncthreads();
@@ -874,8 +983,14 @@ __global__ void __launch_bounds__(256) k_bcore(const TEntry* E, const TChunk* C,
         A[t] = lu[i] * lu[j] * s;
     }
     __syncthreads();
-    cta_jacobi(A, X, n, pairs, jeps);
+    const int sw2 = cta_jacobi(A, X, n, nullptr, jeps, jarel);
     __syncthreads();
+    if (threadIdx.x == 0) {   // (debug statistics: calls, sum ke, sum sweeps, max sweeps of one solve)
+        atomicAdd(&g_trunc_stats[0], 1ull);
+        atomicAdd(&g_trunc_stats[1], (unsigned long long)ke);
+        atomicAdd(&g_trunc_stats[2], (unsigned long long)(sw1 + sw2));
+        atomicMax(&g_trunc_stats[3], (unsigned long long)max(sw1, sw2));
+    }
     __shared__ int ord[TRUNC_KMAX];
     __shared__ int r_sh;
     if (threadIdx.x == 0) {
@@ -909,8 +1024,8 @@ __global__ void __launch_bounds__(256) k_bcore(const TEntry* E, const TChunk* C,
                 sv = fma(ev, lu[q] / sig, sv);
             }
         }
-        Tu[c * k + idx[i]] = su;
-        Tv[c * k + idx[i]] = sv;
+        Tu[c * k + cm[idx[i]]] = su;
+        Tv[c * k + cm[idx[i]]] = sv;
     }
 }
 
@@ -1348,7 +1463,7 @@ static void flush_dirty(fde_lu* L)
         }
         e.c_hi = (int)C.size();
         e.gofs = gofs;
-        gofs += (long long)(e.c_hi - e.c_lo) * B.k * B.k;
+        gofs += (long long)(e.c_hi - e.c_lo) * GRAM_SLOT(B.k);
         e.tofs = tofs;
         tofs += 2LL * B.k * kc;
         kmax = std::max(kmax, B.k);
@@ -1367,10 +1482,8 @@ static void flush_dirty(fde_lu* L)
     double* T = lu_alloc(L, (size_t)std::max<long long>(tofs, 1));
     k_bgram<<<(unsigned)C.size(), 256, 0, L->h->stream>>>(dE.p, dC.p, part);
     FDE_CHECK_LAUNCH();
-    const int ne = (kmax + 1) & ~1;
-    const size_t smem = (size_t)(2 * kmax * kmax + 3 * ne * ne + 2 * ne + 8) * sizeof(double);
-    set_smem_once((const void*)k_bcore, (int)smem);
-    k_bcore<<<(unsigned)E.size(), 256, smem, L->h->stream>>>(dE.p, dC.p, part, L->tol, kc, T, L->dflag.p + 1);
+    double* gscr = lu_alloc(L, E.size() * (size_t)BCORE_GSCR);
+    k_bcore<<<(unsigned)E.size(), 256, 0, L->h->stream>>>(dE.p, dC.p, part, L->tol, kc, T, L->dflag.p + 1, gscr);
     FDE_CHECK_LAUNCH();
     const size_t asmem = (size_t)(kmax * kc + TRUNC_CHUNK * kmax) * sizeof(double);
     set_smem_once((const void*)k_bapply, (int)asmem);

@@ -28,11 +28,13 @@
 // H2_MMAX dofs and dense diagonal leaf tiles.
 
 #include <chrono>
+#include <functional>
 #include <cstdlib>
 #include <set>
 
 #define H2_MMAX 128
 #define H2_STRIP 32
+#define H2_PCH 16      // inverse-panel staging chunk (columns of op)
 #define H2_CP_CHUNK 4096   // elements per copy CTA
 
 struct H2Lu {
@@ -50,6 +52,8 @@ struct H2Panel {
     double* X;
     long long ldx;
     int m, nvec, mode;
+    const double* Ti;   // explicit inverse of the factor (L^{-1} for mode 0, U^{-1} else), or null
+    long long ldi;
 };
 struct H2Term {
     const double* A;
@@ -152,6 +156,82 @@ __global__ void __launch_bounds__(512) k_h2_lu(const H2Lu* tk, int* bad)
     }
 }
 
+// The same LU with the tile in registers: thread (tr, tc) = (tid & 31, tid >> 5)
+// owns rows tr + 32a (a < 4) and columns tc + 16b (b < 8), cyclically, so that
+// for pivot j = 16 jj + tcol (jj unrolled) the owned row / column of the pivot
+// have compile-time register indices (a = jj / 2, b = jj) and whole register
+// rows / columns that are already eliminated are skipped at compile time.  Per
+// pivot the owners publish row j and column j (raw, after the update of pivot
+// j-1) in double-buffered shared vectors; one barrier; every thread forms the
+// multipliers l_i = a_ij / a_jj of its rows and updates its trailing elements.
+// Same arithmetic as k_h2_lu (l = a_ij * (1 / a_jj), a_ik - l u_jk as one fma).
+__global__ void __launch_bounds__(512) k_h2_lu_reg(const H2Lu* tk, int* bad)
+{
+    constexpr int M = H2_MMAX;
+    static_assert(M == 128, "register LU: 128 x 128 tile, 512 threads");
+    __shared__ double rowb[2][M], colb[2][M], rpb[2];
+    const H2Lu d = tk[blockIdx.x];
+    const int m = d.m, tid = threadIdx.x, tr = tid & 31, tc = tid >> 5;
+    if (g_h2_check && !h2_chk(d.D, ((long long)(m - 1) * d.ld + m) * 8, 30, m, 0)) return;
+    double R[4][8];
+#pragma unroll
+    for (int b = 0; b < 8; ++b)
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+            const int i = tr + 32 * a, k = tc + 16 * b;
+            R[a][b] = (i < m && k < m) ? d.D[(long long)k * d.ld + i] : (i == k ? 1.0 : 0.0);
+        }
+    int nbad = 0;
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj) {
+        const int aj = jj >> 1;   // register row of rows 32 aj .. 32 aj + 31
+        for (int tcol = 0; tcol < 16; ++tcol) {
+            const int j = 16 * jj + tcol, buf = j & 1;
+            const int jr = j & 31;   // owner lane of row j
+            // publish row j (owners: tr == jr) and column j (owner warp: tc == tcol)
+            if (tr == jr) {
+#pragma unroll
+                for (int b = jj; b < 8; ++b) rowb[buf][tc + 16 * b] = R[aj][b];
+                if (tc == tcol) {
+                    const double p = R[aj][jj];
+                    if (j < m && (!(fabs(p) > 0.0) || !isfinite(p))) nbad = 1;
+                    rpb[buf] = rcp_nr(p);   // (MUFU reciprocal + 2 Newton steps: on the pivot chain)
+                }
+            }
+            if (tc == tcol) {
+#pragma unroll
+                for (int a = aj; a < 4; ++a) colb[buf][tr + 32 * a] = R[a][jj];
+            }
+            __syncthreads();
+            const double rp = rpb[buf];
+            double l[4];
+#pragma unroll
+            for (int a = aj; a < 4; ++a) l[a] = colb[buf][tr + 32 * a] * rp;
+            double u[8];
+#pragma unroll
+            for (int b = jj; b < 8; ++b) u[b] = rowb[buf][tc + 16 * b];
+#pragma unroll
+            for (int a = aj; a < 4; ++a) {
+                const bool ra = (a > aj) || (tr + 32 * a > j);
+#pragma unroll
+                for (int b = jj; b < 8; ++b) {
+                    const bool cb = (b > jj) || (tc > tcol);
+                    if (ra && cb) R[a][b] = fma(-l[a], u[b], R[a][b]);
+                }
+                if (tc == tcol && ra) R[a][jj] = l[a];   // multipliers of column j
+            }
+        }
+    }
+    if (nbad) *bad = 1;
+#pragma unroll
+    for (int b = 0; b < 8; ++b)
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+            const int i = tr + 32 * a, k = tc + 16 * b;
+            if (i < m && k < m) d.D[(long long)k * d.ld + i] = R[a][b];
+        }
+}
+
 // One CTA per strip of <= 32 vectors.  The packed LU tile T (m x m) and the strip
 // are staged in shared memory with asynchronous copies; T' (lower) is read from
 // the staged tile: mode 0: T'[i][j] = L[i][j] = Ts[j ldT + i] (unit diagonal),
@@ -160,6 +240,81 @@ template <int MODE>
 __device__ __forceinline__ double h2_tp(const double* Ts, int ldT, int i, int j)
 {
     return MODE == 0 ? Ts[j * ldT + i] : Ts[i * ldT + j];
+}
+
+// panel as a product with the explicit inverse of the factor (computed on the
+// LU stream right after the tile's LU): X <- Li X (mode 0), X <- Ui^T X (mode 1),
+// X <- X Ui (mode 2, rows).  op is staged as Ts[q ldT + i] = op(i, q); thread
+// (lane, w) computes rows lane + 32a and vectors w + 8u (a, u < 4).
+template <int MODE>
+__device__ void h2_panel_inv_body(const H2Panel& p, double* psm)
+{
+    // op is staged in chunks of H2_PCH columns (small shared footprint: the CTA
+    // has to fit beside the bulk-update GEMMs of the previous step)
+    const int m = p.m, ldT = (m & 1) ? m + 2 : m + 1, ldB = ldT;
+    double* Bs = psm;                 // vector c, element i at Bs[c * ldB + i]
+    double* Ts = psm + H2_STRIP * ldB;   // Ts[qq * ldT + i] = op(i, q0 + qq)
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int nv = p.nvec;
+    if (MODE == 2) {
+        for (int t = tid; t < nv * m; t += 256) {
+            const int c = t % nv, i = t / nv;
+            cp_async8(Bs + c * ldB + i, p.X + (long long)i * p.ldx + c);
+        }
+    } else {
+        for (int t = tid; t < nv * m; t += 256) {
+            const int i = t % m, c = t / m;
+            cp_async8(Bs + c * ldB + i, p.X + (long long)c * p.ldx + i);
+        }
+    }
+    double acc[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) acc[a][u] = 0.0;
+    int ia[4], cu[4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) ia[a] = min(lane + 32 * a, m - 1);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) cu[u] = min(w + 8 * u, nv - 1);
+    for (int q0 = 0; q0 < m; q0 += H2_PCH) {
+        const int nq = min(H2_PCH, m - q0);
+        if (MODE == 0) {   // op(i, q) = Ti(i, q): columns q0.. of Ti
+            for (int t = tid; t < nq * m; t += 256) {
+                const int i = t % m, qq = t / m;
+                cp_async8(Ts + qq * ldT + i, p.Ti + (long long)(q0 + qq) * p.ldi + i);
+            }
+        } else {           // op(i, q) = Ti(q, i): rows q0.. of Ti
+            for (int t = tid; t < nq * m; t += 256) {
+                const int qq = t % nq, i = t / nq;
+                cp_async8(Ts + qq * ldT + i, p.Ti + (long long)i * p.ldi + q0 + qq);
+            }
+        }
+        cp_async_wait_all();
+        __syncthreads();
+        for (int qq = 0; qq < nq; ++qq) {
+            double o[4], x[4];
+#pragma unroll
+            for (int a = 0; a < 4; ++a) o[a] = Ts[qq * ldT + ia[a]];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) x[u] = Bs[cu[u] * ldB + q0 + qq];
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int u = 0; u < 4; ++u) acc[a][u] = fma(o[a], x[u], acc[a][u]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int i = lane + 32 * a, c = w + 8 * u;
+            if (i < m && c < nv) {
+                if (MODE == 2) p.X[(long long)i * p.ldx + c] = acc[a][u];
+                else p.X[(long long)c * p.ldx + i] = acc[a][u];
+            }
+        }
 }
 
 template <int MODE>
@@ -250,9 +405,15 @@ __global__ void __launch_bounds__(256) k_h2_panel(const H2Panel* P)
         if (!h2_chk(p.T, ((long long)(p.m - 1) * p.ldt + p.m) * 8, 20, p.m, p.mode) || !h2_chk(p.X, ex * 8, 21, p.nvec, p.mode))
             return;
     }
-    if (p.mode == 0) h2_panel_body<0>(p, psm);
-    else if (p.mode == 1) h2_panel_body<1>(p, psm);
-    else h2_panel_body<2>(p, psm);
+    if (p.Ti) {
+        if (p.mode == 0) h2_panel_inv_body<0>(p, psm);
+        else if (p.mode == 1) h2_panel_inv_body<1>(p, psm);
+        else h2_panel_inv_body<2>(p, psm);
+    } else {
+        if (p.mode == 0) h2_panel_body<0>(p, psm);
+        else if (p.mode == 1) h2_panel_body<1>(p, psm);
+        else h2_panel_body<2>(p, psm);
+    }
 }
 
 // grouped multi-term GEMM: every CTA owns a 64 x 64 tile of one task,
@@ -262,7 +423,7 @@ __global__ void __launch_bounds__(256) k_h2_panel(const H2Panel* P)
 // layout / transpose), so two slices are in flight while one is multiplied.
 #define H2G_ST 3
 #define H2G_TMAX 48
-#define H2G_SMEM (2 * H2G_ST * GK * (GT + 1) * (int)sizeof(double))
+#define H2G_SMEM(TG) (2 * H2G_ST * GK * ((TG) + 1) * (int)sizeof(double))
 struct H2Cursor {   // position in the (term, slice) sequence of a tile
     int q, k0;
 };
@@ -275,22 +436,23 @@ __device__ __forceinline__ void h2_next(const H2Term* terms, int t_hi, H2Cursor&
         while (c.q < t_hi && terms[c.q].k <= 0) ++c.q;
     }
 }
+template <int TG>
 __device__ __forceinline__ void h2_stage(const H2Term& T, int m0, int n0, int m, int n, int k0, double* sA, double* sB)
 {
-    // sA[kk][mm] (ld GT + 1), sB[kk][nn]; zero outside the operands
+    // sA[kk][mm] (ld TG + 1), sB[kk][nn]; zero outside the operands
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < TG * GK / 256; ++u) {
         const int t = threadIdx.x + 256 * u;
         int kk, mm;
-        if (T.ta) { mm = t / GK; kk = t % GK; } else { kk = t / GT; mm = t % GT; }
+        if (T.ta) { mm = t / GK; kk = t % GK; } else { kk = t / TG; mm = t % TG; }
         const int gi = m0 + mm, gk = k0 + kk;
-        double* da = sA + kk * (GT + 1) + mm;
+        double* da = sA + kk * (TG + 1) + mm;
         if (gi < m && gk < T.k) cp_async8(da, T.ta ? T.A + (long long)gi * T.lda + gk : T.A + (long long)gk * T.lda + gi);
         else *da = 0.0;
         int nn;
-        if (T.tb) { kk = t / GT; nn = t % GT; } else { nn = t / GK; kk = t % GK; }
+        if (T.tb) { kk = t / TG; nn = t % TG; } else { nn = t / GK; kk = t % GK; }
         const int gj = n0 + nn, gk2 = k0 + kk;
-        double* db = sB + kk * (GT + 1) + nn;
+        double* db = sB + kk * (TG + 1) + nn;
         if (gj < n && gk2 < T.k) cp_async8(db, T.tb ? T.B + (long long)gk2 * T.ldb + gj : T.B + (long long)gj * T.ldb + gk2);
         else *db = 0.0;
     }
@@ -299,14 +461,16 @@ __device__ __forceinline__ void cp_async_commit_group() { asm volatile("cp.async
 template <int N>
 __device__ __forceinline__ void cp_async_wait_group() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
-__global__ void __launch_bounds__(256) k_h2_gemm(const H2Tile* tiles, const H2Task* tasks, const H2Term* terms)
+template <int TG>
+__device__ __forceinline__ void h2_gemm_tile(const H2Tile* tiles, int tile, const H2Task* tasks, const H2Term* terms)
 {
+    constexpr int RT = TG / 16;      // register tile RT x RT per thread (16 x 16 threads)
     extern __shared__ double gsm[];   // H2G_SMEM bytes: [stage] A slice, [stage] B slice
-    double (*sA)[GK * (GT + 1)] = reinterpret_cast<double (*)[GK * (GT + 1)]>(gsm);
-    double (*sB)[GK * (GT + 1)] = reinterpret_cast<double (*)[GK * (GT + 1)]>(gsm + H2G_ST * GK * (GT + 1));
+    double (*sA)[GK * (TG + 1)] = reinterpret_cast<double (*)[GK * (TG + 1)]>(gsm);
+    double (*sB)[GK * (TG + 1)] = reinterpret_cast<double (*)[GK * (TG + 1)]>(gsm + H2G_ST * GK * (TG + 1));
     __shared__ double sAlpha[H2G_ST];
     __shared__ H2Term sT[H2G_TMAX];   // the task's term descriptors (one global read each)
-    const H2Tile tl = tiles[blockIdx.x];
+    const H2Tile tl = tiles[tile];
     const H2Task tk = tasks[tl.task];
     const int nt = tk.t_hi - tk.t_lo;
     const H2Term* tm = terms + tk.t_lo;
@@ -321,7 +485,7 @@ __global__ void __launch_bounds__(256) k_h2_gemm(const H2Tile* tiles, const H2Ta
     if (threadIdx.x == 0) sbad = 0;
     if (g_h2_check && threadIdx.x == 0) {
         // C: columns [n0, n0+64) rows [m0, m0+64) clipped
-        const int mm = min(GT, m - m0), nn = min(GT, n - n0);
+        const int mm = min(TG, m - m0), nn = min(TG, n - n0);
         if (mm > 0 && nn > 0) h2_chk(tk.C + (long long)n0 * tk.ldc + m0, ((long long)(nn - 1) * tk.ldc + mm) * 8, 1, m, n);
         for (int q = 0; q < nt; ++q) {
             const H2Term T = terms[tk.t_lo + q];
@@ -338,11 +502,11 @@ __global__ void __launch_bounds__(256) k_h2_gemm(const H2Tile* tiles, const H2Ta
     }
     __syncthreads();
     if (sbad) return;
-    double acc[4][4];
+    double acc[RT][RT];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < RT; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+        for (int j = 0; j < RT; ++j) acc[i][j] = 0.0;
     H2Cursor ld{0, -GK};   // next slice to load
     while (ld.q < nt && tm[ld.q].k <= 0) ++ld.q;
     ld.k0 = 0;
@@ -353,7 +517,7 @@ __global__ void __launch_bounds__(256) k_h2_gemm(const H2Tile* tiles, const H2Ta
     for (int st = 0; st < H2G_ST - 1; ++st) {
         if (st < nslice) {
             const H2Term& T = tm[ld.q];
-            h2_stage(T, m0, n0, m, n, ld.k0, sA[st], sB[st]);
+            h2_stage<TG>(T, m0, n0, m, n, ld.k0, sA[st], sB[st]);
             if (threadIdx.x == 0) sAlpha[st] = T.alpha;
             h2_next(tm, nt, ld);
         }
@@ -367,7 +531,7 @@ __global__ void __launch_bounds__(256) k_h2_gemm(const H2Tile* tiles, const H2Ta
         if (nx < nslice) {
             const int st = nx % H2G_ST;
             const H2Term& T = tm[ld.q];
-            h2_stage(T, m0, n0, m, n, ld.k0, sA[st], sB[st]);
+            h2_stage<TG>(T, m0, n0, m, n, ld.k0, sA[st], sB[st]);
             if (threadIdx.x == 0) sAlpha[st] = T.alpha;
             h2_next(tm, nt, ld);
         }
@@ -378,28 +542,38 @@ __global__ void __launch_bounds__(256) k_h2_gemm(const H2Tile* tiles, const H2Ta
         const double al = sAlpha[cs];
 #pragma unroll
         for (int kk = 0; kk < GK; ++kk) {
-            double a[4], b[4];
+            double a[RT], b[RT];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) a[i] = al * a_s[kk * (GT + 1) + tx + 16 * i];
+            for (int i = 0; i < RT; ++i) a[i] = al * a_s[kk * (TG + 1) + tx + 16 * i];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) b[j] = b_s[kk * (GT + 1) + ty + 16 * j];
+            for (int j = 0; j < RT; ++j) b[j] = b_s[kk * (TG + 1) + ty + 16 * j];
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
+            for (int i = 0; i < RT; ++i)
 #pragma unroll
-                for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+                for (int j = 0; j < RT; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
         }
     }
     cp_async_wait_group<0>();
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < RT; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < RT; ++j) {
             const int gi = m0 + tx + 16 * i, gj = n0 + ty + 16 * j;
             if (gi < m && gj < n) {
                 double* c = tk.C + (long long)gj * tk.ldc + gi;
                 *c = acc[i][j] + (tk.beta == 0.0 ? 0.0 : tk.beta * *c);
             }
         }
+}
+
+// grid-stride over the tiles: a capped grid leaves SMs to the critical stream
+template <int TG>
+__global__ void __launch_bounds__(256) k_h2_gemm(const H2Tile* tiles, const H2Task* tasks, const H2Term* terms, int ntile)
+{
+    for (int t = blockIdx.x; t < ntile; t += gridDim.x) {
+        h2_gemm_tile<TG>(tiles, t, tasks, terms);
+        __syncthreads();
+    }
 }
 
 __global__ void __launch_bounds__(256) k_h2_copy(const H2Copy* C)
@@ -454,6 +628,8 @@ struct VPanel {
     VRef X;
     int64_t ldx;
     int m, nvec, mode;
+    VRef Ti{-1, 0, 0};   // its explicit inverse (see H2Panel), if computed
+    int64_t ldi = 0;
 };
 struct VTrunc {
     int blk, k;
@@ -483,8 +659,10 @@ struct H2Launch {      // ranges in the flat device arrays
     std::vector<H2Trunc> trmid;             // truncations between the rounds
     int lu = -1;
     int pan0 = 0, npan = 0;
+    int pi0 = 0, npi = 0;                   // inverses of the factors of this step's tile (after its LU)
     int g_tile0[6] = {0, 0, 0, 0, 0, 0}, g_ntile[6] = {0, 0, 0, 0, 0, 0};
     int cp0 = 0, ncp = 0;
+    bool diag_scr = false;                  // the diagonal-tile update reads step scratch
 };
 
 struct H2Plan {
@@ -504,6 +682,8 @@ struct H2Plan {
     double* tr_T = nullptr;
     double* tr_part2 = nullptr;   // overflow truncations (their own stream)
     double* tr_T2 = nullptr;
+    double* tr_scr = nullptr;    // k_bcore global fallback (BCORE_GSCR per entry)
+    double* tr_scr2 = nullptr;
     int launches = 0;
 };
 
@@ -515,6 +695,8 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
     const auto t_plan0 = std::chrono::steady_clock::now();
     const HStruct& S = L->S;
     const bool trunc = L->tol > 0.0;
+    static const bool pan_inv = !getenv("FDE_H2_PANEL_SUBST");
+    static const bool pretrunc = !getenv("FDE_H2_NOPRETRUNC");
     const int R = hm->R, rmax = L->rmax;
     if (trunc && (R > TRUNC_KMAX || rmax > TRUNC_KMAX)) return false;
     // ---- sweep tiles: the leaves of the cluster tree, each split into equal
@@ -650,6 +832,13 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
             } else {   // columns of tiles > k of the row of tile k
                 const int j0 = std::max(s0[c], k + 1);
                 st.panel.push_back({Tk, ldk, {0, c, toff(c, k, j0)}, C.m, mk, (int)(lr0[s1[c] + 1] - lr0[j0]), 0});
+            }
+        }
+        if (pan_inv) {   // panels as products with the tile inverses (computed after LU(k))
+            const int f = leaf_of[k];
+            for (auto& pv : st.panel) {
+                pv.Ti = {pv.mode == 0 ? 4 : 5, f, ioff(f, k, k)};
+                pv.ldi = lfm(f);
             }
         }
         // products: pair scratch offsets
@@ -823,6 +1012,22 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
                 }
             }
         }
+        // early truncation of the panel operands of step k+1 that are not operands of
+        // this step: they run off the critical stream (with the overflow truncations,
+        // before this step's new columns), so that step k+1 only has to recompress
+        // the columns step k adds (rmax + one group instead of up to TRUNC_KMAX)
+        if (trunc && pretrunc && k + 1 < nl) {
+            std::set<int> opnd(Cb.begin(), Cb.end());
+            opnd.insert(Rc.begin(), Rc.end());
+            for (int i = k + 2; i < nl; ++i) {
+                const int b = own(i, k + 1);
+                if (isLR(b) && !opnd.count(b)) add_trunc(b, true);
+            }
+            for (int j = k + 2; j < nl; ++j) {
+                const int c = own(k + 1, j);
+                if (isLR(c) && !opnd.count(c)) add_trunc(c, true);
+            }
+        }
         // slots and copies; a target whose new columns do not fit gets them in rounds,
         // truncated between rounds (formatted addition of the partial sums)
         std::vector<char> u_done(grps.size(), 0);
@@ -922,16 +1127,17 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
     const int64_t off_scr = words;
     words += 2 * scr_max;
     // truncation workspace (max over batches)
-    int64_t gmax = 1, tmax = 1;
+    int64_t gmax = 1, tmax = 1, emax = 1;
     auto tr_size = [&](const std::vector<VTrunc>& v) {
         int64_t g = 0, tt = 0;
         for (auto& e : v) {
             const HBlock& hb = S.bl[e.blk];
-            g += (ceil_div(hb.m, TRUNC_CHUNK) + ceil_div(hb.n, TRUNC_CHUNK)) * e.k * e.k;
+            g += (ceil_div(hb.m, TRUNC_CHUNK) + ceil_div(hb.n, TRUNC_CHUNK)) * GRAM_SLOT(e.k);
             tt += 2LL * e.k * rmax;
         }
         gmax = std::max(gmax, g);
         tmax = std::max(tmax, tt);
+        emax = std::max(emax, (int64_t)v.size());
     };
     tr_size(init_trunc);
     for (auto& st : steps) {
@@ -943,6 +1149,8 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
     words += 2 * gmax;   // [operand truncations | overflow truncations] (two streams)
     const int64_t off_T = words;
     words += 2 * tmax;
+    const int64_t off_cs = words;
+    words += 2 * emax * BCORE_GSCR;
 
     H2Plan* P = new H2Plan();
     L->plan = P;
@@ -959,6 +1167,8 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
     P->tr_T = A + off_T;
     P->tr_part2 = A + off_part + gmax;
     P->tr_T2 = A + off_T + tmax;
+    P->tr_scr = A + off_cs;
+    P->tr_scr2 = A + off_cs + emax * BCORE_GSCR;
     auto res = [&](const VRef& r) -> double* {
         switch (r.sp) {
             case 0: return A + offD[r.id] + r.off;
@@ -1007,7 +1217,7 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
             }
             te.c_hi = (int)vtc.size() - ln.c0;
             te.gofs = gofs;
-            gofs += (long long)(te.c_hi - te.c_lo) * e.k * e.k;
+            gofs += (long long)(te.c_hi - te.c_lo) * GRAM_SLOT(e.k);
             te.tofs = tofs;
             tofs += 2LL * e.k * rmax;
             ln.kmax = std::max(ln.kmax, e.k);
@@ -1016,6 +1226,13 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         ln.ne = (int)vte.size() - ln.e0;
         ln.nc = (int)vtc.size() - ln.c0;
     };
+    double gstat_flop[6] = {0}, gstat_cbytes[6] = {0};   // (FDE_DEBUG_PLAN statistics)
+    // GEMM tile per launch group (cores, products, crit, conversions, rest, diag):
+    // 32 x 32 where a launch has few tiles (latency: more CTAs, shorter chains)
+    int gemm_tg[6] = {64, 64, 64, 64, 64, 32};
+    if (const char* e = getenv("FDE_H2_TG32"))   // e.g. "5", "0125"
+        for (const char* c = e; *c; ++c)
+            if (*c >= '0' && *c <= '5') gemm_tg[*c - '0'] = 32;
     auto put_gemm = [&](const std::vector<VTask>& v, H2Launch& ln, int which) {
         ln.g_tile0[which] = (int)vtile.size();
         for (auto& t : v) {
@@ -1029,10 +1246,13 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
             for (auto& q : t.terms)
                 vterm.push_back({res(q.A), res(q.B), q.lda, q.ldb, q.k, q.ta, q.tb, q.alpha});
             d.t_hi = (int)vterm.size();
+            for (auto& q : t.terms) gstat_flop[which] += 2.0 * t.m * t.n * q.k;
+            gstat_cbytes[which] += 16.0 * t.m * t.n;
             const int ti = (int)vtask.size();
             vtask.push_back(d);
-            for (int m0 = 0; m0 < t.m; m0 += GT)
-                for (int n0 = 0; n0 < t.n; n0 += GT) vtile.push_back({ti, m0, n0});
+            const int tg = gemm_tg[which];
+            for (int m0 = 0; m0 < t.m; m0 += tg)
+                for (int n0 = 0; n0 < t.n; n0 += tg) vtile.push_back({ti, m0, n0});
         }
         ln.g_ntile[which] = (int)vtile.size() - ln.g_tile0[which];
     };
@@ -1068,6 +1288,8 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
                 d.m = p.m;
                 d.nvec = nv;
                 d.mode = p.mode;
+                d.Ti = p.Ti.sp >= 0 ? res(p.Ti) : nullptr;
+                d.ldi = p.ldi;
                 vpan.push_back(d);
             }
         }
@@ -1127,7 +1349,7 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         for (auto& t : v) {
             ++n_task;
             n_term += t.terms.size();
-            n_tile += (size_t)(ceil_div(t.m, GT) * ceil_div(t.n, GT));
+            n_tile += (size_t)(ceil_div(t.m, 32) * ceil_div(t.n, 32));   // (upper bound: 32 x 32 tiles)
         }
     };
     auto cnt_trunc = [&](const std::vector<VTrunc>& v) {
@@ -1209,6 +1431,7 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
     cudaEvent_t evP = L->h->ev_aux[3], evC = L->h->ev_aux[4], evB = L->h->ev_aux[5], evD = L->h->ev_aux[6];
     cudaEvent_t evLU = L->h->ev_aux[7], evDg = L->h->ev_aux[8];
     cudaEvent_t evCp = L->h->ev_aux[10], evOv = L->h->ev_aux[11];
+    cudaEvent_t evPan = L->h->ev_aux[12], evSnap = L->h->ev_aux[13];
     cudaStream_t se = aux_stream6(L->h);   // overflow truncations
     // debug: fold auxiliary streams back onto the critical one (race bisection)
     if (const char* f = getenv("FDE_H2_FOLD")) {
@@ -1247,9 +1470,11 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
     // of step k, which overlap LU(k+1) and the panels of step k+1 (lookahead).
     const int pan_smem = (H2_MMAX + H2_STRIP) * (H2_MMAX + 2) * (int)sizeof(double);
     set_smem_once((const void*)k_h2_panel, pan_smem);
+    const int pan_smem_inv = (H2_STRIP + H2_PCH) * (H2_MMAX + 2) * (int)sizeof(double);
     const int lu_smem = H2_MMAX * (H2_MMAX + 1) * (int)sizeof(double);   // padded 128 x 129
     set_smem_once((const void*)k_h2_lu, lu_smem);
-    set_smem_once((const void*)k_h2_gemm, H2G_SMEM);
+    set_smem_once((const void*)k_h2_gemm<64>, H2G_SMEM(64));
+    set_smem_once((const void*)k_h2_gemm<32>, H2G_SMEM(32));
     int nlaunch = 0;
     // FDE_DEBUG_SERIAL: synchronise after every launch and name the first failing one
     const bool dbg_serial = getenv("FDE_DEBUG_SERIAL") != nullptr;
@@ -1282,6 +1507,7 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         ++nlaunch;
         dbg("copy");
     };
+    std::function<void(int)> tmark = [](int) {};
     auto run_trunc = [&](const H2Trunc& tr, cudaStream_t st, int ws) {
         if (!tr.ne) return;
         const TEntry* E = P->te.p + tr.e0;
@@ -1291,12 +1517,12 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         k_bgram<<<tr.nc, 256, 0, st>>>(E, C, part);
         FDE_CHECK_LAUNCH();
         dbg("bgram");
-        const int kmax = tr.kmax, ne = (kmax + 1) & ~1;
-        const size_t smem = (size_t)(2 * kmax * kmax + 3 * ne * ne + 2 * ne + 8) * sizeof(double);
-        set_smem_once((const void*)k_bcore, (int)smem);
-        k_bcore<<<tr.ne, 256, smem, st>>>(E, C, part, L->tol, rmax, Tt, L->dflag.p + 1);
+        if (!ws) tmark(0);
+        const int kmax = tr.kmax;
+        k_bcore<<<tr.ne, 256, 0, st>>>(E, C, part, L->tol, rmax, Tt, L->dflag.p + 1, ws ? P->tr_scr2 : P->tr_scr);
         FDE_CHECK_LAUNCH();
         dbg("bcore");
+        if (!ws) tmark(1);
         const size_t asmem = (size_t)(kmax * rmax + TRUNC_CHUNK * kmax) * sizeof(double);
         set_smem_once((const void*)k_bapply, (int)asmem);
         k_bapply<<<tr.nc, 256, asmem, st>>>(E, C, Tt, rmax);
@@ -1304,9 +1530,31 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         dbg("bapply");
         nlaunch += 3;
     };
+    static const bool lu_old = getenv("FDE_H2_LU_OLD") != nullptr;
+    auto launch_lu = [&](int kk, cudaStream_t st) {   // LU of tile kk, then the inverses of its factors
+        const H2Lu* t = P->lu.p + P->steps[kk].lu;
+        if (lu_old) k_h2_lu<<<1, 512, lu_smem, st>>>(t, L->dflag.p);
+        else k_h2_lu_reg<<<1, 512, 0, st>>>(t, L->dflag.p);
+        FDE_CHECK_LAUNCH();
+        if (P->steps[kk].npi) {
+            k_h2_panel<<<P->steps[kk].npi, 256, pan_smem, st>>>(P->pan.p + P->steps[kk].pi0);
+            FDE_CHECK_LAUNCH();
+            ++nlaunch;
+        }
+    };
+    int gemm_cap[6];
+    for (int w = 0; w < 6; ++w) gemm_cap[w] = 1 << 30;
+    {
+        const char* e = getenv("FDE_H2_REST_CTAS");
+        gemm_cap[4] = e ? std::max(1, atoi(e)) : gemm_cap[4];
+    }
     auto run_gemm = [&](const H2Launch& ln, int w, cudaStream_t st) {
         if (!ln.g_ntile[w]) return;
-        k_h2_gemm<<<ln.g_ntile[w], 256, H2G_SMEM, st>>>(P->tiles.p + ln.g_tile0[w], P->tasks.p, P->terms.p);
+        const int grid = std::min(ln.g_ntile[w], gemm_cap[w]);
+        if (gemm_tg[w] == 32)
+            k_h2_gemm<32><<<grid, 256, H2G_SMEM(32), st>>>(P->tiles.p + ln.g_tile0[w], P->tasks.p, P->terms.p, ln.g_ntile[w]);
+        else
+            k_h2_gemm<64><<<grid, 256, H2G_SMEM(64), st>>>(P->tiles.p + ln.g_tile0[w], P->tasks.p, P->terms.p, ln.g_ntile[w]);
         FDE_CHECK_LAUNCH();
         ++nlaunch;
         static const char* gname[6] = {"gemm cores", "gemm products", "gemm crit", "gemm conversions", "gemm rest",
@@ -1315,21 +1563,29 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
     };
     auto run_panel = [&](const H2Launch& ln) {
         if (!ln.npan) return;
-        k_h2_panel<<<ln.npan, 256, pan_smem, sa>>>(P->pan.p + ln.pan0);
+        k_h2_panel<<<ln.npan, 256, (&ln != &P->fin && pan_inv) ? pan_smem_inv : pan_smem, sa>>>(P->pan.p + ln.pan0);
         FDE_CHECK_LAUNCH();
         ++nlaunch;
         dbg("panel");
     };
     // init (+ every diagonal-tile LU descriptor: LU(k+1) is issued during step k)
+    if (pan_inv) init_cp.insert(init_cp.end(), fin_cp.begin(), fin_cp.end());   // identities of the tile inverses
     put_copy(init_cp, P->init);
     put_trunc(init_trunc, P->init.tr);
     P->steps.resize(nl);
     for (int k = 0; k < nl; ++k) {
         P->steps[k].lu = (int)vlu.size();
         vlu.push_back({A + offD[steps[k].lu_blk] + steps[k].lu_off, S.bl[steps[k].lu_blk].m, lm(k)});
+        if (pan_inv) {
+            H2Launch tmp;
+            put_panel({fin_pv[2 * k], fin_pv[2 * k + 1]}, tmp);
+            P->steps[k].pi0 = tmp.pan0;
+            P->steps[k].npi = tmp.npan;
+        }
     }
     push();
     FDE_CUDA(cudaMemsetAsync(A + lr_lo, 0, (size_t)(lr_hi - lr_lo) * sizeof(double), sa));
+    if (pan_inv) FDE_CUDA(cudaMemsetAsync(A + inv_lo, 0, (size_t)(inv_hi - inv_lo) * sizeof(double), sa));
     FDE_CUDA(cudaStreamWaitEvent(sa, evD, 0));
     run_copy(P->init, sa);
     run_trunc(P->init.tr, sa, 0);
@@ -1342,8 +1598,11 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
     const int kstop = g_hlu2_stop >= 0 ? std::min(g_hlu2_stop, nl) : nl;   // debug: partial sweep
     // debug timeline (FDE_DEBUG_TIMELINE): timed events per step and stream
     const bool tline = getenv("FDE_DEBUG_TIMELINE") != nullptr;
-    enum { T_LU = 0, T_PAN, T_PROD, T_CRIT, T_OP, T_OV, T_CP, T_REST, T_N };
+    const bool skip_rest = getenv("FDE_H2_SKIPREST") != nullptr;
+    enum { T_LU = 0, T_PAN, T_PROD, T_CRIT, T_OP, T_OV, T_CP, T_REST, T_SNAP, T_DIAG, T_G1, T_G2, T_GRAM, T_CORE, T_PUSH, T_N };
     std::vector<cudaEvent_t> tev;
+    std::vector<double> thost;
+    const auto th0 = std::chrono::steady_clock::now();
     cudaEvent_t t0ev = nullptr;
     if (tline) {
         tev.resize((size_t)kstop * T_N);
@@ -1386,11 +1645,15 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
             std::vector<VTask> diag, crit, rest;
             for (size_t q = 0; q < st.g3.size(); ++q)
                 (st.g3crit[q] == 2 ? diag : st.g3crit[q] ? crit : rest).push_back(std::move(st.g3[q]));
+            ln.diag_scr = false;
+            for (auto& t : diag)
+                for (auto& tm : t.terms) ln.diag_scr |= tm.A.sp == 3 || tm.B.sp == 3;
             put_gemm(crit, ln, 2);
             put_gemm(rest, ln, 4);
             put_gemm(diag, ln, 5);
         }
         push();
+        mark(k, T_PUSH, sd);
         dbg("push");
         FDE_CUDA(cudaStreamWaitEvent(sa, evD, 0));
         FDE_CUDA(cudaStreamWaitEvent(sb, evD, 0));
@@ -1402,17 +1665,21 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         // blocks are disjoint); they only have to precede this step's new columns
         FDE_CUDA(cudaEventRecord(evCp, sb));
         FDE_CUDA(cudaStreamWaitEvent(se, evCp, 0));
+        FDE_CUDA(cudaStreamWaitEvent(se, evSnap, 0));   // snapshots of step k-1 taken
         run_trunc(ln.tr_ov, se, 1);
         FDE_CUDA(cudaEventRecord(evOv, se));
         mark(k, T_OV, se);
+        FDE_CUDA(cudaStreamWaitEvent(sb, evSnap, 0));
+        if (tline) tmark = [&](int w) { mark(k, w ? T_CORE : T_GRAM, sb); };
         run_trunc(ln.tr, sb, 0);
+        tmark = [](int) {};
         FDE_CUDA(cudaEventRecord(evOp, sb));
         mark(k, T_OP, sb);
         // sa: critical chain.  LU(k) ran on sl (k = 0: here), overlapping the
         // products and updates of step k-1; its only input from step k-1 is the
-        // update of the diagonal tile, issued right after the panels of step k-1.
+        // update of the diagonal tile, issued on sl right after the panels of step k-1.
         if (k == 0) {
-            k_h2_lu<<<1, 512, lu_smem, sl>>>(P->lu.p + ln.lu, L->dflag.p);
+            launch_lu(k, sl);
             FDE_CHECK_LAUNCH();
             ++nlaunch;
             FDE_CUDA(cudaEventRecord(evLU, sl));
@@ -1421,29 +1688,46 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         FDE_CUDA(cudaStreamWaitEvent(sa, evOp, 0));
         run_panel(ln);
         mark(k, T_PAN, sa);
+        auto diag_lu = [&](cudaStream_t st) {   // tile (k+1, k+1), then LU(k+1) on sl
+            run_gemm(ln, 5, st);
+            mark(k, T_DIAG, st);
+            if (k + 1 < kstop) {
+                if (st != sl) {
+                    FDE_CUDA(cudaEventRecord(evDg, st));
+                    FDE_CUDA(cudaStreamWaitEvent(sl, evDg, 0));
+                }
+                launch_lu(k + 1, sl);
+                FDE_CHECK_LAUNCH();
+                ++nlaunch;
+                dbg("lu");
+                FDE_CUDA(cudaEventRecord(evLU, sl));
+                mark(k, T_LU, sl);
+            }
+        };
+        if (!ln.diag_scr) {   // dense x dense terms only: beside the products
+            FDE_CUDA(cudaEventRecord(evPan, sa));
+            FDE_CUDA(cudaStreamWaitEvent(sl, evPan, 0));
+            diag_lu(sl);
+        }
+        run_gemm(ln, 0, sa);
+        mark(k, T_G1, sa);
+        run_gemm(ln, 1, sa);
+        mark(k, T_G2, sa);
+        run_gemm(ln, 3, sa);   // conversions to dense (after the products: a block may be
+                               // an operand (row / column k) and a target (rows > k) at once)
+        FDE_CUDA(cudaEventRecord(evP, sa));
+        mark(k, T_PROD, sa);
+        // snapshots of the operand factors for the dense updates (before the
+        // truncations of step k+1 rewrite them: sb / se wait for evSnap)
         if (ln.nsnap) {
             k_h2_copy<<<ln.nsnap, 256, 0, sa>>>(P->cps.p + ln.snap0);
             FDE_CHECK_LAUNCH();
             ++nlaunch;
             dbg("snapshots");
         }
-        run_gemm(ln, 5, sa);                         // diagonal tile (k+1, k+1)
-        if (k + 1 < kstop) {
-            FDE_CUDA(cudaEventRecord(evDg, sa));
-            FDE_CUDA(cudaStreamWaitEvent(sl, evDg, 0));
-            k_h2_lu<<<1, 512, lu_smem, sl>>>(P->lu.p + P->steps[k + 1].lu, L->dflag.p);
-            FDE_CHECK_LAUNCH();
-            ++nlaunch;
-            dbg("lu");
-            FDE_CUDA(cudaEventRecord(evLU, sl));
-            mark(k, T_LU, sl);
-        }
-        run_gemm(ln, 0, sa);
-        run_gemm(ln, 1, sa);
-        run_gemm(ln, 3, sa);   // conversions to dense (after the products: a block may be
-                               // an operand (row / column k) and a target (rows > k) at once)
-        FDE_CUDA(cudaEventRecord(evP, sa));
-        mark(k, T_PROD, sa);
+        FDE_CUDA(cudaEventRecord(evSnap, sa));
+        mark(k, T_SNAP, sa);
+        if (ln.diag_scr) diag_lu(sa);
         FDE_CUDA(cudaStreamWaitEvent(sa, evC, 0));   // remaining updates of step k-1
         run_gemm(ln, 2, sa);                         // row / column k+1
         mark(k, T_CRIT, sa);
@@ -1460,15 +1744,17 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         }
         mark(k, T_CP, sb);
         // sc: the other dense updates of step k
-        FDE_CUDA(cudaStreamWaitEvent(sc, evP, 0));
-        run_gemm(ln, 4, sc);
+        FDE_CUDA(cudaStreamWaitEvent(sc, evSnap, 0));
+        if (!skip_rest) run_gemm(ln, 4, sc);   // (debug FDE_H2_SKIPREST: timing experiments only)
         FDE_CUDA(cudaEventRecord(evC, sc));
         mark(k, T_REST, sc);
+        if (tline) thost.push_back(std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - th0).count());
     }
     if (tline) {
         FDE_CUDA(cudaDeviceSynchronize());
         const char* nm[T_N] = {"LU(k+1) end", "panel end", "products end", "crit end", "trunc_op end", "trunc_ov end",
-                               "copies end", "rest end"};
+                               "copies end", "rest end", "snap end", "diag end", "g1 end", "g2 end", "op gram end",
+                               "op core end", "push done"};
         double prev[T_N] = {0};
         double sum[T_N] = {0};
         for (int k = 0; k < kstop; ++k)
@@ -1480,11 +1766,26 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
             }
         fprintf(stderr, "hlu2 timeline (%d steps): per-step period of each mark (us):", kstop);
         for (int w = 0; w < T_N; ++w) fprintf(stderr, " %s %.1f |", nm[w], 1e3 * sum[w] / std::max(1, kstop - 1));
+        if (kstop > 1)
+            fprintf(stderr, " host enqueue %.1f |", (thost.back() - thost.front()) / (kstop - 1));
         fprintf(stderr, "\n  step 10 marks (ms from start):");
         for (int w = 0; w < T_N && kstop > 10; ++w) {
             float ms = 0;
             cudaEventElapsedTime(&ms, t0ev, tev[(size_t)10 * T_N + w]);
             fprintf(stderr, " %s %.3f |", nm[w], ms);
+        }
+        fprintf(stderr, "\n  mean offset from the previous step's copies end (us):");
+        for (int w = 0; w < T_N; ++w) {
+            double acc = 0;
+            int cnt = 0;
+            for (int k = 4; k + 4 < kstop; ++k) {
+                float a = 0, b = 0;
+                if (cudaEventElapsedTime(&a, t0ev, tev[(size_t)(k - 1) * T_N + T_CP]) != cudaSuccess) continue;
+                if (cudaEventElapsedTime(&b, t0ev, tev[(size_t)k * T_N + w]) != cudaSuccess) continue;
+                acc += b - a;
+                ++cnt;
+            }
+            if (cnt) fprintf(stderr, " %s %.1f |", nm[w], 1e3 * acc / cnt);
         }
         fprintf(stderr, "\n");
         for (auto& e : tev) cudaEventDestroy(e);
@@ -1495,8 +1796,10 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
     FDE_CUDA(cudaStreamWaitEvent(sa, evB, 0));
     FDE_CUDA(cudaStreamWaitEvent(sa, evC, 0));
     if (kstop == nl) {
-        put_copy(fin_cp, P->fin);
-        put_panel(fin_pv, P->fin);
+        if (!pan_inv) {
+            put_copy(fin_cp, P->fin);
+            put_panel(fin_pv, P->fin);
+        }
         P->fin_lv.resize(fin_tt.size());
         for (size_t dd = 0; dd < fin_tt.size(); ++dd) {
             put_gemm(fin_tt[dd], P->fin_lv[dd], 0);
@@ -1504,9 +1807,11 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         }
         push();
         FDE_CUDA(cudaStreamWaitEvent(sa, evD, 0));
-        FDE_CUDA(cudaMemsetAsync(A + inv_lo, 0, (size_t)(inv_hi - inv_lo) * sizeof(double), sa));
-        run_copy(P->fin, sa);
-        run_panel(P->fin);
+        if (!pan_inv) {
+            FDE_CUDA(cudaMemsetAsync(A + inv_lo, 0, (size_t)(inv_hi - inv_lo) * sizeof(double), sa));
+            run_copy(P->fin, sa);
+            run_panel(P->fin);
+        }
         for (auto& lv : P->fin_lv) {
             run_gemm(lv, 0, sa);
             run_gemm(lv, 1, sa);
@@ -1535,6 +1840,25 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
                 wconv += S.bl[b].m * S.bl[b].n;
             }
         fprintf(stderr, "hlu2 plan: %d low-rank blocks converted to dense (%.1f MB)\n", nconv, wconv * 8e-6);
+    }
+    if (getenv("FDE_DEBUG_PLAN")) {
+        double gt[6] = {0}, gmx[6] = {0}, tr = 0, trk = 0, pn = 0, cp = 0;
+        for (auto& ln : P->steps) {
+            for (int w = 0; w < 6; ++w) { gt[w] += ln.g_ntile[w]; gmx[w] = std::max(gmx[w], (double)ln.g_ntile[w]); }
+            tr += ln.tr.ne;
+            trk += ln.tr.nc;
+            pn += ln.npan;
+            for (auto& c : ln.cpr) cp += c.second;
+        }
+        fprintf(stderr, "hlu2 plan: per step: gemm tiles (mean/max) cores %.1f/%g products %.1f/%g crit %.1f/%g "
+                        "conv %.1f/%g rest %.1f/%g diag %.1f/%g | operand trunc entries %.1f chunks %.1f | panel CTAs %.1f "
+                        "| copy CTAs %.1f\n", gt[0] / nl, gmx[0], gt[1] / nl, gmx[1], gt[2] / nl, gmx[2], gt[3] / nl, gmx[3],
+                gt[4] / nl, gmx[4], gt[5] / nl, gmx[5], tr / nl, trk / nl, pn / nl, cp / nl);
+        fprintf(stderr, "hlu2 plan: per step MFLOP / C MB: cores %.1f/%.1f products %.1f/%.1f crit %.1f/%.1f "
+                        "rest %.1f/%.1f diag %.1f/%.1f\n", gstat_flop[0] / nl * 1e-6, gstat_cbytes[0] / nl * 1e-6,
+                gstat_flop[1] / nl * 1e-6, gstat_cbytes[1] / nl * 1e-6, gstat_flop[2] / nl * 1e-6,
+                gstat_cbytes[2] / nl * 1e-6, gstat_flop[4] / nl * 1e-6, gstat_cbytes[4] / nl * 1e-6,
+                gstat_flop[5] / nl * 1e-6, gstat_cbytes[5] / nl * 1e-6);
     }
     if (getenv("FDE_DEBUG_PLAN"))
         fprintf(stderr, "hlu2 plan: nl %d blocks %d | simulate %.2f ms, layout+alloc %.2f ms, counts %.2f ms, "

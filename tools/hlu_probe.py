@@ -23,4 +23,4 @@ for it in range(2):
 import ctypes
 st = (ctypes.c_ulonglong * 4)()
 fde.lib().fde_debug_trunc_stats(st)
-print("trunc calls", st[0], "avg ke", st[1] / max(st[0], 1), "avg sweeps (2 eigs)", st[2] / max(st[0], 1), "max ke", st[3])
+print("trunc calls", st[0], "avg ke", st[1] / max(st[0], 1), "avg sweeps (2 eigs)", st[2] / max(st[0], 1), "max sweeps (one solve)", st[3])
