@@ -423,7 +423,7 @@ __global__ void __launch_bounds__(256) k_h2_panel(const H2Panel* P)
 // layout / transpose), so two slices are in flight while one is multiplied.
 #define H2G_ST 3
 #define H2G_TMAX 48
-#define H2G_SMEM(TG) (2 * H2G_ST * GK * ((TG) + 1) * (int)sizeof(double))
+#define H2G_SMEM(TM, TN) (H2G_ST * GK * ((TM) + (TN) + 2) * (int)sizeof(double))
 struct H2Cursor {   // position in the (term, slice) sequence of a tile
     int q, k0;
 };
@@ -436,23 +436,29 @@ __device__ __forceinline__ void h2_next(const H2Term* terms, int t_hi, H2Cursor&
         while (c.q < t_hi && terms[c.q].k <= 0) ++c.q;
     }
 }
-template <int TG>
+template <int TM, int TN>
 __device__ __forceinline__ void h2_stage(const H2Term& T, int m0, int n0, int m, int n, int k0, double* sA, double* sB)
 {
-    // sA[kk][mm] (ld TG + 1), sB[kk][nn]; zero outside the operands
+    // sA[kk][mm] (ld TM + 1), sB[kk][nn] (ld TN + 1); zero outside the operands
 #pragma unroll
-    for (int u = 0; u < TG * GK / 256; ++u) {
+    for (int u = 0; u < (TM * GK + 255) / 256; ++u) {
         const int t = threadIdx.x + 256 * u;
+        if (TM * GK < 256 && t >= TM * GK) break;
         int kk, mm;
-        if (T.ta) { mm = t / GK; kk = t % GK; } else { kk = t / TG; mm = t % TG; }
+        if (T.ta) { mm = t / GK; kk = t % GK; } else { kk = t / TM; mm = t % TM; }
         const int gi = m0 + mm, gk = k0 + kk;
-        double* da = sA + kk * (TG + 1) + mm;
+        double* da = sA + kk * (TM + 1) + mm;
         if (gi < m && gk < T.k) cp_async8(da, T.ta ? T.A + (long long)gi * T.lda + gk : T.A + (long long)gk * T.lda + gi);
         else *da = 0.0;
-        int nn;
-        if (T.tb) { kk = t / TG; nn = t % TG; } else { nn = t / GK; kk = t % GK; }
+    }
+#pragma unroll
+    for (int u = 0; u < (TN * GK + 255) / 256; ++u) {
+        const int t = threadIdx.x + 256 * u;
+        if (TN * GK < 256 && t >= TN * GK) break;
+        int kk, nn;
+        if (T.tb) { kk = t / TN; nn = t % TN; } else { nn = t / GK; kk = t % GK; }
         const int gj = n0 + nn, gk2 = k0 + kk;
-        double* db = sB + kk * (TG + 1) + nn;
+        double* db = sB + kk * (TN + 1) + nn;
         if (gj < n && gk2 < T.k) cp_async8(db, T.tb ? T.B + (long long)gk2 * T.ldb + gj : T.B + (long long)gj * T.ldb + gk2);
         else *db = 0.0;
     }
@@ -461,13 +467,21 @@ __device__ __forceinline__ void cp_async_commit_group() { asm volatile("cp.async
 template <int N>
 __device__ __forceinline__ void cp_async_wait_group() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
-template <int TG>
+// warp grid of the DMMA path (8 x 8 fragments of mma.sync.m8n8k4.f64): WM x WN warps
+template <int TM, int TN> struct H2Warps {
+    static constexpr int WM = (TN == 16 && TM >= 128) ? 8 : (TM >= 32 ? 4 : 2);
+    static constexpr int WN = (TN == 16 && TM >= 128) ? 1 : 2;
+};
+template <int TM, int TN, bool DM>
 __device__ __forceinline__ void h2_gemm_tile(const H2Tile* tiles, int tile, const H2Task* tasks, const H2Term* terms)
 {
-    constexpr int RT = TG / 16;      // register tile RT x RT per thread (16 x 16 threads)
+    constexpr int RM = TM / 16, RN = TN / 16;   // register tile RM x RN per thread (16 x 16 threads)
+    constexpr int WM = H2Warps<TM, TN>::WM, WN = H2Warps<TM, TN>::WN;
+    constexpr int FM = TM / (8 * WM), FN = TN / (8 * WN);   // DMMA fragments per warp
+    static_assert(FM >= 1 && FN >= 1 && WM * WN <= 8, "warp grid");
     extern __shared__ double gsm[];   // H2G_SMEM bytes: [stage] A slice, [stage] B slice
-    double (*sA)[GK * (TG + 1)] = reinterpret_cast<double (*)[GK * (TG + 1)]>(gsm);
-    double (*sB)[GK * (TG + 1)] = reinterpret_cast<double (*)[GK * (TG + 1)]>(gsm + H2G_ST * GK * (TG + 1));
+    double (*sA)[GK * (TM + 1)] = reinterpret_cast<double (*)[GK * (TM + 1)]>(gsm);
+    double (*sB)[GK * (TN + 1)] = reinterpret_cast<double (*)[GK * (TN + 1)]>(gsm + H2G_ST * GK * (TM + 1));
     __shared__ double sAlpha[H2G_ST];
     __shared__ H2Term sT[H2G_TMAX];   // the task's term descriptors (one global read each)
     const H2Tile tl = tiles[tile];
@@ -485,7 +499,7 @@ __device__ __forceinline__ void h2_gemm_tile(const H2Tile* tiles, int tile, cons
     if (threadIdx.x == 0) sbad = 0;
     if (g_h2_check && threadIdx.x == 0) {
         // C: columns [n0, n0+64) rows [m0, m0+64) clipped
-        const int mm = min(TG, m - m0), nn = min(TG, n - n0);
+        const int mm = min(TM, m - m0), nn = min(TN, n - n0);
         if (mm > 0 && nn > 0) h2_chk(tk.C + (long long)n0 * tk.ldc + m0, ((long long)(nn - 1) * tk.ldc + mm) * 8, 1, m, n);
         for (int q = 0; q < nt; ++q) {
             const H2Term T = terms[tk.t_lo + q];
@@ -502,11 +516,19 @@ __device__ __forceinline__ void h2_gemm_tile(const H2Tile* tiles, int tile, cons
     }
     __syncthreads();
     if (sbad) return;
-    double acc[RT][RT];
+    double acc[RM][RN];
 #pragma unroll
-    for (int i = 0; i < RT; ++i)
+    for (int i = 0; i < RM; ++i)
 #pragma unroll
-        for (int j = 0; j < RT; ++j) acc[i][j] = 0.0;
+        for (int j = 0; j < RN; ++j) acc[i][j] = 0.0;
+    double dacc[FM][FN][2];
+#pragma unroll
+    for (int i = 0; i < FM; ++i)
+#pragma unroll
+        for (int j = 0; j < FN; ++j) dacc[i][j][0] = dacc[i][j][1] = 0.0;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int wm = (warp % WM) * (TM / WM), wn = (warp / WM) * (TN / WN);
+    const bool wact = warp < WM * WN;
     H2Cursor ld{0, -GK};   // next slice to load
     while (ld.q < nt && tm[ld.q].k <= 0) ++ld.q;
     ld.k0 = 0;
@@ -517,7 +539,7 @@ __device__ __forceinline__ void h2_gemm_tile(const H2Tile* tiles, int tile, cons
     for (int st = 0; st < H2G_ST - 1; ++st) {
         if (st < nslice) {
             const H2Term& T = tm[ld.q];
-            h2_stage<TG>(T, m0, n0, m, n, ld.k0, sA[st], sB[st]);
+            h2_stage<TM, TN>(T, m0, n0, m, n, ld.k0, sA[st], sB[st]);
             if (threadIdx.x == 0) sAlpha[st] = T.alpha;
             h2_next(tm, nt, ld);
         }
@@ -531,7 +553,7 @@ __device__ __forceinline__ void h2_gemm_tile(const H2Tile* tiles, int tile, cons
         if (nx < nslice) {
             const int st = nx % H2G_ST;
             const H2Term& T = tm[ld.q];
-            h2_stage<TG>(T, m0, n0, m, n, ld.k0, sA[st], sB[st]);
+            h2_stage<TM, TN>(T, m0, n0, m, n, ld.k0, sA[st], sB[st]);
             if (threadIdx.x == 0) sAlpha[st] = T.alpha;
             h2_next(tm, nt, ld);
         }
@@ -540,24 +562,58 @@ __device__ __forceinline__ void h2_gemm_tile(const H2Tile* tiles, int tile, cons
         const double* a_s = sA[cs];
         const double* b_s = sB[cs];
         const double al = sAlpha[cs];
+        if (DM) {   // FP64 tensor cores: one mma per 8 x 8 x 4 block
+            if (wact) {
 #pragma unroll
-        for (int kk = 0; kk < GK; ++kk) {
-            double a[RT], b[RT];
+                for (int kk = 0; kk < GK; kk += 4) {
+                    double a[FM], b[FN];
+                    const int kr = kk + (lane & 3);
 #pragma unroll
-            for (int i = 0; i < RT; ++i) a[i] = al * a_s[kk * (TG + 1) + tx + 16 * i];
+                    for (int i = 0; i < FM; ++i) a[i] = al * a_s[kr * (TM + 1) + wm + i * 8 + (lane >> 2)];
 #pragma unroll
-            for (int j = 0; j < RT; ++j) b[j] = b_s[kk * (TG + 1) + ty + 16 * j];
+                    for (int j = 0; j < FN; ++j) b[j] = b_s[kr * (TN + 1) + wn + j * 8 + (lane >> 2)];
 #pragma unroll
-            for (int i = 0; i < RT; ++i)
+                    for (int i = 0; i < FM; ++i)
 #pragma unroll
-                for (int j = 0; j < RT; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+                        for (int j = 0; j < FN; ++j) dmma(dacc[i][j][0], dacc[i][j][1], a[i], b[j]);
+                }
+            }
+        } else {
+#pragma unroll
+            for (int kk = 0; kk < GK; ++kk) {
+                double a[RM], b[RN];
+#pragma unroll
+                for (int i = 0; i < RM; ++i) a[i] = al * a_s[kk * (TM + 1) + tx + 16 * i];
+#pragma unroll
+                for (int j = 0; j < RN; ++j) b[j] = b_s[kk * (TN + 1) + ty + 16 * j];
+#pragma unroll
+                for (int i = 0; i < RM; ++i)
+#pragma unroll
+                    for (int j = 0; j < RN; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+            }
         }
     }
     cp_async_wait_group<0>();
+    if (DM) {
+        if (wact)
 #pragma unroll
-    for (int i = 0; i < RT; ++i)
+            for (int i = 0; i < FM; ++i)
 #pragma unroll
-        for (int j = 0; j < RT; ++j) {
+                for (int j = 0; j < FN; ++j)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int gi = m0 + wm + i * 8 + (lane >> 2), gj = n0 + wn + j * 8 + 2 * (lane & 3) + h;
+                        if (gi < m && gj < n) {
+                            double* c = tk.C + (long long)gj * tk.ldc + gi;
+                            *c = dacc[i][j][h] + (tk.beta == 0.0 ? 0.0 : tk.beta * *c);
+                        }
+                    }
+        return;
+    }
+#pragma unroll
+    for (int i = 0; i < RM; ++i)
+#pragma unroll
+        for (int j = 0; j < RN; ++j) {
             const int gi = m0 + tx + 16 * i, gj = n0 + ty + 16 * j;
             if (gi < m && gj < n) {
                 double* c = tk.C + (long long)gj * tk.ldc + gi;
@@ -567,11 +623,11 @@ __device__ __forceinline__ void h2_gemm_tile(const H2Tile* tiles, int tile, cons
 }
 
 // grid-stride over the tiles: a capped grid leaves SMs to the critical stream
-template <int TG>
+template <int TM, int TN, bool DM>
 __global__ void __launch_bounds__(256) k_h2_gemm(const H2Tile* tiles, const H2Task* tasks, const H2Term* terms, int ntile)
 {
     for (int t = blockIdx.x; t < ntile; t += gridDim.x) {
-        h2_gemm_tile<TG>(tiles, t, tasks, terms);
+        h2_gemm_tile<TM, TN, DM>(tiles, t, tasks, terms);
         __syncthreads();
     }
 }
@@ -660,7 +716,7 @@ struct H2Launch {      // ranges in the flat device arrays
     int lu = -1;
     int pan0 = 0, npan = 0;
     int pi0 = 0, npi = 0;                   // inverses of the factors of this step's tile (after its LU)
-    int g_tile0[6] = {0, 0, 0, 0, 0, 0}, g_ntile[6] = {0, 0, 0, 0, 0, 0};
+    int g_tile0[6] = {0, 0, 0, 0, 0, 0}, g_ntile[6] = {0, 0, 0, 0, 0, 0}, g_shape[6] = {0, 0, 0, 0, 0, 0};
     int cp0 = 0, ncp = 0;
     bool diag_scr = false;                  // the diagonal-tile update reads step scratch
 };
@@ -1229,11 +1285,14 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
     double gstat_flop[6] = {0}, gstat_cbytes[6] = {0};   // (FDE_DEBUG_PLAN statistics)
     // GEMM tile per launch group (cores, products, crit, conversions, rest, diag):
     // 32 x 32 where a launch has few tiles (latency: more CTAs, shorter chains)
-    int gemm_tg[6] = {64, 64, 64, 64, 64, 32};
-    if (const char* e = getenv("FDE_H2_TG32"))   // e.g. "5", "0125"
-        for (const char* c = e; *c; ++c)
-            if (*c >= '0' && *c <= '5') gemm_tg[*c - '0'] = 32;
-    auto put_gemm = [&](const std::vector<VTask>& v, H2Launch& ln, int which) {
+    // tile shape per launch group (0 cores, 1 products, 2 crit, 3 conversions, 4 rest,
+    // 5 diag): 0 = 64 x 64, 1 = 32 x 32 (few tiles: more CTAs, shorter chains),
+    // 2 = 128 x 16 (products: outputs rmax wide), 3 = 16 x 16 (cores: rmax x rmax)
+    int gemm_shape[6] = {rmax <= 16 ? 3 : 1, rmax <= 16 ? 2 : 0, 0, 0, 0, 1};
+    if (const char* e = getenv("FDE_H2_SHAPES"))   // debug: six digits
+        for (int w = 0; w < 6 && e[w]; ++w) gemm_shape[w] = (e[w] - '0') & 3;
+    auto put_gemm = [&](const std::vector<VTask>& v, H2Launch& ln, int which, int shape) {
+        ln.g_shape[which] = shape;
         ln.g_tile0[which] = (int)vtile.size();
         for (auto& t : v) {
             H2Task d;
@@ -1250,9 +1309,10 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
             gstat_cbytes[which] += 16.0 * t.m * t.n;
             const int ti = (int)vtask.size();
             vtask.push_back(d);
-            const int tg = gemm_tg[which];
-            for (int m0 = 0; m0 < t.m; m0 += tg)
-                for (int n0 = 0; n0 < t.n; n0 += tg) vtile.push_back({ti, m0, n0});
+            static const int shm[4] = {64, 32, 128, 16}, shn[4] = {64, 32, 16, 16};
+            const int tm = shm[shape], tn = shn[shape];
+            for (int m0 = 0; m0 < t.m; m0 += tm)
+                for (int n0 = 0; n0 < t.n; n0 += tn) vtile.push_back({ti, m0, n0});
         }
         ln.g_ntile[which] = (int)vtile.size() - ln.g_tile0[which];
     };
@@ -1345,11 +1405,12 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
     }
     // ---- exact descriptor counts -> device arrays and the pinned staging buffer
     size_t n_pan = 0, n_task = 0, n_term = 0, n_tile = 0, n_cp = 0, n_te = 0, n_tc = 0;
-    auto cnt_tasks = [&](const std::vector<VTask>& v) {
+    auto cnt_tasks = [&](const std::vector<VTask>& v, int shape) {
+        static const int shm[4] = {64, 32, 128, 16}, shn[4] = {64, 32, 16, 16};
         for (auto& t : v) {
             ++n_task;
             n_term += t.terms.size();
-            n_tile += (size_t)(ceil_div(t.m, 32) * ceil_div(t.n, 32));   // (upper bound: 32 x 32 tiles)
+            n_tile += (size_t)(ceil_div(t.m, shm[shape]) * ceil_div(t.n, shn[shape]));
         }
     };
     auto cnt_trunc = [&](const std::vector<VTrunc>& v) {
@@ -1378,18 +1439,18 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         cnt_trunc(st.trunc);
         cnt_trunc(st.trunc_ov);
         cnt_pan(st.panel);
-        cnt_tasks(st.g0);
-        cnt_tasks(st.g1);
-        cnt_tasks(st.g2);
-        cnt_tasks(st.g3);
+        cnt_tasks(st.g0, gemm_shape[3]);
+        cnt_tasks(st.g1, gemm_shape[0]);
+        cnt_tasks(st.g2, gemm_shape[1]);
+        cnt_tasks(st.g3, 1);   // (crit / rest / diag: at most the tiles of the 32 x 32 shape)
         for (auto& v : st.cpr) cnt_cp(v);
         cnt_cp(st.snap);
         for (auto& v : st.trmid) cnt_trunc(v);
     }
     cnt_cp(fin_cp);
     cnt_pan(fin_pv);
-    for (auto& v : fin_tt) cnt_tasks(v);
-    for (auto& v : fin_tx) cnt_tasks(v);
+    for (auto& v : fin_tt) cnt_tasks(v, 0);
+    for (auto& v : fin_tx) cnt_tasks(v, 0);
     vlu.reserve(nl); vpan.reserve(n_pan); vterm.reserve(n_term); vtask.reserve(n_task);
     vtile.reserve(n_tile); vcp.reserve(n_cp); vte.reserve(n_te); vtc.reserve(n_tc);
     P->lu.alloc(std::max<size_t>(nl, 1));
@@ -1473,8 +1534,15 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
     const int pan_smem_inv = (H2_STRIP + H2_PCH) * (H2_MMAX + 2) * (int)sizeof(double);
     const int lu_smem = H2_MMAX * (H2_MMAX + 1) * (int)sizeof(double);   // padded 128 x 129
     set_smem_once((const void*)k_h2_lu, lu_smem);
-    set_smem_once((const void*)k_h2_gemm<64>, H2G_SMEM(64));
-    set_smem_once((const void*)k_h2_gemm<32>, H2G_SMEM(32));
+    static const bool use_dmma = !getenv("FDE_H2_NODMMA");
+    set_smem_once((const void*)k_h2_gemm<64, 64, true>, H2G_SMEM(64, 64));
+    set_smem_once((const void*)k_h2_gemm<128, 16, true>, H2G_SMEM(128, 16));
+    set_smem_once((const void*)k_h2_gemm<32, 32, true>, H2G_SMEM(32, 32));
+    set_smem_once((const void*)k_h2_gemm<16, 16, true>, H2G_SMEM(16, 16));
+    set_smem_once((const void*)k_h2_gemm<64, 64, false>, H2G_SMEM(64, 64));
+    set_smem_once((const void*)k_h2_gemm<128, 16, false>, H2G_SMEM(128, 16));
+    set_smem_once((const void*)k_h2_gemm<32, 32, false>, H2G_SMEM(32, 32));
+    set_smem_once((const void*)k_h2_gemm<16, 16, false>, H2G_SMEM(16, 16));
     int nlaunch = 0;
     // FDE_DEBUG_SERIAL: synchronise after every launch and name the first failing one
     const bool dbg_serial = getenv("FDE_DEBUG_SERIAL") != nullptr;
@@ -1551,10 +1619,17 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
     auto run_gemm = [&](const H2Launch& ln, int w, cudaStream_t st) {
         if (!ln.g_ntile[w]) return;
         const int grid = std::min(ln.g_ntile[w], gemm_cap[w]);
-        if (gemm_tg[w] == 32)
-            k_h2_gemm<32><<<grid, 256, H2G_SMEM(32), st>>>(P->tiles.p + ln.g_tile0[w], P->tasks.p, P->terms.p, ln.g_ntile[w]);
-        else
-            k_h2_gemm<64><<<grid, 256, H2G_SMEM(64), st>>>(P->tiles.p + ln.g_tile0[w], P->tasks.p, P->terms.p, ln.g_ntile[w]);
+        const H2Tile* tl = P->tiles.p + ln.g_tile0[w];
+#define H2G_LAUNCH(TM_, TN_)                                                                                   \
+    (use_dmma ? k_h2_gemm<TM_, TN_, true><<<grid, 256, H2G_SMEM(TM_, TN_), st>>>(tl, P->tasks.p, P->terms.p, ln.g_ntile[w]) \
+              : k_h2_gemm<TM_, TN_, false><<<grid, 256, H2G_SMEM(TM_, TN_), st>>>(tl, P->tasks.p, P->terms.p, ln.g_ntile[w]))
+        switch (ln.g_shape[w]) {
+            case 1: H2G_LAUNCH(32, 32); break;
+            case 2: H2G_LAUNCH(128, 16); break;
+            case 3: H2G_LAUNCH(16, 16); break;
+            default: H2G_LAUNCH(64, 64);
+        }
+#undef H2G_LAUNCH
         FDE_CHECK_LAUNCH();
         ++nlaunch;
         static const char* gname[6] = {"gemm cores", "gemm products", "gemm crit", "gemm conversions", "gemm rest",
@@ -1621,9 +1696,9 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         put_trunc(st.trunc, ln.tr);
         put_trunc(st.trunc_ov, ln.tr_ov);
         put_panel(st.panel, ln);
-        put_gemm(st.g0, ln, 3);
-        put_gemm(st.g1, ln, 0);
-        put_gemm(st.g2, ln, 1);
+        put_gemm(st.g0, ln, 3, gemm_shape[3]);
+        put_gemm(st.g1, ln, 0, gemm_shape[0]);
+        put_gemm(st.g2, ln, 1, gemm_shape[1]);
         {
             H2Launch tmp;
             put_copy(st.snap, tmp);
@@ -1648,9 +1723,9 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
             ln.diag_scr = false;
             for (auto& t : diag)
                 for (auto& tm : t.terms) ln.diag_scr |= tm.A.sp == 3 || tm.B.sp == 3;
-            put_gemm(crit, ln, 2);
-            put_gemm(rest, ln, 4);
-            put_gemm(diag, ln, 5);
+            put_gemm(crit, ln, 2, gemm_shape[2]);
+            put_gemm(rest, ln, 4, gemm_shape[4]);
+            put_gemm(diag, ln, 5, gemm_shape[5]);
         }
         push();
         mark(k, T_PUSH, sd);
@@ -1802,8 +1877,8 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         }
         P->fin_lv.resize(fin_tt.size());
         for (size_t dd = 0; dd < fin_tt.size(); ++dd) {
-            put_gemm(fin_tt[dd], P->fin_lv[dd], 0);
-            put_gemm(fin_tx[dd], P->fin_lv[dd], 1);
+            put_gemm(fin_tt[dd], P->fin_lv[dd], 0, 0);
+            put_gemm(fin_tx[dd], P->fin_lv[dd], 1, 0);
         }
         push();
         FDE_CUDA(cudaStreamWaitEvent(sa, evD, 0));
