@@ -700,12 +700,15 @@ __global__ void __launch_bounds__(256) k_trunc_core(const double* Gu, const doub
     double* X = Eu + n * n;
     double* lu = X + n * n;
     int* pairs = (int*)(lu + n);
+    __shared__ double sc[256];   // column norms of U: the Gram matrix is scaled to unit diagonal (see k_bcore)
+    for (int t = threadIdx.x; t < ke; t += blockDim.x) sc[t] = sqrt(Gu[idx[t] * k + idx[t]]);
+    __syncthreads();
     for (int t = threadIdx.x; t < n * n; t += blockDim.x) {
         const int i = t % n, j = t / n;
-        A[t] = (i < ke && j < ke) ? Gu[idx[j] * k + idx[i]] : 0.0;
+        A[t] = (i < ke && j < ke) ? Gu[idx[j] * k + idx[i]] / (sc[i] * sc[j]) : 0.0;
     }
     __syncthreads();
-    const int sw1 = cta_jacobi(A, Eu, n, pairs);
+    const int sw1 = cta_jacobi(A, Eu, n, pairs, 1e-15, 1e-16);
     __shared__ double mu;
     if (threadIdx.x == 0) {
         double a = 0.0;
@@ -723,7 +726,7 @@ __global__ void __launch_bounds__(256) k_trunc_core(const double* Gu, const doub
         const int i = t % n, j = t / n;   // (Gv Eu)_ij
         double s = 0.0;
         if (i < ke)
-            for (int q = 0; q < ke; ++q) s = fma(Gv[idx[q] * k + idx[i]], Eu[j * n + q], s);
+            for (int q = 0; q < ke; ++q) s = fma(Gv[idx[q] * k + idx[i]] * (sc[q] * sc[i]), Eu[j * n + q], s);
         X[t] = s;
     }
     __syncthreads();
@@ -734,7 +737,7 @@ __global__ void __launch_bounds__(256) k_trunc_core(const double* Gu, const doub
         A[t] = lu[i] * lu[j] * s;
     }
     __syncthreads();
-    const int sw2 = cta_jacobi(A, X, n, pairs);
+    const int sw2 = cta_jacobi(A, X, n, pairs, 1e-15, 1e-16);
     __syncthreads();
     if (threadIdx.x == 0) {
         atomicAdd(&g_trunc_stats[0], 1ull);
@@ -775,8 +778,8 @@ __global__ void __launch_bounds__(256) k_trunc_core(const double* Gu, const doub
                 sv = fma(e, lu[q] / sig, sv);
             }
         }
-        Tu[c * k + idx[i]] = su;
-        Tv[c * k + idx[i]] = sv;
+        Tu[c * k + idx[i]] = su / sc[i];
+        Tv[c * k + idx[i]] = sv * sc[i];
     }
 }
 
@@ -944,9 +947,15 @@ __global__ void __launch_bounds__(256) k_bcore(const TEntry* E, const TChunk* C,
     double* Eu = A + n * n;
     double* X = Eu + n * n;
     double* lu = X + n * n;
+    __shared__ double sc[TRUNC_KMAX];   // column norms of U (the scaling D^{-1} of the Gram matrix)
+    for (int t = threadIdx.x; t < ke; t += blockDim.x) sc[t] = sqrt(Gu[idx[t] * nm + idx[t]]);
+    __syncthreads();
+    // scaled Gram matrix D Gu D (unit diagonal): its eigen-decomposition resolves
+    // nearly dependent columns relative to their own norms, whatever their scale
+    // (the scale moves into V: Gv <- D^{-1} Gv D^{-1})
     for (int t = threadIdx.x; t < n * n; t += blockDim.x) {
         const int i = t % n, j = t / n;
-        A[t] = (i < ke && j < ke) ? Gu[idx[j] * nm + idx[i]] : 0.0;
+        A[t] = (i < ke && j < ke) ? Gu[idx[j] * nm + idx[i]] / (sc[i] * sc[j]) : 0.0;
     }
     __syncthreads();
     // rotation threshold: converged to 1e-12 relative when truncating to tol >= 1e-6
@@ -954,7 +963,7 @@ __global__ void __launch_bounds__(256) k_bcore(const TEntry* E, const TChunk* C,
     // (and, then, off-diagonal entries below 1e-14 ||A||_F, the rounding noise
     // the rotations themselves leave behind, are not rotated: with a wide
     // eigenvalue range the relative test alone never stops)
-    const double jeps = (tol >= 1e-6) ? 1e-12 : 1e-15, jarel = (tol >= 1e-6) ? 1e-14 : 1e-17;
+    const double jeps = (tol >= 1e-6) ? 1e-12 : 1e-15, jarel = (tol >= 1e-6) ? 1e-14 : 1e-16;
     const int sw1 = cta_jacobi(A, Eu, n, nullptr, jeps, jarel);
     __shared__ double mu;
     if (threadIdx.x == 0) {
@@ -972,7 +981,7 @@ __global__ void __launch_bounds__(256) k_bcore(const TEntry* E, const TChunk* C,
         const int i = t % n, j = t / n;
         double s = 0.0;
         if (i < ke)
-            for (int q = 0; q < ke; ++q) s = fma(Gv[idx[q] * nm + idx[i]], Eu[j * n + q], s);
+            for (int q = 0; q < ke; ++q) s = fma(Gv[idx[q] * nm + idx[i]] * (sc[q] * sc[i]), Eu[j * n + q], s);
         X[t] = s;
     }
     __syncthreads();
@@ -1024,8 +1033,8 @@ __global__ void __launch_bounds__(256) k_bcore(const TEntry* E, const TChunk* C,
                 sv = fma(ev, lu[q] / sig, sv);
             }
         }
-        Tu[c * k + cm[idx[i]]] = su;
-        Tv[c * k + cm[idx[i]]] = sv;
+        Tu[c * k + cm[idx[i]]] = su / sc[i];
+        Tv[c * k + cm[idx[i]]] = sv * sc[i];
     }
 }
 
