@@ -2182,21 +2182,34 @@ __device__ void run_sweep(const SweepDev& S, int backward, double* x, long long 
                 const int col = q / Pj.nchunk, ch = q - col * Pj.nchunk;
                 const int i0 = ch * PROJ_CHUNK, i1 = min(Pj.n, i0 + PROJ_CHUNK);
                 const double* vc = Pj.V + (long long)col * Pj.ldv;
-                for (int c = 0; c < nrhs; ++c) {
-                    const double* xc = x + (long long)c * ldx + Pj.c0;
-                    // all loads of the lane first (independent), then a fixed-order sum
-                    double a[PROJ_CHUNK / 32];
+                // V chunk once per task; right-hand sides four at a time (all loads of
+                // a group in flight together), each summed in a fixed order
+                double v[PROJ_CHUNK / 32];
 #pragma unroll
-                    for (int u = 0; u < PROJ_CHUNK / 32; ++u) {
-                        const int i = i0 + lane + 32 * u;
-                        a[u] = (i < i1) ? vc[i] * ldcg(xc + i) : 0.0;
+                for (int u = 0; u < PROJ_CHUNK / 32; ++u) {
+                    const int i = i0 + lane + 32 * u;
+                    v[u] = (i < i1) ? vc[i] : 0.0;
+                }
+                for (int c0 = 0; c0 < nrhs; c0 += 4) {
+                    double a[4][PROJ_CHUNK / 32];
+#pragma unroll
+                    for (int cc = 0; cc < 4; ++cc) {
+                        const double* xc = x + (long long)min(c0 + cc, nrhs - 1) * ldx + Pj.c0;
+#pragma unroll
+                        for (int u = 0; u < PROJ_CHUNK / 32; ++u) {
+                            const int i = i0 + lane + 32 * u;
+                            a[cc][u] = (i < i1) ? v[u] * ldcg(xc + i) : 0.0;
+                        }
                     }
-                    double acc = 0.0;
 #pragma unroll
-                    for (int u = 0; u < PROJ_CHUNK / 32; ++u) acc += a[u];
+                    for (int cc = 0; cc < 4; ++cc) {
+                        double acc = 0.0;
 #pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-                    if (lane == 0) t[(long long)c * tstride + Pj.tslot + col * Pj.nchunk + ch] = acc;
+                        for (int u = 0; u < PROJ_CHUNK / 32; ++u) acc += a[cc][u];
+#pragma unroll
+                        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+                        if (lane == 0 && c0 + cc < nrhs) t[(long long)(c0 + cc) * tstride + Pj.tslot + col * Pj.nchunk + ch] = acc;
+                    }
                 }
             }
         }
