@@ -2067,6 +2067,98 @@ __device__ __forceinline__ double apply_row_sum(double v, int nrp, double* part)
     return s;
 }
 
+// Many right-hand sides (nrhs > APPLY_RC): the rows x RHS of a leaf step are cut
+// into 8 x 8 output tiles spread over the CTAs; the 512 threads of a CTA are 64
+// outputs x 8 phases of the inner index, reduced in shared memory in a fixed order.
+#define AT_R 8
+#define AT_C 8
+#define AT_NPH (APPLY_THREADS / (AT_R * AT_C))
+__device__ void apply_tile_rows(const SweepDev& S, const SLeaf& L, const double* x, long long ldx, int nrhs, double* z,
+                                const double* t, int tstride, double* part, double* tsm)
+{
+    const int ntr = (L.m + AT_R - 1) / AT_R, ntc = (nrhs + AT_C - 1) / AT_C;
+    const int o = threadIdx.x % (AT_R * AT_C), ph = threadIdx.x / (AT_R * AT_C);
+    const int rr = o % AT_R, cc = o / AT_R;
+    const int nlr = L.l_hi - L.l_lo;
+    bool lr_smem = nlr * 64 * AT_C <= APPLY_TSM;
+    for (int l = L.l_lo; l < L.l_hi && lr_smem; ++l) lr_smem = S.lrr[l].kc <= 64;
+    for (int tile = blockIdx.x; tile < ntr * ntc; tile += gridDim.x) {
+        const int r0 = (tile % ntr) * AT_R, c0 = (tile / ntr) * AT_C;
+        const int row = r0 + rr, col = c0 + cc;
+        const bool valid = row < L.m && col < nrhs;
+        if (lr_smem) {   // chunk sums of the projections t of this tile's right-hand sides
+            for (int e = threadIdx.x; e < nlr * 64 * AT_C; e += APPLY_THREADS) {
+                const int cx = e / (nlr * 64), ee = e % (nlr * 64);
+                const int l = L.l_lo + ee / 64, q = ee % 64;
+                const SLRRow R = S.lrr[l];
+                double tv = 0.0;
+                if (q < R.kc && c0 + cx < nrhs) {
+                    const double* tc = t + (long long)(c0 + cx) * tstride;
+                    for (int ch = 0; ch < R.nchunk; ++ch) tv += ldcg(tc + R.tslot + q * R.nchunk + ch);
+                }
+                tsm[e] = tv;
+            }
+            __syncthreads();
+        }
+        double acc = 0.0;
+        if (valid) {
+            const double* xc = x + (long long)col * ldx;
+            for (int d = L.d_lo; d < L.d_hi; ++d) {
+                const SDense D = S.dense[d];
+                const double* Dr = D.D + D.roff + row;
+#pragma unroll 8
+                for (int j = ph; j < D.nc; j += AT_NPH) acc = fma(Dr[(long long)j * D.ldd], ldcg(xc + D.c0 + j), acc);
+            }
+            for (int lq = ph; lq < nlr * L.kq; lq += AT_NPH) {
+                const int l = L.l_lo + lq / L.kq, q = lq % L.kq;
+                const SLRRow R = S.lrr[l];
+                if (q >= R.kc) continue;
+                double tv;
+                if (lr_smem) {
+                    tv = tsm[cc * (nlr * 64) + (l - L.l_lo) * 64 + q];
+                } else {
+                    tv = 0.0;
+                    const double* tc = t + (long long)col * tstride;
+                    for (int ch = 0; ch < R.nchunk; ++ch) tv += ldcg(tc + R.tslot + q * R.nchunk + ch);
+                }
+                acc = fma(R.U[(long long)q * R.ldu + R.roff + row], tv, acc);
+            }
+        }
+        part[threadIdx.x] = acc;
+        __syncthreads();
+        if (ph == 0 && valid) {
+            double s2 = 0.0;
+            for (int pp = 0; pp < AT_NPH; ++pp) s2 += part[pp * (AT_R * AT_C) + o];
+            z[(long long)col * L.m + row] = ldcg(x + (long long)col * ldx + L.r0 + row) - s2;
+        }
+        __syncthreads();
+    }
+}
+__device__ void apply_tile_inv(const SLeaf& L, double* x, long long ldx, int nrhs, const double* z, double* part)
+{
+    const int ntr = (L.m + AT_R - 1) / AT_R, ntc = (nrhs + AT_C - 1) / AT_C;
+    const int o = threadIdx.x % (AT_R * AT_C), ph = threadIdx.x / (AT_R * AT_C);
+    const int rr = o % AT_R, cc = o / AT_R;
+    for (int tile = blockIdx.x; tile < ntr * ntc; tile += gridDim.x) {
+        const int row = (tile % ntr) * AT_R + rr, col = (tile / ntr) * AT_C + cc;
+        const bool valid = row < L.m && col < nrhs;
+        double acc = 0.0;
+        if (valid) {
+            const double* zc = z + (long long)col * L.m;
+#pragma unroll 8
+            for (int j = ph; j < L.m; j += AT_NPH) acc = fma(L.inv[(long long)j * L.m + row], ldcg(zc + j), acc);
+        }
+        part[threadIdx.x] = acc;
+        __syncthreads();
+        if (ph == 0 && valid) {
+            double s2 = 0.0;
+            for (int pp = 0; pp < AT_NPH; ++pp) s2 += part[pp * (AT_R * AT_C) + o];
+            x[(long long)col * ldx + L.r0 + row] = s2;
+        }
+        __syncthreads();
+    }
+}
+
 __device__ void run_sweep(const SweepDev& S, int backward, double* x, long long ldx, int nrhs, double* z, double* t,
                           int tstride, cg::grid_group& cl)
 {
@@ -2087,10 +2179,12 @@ __device__ void run_sweep(const SweepDev& S, int backward, double* x, long long 
         // r_lo + t % nr and every nph-th column / low-rank term; partial sums are
         // reduced in shared memory in a fixed order (deterministic).
         __shared__ double tsm[APPLY_TSM];
+        const bool tiled = nrhs > APPLY_RC;
+        if (tiled) apply_tile_rows(S, L, x, ldx, nrhs, z, t, tstride, part, tsm);
         const int nlr = L.l_hi - L.l_lo;
         bool lr_smem = nlr * 64 <= APPLY_TSM / APPLY_RC;
         for (int l = L.l_lo; l < L.l_hi && lr_smem; ++l) lr_smem = S.lrr[l].kc <= 64;
-        for (int c0 = 0; c0 < nrhs; c0 += APPLY_RC) {
+        for (int c0 = 0; c0 < nrhs && !tiled; c0 += APPLY_RC) {
             const int nc = min(APPLY_RC, nrhs - c0);
             if (nr == 0) continue;
             if (lr_smem) {
@@ -2170,9 +2264,12 @@ __device__ void run_sweep(const SweepDev& S, int backward, double* x, long long 
         // ---- phase A2: projections enabled by the previous leaf (warp per (block, column, chunk))
         if (prev >= 0) {
             const SLeaf Pv = S.leaf[prev];
+            // many right-hand sides: one task per group of four (more warps in flight)
+            const int ng = tiled ? (nrhs + 3) / 4 : 1;
             int ntask = 0;
             for (int p = Pv.p_lo; p < Pv.p_hi; ++p) ntask += S.proj[p].kc * S.proj[p].nchunk;
-            for (int task = gw; task < ntask; task += nwarps) {
+            for (int task2 = gw; task2 < ntask * ng; task2 += nwarps) {
+                const int task = task2 / ng, grp = task2 % ng;
                 int q = task, p = Pv.p_lo;
                 while (q >= S.proj[p].kc * S.proj[p].nchunk) {
                     q -= S.proj[p].kc * S.proj[p].nchunk;
@@ -2190,7 +2287,7 @@ __device__ void run_sweep(const SweepDev& S, int backward, double* x, long long 
                     const int i = i0 + lane + 32 * u;
                     v[u] = (i < i1) ? vc[i] : 0.0;
                 }
-                for (int c0 = 0; c0 < nrhs; c0 += 4) {
+                for (int c0 = tiled ? 4 * grp : 0; c0 < (tiled ? min(nrhs, 4 * grp + 4) : nrhs); c0 += 4) {
                     double a[4][PROJ_CHUNK / 32];
 #pragma unroll
                     for (int cc = 0; cc < 4; ++cc) {
@@ -2215,7 +2312,8 @@ __device__ void run_sweep(const SweepDev& S, int backward, double* x, long long 
         }
         cl.sync();   // grid barrier (orders global memory across the grid)
         // ---- phase B: x_k = Inv_k z_k (this CTA's row slice), RHS in register chunks
-        if (nr > 0) {
+        if (tiled) apply_tile_inv(L, x, ldx, nrhs, z, part);
+        if (nr > 0 && !tiled) {
             int nrp = 1;
             while (nrp < nr) nrp <<= 1;
             const int nph = APPLY_THREADS / nrp;

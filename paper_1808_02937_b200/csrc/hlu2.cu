@@ -833,11 +833,22 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
                 kcap[b] = std::max(kcap[b], rmax);
             }
     }
+    // (FDE_DEBUG_PLAN: cumulative host time of the simulation phases)
+    double psec[8] = {0};
+    int plast = -1;
+    auto ptp = std::chrono::steady_clock::now();
+    auto ptick = [&](int ph) {
+        const auto now = std::chrono::steady_clock::now();
+        if (plast >= 0) psec[plast] += std::chrono::duration<double, std::milli>(now - ptp).count();
+        plast = ph;
+        ptp = now;
+    };
     std::vector<VStep> steps(nl);
     std::vector<int> stamp(nb, 0), tile_stamp((size_t)nl * nl, 0), tile_task((size_t)nl * nl, 0);
     int stamp_id = 0, tile_stamp_id = 0;
     for (int k = 0; k < nl; ++k) {
         VStep& st = steps[k];
+        ptick(0);
         const int mk = lm(k);
         const int dk = own(k, k);
         std::vector<int> Cb, Rc;   // column-panel blocks (rows > k), row-panel blocks (cols > k)
@@ -897,6 +908,7 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
                 pv.ldi = lfm(f);
             }
         }
+        ptick(1);
         // products: pair scratch offsets
         struct Pair { int b, c; int64_t w; int rw; bool bl, cl; };   // bl/cl: operand types at this step   // w: W (n_c x kc_b) or Z (m_b x kc_c) scratch offset
         std::vector<Pair> pairs;
@@ -949,6 +961,7 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
                 }
                 pairs.push_back(pr);
             }
+        ptick(2);
         // targets
         ++tile_stamp_id;   // dense target tile (i, j) -> g3 task (stamped flat table)
         struct Grp { int t, key, rank; int64_t slot; int round; };
@@ -975,6 +988,7 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
                 i = std::max(i + 1, inext);   // rows of the same owners repeat the same targets
             }
         }
+        ptick(3);
         // low-rank targets that must become dense: a dense x dense product lands
         // in them, or their width would exceed what a low-rank block can hold
         // (TRUNC_KMAX after truncation; min(m, n) / 2 in exact mode)
@@ -1014,6 +1028,7 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
                 }
             }
         }
+        ptick(4);
         for (size_t pi = 0; pi < pairs.size(); ++pi) {
             const Pair& pr = pairs[pi];
             const int b = pr.b, c = pr.c;
@@ -1068,6 +1083,7 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
                 }
             }
         }
+        ptick(5);
         // early truncation of the panel operands of step k+1 that are not operands of
         // this step: they run off the critical stream (with the overflow truncations,
         // before this step's new columns), so that step k+1 only has to recompress
@@ -1084,6 +1100,7 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
                 if (isLR(c) && !opnd.count(c)) add_trunc(c, true);
             }
         }
+        ptick(6);
         // slots and copies; a target whose new columns do not fit gets them in rounds,
         // truncated between rounds (formatted addition of the partial sums)
         std::vector<char> u_done(grps.size(), 0);
@@ -1139,6 +1156,7 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
     auto ms_since = [&](std::chrono::steady_clock::time_point t) {
         return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t).count();
     };
+    ptick(7);
     const double ms_sim = ms_since(t_plan0);
     const auto t_alloc0 = std::chrono::steady_clock::now();
     // ---- arena layout
@@ -1916,6 +1934,10 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
             }
         fprintf(stderr, "hlu2 plan: %d low-rank blocks converted to dense (%.1f MB)\n", nconv, wconv * 8e-6);
     }
+    if (getenv("FDE_DEBUG_PLAN"))
+        fprintf(stderr, "hlu2 plan phases (ms): operands/panels %.2f pairs %.2f targets %.2f conversions %.2f "
+                        "dense terms %.2f pretrunc %.2f slots/copies %.2f\n", psec[0], psec[1], psec[2], psec[3], psec[4],
+                psec[5], psec[6]);
     if (getenv("FDE_DEBUG_PLAN")) {
         double gt[6] = {0}, gmx[6] = {0}, tr = 0, trk = 0, pn = 0, cp = 0;
         for (auto& ln : P->steps) {

@@ -231,6 +231,26 @@ def test_hlu_exact_mode_equals_dense_solve_of_Atilde(fde, h, case, hlu_mode):
         o.free()
 
 
+@pytest.mark.parametrize("nrhs", [9, 19, 64])
+def test_hlu_apply_many_rhs_equals_dense_solve_of_Atilde(fde, h, nrhs):
+    """precond_apply with more right-hand sides than the register chunk (nrhs > 8:
+    8 x 8 output tiles of rows x RHS, ragged at 9 and 19) against the dense solve
+    with the oracle's A~ in exact mode (tol = 0), like the two-RHS test above."""
+    p, n_min = fi.config4(N=96, P=8), 4   # 24 leaves, several low-rank levels
+    op = fde.assemble_problem(h, p)
+    hm = fde.hmatrix_build(h, op, p.R, 1.0, n_min)
+    lu = fde.hlu_factor(h, hm, 0.0)
+    so = oracle_system(p)
+    At, _ = O.hmatrix_dense(p, so, R=p.R, lam=1.0, n_min=n_min)
+    r = np.random.default_rng(nrhs).standard_normal((nrhs, p.n))
+    z = fde.precond_apply(h, lu, torch.tensor(r, device="cuda")).cpu().numpy()
+    zo = np.linalg.solve(At, r.T).T
+    err = np.linalg.norm(z - zo) / np.linalg.norm(zo)
+    assert err <= TOL, err
+    for o in (lu, hm, op):
+        o.free()
+
+
 @pytest.mark.parametrize("case", HLU2_CASES, ids=lambda c: f"{c[0].name}-nmin{c[1]}")
 def test_hlu_preconditioned_gmres_matches_oracle(fde, h, case, hlu_mode):
     """tol = 1e-3: A~^{-1} is only approximate (parity unpinned
