@@ -665,12 +665,36 @@ struct VTerm {
     int k, ta, tb;
     double alpha;
 };
+// the terms of a task: two inline, the rest on the heap (most dense-update tasks
+// have one or two terms; a heap vector per task cost ~1.5 ms of host planning on c4)
+struct VTermList {
+    VTerm inl[2];
+    int n = 0;
+    std::vector<VTerm> more;
+    void push_back(const VTerm& t)
+    {
+        if (n < 2) inl[n] = t;
+        else more.push_back(t);
+        ++n;
+    }
+    size_t size() const { return (size_t)n; }
+    const VTerm& operator[](int i) const { return i < 2 ? inl[i] : more[i - 2]; }
+    struct It {
+        const VTermList* l;
+        int i;
+        const VTerm& operator*() const { return (*l)[i]; }
+        It& operator++() { ++i; return *this; }
+        bool operator!=(const It& o) const { return i != o.i; }
+    };
+    It begin() const { return {this, 0}; }
+    It end() const { return {this, n}; }
+};
 struct VTask {
     VRef C;
     int64_t ldc;
     int m, n;
     double beta;
-    std::vector<VTerm> terms;
+    VTermList terms;
 };
 struct VCopy {
     VRef src, dst;
@@ -696,6 +720,7 @@ struct VStep {
     int lu_blk = -1;
     int64_t lu_off = 0;
     std::vector<VPanel> panel;
+    std::vector<VPanel> npanel;          // the neighbour tiles (k+1, k), (k, k+1): on the LU stream
     std::vector<VTask> g0, g1, g2, g3;   // conversions to dense, cores, products, dense updates
     std::vector<VTask> g3r;              // dense updates of tiles off row / column k+1 (lookahead stream)
     std::vector<char> g3crit;            // per g3 task: 2 tile (k+1, k+1), 1 row / column k+1 or (k+2, k+2), 0 rest
@@ -715,6 +740,7 @@ struct H2Launch {      // ranges in the flat device arrays
     std::vector<H2Trunc> trmid;             // truncations between the rounds
     int lu = -1;
     int pan0 = 0, npan = 0;
+    int np0 = 0, nnp = 0;                   // neighbour-tile panels (LU stream)
     int pi0 = 0, npi = 0;                   // inverses of the factors of this step's tile (after its LU)
     int g_tile0[6] = {0, 0, 0, 0, 0, 0}, g_ntile[6] = {0, 0, 0, 0, 0, 0}, g_shape[6] = {0, 0, 0, 0, 0, 0};
     int cp0 = 0, ncp = 0;
@@ -752,6 +778,7 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
     const HStruct& S = L->S;
     const bool trunc = L->tol > 0.0;
     static const bool pan_inv = !getenv("FDE_H2_PANEL_SUBST");
+    static const bool split_np = !getenv("FDE_H2_NOSPLIT");
     static const bool pretrunc = !getenv("FDE_H2_NOPRETRUNC");
     const int R = hm->R, rmax = L->rmax;
     if (trunc && (R > TRUNC_KMAX || rmax > TRUNC_KMAX)) return false;
@@ -883,13 +910,22 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         st.lu_off = toff(dk, k, k);
         const VRef Tk{0, dk, toff(dk, k, k)};
         const int64_t ldk = S.bl[dk].m;
+        // the panels of the neighbour tiles (k+1, k) and (k, k+1) go to their own
+        // launch on the LU stream when both are dense: the update of tile (k+1, k+1)
+        // and LU(k+1) then wait only for them, not for the whole panel launch
+        const bool nsplit = split_np && k + 1 < nl && !isLR(own(k + 1, k)) && !isLR(own(k, k + 1));
         for (int b : Cb) {
             const HBlock& B = S.bl[b];
             if (isLR(b)) {
                 st.panel.push_back({Tk, ldk, {2, b, lr0[k] - col0(b)}, B.n, mk, kc[b], 1});
             } else {   // rows of tiles > k of the column of tile k
-                const int i0 = std::max(t0[b], k + 1);
-                st.panel.push_back({Tk, ldk, {0, b, toff(b, i0, k)}, B.m, mk, (int)(lr0[t1[b] + 1] - lr0[i0]), 2});
+                int i0 = std::max(t0[b], k + 1);
+                if (nsplit && i0 == k + 1) {
+                    st.npanel.push_back({Tk, ldk, {0, b, toff(b, k + 1, k)}, B.m, mk, lm(k + 1), 2});
+                    ++i0;
+                }
+                if (i0 <= t1[b])
+                    st.panel.push_back({Tk, ldk, {0, b, toff(b, i0, k)}, B.m, mk, (int)(lr0[t1[b] + 1] - lr0[i0]), 2});
             }
         }
         for (int c : Rc) {
@@ -897,16 +933,22 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
             if (isLR(c)) {
                 st.panel.push_back({Tk, ldk, {1, c, lr0[k] - row0(c)}, C.m, mk, kc[c], 0});
             } else {   // columns of tiles > k of the row of tile k
-                const int j0 = std::max(s0[c], k + 1);
-                st.panel.push_back({Tk, ldk, {0, c, toff(c, k, j0)}, C.m, mk, (int)(lr0[s1[c] + 1] - lr0[j0]), 0});
+                int j0 = std::max(s0[c], k + 1);
+                if (nsplit && j0 == k + 1) {
+                    st.npanel.push_back({Tk, ldk, {0, c, toff(c, k, k + 1)}, C.m, mk, lm(k + 1), 0});
+                    ++j0;
+                }
+                if (j0 <= s1[c])
+                    st.panel.push_back({Tk, ldk, {0, c, toff(c, k, j0)}, C.m, mk, (int)(lr0[s1[c] + 1] - lr0[j0]), 0});
             }
         }
         if (pan_inv) {   // panels as products with the tile inverses (computed after LU(k))
             const int f = leaf_of[k];
-            for (auto& pv : st.panel) {
-                pv.Ti = {pv.mode == 0 ? 4 : 5, f, ioff(f, k, k)};
-                pv.ldi = lfm(f);
-            }
+            for (auto* pl : {&st.panel, &st.npanel})
+                for (auto& pv : *pl) {
+                    pv.Ti = {pv.mode == 0 ? 4 : 5, f, ioff(f, k, k)};
+                    pv.ldi = lfm(f);
+                }
         }
         ptick(1);
         // products: pair scratch offsets
@@ -1032,6 +1074,7 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         for (size_t pi = 0; pi < pairs.size(); ++pi) {
             const Pair& pr = pairs[pi];
             const int b = pr.b, c = pr.c;
+            const int64_t su_b = pr.bl ? snapU[b] : 0, sv_c = (!pr.bl && pr.cl) ? snapV[c] : 0;   // (hoisted lookups)
             for (int t : ptg[pi]) {
                 const HBlock& T = S.bl[t];
                 if (!isLR(t)) {
@@ -1043,8 +1086,7 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
                                 ti = (int)st.g3.size();
                                 tile_stamp[key] = tile_stamp_id;
                                 tile_task[key] = ti;
-                                VTask tk{{0, t, (lr0[j] - col0(t)) * T.m + (lr0[i] - row0(t))}, T.m, lm(i), lm(j), 1.0, {}};
-                                st.g3.push_back(tk);
+                                st.g3.push_back(VTask{{0, t, (lr0[j] - col0(t)) * T.m + (lr0[i] - row0(t))}, T.m, lm(i), lm(j), 1.0, {}});
                                 // 2: the next diagonal tile (input of LU(k+1), right after the panels);
                                 // 1: row / column k+1 and the diagonal tile after it (critical stream);
                                 // 0: the rest (lookahead stream)
@@ -1059,10 +1101,10 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
                                 term = {{0, b, (lr0[k] - col0(b)) * B.m + (lr0[i] - row0(b))},
                                         {0, c, (lr0[j] - col0(c)) * C.m + (lr0[k] - row0(c))}, B.m, C.m, mk, 0, 0, -1.0};
                             } else if (pr.bl) {   // U_b[i rows] W[j rows]^T
-                                term = {{3, k & 1, snapU[b] + (lr0[i] - row0(b))}, {3, k & 1, pr.w + (lr0[j] - col0(c))}, B.m, C.n,
+                                term = {{3, k & 1, su_b + (lr0[i] - row0(b))}, {3, k & 1, pr.w + (lr0[j] - col0(c))}, B.m, C.n,
                                         kc[b], 0, 1, -1.0};
                             } else {               // Z[i rows] V_c[j rows]^T
-                                term = {{3, k & 1, pr.w + (lr0[i] - row0(b))}, {3, k & 1, snapV[c] + (lr0[j] - col0(c))}, B.m, C.n,
+                                term = {{3, k & 1, pr.w + (lr0[i] - row0(b))}, {3, k & 1, sv_c + (lr0[j] - col0(c))}, B.m, C.n,
                                         kc[c], 0, 1, -1.0};
                             }
                             st.g3[ti].terms.push_back(term);
@@ -1457,6 +1499,7 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         cnt_trunc(st.trunc);
         cnt_trunc(st.trunc_ov);
         cnt_pan(st.panel);
+        cnt_pan(st.npanel);
         cnt_tasks(st.g0, gemm_shape[3]);
         cnt_tasks(st.g1, gemm_shape[0]);
         cnt_tasks(st.g2, gemm_shape[1]);
@@ -1511,6 +1554,7 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
     cudaEvent_t evLU = L->h->ev_aux[7], evDg = L->h->ev_aux[8];
     cudaEvent_t evCp = L->h->ev_aux[10], evOv = L->h->ev_aux[11];
     cudaEvent_t evPan = L->h->ev_aux[12], evSnap = L->h->ev_aux[13];
+    cudaEvent_t evNP = L->h->ev_aux[14], evCrit = L->h->ev_aux[15];
     cudaStream_t se = aux_stream6(L->h);   // overflow truncations
     // debug: fold auxiliary streams back onto the critical one (race bisection)
     if (const char* f = getenv("FDE_H2_FOLD")) {
@@ -1714,6 +1758,12 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         put_trunc(st.trunc, ln.tr);
         put_trunc(st.trunc_ov, ln.tr_ov);
         put_panel(st.panel, ln);
+        {
+            H2Launch tmp;
+            put_panel(st.npanel, tmp);
+            ln.np0 = tmp.pan0;
+            ln.nnp = tmp.npan;
+        }
         put_gemm(st.g0, ln, 3, gemm_shape[3]);
         put_gemm(st.g1, ln, 0, gemm_shape[0]);
         put_gemm(st.g2, ln, 1, gemm_shape[1]);
@@ -1779,8 +1829,6 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         }
         FDE_CUDA(cudaStreamWaitEvent(sa, evLU, 0));
         FDE_CUDA(cudaStreamWaitEvent(sa, evOp, 0));
-        run_panel(ln);
-        mark(k, T_PAN, sa);
         auto diag_lu = [&](cudaStream_t st) {   // tile (k+1, k+1), then LU(k+1) on sl
             run_gemm(ln, 5, st);
             mark(k, T_DIAG, st);
@@ -1797,7 +1845,21 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
                 mark(k, T_LU, sl);
             }
         };
-        if (!ln.diag_scr) {   // dense x dense terms only: beside the products
+        // (sa has captured evLU = LU(k) above; LU(k+1) may be recorded from here on)
+        if (ln.nnp) {   // neighbour-tile panels, tile (k+1, k+1), LU(k+1): all on the LU stream
+            FDE_CUDA(cudaStreamWaitEvent(sl, evCrit, 0));   // row / column k updated by step k-1
+            k_h2_panel<<<ln.nnp, 256, pan_inv ? pan_smem_inv : pan_smem, sl>>>(P->pan.p + ln.np0);
+            FDE_CHECK_LAUNCH();
+            ++nlaunch;
+            dbg("neighbour panels");
+            FDE_CUDA(cudaEventRecord(evNP, sl));
+            diag_lu(sl);
+        }
+        run_panel(ln);
+        mark(k, T_PAN, sa);
+        if (ln.nnp) {
+            FDE_CUDA(cudaStreamWaitEvent(sa, evNP, 0));   // the products read the neighbour tiles too
+        } else if (!ln.diag_scr) {   // dense x dense terms only: beside the products
             FDE_CUDA(cudaEventRecord(evPan, sa));
             FDE_CUDA(cudaStreamWaitEvent(sl, evPan, 0));
             diag_lu(sl);
@@ -1823,6 +1885,7 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         if (ln.diag_scr) diag_lu(sa);
         FDE_CUDA(cudaStreamWaitEvent(sa, evC, 0));   // remaining updates of step k-1
         run_gemm(ln, 2, sa);                         // row / column k+1
+        FDE_CUDA(cudaEventRecord(evCrit, sa));
         mark(k, T_CRIT, sa);
         // sb: new low-rank columns of step k (after the overflow truncations)
         FDE_CUDA(cudaStreamWaitEvent(sb, evP, 0));
