@@ -549,6 +549,89 @@ __device__ __forceinline__ void jpair(int k, int round, int n, int& p, int& q)
     q = max(a, b);
 }
 
+// The same parallel-cyclic Jacobi by one warp (n <= 32): warp-synchronous, no
+// CTA barriers (the rounds of a small matrix are latency-bound).  Called by all
+// threads of the CTA; warp 0 works, the CTA synchronises once at the end.
+__device__ int warp_jacobi(double* A, double* V, int n, double eps, double arel)
+{
+    __shared__ int wsweeps;
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        for (int t = lane; t < n * n; t += 32) V[t] = ((t % n) == (t / n)) ? 1.0 : 0.0;
+        double f = 0.0;
+        for (int t = lane; t < n * n; t += 32) f = fma(A[t], A[t], f);
+        for (int o = 16; o; o >>= 1) f += __shfl_xor_sync(0xffffffffu, f, o);
+        const double athr = arel * sqrt(f) + 1e-300, eps2 = eps * eps;
+        const int half = n / 2;
+        __syncwarp();
+        int sweep = 0;
+        for (; sweep < 30; ++sweep) {
+            bool rot = false;
+            for (int round = 0; round < n - 1; ++round) {
+                double c = 1.0, sn = 0.0;
+                if (lane < half) {
+                    int p, q;
+                    jpair(lane, round, n, p, q);
+                    const double app = A[p * n + p], aqq = A[q * n + q], apq = A[q * n + p];
+                    if (fabs(apq) > athr && apq * apq > eps2 * fabs(app * aqq)) {
+                        rot = true;
+                        const double d = aqq - app, e = 2.0 * apq;
+                        const double x = fma(d, d, e * e);
+                        double t;
+                        if (x > 1e-290) {
+                            const double h = x * rsqrt_nr(x);
+                            t = (d >= 0.0 ? e : -e) * rcp_nr(fabs(d) + h);
+                        } else {
+                            const double tau = d / e;
+                            t = (tau >= 0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+                        }
+                        c = rsqrt_nr(fma(t, t, 1.0));
+                        sn = t * c;
+                    }
+                }
+                __syncwarp();
+                // A <- J^T A J: blocks (k1, k2), k1 = b % half, k2 = b / half
+                for (int b0 = 0; b0 < half * half; b0 += 32) {
+                    const int b = b0 + lane;
+                    const int k1 = (b < half * half) ? b % half : 0, k2 = (b < half * half) ? b / half : 0;
+                    const double c1 = __shfl_sync(0xffffffffu, c, k1), s1 = __shfl_sync(0xffffffffu, sn, k1);
+                    const double c2 = __shfl_sync(0xffffffffu, c, k2), s2 = __shfl_sync(0xffffffffu, sn, k2);
+                    if (b < half * half) {
+                        int p1, q1, p2, q2;
+                        jpair(k1, round, n, p1, q1);
+                        jpair(k2, round, n, p2, q2);
+                        const double app = A[p2 * n + p1], apq = A[q2 * n + p1], aqp = A[p2 * n + q1], aqq = A[q2 * n + q1];
+                        const double xpp = c2 * app - s2 * apq, xpq = s2 * app + c2 * apq;
+                        const double xqp = c2 * aqp - s2 * aqq, xqq = s2 * aqp + c2 * aqq;
+                        A[p2 * n + p1] = c1 * xpp - s1 * xqp;
+                        A[p2 * n + q1] = s1 * xpp + c1 * xqp;
+                        A[q2 * n + p1] = c1 * xpq - s1 * xqq;
+                        A[q2 * n + q1] = s1 * xpq + c1 * xqq;
+                    }
+                }
+                // V <- V J: items (pair k, row i)
+                for (int b0 = 0; b0 < half * n; b0 += 32) {
+                    const int b = b0 + lane;
+                    const int kk = (b < half * n) ? b / n : 0, i = (b < half * n) ? b % n : 0;
+                    const double ck = __shfl_sync(0xffffffffu, c, kk), sk = __shfl_sync(0xffffffffu, sn, kk);
+                    if (b < half * n) {
+                        int p, q;
+                        jpair(kk, round, n, p, q);
+                        const double vip = V[p * n + i], viq = V[q * n + i];
+                        V[p * n + i] = ck * vip - sk * viq;
+                        V[q * n + i] = sk * vip + ck * viq;
+                    }
+                }
+                __syncwarp();
+            }
+            if (!__any_sync(0xffffffffu, rot)) { ++sweep; break; }
+        }
+        if (lane == 0) wsweeps = sweep;
+    }
+    __syncthreads();
+    return wsweeps;
+}
+
 __device__ int cta_jacobi(double* A, double* V, int n, int* /*unused*/, double eps = 1e-15, double arel = 1e-17)
 {
     // parallel cyclic Jacobi (n even, n <= 256, caller pads); A[c * n + r] symmetric.
@@ -964,56 +1047,111 @@ __global__ void __launch_bounds__(256) k_bcore(const TEntry* E, const TChunk* C,
     // the rotations themselves leave behind, are not rotated: with a wide
     // eigenvalue range the relative test alone never stops)
     const double jeps = (tol >= 1e-6) ? 1e-12 : 1e-15, jarel = (tol >= 1e-6) ? 1e-14 : 1e-16;
-    const int sw1 = cta_jacobi(A, Eu, n, nullptr, jeps, jarel);
-    __shared__ double mu;
-    if (threadIdx.x == 0) {
-        double a = 0.0;
-        for (int i = 0; i < n; ++i) a = fmax(a, A[i * n + i]);
-        mu = a;
-    }
+    // Factor of the scaled Gram by pivoted Cholesky, D Gu D = P R^T R P^T (R: ru x ke,
+    // upper trapezoidal in pivoted order; pivots below 1e-14 of the unit diagonal --
+    // nearly dependent columns -- end it), in place in A: ke sequential steps
+    // instead of a Jacobi eigen-solve.  Then U' V'^T = Q (R P^T V'^T) with
+    // M = R P^T Gv' P R^T = X S^2 X^T (Jacobi), and, in pivoted coordinates,
+    //   T'u = [R11^{-1} X_r S_r ; 0],   T'v = R^T X_r S_r^{-1}.
+    __shared__ int piv[TRUNC_KMAX];
+    __shared__ int pj_sh, ru_sh;
+    __shared__ double dmax_sh;
+    for (int t = threadIdx.x; t < ke; t += blockDim.x) piv[t] = t;
+    if (threadIdx.x == 0) ru_sh = ke;
     __syncthreads();
-    for (int t = threadIdx.x; t < n; t += blockDim.x) {
-        const double l = A[t * n + t];
-        lu[t] = (l > 1e-14 * mu) ? sqrt(l) : 0.0;
+    for (int j = 0; j < ke; ++j) {
+        if (threadIdx.x < 32) {   // pivot: largest remaining diagonal (lowest index on ties)
+            double v = -1.0;
+            int pi = j;
+            for (int a = j + (int)threadIdx.x; a < ke; a += 32)
+                if (A[a * n + a] > v) { v = A[a * n + a]; pi = a; }
+            for (int o = 16; o; o >>= 1) {
+                const double v2 = __shfl_xor_sync(0xffffffffu, v, o);
+                const int p2 = __shfl_xor_sync(0xffffffffu, pi, o);
+                if (v2 > v || (v2 == v && p2 < pi)) { v = v2; pi = p2; }
+            }
+            if (threadIdx.x == 0) {
+                pj_sh = pi;
+                dmax_sh = v;
+                if (!(v > 1e-14)) ru_sh = j;
+                else if (pi != j) { const int tmp = piv[j]; piv[j] = piv[pi]; piv[pi] = tmp; }
+            }
+        }
+        __syncthreads();
+        if (ru_sh == j) break;
+        const int pj = pj_sh;
+        if (pj != j) {   // symmetric swap of rows / columns j and pj
+            for (int t = threadIdx.x; t < ke; t += blockDim.x) {
+                const double a = A[t * n + j];
+                A[t * n + j] = A[t * n + pj];
+                A[t * n + pj] = a;
+            }
+            __syncthreads();
+            for (int t = threadIdx.x; t < ke; t += blockDim.x) {
+                const double a = A[j * n + t];
+                A[j * n + t] = A[pj * n + t];
+                A[pj * n + t] = a;
+            }
+            __syncthreads();
+        }
+        const double rjj = sqrt(dmax_sh), irj = 1.0 / rjj;
+        for (int c = j + 1 + (int)threadIdx.x; c < ke; c += blockDim.x) A[c * n + j] *= irj;   // row j of R
+        __syncthreads();
+        if (threadIdx.x == 0) A[j * n + j] = rjj;
+        for (int t = threadIdx.x; t < (ke - j - 1) * (ke - j - 1); t += blockDim.x) {
+            const int a = j + 1 + t % (ke - j - 1), c = j + 1 + t / (ke - j - 1);
+            A[c * n + a] -= A[a * n + j] * A[c * n + j];
+        }
+        __syncthreads();
     }
-    __syncthreads();
-    for (int t = threadIdx.x; t < n * n; t += blockDim.x) {
-        const int i = t % n, j = t / n;
+    const int ru = ru_sh;
+    const int n2 = (ru + 1) & ~1;
+    // X_temp (ke x ru, in Eu): Gvp R^T, Gvp = pivoted scaled Gv;  M (ru x ru, in X): R X_temp
+    for (int t = threadIdx.x; t < ke * ru; t += blockDim.x) {
+        const int a = t % ke, c = t / ke;
+        const int ia = piv[a];
         double s = 0.0;
-        if (i < ke)
-            for (int q = 0; q < ke; ++q) s = fma(Gv[idx[q] * nm + idx[i]] * (sc[q] * sc[i]), Eu[j * n + q], s);
-        X[t] = s;
+        for (int b = c; b < ke; ++b) {   // R[c][b] = 0 for b < c
+            const int ib = piv[b];
+            s = fma(Gv[idx[ib] * nm + idx[ia]] * (sc[ia] * sc[ib]), A[b * n + c], s);
+        }
+        Eu[c * ke + a] = s;
     }
     __syncthreads();
-    for (int t = threadIdx.x; t < n * n; t += blockDim.x) {
-        const int i = t % n, j = t / n;
+    for (int t = threadIdx.x; t < n2 * n2; t += blockDim.x) {
+        const int r = t % n2, c = t / n2;
         double s = 0.0;
-        for (int q = 0; q < n; ++q) s = fma(Eu[i * n + q], X[j * n + q], s);
-        A[t] = lu[i] * lu[j] * s;
+        if (r < ru && c < ru)
+            for (int a = r; a < ke; ++a) s = fma(A[a * n + r], Eu[c * ke + a], s);
+        X[c * n2 + r] = s;
     }
     __syncthreads();
-    const int sw2 = cta_jacobi(A, X, n, nullptr, jeps, jarel);
+    const int sw2 = (n2 <= 32) ? warp_jacobi(X, Eu, n2, jeps, jarel) : cta_jacobi(X, Eu, n2, nullptr, jeps, jarel);
     __syncthreads();
     if (threadIdx.x == 0) {   // (debug statistics: calls, sum ke, sum sweeps, max sweeps of one solve)
         atomicAdd(&g_trunc_stats[0], 1ull);
         atomicAdd(&g_trunc_stats[1], (unsigned long long)ke);
-        atomicAdd(&g_trunc_stats[2], (unsigned long long)(sw1 + sw2));
-        atomicMax(&g_trunc_stats[3], (unsigned long long)max(sw1, sw2));
+        atomicAdd(&g_trunc_stats[2], (unsigned long long)sw2);
+        atomicMax(&g_trunc_stats[3], (unsigned long long)sw2);
     }
     __shared__ int ord[TRUNC_KMAX];
     __shared__ int r_sh;
-    if (threadIdx.x == 0) {
-        for (int i = 0; i < n; ++i) ord[i] = i;
-        for (int i = 0; i < n; ++i) {
-            int b = i;
-            for (int j = i + 1; j < n; ++j)
-                if (A[ord[j] * n + ord[j]] > A[ord[b] * n + ord[b]]) b = j;
-            const int tmp = ord[i]; ord[i] = ord[b]; ord[b] = tmp;
+    // eigenvalues in decreasing order (ties by index): thread i computes the rank of i
+    for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+        const double li = X[i * n2 + i];
+        int rk = 0;
+        for (int j = 0; j < n2; ++j) {
+            const double lj = X[j * n2 + j];
+            rk += (lj > li) || (lj == li && j < i);
         }
-        const double s1 = sqrt(fmax(A[ord[0] * n + ord[0]], 0.0));
+        ord[rk] = i;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const double s1 = sqrt(fmax(X[ord[0] * n2 + ord[0]], 0.0));
         int r = 0;
-        for (int i = 0; i < n; ++i) {
-            const double si = sqrt(fmax(A[ord[i] * n + ord[i]], 0.0));
+        for (int i = 0; i < n2; ++i) {
+            const double si = sqrt(fmax(X[ord[i] * n2 + ord[i]], 0.0));
             if (s1 > 0.0 && si > tol * s1 && si > 1e-15 * s1) ++r;
         }
         if (r > kc) { r = kc; *flag = 1; }
@@ -1021,20 +1159,29 @@ __global__ void __launch_bounds__(256) k_bcore(const TEntry* E, const TChunk* C,
     }
     __syncthreads();
     const int r = r_sh;
+    // T'v = R^T X_r S_r^{-1} (rows a = 0..ke-1, pivoted) and T'u = R11^{-1} X_r S_r
+    // (back substitution, one thread per kept column); unpivot and unscale on store
     for (int t = threadIdx.x; t < ke * r; t += blockDim.x) {
-        const int i = t % ke, c = t / ke;
+        const int a = t % ke, c = t / ke, col = ord[c];
+        const double sig = sqrt(fmax(X[col * n2 + col], 0.0));
+        double sv = 0.0;
+        for (int b = 0; b <= min(a, ru - 1); ++b) sv = fma(A[a * n + b], Eu[col * n2 + b], sv);
+        const int ia = piv[a];
+        Tv[c * k + cm[idx[ia]]] = sv / sig * sc[ia];
+    }
+    for (int c = threadIdx.x; c < r; c += blockDim.x) {
         const int col = ord[c];
-        const double sig = sqrt(fmax(A[col * n + col], 0.0));
-        double su = 0.0, sv = 0.0;
-        for (int q = 0; q < n; ++q) {
-            const double ev = Eu[q * n + i] * X[col * n + q];
-            if (lu[q] > 0.0) {
-                su = fma(ev, sig / lu[q], su);
-                sv = fma(ev, lu[q] / sig, sv);
-            }
+        const double sig = sqrt(fmax(X[col * n2 + col], 0.0));
+        double y[TRUNC_KMAX];
+        for (int a = ru - 1; a >= 0; --a) {
+            double b = Eu[col * n2 + a] * sig;
+            for (int q = a + 1; q < ru; ++q) b = fma(-A[q * n + a], y[q], b);
+            y[a] = b / A[a * n + a];
         }
-        Tu[c * k + cm[idx[i]]] = su / sc[i];
-        Tv[c * k + cm[idx[i]]] = sv * sc[i];
+        for (int a = 0; a < ke; ++a) {
+            const int ia = piv[a];
+            Tu[c * k + cm[idx[ia]]] = (a < ru ? y[a] : 0.0) / sc[ia];
+        }
     }
 }
 
