@@ -24,6 +24,12 @@
 
 __constant__ double c_glx[FDE_GL_TOTAL];
 __constant__ double c_glw[FDE_GL_TOTAL];
+// Legendre recurrence coefficients L_{k+1} = a_k x L_k - b_k L_{k-1}, a_k = (2k+1)/(k+1),
+// b_k = k/(k+1): multiplications instead of a division per step (the division was
+// the largest single cost of the pair kernel)
+#define FDE_LEG_K 64
+__constant__ double c_leg_a[FDE_LEG_K];
+__constant__ double c_leg_b[FDE_LEG_K];
 
 static int g_gl_uploaded_dev = -1;
 
@@ -41,6 +47,13 @@ static void upload_gl_tables(int dev)
     }
     FDE_CUDA(cudaMemcpyToSymbol(c_glx, X.data(), sizeof(double) * FDE_GL_TOTAL));
     FDE_CUDA(cudaMemcpyToSymbol(c_glw, W.data(), sizeof(double) * FDE_GL_TOTAL));
+    double la[FDE_LEG_K], lb[FDE_LEG_K];
+    for (int k = 0; k < FDE_LEG_K; ++k) {
+        la[k] = (2.0 * k + 1.0) / (k + 1.0);
+        lb[k] = (double)k / (k + 1.0);
+    }
+    FDE_CUDA(cudaMemcpyToSymbol(c_leg_a, la, sizeof(la)));
+    FDE_CUDA(cudaMemcpyToSymbol(c_leg_b, lb, sizeof(lb)));
     g_gl_uploaded_dev = dev;
 }
 
@@ -88,7 +101,7 @@ __device__ inline void leg_all(int P, double x, double* out)
     out[0] = 1.0;
     if (P > 1) out[1] = x;
     for (int k = 1; k + 1 < P; ++k) {
-        double p2 = ((2 * k + 1) * x * p1 - k * p0) / (k + 1);
+        double p2 = fma(c_leg_a[k] * x, p1, -c_leg_b[k] * p0);
         out[k + 1] = p2;
         p0 = p1;
         p1 = p2;
