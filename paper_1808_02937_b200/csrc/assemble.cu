@@ -113,9 +113,12 @@ __device__ inline void leg_all(int P, double x, double* out)
 // sqrt(eta^2-1); error ~ rho^{-(2Q - (P-1))} -> ~1e-17.
 __device__ inline int q_select(double eta, int P, int qm)
 {
-    double rho = eta + sqrt(fmax(eta * eta - 1.0, 0.0));
-    double lr = log10(fmax(0.8 * rho, 1.05));
-    int q = (int)ceil((17.0 / lr + (double)P) * 0.5);
+    // (single precision suffices: the result is a point count; a count that differs
+    // by one near a rounding boundary only moves the quadrature error around 1e-17)
+    const float etaf = (float)fmin(eta, 1e30);
+    const float rho = etaf + sqrtf(fmaxf(etaf * etaf - 1.0f, 0.0f));
+    const float lr = __log10f(fmaxf(0.8f * rho, 1.05f));
+    int q = (int)ceilf((17.0f / lr + (float)P) * 0.5f);
     int qmin = P / 2 + 2;
     if (q < qmin) q = qmin;
     if (q > qm) q = qm;
