@@ -371,8 +371,10 @@ struct DofTerms {
     int ml[2];     // local function index for the mass matrix (0 left hat, P right hat)
 };
 
-__device__ inline DofTerms dof_terms(long long r, long long n, int N, int P)
+template <int PT = 0>
+__device__ inline DofTerms dof_terms(long long r, long long n, int N, int Prt)
 {
+    const int P = PT ? PT : Prt;   // (compile-time P: the division below becomes a multiply)
     DofTerms t;
     if (r == n) {
         t.cnt = 1; t.e[0] = 0; t.m[0] = 0; t.c[0] = -0.5; t.ml[0] = 0;
@@ -382,7 +384,8 @@ __device__ inline DofTerms dof_terms(long long r, long long n, int N, int P)
         t.cnt = 1; t.e[0] = N - 1; t.m[0] = 0; t.c[0] = 0.5; t.ml[0] = P;
         return t;
     }
-    int e = (int)(r / P), q = (int)(r - (long long)e * P);
+    const int ri = (int)r;   // r < 2^31 (n = N P - 1)
+    int e = ri / P, q = ri - e * P;
     if (q < P - 1) {
         int p = q + 1;
         t.cnt = 1; t.e[0] = e; t.m[0] = p; t.c[0] = -(2.0 * p + 1.0); t.ml[0] = p;
@@ -403,8 +406,8 @@ struct KBand {
     int b0, b1, N, P2;
     __device__ const double* get(int i, int j) const
     {
-        if (i >= b0 && i <= b1)
-            return row + ((long long)i * (i + 1) / 2 - (long long)b0 * (b0 + 1) / 2 + j) * P2;
+        if (i >= b0 && i <= b1)   // (i < 2^16: the triangle index fits 32 bits)
+            return row + (long long)((unsigned)i * (unsigned)(i + 1) / 2u - (unsigned)b0 * (unsigned)(b0 + 1) / 2u + (unsigned)j) * P2;
         return col + ((long long)(i - b1 - 1) * (b1 - b0 + 1) + (j - b0)) * P2;
     }
 };
@@ -435,11 +438,12 @@ struct KRect {
     }
 };
 
-template <class KL>
-__device__ inline double a_entry(const KL& K, long long r, long long c, long long n, int N, int P, double theta,
+template <class KL, int PT = 0>
+__device__ inline double a_entry(const KL& K, long long r, long long c, long long n, int N, int Prt, double theta,
                                  double rho, const double* nodes, const double* mref)
 {
-    DofTerms tr = dof_terms(r, n, N, P), tc = dof_terms(c, n, N, P);
+    const int P = PT ? PT : Prt;
+    DofTerms tr = dof_terms<PT>(r, n, N, P), tc = dof_terms<PT>(c, n, N, P);
     const int P2 = P * P;
     (void)P2;
     double sl = 0.0, slt = 0.0, mass = 0.0;
@@ -458,14 +462,16 @@ __device__ inline double a_entry(const KL& K, long long r, long long c, long lon
     return rho * mass + theta * sl + (1.0 - theta) * slt;
 }
 
-__global__ void k_expand_dense(KBand K, long long r0, long long r1, long long n, long long lda, int N, int P,
-                               double theta, double rho, const double* nodes, const double* mref, double* A)
+template <int PT>
+__global__ void __launch_bounds__(256) k_expand_dense(KBand K, long long r0, long long r1, long long n, long long lda,
+                                                      int N, int P, double theta, double rho, const double* nodes,
+                                                      const double* mref, double* A)
 {
     const long long r = r0 + blockIdx.y;
     const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= r1 || c >= lda) return;
     double v = 0.0;
-    if (c < n) v = a_entry(K, r, c, n, N, P, theta, rho, nodes, mref);
+    if (c < n) v = a_entry<KBand, PT>(K, r, c, n, N, P, theta, rho, nodes, mref);
     A[(r - r0) * lda + c] = v;
 }
 
@@ -711,8 +717,16 @@ void asm_expand_dense(fde_ctx* h, fde_op* op, const double* Krow, const double* 
     const long long rows = op->r1 - op->r0;
     if (rows <= 0) return;
     dim3 grid((unsigned)ceil_div(op->lda, 256), (unsigned)rows);
-    k_expand_dense<<<grid, 256, 0, h->stream>>>(K, op->r0, op->r1, op->n, op->lda, op->N, op->P, op->prob.theta,
-                                                 op->prob.rho, op->tab.nodes.p, op->tab.mref.p, op->A.p);
+#define FDE_EXPAND(PT_)                                                                                           \
+    k_expand_dense<PT_><<<grid, 256, 0, h->stream>>>(K, op->r0, op->r1, op->n, op->lda, op->N, op->P, op->prob.theta, \
+                                                     op->prob.rho, op->tab.nodes.p, op->tab.mref.p, op->A.p)
+    switch (op->P) {   // the common degrees with a compile-time P
+        case 4: FDE_EXPAND(4); break;
+        case 8: FDE_EXPAND(8); break;
+        case 16: FDE_EXPAND(16); break;
+        default: FDE_EXPAND(0);
+    }
+#undef FDE_EXPAND
     FDE_CHECK_LAUNCH();
 }
 
