@@ -779,6 +779,14 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
     const bool trunc = L->tol > 0.0;
     static const bool pan_inv = !getenv("FDE_H2_PANEL_SUBST");
     static const bool split_np = !getenv("FDE_H2_NOSPLIT");
+    // deferred dense updates: a dense tile (i, j) gets the terms of the steps before
+    // min(i, j) - 1 in ONE multi-term task at step min(i, j) - 2 (one read / write of
+    // the tile instead of one per step); the step scratch is kept per step for them
+    static const bool defer = !getenv("FDE_H2_NODEFER");
+    // step scratch ring: a pending term from step s is flushed at step s + nring - 2 at the
+    // latest (its task runs on the bulk stream before the critical stream's products of
+    // step s + nring rewrite the buffer); 2 without deferral (double buffering)
+    static const int nring = defer ? std::max(3, getenv("FDE_H2_RING") ? atoi(getenv("FDE_H2_RING")) : 8) : 2;
     static const bool pretrunc = !getenv("FDE_H2_NOPRETRUNC");
     const int R = hm->R, rmax = L->rmax;
     if (trunc && (R > TRUNC_KMAX || rmax > TRUNC_KMAX)) return false;
@@ -871,11 +879,21 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         ptp = now;
     };
     std::vector<VStep> steps(nl);
+    std::vector<std::vector<VTerm>> dpend(defer ? (size_t)nl * nl : 0);   // deferred dense-update terms per tile
+    std::vector<int> dpend_k(defer ? (size_t)nl * nl : 0, 0);            // their summed inner dimension
+    std::vector<size_t> dfull;
+    std::vector<int> dfirst(defer ? (size_t)nl * nl : 0, -1);            // step of a tile's oldest pending term
+    std::vector<std::vector<size_t>> dstarted(defer ? nl : 0);           // tiles whose pending list started at step s
+    // a tile whose pending terms reach this inner dimension is updated right away
+    // (bounds the serial work of one GEMM tile; the tile is still read / written
+    // once per KFLUSH of accumulated rank instead of once per step)
+    static const int kflush = getenv("FDE_H2_KFLUSH") ? std::max(16, atoi(getenv("FDE_H2_KFLUSH"))) : 256;
     std::vector<int> stamp(nb, 0), tile_stamp((size_t)nl * nl, 0), tile_task((size_t)nl * nl, 0);
     int stamp_id = 0, tile_stamp_id = 0;
     for (int k = 0; k < nl; ++k) {
         VStep& st = steps[k];
         ptick(0);
+        const int sid = k % nring;   // step scratch buffer (a ring: deferred dense updates read earlier steps' scratch)
         const int mk = lm(k);
         const int dk = own(k, k);
         std::vector<int> Cb, Rc;   // column-panel blocks (rows > k), row-panel blocks (cols > k)
@@ -962,13 +980,13 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         for (int b : Cb)
             if (isLR(b)) {
                 snapU[b] = scr;
-                st.snap.push_back({{1, b, 0}, {3, k & 1, scr}, S.bl[b].m, S.bl[b].m, (int)S.bl[b].m, kc[b], 0, 1.0});
+                st.snap.push_back({{1, b, 0}, {3, sid, scr}, S.bl[b].m, S.bl[b].m, (int)S.bl[b].m, kc[b], 0, 1.0});
                 scr += S.bl[b].m * kc[b];
             }
         for (int c : Rc)
             if (isLR(c)) {
                 snapV[c] = scr;
-                st.snap.push_back({{2, c, 0}, {3, k & 1, scr}, S.bl[c].n, S.bl[c].n, (int)S.bl[c].n, kc[c], 0, 1.0});
+                st.snap.push_back({{2, c, 0}, {3, sid, scr}, S.bl[c].n, S.bl[c].n, (int)S.bl[c].n, kc[c], 0, 1.0});
                 scr += S.bl[c].n * kc[c];
             }
         for (int b : Cb)
@@ -980,16 +998,16 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
                     if (isLR(c)) {   // core = U_c[k]^T V_b[k]  (kc_c x kc_b)
                         core = scr;
                         scr += (int64_t)kc[c] * kc[b];
-                        VTask t{{3, k & 1, core}, kc[c], kc[c], kc[b], 0.0, {}};
+                        VTask t{{3, sid, core}, kc[c], kc[c], kc[b], 0.0, {}};
                         t.terms.push_back({{1, c, lr0[k] - row0(c)}, {2, b, lr0[k] - col0(b)}, C.m, B.n, mk, 1, 0, 1.0});
                         st.g1.push_back(t);
                     }
                     pr.w = scr;
                     pr.rw = kc[b];
                     scr += C.n * kc[b];
-                    VTask t{{3, k & 1, pr.w}, C.n, (int)C.n, kc[b], 0.0, {}};
+                    VTask t{{3, sid, pr.w}, C.n, (int)C.n, kc[b], 0.0, {}};
                     if (isLR(c))   // W = V_c core
-                        t.terms.push_back({{2, c, 0}, {3, k & 1, core}, C.n, kc[c], kc[c], 0, 0, 1.0});
+                        t.terms.push_back({{2, c, 0}, {3, sid, core}, C.n, kc[c], kc[c], 0, 0, 1.0});
                     else           // W = D_c[k rows, :]^T V_b[k]
                         t.terms.push_back({{0, c, lr0[k] - row0(c)}, {2, b, lr0[k] - col0(b)}, C.m, B.n, mk, 1, 0, 1.0});
                     st.g2.push_back(t);
@@ -997,7 +1015,7 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
                     pr.w = scr;
                     pr.rw = kc[c];
                     scr += B.m * kc[c];
-                    VTask t{{3, k & 1, pr.w}, B.m, (int)B.m, kc[c], 0.0, {}};
+                    VTask t{{3, sid, pr.w}, B.m, (int)B.m, kc[c], 0.0, {}};
                     t.terms.push_back({{0, b, (lr0[k] - col0(b)) * B.m}, {1, c, lr0[k] - row0(c)}, B.m, C.m, mk, 0, 0, 1.0});
                     st.g2.push_back(t);
                 }
@@ -1081,8 +1099,11 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
                     for (int i = std::max(std::max(t0[b], t0[t]), k + 1); i <= std::min(t1[b], t1[t]); ++i)
                         for (int j = std::max(std::max(s0[c], s0[t]), k + 1); j <= std::min(s1[c], s1[t]); ++j) {
                             const size_t key = (size_t)i * nl + j;
-                            int ti;
-                            if (tile_stamp[key] != tile_stamp_id) {
+                            const bool to_pend = defer && i != k + 1 && j != k + 1;
+                            int ti = -1;
+                            if (to_pend) {
+                                // (the term is built below and appended to pend[key])
+                            } else if (tile_stamp[key] != tile_stamp_id) {
                                 ti = (int)st.g3.size();
                                 tile_stamp[key] = tile_stamp_id;
                                 tile_task[key] = ti;
@@ -1101,13 +1122,21 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
                                 term = {{0, b, (lr0[k] - col0(b)) * B.m + (lr0[i] - row0(b))},
                                         {0, c, (lr0[j] - col0(c)) * C.m + (lr0[k] - row0(c))}, B.m, C.m, mk, 0, 0, -1.0};
                             } else if (pr.bl) {   // U_b[i rows] W[j rows]^T
-                                term = {{3, k & 1, su_b + (lr0[i] - row0(b))}, {3, k & 1, pr.w + (lr0[j] - col0(c))}, B.m, C.n,
+                                term = {{3, sid, su_b + (lr0[i] - row0(b))}, {3, sid, pr.w + (lr0[j] - col0(c))}, B.m, C.n,
                                         kc[b], 0, 1, -1.0};
                             } else {               // Z[i rows] V_c[j rows]^T
-                                term = {{3, k & 1, pr.w + (lr0[i] - row0(b))}, {3, k & 1, sv_c + (lr0[j] - col0(c))}, B.m, C.n,
+                                term = {{3, sid, pr.w + (lr0[i] - row0(b))}, {3, sid, sv_c + (lr0[j] - col0(c))}, B.m, C.n,
                                         kc[c], 0, 1, -1.0};
                             }
-                            st.g3[ti].terms.push_back(term);
+                            if (to_pend) {
+                                if (dpend[key].empty()) {
+                                    dfirst[key] = k;
+                                    dstarted[k].push_back(key);
+                                }
+                                dpend[key].push_back(term);
+                                if ((dpend_k[key] += term.k) >= kflush) dfull.push_back(key);
+                            }
+                            else st.g3[ti].terms.push_back(term);
                         }
                 } else {
                     const int key = pr.bl ? b : (nb + c);
@@ -1123,6 +1152,35 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
                     }
                     lterms.push_back({(int)pi, gi});
                 }
+            }
+        }
+        if (defer) {   // flush full tiles, and the pending terms of row / column k+2
+            const int m2 = k + 2;
+            auto flush = [&](int i, int j) {
+                std::vector<VTerm>& pv = dpend[(size_t)i * nl + j];
+                if (pv.empty()) return;
+                dpend_k[(size_t)i * nl + j] = 0;
+                dfirst[(size_t)i * nl + j] = -1;
+                const int t = own(i, j);
+                const HBlock& T = S.bl[t];
+                VTask tk{{0, t, (lr0[j] - col0(t)) * T.m + (lr0[i] - row0(t))}, T.m, lm(i), lm(j), 1.0, {}};
+                for (const VTerm& q : pv) tk.terms.push_back(q);
+                st.g3.push_back(std::move(tk));
+                // (k+2, k+2) on the critical stream: it is the input of LU(k+2) next step
+                st.g3crit.push_back(i == m2 && j == m2 ? 1 : 0);
+                std::vector<VTerm>().swap(pv);
+            };
+            for (size_t key : dfull) flush((int)(key / nl), (int)(key % nl));
+            dfull.clear();
+            const int s_old = k - nring + 2;   // scratch buffer of step s_old is rewritten at step s_old + nring
+            if (s_old >= 0) {
+                for (size_t key : dstarted[s_old])
+                    if (dfirst[key] == s_old) flush((int)(key / nl), (int)(key % nl));
+                std::vector<size_t>().swap(dstarted[s_old]);
+            }
+            if (m2 < nl) {
+                for (int j = m2; j < nl; ++j) flush(m2, j);
+                for (int i = m2 + 1; i < nl; ++i) flush(i, m2);
             }
         }
         ptick(5);
@@ -1180,13 +1238,13 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
                     u_done[lt.second] = 1;
                     st.cpr[g.round].push_back({{1, b, R0 - row0(b)}, {1, t, us}, B.m, T.m, (int)(R1 - R0), g.rank, 0, 1.0});
                 }
-                st.cpr[g.round].push_back({{3, k & 1, pr.w + (C0 - col0(c))}, {2, t, vs}, C.n, T.n, (int)(C1 - C0), g.rank, 0, -1.0});
+                st.cpr[g.round].push_back({{3, sid, pr.w + (C0 - col0(c))}, {2, t, vs}, C.n, T.n, (int)(C1 - C0), g.rank, 0, -1.0});
             } else {
                 if (!u_done[lt.second]) {   // V slot rows C = -V_c rows (once per group)
                     u_done[lt.second] = 1;
                     st.cpr[g.round].push_back({{2, c, C0 - col0(c)}, {2, t, vs}, C.n, T.n, (int)(C1 - C0), g.rank, 0, -1.0});
                 }
-                st.cpr[g.round].push_back({{3, k & 1, pr.w + (R0 - row0(b))}, {1, t, us}, B.m, T.m, (int)(R1 - R0), g.rank, 0, 1.0});
+                st.cpr[g.round].push_back({{3, sid, pr.w + (R0 - row0(b))}, {1, t, us}, B.m, T.m, (int)(R1 - R0), g.rank, 0, 1.0});
             }
         }
         st.scratch = scr;
@@ -1237,11 +1295,13 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
                     if (std::abs(i - j) == dd) w += (int64_t)lm(i) * lm(j);
         scr_max = std::max(scr_max, w);
     }
-    // step scratch (W / Z products, cores), double-buffered: the products of step k
-    // are read by the copies (stream sb) and the bulk updates (stream sc) of step k,
-    // which complete before the critical stream reaches the products of step k+2
+    // step scratch (W / Z products, cores, operand snapshots).  Deferred dense
+    // updates read the scratch of earlier steps: one buffer per step.  Otherwise
+    // double-buffered: the products of step k are read by the copies (stream sb) and
+    // the bulk updates (stream sc) of step k, which complete before the critical
+    // stream reaches the products of step k+2.
     const int64_t off_scr = words;
-    words += 2 * scr_max;
+    words += (int64_t)nring * scr_max;
     // truncation workspace (max over batches)
     int64_t gmax = 1, tmax = 1, emax = 1;
     auto tr_size = [&](const std::vector<VTrunc>& v) {
