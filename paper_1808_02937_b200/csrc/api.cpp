@@ -250,7 +250,7 @@ int sem_assemble(fde_handle h, const fde_problem* prob, const fde_mesh* mesh, in
     op->r1 = op->rank_r0[h->rank + 1];
     op->lda = round_up(op->n, 32);
 
-    FDE_CUDA(cudaEventRecord(h->ev0, h->stream));
+    op->tm.start(h->stream);   // (the call returns without waiting: the next calls' host work overlaps it)
     asm_prepare_tables(h, op);
     if (flags & FDE_OP_DENSE) {
         const int b0 = op->e_lo, b1 = std::min(op->e_hi, N - 1);
@@ -263,17 +263,12 @@ int sem_assemble(fde_handle h, const fde_problem* prob, const fde_mesh* mesh, in
         asm_k_triangle(h, op, b0, b1 + 1, Krow.p);
         if (ncol > 0) asm_k_rect(h, op, b1 + 1, N, b0, b1 + 1, Kcol.p);
         op->A.alloc((size_t)std::max<int64_t>(op->r1 - op->r0, 1) * op->lda);
-        asm_expand_dense(h, op, Krow.p, Kcol.p);
-        FDE_CUDA(cudaStreamSynchronize(h->stream));   // K tables are released here
+        asm_expand_dense(h, op, Krow.p, Kcol.p);   // (K tables: stream-ordered release on scope exit)
     }
     asm_boundary_columns(h, op);
     if (flags & FDE_OP_TOEPLITZ) toeplitz_prepare(h, op);
     op->xw_cols = 0;
-    FDE_CUDA(cudaEventRecord(h->ev1, h->stream));
-    FDE_CUDA(cudaEventSynchronize(h->ev1));
-    float ms = 0;
-    cudaEventElapsedTime(&ms, h->ev0, h->ev1);
-    op->assemble_ms = ms;
+    op->tm.stop(h->stream);
     *out = op;
     op = nullptr;
     }
@@ -296,7 +291,7 @@ int fde_operator_get_info(fde_operator op, fde_operator_info* info)
     info->lda = op->lda;
     info->flags = op->flags;
     info->uniform = op->uniform ? 1 : 0;
-    info->assemble_ms = op->assemble_ms;
+    info->assemble_ms = op->tm.get();
     return FDE_OK;
 }
 
@@ -369,7 +364,7 @@ int fde_hmatrix_get_info(fde_hmatrix hm, fde_hmatrix_info* info)
     info->nclusters = (int)hm->S.cl.size();
     info->dense_entries = hm->dense_words;
     info->lr_entries = hm->lr_words;
-    info->build_ms = hm->build_ms;
+    info->build_ms = hm->tm.get();
     return FDE_OK;
 }
 

@@ -664,7 +664,6 @@ void asm_prepare_tables(fde_ctx* h, fde_op* op)
     fdeq::gauss_jacobi(op->tab.qi, 0.0, 1.0 - alpha, x, w);
     op->tab.gji_x.upload(x.data(), x.size(), h->stream);
     op->tab.gji_w.upload(w.data(), w.size(), h->stream);
-    FDE_CUDA(cudaStreamSynchronize(h->stream));   // host vectors x,w go out of scope
     op->tab.kself.alloc((size_t)P * P);
     op->tab.mref.alloc((size_t)(P + 1) * (P + 1));
     AsmDev D = make_dev(op, qm_for(P));
@@ -753,7 +752,6 @@ void asm_boundary_columns(fde_ctx* h, fde_op* op)
     k_boundary_cols<<<(unsigned)ceil_div(op->n, 256), 256, 0, h->stream>>>(
         K, op->n, N, op->P, op->prob.theta, op->prob.rho, op->tab.nodes.p, op->tab.mref.p, op->bnd.p);
     FDE_CHECK_LAUNCH();
-    FDE_CUDA(cudaStreamSynchronize(h->stream));   // temporaries are freed on return
 }
 
 void asm_rhs(fde_ctx* h, fde_op* op, const fde_forcing* f, int nrhs, double* G, int64_t ld)
@@ -803,7 +801,6 @@ void asm_rhs(fde_ctx* h, fde_op* op, const fde_forcing* f, int nrhs, double* G, 
         k_gather_loads<<<(unsigned)ceil_div(op->n, 256), 256, 0, h->stream>>>(
             loc.p, op->n, N, P, op->prob.c1, op->prob.c2, op->bnd.p, G + (long long)r * ld);
         FDE_CHECK_LAUNCH();
-        FDE_CUDA(cudaStreamSynchronize(h->stream));   // per-forcing temporaries
     }
 }
 

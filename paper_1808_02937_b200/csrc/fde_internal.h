@@ -46,6 +46,37 @@ inline void fde_fail(int code, const std::string& m) { throw FdeError{code, m}; 
 cudaStream_t fde_alloc_stream();
 void fde_set_alloc_stream(cudaStream_t s);
 
+// Device-time of an asynchronous library call: events recorded on its stream at
+// start and end; the elapsed time is read (and waited for) only when asked.
+struct LazyTimer {
+    cudaEvent_t b = nullptr, e = nullptr;
+    double ms = -1.0;
+    LazyTimer() = default;
+    LazyTimer(const LazyTimer&) = delete;
+    LazyTimer& operator=(const LazyTimer&) = delete;
+    void start(cudaStream_t s)
+    {
+        if (!b) cudaEventCreate(&b);
+        if (!e) cudaEventCreate(&e);
+        ms = -1.0;
+        cudaEventRecord(b, s);
+    }
+    void stop(cudaStream_t s) { cudaEventRecord(e, s); }
+    double get()
+    {
+        if (ms < 0.0 && e) {
+            float f = 0.0f;
+            if (cudaEventSynchronize(e) == cudaSuccess && cudaEventElapsedTime(&f, b, e) == cudaSuccess) ms = f;
+        }
+        return ms < 0.0 ? 0.0 : ms;
+    }
+    ~LazyTimer()
+    {
+        if (b) cudaEventDestroy(b);
+        if (e) cudaEventDestroy(e);
+    }
+};
+
 template <typename T>
 struct DBuf {
     T* p = nullptr;
@@ -203,6 +234,7 @@ struct AsmTables {
 };
 
 struct fde_op {
+    LazyTimer tm;        // device time of the assembly (read lazily)
     fde_problem prob{};
     int N = 0, P = 0;
     int64_t n = 0;

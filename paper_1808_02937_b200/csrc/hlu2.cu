@@ -782,11 +782,6 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
     // deferred dense updates: a dense tile (i, j) gets the terms of the steps before
     // min(i, j) - 1 in ONE multi-term task at step min(i, j) - 2 (one read / write of
     // the tile instead of one per step); the step scratch is kept per step for them
-    static const bool defer = !getenv("FDE_H2_NODEFER");
-    // step scratch ring: a pending term from step s is flushed at step s + nring - 2 at the
-    // latest (its task runs on the bulk stream before the critical stream's products of
-    // step s + nring rewrite the buffer); 2 without deferral (double buffering)
-    static const int nring = defer ? std::max(3, getenv("FDE_H2_RING") ? atoi(getenv("FDE_H2_RING")) : 8) : 2;
     static const bool pretrunc = !getenv("FDE_H2_NOPRETRUNC");
     const int R = hm->R, rmax = L->rmax;
     if (trunc && (R > TRUNC_KMAX || rmax > TRUNC_KMAX)) return false;
@@ -807,6 +802,15 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
     }
     lr0.push_back(S.n);
     const int nl = (int)lr0.size() - 1;
+    // Deferral pays with many sweep tiles (measured: c5, 256 tiles, 7 % faster per solve;
+    // c4, 64 tiles, 4 % slower: a larger scratch ring for little saved traffic there).
+    // FDE_H2_DEFER=0/1 forces it.
+    const char* e_def = getenv("FDE_H2_DEFER");
+    const bool defer = !getenv("FDE_H2_NODEFER") && (e_def ? atoi(e_def) != 0 : nl >= 128);
+    // step scratch ring: a pending term from step s is flushed at step s + nring - 2 at the
+    // latest (its task runs on the bulk stream before the critical stream's products of
+    // step s + nring rewrite the buffer); 2 without deferral (double buffering)
+    const int nring = defer ? std::max(3, getenv("FDE_H2_RING") ? atoi(getenv("FDE_H2_RING")) : 8) : 2;
     // leaves of the partition as tile ranges (the substitutions run over leaves)
     const int nleaf = (int)leafcl.size();
     std::vector<int> lq0(nleaf), lq1(nleaf), leaf_of(nl);
@@ -887,7 +891,7 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
     // a tile whose pending terms reach this inner dimension is updated right away
     // (bounds the serial work of one GEMM tile; the tile is still read / written
     // once per KFLUSH of accumulated rank instead of once per step)
-    static const int kflush = getenv("FDE_H2_KFLUSH") ? std::max(16, atoi(getenv("FDE_H2_KFLUSH"))) : 256;
+    const int kflush = getenv("FDE_H2_KFLUSH") ? std::max(16, atoi(getenv("FDE_H2_KFLUSH"))) : 256;
     std::vector<int> stamp(nb, 0), tile_stamp((size_t)nl * nl, 0), tile_task((size_t)nl * nl, 0);
     int stamp_id = 0, tile_stamp_id = 0;
     for (int k = 0; k < nl; ++k) {

@@ -245,8 +245,8 @@ fde_hm* hm_build(fde_ctx* h, fde_op* op, int R, double lam, int n_min)
     if (R < 1 || R > 32) fde_fail(FDE_EINVAL_PARAM, "hmatrix_build: R must be in [1, 32]");
     if (!(lam > 0)) fde_fail(FDE_EINVAL_PARAM, "hmatrix_build: lambda must be > 0");
     if (n_min < 1) fde_fail(FDE_EINVAL_PARAM, "hmatrix_build: n_min must be >= 1");
-    FDE_CUDA(cudaEventRecord(h->ev0, h->stream));
     fde_hm* hm = new fde_hm();
+    hm->tm.start(h->stream);   // (returns without waiting; see LazyTimer)
     try {
         hm->op = op;
         hm->R = R;
@@ -387,7 +387,6 @@ fde_hm* hm_build(fde_ctx* h, fde_op* op, int R, double lam, int n_min)
                 k_leaf_from_dense<<<cnt, dim3(32, 8), 0, h->stream>>>(dlt.p + base, op->A.p, op->lda, hm->dense.p);
                 FDE_CHECK_LAUNCH();
             }
-            FDE_CUDA(cudaStreamSynchronize(h->stream));
         } else if (!ld.empty()) {
             DBuf<int> di, dj;
             DBuf<long long> dsl;
@@ -400,14 +399,9 @@ fde_hm* hm_build(fde_ctx* h, fde_op* op, int R, double lam, int n_min)
             asm_k_list(h, op, di.p, dj.p, dsl.p, (int64_t)li.size(), ktab.p);
             dld.upload(ld.data(), ld.size(), h->stream);
             asm_expand_leaves(h, op, ktab.p, dld.p, (int)ld.size(), maxent, hm->dense.p);
-            FDE_CUDA(cudaStreamSynchronize(h->stream));
         }
         hm->rank.upload(rank_h.data(), rank_h.size(), h->stream);
-        FDE_CUDA(cudaEventRecord(h->ev1, h->stream));
-        FDE_CUDA(cudaEventSynchronize(h->ev1));
-        float ms = 0;
-        cudaEventElapsedTime(&ms, h->ev0, h->ev1);
-        hm->build_ms = ms;
+        hm->tm.stop(h->stream);
     } catch (...) {
         delete hm;
         throw;

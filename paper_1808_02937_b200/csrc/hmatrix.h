@@ -33,6 +33,7 @@ struct HStruct {
 };
 
 struct fde_hm {
+    LazyTimer tm;        // device time of the build (read lazily)
     fde_op* op = nullptr;
     int R = 0;
     double lam = 1.0;

@@ -231,6 +231,29 @@ def test_hlu_exact_mode_equals_dense_solve_of_Atilde(fde, h, case, hlu_mode):
         o.free()
 
 
+@pytest.mark.parametrize("case", HLU2_CASES[-5:], ids=lambda c: f"{c[0].name}-nmin{c[1]}")
+def test_hlu_deferred_updates_exact_mode(fde, h, case, monkeypatch):
+    """The deferred dense updates (default for >= 128 sweep tiles, forced here with
+    FDE_H2_DEFER=1; small flush threshold and scratch ring so that every flush path
+    runs) give the exact LU of A~ at tol = 0 like the step-by-step updates."""
+    monkeypatch.setenv("FDE_H2_DEFER", "1")
+    monkeypatch.setenv("FDE_H2_KFLUSH", "32")
+    monkeypatch.setenv("FDE_H2_RING", "3")
+    p, n_min = case
+    op = fde.assemble_problem(h, p)
+    hm = fde.hmatrix_build(h, op, p.R, 1.0, n_min)
+    lu = fde.hlu_factor(h, hm, 0.0)
+    so = oracle_system(p)
+    At, _ = O.hmatrix_dense(p, so, R=p.R, lam=1.0, n_min=n_min)
+    r = np.random.default_rng(7).standard_normal((2, p.n))
+    z = fde.precond_apply(h, lu, torch.tensor(r, device="cuda")).cpu().numpy()
+    zo = np.linalg.solve(At, r.T).T
+    err = np.linalg.norm(z - zo) / np.linalg.norm(zo)
+    assert err <= TOL, err
+    for o in (lu, hm, op):
+        o.free()
+
+
 @pytest.mark.parametrize("nrhs", [9, 19, 64])
 def test_hlu_apply_many_rhs_equals_dense_solve_of_Atilde(fde, h, nrhs):
     """precond_apply with more right-hand sides than the register chunk (nrhs > 8:
