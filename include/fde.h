@@ -150,9 +150,14 @@ typedef struct {
     int64_t lda;          /* leading dimension of the dense shard               */
     int32_t flags;
     int32_t uniform;      /* mesh verified uniform                               */
-    double assemble_ms;   /* device time of the last assembly                    */
+    double assemble_ms;   /* device time of the assembly; -1 while it still runs */
 } fde_operator_info;
+/* sem_assemble and hmatrix_build return as soon as their device work is
+ * enqueued on the handle's stream (results are stream-ordered: later calls and
+ * stream work see them complete); get_info never waits, *_wait blocks until the
+ * object's device work is done (then the timing fields are final). */
 int fde_operator_get_info(fde_operator op, fde_operator_info* info);
+int fde_operator_wait(fde_operator op);
 
 /* Copy the dense operator rows [r0,r1) x all columns, PAPER order, into the
  * device buffer out (row-major, ldo >= n).  World==1 only (test helper). */
@@ -188,9 +193,10 @@ int hmatrix_build(fde_handle h, fde_operator op, int R, double lambda, int n_min
 typedef struct {
     int32_t nblocks_dense, nblocks_lr, depth, nclusters;
     int64_t dense_entries, lr_entries;   /* stored fp64 words              */
-    double build_ms;
+    double build_ms;      /* device time of the build; -1 while it still runs    */
 } fde_hmatrix_info;
 int fde_hmatrix_get_info(fde_hmatrix hm, fde_hmatrix_info* info);
+int fde_hmatrix_wait(fde_hmatrix hm);
 /* Expand A~ into a dense n x n matrix, paper order, column-major with ldo >= n,
  * device buffer (test / diagnostics helper; O(n^2) memory). */
 int fde_hmatrix_dense_paper(fde_handle h, fde_hmatrix hm, double* out, int64_t ldo);

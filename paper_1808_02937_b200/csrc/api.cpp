@@ -280,6 +280,20 @@ int sem_assemble(fde_handle h, const fde_problem* prob, const fde_mesh* mesh, in
     return FDE_OK;
 }
 
+int fde_operator_wait(fde_operator op)
+{
+    if (!op) return FDE_EINVAL_PARAM;
+    op->tm.get();
+    return FDE_OK;
+}
+
+int fde_hmatrix_wait(fde_hmatrix hm)
+{
+    if (!hm) return FDE_EINVAL_PARAM;
+    hm->tm.get();
+    return FDE_OK;
+}
+
 int fde_operator_get_info(fde_operator op, fde_operator_info* info)
 {
     if (!op || !info) return FDE_EINVAL_PARAM;
@@ -291,7 +305,7 @@ int fde_operator_get_info(fde_operator op, fde_operator_info* info)
     info->lda = op->lda;
     info->flags = op->flags;
     info->uniform = op->uniform ? 1 : 0;
-    info->assemble_ms = op->tm.get();
+    info->assemble_ms = op->tm.peek();   // -1 while the (asynchronous) assembly runs
     return FDE_OK;
 }
 
@@ -364,7 +378,7 @@ int fde_hmatrix_get_info(fde_hmatrix hm, fde_hmatrix_info* info)
     info->nclusters = (int)hm->S.cl.size();
     info->dense_entries = hm->dense_words;
     info->lr_entries = hm->lr_words;
-    info->build_ms = hm->tm.get();
+    info->build_ms = hm->tm.peek();      // -1 while the (asynchronous) build runs
     return FDE_OK;
 }
 

@@ -62,6 +62,8 @@ struct LazyTimer {
         cudaEventRecord(b, s);
     }
     void stop(cudaStream_t s) { cudaEventRecord(e, s); }
+    bool ready() { return ms >= 0.0 || !e || cudaEventQuery(e) == cudaSuccess; }
+    double peek() { return ready() ? get() : -1.0; }   // -1: still running (does not wait)
     double get()
     {
         if (ms < 0.0 && e) {

@@ -40,6 +40,7 @@ EXPORTED = [
     "hlu_factor", "fde_hlu_get_info", "fde_hlu_dense_internal", "precond_apply", "solve", "fde_solve",
     "fde_free_operator", "fde_free_hmatrix", "fde_free_hlu", "fde_profile", "fde_profile_collect",
     "fde_launch_count", "fde_shard_rows", "fde_debug_hlu_mode", "fde_debug_pool_bytes",
+    "fde_operator_wait", "fde_hmatrix_wait",
 ]
 
 
@@ -204,9 +205,17 @@ class Operator:
     def __init__(self, handle: Handle, ptr: ctypes.c_void_p):
         self.handle, self.ptr = handle, ptr
         inf = OperatorInfo()
-        _check(lib().fde_operator_get_info(ptr, ctypes.byref(inf)))
-        self.info = inf
+        _check(lib().fde_operator_get_info(ptr, ctypes.byref(inf)))   # (does not wait)
+        self._info = inf
         self.n = inf.n
+
+    @property
+    def info(self):
+        """Operator facts; assemble_ms is final once the assembly completed (waits for it)."""
+        if self._info.assemble_ms < 0:
+            _check(lib().fde_operator_wait(self.ptr))
+            _check(lib().fde_operator_get_info(self.ptr, ctypes.byref(self._info)))
+        return self._info
 
     def free(self):
         if self.ptr:
@@ -286,8 +295,16 @@ class HMatrix:
     def __init__(self, handle, ptr, n):
         self.handle, self.ptr, self.n = handle, ptr, n
         inf = HMatrixInfo()
-        _check(lib().fde_hmatrix_get_info(ptr, ctypes.byref(inf)))
-        self.info = inf
+        _check(lib().fde_hmatrix_get_info(ptr, ctypes.byref(inf)))   # (does not wait)
+        self._info = inf
+
+    @property
+    def info(self):
+        """H-matrix facts; build_ms is final once the build completed (waits for it)."""
+        if self._info.build_ms < 0:
+            _check(lib().fde_hmatrix_wait(self.ptr))
+            _check(lib().fde_hmatrix_get_info(self.ptr, ctypes.byref(self._info)))
+        return self._info
 
     def free(self):
         if self.ptr:
