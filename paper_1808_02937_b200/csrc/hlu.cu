@@ -2012,14 +2012,14 @@ fde_lu* hlu_build(fde_ctx* h, fde_hm* hm, double tol)
         flush_dirty(L);
         hlu_rec(L, L->S.root);
         }
+        // the substitution schedule is built on the host while the device finishes the
+        // factorisation (it needs the block structure only); then one wait for the flags
+        L->ap = apply_sched_build(L);
         FDE_CUDA(cudaMemcpyAsync(L->pinned, L->dflag.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, h->stream));
         FDE_CUDA(cudaEventRecord(h->ev1, h->stream));
         FDE_CUDA(cudaEventSynchronize(h->ev1));
         if (L->pinned[0]) fde_fail(FDE_ESINGULAR_PIVOT, "H-LU: zero or non-finite pivot in a leaf factorisation");
         if (L->pinned[1]) fde_fail(FDE_ERANK, "H-LU: truncated rank exceeded the block capacity");
-        L->ap = apply_sched_build(L);
-        FDE_CUDA(cudaEventRecord(h->ev1, h->stream));
-        FDE_CUDA(cudaEventSynchronize(h->ev1));
         float ms = 0;
         cudaEventElapsedTime(&ms, h->ev0, h->ev1);
         L->factor_ms = ms;
@@ -2659,7 +2659,8 @@ static ApplySched* apply_sched_build(fde_lu* L)
         if (!dv.empty()) Do.upload(dv.data(), dv.size(), L->h->stream); else Do.alloc(1);
         if (!rv.empty()) Ro.upload(rv.data(), rv.size(), L->h->stream); else Ro.alloc(1);
         if (!pv.empty()) Po.upload(pv.data(), pv.size(), L->h->stream); else Po.alloc(1);
-        FDE_CUDA(cudaStreamSynchronize(L->h->stream));   // host vectors go out of scope
+        // (pageable uploads are staged before cudaMemcpyAsync returns: the host
+        // vectors may go out of scope without waiting)
     };
     flatten(df, lf, pf, 0, A->leaf_f, A->dense_f, A->lrr_f, A->proj_f);
     flatten(db, lb, pb, 1, A->leaf_b, A->dense_b, A->lrr_b, A->proj_b);
