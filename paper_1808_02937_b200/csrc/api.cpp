@@ -24,10 +24,37 @@ void hlu_trunc_stats(unsigned long long* out4);
 
 static thread_local std::string g_noctx_err;
 static thread_local cudaStream_t g_alloc_stream = nullptr;
+static thread_local fde_ctx* g_cur_ctx = nullptr;
 cudaStream_t fde_alloc_stream() { return g_alloc_stream; }
 void fde_set_alloc_stream(cudaStream_t s) { g_alloc_stream = s; }
 
-#define API_BEGIN try { if (h) fde_set_alloc_stream(h->stream);
+#define FDE_RING_HALF ((size_t)16 << 20)
+bool fde_ring_upload(void* dst, const void* src, size_t bytes, cudaStream_t s)
+{
+    fde_ctx* h = g_cur_ctx;
+    if (!h || bytes == 0 || bytes > FDE_RING_HALF) return false;
+    if (!h->ring) {
+        if (cudaMallocHost((void**)&h->ring, 2 * FDE_RING_HALF) != cudaSuccess) {
+            h->ring = nullptr;
+            return false;
+        }
+        for (auto& e : h->ring_ev) FDE_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    if (h->ring_off + bytes > FDE_RING_HALF) {   // next half (its last copies were long ago)
+        h->ring_cur ^= 1;
+        if (h->ring_rec[h->ring_cur]) FDE_CUDA(cudaEventSynchronize(h->ring_ev[h->ring_cur]));
+        h->ring_off = 0;
+    }
+    char* p = h->ring + (size_t)h->ring_cur * FDE_RING_HALF + h->ring_off;
+    memcpy(p, src, bytes);
+    FDE_CUDA(cudaMemcpyAsync(dst, p, bytes, cudaMemcpyHostToDevice, s));
+    FDE_CUDA(cudaEventRecord(h->ring_ev[h->ring_cur], s));
+    h->ring_rec[h->ring_cur] = true;
+    h->ring_off += (bytes + 255) & ~(size_t)255;
+    return true;
+}
+
+#define API_BEGIN try { if (h) fde_set_alloc_stream(h->stream); g_cur_ctx = h;
 #define API_END(h)                                                   \
     }                                                                \
     catch (FdeError & e) {                                           \
@@ -91,6 +118,9 @@ void fde_destroy(fde_handle h)
     if (h->ev1) cudaEventDestroy(h->ev1);
     if (h->pinned) cudaFreeHost(h->pinned);
     if (h->stage) cudaFreeHost(h->stage);
+    if (h->ring) cudaFreeHost(h->ring);
+    for (auto e : h->ring_ev)
+        if (e) cudaEventDestroy(e);
     if (h->aux) {
         cudaStreamSynchronize(h->aux);
         cudaStreamSynchronize(h->aux2);

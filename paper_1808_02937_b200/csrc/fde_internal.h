@@ -45,6 +45,11 @@ inline void fde_fail(int code, const std::string& m) { throw FdeError{code, m}; 
 // cudaMalloc/cudaFree page mapping and implicit device synchronisation.
 cudaStream_t fde_alloc_stream();
 void fde_set_alloc_stream(cudaStream_t s);
+// Host -> device uploads staged through a page-locked ring of the calling handle
+// (set by API_BEGIN): a copy from pageable memory may wait for the stream's
+// pending work, which serialised the host's next steps behind the device.
+// Returns false (caller copies directly) when no handle / ring is available.
+bool fde_ring_upload(void* dst, const void* src, size_t bytes, cudaStream_t s);
 
 // Device-time of an asynchronous library call: events recorded on its stream at
 // start and end; the elapsed time is read (and waited for) only when asked.
@@ -106,7 +111,8 @@ struct DBuf {
     }
     void upload(const T* h, size_t count, cudaStream_t s) {
         if (count > n) alloc(count);
-        if (count) FDE_CUDA(cudaMemcpyAsync(p, h, count * sizeof(T), cudaMemcpyHostToDevice, s));
+        if (count && !fde_ring_upload(p, h, count * sizeof(T), s))
+            FDE_CUDA(cudaMemcpyAsync(p, h, count * sizeof(T), cudaMemcpyHostToDevice, s));
     }
     void zero(cudaStream_t s) {
         if (n) FDE_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), s));
@@ -141,6 +147,13 @@ struct fde_ctx {
     cudaEvent_t ev_aux[16] = {};
     void* stage = nullptr;   // page-locked staging of descriptor uploads (grow-only)
     size_t stage_bytes = 0;
+    // upload ring (fde_ring_upload): two halves; a half is reused after the event
+    // recorded behind its last copy completes
+    char* ring = nullptr;
+    size_t ring_off = 0;
+    int ring_cur = 0;
+    cudaEvent_t ring_ev[2] = {};
+    bool ring_rec[2] = {};
 };
 
 // page-locked staging buffer of at least `bytes` (the previous contents are dropped;

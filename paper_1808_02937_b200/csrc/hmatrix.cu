@@ -1,3 +1,4 @@
+#include <chrono>
 // hmatrix_build: H-matrix approximation A~ = rho M + theta H + (1-theta) H^T of
 // the SEM stiffness (Eq. (approxmat)/(approxsys); reading A2).
 //
@@ -247,6 +248,14 @@ fde_hm* hm_build(fde_ctx* h, fde_op* op, int R, double lam, int n_min)
     if (n_min < 1) fde_fail(FDE_EINVAL_PARAM, "hmatrix_build: n_min must be >= 1");
     fde_hm* hm = new fde_hm();
     hm->tm.start(h->stream);   // (returns without waiting; see LazyTimer)
+    static const bool dbg_t = getenv("FDE_DEBUG_HBUILD") != nullptr;
+    auto t0 = std::chrono::steady_clock::now();
+    auto tick = [&](const char* what) {
+        if (!dbg_t) return;
+        const auto t1 = std::chrono::steady_clock::now();
+        fprintf(stderr, "hbuild host %-12s %.3f ms\n", what, std::chrono::duration<double, std::milli>(t1 - t0).count());
+        t0 = t1;
+    };
     try {
         hm->op = op;
         hm->R = R;
@@ -254,6 +263,7 @@ fde_hm* hm_build(fde_ctx* h, fde_op* op, int R, double lam, int n_min)
         hm->n_min = n_min;
         HStruct& S = hm->S;
         hstruct_build(S, op->nodes_h, op->P, n_min, lam);
+        tick("structure");
         const int N = op->N, P = op->P;
         const std::vector<double>& x = op->nodes_h;
         std::vector<int> lv;
@@ -277,6 +287,7 @@ fde_hm* hm_build(fde_ctx* h, fde_op* op, int R, double lam, int n_min)
         hm->lr_words = loff;
         hm->dense.alloc(std::max<int64_t>(doff, 1));
         hm->lr.alloc(std::max<int64_t>(loff, 1));
+        tick("arenas");
         std::vector<int> rank_h(S.bl.size(), 0);
         // ---- low-rank factors
         std::vector<FDesc> fd;
@@ -337,6 +348,7 @@ fde_hm* hm_build(fde_ctx* h, fde_op* op, int R, double lam, int n_min)
                 FDE_CHECK_LAUNCH();
             }
         }
+        tick("factors");
         // ---- dense leaves: K tables + expansion
         std::vector<LeafDesc> ld;
         std::vector<int> li, lj;
@@ -358,13 +370,6 @@ fde_hm* hm_build(fde_ctx* h, fde_op* op, int R, double lam, int n_min)
             L.nj = std::min(Sg.e1 + 1, N) - Sg.e0;
             L.ktab = kslot;
             L.out = B.off;
-            for (int a = 0; a < L.ni; ++a)
-                for (int c = 0; c < L.nj; ++c) {
-                    int i = L.i0 + a, j = L.j0 + c;
-                    li.push_back(std::max(i, j));
-                    lj.push_back(std::min(i, j));
-                    ls.push_back(kslot + (int64_t)a * L.nj + c);
-                }
             kslot += (int64_t)L.ni * L.nj;
             maxent = std::max(maxent, L.m * L.nc);
             ld.push_back(L);
@@ -388,6 +393,15 @@ fde_hm* hm_build(fde_ctx* h, fde_op* op, int R, double lam, int n_min)
                 FDE_CHECK_LAUNCH();
             }
         } else if (!ld.empty()) {
+            // element pairs of the dense leaves (only needed when they are recomputed)
+            for (const LeafDesc& L : ld)
+                for (int a = 0; a < L.ni; ++a)
+                    for (int c = 0; c < L.nj; ++c) {
+                        const int i = L.i0 + a, j = L.j0 + c;
+                        li.push_back(std::max(i, j));
+                        lj.push_back(std::min(i, j));
+                        ls.push_back(L.ktab + (int64_t)a * L.nj + c);
+                    }
             DBuf<int> di, dj;
             DBuf<long long> dsl;
             DBuf<double> ktab;
@@ -400,8 +414,10 @@ fde_hm* hm_build(fde_ctx* h, fde_op* op, int R, double lam, int n_min)
             dld.upload(ld.data(), ld.size(), h->stream);
             asm_expand_leaves(h, op, ktab.p, dld.p, (int)ld.size(), maxent, hm->dense.p);
         }
+        tick("leaves");
         hm->rank.upload(rank_h.data(), rank_h.size(), h->stream);
         hm->tm.stop(h->stream);
+        tick("end");
     } catch (...) {
         delete hm;
         throw;
