@@ -647,7 +647,15 @@ static AsmDev make_dev(fde_op* op, int qm)
     return D;
 }
 
-static int qm_for(int P) { int q = P + 2; if (q < 24) q = 24; if (q > FDE_QMAX) q = FDE_QMAX; return q; }
+static int qm_for(int P)
+{
+    // per-direction point capacity of the warp workspace (FDE_ASM_QM overrides)
+    static const int env = getenv("FDE_ASM_QM") ? atoi(getenv("FDE_ASM_QM")) : 0;
+    int q = P + 2;
+    if (q < (env ? env : 24)) q = env ? env : 24;
+    if (q > FDE_QMAX) q = FDE_QMAX;
+    return q;
+}
 
 void asm_prepare_tables(fde_ctx* h, fde_op* op)
 {
