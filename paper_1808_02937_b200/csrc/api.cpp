@@ -118,6 +118,7 @@ void fde_destroy(fde_handle h)
     if (h->ev1) cudaEventDestroy(h->ev1);
     if (h->pinned) cudaFreeHost(h->pinned);
     if (h->stage) cudaFreeHost(h->stage);
+    krylov_ws_free(h);
     if (h->ring) cudaFreeHost(h->ring);
     for (auto e : h->ring_ev)
         if (e) cudaEventDestroy(e);
@@ -285,11 +286,13 @@ int sem_assemble(fde_handle h, const fde_problem* prob, const fde_mesh* mesh, in
     if (flags & FDE_OP_DENSE) {
         const int b0 = op->e_lo, b1 = std::min(op->e_hi, N - 1);
         const int64_t P2 = (int64_t)P * P;
-        DBuf<double> Krow, Kcol;
+        // (handle-owned, grow-only: 4.3 GB for c5, not re-allocated per assembly)
+        DBuf<double>& Krow = h->kt_row;
+        DBuf<double>& Kcol = h->kt_col;
         const int64_t nrow = (int64_t)(b1 + 1) * (b1 + 2) / 2 - (int64_t)b0 * (b0 + 1) / 2;
         const int64_t ncol = (int64_t)(N - 1 - b1) * (b1 - b0 + 1);
-        Krow.alloc((size_t)std::max<int64_t>(nrow, 1) * P2);
-        if (ncol > 0) Kcol.alloc((size_t)ncol * P2);
+        if (Krow.n < (size_t)std::max<int64_t>(nrow, 1) * P2) Krow.alloc((size_t)std::max<int64_t>(nrow, 1) * P2);
+        if (ncol > 0 && Kcol.n < (size_t)ncol * P2) Kcol.alloc((size_t)ncol * P2);
         asm_k_triangle(h, op, b0, b1 + 1, Krow.p);
         if (ncol > 0) asm_k_rect(h, op, b1 + 1, N, b0, b1 + 1, Kcol.p);
         op->A.alloc((size_t)std::max<int64_t>(op->r1 - op->r0, 1) * op->lda);

@@ -50,6 +50,8 @@ void fde_set_alloc_stream(cudaStream_t s);
 // pending work, which serialised the host's next steps behind the device.
 // Returns false (caller copies directly) when no handle / ring is available.
 bool fde_ring_upload(void* dst, const void* src, size_t bytes, cudaStream_t s);
+struct fde_ctx;
+void krylov_ws_free(fde_ctx* h);
 
 // Device-time of an asynchronous library call: events recorded on its stream at
 // start and end; the elapsed time is read (and waited for) only when asked.
@@ -149,6 +151,8 @@ struct fde_ctx {
     size_t stage_bytes = 0;
     // upload ring (fde_ring_upload): two halves; a half is reused after the event
     // recorded behind its last copy completes
+    void* kws = nullptr;     // Krylov workspace (krylov.cu), grow-only
+    DBuf<double> kt_row, kt_col;   // pair-moment tables of the assembly (transient), grow-only
     char* ring = nullptr;
     size_t ring_off = 0;
     int ring_cur = 0;

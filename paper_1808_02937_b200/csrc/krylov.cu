@@ -172,6 +172,11 @@ struct KrylovWS {
     DBuf<double> V, H, cs, sn, g, y, hbuf, nrm, res, w, t, x;
     DBuf<int> active, kc;
 };
+void krylov_ws_free(fde_ctx* h)
+{
+    delete (KrylovWS*)h->kws;
+    h->kws = nullptr;
+}
 
 static void apply_MA(fde_ctx* h, fde_op* op, fde_lu* lu, const double* x, long long ldx, double* out, long long ldo,
                      double* tmp, int nrhs, int path)
@@ -192,20 +197,27 @@ void krylov_gmres(fde_ctx* h, fde_op* op, fde_lu* lu, const double* G, double* X
     const int m = std::max(1, std::min(o->restart > 0 ? o->restart : 50, 200));
     const int maxit = o->maxiter > 0 ? o->maxiter : 500;
     const double tol = o->tol > 0 ? o->tol : 1e-12;
-    KrylovWS W;
-    W.V.alloc((size_t)(m + 1) * nrhs * ldv);
-    W.H.alloc((size_t)nrhs * (m + 1) * m);
-    W.cs.alloc((size_t)nrhs * m);
-    W.sn.alloc((size_t)nrhs * m);
-    W.g.alloc((size_t)nrhs * (m + 1));
-    W.y.alloc((size_t)nrhs * (m + 1));
-    W.hbuf.alloc((size_t)nrhs * (m + 1));
-    W.nrm.alloc(nrhs);
-    W.res.alloc(nrhs);
-    W.w.alloc((size_t)nrhs * ldv);
-    W.t.alloc((size_t)nrhs * ldv);
-    W.active.alloc(nrhs);
-    W.kc.alloc(nrhs);
+    // handle-owned, grow-only workspace: the Krylov basis ((m+1) x nrhs x n, 0.86 GB for
+    // c5) is not re-allocated per solve (pool growth behind large transient
+    // allocations stalled some c5 solves by hundreds of ms)
+    if (!h->kws) h->kws = new KrylovWS();
+    KrylovWS& W = *(KrylovWS*)h->kws;
+    auto need = [](auto& b, size_t cnt) {
+        if (b.n < cnt) b.alloc(cnt);
+    };
+    need(W.V, (size_t)(m + 1) * nrhs * ldv);
+    need(W.H, (size_t)nrhs * (m + 1) * m);
+    need(W.cs, (size_t)nrhs * m);
+    need(W.sn, (size_t)nrhs * m);
+    need(W.g, (size_t)nrhs * (m + 1));
+    need(W.y, (size_t)nrhs * (m + 1));
+    need(W.hbuf, (size_t)nrhs * (m + 1));
+    need(W.nrm, (size_t)nrhs);
+    need(W.res, (size_t)nrhs);
+    need(W.w, (size_t)nrhs * ldv);
+    need(W.t, (size_t)nrhs * ldv);
+    need(W.active, (size_t)nrhs);
+    need(W.kc, (size_t)nrhs);
     cudaStream_t s = h->stream;
     const dim3 gv((unsigned)ceil_div(ldv, KB), (unsigned)nrhs);
     FDE_CUDA(cudaMemsetAsync(X, 0, sizeof(double) * ldv * nrhs, s));
