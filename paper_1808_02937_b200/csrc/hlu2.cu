@@ -883,6 +883,7 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         ptp = now;
     };
     std::vector<VStep> steps(nl);
+    size_t g3_hint = 64;
     std::vector<std::vector<VTerm>> dpend(defer ? (size_t)nl * nl : 0);   // deferred dense-update terms per tile
     std::vector<int> dpend_k(defer ? (size_t)nl * nl : 0, 0);            // their summed inner dimension
     std::vector<size_t> dfull;
@@ -1027,6 +1028,8 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
             }
         ptick(2);
         // targets
+        st.g3.reserve(g3_hint);
+        st.g3crit.reserve(g3_hint);
         ++tile_stamp_id;   // dense target tile (i, j) -> g3 task (stamped flat table)
         struct Grp { int t, key, rank; int64_t slot; int round; };
         std::map<std::pair<int, int>, int> lgrp;     // (target, key) -> group index
@@ -1187,6 +1190,7 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
                 for (int i = m2 + 1; i < nl; ++i) flush(i, m2);
             }
         }
+        g3_hint = st.g3.size() + 64;   // (reserve for the next step: fewer reallocations)
         ptick(5);
         // early truncation of the panel operands of step k+1 that are not operands of
         // this step: they run off the critical stream (with the overflow truncations,
@@ -1803,6 +1807,7 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
     enum { T_LU = 0, T_PAN, T_PROD, T_CRIT, T_OP, T_OV, T_CP, T_REST, T_SNAP, T_DIAG, T_G1, T_G2, T_GRAM, T_CORE, T_PUSH, T_N };
     std::vector<cudaEvent_t> tev;
     std::vector<double> thost;
+    double eq_us[3] = {0, 0, 0};   // host: flatten, push, launches (timeline mode)
     const auto th0 = std::chrono::steady_clock::now();
     cudaEvent_t t0ev = nullptr;
     if (tline) {
@@ -1816,6 +1821,7 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
     };
     for (int k = 0; k < kstop; ++k) {
         dbg_step = k;
+        const auto te0 = std::chrono::steady_clock::now();
         // flatten step k (the device is still busy with step k-1) and stage it
         H2Launch& ln = P->steps[k];
         VStep& st = steps[k];
@@ -1859,7 +1865,9 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
             put_gemm(rest, ln, 4, gemm_shape[4]);
             put_gemm(diag, ln, 5, gemm_shape[5]);
         }
+        const auto te1 = std::chrono::steady_clock::now();
         push();
+        const auto te2 = std::chrono::steady_clock::now();
         mark(k, T_PUSH, sd);
         dbg("push");
         FDE_CUDA(cudaStreamWaitEvent(sa, evD, 0));
@@ -1969,6 +1977,12 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         FDE_CUDA(cudaEventRecord(evC, sc));
         mark(k, T_REST, sc);
         if (tline) thost.push_back(std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - th0).count());
+        if (tline) {
+            const auto te3 = std::chrono::steady_clock::now();
+            eq_us[0] += std::chrono::duration<double, std::micro>(te1 - te0).count();
+            eq_us[1] += std::chrono::duration<double, std::micro>(te2 - te1).count();
+            eq_us[2] += std::chrono::duration<double, std::micro>(te3 - te2).count();
+        }
     }
     if (tline) {
         FDE_CUDA(cudaDeviceSynchronize());
@@ -1987,7 +2001,8 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         fprintf(stderr, "hlu2 timeline (%d steps): per-step period of each mark (us):", kstop);
         for (int w = 0; w < T_N; ++w) fprintf(stderr, " %s %.1f |", nm[w], 1e3 * sum[w] / std::max(1, kstop - 1));
         if (kstop > 1)
-            fprintf(stderr, " host enqueue %.1f |", (thost.back() - thost.front()) / (kstop - 1));
+            fprintf(stderr, " host enqueue %.1f (flatten %.1f, push %.1f, launches %.1f) |",
+                    (thost.back() - thost.front()) / (kstop - 1), eq_us[0] / kstop, eq_us[1] / kstop, eq_us[2] / kstop);
         fprintf(stderr, "\n  step 10 marks (ms from start):");
         for (int w = 0; w < T_N && kstop > 10; ++w) {
             float ms = 0;
