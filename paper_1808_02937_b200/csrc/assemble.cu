@@ -462,6 +462,68 @@ __device__ inline double a_entry(const KL& K, long long r, long long c, long lon
     return rho * mass + theta * sl + (1.0 - theta) * slt;
 }
 
+// Expansion per element pair: thread (ei, ej) writes the P x P entries A[rows of
+// element ei][columns of element ej] (8 contiguous doubles per row: a warp writes
+// 32 consecutive segments, coalesced).  The index arithmetic of dof_terms /
+// K.get is done once per pair (base pointers of the <= 4 neighbouring pair blocks
+// in both orientations) instead of once per entry.  Same terms in the same order
+// as a_entry: bit-identical entries.
+template <int PT>
+__global__ void __launch_bounds__(128) k_expand_pairs(KBand K, long long r0, long long r1, long long n, long long lda,
+                                                      int N, int Prt, double theta, double rho, const double* nodes,
+                                                      const double* mref, double* A)
+{
+    const int P = PT ? PT : Prt;
+    const int ej = blockIdx.x * blockDim.x + threadIdx.x;
+    const int ei = (int)(r0 / P) + blockIdx.y;
+    const long long c0 = (long long)ej * P;
+    if (c0 >= lda) return;
+    // pair blocks: lower K(a, b) (b <= a) and upper K(b, a) (a <= b), a in {ei, ei+1}, b in {ej, ej+1}
+    const double* kl[2][2];
+    const double* ku[2][2];
+#pragma unroll
+    for (int da = 0; da < 2; ++da)
+#pragma unroll
+        for (int db = 0; db < 2; ++db) {
+            const int a = ei + da, b = ej + db;
+            const bool ok = a < N && b < N;
+            kl[da][db] = (ok && b <= a) ? K.get(a, b) : nullptr;
+            ku[da][db] = (ok && a <= b) ? K.get(b, a) : nullptr;
+        }
+    const double hi = ei < N ? 0.5 * (nodes[ei + 1] - nodes[ei]) : 0.0;
+    const double hi1 = ei + 1 < N ? 0.5 * (nodes[ei + 2] - nodes[ei + 1]) : 0.0;
+    for (int qr = 0; qr < P; ++qr) {
+        const long long r = (long long)ei * P + qr;
+        if (r < r0 || r >= r1) continue;
+        const DofTerms tr = dof_terms<PT>(r, n, N, P);
+        double* Ar = A + (r - r0) * lda + c0;
+        for (int qc = 0; qc < P; ++qc) {
+            const long long c = c0 + qc;
+            if (c >= lda) break;
+            double v = 0.0;
+            if (c < n && ej < N) {
+                const DofTerms tc = dof_terms<PT>(c, n, N, P);
+                double sl = 0.0, slt = 0.0, mass = 0.0;
+                for (int x = 0; x < tr.cnt; ++x) {
+                    const int eiX = tr.e[x];
+                    if (eiX < 0 || eiX >= N) continue;
+                    for (int y = 0; y < tc.cnt; ++y) {
+                        const int ejY = tc.e[y];
+                        if (ejY < 0 || ejY >= N) continue;
+                        const double cc = tr.c[x] * tc.c[y];
+                        const int da = eiX - ei, db = ejY - ej;
+                        if (ejY <= eiX) sl = fma(cc, kl[da][db][tr.m[x] * P + tc.m[y]], sl);
+                        if (eiX <= ejY) slt = fma(cc, ku[da][db][tc.m[y] * P + tr.m[x]], slt);
+                        if (eiX == ejY) mass = fma(da ? hi1 : hi, mref[tr.ml[x] * (P + 1) + tc.ml[y]], mass);
+                    }
+                }
+                v = rho * mass + theta * sl + (1.0 - theta) * slt;
+            }
+            Ar[qc] = v;
+        }
+    }
+}
+
 template <int PT>
 __global__ void __launch_bounds__(256) k_expand_dense(KBand K, long long r0, long long r1, long long n, long long lda,
                                                       int N, int P, double theta, double rho, const double* nodes,
@@ -727,11 +789,28 @@ void asm_expand_dense(fde_ctx* h, fde_op* op, const double* Krow, const double* 
 #define FDE_EXPAND(PT_)                                                                                           \
     k_expand_dense<PT_><<<grid, 256, 0, h->stream>>>(K, op->r0, op->r1, op->n, op->lda, op->N, op->P, op->prob.theta, \
                                                      op->prob.rho, op->tab.nodes.p, op->tab.mref.p, op->A.p)
-    switch (op->P) {   // the common degrees with a compile-time P
-        case 4: FDE_EXPAND(4); break;
-        case 8: FDE_EXPAND(8); break;
-        case 16: FDE_EXPAND(16); break;
-        default: FDE_EXPAND(0);
+    static const bool per_entry = getenv("FDE_EXPAND_ENTRY") != nullptr;   // (the previous per-entry kernel)
+    if (per_entry) {
+        switch (op->P) {   // the common degrees with a compile-time P
+            case 4: FDE_EXPAND(4); break;
+            case 8: FDE_EXPAND(8); break;
+            case 16: FDE_EXPAND(16); break;
+            default: FDE_EXPAND(0);
+        }
+    } else {
+        const long long e_first = op->r0 / op->P, e_last = (op->r1 - 1) / op->P;
+        const long long col_elems = ceil_div(op->lda, (long long)op->P);
+        dim3 pg((unsigned)ceil_div(col_elems, 128LL), (unsigned)(e_last - e_first + 1));
+#define FDE_EXPAND_P(PT_)                                                                                       \
+    k_expand_pairs<PT_><<<pg, 128, 0, h->stream>>>(K, op->r0, op->r1, op->n, op->lda, op->N, op->P, op->prob.theta, \
+                                                    op->prob.rho, op->tab.nodes.p, op->tab.mref.p, op->A.p)
+        switch (op->P) {
+            case 4: FDE_EXPAND_P(4); break;
+            case 8: FDE_EXPAND_P(8); break;
+            case 16: FDE_EXPAND_P(16); break;
+            default: FDE_EXPAND_P(0);
+        }
+#undef FDE_EXPAND_P
     }
 #undef FDE_EXPAND
     FDE_CHECK_LAUNCH();

@@ -2683,7 +2683,9 @@ static void apply_sched_run(fde_ctx* h, fde_lu* L, double* x, int64_t ldx, int n
     // cooperative launch: one CTA per SM (all resident), grid barriers between steps
     int per_sm = 0;
     FDE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_apply, APPLY_THREADS, 0));
-    const int nblk = std::max(1, std::min(per_sm, 1)) * h->num_sms;
+    int nblk = std::max(1, std::min(per_sm, 1)) * h->num_sms;
+    static const int env_ctas = getenv("FDE_APPLY_CTAS") ? atoi(getenv("FDE_APPLY_CTAS")) : 0;
+    if (env_ctas > 0) nblk = std::min(nblk, env_ctas);
     void* args[] = {&f, &b, &x, &ldx, &nrhs, &A->z.p, &A->t.p, &A->tslots};
     long long ldx_ll = ldx;
     args[3] = &ldx_ll;
