@@ -30,6 +30,8 @@ __constant__ double c_glw[FDE_GL_TOTAL];
 #define FDE_LEG_K 64
 __constant__ double c_leg_a[FDE_LEG_K];
 __constant__ double c_leg_b[FDE_LEG_K];
+// digits targeted by the quadrature order selection (FDE_ASM_DIGITS, default 17)
+__constant__ float c_qdigits = 17.0f;
 
 static int g_gl_uploaded_dev = -1;
 
@@ -54,6 +56,8 @@ static void upload_gl_tables(int dev)
     }
     FDE_CUDA(cudaMemcpyToSymbol(c_leg_a, la, sizeof(la)));
     FDE_CUDA(cudaMemcpyToSymbol(c_leg_b, lb, sizeof(lb)));
+    const float qd = getenv("FDE_ASM_DIGITS") ? (float)atof(getenv("FDE_ASM_DIGITS")) : 17.0f;
+    FDE_CUDA(cudaMemcpyToSymbol(c_qdigits, &qd, sizeof(qd)));
     g_gl_uploaded_dev = dev;
 }
 
@@ -118,7 +122,7 @@ __device__ inline int q_select(double eta, int P, int qm)
     const float etaf = (float)fmin(eta, 1e30);
     const float rho = etaf + sqrtf(fmaxf(etaf * etaf - 1.0f, 0.0f));
     const float lr = __log10f(fmaxf(0.8f * rho, 1.05f));
-    int q = (int)ceilf((17.0f / lr + (float)P) * 0.5f);
+    int q = (int)ceilf((c_qdigits / lr + (float)P) * 0.5f);
     int qmin = P / 2 + 2;
     if (q < qmin) q = qmin;
     if (q > qm) q = qm;
