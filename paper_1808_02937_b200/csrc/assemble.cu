@@ -122,7 +122,7 @@ __device__ inline int q_select(double eta, int P, int qm)
     const float etaf = (float)fmin(eta, 1e30);
     const float rho = etaf + sqrtf(fmaxf(etaf * etaf - 1.0f, 0.0f));
     const float lr = __log10f(fmaxf(0.8f * rho, 1.05f));
-    int q = (int)ceilf((c_qdigits / lr + (float)P) * 0.5f);
+    int q = (int)ceilf((__fdividef(c_qdigits, lr) + (float)P) * 0.5f);
     int qmin = P / 2 + 2;
     if (q < qmin) q = qmin;
     if (q > qm) q = qm;
@@ -131,10 +131,11 @@ __device__ inline int q_select(double eta, int P, int qm)
 
 // One tensor Gauss-Legendre cell [u0,u1]x[v0,v1] of the (u,v) rectangle;
 // accumulates sum w_a w_b L_m(xi_a) L_n(eta_b) (d+u_a+v_b)^{1-alpha} into acc.
+template <int PT>
 __device__ void warp_cell(const AsmDev& D, const WarpWS& ws, double d, double hi, double hj, double u0,
                           double u1, double v0, double v1, int lane)
 {
-    const int P = D.P;
+    const int P = PT ? PT : D.P;
     const double du = u1 - u0, dv = v1 - v0;
     const double dist = d + u0 + v0;
     const int Qu = q_select(1.0 + 2.0 * dist / du, P, D.qm);
@@ -159,8 +160,9 @@ __device__ void warp_cell(const AsmDev& D, const WarpWS& ws, double d, double hi
     const double uc = 0.5 * (u0 + u1), vc = 0.5 * (v0 + v1);
     const double zc = d + uc + vc;
     const double kc = pow(zc, D.oma), izc = 1.0 / zc;
+    const float rQv = 1.0f / (float)Qv;
     for (int idx = lane; idx < Qu * Qv; idx += 32) {
-        int a = idx / Qv, b = idx - a * Qv;
+        const int a = (int)(((float)idx + 0.5f) * rQv), b = idx - a * Qv;   // (exact: idx < 24^2)
         double delta = ((ws.ua[a] - uc) + (ws.vb[b] - vc)) * izc;
         ws.kv[idx] = ws.wa[a] * ws.wb[b] * kc * exp(D.oma * log1p(delta));
     }
@@ -183,6 +185,7 @@ __device__ void warp_cell(const AsmDev& D, const WarpWS& ws, double d, double hi
 }
 
 // graded composite rule on the rectangle [u0,u1]x[v0,v1] (needs d+u0+v0 > 0)
+template <int PT>
 __device__ void warp_graded(const AsmDev& D, const WarpWS& ws, double d, double hi, double hj, double u0,
                             double u1, double v0, double v1, int lane)
 {
@@ -197,7 +200,7 @@ __device__ void warp_graded(const AsmDev& D, const WarpWS& ws, double d, double 
         while (va < v1 && g2++ < 400) {
             double vb = fmin(v1, va + c * (d + u0 + va));
             if (v1 - vb < 1e-3 * (vb - va)) vb = v1;
-            warp_cell(D, ws, d, hi, hj, ua, ub, va, vb, lane);
+            warp_cell<PT>(D, ws, d, hi, hj, ua, ub, va, vb, lane);
             va = vb;
         }
         ua = ub;
@@ -207,9 +210,10 @@ __device__ void warp_graded(const AsmDev& D, const WarpWS& ws, double d, double 
 // Duffy treatment of the corner square [0,c0]^2 of a touching pair (d = 0):
 //  v <= u: v = u w:  int_0^c0 u^{2-a} L_m(xi(u)) int_0^1 (1+w)^{1-a} L_n(eta(u w)) dw du
 //  u <= v: u = v w:  int_0^c0 v^{2-a} L_n(eta(v)) int_0^1 (1+w)^{1-a} L_m(xi(v w)) dw dv
+template <int PT>
 __device__ void warp_duffy(const AsmDev& D, const WarpWS& ws, double hi, double hj, double c0, int lane)
 {
-    const int P = D.P;
+    const int P = PT ? PT : D.P;
     const int Qr = D.qr;
     const int Qw = q_select(3.0, P, D.qm);
     const double* gxw = c_glx + Qw * (Qw - 1) / 2;
@@ -252,9 +256,10 @@ __device__ void warp_duffy(const AsmDev& D, const WarpWS& ws, double hi, double 
 }
 
 // compute the moment block of pair (i, j), i >= j, into out[P*P]
+template <int PT>
 __device__ void warp_pair(const AsmDev& D, const WarpWS& ws, int i, int j, double* out, int lane)
 {
-    const int P = D.P;
+    const int P = PT ? PT : D.P;
     const double hi = D.nodes[i + 1] - D.nodes[i];
     if (i == j) {
         const double s = pow(0.5 * hi, D.oma);
@@ -266,14 +271,14 @@ __device__ void warp_pair(const AsmDev& D, const WarpWS& ws, int i, int j, doubl
     for (int idx = lane; idx < P * P; idx += 32) ws.acc[idx] = 0.0;
     __syncwarp();
     if (d > 0.0) {
-        warp_graded(D, ws, d, hi, hj, 0.0, hi, 0.0, hj, lane);
+        warp_graded<PT>(D, ws, d, hi, hj, 0.0, hi, 0.0, hj, lane);
     } else {
         const double c0 = fmin(hi, hj);
-        warp_duffy(D, ws, hi, hj, c0, lane);
+        warp_duffy<PT>(D, ws, hi, hj, c0, lane);
         if (hi > hj * (1.0 + 1e-12))
-            warp_graded(D, ws, 0.0, hi, hj, c0, hi, 0.0, hj, lane);
+            warp_graded<PT>(D, ws, 0.0, hi, hj, c0, hi, 0.0, hj, lane);
         else if (hj > hi * (1.0 + 1e-12))
-            warp_graded(D, ws, 0.0, hi, hj, 0.0, hi, c0, hj, lane);
+            warp_graded<PT>(D, ws, 0.0, hi, hj, 0.0, hi, c0, hj, lane);
     }
     const double sc = D.g0 * (2.0 / hi) * (2.0 / hj);
     for (int idx = lane; idx < P * P; idx += 32) out[idx] = sc * ws.acc[idx];
@@ -285,6 +290,7 @@ __device__ void warp_pair(const AsmDev& D, const WarpWS& ws, int i, int j, doubl
 // mode 0: triangle rows [i0,i1): pair p -> (i, j<=i), slot p - T(i0)
 // mode 1: rectangle i in [i0,i1) x j in [j0,j1)
 // mode 2: explicit list
+template <int PT>
 __global__ void __launch_bounds__(32 * ASM_WARPS) k_pairs_kernel(AsmDev D, int mode, int i0, int i1, int j0,
                                                                 int j1, const int* li, const int* lj,
                                                                 const long long* lslot, long long count,
@@ -316,7 +322,7 @@ __global__ void __launch_bounds__(32 * ASM_WARPS) k_pairs_kernel(AsmDev D, int m
         j = lj[p];
         slot = lslot[p];
     }
-    warp_pair(D, ws, i, j, out + slot * (long long)D.P * D.P, lane);
+    warp_pair<PT>(D, ws, i, j, out + slot * (long long)D.P * D.P, lane);
 }
 
 // Kself[m][n] = gamma0 2^{alpha-2} sum_k sum_l wo_k wi_l L_m(xi_k) L_n(xi_k - (1+xi_k)(1+y_l)/2)
@@ -752,11 +758,21 @@ static void launch_pairs(fde_ctx* h, fde_op* op, int mode, int i0, int i1, int j
     const int qm = qm_for(op->P);
     AsmDev D = make_dev(op, qm);
     size_t smem = (size_t)ASM_WARPS * ws_doubles(op->P, qm) * sizeof(double);
-    FDE_CUDA(cudaFuncSetAttribute(k_pairs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     long long blocks = ceil_div(count, ASM_WARPS);
-    // grid.x limit is 2^31-1: fine for the sizes we handle
-    k_pairs_kernel<<<(unsigned)blocks, 32 * ASM_WARPS, smem, h->stream>>>(D, mode, i0, i1, j0, j1, li, lj, ls,
-                                                                           count, out);
+    // grid.x limit is 2^31-1: fine for the sizes we handle; the common degrees with a compile-time P
+#define FDE_PAIRS(PT_)                                                                                          \
+    do {                                                                                                        \
+        FDE_CUDA(cudaFuncSetAttribute(k_pairs_kernel<PT_>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+        k_pairs_kernel<PT_><<<(unsigned)blocks, 32 * ASM_WARPS, smem, h->stream>>>(D, mode, i0, i1, j0, j1, li, lj, ls, \
+                                                                                  count, out);                   \
+    } while (0)
+    switch (op->P) {
+        case 4: FDE_PAIRS(4); break;
+        case 8: FDE_PAIRS(8); break;
+        case 16: FDE_PAIRS(16); break;
+        default: FDE_PAIRS(0);
+    }
+#undef FDE_PAIRS
     FDE_CHECK_LAUNCH();
 }
 
