@@ -665,20 +665,20 @@ struct VTerm {
     int k, ta, tb;
     double alpha;
 };
-// the terms of a task: two inline, the rest on the heap (most dense-update tasks
-// have one or two terms; a heap vector per task cost ~1.5 ms of host planning on c4)
+// the terms of a task: one inline, the rest on the heap (most dense-update tasks
+// have one term; a heap vector per task cost ~1.5 ms of host planning on c4)
 struct VTermList {
-    VTerm inl[2];
+    VTerm inl[1];
     int n = 0;
     std::vector<VTerm> more;
     void push_back(const VTerm& t)
     {
-        if (n < 2) inl[n] = t;
+        if (n < 1) inl[n] = t;
         else more.push_back(t);
         ++n;
     }
     size_t size() const { return (size_t)n; }
-    const VTerm& operator[](int i) const { return i < 2 ? inl[i] : more[i - 2]; }
+    const VTerm& operator[](int i) const { return i < 1 ? inl[i] : more[i - 1]; }
     struct It {
         const VTermList* l;
         int i;
@@ -770,6 +770,43 @@ struct H2Plan {
 };
 
 static void hlu2_plan_free(H2Plan* p) { delete p; }
+
+// per-step (target block, key) -> value with a short list per target (replaces
+// std::map / std::set in the plan: no allocation per entry)
+struct TKMap {
+    std::vector<int> stamp, head, kk, vv, nx;
+    int sid = 0;
+    void init(int nb)
+    {
+        stamp.assign(nb, 0);
+        head.assign(nb, -1);
+    }
+    void clear()
+    {
+        ++sid;
+        kk.clear();
+        vv.clear();
+        nx.clear();
+    }
+    int* find(int t, int key)
+    {
+        if (stamp[t] != sid) return nullptr;
+        for (int e = head[t]; e >= 0; e = nx[e])
+            if (kk[e] == key) return &vv[e];
+        return nullptr;
+    }
+    void put(int t, int key, int v)
+    {
+        if (stamp[t] != sid) {
+            stamp[t] = sid;
+            head[t] = -1;
+        }
+        kk.push_back(key);
+        vv.push_back(v);
+        nx.push_back(head[t]);
+        head[t] = (int)kk.size() - 1;
+    }
+};
 int g_hlu2_stop = -1;   // debug: run only the first g_hlu2_stop leaf steps
 
 static bool hlu2_factor(fde_lu* L, fde_hm* hm)
@@ -883,6 +920,11 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         ptp = now;
     };
     std::vector<VStep> steps(nl);
+    TKMap lgrp, gseen;
+    lgrp.init(nb);
+    gseen.init(nb);
+    std::vector<int> rnd_stamp(nb, 0), rnd_val(nb, 0);
+    int rnd_sid = 0;
     size_t g3_hint = 64;
     std::vector<std::vector<VTerm>> dpend(defer ? (size_t)nl * nl : 0);   // deferred dense-update terms per tile
     std::vector<int> dpend_k(defer ? (size_t)nl * nl : 0, 0);            // their summed inner dimension
@@ -1032,7 +1074,7 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         st.g3crit.reserve(g3_hint);
         ++tile_stamp_id;   // dense target tile (i, j) -> g3 task (stamped flat table)
         struct Grp { int t, key, rank; int64_t slot; int round; };
-        std::map<std::pair<int, int>, int> lgrp;     // (target, key) -> group index
+        lgrp.clear();                                 // (target, key) -> group index
         std::vector<Grp> grps;
         std::vector<int> incoming(nb, 0);
         std::vector<std::pair<int, int>> lterms;     // (pair index, group index)
@@ -1060,7 +1102,7 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         // in them, or their width would exceed what a low-rank block can hold
         // (TRUNC_KMAX after truncation; min(m, n) / 2 in exact mode)
         {
-            std::set<std::pair<int, int>> gseen;
+            gseen.clear();
             std::vector<char> conv(nb, 0);
             for (size_t pi = 0; pi < pairs.size(); ++pi) {
                 const int b = pairs[pi].b, c = pairs[pi].c;
@@ -1069,7 +1111,10 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
                     if (!isLR(t)) continue;
                     if (!bl && !cl) { conv[t] = 1; continue; }
                     const int key = bl ? b : (nb + c);
-                    if (gseen.insert(std::make_pair(t, key)).second) incoming[t] += bl ? kc[b] : kc[c];
+                    if (!gseen.find(t, key)) {
+                        gseen.put(t, key, 1);
+                        incoming[t] += bl ? kc[b] : kc[c];
+                    }
                 }
             }
             for (int t = 0; t < nb; ++t) {
@@ -1147,15 +1192,13 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
                         }
                 } else {
                     const int key = pr.bl ? b : (nb + c);
-                    auto gk = std::make_pair(t, key);
-                    auto it = lgrp.find(gk);
                     int gi;
-                    if (it == lgrp.end()) {
-                        gi = (int)grps.size();
-                        lgrp[gk] = gi;
-                        grps.push_back({t, key, pr.bl ? kc[b] : kc[c], -1, 0});
+                    if (int* f = lgrp.find(t, key)) {
+                        gi = *f;
                     } else {
-                        gi = it->second;
+                        gi = (int)grps.size();
+                        lgrp.put(t, key, gi);
+                        grps.push_back({t, key, pr.bl ? kc[b] : kc[c], -1, 0});
                     }
                     lterms.push_back({(int)pi, gi});
                 }
@@ -1212,10 +1255,14 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         // slots and copies; a target whose new columns do not fit gets them in rounds,
         // truncated between rounds (formatted addition of the partial sums)
         std::vector<char> u_done(grps.size(), 0);
-        std::map<int, int> rnd;   // target -> current round
+        ++rnd_sid;   // target -> current round (stamped)
         for (size_t g = 0; g < grps.size(); ++g) {
             const int t = grps[g].t;
-            int& r = rnd[t];
+            if (rnd_stamp[t] != rnd_sid) {
+                rnd_stamp[t] = rnd_sid;
+                rnd_val[t] = 0;
+            }
+            int& r = rnd_val[t];
             if (trunc && kc[t] + grps[g].rank > TRUNC_KMAX) {
                 if (rmax + grps[g].rank > TRUNC_KMAX) return false;   // a single group never exceeds it
                 if ((int)st.trmid.size() <= r) st.trmid.resize(r + 1);
