@@ -329,8 +329,8 @@ def run_ours(args):
                 "kernel": "k_gemv_bulk (dense stiffness matvec, PAPER.md:629; TMA-engine bulk copies)", "bound": "hbm",
                 "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "peak_kind": peak_kind,
-                "traffic": 536897536 + 5126656 if (args.config == "c4" and world == 1) else None,
-                "traffic_source": "profiles/r1c_full.txt (ncu --set full, dram read+write of one k_gemv_bulk launch)",
+                "traffic": 536890368 + 4714240 if (args.config == "c4" and world == 1) else None,
+                "traffic_source": "profiles/r1e_full.txt (ncu --set full, dram read+write of one k_gemv_bulk launch)",
                 "launches": int(gemv_n), "avg_launch_us": (gemv_ms / gemv_n * 1e3) if gemv_n else None,
                 "share_of_step": gemv_ms / ms if ms else None,
                 "algorithmic_bytes_per_launch": (gemv_bytes / gemv_n) if gemv_n else None},
