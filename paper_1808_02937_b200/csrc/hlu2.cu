@@ -722,6 +722,12 @@ struct VStep {
     std::vector<VPanel> panel;
     std::vector<VPanel> npanel;          // the neighbour tiles (k+1, k), (k, k+1): on the LU stream
     std::vector<VTask> g0, g1, g2, g3;   // conversions to dense, cores, products, dense updates
+    // dense-target updates recorded compactly by the plan and expanded into g3 when the
+    // step is flattened (the expansion then overlaps the device; without deferral)
+    struct DPair { int b, c; int64_t w, su, sv; int kcb, kcc; bool bl, cl; };
+    std::vector<DPair> dpairs;
+    std::vector<std::pair<int, int>> dts;   // (pair, dense target block)
+    int sid = 0, mk = 0;
     std::vector<VTask> g3r;              // dense updates of tiles off row / column k+1 (lookahead stream)
     std::vector<char> g3crit;            // per g3 task: 2 tile (k+1, k+1), 1 row / column k+1 or (k+2, k+2), 0 rest
     std::vector<std::vector<VCopy>> cpr;    // new low-rank target columns, by round
@@ -942,6 +948,8 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         ptick(0);
         const int sid = k % nring;   // step scratch buffer (a ring: deferred dense updates read earlier steps' scratch)
         const int mk = lm(k);
+        st.sid = sid;
+        st.mk = mk;
         const int dk = own(k, k);
         std::vector<int> Cb, Rc;   // column-panel blocks (rows > k), row-panel blocks (cols > k)
         for (int i = k + 1; i < nl; ++i) {
@@ -1145,9 +1153,14 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
             const Pair& pr = pairs[pi];
             const int b = pr.b, c = pr.c;
             const int64_t su_b = pr.bl ? snapU[b] : 0, sv_c = (!pr.bl && pr.cl) ? snapV[c] : 0;   // (hoisted lookups)
+            if (!defer) {   // compact record; expanded at flatten time
+                st.dpairs.push_back({b, c, pr.w, su_b, sv_c, kc[b], kc[c], pr.bl, pr.cl});
+            }
             for (int t : ptg[pi]) {
                 const HBlock& T = S.bl[t];
-                if (!isLR(t)) {
+                if (!isLR(t) && !defer) {
+                    st.dts.push_back({(int)st.dpairs.size() - 1, t});
+                } else if (!isLR(t)) {
                     for (int i = std::max(std::max(t0[b], t0[t]), k + 1); i <= std::min(t1[b], t1[t]); ++i)
                         for (int j = std::max(std::max(s0[c], s0[t]), k + 1); j <= std::min(s1[c], s1[t]); ++j) {
                             const size_t key = (size_t)i * nl + j;
@@ -1619,6 +1632,16 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         cnt_tasks(st.g1, gemm_shape[0]);
         cnt_tasks(st.g2, gemm_shape[1]);
         cnt_tasks(st.g3, 1);   // (crit / rest / diag: at most the tiles of the 32 x 32 shape)
+        for (auto& dt : st.dts) {   // compact dense work (expanded later): one term, at most one task per tile
+            const auto& dp = st.dpairs[dt.first];
+            const int t = dt.second;
+            const int k = (int)(&st - &steps[0]);
+            const int64_t ni = std::max(0, std::min(t1[dp.b], t1[t]) - std::max(std::max(t0[dp.b], t0[t]), k + 1) + 1);
+            const int64_t nj = std::max(0, std::min(s1[dp.c], s1[t]) - std::max(std::max(s0[dp.c], s0[t]), k + 1) + 1);
+            n_term += (size_t)(ni * nj);
+            n_task += (size_t)(ni * nj);
+            n_tile += (size_t)(ni * nj) * ceil_div(H2_MMAX, 32) * ceil_div(H2_MMAX, 32);
+        }
         for (auto& v : st.cpr) cnt_cp(v);
         cnt_cp(st.snap);
         for (auto& v : st.trmid) cnt_trunc(v);
@@ -1863,6 +1886,8 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         FDE_CUDA(cudaEventCreate(&t0ev));
         FDE_CUDA(cudaEventRecord(t0ev, sa));
     }
+    std::vector<int> xtile_stamp((size_t)nl * nl, 0), xtile_task((size_t)nl * nl, 0);   // (flatten-time tile -> task)
+    int xtile_stamp_id = 0;
     auto mark = [&](int k, int w, cudaStream_t st) {
         if (tline) FDE_CUDA(cudaEventRecord(tev[(size_t)k * T_N + w], st));
     };
@@ -1899,6 +1924,42 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
             if (r < st.trmid.size()) {
                 ln.trmid.emplace_back();
                 put_trunc(st.trmid[r], ln.trmid.back());
+            }
+        }
+        if (!st.dts.empty()) {   // expand the compact dense-target work of the plan (same order as before)
+            ++xtile_stamp_id;
+            const int sid = st.sid, mk = st.mk;
+            for (size_t q = 0; q < st.dts.size(); ++q) {
+                const auto& dp = st.dpairs[st.dts[q].first];
+                const int t = st.dts[q].second, b = dp.b, c = dp.c;
+                const HBlock &T = S.bl[t], &B = S.bl[b], &C = S.bl[c];
+                for (int i = std::max(std::max(t0[b], t0[t]), k + 1); i <= std::min(t1[b], t1[t]); ++i)
+                    for (int j = std::max(std::max(s0[c], s0[t]), k + 1); j <= std::min(s1[c], s1[t]); ++j) {
+                        const size_t key = (size_t)i * nl + j;
+                        int ti;
+                        if (xtile_stamp[key] != xtile_stamp_id) {
+                            ti = (int)st.g3.size();
+                            xtile_stamp[key] = xtile_stamp_id;
+                            xtile_task[key] = ti;
+                            st.g3.push_back(VTask{{0, t, (lr0[j] - col0(t)) * T.m + (lr0[i] - row0(t))}, T.m, lm(i), lm(j), 1.0, {}});
+                            st.g3crit.push_back((i == k + 1 && j == k + 1) ? 2
+                                                : (i == k + 1 || j == k + 1 || (i == k + 2 && j == k + 2)));
+                        } else {
+                            ti = xtile_task[key];
+                        }
+                        VTerm term;
+                        if (!dp.bl && !dp.cl) {
+                            term = {{0, b, (lr0[k] - col0(b)) * B.m + (lr0[i] - row0(b))},
+                                    {0, c, (lr0[j] - col0(c)) * C.m + (lr0[k] - row0(c))}, B.m, C.m, mk, 0, 0, -1.0};
+                        } else if (dp.bl) {   // U_b[i rows] W[j rows]^T
+                            term = {{3, sid, dp.su + (lr0[i] - row0(b))}, {3, sid, dp.w + (lr0[j] - col0(c))}, B.m, C.n,
+                                    dp.kcb, 0, 1, -1.0};
+                        } else {               // Z[i rows] V_c[j rows]^T
+                            term = {{3, sid, dp.w + (lr0[i] - row0(b))}, {3, sid, dp.sv + (lr0[j] - col0(c))}, B.m, C.n,
+                                    dp.kcc, 0, 1, -1.0};
+                        }
+                        st.g3[ti].terms.push_back(term);
+                    }
             }
         }
         {   // split the dense updates: row / column k+1 (needed by step k+1) vs the rest
