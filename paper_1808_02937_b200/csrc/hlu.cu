@@ -2509,6 +2509,17 @@ __global__ void __launch_bounds__(APPLY_THREADS)
 
 // --------------------------------------------------------- schedule (host)
 struct ApplySched {
+    // host copies of the schedule (the many-RHS GEMM path builds its tasks from them)
+    std::vector<SLeaf> hleaf[2];
+    std::vector<SDense> hdense[2];
+    std::vector<SLRRow> hlrr[2];
+    std::vector<SProj> hproj[2];
+    std::vector<cudaEvent_t> gev;   // GEMM path: per-leaf projection events (+ 1)
+    ~ApplySched()
+    {
+        for (auto e : gev)
+            if (e) cudaEventDestroy(e);
+    }
     DBuf<SLeaf> leaf_f, leaf_b;
     DBuf<SDense> dense_f, dense_b;
     DBuf<SLRRow> lrr_f, lrr_b;
@@ -2655,6 +2666,10 @@ static ApplySched* apply_sched_build(fde_lu* L)
             pv.insert(pv.end(), p[q].begin(), p[q].end());
             s.p_hi = (int)pv.size();
         }
+        A->hleaf[which] = lv;
+        A->hdense[which] = dv;
+        A->hlrr[which] = rv;
+        A->hproj[which] = pv;
         Lo.upload(lv.data(), lv.size(), L->h->stream);
         if (!dv.empty()) Do.upload(dv.data(), dv.size(), L->h->stream); else Do.alloc(1);
         if (!rv.empty()) Ro.upload(rv.data(), rv.size(), L->h->stream); else Ro.alloc(1);
@@ -2667,9 +2682,19 @@ static ApplySched* apply_sched_build(fde_lu* L)
     return A;
 }
 
+void apply_gemm_path(fde_ctx* h, ApplySched* A, double* x, int64_t ldx, int nrhs);   // hlu2.cu
+
 static void apply_sched_run(fde_ctx* h, fde_lu* L, double* x, int64_t ldx, int nrhs)
 {
     ApplySched* A = L->ap;
+    // (the GEMM-task path is measured slower than the 8 x 8 tile path here -- its row
+    // tasks have long serial inner dimensions -- so it is opt-in: FDE_APPLY_GEMM_MIN=n)
+    const char* e_gm = getenv("FDE_APPLY_GEMM_MIN");
+    const int gemm_min = e_gm ? atoi(e_gm) : 0;
+    if (gemm_min > 0 && nrhs >= gemm_min) {   // many right-hand sides: multi-term GEMM tasks per leaf
+        apply_gemm_path(h, A, x, ldx, nrhs);
+        return;
+    }
     if ((size_t)A->zmax * nrhs > A->zcap) {
         A->z.alloc((size_t)A->zmax * nrhs);
         A->zcap = (size_t)A->zmax * nrhs;

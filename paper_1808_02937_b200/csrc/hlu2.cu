@@ -2243,3 +2243,150 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
 }
 
 
+
+// ------------------------------------------- many-RHS substitutions as GEMM tasks
+// precond_apply with nrhs >= FDE_APPLY_GEMM_MIN right-hand sides (opt-in): the
+// same leaf-sequential substitutions as k_apply, each leaf step as
+// multi-term GEMM tasks on the FP64 tensor cores (k_h2_gemm):
+//   x_k <- x_k - sum_d D_d x_{c_d} - sum_{l, chunk} U_l T_{l, chunk}   (in place, beta 1)
+//   z   <- Inv_k x_k ;  x_k <- z                                          (strided copy)
+//   T_{b, chunk} <- V_b[chunk]^T x_sigma[chunk]   for the blocks whose columns complete
+//                                                 at leaf k (second stream)
+// The projections of 256-row chunks enter the row task as separate terms (no
+// reduction step).  A row task waits for the projections of two leaves back: a
+// block whose columns end at leaf k-1 has no rows at leaf k (admissibility gap).
+void apply_gemm_path(fde_ctx* h, ApplySched* A, double* x, int64_t ldx, int nrhs)
+{
+    cudaStream_t s = h->stream, sp = aux_stream6(h);
+    if ((size_t)A->zmax * nrhs > A->zcap) {
+        A->z.alloc((size_t)A->zmax * nrhs);
+        A->zcap = (size_t)A->zmax * nrhs;
+    }
+    if ((size_t)A->tslots * nrhs > A->tcap) {
+        A->t.alloc((size_t)A->tslots * nrhs);
+        A->tcap = (size_t)A->tslots * nrhs;
+    }
+    const int nl = A->nleaf;
+    if ((int)A->gev.size() < nl + 1) {
+        for (auto e : A->gev)
+            if (e) cudaEventDestroy(e);
+        A->gev.assign(nl + 1, nullptr);
+        for (auto& e : A->gev) FDE_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    double* Tb = A->t.p;
+    double* Z = A->z.p;
+    // descriptors: per sweep and leaf, three launches (row task, inverse task, projections)
+    std::vector<H2Task> tasks;
+    std::vector<H2Term> terms;
+    std::vector<H2Tile> tiles;
+    struct Rng { int t0, nt; };
+    std::vector<Rng> rrow, rinv, rproj;   // [sweep * nl + step]
+    auto add_task = [&](double* C, long long ldc, int m, int n, double beta, int tm, int tn) {
+        H2Task d;
+        d.C = C;
+        d.ldc = ldc;
+        d.m = m;
+        d.n = n;
+        d.beta = beta;
+        d.t_lo = (int)terms.size();
+        d.t_hi = d.t_lo;
+        tasks.push_back(d);
+        (void)tm;
+        (void)tn;
+        return (int)tasks.size() - 1;
+    };
+    auto add_tiles = [&](int ti, int tm, int tn) {
+        for (int m0 = 0; m0 < tasks[ti].m; m0 += tm)
+            for (int n0 = 0; n0 < tasks[ti].n; n0 += tn) tiles.push_back({ti, m0, n0});
+    };
+    for (int w = 0; w < 2; ++w) {
+        const std::vector<SLeaf>& LV = A->hleaf[w];
+        const std::vector<SDense>& DV = A->hdense[w];
+        const std::vector<SLRRow>& RV = A->hlrr[w];
+        const std::vector<SProj>& PV = A->hproj[w];
+        for (int st = 0; st < nl; ++st) {
+            const int k = w ? nl - 1 - st : st;
+            const SLeaf& L = LV[k];
+            // row task (in place on the leaf's rows)
+            {
+                const int t0 = (int)tiles.size();
+                const int ti = add_task(x + L.r0, ldx, L.m, nrhs, 1.0, 64, 64);
+                for (int d = L.d_lo; d < L.d_hi; ++d) {
+                    const SDense& D = DV[d];
+                    terms.push_back({D.D + D.roff, x + D.c0, D.ldd, ldx, D.nc, 0, 0, -1.0});
+                }
+                for (int l = L.l_lo; l < L.l_hi; ++l) {
+                    const SLRRow& R = RV[l];
+                    for (int ch = 0; ch < R.nchunk; ++ch)
+                        terms.push_back({R.U + R.roff, Tb + (long long)(R.tslot + ch * R.kc) * nrhs, R.ldu, R.kc,
+                                         R.kc, 0, 0, -1.0});
+                }
+                tasks[ti].t_hi = (int)terms.size();
+                add_tiles(ti, 32, 32);
+                rrow.push_back({t0, (int)tiles.size() - t0});
+            }
+            // inverse task: z = Inv_k x_k
+            {
+                const int t0 = (int)tiles.size();
+                const int ti = add_task(Z, L.m, L.m, nrhs, 0.0, 64, 64);
+                terms.push_back({L.inv, x + L.r0, L.m, ldx, L.m, 0, 0, 1.0});
+                tasks[ti].t_hi = (int)terms.size();
+                add_tiles(ti, 32, 32);
+                rinv.push_back({t0, (int)tiles.size() - t0});
+            }
+            // projections enabled by this leaf: T_{b, ch} = V_b[ch]^T x_sigma[ch]
+            {
+                const int t0 = (int)tiles.size();
+                for (int p = L.p_lo; p < L.p_hi; ++p) {
+                    const SProj& Pj = PV[p];
+                    for (int ch = 0; ch < Pj.nchunk; ++ch) {
+                        const int r0 = ch * PROJ_CHUNK, rows = std::min(PROJ_CHUNK, Pj.n - r0);
+                        const int ti = add_task(Tb + (long long)(Pj.tslot + ch * Pj.kc) * nrhs, Pj.kc, Pj.kc, nrhs, 0.0,
+                                                16, 16);
+                        terms.push_back({Pj.V + r0, x + Pj.c0 + r0, Pj.ldv, ldx, rows, 1, 0, 1.0});
+                        tasks[ti].t_hi = (int)terms.size();
+                        add_tiles(ti, 16, 16);
+                    }
+                }
+                rproj.push_back({t0, (int)tiles.size() - t0});
+            }
+        }
+    }
+    DBuf<H2Task> dtask;
+    DBuf<H2Term> dterm;
+    DBuf<H2Tile> dtile;
+    dtask.upload(tasks.data(), tasks.size(), s);
+    dterm.upload(terms.data(), terms.size(), s);
+    dtile.upload(tiles.data(), tiles.size(), s);
+    set_smem_once((const void*)k_h2_gemm<32, 32, true>, H2G_SMEM(32, 32));
+    set_smem_once((const void*)k_h2_gemm<16, 16, true>, H2G_SMEM(16, 16));
+    cudaEvent_t evx = h->ev_aux[14];   // (the H-LU's neighbour-panel event: free outside the factorisation)
+    FDE_CUDA(cudaEventRecord(evx, s));
+    FDE_CUDA(cudaStreamWaitEvent(sp, evx, 0));
+    for (int w = 0; w < 2; ++w)
+        for (int st = 0; st < nl; ++st) {
+            const int q = w * nl + st;
+            const int k = w ? nl - 1 - st : st;
+            const SLeaf& L = A->hleaf[w][k];
+            if (st >= 2) FDE_CUDA(cudaStreamWaitEvent(s, A->gev[st - 2], 0));
+            if (rrow[q].nt)
+                k_h2_gemm<32, 32, true><<<rrow[q].nt, 256, H2G_SMEM(32, 32), s>>>(dtile.p + rrow[q].t0, dtask.p, dterm.p,
+                                                                                 rrow[q].nt);
+            FDE_CHECK_LAUNCH();
+            k_h2_gemm<32, 32, true><<<rinv[q].nt, 256, H2G_SMEM(32, 32), s>>>(dtile.p + rinv[q].t0, dtask.p, dterm.p,
+                                                                             rinv[q].nt);
+            FDE_CHECK_LAUNCH();
+            FDE_CUDA(cudaMemcpy2DAsync(x + L.r0, (size_t)ldx * sizeof(double), Z, (size_t)L.m * sizeof(double),
+                                       (size_t)L.m * sizeof(double), (size_t)nrhs, cudaMemcpyDeviceToDevice, s));
+            FDE_CUDA(cudaEventRecord(evx, s));
+            FDE_CUDA(cudaStreamWaitEvent(sp, evx, 0));
+            if (rproj[q].nt) {
+                k_h2_gemm<16, 16, true><<<rproj[q].nt, 256, H2G_SMEM(16, 16), sp>>>(dtile.p + rproj[q].t0, dtask.p,
+                                                                                   dterm.p, rproj[q].nt);
+                FDE_CHECK_LAUNCH();
+            }
+            FDE_CUDA(cudaEventRecord(A->gev[st], sp));
+        }
+    FDE_CUDA(cudaEventRecord(A->gev[nl], sp));
+    FDE_CUDA(cudaStreamWaitEvent(s, A->gev[nl], 0));
+}

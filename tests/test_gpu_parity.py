@@ -254,12 +254,15 @@ def test_hlu_deferred_updates_exact_mode(fde, h, case, monkeypatch):
         o.free()
 
 
+@pytest.mark.parametrize("gemm_path", [False, True], ids=["tiles", "gemm-tasks"])
 @pytest.mark.parametrize("nrhs", [9, 19, 64])
-def test_hlu_apply_many_rhs_equals_dense_solve_of_Atilde(fde, h, nrhs):
+def test_hlu_apply_many_rhs_equals_dense_solve_of_Atilde(fde, h, nrhs, gemm_path, monkeypatch):
     """precond_apply with more right-hand sides than the register chunk (nrhs > 8:
     8 x 8 output tiles of rows x RHS, ragged at 9 and 19) against the dense solve
     with the oracle's A~ in exact mode (tol = 0), like the two-RHS test above."""
     p, n_min = fi.config4(N=96, P=8), 4   # 24 leaves, several low-rank levels
+    if gemm_path:   # the opt-in multi-term GEMM-task substitutions (nrhs >= 16)
+        monkeypatch.setenv("FDE_APPLY_GEMM_MIN", "16")
     op = fde.assemble_problem(h, p)
     hm = fde.hmatrix_build(h, op, p.R, 1.0, n_min)
     lu = fde.hlu_factor(h, hm, 0.0)
