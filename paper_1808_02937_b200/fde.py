@@ -223,7 +223,10 @@ class Operator:
             self.ptr = None
 
     def __del__(self):
-        self.free()
+        try:
+            self.free()
+        except Exception:   # interpreter shutdown: module globals already cleared
+            pass
 
 
 def sem_assemble(handle: Handle, a, b, alpha, theta, rho, c1, c2, nodes: np.ndarray, P: int,
@@ -312,7 +315,10 @@ class HMatrix:
             self.ptr = None
 
     def __del__(self):
-        self.free()
+        try:
+            self.free()
+        except Exception:   # interpreter shutdown: module globals already cleared
+            pass
 
 
 def hmatrix_build(handle: Handle, op: Operator, R: int, lam: float = 1.0, n_min: int = 16) -> HMatrix:
@@ -341,7 +347,10 @@ class HLU:
             self.ptr = None
 
     def __del__(self):
-        self.free()
+        try:
+            self.free()
+        except Exception:   # interpreter shutdown: module globals already cleared
+            pass
 
 
 def hlu_factor(handle: Handle, hm: HMatrix, tol: float = 1e-3) -> HLU:
