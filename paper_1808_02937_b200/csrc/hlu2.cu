@@ -1479,10 +1479,19 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
     int gemm_shape[6] = {rmax <= 16 ? 3 : 1, rmax <= 16 ? 2 : 0, 0, 0, 0, 1};
     if (const char* e = getenv("FDE_H2_SHAPES"))   // debug: six digits
         for (int w = 0; w < 6 && e[w]; ++w) gemm_shape[w] = (e[w] - '0') & 3;
-    auto put_gemm = [&](const std::vector<VTask>& v, H2Launch& ln, int which, int shape) {
+    const bool plan_stats = getenv("FDE_DEBUG_PLAN") != nullptr;
+    // tasks of v (then v2) with sel[q] == want (sel null: all), in order
+    auto put_gemm_sel = [&](const std::vector<VTask>& v, const std::vector<char>* sel, char want, H2Launch& ln,
+                            int which, int shape, const std::vector<VTask>* v2 = nullptr,
+                            const std::vector<char>* sel2 = nullptr) {
         ln.g_shape[which] = shape;
         ln.g_tile0[which] = (int)vtile.size();
-        for (auto& t : v) {
+        static const int shm[4] = {64, 32, 128, 16}, shn[4] = {64, 32, 16, 16};
+        const int tm = shm[shape], tn = shn[shape];
+        const size_t n1 = v.size(), n2 = v2 ? v2->size() : 0;
+        for (size_t q = 0; q < n1 + n2; ++q) {
+            if (q < n1 ? (sel && (*sel)[q] != want) : (*sel2)[q - n1] != want) continue;
+            const VTask& t = q < n1 ? v[q] : (*v2)[q - n1];
             H2Task d;
             d.C = res(t.C);
             d.ldc = t.ldc;
@@ -1493,16 +1502,19 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
             for (auto& q : t.terms)
                 vterm.push_back({res(q.A), res(q.B), q.lda, q.ldb, q.k, q.ta, q.tb, q.alpha});
             d.t_hi = (int)vterm.size();
-            for (auto& q : t.terms) gstat_flop[which] += 2.0 * t.m * t.n * q.k;
-            gstat_cbytes[which] += 16.0 * t.m * t.n;
+            if (plan_stats) {
+                for (auto& q : t.terms) gstat_flop[which] += 2.0 * t.m * t.n * q.k;
+                gstat_cbytes[which] += 16.0 * t.m * t.n;
+            }
             const int ti = (int)vtask.size();
             vtask.push_back(d);
-            static const int shm[4] = {64, 32, 128, 16}, shn[4] = {64, 32, 16, 16};
-            const int tm = shm[shape], tn = shn[shape];
             for (int m0 = 0; m0 < t.m; m0 += tm)
                 for (int n0 = 0; n0 < t.n; n0 += tn) vtile.push_back({ti, m0, n0});
         }
         ln.g_ntile[which] = (int)vtile.size() - ln.g_tile0[which];
+    };
+    auto put_gemm = [&](const std::vector<VTask>& v, H2Launch& ln, int which, int shape) {
+        put_gemm_sel(v, nullptr, 0, ln, which, shape);
     };
     auto put_copy = [&](const std::vector<VCopy>& v, H2Launch& ln) {
         ln.cp0 = (int)vcp.size();
@@ -1878,6 +1890,7 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
     std::vector<cudaEvent_t> tev;
     std::vector<double> thost;
     double eq_us[3] = {0, 0, 0};   // host: flatten, push, launches (timeline mode)
+    double fl_us[3] = {0, 0, 0};   // flatten: plan lists, dense-target expansion, split + dense tasks
     const auto th0 = std::chrono::steady_clock::now();
     cudaEvent_t t0ev = nullptr;
     if (tline) {
@@ -1888,6 +1901,8 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
     }
     std::vector<int> xtile_stamp((size_t)nl * nl, 0), xtile_task((size_t)nl * nl, 0);   // (flatten-time tile -> task)
     int xtile_stamp_id = 0;
+    std::vector<VTask> xg3;    // the expanded dense-target tasks of the current step (capacity reused)
+    std::vector<char> xg3c;
     auto mark = [&](int k, int w, cudaStream_t st) {
         if (tline) FDE_CUDA(cudaEventRecord(tev[(size_t)k * T_N + w], st));
     };
@@ -1926,6 +1941,9 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
                 put_trunc(st.trmid[r], ln.trmid.back());
             }
         }
+        const auto tf1 = std::chrono::steady_clock::now();
+        xg3.clear();
+        xg3c.clear();
         if (!st.dts.empty()) {   // expand the compact dense-target work of the plan (same order as before)
             ++xtile_stamp_id;
             const int sid = st.sid, mk = st.mk;
@@ -1938,11 +1956,11 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
                         const size_t key = (size_t)i * nl + j;
                         int ti;
                         if (xtile_stamp[key] != xtile_stamp_id) {
-                            ti = (int)st.g3.size();
+                            ti = (int)xg3.size();
                             xtile_stamp[key] = xtile_stamp_id;
                             xtile_task[key] = ti;
-                            st.g3.push_back(VTask{{0, t, (lr0[j] - col0(t)) * T.m + (lr0[i] - row0(t))}, T.m, lm(i), lm(j), 1.0, {}});
-                            st.g3crit.push_back((i == k + 1 && j == k + 1) ? 2
+                            xg3.push_back(VTask{{0, t, (lr0[j] - col0(t)) * T.m + (lr0[i] - row0(t))}, T.m, lm(i), lm(j), 1.0, {}});
+                            xg3c.push_back((i == k + 1 && j == k + 1) ? 2
                                                 : (i == k + 1 || j == k + 1 || (i == k + 2 && j == k + 2)));
                         } else {
                             ti = xtile_task[key];
@@ -1958,20 +1976,27 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
                             term = {{3, sid, dp.w + (lr0[i] - row0(b))}, {3, sid, dp.sv + (lr0[j] - col0(c))}, B.m, C.n,
                                     dp.kcc, 0, 1, -1.0};
                         }
-                        st.g3[ti].terms.push_back(term);
+                        xg3[ti].terms.push_back(term);
                     }
             }
         }
+        const auto tf2 = std::chrono::steady_clock::now();
+        if (tline) {
+            fl_us[0] += std::chrono::duration<double, std::micro>(tf1 - te0).count();
+            fl_us[1] += std::chrono::duration<double, std::micro>(tf2 - tf1).count();
+        }
         {   // split the dense updates: row / column k+1 (needed by step k+1) vs the rest
-            std::vector<VTask> diag, crit, rest;
-            for (size_t q = 0; q < st.g3.size(); ++q)
-                (st.g3crit[q] == 2 ? diag : st.g3crit[q] ? crit : rest).push_back(std::move(st.g3[q]));
+            // (selected in place: no task moves)
             ln.diag_scr = false;
-            for (auto& t : diag)
-                for (auto& tm : t.terms) ln.diag_scr |= tm.A.sp == 3 || tm.B.sp == 3;
-            put_gemm(crit, ln, 2, gemm_shape[2]);
-            put_gemm(rest, ln, 4, gemm_shape[4]);
-            put_gemm(diag, ln, 5, gemm_shape[5]);
+            for (size_t q = 0; q < st.g3.size(); ++q)
+                if (st.g3crit[q] == 2)
+                    for (auto& tm : st.g3[q].terms) ln.diag_scr |= tm.A.sp == 3 || tm.B.sp == 3;
+            for (size_t q = 0; q < xg3.size(); ++q)
+                if (xg3c[q] == 2)
+                    for (auto& tm : xg3[q].terms) ln.diag_scr |= tm.A.sp == 3 || tm.B.sp == 3;
+            put_gemm_sel(st.g3, &st.g3crit, 1, ln, 2, gemm_shape[2], &xg3, &xg3c);
+            put_gemm_sel(st.g3, &st.g3crit, 0, ln, 4, gemm_shape[4], &xg3, &xg3c);
+            put_gemm_sel(st.g3, &st.g3crit, 2, ln, 5, gemm_shape[5], &xg3, &xg3c);
         }
         const auto te1 = std::chrono::steady_clock::now();
         push();
@@ -2109,8 +2134,9 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         fprintf(stderr, "hlu2 timeline (%d steps): per-step period of each mark (us):", kstop);
         for (int w = 0; w < T_N; ++w) fprintf(stderr, " %s %.1f |", nm[w], 1e3 * sum[w] / std::max(1, kstop - 1));
         if (kstop > 1)
-            fprintf(stderr, " host enqueue %.1f (flatten %.1f, push %.1f, launches %.1f) |",
-                    (thost.back() - thost.front()) / (kstop - 1), eq_us[0] / kstop, eq_us[1] / kstop, eq_us[2] / kstop);
+            fprintf(stderr, " host enqueue %.1f (flatten %.1f [lists %.1f, expansion %.1f, split %.1f], push %.1f, launches %.1f) |",
+                    (thost.back() - thost.front()) / (kstop - 1), eq_us[0] / kstop, fl_us[0] / kstop, fl_us[1] / kstop,
+                    (eq_us[0] - fl_us[0] - fl_us[1]) / kstop, eq_us[1] / kstop, eq_us[2] / kstop);
         fprintf(stderr, "\n  step 10 marks (ms from start):");
         for (int w = 0; w < T_N && kstop > 10; ++w) {
             float ms = 0;
