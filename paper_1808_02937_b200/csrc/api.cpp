@@ -132,6 +132,8 @@ void fde_destroy(fde_handle h)
         cudaStreamDestroy(h->aux5);
         cudaStreamSynchronize(h->aux6);
         cudaStreamDestroy(h->aux6);
+        cudaStreamSynchronize(h->aux7);
+        cudaStreamDestroy(h->aux7);
         cudaStreamDestroy(h->aux);
         cudaStreamDestroy(h->aux2);
         cudaStreamDestroy(h->aux3);

@@ -145,8 +145,9 @@ struct fde_ctx {
     // auxiliary stream + events for work that overlaps the caller's stream
     // (created on first use; ordered by events, never by implicit synchronisation)
     int* pinned = nullptr;   // small page-locked read-back buffer (allocated once per handle)
-    cudaStream_t aux = nullptr, aux2 = nullptr, aux3 = nullptr, aux4 = nullptr, aux5 = nullptr, aux6 = nullptr;
-    cudaEvent_t ev_aux[16] = {};
+    cudaStream_t aux = nullptr, aux2 = nullptr, aux3 = nullptr, aux4 = nullptr, aux5 = nullptr, aux6 = nullptr,
+                 aux7 = nullptr;
+    cudaEvent_t ev_aux[20] = {};
     void* stage = nullptr;   // page-locked staging of descriptor uploads (grow-only)
     size_t stage_bytes = 0;
     // upload ring (fde_ring_upload): two halves; a half is reused after the event
@@ -196,6 +197,7 @@ inline cudaStream_t aux_stream(fde_ctx* h)
         FDE_CUDA(cudaStreamCreateWithPriority(&h->aux4, cudaStreamNonBlocking, hi));
         FDE_CUDA(cudaStreamCreateWithPriority(&h->aux5, cudaStreamNonBlocking, hi));
         FDE_CUDA(cudaStreamCreateWithPriority(&h->aux6, cudaStreamNonBlocking, hi));
+        FDE_CUDA(cudaStreamCreateWithPriority(&h->aux7, cudaStreamNonBlocking, hi));
         for (auto& e : h->ev_aux) FDE_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
     return h->aux;
@@ -224,6 +226,11 @@ inline cudaStream_t aux_stream6(fde_ctx* h)
 {
     aux_stream(h);
     return h->aux6;
+}
+inline cudaStream_t aux_stream7(fde_ctx* h)
+{
+    aux_stream(h);
+    return h->aux7;
 }
 
 // ------------------------------------------------------- quadrature tables

@@ -89,6 +89,9 @@ __device__ __forceinline__ void cp_async8(double* sdst, const double* gsrc)
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gsrc));
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
+__device__ __forceinline__ void cp_async_commit_group() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait_group() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 // LU without pivoting of an m x m tile (m <= 128), right-looking in shared memory
 // with all 512 threads: thread (ti, tj) updates rows k+1+ti+32a and columns
@@ -249,8 +252,9 @@ __device__ __forceinline__ double h2_tp(const double* Ts, int ldT, int i, int j)
 template <int MODE>
 __device__ void h2_panel_inv_body(const H2Panel& p, double* psm)
 {
-    // op is staged in chunks of H2_PCH columns (small shared footprint: the CTA
-    // has to fit beside the bulk-update GEMMs of the previous step)
+    // op is staged in chunks of H2_PCH columns, double-buffered (the next chunk's
+    // copies are in flight while one is multiplied; small shared footprint: the
+    // CTA has to fit beside the bulk-update GEMMs of the previous step)
     const int m = p.m, ldT = (m & 1) ? m + 2 : m + 1, ldB = ldT;
     double* Bs = psm;                 // vector c, element i at Bs[c * ldB + i]
     double* Ts = psm + H2_STRIP * ldB;   // Ts[qq * ldT + i] = op(i, q0 + qq)
@@ -277,25 +281,37 @@ __device__ void h2_panel_inv_body(const H2Panel& p, double* psm)
     for (int a = 0; a < 4; ++a) ia[a] = min(lane + 32 * a, m - 1);
 #pragma unroll
     for (int u = 0; u < 4; ++u) cu[u] = min(w + 8 * u, nv - 1);
-    for (int q0 = 0; q0 < m; q0 += H2_PCH) {
+    auto stage = [&](int q0, double* Tb) {
         const int nq = min(H2_PCH, m - q0);
         if (MODE == 0) {   // op(i, q) = Ti(i, q): columns q0.. of Ti
             for (int t = tid; t < nq * m; t += 256) {
                 const int i = t % m, qq = t / m;
-                cp_async8(Ts + qq * ldT + i, p.Ti + (long long)(q0 + qq) * p.ldi + i);
+                cp_async8(Tb + qq * ldT + i, p.Ti + (long long)(q0 + qq) * p.ldi + i);
             }
         } else {           // op(i, q) = Ti(q, i): rows q0.. of Ti
             for (int t = tid; t < nq * m; t += 256) {
                 const int qq = t % nq, i = t / nq;
-                cp_async8(Ts + qq * ldT + i, p.Ti + (long long)i * p.ldi + q0 + qq);
+                cp_async8(Tb + qq * ldT + i, p.Ti + (long long)i * p.ldi + q0 + qq);
             }
         }
-        cp_async_wait_all();
+    };
+    stage(0, Ts);
+    cp_async_commit_group();   // (with the vectors)
+    for (int q0 = 0, c = 0; q0 < m; q0 += H2_PCH, ++c) {
+        const int nq = min(H2_PCH, m - q0);
+        double* Tc = Ts + (c & 1) * H2_PCH * ldT;
+        if (q0 + H2_PCH < m) {
+            stage(q0 + H2_PCH, Ts + ((c + 1) & 1) * H2_PCH * ldT);
+            cp_async_commit_group();
+            cp_async_wait_group<1>();
+        } else {
+            cp_async_wait_group<0>();
+        }
         __syncthreads();
         for (int qq = 0; qq < nq; ++qq) {
             double o[4], x[4];
 #pragma unroll
-            for (int a = 0; a < 4; ++a) o[a] = Ts[qq * ldT + ia[a]];
+            for (int a = 0; a < 4; ++a) o[a] = Tc[qq * ldT + ia[a]];
 #pragma unroll
             for (int u = 0; u < 4; ++u) x[u] = Bs[cu[u] * ldB + q0 + qq];
 #pragma unroll
@@ -463,9 +479,6 @@ __device__ __forceinline__ void h2_stage(const H2Term& T, int m0, int n0, int m,
         else *db = 0.0;
     }
 }
-__device__ __forceinline__ void cp_async_commit_group() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait_group() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 // warp grid of the DMMA path (8 x 8 fragments of mma.sync.m8n8k4.f64): WM x WN warps
 template <int TM, int TN> struct H2Warps {
@@ -651,6 +664,15 @@ __global__ void __launch_bounds__(256) k_h2_copy(const H2Copy* C)
     }
 }
 
+__global__ void k_h2_spin(long long us)   // (debug FDE_H2_HOLD_US)
+{
+    unsigned long long t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    do {
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    } while (t - t0 < (unsigned long long)us * 1000ull);
+}
+
 // ------------------------------------------------------------------ plan
 // Pointers are resolved after the arena layout is known: a reference is
 // (space, id, offset): space 0 = dense block id, 1 = U of block id, 2 = V of
@@ -821,6 +843,9 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
     const HStruct& S = L->S;
     const bool trunc = L->tol > 0.0;
     static const bool pan_inv = !getenv("FDE_H2_PANEL_SUBST");
+    // neighbour-tile panels by substitution on the LU stream, so the tile inverses
+    // (needed by the other panels only) run beside them on a stream of their own
+    static const bool np_subst = pan_inv && getenv("FDE_H2_NP_INV") == nullptr;   // (FDE_H2_NP_INV: old order)
     static const bool split_np = !getenv("FDE_H2_NOSPLIT");
     // deferred dense updates: a dense tile (i, j) gets the terms of the steps before
     // min(i, j) - 1 in ONE multi-term task at step min(i, j) - 2 (one read / write of
@@ -1019,6 +1044,7 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
             const int f = leaf_of[k];
             for (auto* pl : {&st.panel, &st.npanel})
                 for (auto& pv : *pl) {
+                    if (np_subst && pl == &st.npanel) continue;
                     pv.Ti = {pv.mode == 0 ? 4 : 5, f, ioff(f, k, k)};
                     pv.ldi = lfm(f);
                 }
@@ -1706,6 +1732,8 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
     cudaEvent_t evPan = L->h->ev_aux[12], evSnap = L->h->ev_aux[13];
     cudaEvent_t evNP = L->h->ev_aux[14], evCrit = L->h->ev_aux[15];
     cudaStream_t se = aux_stream6(L->h);   // overflow truncations
+    cudaStream_t si = aux_stream7(L->h);   // tile inverses (np_subst)
+    cudaEvent_t evLUo = L->h->ev_aux[16], evInv = L->h->ev_aux[17];
     // debug: fold auxiliary streams back onto the critical one (race bisection)
     if (const char* f = getenv("FDE_H2_FOLD")) {
         const std::string fs(f);
@@ -1743,7 +1771,7 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
     // of step k, which overlap LU(k+1) and the panels of step k+1 (lookahead).
     const int pan_smem = (H2_MMAX + H2_STRIP) * (H2_MMAX + 2) * (int)sizeof(double);
     set_smem_once((const void*)k_h2_panel, pan_smem);
-    const int pan_smem_inv = (H2_STRIP + H2_PCH) * (H2_MMAX + 2) * (int)sizeof(double);
+    const int pan_smem_inv = (H2_STRIP + 2 * H2_PCH) * (H2_MMAX + 2) * (int)sizeof(double);   // (double-buffered op)
     const int lu_smem = H2_MMAX * (H2_MMAX + 1) * (int)sizeof(double);   // padded 128 x 129
     set_smem_once((const void*)k_h2_lu, lu_smem);
     static const bool use_dmma = !getenv("FDE_H2_NODMMA");
@@ -1817,9 +1845,16 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         else k_h2_lu_reg<<<1, 512, 0, st>>>(t, L->dflag.p);
         FDE_CHECK_LAUNCH();
         if (P->steps[kk].npi) {
-            k_h2_panel<<<P->steps[kk].npi, 256, pan_smem, st>>>(P->pan.p + P->steps[kk].pi0);
+            cudaStream_t sv = st;
+            if (np_subst) {
+                FDE_CUDA(cudaEventRecord(evLUo, st));
+                FDE_CUDA(cudaStreamWaitEvent(si, evLUo, 0));
+                sv = si;
+            }
+            k_h2_panel<<<P->steps[kk].npi, 256, pan_smem, sv>>>(P->pan.p + P->steps[kk].pi0);
             FDE_CHECK_LAUNCH();
             ++nlaunch;
+            if (np_subst) FDE_CUDA(cudaEventRecord(evInv, si));
         }
     };
     int gemm_cap[6];
@@ -1874,6 +1909,10 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
     FDE_CUDA(cudaMemsetAsync(A + lr_lo, 0, (size_t)(lr_hi - lr_lo) * sizeof(double), sa));
     if (pan_inv) FDE_CUDA(cudaMemsetAsync(A + inv_lo, 0, (size_t)(inv_hi - inv_lo) * sizeof(double), sa));
     FDE_CUDA(cudaStreamWaitEvent(sa, evD, 0));
+    if (const char* e = getenv("FDE_H2_HOLD_US")) {   // debug: hold the device while the host enqueues
+        k_h2_spin<<<1, 1, 0, sa>>>(atoll(e));          // (the timeline then shows the device-bound period)
+        FDE_CHECK_LAUNCH();
+    }
     run_copy(P->init, sa);
     run_trunc(P->init.tr, sa, 0);
     FDE_CUDA(cudaEventRecord(evA, sa));
@@ -2033,6 +2072,7 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
             FDE_CUDA(cudaEventRecord(evLU, sl));
         }
         FDE_CUDA(cudaStreamWaitEvent(sa, evLU, 0));
+        if (np_subst) FDE_CUDA(cudaStreamWaitEvent(sa, evInv, 0));
         FDE_CUDA(cudaStreamWaitEvent(sa, evOp, 0));
         auto diag_lu = [&](cudaStream_t st) {   // tile (k+1, k+1), then LU(k+1) on sl
             run_gemm(ln, 5, st);
@@ -2053,7 +2093,7 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         // (sa has captured evLU = LU(k) above; LU(k+1) may be recorded from here on)
         if (ln.nnp) {   // neighbour-tile panels, tile (k+1, k+1), LU(k+1): all on the LU stream
             FDE_CUDA(cudaStreamWaitEvent(sl, evCrit, 0));   // row / column k updated by step k-1
-            k_h2_panel<<<ln.nnp, 256, pan_inv ? pan_smem_inv : pan_smem, sl>>>(P->pan.p + ln.np0);
+            k_h2_panel<<<ln.nnp, 256, (pan_inv && !np_subst) ? pan_smem_inv : pan_smem, sl>>>(P->pan.p + ln.np0);
             FDE_CHECK_LAUNCH();
             ++nlaunch;
             dbg("neighbour panels");
