@@ -1169,6 +1169,24 @@ __global__ void __launch_bounds__(256) k_bcore(const TEntry* E, const TChunk* C,
         const int ia = piv[a];
         Tv[c * k + cm[idx[ia]]] = sv / sig * sc[ia];
     }
+    if (ru <= 32) {   // one warp per kept column, lane = row: ru steps of one shuffle each
+        const int lane = threadIdx.x & 31;
+        for (int c = threadIdx.x >> 5; c < r; c += blockDim.x >> 5) {
+            const int col = ord[c];
+            const double sig = sqrt(fmax(X[col * n2 + col], 0.0));
+            double b = (lane < ru) ? Eu[col * n2 + lane] * sig : 0.0, y = 0.0;
+            for (int a = ru - 1; a >= 0; --a) {
+                const double ya = __shfl_sync(0xffffffffu, b, a) / A[a * n + a];
+                if (lane == a) y = ya;
+                if (lane < a) b = fma(-A[a * n + lane], ya, b);
+            }
+            for (int a = lane; a < ke; a += 32) {
+                const int ia = piv[a];
+                Tu[c * k + cm[idx[ia]]] = (a < ru ? y : 0.0) / sc[ia];
+            }
+        }
+        return;
+    }
     for (int c = threadIdx.x; c < r; c += blockDim.x) {
         const int col = ord[c];
         const double sig = sqrt(fmax(X[col * n2 + col], 0.0));
