@@ -753,6 +753,7 @@ __device__ __forceinline__ bool h2_chk(const void* p, long long nbytes, int tag,
 }
 
 __device__ unsigned long long g_trunc_stats[4];
+__device__ double g_trunc_jeps = 0.0;   // (debug FDE_TRUNC_JEPS)
 __device__ int g_trunc_check = 0;   // descriptor checks (FDE_DEBUG_SERIAL)   // calls, sum ke, sum sweeps, max ke
 
 // Truncation core (one CTA).  Input: Gram matrices Gu = U^T U, Gv = V^T V of a
@@ -1046,7 +1047,9 @@ __global__ void __launch_bounds__(256) k_bcore(const TEntry* E, const TChunk* C,
     // (and, then, off-diagonal entries below 1e-14 ||A||_F, the rounding noise
     // the rotations themselves leave behind, are not rotated: with a wide
     // eigenvalue range the relative test alone never stops)
-    const double jeps = (tol >= 1e-6) ? 1e-12 : 1e-15, jarel = (tol >= 1e-6) ? 1e-14 : 1e-16;
+    // (FDE_TRUNC_JEPS: debug override of the relative rotation threshold)
+    const double jeps = g_trunc_jeps > 0.0 ? g_trunc_jeps : (tol >= 1e-6) ? 1e-12 : 1e-15,
+                 jarel = (tol >= 1e-6) ? 1e-14 : 1e-16;
     // Factor of the scaled Gram by pivoted Cholesky, D Gu D = P R^T R P^T (R: ru x ke,
     // upper trapezoidal in pivoted order; pivots below 1e-14 of the unit diagonal --
     // nearly dependent columns -- end it), in place in A: ke sequential steps

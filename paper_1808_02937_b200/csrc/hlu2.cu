@@ -1798,6 +1798,8 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
     {
         const int chk = dbg_serial ? 1 : 0;
         FDE_CUDA(cudaMemcpyToSymbolAsync(g_trunc_check, &chk, sizeof(int), 0, cudaMemcpyHostToDevice, sa));
+        static const double jeps = getenv("FDE_TRUNC_JEPS") ? atof(getenv("FDE_TRUNC_JEPS")) : 0.0;
+        FDE_CUDA(cudaMemcpyToSymbolAsync(g_trunc_jeps, &jeps, sizeof(double), 0, cudaMemcpyHostToDevice, sa));
     }
     int dbg_step = -1;
     auto dbg = [&](const char* what) {
