@@ -82,10 +82,11 @@ def geometric_mesh(a: float, b: float, N: int, qhat: float) -> np.ndarray:
     """h_{i+1} = qhat h_i."""
     if qhat == 1.0:
         return uniform_mesh(a, b, N)
-    h1 = (b - a) * (1 - qhat) / (1 - qhat ** N)
-    h = h1 * qhat ** np.arange(N)
-    x = np.concatenate([[a], a + np.cumsum(h)])
-    x[-1] = b
+    # every node from its own power (not a running sum): relative spacing errors
+    # stay at rounding level for long meshes
+    k = np.arange(N + 1, dtype=np.float64)
+    x = a + (b - a) * np.expm1(k * np.log(qhat)) / np.expm1(N * np.log(qhat))
+    x[0], x[-1] = a, b
     return x
 
 
@@ -181,6 +182,15 @@ def config2(alpha: float = 1.5, seed: Optional[int] = None, N: int = 256, P: int
         seed = {1.2: 0, 1.5: 1, 1.8: 2}.get(alpha, 0)
     return Problem(f"c2-a{alpha}-N{N}-P{P}", 0.0, 1.0, alpha, 0.3, 1.0, 0.5, -1.0, uniform_mesh(0, 1, N), P, 8,
                    forcings=[random_legendre_forcing(seed)], mesh_kind="uniform")
+
+
+def geometric_problem(qhat: float, N: int = 64, P: int = 8, alpha: float = 1.5, theta: float = 0.3,
+                      rho: float = 1.0, seed: int = 0) -> Problem:
+    """Single-ratio geometric mesh on (0, 1) (h_{i+1} = qhat h_i): the
+    paper's second structured case for the Toeplitz matvec."""
+    return Problem(f"geo-q{qhat}-N{N}-P{P}-a{alpha}", 0.0, 1.0, alpha, theta, rho, 0.0, 0.0,
+                   geometric_mesh(0, 1, N, qhat), P, 8, forcings=[random_legendre_forcing(seed)],
+                   mesh_kind="geometric")
 
 
 def config3(P: int = 16) -> Problem:

@@ -134,8 +134,11 @@ enum { FDE_OP_DENSE = 1, FDE_OP_TOEPLITZ = 2 };
 /* Builds the operator A = rho M + theta S_l + (1-theta) S_l^T of Eq. (lsys)
  * on the device.  FDE_OP_DENSE stores this rank's row shard
  * of the dense fp64 matrix (element-interleaved internal order, row-major);
- * FDE_OP_TOEPLITZ (uniform meshes only) stores the P x P block-Toeplitz lag
- * symbols and their 2N-point circulant spectra.  Both may be
+ * FDE_OP_TOEPLITZ stores the P x P block-Toeplitz lag symbols and their
+ * 2N-point circulant spectra: on uniform meshes, and on
+ * single-ratio geometric meshes (h_{e+1} = q h_e for every element to 1e-10,
+ * PAPER.md:632-735; there K_ij = (h_j/h_0)^{1-alpha} K_{i-j,0}, two spectral
+ * passes); any other mesh fails with FDE_EUNSUPPORTED_MESH.  Both may be
  * requested together.  Entries are computed by Gauss quadrature of the pair
  * moments K_ij[m][n] = gamma0 int int L_m L_n (t-s)_+^{1-alpha} with
  * Gauss-Jacobi / Duffy treatment of the diagonal and touching pairs and graded

@@ -263,9 +263,18 @@ int sem_assemble(fde_handle h, const fde_problem* prob, const fde_mesh* mesh, in
         for (int i = 0; i < op->N; ++i)
             if (std::fabs((op->nodes_h[i + 1] - op->nodes_h[i]) - h0) > 1e-12 * h0) uni = false;
         op->uniform = uni;
+        // one geometric progression of element sizes: the pair
+        // moments are then Toeplitz after a diagonal scaling (toeplitz.cu)
+        bool geo = !uni && op->N >= 2;
+        const double q = (op->nodes_h[2] - op->nodes_h[1]) / h0;
+        for (int i = 1; i < op->N && geo; ++i) {
+            const double hp = op->nodes_h[i] - op->nodes_h[i - 1], hi = op->nodes_h[i + 1] - op->nodes_h[i];
+            if (std::fabs(hi - q * hp) > 1e-10 * hi) geo = false;   // (the matvec parity tolerance)
+        }
+        op->geometric = geo;
     }
-    if ((flags & FDE_OP_TOEPLITZ) && !op->uniform)
-        fde_fail(FDE_EUNSUPPORTED_MESH, "unsupported mesh: the Toeplitz path needs a uniform mesh");
+    if ((flags & FDE_OP_TOEPLITZ) && !op->uniform && !op->geometric)
+        fde_fail(FDE_EUNSUPPORTED_MESH, "unsupported mesh: the Toeplitz path needs a uniform or single-ratio geometric mesh");
     if (op->n < 1) fde_fail(FDE_EINVAL_SIZE, "no unknowns (N*P - 1 < 1)");
     // element partition over ranks
     const int G = h->world, N = op->N, P = op->P;

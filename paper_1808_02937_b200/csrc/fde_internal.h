@@ -266,6 +266,7 @@ struct fde_op {
     int64_t n = 0;
     int flags = 0;
     bool uniform = false;
+    bool geometric = false;         // one geometric progression h_{e+1} = q h_e (Toeplitz after scaling)
     double g0 = 0;                  // 1/Gamma(2-alpha)
     std::vector<double> nodes_h;
     AsmTables tab;
@@ -282,6 +283,8 @@ struct fde_op {
     int L = 0;                      // FFT length
     DBuf<double> sym;               // N x P*P lag moments K_{k,0}
     DBuf<double> spec;              // L x P x P complex (interleaved re,im): theta K^ + (1-theta) K^H
+                                    // (geometric: theta K^, then (1-theta) K^H, two arrays)
+    DBuf<double> wsc;               // geometric: column scales w_e = (h_e / h_0)^(1-alpha)
     DBuf<double> twid;              // L/2 complex twiddles
     // scratch
     DBuf<double> xw, yw, gw;        // internal-order work vectors

@@ -127,6 +127,36 @@ def test_toeplitz_fft_matvec_matches_oracle(fde, h, alpha, N):
     op.free()
 
 
+@pytest.mark.parametrize("qhat,N,P,alpha", [(1.05, 24, 8, 1.5), (0.9, 24, 4, 1.3), (1.2, 24, 6, 1.8),
+                                           (1.02, 100, 8, 1.6), (0.97, 100, 5, 1.4)])
+def test_toeplitz_fft_matvec_geometric_mesh(fde, h, qhat, N, P, alpha):
+    """Geometric meshes: K_ij = w_j K_{i-j,0}, Toeplitz after a
+    diagonal scaling; the FFT matvec equals the dense one and (N = 24) the oracle's A x."""
+    p = fi.geometric_problem(qhat, N=N, P=P, alpha=alpha)
+    op = fde.assemble_problem(h, p, flags=fde.OP_DENSE | fde.OP_TOEPLITZ)
+    rng = np.random.default_rng(3)
+    X = torch.tensor(rng.standard_normal((3, p.n)), device="cuda")
+    Yf = fde.stiffness_matvec(h, op, X, path=fde.PATH_TOEPLITZ).cpu().numpy()
+    Yd = fde.stiffness_matvec(h, op, X, path=fde.PATH_DENSE).cpu().numpy()
+    Ag = fde.operator_dense_paper(h, op).cpu().numpy()
+    den = (np.abs(Ag) @ np.abs(X.cpu().numpy().T)).T
+    assert np.max(np.abs(Yf - Yd) / den) <= TOL
+    if N == 24:
+        so = oracle_system(p)
+        Yo = (so.A @ X.cpu().numpy().T).T
+        assert np.max(np.abs(Yf - Yo) / den) <= TOL
+    op.free()
+
+
+def test_toeplitz_rejects_graded_mesh_but_not_geometric(fde, h):
+    p = fi.config4(N=16, P=4)   # x_j = (2j/N)^2 / 2: ratios vary
+    with pytest.raises(fde.FdeError) as e:
+        fde.assemble_problem(h, p, flags=fde.OP_TOEPLITZ)
+    assert e.value.name == "FDE_EUNSUPPORTED_MESH"
+    op = fde.assemble_problem(h, fi.geometric_problem(1.1, N=16, P=4), flags=fde.OP_TOEPLITZ)
+    op.free()
+
+
 def test_toeplitz_rejects_nonuniform(fde, h):
     p = fi.config4(N=16, P=4)
     with pytest.raises(fde.FdeError) as e:

@@ -177,6 +177,23 @@ def test_theta_half_symmetric_and_toeplitz_uniform():
             assert np.abs(O.pair_integral(P, alpha, nodes, i, i - k) - ref[k]).max() <= 1e-13 * np.abs(ref[k]).max()
 
 
+def test_geometric_mesh_pair_scaling_law():
+    """Single-ratio geometric mesh: the nodes are o + c q^e, so
+    t_i - s_j = q^j (t_{i-j} - s_0) and every pair integral is the first-column one
+    scaled by w_j = (h_j/h_0)^{1-alpha} (the reading the geometric Toeplitz matvec
+    uses); pinned against the oracle's per-pair quadrature."""
+    for q, alpha in [(1.25, 1.6), (0.8, 1.3)]:
+        nodes = fi.geometric_mesh(0, 1, 9, q)
+        P = 3
+        h = np.diff(nodes)
+        for i in range(2, 9):
+            for j in range(1, i + 1):
+                ref = O.pair_integral(P, alpha, nodes, i - j, 0)
+                got = O.pair_integral(P, alpha, nodes, i, j)
+                w = (h[j] / h[0]) ** (1 - alpha)
+                assert np.abs(got - w * ref).max() <= 1e-12 * np.abs(w * ref).max()
+
+
 def test_coercivity_symmetric_part_positive_definite():
     """Theorem 2.1: the symmetric part of A is positive definite."""
     p = fi.config2(1.8, N=12, P=4)
