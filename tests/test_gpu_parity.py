@@ -417,3 +417,21 @@ def test_hlu_leaf_ordered_matches_recursive_factors(fde, h):
     assert np.max(np.abs(F[0] - F[1]) / (d[:, None] * d[None, :])) <= 1e-9
     hm.free()
     op.free()
+
+
+def test_condition_numbers_example51(fde, h):
+    """NEXT-4: on Example 5.1's graded mesh cond_2(A)
+    grows past 1e9 already at N = 300 (6.8e11 at N = 1000, profiles/r1f_cond_diag.jsonl)
+    while the H-LU-preconditioned operator A~^{-1} A (Tol_HLU = 1e-3) has
+    cond_2 < 10; A~^{-1} A formed column by column through precond_apply."""
+    p = fi.example51(N=300, P=3)
+    op = fde.assemble_problem(h, p)
+    hm = fde.hmatrix_build(h, op, p.R, p.lam, p.n_min)
+    lu = fde.hlu_factor(h, hm, 1e-3)
+    A = fde.operator_dense_paper(h, op)
+    s = torch.linalg.svdvals(A)
+    MA = fde.precond_apply(h, lu, A.T.contiguous()).T
+    sp = torch.linalg.svdvals(MA)
+    assert (s[0] / s[-1]).item() > 1e9
+    assert (sp[0] / sp[-1]).item() < 10.0
+    lu.free(); hm.free(); op.free()
