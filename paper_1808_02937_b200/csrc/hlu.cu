@@ -1998,7 +1998,10 @@ fde_lu* hlu_build(fde_ctx* h, fde_hm* hm, double tol)
         L->h = h;
         L->S = hm->S;
         L->tol = tol;
-        L->rmax = std::max(16, hm->R);   // rank capacity of the truncated blocks
+        // rank capacity of the truncated blocks (a standalone solve at a tight
+        // tolerance, NEXT-3, keeps wider blocks: 32, so a sum of two still fits the
+        // 64-column truncation kernels)
+        L->rmax = std::max(tol < 1e-8 ? 32 : 16, hm->R);
         L->pinned = ctx_pinned(h);   // owned by the handle (no page locking per factorisation)
         L->dflag.alloc(4);
         L->dflag.zero(h->stream);
