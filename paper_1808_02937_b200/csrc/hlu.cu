@@ -2251,16 +2251,16 @@ __device__ void apply_tile_rows(const SweepDev& S, const SLeaf& L, const double*
     const int o = threadIdx.x % (AT_R * AT_C), ph = threadIdx.x / (AT_R * AT_C);
     const int rr = o % AT_R, cc = o / AT_R;
     const int nlr = L.l_hi - L.l_lo;
-    bool lr_smem = nlr * 64 * AT_C <= APPLY_TSM;
-    for (int l = L.l_lo; l < L.l_hi && lr_smem; ++l) lr_smem = S.lrr[l].kc <= 64;
+    const int kq = L.kq;   // (max rank of the leaf's low-rank row terms: the staging stride)
+    const bool lr_smem = nlr * kq * AT_C <= APPLY_TSM;
     for (int tile = blockIdx.x; tile < ntr * ntc; tile += gridDim.x) {
         const int r0 = (tile % ntr) * AT_R, c0 = (tile / ntr) * AT_C;
         const int row = r0 + rr, col = c0 + cc;
         const bool valid = row < L.m && col < nrhs;
         if (lr_smem) {   // chunk sums of the projections t of this tile's right-hand sides
-            for (int e = threadIdx.x; e < nlr * 64 * AT_C; e += APPLY_THREADS) {
-                const int cx = e / (nlr * 64), ee = e % (nlr * 64);
-                const int l = L.l_lo + ee / 64, q = ee % 64;
+            for (int e = threadIdx.x; e < nlr * kq * AT_C; e += APPLY_THREADS) {
+                const int cx = e / (nlr * kq), ee = e % (nlr * kq);
+                const int l = L.l_lo + ee / kq, q = ee % kq;
                 const SLRRow R = S.lrr[l];
                 double tv = 0.0;
                 if (q < R.kc && c0 + cx < nrhs) {
@@ -2286,7 +2286,7 @@ __device__ void apply_tile_rows(const SweepDev& S, const SLeaf& L, const double*
                 if (q >= R.kc) continue;
                 double tv;
                 if (lr_smem) {
-                    tv = tsm[cc * (nlr * 64) + (l - L.l_lo) * 64 + q];
+                    tv = tsm[cc * (nlr * kq) + (l - L.l_lo) * kq + q];
                 } else {
                     tv = 0.0;
                     const double* tc = t + (long long)col * tstride;
@@ -2353,15 +2353,15 @@ __device__ void run_sweep(const SweepDev& S, int backward, double* x, long long 
         const bool tiled = nrhs > APPLY_RC;
         if (tiled) apply_tile_rows(S, L, x, ldx, nrhs, z, t, tstride, part, tsm);
         const int nlr = L.l_hi - L.l_lo;
-        bool lr_smem = nlr * 64 <= APPLY_TSM / APPLY_RC;
-        for (int l = L.l_lo; l < L.l_hi && lr_smem; ++l) lr_smem = S.lrr[l].kc <= 64;
+        const int kq = L.kq;
+        const bool lr_smem = nlr * kq <= APPLY_TSM / APPLY_RC;
         for (int c0 = 0; c0 < nrhs && !tiled; c0 += APPLY_RC) {
             const int nc = min(APPLY_RC, nrhs - c0);
             if (nr == 0) continue;
             if (lr_smem) {
-                for (int e = threadIdx.x; e < nlr * 64 * nc; e += APPLY_THREADS) {
-                    const int cc = e / (nlr * 64), ee = e % (nlr * 64);
-                    const int l = L.l_lo + ee / 64, q = ee % 64;
+                for (int e = threadIdx.x; e < nlr * kq * nc; e += APPLY_THREADS) {
+                    const int cc = e / (nlr * kq), ee = e % (nlr * kq);
+                    const int l = L.l_lo + ee / kq, q = ee % kq;
                     const SLRRow R = S.lrr[l];
                     const double* tc = t + (long long)(c0 + cc) * tstride;
                     double tv = 0.0;
@@ -2412,7 +2412,7 @@ __device__ void run_sweep(const SweepDev& S, int backward, double* x, long long 
                             if (cc >= nc) continue;
                             double tv;
                             if (lr_smem) {
-                                tv = tsm[cc * (APPLY_TSM / APPLY_RC) + (l - L.l_lo) * 64 + q];
+                                tv = tsm[cc * (APPLY_TSM / APPLY_RC) + (l - L.l_lo) * kq + q];
                             } else {
                                 tv = 0.0;
                                 const double* tc = t + (long long)(c0 + cc) * tstride;
