@@ -4,7 +4,7 @@ sys.path.insert(0, '.')
 import torch
 import fde_inputs as fi
 from paper_1808_02937_b200 import fde
-p = fi.config4()
+p = fi.config5() if (len(sys.argv) > 1 and sys.argv[1] == 'c5') else fi.config4()
 h = fde.Handle(0)
 op = fde.assemble_problem(h, p)
 hm = fde.hmatrix_build(h, op, p.R, p.lam, p.n_min)
