@@ -271,16 +271,14 @@ __device__ void h2_panel_inv_body(const H2Panel& p, double* psm)
             cp_async8(Bs + c * ldB + i, p.X + (long long)c * p.ldx + i);
         }
     }
-    double acc[4][4];
+    // FP64 tensor cores (mma.sync m8n8k4): warp w owns rows wm..wm+31 and vectors
+    // wn..wn+15 of the 128 x 32 output (4 x 2 fragments of 8 x 8)
+    const int wm = (w & 3) * 32, wn = (w >> 2) * 16;
+    double dacc[4][2][2];
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
+    for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int u = 0; u < 4; ++u) acc[a][u] = 0.0;
-    int ia[4], cu[4];
-#pragma unroll
-    for (int a = 0; a < 4; ++a) ia[a] = min(lane + 32 * a, m - 1);
-#pragma unroll
-    for (int u = 0; u < 4; ++u) cu[u] = min(w + 8 * u, nv - 1);
+        for (int j = 0; j < 2; ++j) dacc[i][j][0] = dacc[i][j][1] = 0.0;
     auto stage = [&](int q0, double* Tb) {
         const int nq = min(H2_PCH, m - q0);
         if (MODE == 0) {   // op(i, q) = Ti(i, q): columns q0.. of Ti
@@ -308,29 +306,36 @@ __device__ void h2_panel_inv_body(const H2Panel& p, double* psm)
             cp_async_wait_group<0>();
         }
         __syncthreads();
-        for (int qq = 0; qq < nq; ++qq) {
-            double o[4], x[4];
+        // (rows >= m / vectors >= nv of the staging buffers are stale: they only
+        // reach outputs that are not stored; k beyond the chunk is zeroed)
 #pragma unroll
-            for (int a = 0; a < 4; ++a) o[a] = Tc[qq * ldT + ia[a]];
+        for (int kk = 0; kk < H2_PCH; kk += 4) {
+            const int kr = kk + (lane & 3);
+            const bool kv = kr < nq;
+            double a[4], b[2];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) x[u] = Bs[cu[u] * ldB + q0 + qq];
+            for (int i = 0; i < 4; ++i) a[i] = kv ? Tc[kr * ldT + wm + i * 8 + (lane >> 2)] : 0.0;
 #pragma unroll
-            for (int a = 0; a < 4; ++a)
+            for (int j = 0; j < 2; ++j) b[j] = kv ? Bs[(wn + j * 8 + (lane >> 2)) * ldB + q0 + kr] : 0.0;
 #pragma unroll
-                for (int u = 0; u < 4; ++u) acc[a][u] = fma(o[a], x[u], acc[a][u]);
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 2; ++j) dmma(dacc[i][j][0], dacc[i][j][1], a[i], b[j]);
         }
         __syncthreads();
     }
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
+    for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int i = lane + 32 * a, c = w + 8 * u;
-            if (i < m && c < nv) {
-                if (MODE == 2) p.X[(long long)i * p.ldx + c] = acc[a][u];
-                else p.X[(long long)c * p.ldx + i] = acc[a][u];
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+                const int r = wm + i * 8 + (lane >> 2), cv = wn + j * 8 + 2 * (lane & 3) + hh;
+                if (r < m && cv < nv) {
+                    if (MODE == 2) p.X[(long long)r * p.ldx + cv] = dacc[i][j][hh];
+                    else p.X[(long long)cv * p.ldx + r] = dacc[i][j][hh];
+                }
             }
-        }
 }
 
 template <int MODE>
