@@ -237,7 +237,7 @@ def run_ours(args):
     # some steps of this host-launch-heavy path by ~100 ms); FDE_CLOCKS=smi selects it
     mode = os.environ.get("FDE_CLOCKS", "nvml")
     clocks = (ClockSampler(local) if mode == "smi" else
-              NvmlSampler(local, period_s=float(os.environ.get("FDE_CLOCKS_PERIOD", "0.1"))))
+              NvmlSampler(local, period_s=float(os.environ.get("FDE_CLOCKS_PERIOD", "0.01"))))
     if mode == "none":
         clocks.start = lambda: None
         clocks.stop = lambda: {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["not sampled (FDE_CLOCKS=none)"]}
