@@ -338,18 +338,18 @@ __device__ void h2_panel_inv_body(const H2Panel& p, double* psm)
             }
 }
 
+// Substitution panel: the 32-column block panels of T' are staged one at a time,
+// double-buffered (~100 KB of shared memory instead of the whole 128 x 128 tile:
+// the CTA then fits beside the bulk-update GEMMs and starts without waiting for
+// an SM to drain).  Tb[q ldT + i] = T'(i, b0 + q) for the rows i >= b0 it needs.
 template <int MODE>
 __device__ void h2_panel_body(const H2Panel& p, double* psm)
 {
     const int m = p.m, ldT = (m & 1) ? m + 2 : m + 1, ldB = ldT;
-    double* Ts = psm;
-    double* Bs = psm + m * ldT;       // vector c, element i at Bs[c * ldB + i]
+    double* Bs = psm;                         // vector c, element i at Bs[c * ldB + i]
+    double* Tb = psm + H2_STRIP * ldB;        // two block panels of 32 columns
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const int nv = p.nvec;
-    for (int t = tid; t < m * m; t += 256) {
-        const int i = t % m, j = t / m;
-        cp_async8(Ts + j * ldT + i, p.T + (long long)j * p.ldt + i);
-    }
     if (MODE == 2) {   // rows of X are the vectors
         for (int t = tid; t < nv * m; t += 256) {
             const int c = t % nv, i = t / nv;
@@ -361,11 +361,34 @@ __device__ void h2_panel_body(const H2Panel& p, double* psm)
             cp_async8(Bs + c * ldB + i, p.X + (long long)c * p.ldx + i);
         }
     }
-    cp_async_wait_all();
-    __syncthreads();
+    auto stage = [&](int bi, double* dst) {
+        const int b0 = bi * 32, bs = min(32, m - b0), nr = m - b0;
+        if (MODE == 0) {   // T'(i, j) = L[i][j] = T[j ldt + i]
+            for (int t = tid; t < bs * nr; t += 256) {
+                const int q = t / nr, i = b0 + t % nr;
+                cp_async8(dst + q * ldT + i, p.T + (long long)(b0 + q) * p.ldt + i);
+            }
+        } else {           // T'(i, j) = U[j][i] = T[i ldt + j]
+            for (int t = tid; t < bs * nr; t += 256) {
+                const int q = t % bs, i = b0 + t / bs;
+                cp_async8(dst + q * ldT + i, p.T + (long long)i * p.ldt + b0 + q);
+            }
+        }
+    };
     const int nb = (m + 31) / 32;
+    stage(0, Tb);
+    cp_async_commit_group();   // (with the vectors)
     for (int bi = 0; bi < nb; ++bi) {
         const int b0 = bi * 32, bs = min(32, m - b0);
+        const double* Tc = Tb + (bi & 1) * 32 * ldT;
+        if (bi + 1 < nb) {
+            stage(bi + 1, Tb + ((bi + 1) & 1) * 32 * ldT);
+            cp_async_commit_group();
+            cp_async_wait_group<1>();
+        } else {
+            cp_async_wait_group<0>();
+        }
+        __syncthreads();
         // diagonal block: warp w solves vectors w + 8u (u = 0..3) together (lane = row)
         {
             double v[4];
@@ -375,8 +398,8 @@ __device__ void h2_panel_body(const H2Panel& p, double* psm)
                 v[u] = (c < nv && lane < bs) ? Bs[c * ldB + b0 + lane] : 0.0;
             }
             for (int q = 0; q < bs; ++q) {
-                const double tq = (lane > q && lane < bs) ? h2_tp<MODE>(Ts, ldT, b0 + lane, b0 + q) : 0.0;
-                const double rq = MODE == 0 ? 1.0 : 1.0 / h2_tp<MODE>(Ts, ldT, b0 + q, b0 + q);
+                const double tq = (lane > q && lane < bs) ? Tc[q * ldT + b0 + lane] : 0.0;
+                const double rq = MODE == 0 ? 1.0 : 1.0 / Tc[q * ldT + b0 + q];
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
                     const double y = __shfl_sync(0xffffffffu, v[u], q) * rq;
@@ -398,7 +421,7 @@ __device__ void h2_panel_body(const H2Panel& p, double* psm)
                 const int i = r0 + t % (m - r0), c = t / (m - r0);
                 double s = Bs[c * ldB + i];
 #pragma unroll 8
-                for (int q = 0; q < bs; ++q) s = fma(-h2_tp<MODE>(Ts, ldT, i, b0 + q), Bs[c * ldB + b0 + q], s);
+                for (int q = 0; q < bs; ++q) s = fma(-Tc[q * ldT + i], Bs[c * ldB + b0 + q], s);
                 Bs[c * ldB + i] = s;
             }
         }
@@ -1774,7 +1797,7 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
     // k+1); sb: truncations (operands before the panels, overflowing targets before
     // the new columns) and the new low-rank columns; sc: the remaining dense updates
     // of step k, which overlap LU(k+1) and the panels of step k+1 (lookahead).
-    const int pan_smem = (H2_MMAX + H2_STRIP) * (H2_MMAX + 2) * (int)sizeof(double);
+    const int pan_smem = (H2_STRIP + 64) * (H2_MMAX + 2) * (int)sizeof(double);   // (two 32-column block panels)
     set_smem_once((const void*)k_h2_panel, pan_smem);
     const int pan_smem_inv = (H2_STRIP + 2 * H2_PCH) * (H2_MMAX + 2) * (int)sizeof(double);   // (double-buffered op)
     const int lu_smem = H2_MMAX * (H2_MMAX + 1) * (int)sizeof(double);   // padded 128 x 129
