@@ -374,3 +374,15 @@ def test_lemma32_kernel_bound():
                     kt += cnu * (t - s0) ** (1 - alpha - nu) * (s - s0) ** nu
                 worst = max(worst, abs((t - s) ** (1 - alpha) - kt))
         assert worst <= bound
+
+
+def test_geometric_mesh_recipe_single_ratio():
+    """The seeded-input recipe for geometric meshes (fde_inputs.geometric_mesh,
+    PAPER.md:634): every node from its own power, so h_{e+1}/h_e equals q to far
+    below the 1e-10 the library's single-ratio test (and Toeplitz path) requires,
+    even on long meshes; endpoints exact, nodes strictly increasing."""
+    for q, N in [(1.001, 4096), (1.01, 256), (0.97, 100), (1.2, 24), (0.8, 9)]:
+        x = fi.geometric_mesh(0.0, 1.0, N, q)
+        h = np.diff(x)
+        assert x[0] == 0.0 and x[-1] == 1.0 and (h > 0).all()
+        assert np.abs(h[1:] / h[:-1] / q - 1).max() < 1e-11
