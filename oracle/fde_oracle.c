@@ -27,7 +27,7 @@
  *                     touching pair (d=0) is dropped once its a-priori bound is
  *                     below 1e-19 of the pair scale.
  * Every table (Gauss-Legendre by Newton on the recurrence, Gauss-Jacobi by
- * Golub-Welsch + Newton polish) is computed here in long double.
+ * sign-change bracketing + bisection + Newton on P_n^{(a,b)}) is computed here in long double.
  */
 #include <math.h>
 #include <stdlib.h>
@@ -118,82 +118,56 @@ static void jacobi_ld(int n, ld a, ld b, ld x, ld *val, ld *der)
     *val = p1;
 }
 
-/* symmetric tridiagonal QL with implicit shifts; d: diag, e: sub-diag (e[0..n-2]),
- * z: first row of the eigenvector matrix (only that row is needed for weights). */
-static int tql_first_row(int n, ld *d, ld *e, ld *z)
-{
-    for (int i = 0; i < n; ++i) z[i] = (i == 0) ? 1.0L : 0.0L;
-    e[n - 1] = 0.0L;
-    for (int l = 0; l < n; ++l) {
-        int iter = 0, m;
-        do {
-            for (m = l; m < n - 1; ++m) {
-                ld dd = fabsl(d[m]) + fabsl(d[m + 1]);
-                if (fabsl(e[m]) <= 1e-22L * dd) break;
-            }
-            if (m != l) {
-                if (iter++ == 200) return -1;
-                ld g = (d[l + 1] - d[l]) / (2.0L * e[l]);
-                ld r = hypotl(g, 1.0L);
-                g = d[m] - d[l] + e[l] / (g + (g >= 0 ? fabsl(r) : -fabsl(r)));
-                ld s = 1.0L, c = 1.0L, p = 0.0L;
-                int i;
-                for (i = m - 1; i >= l; --i) {
-                    ld f = s * e[i], b = c * e[i];
-                    r = hypotl(f, g);
-                    e[i + 1] = r;
-                    if (r == 0.0L) { d[i + 1] -= p; e[m] = 0.0L; break; }
-                    s = f / r; c = g / r;
-                    g = d[i + 1] - p;
-                    r = (d[i] - g) * s + 2.0L * c * b;
-                    p = s * r;
-                    d[i + 1] = g + p;
-                    g = c * r - b;
-                    /* rotate eigenvector first-row entries */
-                    f = z[i + 1];
-                    z[i + 1] = s * z[i] + c * f;
-                    z[i] = c * z[i] - s * f;
-                }
-                if (r == 0.0L && i >= l) continue;
-                d[l] -= p; e[l] = g; e[m] = 0.0L;
-            }
-        } while (m != l);
-    }
-    return 0;
-}
-
+/* Gauss-Jacobi rule from the polynomial itself: the nodes are the n simple zeros
+ * of P_n^{(a,b)} in (-1,1).  They are bracketed by sign changes of P_n on a
+ * Chebyshev-spaced grid of 256 n + 1 points (dense near +-1, where the zeros
+ * crowd like O(1/n^2)), each bracket is narrowed by bisection and polished by
+ * Newton steps.  Weights from the closed form (Szego, Orthogonal Polynomials,
+ * Thm. 15.3.1 / Abramowitz-Stegun 25.4.33, second form):
+ *   w_i = 2^{a+b+1} Gamma(n+a+1) Gamma(n+b+1) / (Gamma(n+a+b+1) n!)
+ *         / ((1 - x_i^2) P_n'(x_i)^2).
+ * Pinned by tests/test_oracle_pins.py::test_gauss_jacobi_exact_on_moments
+ * (exactness on (1+x)^k, k <= 2n-1). */
 int orc_gauss_jacobi(int n, ld a, ld b, ld *x, ld *w)
 {
     if (n < 1 || n > MAXQ) return -1;
-    ld d[MAXQ], e[MAXQ], z[MAXQ];
-    for (int k = 0; k < n; ++k) {
-        ld c = 2 * k + a + b;
-        if (k == 0) d[k] = (b - a) / (a + b + 2);
-        else d[k] = (b * b - a * a) / (c * (c + 2));
-        if (k < n - 1) {
-            ld kk = k + 1, cc = 2 * kk + a + b;
-            ld num = 4 * kk * (kk + a) * (kk + b) * (kk + a + b);
-            ld den = cc * cc * (cc + 1) * (cc - 1);
-            e[k] = sqrtl(num / den);
+    const ld pi = 3.141592653589793238462643383279502884L;
+    const int M = 256 * n;
+    int found = 0;
+    ld xl = -1.0L, vl, dv;
+    jacobi_ld(n, a, b, xl, &vl, &dv);
+    for (int k = M - 1; k >= 0 && found < n; --k) {
+        ld xr = cosl(pi * k / M), vr;           /* ascending from -1 to +1 */
+        jacobi_ld(n, a, b, xr, &vr, &dv);
+        if (vl == 0.0L) { x[found++] = xl; }
+        else if ((vl < 0) != (vr < 0) && vr != 0.0L) {
+            ld lo = xl, hi = xr, flo = vl;
+            for (int it = 0; it < 200 && hi - lo > 1e-12L * (1 + fabsl(lo)); ++it) {
+                ld mid = 0.5L * (lo + hi), fm;
+                jacobi_ld(n, a, b, mid, &fm, &dv);
+                if ((fm < 0) == (flo < 0)) { lo = mid; flo = fm; } else hi = mid;
+            }
+            ld z = 0.5L * (lo + hi);
+            for (int it = 0; it < 6; ++it) {
+                ld v, d;
+                jacobi_ld(n, a, b, z, &v, &d);
+                if (d == 0) break;
+                ld zn = z - v / d;
+                if (zn <= lo || zn >= hi) break;      /* stay inside the bracket */
+                z = zn;
+            }
+            x[found++] = z;
         }
+        xl = xr; vl = vr;
     }
-    if (tql_first_row(n, d, e, z)) return -2;
-    ld mu0 = powl(2.0L, a + b + 1) * tgammal(a + 1) * tgammal(b + 1) / tgammal(a + b + 2);
-    /* sort ascending (selection) */
+    if (found != n) return -2;
+    ld lc = (a + b + 1) * logl(2.0L) + lgammal(n + a + 1) + lgammal(n + b + 1)
+          - lgammal(n + a + b + 1) - lgammal(n + 1.0L);
+    ld c = expl(lc);
     for (int i = 0; i < n; ++i) {
-        int k = i;
-        for (int j = i + 1; j < n; ++j) if (d[j] < d[k]) k = j;
-        ld t = d[i]; d[i] = d[k]; d[k] = t; t = z[i]; z[i] = z[k]; z[k] = t;
-    }
-    for (int i = 0; i < n; ++i) {
-        ld xx = d[i], v, dv;
-        for (int it = 0; it < 4; ++it) {       /* Newton polish */
-            jacobi_ld(n, a, b, xx, &v, &dv);
-            if (dv == 0) break;
-            xx -= v / dv;
-        }
-        x[i] = xx;
-        w[i] = mu0 * z[i] * z[i];
+        ld v, d;
+        jacobi_ld(n, a, b, x[i], &v, &d);
+        w[i] = c / ((1 - x[i] * x[i]) * d * d);
     }
     return 0;
 }
@@ -487,24 +461,27 @@ int orc_load(int N, const double *nodes, int P, double a, double b,
             }
         }
         /* non-integer powers away from their base element: composite Gauss-Legendre on
-         * cells [o, 2o] of the distance o to the base point (cell size = distance) */
+         * cells [o, 2o] of the distance o to the base point (cell size = distance).
+         * Points are placed by their offset u = o - o0 in [0, h] from the element's
+         * near end, so the reference coordinate xi is formed without cancellation
+         * (o0 can exceed h by many orders of magnitude on graded meshes). */
         for (int t = 0; t < nterm; ++t) {
             int touches = (side[t] == 0) ? (e == 0) : (e == N - 1);
             int integer_pw = (pw[t] == floor(pw[t]) && pw[t] >= 0);
             if (touches || integer_pw) continue;
             ld o0 = (side[t] == 0) ? ((ld)nodes[e] - A) : (B - (ld)nodes[e + 1]);
-            ld oend = o0 + h, oa = o0;
-            while (oa < oend) {
-                ld ob = 2 * oa < oend ? 2 * oa : oend;
+            ld ua = 0;
+            while (ua < h) {
+                ld ub = o0 + 2 * ua < h ? o0 + 2 * ua : h;     /* o_b = 2 o_a, capped */
                 for (int k = 0; k < q; ++k) {
-                    ld o = oa + 0.5L * (ob - oa) * (gx[k] + 1);
-                    ld w = 0.5L * (ob - oa) * gw[k] * coef[t] * powl(o, (ld)pw[t]);
-                    ld xi = (side[t] == 0) ? (2 * (o - o0) / h - 1) : (1 - 2 * (o - o0) / h);
+                    ld u = ua + 0.5L * (ub - ua) * (gx[k] + 1);
+                    ld w = 0.5L * (ub - ua) * gw[k] * coef[t] * powl(o0 + u, (ld)pw[t]);
+                    ld xi = (side[t] == 0) ? (2 * u / h - 1) : (1 - 2 * u / h);
                     ld v[MAXP + 1];
                     local_value(P, xi, v);
                     for (int k2 = 0; k2 < M; ++k2) loc[k2] += w * v[k2];
                 }
-                oa = ob;
+                ua = ub;
             }
         }
         /* singular power terms on the touching element: Gauss-Jacobi */

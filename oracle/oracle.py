@@ -7,7 +7,11 @@ Index conventions (oracle side, independent of the CUDA path):
   * paper order: X = [u^1_1..u^{P-1}_1; ...; u^1_N..u^{P-1}_N; u~_1..u~_{N-1}]
   * extended order = paper order + [hat of node 0, hat of node N] (for lifting).
 
-Parity: every function here is pinned in tests/test_oracle_pins.py except
+Parity: every function here is pinned in tests/test_oracle_pins.py and
+tests/test_oracle_branch_pins.py (the latter also runs each pin against a
+deliberately broken copy of the branch it pins, which must fail): theta != 1/2
+orientation, t-expansion and upper (1-theta) W Q^T blocks, Legendre-series and
+singular power loads, boundary-hat lifting.  Not pinned:
   * `hlu`-related behaviour at Tol_HLU = 1e-3, which has no plain definition
     (DESIGN.md "parity unpinned" list).
 """
@@ -35,30 +39,36 @@ def build_oracle(force: bool = False) -> str:
     return _SO
 
 
+def load_library(path: str):
+    """ctypes handle of a compiled oracle library with its signatures declared
+    (the mutation pins load deliberately broken copies through this)."""
+    L = ctypes.CDLL(path)
+    dp = ctypes.POINTER(ctypes.c_double)
+    ip = ctypes.POINTER(ctypes.c_int)
+    L.orc_pair_offdiag.restype = ctypes.c_long
+    L.orc_pair_offdiag.argtypes = [ctypes.c_int, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                   ctypes.c_double, dp]
+    L.orc_pair_self.argtypes = [ctypes.c_int, ctypes.c_double, ctypes.c_double, dp]
+    L.orc_assemble_Sl.argtypes = [ctypes.c_int, dp, ctypes.c_int, ctypes.c_double, ctypes.c_int,
+                                  ctypes.c_int, dp, ctypes.c_int]
+    L.orc_assemble_mass.argtypes = [ctypes.c_int, dp, ctypes.c_int, dp]
+    L.orc_load.argtypes = [ctypes.c_int, dp, ctypes.c_int, ctypes.c_double, ctypes.c_double,
+                           ctypes.c_int, dp, ctypes.c_int, ip, dp, dp, dp]
+    L.orc_eval_solution.argtypes = [ctypes.c_int, ctypes.c_int, dp, ctypes.c_int, dp, dp]
+    L.orc_gl_table.argtypes = [ctypes.c_int, dp, dp]
+    L.orc_gj_table.argtypes = [ctypes.c_int, ctypes.c_double, ctypes.c_double, dp, dp]
+    L.orc_local_deriv.argtypes = [ctypes.c_int, ctypes.c_double, ctypes.c_double, dp]
+    L.orc_local_value.argtypes = [ctypes.c_int, ctypes.c_double, dp]
+    L.orc_frac_integral_monomial.restype = ctypes.c_double
+    L.orc_frac_integral_monomial.argtypes = [ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_int]
+    return L
+
+
 def lib():
     global _lib
     if _lib is None:
         build_oracle()
-        L = ctypes.CDLL(_SO)
-        dp = ctypes.POINTER(ctypes.c_double)
-        ip = ctypes.POINTER(ctypes.c_int)
-        L.orc_pair_offdiag.restype = ctypes.c_long
-        L.orc_pair_offdiag.argtypes = [ctypes.c_int, ctypes.c_double, ctypes.c_double, ctypes.c_double,
-                                       ctypes.c_double, dp]
-        L.orc_pair_self.argtypes = [ctypes.c_int, ctypes.c_double, ctypes.c_double, dp]
-        L.orc_assemble_Sl.argtypes = [ctypes.c_int, dp, ctypes.c_int, ctypes.c_double, ctypes.c_int,
-                                      ctypes.c_int, dp, ctypes.c_int]
-        L.orc_assemble_mass.argtypes = [ctypes.c_int, dp, ctypes.c_int, dp]
-        L.orc_load.argtypes = [ctypes.c_int, dp, ctypes.c_int, ctypes.c_double, ctypes.c_double,
-                               ctypes.c_int, dp, ctypes.c_int, ip, dp, dp, dp]
-        L.orc_eval_solution.argtypes = [ctypes.c_int, ctypes.c_int, dp, ctypes.c_int, dp, dp]
-        L.orc_gl_table.argtypes = [ctypes.c_int, dp, dp]
-        L.orc_gj_table.argtypes = [ctypes.c_int, ctypes.c_double, ctypes.c_double, dp, dp]
-        L.orc_local_deriv.argtypes = [ctypes.c_int, ctypes.c_double, ctypes.c_double, dp]
-        L.orc_local_value.argtypes = [ctypes.c_int, ctypes.c_double, dp]
-        L.orc_frac_integral_monomial.restype = ctypes.c_double
-        L.orc_frac_integral_monomial.argtypes = [ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_int]
-        _lib = L
+        _lib = load_library(_SO)
     return _lib
 
 
