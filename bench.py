@@ -207,7 +207,7 @@ def run_ours(args):
         G = fde.sem_rhs(h, op, prob.forcings)
         hm = fde.hmatrix_build(h, op, prob.R, prob.lam, prob.n_min)
         lu = fde.hlu_factor(h, hm, 1e-3)
-        X, rep = fde.solve(h, op, lu, G, tol=1e-12, restart=50, maxiter=500)
+        X, rep = fde.solve(h, op, lu, G, tol=1e-12, restart=50, maxiter=500, verify=False)
         info = dict(assemble_ms=op.info.assemble_ms, hbuild_ms=hm.info.build_ms, hlu_ms=lu.info.factor_ms,
                     solve_ms=rep.solve_ms, iters=rep.iterations, matvecs=rep.matvecs, relres=rep.relres,
                     hlu_max_rank=lu.info.max_rank, hlu_ops=lu.info.nops)

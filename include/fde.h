@@ -20,7 +20,11 @@
  *    the host except solve (returns after convergence) and calls that
  *    return host data.
  *  - Opaque objects are created by the library and released with the
- *    matching fde_free_* call.  Mesh nodes are copied.
+ *    matching fde_free_* call.  Mesh nodes are copied.  Lifetimes: an
+ *    fde_hmatrix keeps a pointer to the fde_operator it was built from, and an
+ *    fde_hlu to that operator too (precond_apply / solve read its sizes and
+ *    work vectors): free an operator only after every H-matrix and H-LU built
+ *    from it.  All objects must be used with the handle that created them.
  *  - Return value: FDE_OK (0) or a negative FDE_E* code; fde_last_error()
  *    gives the message.  No entry point falls back to the CPU: without a
  *    usable CUDA device fde_create returns FDE_ECUDA.
@@ -94,6 +98,13 @@ typedef struct fde_lu* fde_hlu;
 int fde_create(fde_handle* out, int device, void* cuda_stream, const void* nccl_unique_id,
                int rank, int world);
 void fde_destroy(fde_handle h);
+/* Test / diagnostics: a handle that BEHAVES as rank `rank` of `world` ranks
+ * without a communicator, so one process on one GPU can run each rank's local
+ * work of the row-sharded path (sharded assembly, the near-field recompute of
+ * hmatrix_build, fde_shard_matvec, the all-gather compaction through
+ * fde_debug_compact_gather).  Calls that need the collective (the dense
+ * stiffness_matvec and solve at world > 1) fail with FDE_ENCCL. */
+int fde_create_virtual_rank(fde_handle* out, int device, void* cuda_stream, int rank, int world);
 const char* fde_last_error(fde_handle h);
 int fde_sync(fde_handle h);                   /* cudaStreamSynchronize(stream)    */
 int fde_nccl_unique_id(void* out128);          /* ncclGetUniqueId, for rank 0     */
@@ -168,6 +179,10 @@ int fde_operator_dense_paper(fde_handle h, fde_operator op, double* out, int64_t
 /* Columns of the boundary hats (node 0, node N) of the full operator, length n
  * each, paper order, into device buffer out[2*n] (used for the lifting). */
 int fde_operator_boundary_columns(fde_handle h, fde_operator op, double* out);
+/* This rank's dense rows [row_begin, row_end) x n in the INTERNAL
+ * element-interleaved order (fde_hlu_dense_internal's convention), row-major
+ * into device buffer out with ldo >= n; any world (test helper). */
+int fde_operator_rows_internal(fde_handle h, fde_operator op, double* out, int64_t ldo);
 
 /* -------------------------------------------------------------- sem_rhs */
 /* G[:, r] = (f_r, phi_I) - A[:, {0,N}] [c1, c2]  (lifting
@@ -183,6 +198,17 @@ enum { FDE_PATH_AUTO = 0, FDE_PATH_DENSE = 1, FDE_PATH_TOEPLITZ = 2 };
  * y over NCCL. */
 int stiffness_matvec(fde_handle h, fde_operator op, const double* x, double* y, int nrhs,
                      int64_t ld, int path);
+/* The local half of the sharded dense matvec: y_loc = A[r0:r1, :] x for this
+ * rank's rows only (no all-gather).  x device, paper order, ld ldx >= n; y_loc
+ * device, internal order, rows r0..r1 of column c at y_loc + c * ldy,
+ * ldy >= the largest shard (fde_shard_rows' rows_max). */
+int fde_shard_matvec(fde_handle h, fde_operator op, const double* x, int64_t ldx, double* y_loc, int64_t ldy,
+                     int nrhs);
+/* The step after ncclAllGather in the sharded matvec, on a caller-supplied
+ * buffer in the all-gather layout: gathered[(g * nrhs + c) * rows_max + r] =
+ * row r0(g) + r of column c from rank g.  Writes y (device, paper order, ld). */
+int fde_debug_compact_gather(fde_handle h, fde_operator op, const double* gathered, double* y, int64_t ld,
+                             int nrhs);
 
 /* -------------------------------------------------------- hmatrix_build */
 /* H-matrix H ~ S_l on the element-cluster block tree with admissibility
@@ -241,6 +267,10 @@ typedef struct {
     int32_t maxiter;      /* total iterations                                    */
     int32_t restart;      /* GMRES(m)                                            */
     int32_t path;         /* FDE_PATH_* for the matvec                           */
+    int32_t verify;       /* GMRES: 1 = at convergence recompute the true
+                             preconditioned residual ||A~^{-1}(G - A X)|| and restart
+                             the columns still above tol (one more matvec + apply);
+                             0 = trust the Givens estimate                         */
 } fde_solve_opts;
 
 typedef struct {
@@ -249,6 +279,7 @@ typedef struct {
     int32_t converged;    /* number of converged RHS columns                    */
     double relres;        /* max final preconditioned relative residual          */
     double solve_ms;
+    double relres_true;   /* max recomputed ||A~^{-1}(G-AX)||/||A~^{-1}G|| (verify=1), else -1 */
 } fde_solve_report;
 
 /* Solve A~^{-1} A X = A~^{-1} G (Eq. (precondsys)) from

@@ -69,45 +69,61 @@ bool fde_ring_upload(void* dst, const void* src, size_t bytes, cudaStream_t s)
 
 extern "C" {
 
-int fde_create(fde_handle* out, int device, void* cuda_stream, const void* nccl_unique_id, int rank, int world)
+static int create_ctx(fde_handle* out, int device, void* cuda_stream, const void* nccl_unique_id, int rank, int world,
+                      bool virt)
 {
     fde_ctx* h = nullptr;
-    API_BEGIN
-    if (!out) fde_fail(FDE_EINVAL_PARAM, "fde_create: out is NULL");
-    if (world < 1 || rank < 0 || rank >= world) fde_fail(FDE_EINVAL_PARAM, "fde_create: bad rank/world");
-    if (world > 1 && !nccl_unique_id) fde_fail(FDE_EINVAL_PARAM, "fde_create: world > 1 needs an NCCL unique id");
-    int ndev = 0;
-    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) fde_fail(FDE_ECUDA, "no CUDA device");
-    h = new fde_ctx();
-    h->device = device;
-    h->rank = rank;
-    h->world = world;
-    FDE_CUDA(cudaSetDevice(device));
-    // NULL is the legacy default stream (stream 0), as everywhere in CUDA;
-    // work is always ordered on the caller's stream.
-    h->stream = (cudaStream_t)cuda_stream;
-    h->own_stream = false;
-    FDE_CUDA(cudaEventCreate(&h->ev0));
-    FDE_CUDA(cudaEventCreate(&h->ev1));
-    FDE_CUDA(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, device));
-    {
-        // keep freed stream-ordered allocations in the pool (the H-LU allocates
-        // and frees many small temporaries; returning them to the OS at every
-        // synchronisation costs tens of microseconds per allocation)
-        cudaMemPool_t pool;
-        FDE_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
-        uint64_t thr = UINT64_MAX;
-        FDE_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
-    }
-    if (world > 1) comm_init(h, nccl_unique_id);
-    *out = h;
-    }
-    catch (FdeError& e) {
+    try {
+        if (!out) fde_fail(FDE_EINVAL_PARAM, "fde_create: out is NULL");
+        if (world < 1 || rank < 0 || rank >= world) fde_fail(FDE_EINVAL_PARAM, "fde_create: bad rank/world");
+        if (world > 1 && !nccl_unique_id && !virt)
+            fde_fail(FDE_EINVAL_PARAM, "fde_create: world > 1 needs an NCCL unique id");
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) fde_fail(FDE_ECUDA, "no CUDA device");
+        h = new fde_ctx();
+        h->device = device;
+        h->rank = rank;
+        h->world = world;
+        h->virt = virt;
+        FDE_CUDA(cudaSetDevice(device));
+        // NULL is the legacy default stream (stream 0), as everywhere in CUDA;
+        // work is always ordered on the caller's stream.
+        h->stream = (cudaStream_t)cuda_stream;
+        h->own_stream = false;
+        FDE_CUDA(cudaEventCreate(&h->ev0));
+        FDE_CUDA(cudaEventCreate(&h->ev1));
+        FDE_CUDA(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, device));
+        {
+            // keep freed stream-ordered allocations in the pool (the H-LU allocates
+            // and frees many small temporaries; returning them to the OS at every
+            // synchronisation costs tens of microseconds per allocation)
+            cudaMemPool_t pool;
+            FDE_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+            uint64_t thr = UINT64_MAX;
+            FDE_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+        }
+        if (world > 1 && !virt) comm_init(h, nccl_unique_id);
+        *out = h;
+    } catch (FdeError& e) {
         g_noctx_err = e.msg;
         delete h;
         return e.code;
+    } catch (std::exception& e) {
+        g_noctx_err = e.what();
+        delete h;
+        return FDE_ENOMEM;
     }
     return FDE_OK;
+}
+
+int fde_create(fde_handle* out, int device, void* cuda_stream, const void* nccl_unique_id, int rank, int world)
+{
+    return create_ctx(out, device, cuda_stream, nccl_unique_id, rank, world, false);
+}
+
+int fde_create_virtual_rank(fde_handle* out, int device, void* cuda_stream, int rank, int world)
+{
+    return create_ctx(out, device, cuda_stream, nullptr, rank, world, true);
 }
 
 void fde_destroy(fde_handle h)
@@ -244,7 +260,11 @@ static void validate(const fde_problem* p, const fde_mesh* m)
 int sem_assemble(fde_handle h, const fde_problem* prob, const fde_mesh* mesh, int flags, fde_operator* out)
 {
     fde_op* op = nullptr;
-    API_BEGIN
+    try {
+    if (!h) fde_fail(FDE_EINVAL_PARAM, "sem_assemble: handle is NULL");
+    if (!out) fde_fail(FDE_EINVAL_PARAM, "sem_assemble: out is NULL");
+    fde_set_alloc_stream(h->stream);
+    g_cur_ctx = h;
     validate(prob, mesh);
     if (!(flags & (FDE_OP_DENSE | FDE_OP_TOEPLITZ))) fde_fail(FDE_EINVAL_PARAM, "flags: DENSE and/or TOEPLITZ");
     FDE_CUDA(cudaSetDevice(h->device));
@@ -266,7 +286,7 @@ int sem_assemble(fde_handle h, const fde_problem* prob, const fde_mesh* mesh, in
         // one geometric progression of element sizes: the pair
         // moments are then Toeplitz after a diagonal scaling (toeplitz.cu)
         bool geo = !uni && op->N >= 2;
-        const double q = (op->nodes_h[2] - op->nodes_h[1]) / h0;
+        const double q = op->N >= 2 ? (op->nodes_h[2] - op->nodes_h[1]) / h0 : 1.0;
         for (int i = 1; i < op->N && geo; ++i) {
             const double hp = op->nodes_h[i] - op->nodes_h[i - 1], hi = op->nodes_h[i + 1] - op->nodes_h[i];
             if (std::fabs(hi - q * hp) > 1e-10 * hi) geo = false;   // (the matvec parity tolerance)
@@ -317,9 +337,14 @@ int sem_assemble(fde_handle h, const fde_problem* prob, const fde_mesh* mesh, in
     op = nullptr;
     }
     catch (FdeError& e) {
-        h->err = e.msg;
+        if (h) h->err = e.msg; else g_noctx_err = e.msg;
         delete op;
         return e.code;
+    }
+    catch (std::exception& e) {
+        if (h) h->err = e.what(); else g_noctx_err = e.what();
+        delete op;
+        return FDE_ENOMEM;
     }
     return FDE_OK;
 }
@@ -370,6 +395,19 @@ int fde_operator_boundary_columns(fde_handle h, fde_operator op, double* out)
     API_END(h)
 }
 
+int fde_operator_rows_internal(fde_handle h, fde_operator op, double* out, int64_t ldo)
+{
+    API_BEGIN
+    if (!(op->flags & FDE_OP_DENSE)) fde_fail(FDE_EINVAL_PARAM, "operator has no dense form");
+    if (ldo < op->n) fde_fail(FDE_EINVAL_SIZE, "ldo < n");
+    const int64_t rows = op->r1 - op->r0;
+    if (rows > 0)
+        FDE_CUDA(cudaMemcpy2DAsync(out, (size_t)ldo * sizeof(double), op->A.p, (size_t)op->lda * sizeof(double),
+                                   (size_t)op->n * sizeof(double), (size_t)rows, cudaMemcpyDeviceToDevice, h->stream));
+    API_END(h)
+}
+
+
 // ------------------------------------------------------------------ work
 static void ensure_work(fde_op* op, int nrhs)
 {
@@ -401,6 +439,32 @@ int stiffness_matvec(fde_handle h, fde_operator op, const double* x, double* y, 
     ensure_work(op, nrhs);
     perm_paper_to_internal(h, op->N, op->P, x, ld, op->xw.p, op->lda, nrhs);
     op_apply_internal(h, op, op->xw.p, op->lda, op->yw.p, op->lda, nrhs, path);
+    perm_internal_to_paper(h, op->N, op->P, op->yw.p, op->lda, y, ld, nrhs);
+    API_END(h)
+}
+
+// y_loc = A[r0:r1, :] x on this rank's shard (no all-gather): x paper order,
+// y_loc internal order, rows r0..r1 of every column at stride ldy (>= rows_max)
+int fde_shard_matvec(fde_handle h, fde_operator op, const double* x, int64_t ldx, double* y_loc, int64_t ldy,
+                     int nrhs)
+{
+    API_BEGIN
+    if (!(op->flags & FDE_OP_DENSE)) fde_fail(FDE_EINVAL_PARAM, "operator has no dense form");
+    if (nrhs < 1 || ldx < op->n || ldy < op->rows_max) fde_fail(FDE_EINVAL_SIZE, "fde_shard_matvec: sizes");
+    ensure_work(op, nrhs);
+    perm_paper_to_internal(h, op->N, op->P, x, ldx, op->xw.p, op->lda, nrhs);
+    dense_gemv(h, op, op->xw.p, op->lda, y_loc, ldy, nrhs);
+    API_END(h)
+}
+
+// the compaction + permutation step that follows the all-gather, on a buffer
+// in the all-gather layout (world x nrhs x rows_max) -> y paper order (ld)
+int fde_debug_compact_gather(fde_handle h, fde_operator op, const double* gathered, double* y, int64_t ld, int nrhs)
+{
+    API_BEGIN
+    if (nrhs < 1 || ld < op->n) fde_fail(FDE_EINVAL_SIZE, "fde_debug_compact_gather: sizes");
+    ensure_work(op, nrhs);
+    comm_compact_gathered(h, op, gathered, op->yw.p, op->lda, nrhs);
     perm_internal_to_paper(h, op->N, op->P, op->yw.p, op->lda, y, ld, nrhs);
     API_END(h)
 }

@@ -33,11 +33,11 @@ __constant__ double c_leg_b[FDE_LEG_K];
 // digits targeted by the quadrature order selection (FDE_ASM_DIGITS, default 17)
 __constant__ float c_qdigits = 17.0f;
 
-static int g_gl_uploaded_dev = -1;
+static bool g_gl_uploaded[64] = {};   // __constant__ memory is per device
 
 static void upload_gl_tables(int dev)
 {
-    if (g_gl_uploaded_dev == dev) return;
+    if (g_gl_uploaded[dev & 63]) return;
     std::vector<double> X(FDE_GL_TOTAL), W(FDE_GL_TOTAL);
     for (int q = 1; q <= FDE_QMAX; ++q) {
         std::vector<double> x, w;
@@ -58,7 +58,7 @@ static void upload_gl_tables(int dev)
     FDE_CUDA(cudaMemcpyToSymbol(c_leg_b, lb, sizeof(lb)));
     const float qd = getenv("FDE_ASM_DIGITS") ? (float)atof(getenv("FDE_ASM_DIGITS")) : 17.0f;
     FDE_CUDA(cudaMemcpyToSymbol(c_qdigits, &qd, sizeof(qd)));
-    g_gl_uploaded_dev = dev;
+    g_gl_uploaded[dev & 63] = true;
 }
 
 // --------------------------------------------------------------- device side

@@ -139,6 +139,7 @@ struct fde_ctx {
     bool own_stream = false;
     int rank = 0, world = 1;
     void* nccl = nullptr;   // ncclComm_t
+    bool virt = false;      // virtual rank (fde_create_virtual_rank): world > 1, no communicator
     std::string err;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     int num_sms = 148;
@@ -154,6 +155,13 @@ struct fde_ctx {
     // recorded behind its last copy completes
     void* kws = nullptr;     // Krylov workspace (krylov.cu), grow-only
     DBuf<double> kt_row, kt_col;   // pair-moment tables of the assembly (transient), grow-only
+    // per-handle scratch of the operator application (several handles may run
+    // concurrently on different streams / devices): the local GEMV shard, the
+    // all-gather receive buffer and row starts, the Toeplitz spectra
+    DBuf<double> mv_loc, g_recv;
+    DBuf<int64_t> g_rstart;
+    DBuf<double2> t_Dhat, t_What;
+    DBuf<double> t_wv;
     char* ring = nullptr;
     size_t ring_off = 0;
     int ring_cur = 0;
@@ -337,6 +345,8 @@ void op_apply_internal(fde_ctx* h, fde_op* op, const double* x, int64_t ldx, dou
 
 // communication
 void comm_allgather_rows(fde_ctx* h, fde_op* op, const double* local, double* full, int64_t ldfull, int nrhs);
+// the compaction step of comm_allgather_rows on an already gathered buffer
+void comm_compact_gathered(fde_ctx* h, fde_op* op, const double* gathered, double* full, int64_t ldfull, int nrhs);
 
 // profiling helpers (no-ops unless h->profiling)
 int prof_begin(fde_ctx* h, int cls, double bytes);

@@ -234,18 +234,18 @@ template <int NR, int CW>
 static void gemv_bulk_launch(cudaStream_t s, const double* A, long long lda, long long rows, const double* x,
                              long long ldx, double* y, long long ldy)
 {
-    static int smem_set = 0;
+    // the shared-memory opt-in and the SM count are per device
+    static int smem_set[64] = {}, nsm_dev[64] = {};
     constexpr int smem = gv_smem_bytes<NR, CW>();
-    if (!smem_set) {
+    int dev = 0;
+    FDE_CUDA(cudaGetDevice(&dev));
+    const int d = dev & 63;
+    if (!smem_set[d]) {
         FDE_CUDA(cudaFuncSetAttribute(k_gemv_bulk<NR, CW>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        smem_set = 1;
+        smem_set[d] = 1;
     }
-    static int nsm = 0;
-    if (!nsm) {
-        int dev = 0;
-        FDE_CUDA(cudaGetDevice(&dev));
-        FDE_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    }
+    if (!nsm_dev[d]) FDE_CUDA(cudaDeviceGetAttribute(&nsm_dev[d], cudaDevAttrMultiProcessorCount, dev));
+    const int nsm = nsm_dev[d];
     const long long nblk = (rows + 7) / 8;
     k_gemv_bulk<NR, CW><<<(unsigned)std::min<long long>(nsm, nblk), 288, smem, s>>>(A, lda, rows, x, ldx, y, ldy);
     FDE_CHECK_LAUNCH();
@@ -381,45 +381,33 @@ __global__ void k_compact_gather(const double* gath, long long rows_max, int wor
     full[c * ldfull + r] = gath[((long long)g * nrhs + c) * rows_max + loc];
 }
 
-struct GatherScratch {
-    DBuf<double> send, recv;
-    DBuf<int64_t> rstart;
-};
-static GatherScratch& gscratch()
+// gathered: world blocks of nrhs columns of rows_max rows (the all-gather
+// layout) -> full: n rows per column (internal order), ldfull
+void comm_compact_gathered(fde_ctx* h, fde_op* op, const double* gathered, double* full, int64_t ldfull, int nrhs)
 {
-    static GatherScratch g;
-    return g;
+    if (h->g_rstart.n < (size_t)op->world) h->g_rstart.alloc(op->world);
+    h->g_rstart.upload(op->rank_r0.data(), op->world, h->stream);
+    dim3 g((unsigned)ceil_div(op->n, 256), (unsigned)nrhs);
+    k_compact_gather<<<g, 256, 0, h->stream>>>(gathered, op->rows_max, op->world, h->g_rstart.p, op->n, full, ldfull,
+                                                nrhs);
+    FDE_CHECK_LAUNCH();
 }
 
 // local: (r1-r0) rows per column with ld = rows_max ; full: n rows with ldfull
 void comm_allgather_rows(fde_ctx* h, fde_op* op, const double* local, double* full, int64_t ldfull, int nrhs)
 {
-    GatherScratch& G = gscratch();
+    if (!h->nccl)
+        fde_fail(FDE_ENCCL, h->virt ? "virtual rank handle: no communicator for the row all-gather"
+                                    : "world > 1 without an NCCL communicator");
     const size_t chunk = (size_t)op->rows_max * nrhs;
-    if (G.recv.n < chunk * h->world) G.recv.alloc(chunk * h->world);
-    if (G.rstart.n < (size_t)h->world) {
-        G.rstart.alloc(h->world);
-    }
-    G.rstart.upload(op->rank_r0.data(), h->world, h->stream);
-    int r = nccl_api().allgather(local, G.recv.p, chunk, /*ncclFloat64*/ 8, h->nccl, h->stream);
+    if (h->g_recv.n < chunk * h->world) h->g_recv.alloc(chunk * h->world);
+    int r = nccl_api().allgather(local, h->g_recv.p, chunk, /*ncclFloat64*/ 8, h->nccl, h->stream);
     if (r != 0) fde_fail(FDE_ENCCL, "ncclAllGather failed");
-    dim3 g((unsigned)ceil_div(op->n, 256), (unsigned)nrhs);
-    k_compact_gather<<<g, 256, 0, h->stream>>>(G.recv.p, op->rows_max, h->world, G.rstart.p, op->n, full, ldfull,
-                                                nrhs);
-    FDE_CHECK_LAUNCH();
+    comm_compact_gathered(h, op, h->g_recv.p, full, ldfull, nrhs);
 }
 
 // --------------------------------------------------- operator application
 // x: internal order (padded, ld ldx >= lda); y: internal order, full n rows.
-struct ApplyScratch {
-    DBuf<double> loc;
-};
-static ApplyScratch& ascratch()
-{
-    static ApplyScratch a;
-    return a;
-}
-
 void op_apply_internal(fde_ctx* h, fde_op* op, const double* x, int64_t ldx, double* y, int64_t ldy, int nrhs,
                        int path)
 {
@@ -441,13 +429,14 @@ void op_apply_internal(fde_ctx* h, fde_op* op, const double* x, int64_t ldx, dou
         prof_end(h, pi);
         return;
     }
-    ApplyScratch& S = ascratch();
+    if (!h->nccl)
+        fde_fail(FDE_ENCCL, "virtual rank handle: the full operator application needs the row all-gather");
     const size_t need = (size_t)op->rows_max * nrhs;
-    if (S.loc.n < need) S.loc.alloc(need);
+    if (h->mv_loc.n < need) h->mv_loc.alloc(need);
     const int pi = prof_begin(h, PROF_GEMV, gemv_bytes);
-    dense_gemv(h, op, x, ldx, S.loc.p, op->rows_max, nrhs);
+    dense_gemv(h, op, x, ldx, h->mv_loc.p, op->rows_max, nrhs);
     prof_end(h, pi);
-    comm_allgather_rows(h, op, S.loc.p, y, ldy, nrhs);
+    comm_allgather_rows(h, op, h->mv_loc.p, y, ldy, nrhs);
 }
 
 // ------------------------------------------------- dense exports (tests)

@@ -191,16 +191,6 @@ __global__ void k_toeplitz_scatter(const double* wv, const double* x, long long 
     y[c * ldy + r] = v + rho * mass;
 }
 
-struct ToeplitzScratch {
-    DBuf<double2> Dhat, What;
-    DBuf<double> wv;
-};
-static ToeplitzScratch& tscratch()
-{
-    static ToeplitzScratch t;
-    return t;
-}
-
 static int ilog2(int L)
 {
     int k = 0;
@@ -265,11 +255,14 @@ void toeplitz_prepare(fde_ctx* h, fde_op* op)
 void toeplitz_matvec(fde_ctx* h, fde_op* op, const double* x, int64_t ldx, double* y, int64_t ldy, int nrhs)
 {
     const int N = op->N, P = op->P, L = op->L, logL = ilog2(L);
-    ToeplitzScratch& S = tscratch();
+    // (handle-owned scratch: the spectra of x and of the product, the inverse transforms)
+    DBuf<double2>& Dhat = h->t_Dhat;
+    DBuf<double2>& What = h->t_What;
+    DBuf<double>& wv = h->t_wv;
     const size_t need = (size_t)nrhs * P * L;
-    if (S.Dhat.n < need) S.Dhat.alloc(need);
-    if (S.What.n < need) S.What.alloc(need);
-    if (S.wv.n < (size_t)nrhs * P * N) S.wv.alloc((size_t)nrhs * P * N);
+    if (Dhat.n < need) Dhat.alloc(need);
+    if (What.n < need) What.alloc(need);
+    if (wv.n < (size_t)nrhs * P * N) wv.alloc((size_t)nrhs * P * N);
     const double2* tw = reinterpret_cast<const double2*>(op->twid.p);
     const size_t smem = (size_t)L * sizeof(double2);
     const double2* spec = reinterpret_cast<const double2*>(op->spec.p);
@@ -278,15 +271,15 @@ void toeplitz_matvec(fde_ctx* h, fde_op* op, const double* x, int64_t ldx, doubl
     for (int pass = 0; pass < (op->geometric ? 2 : 1); ++pass) {
         const double* win = (op->geometric && pass == 0) ? op->wsc.p : nullptr;
         const double* wout = (op->geometric && pass == 1) ? op->wsc.p : nullptr;
-        k_gather_fft<<<dim3(P, nrhs), FFT_THREADS, smem, h->stream>>>(x, ldx, N, P, L, logL, tw, S.Dhat.p, win);
+        k_gather_fft<<<dim3(P, nrhs), FFT_THREADS, smem, h->stream>>>(x, ldx, N, P, L, logL, tw, Dhat.p, win);
         FDE_CHECK_LAUNCH();
         k_symbol_apply<<<dim3((unsigned)ceil_div((long long)L * P, 256), nrhs), 256, 0, h->stream>>>(
-            spec + (size_t)pass * L * P * P, S.Dhat.p, P, L, nrhs, S.What.p);
+            spec + (size_t)pass * L * P * P, Dhat.p, P, L, nrhs, What.p);
         FDE_CHECK_LAUNCH();
-        k_ifft<<<dim3(P, nrhs), FFT_THREADS, smem, h->stream>>>(S.What.p, N, P, L, logL, tw, S.wv.p, wout);
+        k_ifft<<<dim3(P, nrhs), FFT_THREADS, smem, h->stream>>>(What.p, N, P, L, logL, tw, wv.p, wout);
         FDE_CHECK_LAUNCH();
     }
     k_toeplitz_scatter<<<dim3((unsigned)ceil_div(op->n, 256), nrhs), 256, 0, h->stream>>>(
-        S.wv.p, x, ldx, op->tab.nodes.p, op->tab.mref.p, N, P, op->n, op->prob.rho, y, ldy);
+        wv.p, x, ldx, op->tab.nodes.p, op->tab.mref.p, N, P, op->n, op->prob.rho, y, ldy);
     FDE_CHECK_LAUNCH();
 }

@@ -40,7 +40,8 @@ EXPORTED = [
     "hlu_factor", "fde_hlu_get_info", "fde_hlu_dense_internal", "precond_apply", "solve", "fde_solve",
     "fde_free_operator", "fde_free_hmatrix", "fde_free_hlu", "fde_profile", "fde_profile_collect",
     "fde_launch_count", "fde_shard_rows", "fde_debug_hlu_mode", "fde_debug_pool_bytes",
-    "fde_operator_wait", "fde_hmatrix_wait",
+    "fde_operator_wait", "fde_hmatrix_wait", "fde_create_virtual_rank", "fde_operator_rows_internal",
+    "fde_shard_matvec", "fde_debug_compact_gather",
 ]
 
 
@@ -88,12 +89,12 @@ class HluInfo(ctypes.Structure):
 
 class SolveOpts(ctypes.Structure):
     _fields_ = [("method", ctypes.c_int32), ("tol", ctypes.c_double), ("maxiter", ctypes.c_int32),
-                ("restart", ctypes.c_int32), ("path", ctypes.c_int32)]
+                ("restart", ctypes.c_int32), ("path", ctypes.c_int32), ("verify", ctypes.c_int32)]
 
 
 class SolveReport(ctypes.Structure):
     _fields_ = [("iterations", ctypes.c_int32), ("matvecs", ctypes.c_int32), ("converged", ctypes.c_int32),
-                ("relres", ctypes.c_double), ("solve_ms", ctypes.c_double)]
+                ("relres", ctypes.c_double), ("solve_ms", ctypes.c_double), ("relres_true", ctypes.c_double)]
 
 
 def lib_path() -> str:
@@ -109,6 +110,10 @@ def lib():
         L = ctypes.CDLL(_SO)
         vp, i32, i64, dbl = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_double
         L.fde_create.argtypes = [ctypes.POINTER(vp), i32, vp, vp, i32, i32]
+        L.fde_create_virtual_rank.argtypes = [ctypes.POINTER(vp), i32, vp, i32, i32]
+        L.fde_operator_rows_internal.argtypes = [vp, vp, vp, i64]
+        L.fde_shard_matvec.argtypes = [vp, vp, vp, i64, vp, i64, i32]
+        L.fde_debug_compact_gather.argtypes = [vp, vp, vp, vp, i64, i32]
         L.fde_destroy.argtypes = [vp]
         L.fde_destroy.restype = None
         L.fde_last_error.argtypes = [vp]
@@ -161,14 +166,19 @@ class Handle:
     """fde_create on the current torch CUDA stream (one process per GPU)."""
 
     def __init__(self, device: int = 0, stream: Optional[int] = None, nccl_id: Optional[bytes] = None,
-                 rank: int = 0, world: int = 1):
+                 rank: int = 0, world: int = 1, virtual: bool = False):
+        """virtual=True: fde_create_virtual_rank (rank `rank` of `world` without a
+        communicator; test helper for the sharded path on one GPU)."""
         import torch
         if stream is None:
             stream = torch.cuda.current_stream(device).cuda_stream
         self.h = ctypes.c_void_p()
-        idbuf = ctypes.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
-        rc = lib().fde_create(ctypes.byref(self.h), device, ctypes.c_void_p(stream),
-                              ctypes.cast(idbuf, ctypes.c_void_p) if idbuf is not None else None, rank, world)
+        if virtual:
+            rc = lib().fde_create_virtual_rank(ctypes.byref(self.h), device, ctypes.c_void_p(stream), rank, world)
+        else:
+            idbuf = ctypes.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
+            rc = lib().fde_create(ctypes.byref(self.h), device, ctypes.c_void_p(stream),
+                                  ctypes.cast(idbuf, ctypes.c_void_p) if idbuf is not None else None, rank, world)
         if rc != 0:
             raise FdeError(rc, lib().fde_last_error(None).decode())
         self.device, self.rank, self.world = device, rank, world
@@ -287,6 +297,33 @@ def operator_dense_paper(handle: Handle, op: Operator):
     return A     # row-major: A[I, J]
 
 
+def operator_rows_internal(handle: Handle, op: Operator):
+    """This rank's dense rows (internal order), shape (row_end - row_begin, n)."""
+    import torch
+    inf = op.info
+    A = torch.empty((max(inf.row_end - inf.row_begin, 0), op.n), dtype=torch.float64, device=f"cuda:{handle.device}")
+    _check(lib().fde_operator_rows_internal(handle.h, op.ptr, _ptr(A), op.n), handle.h)
+    return A
+
+
+def shard_matvec(handle: Handle, op: Operator, x, rows_max: int):
+    """Local rows of A x (internal order) on this rank's shard: (nrhs, rows_max)."""
+    import torch
+    x = x.reshape(-1, op.n).contiguous()
+    y = torch.zeros((x.shape[0], rows_max), dtype=torch.float64, device=x.device)
+    _check(lib().fde_shard_matvec(handle.h, op.ptr, _ptr(x), op.n, _ptr(y), rows_max, x.shape[0]), handle.h)
+    return y
+
+
+def compact_gather(handle: Handle, op: Operator, gathered, nrhs: int):
+    """The post-all-gather compaction on a (world, nrhs, rows_max) buffer -> (nrhs, n) paper order."""
+    import torch
+    g = gathered.contiguous()
+    y = torch.empty((nrhs, op.n), dtype=torch.float64, device=g.device)
+    _check(lib().fde_debug_compact_gather(handle.h, op.ptr, _ptr(g), _ptr(y), op.n, nrhs), handle.h)
+    return y
+
+
 def operator_boundary_columns(handle: Handle, op: Operator):
     import torch
     B = torch.empty((2, op.n), dtype=torch.float64, device=f"cuda:{handle.device}")
@@ -295,8 +332,10 @@ def operator_boundary_columns(handle: Handle, op: Operator):
 
 
 class HMatrix:
-    def __init__(self, handle, ptr, n):
-        self.handle, self.ptr, self.n = handle, ptr, n
+    def __init__(self, handle, ptr, n, op=None):
+        # the library's H-matrix points at its operator (fde.h lifetime rule):
+        # keep the Python object alive as long as this one
+        self.handle, self.ptr, self.n, self._op = handle, ptr, n, op
         inf = HMatrixInfo()
         _check(lib().fde_hmatrix_get_info(ptr, ctypes.byref(inf)))   # (does not wait)
         self._info = inf
@@ -324,7 +363,7 @@ class HMatrix:
 def hmatrix_build(handle: Handle, op: Operator, R: int, lam: float = 1.0, n_min: int = 16) -> HMatrix:
     out = ctypes.c_void_p()
     _check(lib().hmatrix_build(handle.h, op.ptr, R, lam, n_min, ctypes.byref(out)), handle.h)
-    return HMatrix(handle, out, op.n)
+    return HMatrix(handle, out, op.n, op)
 
 
 def hmatrix_dense_paper(handle: Handle, hm: HMatrix):
@@ -335,8 +374,9 @@ def hmatrix_dense_paper(handle: Handle, hm: HMatrix):
 
 
 class HLU:
-    def __init__(self, handle, ptr, n):
-        self.handle, self.ptr, self.n = handle, ptr, n
+    def __init__(self, handle, ptr, n, hm=None):
+        # keeps its H-matrix (and through it the operator) alive: fde.h lifetime rule
+        self.handle, self.ptr, self.n, self._hm = handle, ptr, n, hm
         inf = HluInfo()
         _check(lib().fde_hlu_get_info(ptr, ctypes.byref(inf)))
         self.info = inf
@@ -356,7 +396,7 @@ class HLU:
 def hlu_factor(handle: Handle, hm: HMatrix, tol: float = 1e-3) -> HLU:
     out = ctypes.c_void_p()
     _check(lib().hlu_factor(handle.h, hm.ptr, tol, ctypes.byref(out)), handle.h)
-    return HLU(handle, out, hm.n)
+    return HLU(handle, out, hm.n, hm)
 
 
 def hlu_dense_internal(handle: Handle, lu: HLU):
@@ -383,12 +423,13 @@ def precond_apply(handle: Handle, lu: HLU, r, out=None):
 
 
 def solve(handle: Handle, op: Operator, lu: Optional[HLU], G, method: int = GMRES, tol: float = 1e-12,
-          maxiter: int = 500, restart: int = 50, path: int = PATH_AUTO, out=None):
-    """X = solve(A~^{-1} A X = A~^{-1} G); returns (X, report)."""
+          maxiter: int = 500, restart: int = 50, path: int = PATH_AUTO, out=None, verify: bool = True):
+    """X = solve(A~^{-1} A X = A~^{-1} G); returns (X, report).  verify (GMRES):
+    confirm convergence on the recomputed preconditioned residual (report.relres_true)."""
     import torch
     G = G.reshape(-1, op.n).contiguous()
     X = out if out is not None else torch.empty_like(G)
-    o = SolveOpts(method, tol, maxiter, restart, path)
+    o = SolveOpts(method, tol, maxiter, restart, path, 1 if verify else 0)
     rep = SolveReport()
     _check(lib().solve(handle.h, op.ptr, lu.ptr if lu is not None else None, _ptr(G), _ptr(X), G.shape[0], op.n,
                        ctypes.byref(o), ctypes.byref(rep)), handle.h)

@@ -10,6 +10,7 @@ import pytest
 
 import fde_inputs as fi
 import oracle as O
+from parity_util import md_check
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -171,11 +172,7 @@ def test_unpreconditioned_gmres_matches_oracle(fde, h, p):
     X, rep = fde.solve(h, op, None, G, tol=1e-13, maxiter=4000, restart=200)
     so = oracle_system(p)
     Go = O.rhs(p, so, p.forcings[0])
-    Xo = O.solve_dense(so.A, Go)
-    x = X.cpu().numpy()[0]
-    D = np.abs(np.diag(so.A))
-    err = np.sqrt(np.sum(D * (x - Xo) ** 2) / np.sum(D * Xo ** 2))
-    assert err <= 1e-9, (err, rep.iterations)
+    md_check(p, X.cpu().numpy()[0], so, Go)      # M-D: D-norm, u_h pointwise, backward error
     op.free()
 
 
@@ -325,11 +322,7 @@ def test_hlu_preconditioned_gmres_matches_oracle(fde, h, case, hlu_mode):
         assert e.name == "FDE_EMAXITER"
         its0 = 10 ** 9
     so = oracle_system(p)
-    Xo = O.solve_dense(so.A, O.rhs(p, so, p.forcings[0]))
-    x = X.cpu().numpy()[0]
-    D = np.abs(np.diag(so.A))
-    err = np.sqrt(np.sum(D * (x - Xo) ** 2) / np.sum(D * Xo ** 2))
-    assert err <= 1e-9, err
+    md_check(p, X.cpu().numpy()[0], so, O.rhs(p, so, p.forcings[0]))   # M-D, all three parts
     assert rep.iterations < its0
     # the factor approximates A~: ||A~ z - r|| small relative to ||r||
     At, _ = O.hmatrix_dense(p, so, R=p.R, lam=1.0, n_min=n_min)
@@ -385,10 +378,8 @@ def test_example51_bicgstab_iterations_pattern(fde, h):
         its.append(rep.iterations)
         if R == 7:
             so = oracle_system(p)
-            Xo = O.solve_dense(so.A, O.rhs(p, so, p.forcings[0]))
             x = X.cpu().numpy()[0]
-            D = np.abs(np.diag(so.A))
-            assert np.sqrt(np.sum(D * (x - Xo) ** 2) / np.sum(D * Xo ** 2)) <= 1e-9
+            md_check(p, x, so, O.rhs(p, so, p.forcings[0]))
             xis = np.linspace(-1, 1, 9)
             uh = O.eval_solution(p, x, xis)
             hh = np.diff(p.nodes)
