@@ -224,6 +224,18 @@ int fde_debug_hlu_mode(int mode)
     API_END(h)
 }
 
+extern unsigned long long* g_apply_tl;
+extern size_t g_apply_tl_n;
+// debug: copy the last preconditioner-application timeline (FDE_APPLY_TIMELINE=1) to host
+int fde_debug_apply_timeline(unsigned long long* out, long long cap)
+{
+    if (!g_apply_tl) return 0;
+    const size_t n = std::min((size_t)cap, g_apply_tl_n);
+    if (cudaDeviceSynchronize() != cudaSuccess) return FDE_ECUDA;
+    if (cudaMemcpy(out, g_apply_tl, n * 8, cudaMemcpyDeviceToHost) != cudaSuccess) return FDE_ECUDA;
+    return (int)n;
+}
+
 long long fde_launch_count(void) { return __atomic_load_n(&g_fde_launches, __ATOMIC_RELAXED); }
 
 // Row-block partition of the dense operator (host logic, no device needed):

@@ -2163,6 +2163,19 @@ struct SLeaf {
     int l_lo, l_hi;         // low-rank row contributions
     int kq;                 // max kc over [l_lo, l_hi)
     int p_lo, p_hi;         // projections enabled after this leaf
+    int wA;                 // flattened width of the row terms: sum of dense nc + low-rank kc
+    int s_lo, s_hi;         // k_apply_pf: segments of the row terms
+    int pt_lo, pt_hi;       // k_apply_pf: projection tasks enabled after this leaf
+    int wAp, mp;            // k_apply_pf: row strides of the packed copies (wA, m rounded up to even)
+    long long pa_off, pb_off;   // k_apply_pf: offsets of the leaf's rows in packA / packB
+};
+// k_apply_pf's flattened row-term segment (host-built): dense columns read x + off,
+// low-rank columns the nchunk projection partials at t + off + q * nchunk
+struct PfSegH {
+    long long off;
+    const double* M;        // factor entries of the leaf's row 0 (D + roff / U + roff), column stride ldm
+    long long ldm;
+    int start, ncols, nchunk, pad;
 };
 struct SDense {
     const double* D;        // leaf rows x nc, column-major, ld = ldd
@@ -2195,6 +2208,10 @@ struct SweepDev {
     const SDense* dense;
     const SLRRow* lrr;
     const SProj* proj;
+    const PfSegH* pseg = nullptr;   // k_apply_pf
+    const int4* ptask = nullptr;    // k_apply_pf: (projection, column, chunk)
+    const double* packA = nullptr;  // k_apply_pf: leaf row terms, row-major [row][wAp]
+    const double* packB = nullptr;  // k_apply_pf: leaf inverses, row-major [row][mp]
 };
 
 __device__ __forceinline__ double ldcg(const double* p) { return __ldcg(p); }
@@ -2546,6 +2563,424 @@ __global__ void __launch_bounds__(APPLY_THREADS)
 }
 
 
+// ------------------------------------------------------------------------
+// k_apply_pf: the leaf-sequential substitutions for up to APPLY_RC right-hand
+// sides with the factor data PREFETCHED.  Per leaf k of a sweep (
+// same arithmetic as k_apply, different summation order):
+//   phase A  z_k = x_k - sum_dense D x_cols - sum_lowrank U t      (rows of leaf k)
+//            + the projections t = V^T x_sigma enabled by the previous leaf
+//   phase B  x_k = Inv_k z_k
+// with a grid barrier after each phase.  Only x, z and t depend on earlier
+// steps; the factor entries (D, U rows of this CTA, the inverse rows) do not,
+// so every phase's entries are copied into shared memory with cp.async one
+// phase AHEAD (A(k) during B(k-1), B(k) during A(k)) and each phase after its
+// barrier only waits for the x / z / t loads.  The CTA's rows of a leaf are
+// summed by T = 512 / nrp threads each (warp shuffles, then a fixed-order sum
+// over the warps of the row: deterministic).
+#define PF_THREADS 512
+#define PF_CAP_A 10240            // doubles of staged phase-A factor entries (80 KB)
+#define PF_CAP_B 8192             // doubles of staged phase-B factor entries (64 KB)
+#define PF_CAP_S 6144             // doubles of gathered sources (x / t / z) of one phase (48 KB)
+#define PF_SMEM ((PF_CAP_A + PF_CAP_B + PF_CAP_S) * 8)
+#define PF_MAXLEAF 128            // leaf descriptors of both sweeps kept in shared memory
+
+__device__ __forceinline__ void pf_cp8(double* sdst, const double* gsrc)
+{
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void pf_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void pf_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+
+struct PfRows {
+    int r_lo, nr;
+};
+__device__ __forceinline__ PfRows pf_rows(int m)
+{
+    const int per = max(1, (m + (int)gridDim.x - 1) / (int)gridDim.x);
+    PfRows R;
+    R.r_lo = blockIdx.x * per;
+    R.nr = max(0, min(m - R.r_lo, per));
+    return R;
+}
+
+// flattened row terms of a leaf in phase A: dense columns (source x + c0 + j) then
+// low-rank columns (source = the sum of the nchunk projection partials t + tslot + q*nchunk)
+#define PF_MAXSEG 64
+struct PfSeg {
+    const double* src;      // x + c0 (dense) or t + tslot (low rank), column 0 of the RHS block
+    const double* M;        // factor entries of the leaf's row 0, column stride ldm
+    long long ldm;
+    int start, ncols, nchunk;   // nchunk = 0: dense
+};
+
+// stage phase A of leaf L: the segment table and this CTA's rows of every dense /
+// low-rank row term, row-major [row][flattened column]
+__device__ __forceinline__ void pf_cp16(double* sdst, const double* gsrc)
+{
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gsrc) : "memory");
+}
+
+// this CTA's rows of a packed (row-major, even stride) leaf block -> shared memory:
+// one contiguous range, 16-byte copies (coalesced, DRAM-friendly), up to cap doubles
+__device__ __forceinline__ void pf_stage_rows(const double* src, int count, int cap, double* buf)
+{
+    const int n2 = min(count, cap) >> 1;
+    for (int e = threadIdx.x; e < n2; e += PF_THREADS) pf_cp16(buf + 2 * e, src + 2 * e);
+}
+
+__device__ void pf_stage_A(const SweepDev& S, const SLeaf& L, double* buf, PfSeg* seg, const double* x,
+                           const double* t)
+{
+    const int nseg = L.s_hi - L.s_lo;
+    if (threadIdx.x < nseg) {
+        const PfSegH G = S.pseg[L.s_lo + threadIdx.x];
+        PfSeg g;
+        g.src = (G.nchunk == 0 ? x : t) + G.off;
+        g.M = G.M;
+        g.ldm = G.ldm;
+        g.start = G.start;
+        g.ncols = G.ncols;
+        g.nchunk = G.nchunk;
+        seg[threadIdx.x] = g;
+    }
+    const PfRows R = pf_rows(L.m);
+    if (R.nr > 0) pf_stage_rows(S.packA + L.pa_off + (long long)R.r_lo * L.wAp, R.nr * L.wAp, PF_CAP_A, buf);
+}
+
+__device__ void pf_stage_B(const SweepDev& S, const SLeaf& L, double* buf)
+{
+    const PfRows R = pf_rows(L.m);
+    if (R.nr > 0) pf_stage_rows(S.packB + L.pb_off + (long long)R.r_lo * L.mp, R.nr * L.mp, PF_CAP_B, buf);
+}
+
+// sum over the T threads of each row group (T = PF_THREADS / nrp), fixed order;
+// returns the row sum to the first thread of the group
+__device__ __forceinline__ double pf_group_sum(double v, int T, double* red)
+{
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (T < 32) {
+        for (int o = T >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        return v;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) red[w] = v;
+    __syncthreads();
+    double s = 0.0;
+    if ((threadIdx.x % T) == 0) {
+        const int w0 = threadIdx.x >> 5, nw = T >> 5;
+        for (int q = 0; q < nw; ++q) s += red[w0 + q];
+    }
+    __syncthreads();
+    return s;
+}
+
+// row-term entries per thread whose source loads are in flight together (x RC columns)
+#define PF_BATCH_OF(RC) ((RC) <= 2 ? 8 : ((RC) == 4 ? 4 : 2))
+
+// segment of flattened column j (binary search over the staged starts)
+__device__ __forceinline__ int pf_seg_of(const PfSeg* seg, int nseg, int j)
+{
+    int lo = 0, hi = nseg - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (seg[mid].start <= j) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+// source value of flattened column j for right-hand side c: x (dense) or the sum of
+// the projection partials t (low rank), with the partial loads in flight together
+__device__ __forceinline__ double pf_source(const PfSeg& g, int j, int c, long long ldx, int tstride)
+{
+    const int jj = j - g.start;
+    if (g.nchunk == 0) return ldcg(g.src + (long long)c * ldx + jj);
+    return ldcg(g.src + (long long)c * tstride + jj * g.nchunk);   // (the chunk partials folded into chunk 0)
+}
+
+// fold the chunk partials of the projections of the blocks enabled by leaf Pv
+// into their chunk 0 (one thread per (block, column q, right-hand side), the
+// partials added in chunk order: deterministic); threads of the LAST CTAs first
+__device__ void pf_fold(const SweepDev& S, const SLeaf& Pv, int nrhs, double* t, int tstride)
+{
+    const int nthr = gridDim.x * PF_THREADS;
+    const int gt = (gridDim.x - 1 - blockIdx.x) * PF_THREADS + threadIdx.x;
+    int base = 0;
+    for (int p = Pv.p_lo; p < Pv.p_hi; ++p) {
+        const SProj Pj = S.proj[p];
+        const int cnt = Pj.kc * nrhs;
+        if (Pj.nchunk > 1)
+            for (int i = gt - base; i < cnt; i += nthr) {
+                if (i < 0) continue;
+                const int q = i % Pj.kc, c = i / Pj.kc;
+                double* tp = t + (long long)c * tstride + Pj.tslot + q * Pj.nchunk;
+                double v[8];
+                double sum = 0.0;
+                for (int ch = 0; ch < Pj.nchunk; ch += 8) {   // eight partials in flight
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) v[u] = ch + u < Pj.nchunk ? ldcg(tp + ch + u) : 0.0;
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) sum += v[u];
+                }
+                tp[0] = sum;
+            }
+        base += cnt;
+    }
+}
+
+// Phase A.  The sources of the leaf's row terms (the x entries of the dense
+// columns, the summed projections of the low-rank columns) are the same for every
+// row of the CTA: they are gathered ONCE per CTA into shared memory (one round of
+// loads, four entries per thread in flight), then every row group multiplies its
+// staged factor entries with them from shared memory.
+template <int RC>
+__device__ void pf_phase_A(const SweepDev& S, const SLeaf& L, const double* x, long long ldx, int nrhs, double* z,
+                           int tstride, const double* buf, const PfSeg* seg, double* bufS, double* red)
+{
+    const PfRows R = pf_rows(L.m);
+    if (R.nr == 0) return;            // (uniform per CTA: no barrier inside is skipped by part of it)
+    const int W = L.wA;
+    const int nseg = L.s_hi - L.s_lo;
+    const bool ssm = W * nrhs <= PF_CAP_S;
+    if (ssm) {
+        for (int e0 = threadIdx.x; e0 < W * nrhs; e0 += 4 * PF_THREADS) {
+            double val[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int e = e0 + u * PF_THREADS;
+                val[u] = 0.0;
+                if (e < W * nrhs) {
+                    const int c = e / W, j = e - c * W;
+                    val[u] = pf_source(seg[pf_seg_of(seg, nseg, j)], j, c, ldx, tstride);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (e0 + u * PF_THREADS < W * nrhs) bufS[e0 + u * PF_THREADS] = val[u];
+        }
+        __syncthreads();
+    }
+    int nrp = 1;
+    while (nrp < R.nr) nrp <<= 1;
+    const int T = PF_THREADS / nrp;
+    const int row = threadIdx.x / T, li = threadIdx.x % T;
+    double acc[RC];
+#pragma unroll
+    for (int c = 0; c < RC; ++c) acc[c] = 0.0;
+    if (row < R.nr) {
+        const int grow = R.r_lo + row;
+        int sg = 0;
+        for (int j = li; j < W; j += T) {
+            const int idx = row * L.wAp + j;
+            // (beyond the staging capacity: straight from the packed copy)
+            const double a = idx < PF_CAP_A ? buf[idx] : S.packA[L.pa_off + (long long)grow * L.wAp + j];
+            if (ssm) {
+#pragma unroll
+                for (int c = 0; c < RC; ++c)
+                    if (c < nrhs) acc[c] = fma(a, bufS[c * W + j], acc[c]);
+            } else {
+                while (sg + 1 < nseg && j >= seg[sg + 1].start) ++sg;
+#pragma unroll
+                for (int c = 0; c < RC; ++c)
+                    if (c < nrhs) acc[c] = fma(a, pf_source(seg[sg], j, c, ldx, tstride), acc[c]);
+            }
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < RC; ++c) {
+        if (c >= nrhs) break;
+        const double sum = pf_group_sum(acc[c], T, red);
+        if (row < R.nr && li == 0) {
+            const int grow = R.r_lo + row;
+            z[(long long)c * L.m + grow] = ldcg(x + (long long)c * ldx + L.r0 + grow) - sum;
+        }
+    }
+}
+
+// Phase B: x_k = Inv_k z_k, z_k gathered once per CTA into shared memory.
+template <int RC>
+__device__ void pf_phase_B(const SweepDev& S, const SLeaf& L, double* x, long long ldx, int nrhs, const double* z, const double* buf,
+                           double* bufS, double* red)
+{
+    const PfRows R = pf_rows(L.m);
+    if (R.nr == 0) return;
+    const bool ssm = L.m * nrhs <= PF_CAP_S;
+    if (ssm) {
+        for (int e0 = threadIdx.x; e0 < L.m * nrhs; e0 += 4 * PF_THREADS) {
+            double val[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int e = e0 + u * PF_THREADS;
+                val[u] = e < L.m * nrhs ? ldcg(z + e) : 0.0;   // (z: column stride m)
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (e0 + u * PF_THREADS < L.m * nrhs) bufS[e0 + u * PF_THREADS] = val[u];
+        }
+        __syncthreads();
+    }
+    int nrp = 1;
+    while (nrp < R.nr) nrp <<= 1;
+    const int T = PF_THREADS / nrp;
+    const int row = threadIdx.x / T, li = threadIdx.x % T;
+    double acc[RC];
+#pragma unroll
+    for (int c = 0; c < RC; ++c) acc[c] = 0.0;
+    if (row < R.nr) {
+        const int grow = R.r_lo + row;
+        for (int j = li; j < L.m; j += T) {
+            const int idx = row * L.mp + j;
+            const double a = idx < PF_CAP_B ? buf[idx] : S.packB[L.pb_off + (long long)grow * L.mp + j];
+#pragma unroll
+            for (int c = 0; c < RC; ++c)
+                if (c < nrhs) acc[c] = fma(a, ssm ? bufS[c * L.m + j] : ldcg(z + (long long)c * L.m + j), acc[c]);
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < RC; ++c) {
+        if (c >= nrhs) break;
+        const double sum = pf_group_sum(acc[c], T, red);
+        if (row < R.nr && li == 0) x[(long long)c * ldx + L.r0 + R.r_lo + row] = sum;
+    }
+}
+
+// projections t = V^T x_sigma of the blocks whose sigma completed with leaf Pv:
+// one warp per (block, column, 256-row chunk), right-hand sides four at a time
+__device__ void pf_projections(const SweepDev& S, const SLeaf& Pv, const double* x, long long ldx, int nrhs, double* t,
+                               int tstride)
+{
+    // warps of the LAST CTAs first: with m rows over the grid the first ceil(m / rows_per)
+    // CTAs carry the leaf rows, the others would idle
+    const int nwarps = gridDim.x * (PF_THREADS / 32);
+    const int gw = (gridDim.x - 1 - blockIdx.x) * (PF_THREADS / 32) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    for (int task = Pv.pt_lo + gw; task < Pv.pt_hi; task += nwarps) {
+        const int4 tk = S.ptask[task];
+        const int p = tk.x;
+        const SProj Pj = S.proj[p];
+        const int col = tk.y, ch = tk.z;
+        const int i0 = ch * PROJ_CHUNK, i1 = min(Pj.n, i0 + PROJ_CHUNK);
+        const double* vc = Pj.V + (long long)col * Pj.ldv;
+        double v[PROJ_CHUNK / 32];
+#pragma unroll
+        for (int u = 0; u < PROJ_CHUNK / 32; ++u) {
+            const int i = i0 + lane + 32 * u;
+            v[u] = (i < i1) ? vc[i] : 0.0;
+        }
+        for (int c0 = 0; c0 < nrhs; c0 += 4) {
+            double a[4][PROJ_CHUNK / 32];
+#pragma unroll
+            for (int cc = 0; cc < 4; ++cc) {
+                const double* xc = x + (long long)min(c0 + cc, nrhs - 1) * ldx + Pj.c0;
+#pragma unroll
+                for (int u = 0; u < PROJ_CHUNK / 32; ++u) {
+                    const int i = i0 + lane + 32 * u;
+                    a[cc][u] = (i < i1) ? v[u] * ldcg(xc + i) : 0.0;
+                }
+            }
+#pragma unroll
+            for (int cc = 0; cc < 4; ++cc) {
+                double acc = 0.0;
+#pragma unroll
+                for (int u = 0; u < PROJ_CHUNK / 32; ++u) acc += a[cc][u];
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+                if (lane == 0 && c0 + cc < nrhs) t[(long long)(c0 + cc) * tstride + Pj.tslot + col * Pj.nchunk + ch] = acc;
+            }
+        }
+    }
+}
+
+template <int RC>
+__global__ void __launch_bounds__(PF_THREADS, 1)
+    k_apply_pf(SweepDev fwd, SweepDev bwd, double* x, long long ldx, int nrhs, double* z, double* t, int tstride,
+               unsigned long long* tl)
+{
+    // tl (debug timeline, FDE_APPLY_TIMELINE): per step and CTA the globaltimer at
+    // [start A, A computed, B staged, B computed]
+    auto mark = [&](int s, int q) {
+        if (tl && threadIdx.x == 0) {
+            unsigned long long g;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+            tl[((size_t)s * gridDim.x + blockIdx.x) * 4 + q] = g;
+        }
+    };
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ __align__(16) double pf_smem[];
+    double* bufA = pf_smem;
+    double* bufB = pf_smem + PF_CAP_A;
+    double* bufS = bufB + PF_CAP_B;
+    __shared__ double red[PF_THREADS / 32];
+    __shared__ PfSeg seg[PF_MAXSEG];
+    __shared__ SLeaf sleaf[2][PF_MAXLEAF];   // the leaf descriptors (off the per-step critical path)
+    const int nl = fwd.nleaf;
+    const bool lsm = nl <= PF_MAXLEAF;
+    if (lsm)
+        for (int i = threadIdx.x; i < 2 * nl; i += PF_THREADS) sleaf[i / nl][i % nl] = (i < nl ? fwd : bwd).leaf[i % nl];
+    __syncthreads();
+    auto leaf = [&](bool back, int k) -> SLeaf { return lsm ? sleaf[back][k] : (back ? bwd : fwd).leaf[k]; };
+    pf_stage_A(fwd, leaf(false, 0), bufA, seg, x, t);
+    pf_commit();
+    for (int s = 0; s < 2 * nl; ++s) {
+        const bool back = s >= nl;
+        const SweepDev& S = back ? bwd : fwd;
+        const int k = back ? 2 * nl - 1 - s : s;
+        const SLeaf L = leaf(back, k);
+        // ---- phase A(k)   (x of the previous leaf complete)
+        if (s > 0) grid.sync();
+        mark(s, 0);
+        pf_stage_B(S, L, bufB);
+        pf_commit();
+        pf_wait1();                // A(k) staged (B(k) may still be in flight)
+        __syncthreads();
+        pf_phase_A<RC>(S, L, x, ldx, nrhs, z, tstride, bufA, seg, bufS, red);
+        // the projections enabled by the previous leaf (first read by leaf k+1: the
+        // admissibility gap) beside phase A, their chunk partials folded beside phase B
+        const int prev = (s == 0 || s == nl) ? -1 : (back ? k + 1 : k - 1);
+        if (prev >= 0) pf_projections(S, leaf(back, prev), x, ldx, nrhs, t, tstride);
+        mark(s, 1);
+        grid.sync();               // z_k complete
+        // ---- phase B(k)
+        asm volatile("cp.async.wait_all;\n" ::: "memory");   // B(k) staged
+        __syncthreads();
+        mark(s, 2);
+        pf_phase_B<RC>(S, L, x, ldx, nrhs, z, bufB, bufS, red);
+        if (prev >= 0) pf_fold(S, leaf(back, prev), nrhs, t, tstride);
+        mark(s, 3);
+        // stage A(k+1) behind B(k): its copies overlap the barrier
+        if (s + 1 < 2 * nl) {
+            const bool nb = s + 1 >= nl;
+            const SweepDev& S2 = nb ? bwd : fwd;
+            __syncthreads();       // (the segment table of A(k) is no longer read)
+            pf_stage_A(S2, leaf(nb, nb ? 2 * nl - 2 - s : s + 1), bufA, seg, x, t);
+        }
+        pf_commit();
+    }
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+}
+
+// packed copies for k_apply_pf: tiled 32 x 32 transposes of column-major factor
+// blocks into row-major leaf rows (tile list built on the host)
+struct PackTile {
+    const double* src;      // column-major, ld lds: element (r, j) at src[j * lds + r]
+    double* dst;            // row-major, ld ldd: element (r, j) at dst[r * ldd + j]
+    long long lds, ldd;
+    int rows, cols;         // of this tile (<= 32)
+};
+__global__ void k_pack_tiles(const PackTile* T)
+{
+    __shared__ double tile[32][33];
+    const PackTile P = T[blockIdx.x];
+    for (int j = threadIdx.y; j < P.cols; j += 8)
+        if (threadIdx.x < P.rows) tile[j][threadIdx.x] = P.src[(long long)j * P.lds + threadIdx.x];
+    __syncthreads();
+    for (int r = threadIdx.y; r < P.rows; r += 8)
+        if (threadIdx.x < P.cols) P.dst[(long long)r * P.ldd + threadIdx.x] = tile[threadIdx.x][r];
+}
+
+
 // --------------------------------------------------------- schedule (host)
 struct ApplySched {
     // host copies of the schedule (the many-RHS GEMM path builds its tasks from them)
@@ -2563,9 +2998,13 @@ struct ApplySched {
     DBuf<SDense> dense_f, dense_b;
     DBuf<SLRRow> lrr_f, lrr_b;
     DBuf<SProj> proj_f, proj_b;
+    DBuf<PfSegH> pseg_f, pseg_b;
+    DBuf<int4> ptask_f, ptask_b;
+    DBuf<double> packA_f, packA_b, packB_f, packB_b;   // k_apply_pf's row-major copies
     DBuf<double> inv;       // leaf inverses
     DBuf<double> z, t;
     int nleaf = 0, zmax = 0, tslots = 0;
+    int maxseg = 0;         // most dense + low-rank row terms of one leaf (k_apply_pf's table)
     size_t zcap = 0, tcap = 0;
 };
 
@@ -2681,11 +3120,14 @@ static ApplySched* apply_sched_build(fde_lu* L)
     A->tslots = std::max(tslot, 1);
     auto flatten = [&](std::vector<std::vector<SDense>>& d, std::vector<std::vector<SLRRow>>& l,
                        std::vector<std::vector<SProj>>& p, int which, DBuf<SLeaf>& Lo, DBuf<SDense>& Do,
-                       DBuf<SLRRow>& Ro, DBuf<SProj>& Po) {
+                       DBuf<SLRRow>& Ro, DBuf<SProj>& Po, DBuf<PfSegH>& Go, DBuf<int4>& To) {
         std::vector<SLeaf> lv(nl);
         std::vector<SDense> dv;
         std::vector<SLRRow> rv;
         std::vector<SProj> pv;
+        std::vector<PfSegH> sg;
+        std::vector<int4> tk;
+        long long pa_words = 0, pb_words = 0;
         for (int q = 0; q < nl; ++q) {
             SLeaf& s = lv[q];
             const HCluster& c = S.cl[leafcl[q]];
@@ -2701,6 +3143,30 @@ static ApplySched* apply_sched_build(fde_lu* L)
             s.l_hi = (int)rv.size();
             s.kq = 0;
             for (const SLRRow& r : l[q]) s.kq = std::max(s.kq, r.kc);
+            A->maxseg = std::max(A->maxseg, (int)(d[q].size() + l[q].size()));
+            s.wA = 0;
+            s.s_lo = (int)sg.size();
+            for (const SDense& dd : d[q]) {
+                sg.push_back(PfSegH{dd.c0, dd.D + dd.roff, dd.ldd, s.wA, dd.nc, 0, 0});
+                s.wA += dd.nc;
+            }
+            for (const SLRRow& r : l[q]) {
+                sg.push_back(PfSegH{r.tslot, r.U + r.roff, r.ldu, s.wA, r.kc, r.nchunk, 0});
+                s.wA += r.kc;
+            }
+            s.s_hi = (int)sg.size();
+            s.wAp = (s.wA + 1) & ~1;
+            s.mp = (s.m + 1) & ~1;
+            s.pa_off = pa_words;
+            s.pb_off = pb_words;
+            pa_words += (long long)s.m * s.wAp;
+            pb_words += (long long)s.m * s.mp;
+            s.pt_lo = (int)tk.size();
+            for (size_t pp = 0; pp < p[q].size(); ++pp)
+                for (int col = 0; col < p[q][pp].kc; ++col)
+                    for (int ch = 0; ch < p[q][pp].nchunk; ++ch)
+                        tk.push_back(make_int4((int)(pv.size() + pp), col, ch, 0));
+            s.pt_hi = (int)tk.size();
             s.p_lo = (int)pv.size();
             pv.insert(pv.end(), p[q].begin(), p[q].end());
             s.p_hi = (int)pv.size();
@@ -2713,16 +3179,47 @@ static ApplySched* apply_sched_build(fde_lu* L)
         if (!dv.empty()) Do.upload(dv.data(), dv.size(), L->h->stream); else Do.alloc(1);
         if (!rv.empty()) Ro.upload(rv.data(), rv.size(), L->h->stream); else Ro.alloc(1);
         if (!pv.empty()) Po.upload(pv.data(), pv.size(), L->h->stream); else Po.alloc(1);
+        if (!sg.empty()) Go.upload(sg.data(), sg.size(), L->h->stream); else Go.alloc(1);
+        if (!tk.empty()) To.upload(tk.data(), tk.size(), L->h->stream); else To.alloc(1);
+        // packed row-major copies of every leaf's row terms and inverse (k_apply_pf)
+        DBuf<double>& PA = which ? A->packA_b : A->packA_f;
+        DBuf<double>& PB = which ? A->packB_b : A->packB_f;
+        PA.alloc(std::max<long long>(pa_words, 2));
+        PB.alloc(std::max<long long>(pb_words, 2));
+        std::vector<PackTile> pt;
+        auto add = [&](const double* src, long long lds, int rows, int cols, double* dst, long long ldd) {
+            for (int c0 = 0; c0 < cols; c0 += 32)
+                for (int r0 = 0; r0 < rows; r0 += 32)
+                    pt.push_back(PackTile{src + (long long)c0 * lds + r0, dst + (long long)r0 * ldd + c0, lds, ldd,
+                                          std::min(32, rows - r0), std::min(32, cols - c0)});
+        };
+        for (int q = 0; q < nl; ++q) {
+            const SLeaf& sq = lv[q];
+            for (int g = sq.s_lo; g < sq.s_hi; ++g)
+                add(sg[g].M, sg[g].ldm, sq.m, sg[g].ncols, PA.p + sq.pa_off + sg[g].start, sq.wAp);
+            add(sq.inv, sq.m, sq.m, sq.m, PB.p + sq.pb_off, sq.mp);
+        }
+        if (!pt.empty()) {
+            DBuf<PackTile> dpt;
+            dpt.upload(pt.data(), pt.size(), L->h->stream);
+            for (size_t base = 0; base < pt.size(); base += 1u << 30) {
+                const unsigned cnt = (unsigned)std::min<size_t>(1u << 30, pt.size() - base);
+                k_pack_tiles<<<cnt, dim3(32, 8), 0, L->h->stream>>>(dpt.p + base);
+                FDE_CHECK_LAUNCH();
+            }
+        }
         // (pageable uploads are staged before cudaMemcpyAsync returns: the host
         // vectors may go out of scope without waiting)
     };
-    flatten(df, lf, pf, 0, A->leaf_f, A->dense_f, A->lrr_f, A->proj_f);
-    flatten(db, lb, pb, 1, A->leaf_b, A->dense_b, A->lrr_b, A->proj_b);
+    flatten(df, lf, pf, 0, A->leaf_f, A->dense_f, A->lrr_f, A->proj_f, A->pseg_f, A->ptask_f);
+    flatten(db, lb, pb, 1, A->leaf_b, A->dense_b, A->lrr_b, A->proj_b, A->pseg_b, A->ptask_b);
     return A;
 }
 
 void apply_gemm_path(fde_ctx* h, ApplySched* A, double* x, int64_t ldx, int nrhs);   // hlu2.cu
 
+unsigned long long* g_apply_tl = nullptr;   // debug timeline of the last k_apply_pf (FDE_APPLY_TIMELINE)
+size_t g_apply_tl_n = 0;
 static void apply_sched_run(fde_ctx* h, fde_lu* L, double* x, int64_t ldx, int nrhs)
 {
     ApplySched* A = L->ap;
@@ -2742,9 +3239,44 @@ static void apply_sched_run(fde_ctx* h, fde_lu* L, double* x, int64_t ldx, int n
         A->t.alloc((size_t)A->tslots * nrhs);
         A->tcap = (size_t)A->tslots * nrhs;
     }
-    SweepDev f{A->leaf_f.p, A->nleaf, A->dense_f.p, A->lrr_f.p, A->proj_f.p};
-    SweepDev b{A->leaf_b.p, A->nleaf, A->dense_b.p, A->lrr_b.p, A->proj_b.p};
+    SweepDev f{A->leaf_f.p, A->nleaf, A->dense_f.p, A->lrr_f.p, A->proj_f.p, A->pseg_f.p, A->ptask_f.p, A->packA_f.p,
+               A->packB_f.p};
+    SweepDev b{A->leaf_b.p, A->nleaf, A->dense_b.p, A->lrr_b.p, A->proj_b.p, A->pseg_b.p, A->ptask_b.p, A->packA_b.p,
+               A->packB_b.p};
     // cooperative launch: one CTA per SM (all resident), grid barriers between steps
+    static const bool old_apply = getenv("FDE_APPLY_OLD") != nullptr;   // (the round-1 kernel, for A/B runs)
+    if (nrhs <= APPLY_RC && !old_apply && A->maxseg <= PF_MAXSEG) {
+        static bool pf_attr[64] = {};
+        int dev = 0;
+        FDE_CUDA(cudaGetDevice(&dev));
+        if (!pf_attr[dev & 63]) {
+            FDE_CUDA(cudaFuncSetAttribute(k_apply_pf<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, PF_SMEM));
+            FDE_CUDA(cudaFuncSetAttribute(k_apply_pf<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, PF_SMEM));
+            FDE_CUDA(cudaFuncSetAttribute(k_apply_pf<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, PF_SMEM));
+            FDE_CUDA(cudaFuncSetAttribute(k_apply_pf<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, PF_SMEM));
+            pf_attr[dev & 63] = true;
+        }
+        void* kfn = nrhs <= 1 ? (void*)k_apply_pf<1> : nrhs <= 2 ? (void*)k_apply_pf<2>
+                  : nrhs <= 4 ? (void*)k_apply_pf<4> : (void*)k_apply_pf<8>;
+        int nblk = h->num_sms;
+        static const int env_ctas = getenv("FDE_APPLY_CTAS") ? atoi(getenv("FDE_APPLY_CTAS")) : 0;
+        if (env_ctas > 0) nblk = std::min(nblk, env_ctas);
+        long long ldx_ll = ldx;
+        static const bool tl_on = getenv("FDE_APPLY_TIMELINE") != nullptr;
+        unsigned long long* tl = nullptr;
+        if (tl_on) {
+            static DBuf<unsigned long long> tlb;
+            const size_t need = (size_t)2 * A->nleaf * nblk * 4;
+            if (tlb.n < need) tlb.alloc(need);
+            tl = tlb.p;
+            g_apply_tl = tl;
+            g_apply_tl_n = need;
+        }
+        void* args[] = {&f, &b, &x, &ldx_ll, &nrhs, &A->z.p, &A->t.p, &A->tslots, &tl};
+        FDE_CUDA(cudaLaunchCooperativeKernel(kfn, nblk, PF_THREADS, args, PF_SMEM, h->stream));
+        FDE_CHECK_LAUNCH();
+        return;
+    }
     int per_sm = 0;
     FDE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_apply, APPLY_THREADS, 0));
     int nblk = std::max(1, std::min(per_sm, 1)) * h->num_sms;
