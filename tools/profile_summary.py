@@ -37,6 +37,8 @@ FULL_METRICS = [
     "sm__warps_active.avg.pct_of_peak_sustained_active",
     "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
     "smsp__inst_executed.sum", "smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio",
+    "sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active",
+    "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
 ]
 
 
@@ -56,6 +58,18 @@ def full(path):
 
 def main():
     lcsv, prefix, reps = sys.argv[1], sys.argv[2], sys.argv[3:]
+    if lcsv != "-":   # ("-": full-set summaries only)
+        write_launches(lcsv, prefix)
+    with open(prefix + "_full.txt", "w") as f:
+        f.write("# ncu --set full --clock-control none (one launch each)\n")
+        for rep in reps:
+            for d in full(rep):
+                f.write(f"\n[{d.pop('kernel')}]  ({rep.split('/')[-1]})\n")
+                for k, v in d.items():
+                    f.write(f"  {k:62s} {v}\n")
+
+
+def write_launches(lcsv, prefix):
     tot, cnt = launches(lcsv)
     S = sum(tot.values())
     with open(prefix + "_launches.txt", "w") as f:
@@ -66,13 +80,6 @@ def main():
         f.write(f"{'kernel':30s} {'launches':>9s} {'total_ms':>10s} {'share':>7s} {'avg_us':>9s}\n")
         for k, v in tot.most_common():
             f.write(f"{k:30s} {cnt[k]:9d} {v / 1e3:10.2f} {100 * v / S:6.1f}% {v / cnt[k]:9.2f}\n")
-    with open(prefix + "_full.txt", "w") as f:
-        f.write("# ncu --set full --clock-control none (one launch each)\n")
-        for rep in reps:
-            for d in full(rep):
-                f.write(f"\n[{d.pop('kernel')}]  ({rep.split('/')[-1]})\n")
-                for k, v in d.items():
-                    f.write(f"  {k:62s} {v}\n")
 
 
 if __name__ == "__main__":
