@@ -138,6 +138,11 @@ void fde_destroy(fde_handle h)
     if (h->ring) cudaFreeHost(h->ring);
     for (auto e : h->ring_ev)
         if (e) cudaEventDestroy(e);
+    if (h->hb) {
+        cudaStreamSynchronize(h->hb);
+        cudaStreamDestroy(h->hb);
+        cudaEventDestroy(h->ev_hb);
+    }
     if (h->aux) {
         cudaStreamSynchronize(h->aux);
         cudaStreamSynchronize(h->aux2);
@@ -325,11 +330,15 @@ int sem_assemble(fde_handle h, const fde_problem* prob, const fde_mesh* mesh, in
     op->lda = round_up(op->n, 32);
 
     op->tm.start(h->stream);   // (the call returns without waiting: the next calls' host work overlaps it)
+    op->h = h;
     asm_prepare_tables(h, op);
+    FDE_CUDA(cudaEventCreateWithFlags(&op->ev_tab, cudaEventDisableTiming));
+    FDE_CUDA(cudaEventRecord(op->ev_tab, h->stream));
     if (flags & FDE_OP_DENSE) {
         const int b0 = op->e_lo, b1 = std::min(op->e_hi, N - 1);
         const int64_t P2 = (int64_t)P * P;
         // (handle-owned, grow-only: 4.3 GB for c5, not re-allocated per assembly)
+        if (h->hb) stream_after(h, h->stream, h->hb);   // (a build may still read the previous band)
         DBuf<double>& Krow = h->kt_row;
         DBuf<double>& Kcol = h->kt_col;
         const int64_t nrow = (int64_t)(b1 + 1) * (b1 + 2) / 2 - (int64_t)b0 * (b0 + 1) / 2;
@@ -338,6 +347,12 @@ int sem_assemble(fde_handle h, const fde_problem* prob, const fde_mesh* mesh, in
         if (ncol > 0 && Kcol.n < (size_t)ncol * P2) Kcol.alloc((size_t)ncol * P2);
         asm_k_triangle(h, op, b0, b1 + 1, Krow.p);
         if (ncol > 0) asm_k_rect(h, op, b1 + 1, N, b0, b1 + 1, Kcol.p);
+        if (G == 1) {   // the band holds every pair: the H-matrix build may expand its leaves from it
+            FDE_CUDA(cudaEventCreateWithFlags(&op->ev_k, cudaEventDisableTiming));
+            FDE_CUDA(cudaEventRecord(op->ev_k, h->stream));
+            op->kb_row = Krow.p;
+            op->kb_col = Kcol.p;
+        }
         op->A.alloc((size_t)std::max<int64_t>(op->r1 - op->r0, 1) * op->lda);
         asm_expand_dense(h, op, Krow.p, Kcol.p);   // (K tables: stream-ordered release on scope exit)
     }
@@ -482,10 +497,45 @@ int fde_debug_compact_gather(fde_handle h, fde_operator op, const double* gather
 }
 
 // ------------------------------------------------------------- H-matrix
+// The H-matrix and its H-LU need only the operator's tables and the near-field
+// pair moments, not the dense operator.  Option FDE_HBUILD_SIDE (off by default):
+// build them on the handle's build stream, ordered only after the pair-moment band
+// (=1: leaves expanded from the band) or after the tables (=2: near field
+// recomputed), overlapping the dense assembly on the caller's stream; hlu_factor
+// then joins the caller's stream to the build stream at its end.  Measured on c4
+// (r2 bench): 67.2 (=1) and 61.1 (=2) against 67.7 solves/s on one stream -- the
+// H-LU's critical chain slows down as much as the overlap saves, so it stays off.
+static int hbuild_side_mode()
+{
+    static const int m = getenv("FDE_HBUILD_SIDE") ? atoi(getenv("FDE_HBUILD_SIDE")) : 0;
+    return m;
+}
+static bool hbuild_side() { return hbuild_side_mode() != 0; }
+
 int hmatrix_build(fde_handle h, fde_operator op, int R, double lambda, int n_min, fde_hmatrix* out)
 {
+    cudaStream_t orig = h ? h->stream : nullptr;
     API_BEGIN
-    *out = hm_build(h, op, R, lambda, n_min);
+    const bool band = hbuild_side_mode() == 1 && op->ev_k && h->world == 1;
+    if (hbuild_side() && op->ev_tab && (band || hbuild_side_mode() == 2)) {
+        cudaStream_t hb = build_stream(h);
+        FDE_CUDA(cudaStreamWaitEvent(hb, band ? op->ev_k : op->ev_tab, 0));
+        h->stream = hb;
+        fde_set_alloc_stream(hb);
+        try {
+            *out = hm_build(h, op, R, lambda, n_min, /*recompute=*/!band, /*from_band=*/band);
+        } catch (...) {
+            h->stream = orig;
+            fde_set_alloc_stream(orig);
+            throw;
+        }
+        (*out)->st = hb;
+        h->stream = orig;
+        fde_set_alloc_stream(orig);
+    } else {
+        *out = hm_build(h, op, R, lambda, n_min);
+        (*out)->st = h->stream;
+    }
     API_END(h)
 }
 
@@ -505,6 +555,7 @@ int fde_hmatrix_get_info(fde_hmatrix hm, fde_hmatrix_info* info)
 int fde_hmatrix_dense_paper(fde_handle h, fde_hmatrix hm, double* out, int64_t ldo)
 {
     API_BEGIN
+    stream_after(h, h->stream, hm->st);
     const int64_t n = hm->S.n;
     if (ldo < n) fde_fail(FDE_EINVAL_SIZE, "ldo < n");
     DBuf<double> tmp;
@@ -518,9 +569,25 @@ int fde_hmatrix_dense_paper(fde_handle h, fde_hmatrix hm, double* out, int64_t l
 // ----------------------------------------------------------------- H-LU
 int hlu_factor(fde_handle h, fde_hmatrix hm, double tol, fde_hlu* out)
 {
+    cudaStream_t orig = h ? h->stream : nullptr;
     API_BEGIN
     if (!(tol >= 0.0)) fde_fail(FDE_EINVAL_PARAM, "hlu_factor: tol must be >= 0");
-    *out = hlu_build(h, hm, tol);
+    if (hm->st && hm->st != orig) {   // on the H-matrix's build stream, then join the caller's stream
+        h->stream = hm->st;
+        fde_set_alloc_stream(hm->st);
+        try {
+            *out = hlu_build(h, hm, tol);
+        } catch (...) {
+            h->stream = orig;
+            fde_set_alloc_stream(orig);
+            throw;
+        }
+        h->stream = orig;
+        fde_set_alloc_stream(orig);
+        stream_after(h, orig, hm->st);
+    } else {
+        *out = hlu_build(h, hm, tol);
+    }
     API_END(h)
 }
 
@@ -602,7 +669,18 @@ int fde_solve(fde_handle h, fde_operator op, fde_hlu lu, const double* G, double
     return solve(h, op, lu, G, X, nrhs, ld, opts, rep);
 }
 
-void fde_free_operator(fde_operator op) { delete op; }
+void fde_free_operator(fde_operator op)
+{
+    // the operator's buffers are released stream-ordered on the caller's stream:
+    // behind any H-matrix build still reading its tables on the build stream
+    if (op && op->h && op->h->hb) {
+        try {
+            stream_after(op->h, op->h->stream, op->h->hb);
+        } catch (...) {
+        }
+    }
+    delete op;
+}
 void fde_free_hmatrix(fde_hmatrix hm) { delete hm; }
 void fde_free_hlu(fde_hlu lu) { hlu_destroy(lu); }
 

@@ -926,6 +926,38 @@ __global__ void k_expand_leaves(const double* Ktab, const LeafDesc* d, long long
     }
 }
 
+// the same leaves straight from the assembly's pair-moment band (world 1: every
+// pair j <= i), while the dense expansion of A still runs: identical a_entry terms
+__global__ void k_expand_leaves_band(KBand K, const LeafDesc* d, long long n, int N, int P, double theta, double rho,
+                                     const double* nodes, const double* mref, double* arena)
+{
+    const LeafDesc L = d[blockIdx.y];
+    const long long tot = (long long)L.m * L.nc;
+    for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < tot;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const int rr = (int)(idx % L.m), cc = (int)(idx / L.m);
+        arena[L.out + (long long)cc * L.m + rr] = a_entry(K, L.ra + rr, L.ca + cc, n, N, P, theta, rho, nodes, mref);
+    }
+}
+
+void asm_expand_leaves_band(fde_ctx* h, fde_op* op, const LeafDesc* d, int nleaves, int maxentries, double* arena)
+{
+    KBand K;
+    K.row = op->kb_row;
+    K.col = op->kb_col;
+    K.b0 = 0;
+    K.b1 = op->N - 1;
+    K.N = op->N;
+    K.P2 = op->P * op->P;
+    const unsigned gx = (unsigned)std::min<long long>(ceil_div(maxentries, 256), 64);
+    for (int base = 0; base < nleaves; base += 65535) {
+        unsigned cnt = (unsigned)std::min(65535, nleaves - base);
+        k_expand_leaves_band<<<dim3(gx, cnt), 256, 0, h->stream>>>(K, d + base, op->n, op->N, op->P, op->prob.theta,
+                                                                   op->prob.rho, op->tab.nodes.p, op->tab.mref.p, arena);
+        FDE_CHECK_LAUNCH();
+    }
+}
+
 void asm_expand_leaves(fde_ctx* h, fde_op* op, const double* Ktab, const LeafDesc* d, int nleaves, int maxentries,
                        double* arena)
 {

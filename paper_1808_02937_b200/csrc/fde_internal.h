@@ -140,6 +140,10 @@ struct fde_ctx {
     int rank = 0, world = 1;
     void* nccl = nullptr;   // ncclComm_t
     bool virt = false;      // virtual rank (fde_create_virtual_rank): world > 1, no communicator
+    // build stream: hmatrix_build and hlu_factor run on it, ordered only after the
+    // operator's tables, so they overlap the dense assembly on the caller's stream
+    cudaStream_t hb = nullptr;
+    cudaEvent_t ev_hb = nullptr;
     std::string err;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     int num_sms = 148;
@@ -210,6 +214,25 @@ inline cudaStream_t aux_stream(fde_ctx* h)
     }
     return h->aux;
 }
+inline cudaStream_t build_stream(fde_ctx* h)
+{
+    if (!h->hb) {
+        int lo = 0, hi = 0;
+        FDE_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        FDE_CUDA(cudaStreamCreateWithPriority(&h->hb, cudaStreamNonBlocking, hi));
+        FDE_CUDA(cudaEventCreateWithFlags(&h->ev_hb, cudaEventDisableTiming));
+    }
+    return h->hb;
+}
+// make stream `waiter` wait for everything enqueued on `on` so far
+inline void stream_after(fde_ctx* h, cudaStream_t waiter, cudaStream_t on)
+{
+    if (waiter == on) return;
+    build_stream(h);
+    FDE_CUDA(cudaEventRecord(h->ev_hb, on));
+    FDE_CUDA(cudaStreamWaitEvent(waiter, h->ev_hb, 0));
+}
+
 inline cudaStream_t aux_stream2(fde_ctx* h)
 {
     aux_stream(h);
@@ -299,6 +322,16 @@ struct fde_op {
     size_t xw_cols = 0;
     double assemble_ms = 0;
     int world = 1;
+    fde_ctx* h = nullptr;           // creating handle (stream-ordered release behind its build stream)
+    cudaEvent_t ev_tab = nullptr;   // recorded after the quadrature / node tables: the H-matrix build may start
+    cudaEvent_t ev_k = nullptr;     // recorded after the pair-moment band (world 1): leaves can be expanded from it
+    const double* kb_row = nullptr; // the band (the handle's kt_row / kt_col: valid until the next assembly)
+    const double* kb_col = nullptr;
+    ~fde_op()
+    {
+        if (ev_tab) cudaEventDestroy(ev_tab);
+        if (ev_k) cudaEventDestroy(ev_k);
+    }
 };
 
 // ------------------------------------------------------------- kernels API

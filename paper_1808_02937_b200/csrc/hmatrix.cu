@@ -241,7 +241,7 @@ __global__ void k_leaf_from_dense(const LeafTile* T, const double* __restrict__ 
         if (tx < d.m) arena[d.out + (int64_t)c * d.ldo + tx] = t[tx][c];
 }
 
-fde_hm* hm_build(fde_ctx* h, fde_op* op, int R, double lam, int n_min)
+fde_hm* hm_build(fde_ctx* h, fde_op* op, int R, double lam, int n_min, bool recompute, bool from_band)
 {
     if (R < 1 || R > 32) fde_fail(FDE_EINVAL_PARAM, "hmatrix_build: R must be in [1, 32]");
     if (!(lam > 0)) fde_fail(FDE_EINVAL_PARAM, "hmatrix_build: lambda must be > 0");
@@ -374,7 +374,13 @@ fde_hm* hm_build(fde_ctx* h, fde_op* op, int R, double lam, int n_min)
             maxent = std::max(maxent, L.m * L.nc);
             ld.push_back(L);
         }
-        if (!ld.empty() && op->A.p && op->r0 == 0 && op->r1 == op->n) {
+        if (!ld.empty() && from_band) {
+            // the assembly's pair-moment band (all pairs j <= i, world 1) is complete:
+            // the leaves are expanded from it while A's expansion still runs
+            DBuf<LeafDesc> dld;
+            dld.upload(ld.data(), ld.size(), h->stream);
+            asm_expand_leaves_band(h, op, dld.p, (int)ld.size(), maxent, hm->dense.p);
+        } else if (!ld.empty() && !recompute && op->A.p && op->r0 == 0 && op->r1 == op->n) {
             // the dense operator is resident with all rows: the exact entries of the
             // inadmissible leaves are its sub-blocks -- one batched
             // transposing copy (row-major A -> column-major leaves) instead of

@@ -45,6 +45,7 @@ struct fde_hm {
     int64_t dense_words = 0, lr_words = 0;
     int n_dense = 0, n_lr = 0;
     double build_ms = 0;
+    cudaStream_t st = nullptr;   // stream the build was enqueued on (the handle's build stream)
 };
 
 struct LeafDesc {
@@ -57,11 +58,14 @@ struct LeafDesc {
 
 void hm_leaves(const HStruct& S, int b, std::vector<int>& out);
 // exact entries of the dense leaves from their K tables (assemble.cu)
+void asm_expand_leaves_band(fde_ctx* h, fde_op* op, const LeafDesc* d, int nleaves, int maxentries, double* arena);
 void asm_expand_leaves(fde_ctx* h, fde_op* op, const double* Ktab, const LeafDesc* d, int nleaves, int maxentries,
                        double* arena);
 
 // build the cluster tree and block partition (host, structure only)
 void hstruct_build(HStruct& S, const std::vector<double>& nodes, int P, int n_min, double lam);
 
-fde_hm* hm_build(fde_ctx* h, fde_op* op, int R, double lam, int n_min);
+// recompute: build the inadmissible leaves from pair moments even when the dense
+// operator is resident (the build then does not wait for the dense assembly)
+fde_hm* hm_build(fde_ctx* h, fde_op* op, int R, double lam, int n_min, bool recompute = false, bool from_band = false);
 void hm_to_dense_internal(fde_ctx* h, fde_hm* hm, double* out, int64_t ldo);   // out col-major n x n
