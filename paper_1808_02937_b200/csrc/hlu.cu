@@ -2578,9 +2578,10 @@ __global__ void __launch_bounds__(APPLY_THREADS)
 // summed by T = 512 / nrp threads each (warp shuffles, then a fixed-order sum
 // over the warps of the row: deterministic).
 #define PF_THREADS 512
-#define PF_CAP_A 10240            // doubles of staged phase-A factor entries (80 KB)
-#define PF_CAP_B 8192             // doubles of staged phase-B factor entries (64 KB)
-#define PF_CAP_S 6144             // doubles of gathered sources (x / t / z) of one phase (48 KB)
+#define PF_CAP_A 8192             // doubles of staged phase-A factor entries (64 KB)
+#define PF_CAP_B 4096             // doubles of staged phase-B factor entries (32 KB)
+#define PF_CAP_S 12288            // doubles of gathered sources (x / t / z) of one phase (96 KB)
+#define PF_MANY 16                // template tag: more than APPLY_RC right-hand sides
 #define PF_SMEM ((PF_CAP_A + PF_CAP_B + PF_CAP_S) * 8)
 #define PF_MAXLEAF 128            // leaf descriptors of both sweeps kept in shared memory
 
@@ -2631,7 +2632,7 @@ __device__ __forceinline__ void pf_stage_rows(const double* src, int count, int 
 }
 
 __device__ void pf_stage_A(const SweepDev& S, const SLeaf& L, double* buf, PfSeg* seg, const double* x,
-                           const double* t)
+                           const double* t, bool rows = true)
 {
     const int nseg = L.s_hi - L.s_lo;
     if (threadIdx.x < nseg) {
@@ -2646,7 +2647,7 @@ __device__ void pf_stage_A(const SweepDev& S, const SLeaf& L, double* buf, PfSeg
         seg[threadIdx.x] = g;
     }
     const PfRows R = pf_rows(L.m);
-    if (R.nr > 0) pf_stage_rows(S.packA + L.pa_off + (long long)R.r_lo * L.wAp, R.nr * L.wAp, PF_CAP_A, buf);
+    if (rows && R.nr > 0) pf_stage_rows(S.packA + L.pa_off + (long long)R.r_lo * L.wAp, R.nr * L.wAp, PF_CAP_A, buf);
 }
 
 __device__ void pf_stage_B(const SweepDev& S, const SLeaf& L, double* buf)
@@ -2846,6 +2847,114 @@ __device__ void pf_phase_B(const SweepDev& S, const SLeaf& L, double* x, long lo
     }
 }
 
+// Many right-hand sides (nrhs > APPLY_RC): the phase is a small GEMM,
+// Z = X_k - F S (phase A: F the leaf's row terms, S their sources) and
+// X_k = Inv Z (phase B).  Output tiles of 32 rows x 8 right-hand sides, one per
+// CTA (ceil(m / 32) x ceil(nrhs / 8) tiles; the CTAs without a tile run the
+// projections): the tile's sources S[:, 8 columns] are gathered once into shared
+// memory (column-major, cp.async), then warp w owns rows 2w, 2w + 1 and its lanes
+// split the inner index: each lane reads F[row][j] (row-contiguous packed copy,
+// coalesced) and the 8 sources from shared memory and keeps 16 accumulators;
+// shuffle sums in a fixed order (deterministic).
+#define PF_TR 32
+#define PF_TC 8
+template <bool PHASE_B>
+__device__ void pf_phase_many(const SweepDev& S, const SLeaf& L, double* x, long long ldx, int nrhs, double* z,
+                              int tstride, const PfSeg* seg, double* bufS)
+{
+    const int W = PHASE_B ? L.m : L.wA, ld = PHASE_B ? L.mp : L.wAp;
+    const int nseg = L.s_hi - L.s_lo;
+    const int nrg = (L.m + PF_TR - 1) / PF_TR, ncg = (nrhs + PF_TC - 1) / PF_TC;
+    const double* F = PHASE_B ? S.packB + L.pb_off : S.packA + L.pa_off;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const bool ssm = W * PF_TC <= PF_CAP_S;
+    for (int tile = blockIdx.x; tile < nrg * ncg; tile += gridDim.x) {
+        const int r0 = (tile % nrg) * PF_TR, c0 = (tile / nrg) * PF_TC;
+        if (ssm) {
+            __syncthreads();   // (the previous tile's sources are no longer read)
+            for (int e = threadIdx.x; e < W * PF_TC; e += PF_THREADS) {
+                const int col = e / W, j = e - col * W, c = c0 + col;
+                if (c >= nrhs) {
+                    bufS[e] = 0.0;
+                    continue;
+                }
+                const double* src;
+                if (PHASE_B) {
+                    src = z + (long long)c * L.m + j;
+                } else {
+                    const PfSeg& g = seg[pf_seg_of(seg, nseg, j)];
+                    const int jj = j - g.start;
+                    src = g.nchunk == 0 ? g.src + (long long)c * ldx + jj : g.src + (long long)c * tstride + jj * g.nchunk;
+                }
+                pf_cp8(bufS + e, src);
+            }
+            asm volatile("cp.async.wait_all;\n" ::: "memory");
+            __syncthreads();
+        }
+        const int ra = r0 + 2 * w, rb = ra + 1;
+        double acc[2][PF_TC];
+#pragma unroll
+        for (int q = 0; q < 2; ++q)
+#pragma unroll
+            for (int c = 0; c < PF_TC; ++c) acc[q][c] = 0.0;
+        if (ra < L.m) {
+            const double* Fa = F + (long long)ra * ld;
+            const double* Fb = F + (long long)(rb < L.m ? rb : ra) * ld;
+            int sg = 0;
+            for (int j0 = lane; j0 < W; j0 += 4 * 32) {   // four factor pairs in flight per lane
+                double fa[4], fb[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int j = j0 + 32 * u;
+                    fa[u] = j < W ? Fa[j] : 0.0;
+                    fb[u] = j < W ? Fb[j] : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int j = j0 + 32 * u;
+                    if (j >= W) break;
+                    double sv[PF_TC];
+                    if (ssm) {
+#pragma unroll
+                        for (int c = 0; c < PF_TC; ++c) sv[c] = bufS[c * W + j];
+                    } else {   // (sources beyond the shared-memory capacity: straight from global)
+                        while (!PHASE_B && sg + 1 < nseg && j >= seg[sg + 1].start) ++sg;
+#pragma unroll
+                        for (int c = 0; c < PF_TC; ++c)
+                            sv[c] = c0 + c >= nrhs ? 0.0
+                                  : PHASE_B ? ldcg(z + (long long)(c0 + c) * L.m + j)
+                                            : pf_source(seg[sg], j, c0 + c, ldx, tstride);
+                    }
+#pragma unroll
+                    for (int c = 0; c < PF_TC; ++c) {
+                        acc[0][c] = fma(fa[u], sv[c], acc[0][c]);
+                        acc[1][c] = fma(fb[u], sv[c], acc[1][c]);
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < 2; ++q)
+#pragma unroll
+            for (int c = 0; c < PF_TC; ++c)
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) acc[q][c] += __shfl_xor_sync(0xffffffffu, acc[q][c], off);
+        if (lane < 2 * PF_TC) {
+            const int q = lane / PF_TC, c = lane % PF_TC, row = ra + q, cc = c0 + c;
+            double v = 0.0;
+#pragma unroll
+            for (int qq = 0; qq < 2; ++qq)
+#pragma unroll
+                for (int c2 = 0; c2 < PF_TC; ++c2)
+                    if (qq == q && c2 == c) v = acc[qq][c2];
+            if (row < L.m && cc < nrhs) {
+                if (PHASE_B) x[(long long)cc * ldx + L.r0 + row] = v;
+                else z[(long long)cc * L.m + row] = ldcg(x + (long long)cc * ldx + L.r0 + row) - v;
+            }
+        }
+    }
+}
+
 // projections t = V^T x_sigma of the blocks whose sigma completed with leaf Pv:
 // one warp per (block, column, 256-row chunk), right-hand sides four at a time
 __device__ void pf_projections(const SweepDev& S, const SLeaf& Pv, const double* x, long long ldx, int nrhs, double* t,
@@ -2856,7 +2965,10 @@ __device__ void pf_projections(const SweepDev& S, const SLeaf& Pv, const double*
     const int nwarps = gridDim.x * (PF_THREADS / 32);
     const int gw = (gridDim.x - 1 - blockIdx.x) * (PF_THREADS / 32) + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
-    for (int task = Pv.pt_lo + gw; task < Pv.pt_hi; task += nwarps) {
+    // (many right-hand sides: one task per group of four, more warps in flight)
+    const int ng = nrhs > APPLY_RC ? (nrhs + 3) / 4 : 1;
+    for (int task2 = gw; task2 < (Pv.pt_hi - Pv.pt_lo) * ng; task2 += nwarps) {
+        const int task = Pv.pt_lo + task2 / ng, grp = task2 % ng;
         const int4 tk = S.ptask[task];
         const int p = tk.x;
         const SProj Pj = S.proj[p];
@@ -2869,7 +2981,7 @@ __device__ void pf_projections(const SweepDev& S, const SLeaf& Pv, const double*
             const int i = i0 + lane + 32 * u;
             v[u] = (i < i1) ? vc[i] : 0.0;
         }
-        for (int c0 = 0; c0 < nrhs; c0 += 4) {
+        for (int c0 = ng > 1 ? 4 * grp : 0; c0 < (ng > 1 ? min(nrhs, 4 * grp + 4) : nrhs); c0 += 4) {
             double a[4][PROJ_CHUNK / 32];
 #pragma unroll
             for (int cc = 0; cc < 4; ++cc) {
@@ -2921,7 +3033,8 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
         for (int i = threadIdx.x; i < 2 * nl; i += PF_THREADS) sleaf[i / nl][i % nl] = (i < nl ? fwd : bwd).leaf[i % nl];
     __syncthreads();
     auto leaf = [&](bool back, int k) -> SLeaf { return lsm ? sleaf[back][k] : (back ? bwd : fwd).leaf[k]; };
-    pf_stage_A(fwd, leaf(false, 0), bufA, seg, x, t);
+    constexpr bool rows = RC != PF_MANY;   // (many RHS: the factor rows are read in place)
+    pf_stage_A(fwd, leaf(false, 0), bufA, seg, x, t, rows);
     pf_commit();
     for (int s = 0; s < 2 * nl; ++s) {
         const bool back = s >= nl;
@@ -2931,11 +3044,12 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
         // ---- phase A(k)   (x of the previous leaf complete)
         if (s > 0) grid.sync();
         mark(s, 0);
-        pf_stage_B(S, L, bufB);
+        if (rows) pf_stage_B(S, L, bufB);
         pf_commit();
         pf_wait1();                // A(k) staged (B(k) may still be in flight)
         __syncthreads();
-        pf_phase_A<RC>(S, L, x, ldx, nrhs, z, tstride, bufA, seg, bufS, red);
+        if (RC == PF_MANY) pf_phase_many<false>(S, L, x, ldx, nrhs, z, tstride, seg, bufS);
+        else pf_phase_A<RC == PF_MANY ? 1 : RC>(S, L, x, ldx, nrhs, z, tstride, bufA, seg, bufS, red);
         // the projections enabled by the previous leaf (first read by leaf k+1: the
         // admissibility gap) beside phase A, their chunk partials folded beside phase B
         const int prev = (s == 0 || s == nl) ? -1 : (back ? k + 1 : k - 1);
@@ -2946,7 +3060,8 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
         asm volatile("cp.async.wait_all;\n" ::: "memory");   // B(k) staged
         __syncthreads();
         mark(s, 2);
-        pf_phase_B<RC>(S, L, x, ldx, nrhs, z, bufB, bufS, red);
+        if (RC == PF_MANY) pf_phase_many<true>(S, L, x, ldx, nrhs, z, tstride, seg, bufS);
+        else pf_phase_B<RC == PF_MANY ? 1 : RC>(S, L, x, ldx, nrhs, z, bufB, bufS, red);
         if (prev >= 0) pf_fold(S, leaf(back, prev), nrhs, t, tstride);
         mark(s, 3);
         // stage A(k+1) behind B(k): its copies overlap the barrier
@@ -2954,7 +3069,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
             const bool nb = s + 1 >= nl;
             const SweepDev& S2 = nb ? bwd : fwd;
             __syncthreads();       // (the segment table of A(k) is no longer read)
-            pf_stage_A(S2, leaf(nb, nb ? 2 * nl - 2 - s : s + 1), bufA, seg, x, t);
+            pf_stage_A(S2, leaf(nb, nb ? 2 * nl - 2 - s : s + 1), bufA, seg, x, t, rows);
         }
         pf_commit();
     }
@@ -3245,7 +3360,8 @@ static void apply_sched_run(fde_ctx* h, fde_lu* L, double* x, int64_t ldx, int n
                A->packB_b.p};
     // cooperative launch: one CTA per SM (all resident), grid barriers between steps
     static const bool old_apply = getenv("FDE_APPLY_OLD") != nullptr;   // (the round-1 kernel, for A/B runs)
-    if (nrhs <= APPLY_RC && !old_apply && A->maxseg <= PF_MAXSEG) {
+    static const bool many_old = getenv("FDE_APPLY_MANY_OLD") != nullptr;   // (round 1's tile path for > 8 RHS)
+    if ((nrhs <= APPLY_RC || !many_old) && !old_apply && A->maxseg <= PF_MAXSEG) {
         static bool pf_attr[64] = {};
         int dev = 0;
         FDE_CUDA(cudaGetDevice(&dev));
@@ -3254,10 +3370,11 @@ static void apply_sched_run(fde_ctx* h, fde_lu* L, double* x, int64_t ldx, int n
             FDE_CUDA(cudaFuncSetAttribute(k_apply_pf<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, PF_SMEM));
             FDE_CUDA(cudaFuncSetAttribute(k_apply_pf<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, PF_SMEM));
             FDE_CUDA(cudaFuncSetAttribute(k_apply_pf<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, PF_SMEM));
+            FDE_CUDA(cudaFuncSetAttribute(k_apply_pf<PF_MANY>, cudaFuncAttributeMaxDynamicSharedMemorySize, PF_SMEM));
             pf_attr[dev & 63] = true;
         }
         void* kfn = nrhs <= 1 ? (void*)k_apply_pf<1> : nrhs <= 2 ? (void*)k_apply_pf<2>
-                  : nrhs <= 4 ? (void*)k_apply_pf<4> : (void*)k_apply_pf<8>;
+                  : nrhs <= 4 ? (void*)k_apply_pf<4> : nrhs <= 8 ? (void*)k_apply_pf<8> : (void*)k_apply_pf<PF_MANY>;
         int nblk = h->num_sms;
         static const int env_ctas = getenv("FDE_APPLY_CTAS") ? atoi(getenv("FDE_APPLY_CTAS")) : 0;
         if (env_ctas > 0) nblk = std::min(nblk, env_ctas);
