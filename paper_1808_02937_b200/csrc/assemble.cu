@@ -534,6 +534,79 @@ __global__ void __launch_bounds__(128) k_expand_pairs(KBand K, long long r0, lon
     }
 }
 
+// Expansion by tiles of 8 x 8 element pairs (world 1: the whole triangle K table).
+// A tile (I, J), J <= I, needs the pair blocks K(max(a,b), min(a,b)) for a in
+// I + {next element}, b in J + {next element} (the hats of an element's right
+// node reach into the next element): 9 x 9 blocks staged ONCE in shared memory
+// with 16-byte copies, from which the CTA writes both A[rows of I][cols of J]
+// (S_l part theta, S_l^T part 1-theta, mass) and the mirrored A[rows of J][cols
+// of I] -- each pair block is read about 1.27 times instead of once per use (the
+// per-pair kernel re-read the table 2.2 times), and every row segment is written
+// by consecutive threads.  Same terms in the same order as a_entry (bit-identical).
+#define EX_TE 8
+template <int PT>
+__global__ void __launch_bounds__(256) k_expand_tiles(const double* Ktri, long long n, long long lda, int N, double theta,
+                                                      double rho, const double* nodes, const double* mref_g, double* A)
+{
+    constexpr int P = PT, P2 = PT * PT, NB = EX_TE + 1;
+    extern __shared__ __align__(16) double ksm[];   // [a][b] slots of P2 doubles
+    __shared__ double mref[(PT + 1) * (PT + 1)];
+    __shared__ double hh[2 * EX_TE + 2];
+    // tile index -> (ti, tj), tj <= ti (lower triangle, row by row)
+    const long long bidx = blockIdx.x;
+    int ti = (int)((sqrt(8.0 * (double)bidx + 1.0) - 1.0) * 0.5);
+    while ((long long)ti * (ti + 1) / 2 > bidx) --ti;
+    while ((long long)(ti + 1) * (ti + 2) / 2 <= bidx) ++ti;
+    const int tj = (int)(bidx - (long long)ti * (ti + 1) / 2);
+    const int I0 = ti * EX_TE, J0 = tj * EX_TE;
+    for (int e = threadIdx.x; e < (P + 1) * (P + 1); e += 256) mref[e] = mref_g[e];
+    for (int e = threadIdx.x; e < 2 * NB; e += 256) {
+        const int el = e < NB ? I0 + e : J0 + e - NB;
+        hh[e] = el < N ? 0.5 * (nodes[el + 1] - nodes[el]) : 0.0;
+    }
+    // stage the slots (16-byte copies; P2 even)
+    for (int e = threadIdx.x; e < NB * NB * (P2 / 2); e += 256) {
+        const int slot = e / (P2 / 2), w = e - slot * (P2 / 2);
+        const int a = I0 + slot / NB, b = J0 + slot % NB;
+        const int hi = a > b ? a : b, lo = a > b ? b : a;
+        double2 v = make_double2(0.0, 0.0);
+        if (hi < N) v = reinterpret_cast<const double2*>(Ktri + ((long long)hi * (hi + 1) / 2 + lo) * P2)[w];
+        reinterpret_cast<double2*>(ksm + (long long)slot * P2)[w] = v;
+    }
+    __syncthreads();
+    // the two blocks: (rows I, cols J) and, off the diagonal, (rows J, cols I)
+    for (int blk = 0; blk < (ti == tj ? 1 : 2); ++blk) {
+        const int R0 = blk ? J0 : I0, C0 = blk ? I0 : J0;
+        constexpr int nr = EX_TE * P, nc = EX_TE * P, nph = 256 / nc;   // (nc divides 256 for P = 4, 8, 16)
+        const int cc2 = threadIdx.x % nc;
+        const long long c = (long long)C0 * P + cc2;   // this thread's column: its terms once
+        const DofTerms tc = dof_terms<PT>(c < n ? c : 0, n, N, P);
+        for (int rr = threadIdx.x / nc; rr < nr; rr += nph) {
+            const long long r = (long long)R0 * P + rr;
+            if (r >= n || c >= n) continue;
+            const DofTerms tr = dof_terms<PT>(r, n, N, P);
+            double sl = 0.0, slt = 0.0, mass = 0.0;
+            for (int x = 0; x < tr.cnt; ++x) {
+                const int ei = tr.e[x];
+                if (ei < 0 || ei >= N) continue;
+                for (int y = 0; y < tc.cnt; ++y) {
+                    const int ej = tc.e[y];
+                    if (ej < 0 || ej >= N) continue;
+                    const double cf = tr.c[x] * tc.c[y];
+                    // slot of the pair (ei, ej): row index from I, column from J (or mirrored)
+                    const int sa = blk ? ej - I0 : ei - I0, sb = blk ? ei - J0 : ej - J0;
+                    const double* kb = ksm + (sa * NB + sb) * P2;   // K(max(ei,ej), min(ei,ej))
+                    if (ej <= ei) sl = fma(cf, kb[tr.m[x] * P + tc.m[y]], sl);
+                    if (ei <= ej) slt = fma(cf, kb[tc.m[y] * P + tr.m[x]], slt);
+                    if (ei == ej)
+                        mass = fma(hh[blk ? NB + (ei - J0) : (ei - I0)], mref[tr.ml[x] * (P + 1) + tc.ml[y]], mass);
+                }
+            }
+            A[r * lda + c] = rho * mass + theta * sl + (1.0 - theta) * slt;
+        }
+    }
+}
+
 template <int PT>
 __global__ void __launch_bounds__(256) k_expand_dense(KBand K, long long r0, long long r1, long long n, long long lda,
                                                       int N, int P, double theta, double rho, const double* nodes,
@@ -810,6 +883,26 @@ void asm_expand_dense(fde_ctx* h, fde_op* op, const double* Krow, const double* 
     k_expand_dense<PT_><<<grid, 256, 0, h->stream>>>(K, op->r0, op->r1, op->n, op->lda, op->N, op->P, op->prob.theta, \
                                                      op->prob.rho, op->tab.nodes.p, op->tab.mref.p, op->A.p)
     static const bool per_entry = getenv("FDE_EXPAND_ENTRY") != nullptr;   // (the previous per-entry kernel)
+    static const bool per_pair = getenv("FDE_EXPAND_PAIRS") != nullptr;   // (round 1's per-pair kernel)
+    const bool whole = op->r0 == 0 && op->r1 == op->n && K.b0 == 0 && K.b1 == op->N - 1;
+    if (!per_entry && !per_pair && whole && (op->P == 4 || op->P == 8 || op->P == 16)) {
+        // tiles of 8 x 8 element pairs over the whole triangle (world 1)
+        const long long nt = ceil_div(op->N, EX_TE);
+        const unsigned ntiles = (unsigned)(nt * (nt + 1) / 2);
+        if (op->lda > op->n)   // padding columns [n, lda) of every row
+            FDE_CUDA(cudaMemset2DAsync(op->A.p + op->n, op->lda * sizeof(double), 0, (op->lda - op->n) * sizeof(double),
+                                       op->n, h->stream));
+        const size_t smem = (size_t)(EX_TE + 1) * (EX_TE + 1) * op->P * op->P * sizeof(double);
+#define FDE_EXPAND_T(PT_)                                                                                              do {                                                                                                                   FDE_CUDA(cudaFuncSetAttribute(k_expand_tiles<PT_>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));         k_expand_tiles<PT_><<<ntiles, 256, smem, h->stream>>>(Krow, op->n, op->lda, op->N, op->prob.theta,                                                                     op->prob.rho, op->tab.nodes.p, op->tab.mref.p, op->A.p);     } while (0)
+        switch (op->P) {
+            case 4: FDE_EXPAND_T(4); break;
+            case 8: FDE_EXPAND_T(8); break;
+            default: FDE_EXPAND_T(16);
+        }
+#undef FDE_EXPAND_T
+        FDE_CHECK_LAUNCH();
+        return;
+    }
     if (per_entry) {
         switch (op->P) {   // the common degrees with a compile-time P
             case 4: FDE_EXPAND(4); break;
