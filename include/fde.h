@@ -119,7 +119,8 @@ int fde_profile_collect(fde_handle h, double* out9, int reset);
 /* Number of kernels this library has launched in the process so far. */
 long long fde_launch_count(void);
 /* Diagnostics: H-LU truncation statistics since load: out4 = {calls, sum of
- * compacted widths, sum of Jacobi sweeps, max width}. */
+ * compacted widths, sum of Jacobi sweeps, max width}; counted only when the
+ * process runs with FDE_TRUNC_STATS=1 (no atomics on the hot path otherwise). */
 int fde_debug_trunc_stats(unsigned long long* out4);
 /* Diagnostics: H-LU algorithm selection for later hlu_factor calls (process
  * wide).  mode 0 (default): the leaf-ordered batched factorisation whenever the

@@ -753,6 +753,7 @@ __device__ __forceinline__ bool h2_chk(const void* p, long long nbytes, int tag,
 }
 
 __device__ unsigned long long g_trunc_stats[4];
+__constant__ int g_trunc_stats_on = 0;   // debug statistics only with FDE_TRUNC_STATS=1 (no atomics on the hot path)
 __device__ double g_trunc_jeps = 0.0;   // (debug FDE_TRUNC_JEPS)
 __device__ int g_trunc_check = 0;   // descriptor checks (FDE_DEBUG_SERIAL)   // calls, sum ke, sum sweeps, max ke
 
@@ -823,7 +824,7 @@ __global__ void __launch_bounds__(256) k_trunc_core(const double* Gu, const doub
     __syncthreads();
     const int sw2 = cta_jacobi(A, X, n, pairs, 1e-15, 1e-16);
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (g_trunc_stats_on && threadIdx.x == 0) {
         atomicAdd(&g_trunc_stats[0], 1ull);
         atomicAdd(&g_trunc_stats[1], (unsigned long long)ke);
         atomicAdd(&g_trunc_stats[2], (unsigned long long)(sw1 + sw2));
@@ -1131,7 +1132,7 @@ __global__ void __launch_bounds__(256) k_bcore(const TEntry* E, const TChunk* C,
     __syncthreads();
     const int sw2 = (n2 <= 32) ? warp_jacobi(X, Eu, n2, jeps, jarel) : cta_jacobi(X, Eu, n2, nullptr, jeps, jarel);
     __syncthreads();
-    if (threadIdx.x == 0) {   // (debug statistics: calls, sum ke, sum sweeps, max sweeps of one solve)
+    if (g_trunc_stats_on && threadIdx.x == 0) {   // (debug statistics: calls, sum ke, sum sweeps, max sweeps)
         atomicAdd(&g_trunc_stats[0], 1ull);
         atomicAdd(&g_trunc_stats[1], (unsigned long long)ke);
         atomicAdd(&g_trunc_stats[2], (unsigned long long)sw2);
@@ -1992,6 +1993,12 @@ int g_hlu_mode = 0;   // 0: leaf-ordered batched H-LU when the partition allows 
 
 fde_lu* hlu_build(fde_ctx* h, fde_hm* hm, double tol)
 {
+    static bool stats_set[64] = {};
+    if (!stats_set[h->device & 63]) {   // (per device: __constant__ memory)
+        const int on = getenv("FDE_TRUNC_STATS") ? 1 : 0;
+        FDE_CUDA(cudaMemcpyToSymbol(g_trunc_stats_on, &on, sizeof(int)));
+        stats_set[h->device & 63] = true;
+    }
     fde_lu* L = new fde_lu();
     try {
         L->op = hm->op;
