@@ -3,6 +3,7 @@
 usage: python tools/profile_summary.py <launches.csv> <out_prefix> <full.ncu-rep> [more.ncu-rep ...]
 """
 import collections
+import os
 import csv
 import subprocess
 import sys
@@ -74,8 +75,8 @@ def write_launches(lcsv, prefix):
     S = sum(tot.values())
     with open(prefix + "_launches.txt", "w") as f:
         f.write(f"# ncu --metrics gpu__time_duration.sum --clock-control none launch list of\n"
-                f"#   python bench.py --steps 1 --warmup 1 --no-cpu-baseline  (cold-cache, serialised;\n"
-                f"#   the warm-up step and the end-to-end step are in the list too: 3 cold solves)\n"
+                f"#   {os.environ.get('FDE_LAUNCH_CMD', 'python bench.py --steps 1 --warmup 1 --no-cpu-baseline')}\n"
+                f"#   (cold-cache, serialised)\n"
                 f"# {sum(cnt.values())} launches, {S / 1e3:.1f} ms device time in total\n")
         f.write(f"{'kernel':30s} {'launches':>9s} {'total_ms':>10s} {'share':>7s} {'avg_us':>9s}\n")
         for k, v in tot.most_common():
