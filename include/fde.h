@@ -220,6 +220,21 @@ int fde_debug_compact_gather(fde_handle h, fde_operator op, const double* gather
  * (Eq. (approxsys), reading A2).  Replicated on every rank. */
 int hmatrix_build(fde_handle h, fde_operator op, int R, double lambda, int n_min, fde_hmatrix* out);
 
+/* The same with a choice of cluster partition:
+ *  FDE_PARTITION_INTERLEAVED (the default of hmatrix_build, reading A9):
+ *    one binary tree over element ranges, a cluster holding the modal functions
+ *    of its elements and the hats of their right nodes;
+ *  FDE_PARTITION_PAPER (Fig. fig200, Eq. (approxmat)): separate
+ *    trees for the modal functions (clusters of elements, support = their union)
+ *    and the nodal hats (clusters of interior nodes, support = union of
+ *    [x_{j-1}, x_{j+1}]), under a root whose first block level is the 2 x 2
+ *    superblock [B F; E C] of S_l; the H-matrix, its H-LU and precond_apply then
+ *    work in the paper's dof order internally.  Needs the resident dense
+ *    operator (world 1, FDE_OP_DENSE): FDE_EINVAL_PARAM otherwise. */
+enum { FDE_PARTITION_INTERLEAVED = 0, FDE_PARTITION_PAPER = 1 };
+int hmatrix_build_partition(fde_handle h, fde_operator op, int R, double lambda, int n_min, int partition,
+                            fde_hmatrix* out);
+
 typedef struct {
     int32_t nblocks_dense, nblocks_lr, depth, nclusters;
     int64_t dense_entries, lr_entries;   /* stored fp64 words              */

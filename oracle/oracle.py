@@ -260,6 +260,62 @@ def cluster_support(nodes: np.ndarray, c: Cluster) -> Tuple[float, float]:
     return nodes[c.e0], nodes[min(c.e1 + 1, N)]
 
 
+# The paper's own partition (Fig. fig200): the modal functions
+# and the nodal hats are clustered separately; S_l = [B F; E C]
+# is the first block level.  Dofs in the paper order.
+@dataclass
+class PCluster:
+    kind: str            # "modal" (elements [a, b)), "nodal" (interior nodes [a, b)), "root"
+    a: int
+    b: int
+    children: Tuple["PCluster", ...] = ()
+
+
+def paper_cluster_tree(N: int, P: int, n_min: int) -> PCluster:
+    """Median bisection of the element range (modal tree) and of the interior node
+    range 1..N-1 (nodal tree) down to n_min elements / nodes, under a virtual root."""
+    def rec(kind, a, b):
+        c = PCluster(kind, a, b)
+        if b - a > n_min:
+            m = (a + b) // 2
+            c.children = (rec(kind, a, m), rec(kind, m, b))
+        return c
+    parts = []
+    if P > 1:
+        parts.append(rec("modal", 0, N))
+    if N > 1:
+        parts.append(rec("nodal", 1, N))
+    return parts[0] if len(parts) == 1 else PCluster("root", 0, N, tuple(parts))
+
+
+def pcluster_support(nodes: np.ndarray, c: PCluster) -> Tuple[float, float]:
+    """Union of the supports: element e is [x_e, x_{e+1}], the hat of node j is
+    [x_{j-1}, x_{j+1}] (PAPER.md:124, 333-336)."""
+    if c.kind == "modal":
+        return nodes[c.a], nodes[c.b]
+    if c.kind == "nodal":
+        return nodes[c.a - 1], nodes[c.b]
+    return nodes[0], nodes[-1]
+
+
+def pcluster_dofs(N: int, P: int, c: PCluster) -> np.ndarray:
+    """Paper-order indices of the cluster's dofs."""
+    nm = N * (P - 1)
+    if c.kind == "modal":
+        return np.array([e * (P - 1) + p - 1 for e in range(c.a, c.b) for p in range(1, P)], dtype=np.int64)
+    if c.kind == "nodal":
+        return np.array([nm + j - 1 for j in range(c.a, c.b)], dtype=np.int64)
+    return np.arange(N * P - 1, dtype=np.int64)
+
+
+def support_of(nodes, c):
+    return cluster_support(nodes, c) if isinstance(c, Cluster) else pcluster_support(nodes, c)
+
+
+def dofs_of(N, P, c):
+    return paper_index_of_element_dofs(N, P, c.e0, c.e1) if isinstance(c, Cluster) else pcluster_dofs(N, P, c)
+
+
 def admissible(tau: Tuple[float, float], sig: Tuple[float, float], lam: float) -> bool:
     """max(diam tau, diam sigma) <= lambda dist(tau, sigma)  (Eq. (admis))."""
     diam = max(tau[1] - tau[0], sig[1] - sig[0])
@@ -267,12 +323,13 @@ def admissible(tau: Tuple[float, float], sig: Tuple[float, float], lam: float) -
     return dist > 0 and diam <= lam * dist
 
 
-def block_partition(nodes, root: Cluster, lam: float):
-    """Leaves of the block tree: list of (tau, sigma, 'lr'|'dense')."""
+def block_partition(nodes, root, lam: float):
+    """Leaves of the block tree: list of (tau, sigma, 'lr'|'dense'); root is a
+    Cluster (interleaved tree) or a PCluster (the paper's partition)."""
     out = []
 
-    def rec(t: Cluster, s: Cluster):
-        if admissible(cluster_support(nodes, t), cluster_support(nodes, s), lam):
+    def rec(t, s):
+        if admissible(support_of(nodes, t), support_of(nodes, s), lam):
             out.append((t, s, "lr"))
         elif not t.children or not s.children:
             out.append((t, s, "dense"))
@@ -298,45 +355,55 @@ def _elem_dof_derivs(nodes, P, e, xs_ref):
     return np.array([local_deriv(P, h, xr) for xr in xs_ref])  # (q, P+1)
 
 
-def taylor_factors(prob, test: Cluster, trial: Cluster, R: int, q: int = 48):
+def taylor_factors(prob, test, trial, R: int, q: int = 48):
     """Low-rank factors of S_l on an admissible block with `test` right of `trial`.
 
     s-expansion about s0 = mid(trial support) unless diam(trial) > diam(test),
     then t-expansion about t0 = mid(test support) (Lemma 3.2 Eq. (eqn:Lexpan),
     PAPER.md:229-235; Remark PAPER.md:285-298; reading A10).  Returns (Q, W) with
-    rows in the order of paper_index_of_element_dofs and
+    rows in the order of the clusters' dofs (paper_index_of_element_dofs for the
+    interleaved tree, pcluster_dofs for the paper's partition) and
         S_l[test, trial] ~= Q @ W.T,   Q = gamma0 int h_nu phi_I',  W = int g_nu phi_J'
     (PAPER.md:365-370, 383-388)."""
     nodes, P, alpha = prob.nodes, prob.P, prob.alpha
     N = len(nodes) - 1
     g0 = 1.0 / math.gamma(2 - alpha)
-    ts = cluster_support(nodes, test)
-    ss = cluster_support(nodes, trial)
+    ts = support_of(nodes, test)
+    ss = support_of(nodes, trial)
     c = np.array([_rising(alpha - 1, nu) / math.factorial(nu) for nu in range(R)])  # (alpha-1)_nu/nu!
     gx, gw = gl_table(q)
     s_expand = (ss[1] - ss[0]) <= (ts[1] - ts[0])
 
-    def factor(cl: Cluster, fn):
+    def factor(cl, fn):
         """int fn(x) phi_I'(x) dx for the cluster's dofs (rows in cluster dof order)."""
-        rows = []
-        for e in range(cl.e0, cl.e1):
-            pass
-        # integrate element by element, then combine into dofs
         per_elem = {}
-        for e in range(max(cl.e0, 0), min(cl.e1 + 1, N)):
-            h = nodes[e + 1] - nodes[e]
-            xs = nodes[e] + 0.5 * h * (gx + 1)
-            D = _elem_dof_derivs(nodes, P, e, gx)            # (q, P+1)
-            F = fn(xs, e)                                       # (q, R)
-            per_elem[e] = (0.5 * h * gw[:, None] * D).T @ F     # (P+1, R)
-        for e in range(cl.e0, cl.e1):
-            for p in range(1, P):
-                rows.append(per_elem[e][p])
-            if e + 1 <= N - 1:
-                r = per_elem[e][P].copy()                       # rising half on element e
-                if e + 1 in per_elem:
-                    r = r + per_elem[e + 1][0]                   # falling half on element e+1
-                rows.append(r)
+
+        def elem(e):   # (P+1, R): the element's local functions against fn
+            if e not in per_elem:
+                h = nodes[e + 1] - nodes[e]
+                xs = nodes[e] + 0.5 * h * (gx + 1)
+                D = _elem_dof_derivs(nodes, P, e, gx)            # (q, P+1)
+                F = fn(xs, e)                                       # (q, R)
+                per_elem[e] = (0.5 * h * gw[:, None] * D).T @ F     # (P+1, R)
+            return per_elem[e]
+
+        def hat(j):    # hat of interior node j: rising half on element j-1, falling half on j
+            return elem(j - 1)[P] + elem(j)[0]
+
+        rows = []
+        if isinstance(cl, Cluster):
+            for e in range(cl.e0, cl.e1):
+                for p in range(1, P):
+                    rows.append(elem(e)[p])
+                if e + 1 <= N - 1:
+                    rows.append(hat(e + 1))
+        elif cl.kind == "modal":
+            for e in range(cl.a, cl.b):
+                for p in range(1, P):
+                    rows.append(elem(e)[p])
+        else:
+            for j in range(cl.a, cl.b):
+                rows.append(hat(j))
         return np.array(rows).reshape(-1, R)
 
     nus = np.arange(R)
@@ -351,22 +418,24 @@ def taylor_factors(prob, test: Cluster, trial: Cluster, R: int, q: int = 48):
     return Q, W
 
 
-def hmatrix_dense(prob, sysm: System, R: int, lam: float = 1.0, n_min: int = 16):
+def hmatrix_dense(prob, sysm: System, R: int, lam: float = 1.0, n_min: int = 16, partition: str = "interleaved"):
     """Dense A~ = rho M + theta H + (1-theta) H^T (Eq. (approxsys) PAPER.md:594,
     reading A2): exact entries on inadmissible leaves, Taylor
-    low-rank factors on admissible leaves.  Paper order.  Returns (A~, partition)."""
+    low-rank factors on admissible leaves.  Paper order.  partition:
+    "interleaved" (reading A9) or "paper" (separate modal / nodal trees,
+    PAPER.md:327-338).  Returns (A~, partition)."""
     N, P = prob.N, prob.P
-    root = cluster_tree(N, n_min)
+    root = cluster_tree(N, n_min) if partition == "interleaved" else paper_cluster_tree(N, P, n_min)
     part = block_partition(prob.nodes, root, lam)
     At = sysm.A.copy()
     for t, s, kind in part:
         if kind != "lr":
             continue
-        rows = paper_index_of_element_dofs(N, P, t.e0, t.e1)
-        cols = paper_index_of_element_dofs(N, P, s.e0, s.e1)
+        rows = dofs_of(N, P, t)
+        cols = dofs_of(N, P, s)
         if len(rows) == 0 or len(cols) == 0:
             continue
-        if prob.nodes[t.e0] >= prob.nodes[s.e1]:        # test cluster right of trial: lower part
+        if support_of(prob.nodes, t)[0] >= support_of(prob.nodes, s)[1]:   # test cluster right of trial: lower part
             Q, W = taylor_factors(prob, t, s, R)
             At[np.ix_(rows, cols)] = prob.theta * (Q @ W.T)
         else:                                           # upper part: (1-theta) (S_l[s,t])^T

@@ -539,6 +539,17 @@ int hmatrix_build(fde_handle h, fde_operator op, int R, double lambda, int n_min
     API_END(h)
 }
 
+int hmatrix_build_partition(fde_handle h, fde_operator op, int R, double lambda, int n_min, int partition,
+                            fde_hmatrix* out)
+{
+    if (partition == FDE_PARTITION_INTERLEAVED) return hmatrix_build(h, op, R, lambda, n_min, out);
+    API_BEGIN
+    if (partition != FDE_PARTITION_PAPER) fde_fail(FDE_EINVAL_PARAM, "hmatrix_build_partition: unknown partition");
+    *out = hm_build(h, op, R, lambda, n_min, false, false, 1);
+    (*out)->st = h->stream;
+    API_END(h)
+}
+
 int fde_hmatrix_get_info(fde_hmatrix hm, fde_hmatrix_info* info)
 {
     if (!hm || !info) return FDE_EINVAL_PARAM;
@@ -561,7 +572,11 @@ int fde_hmatrix_dense_paper(fde_handle h, fde_hmatrix hm, double* out, int64_t l
     DBuf<double> tmp;
     tmp.alloc((size_t)n * n);
     hm_to_dense_internal(h, hm, tmp.p, n);
-    internal_dense_to_paper(h, hm->S.N, hm->S.P, tmp.p, n, out, ldo);
+    if (hm->S.paper)   // (the paper partition's blocks are already in the paper order)
+        FDE_CUDA(cudaMemcpy2DAsync(out, (size_t)ldo * sizeof(double), tmp.p, (size_t)n * sizeof(double),
+                                   (size_t)n * sizeof(double), (size_t)n, cudaMemcpyDeviceToDevice, h->stream));
+    else
+        internal_dense_to_paper(h, hm->S.N, hm->S.P, tmp.p, n, out, ldo);
     FDE_CUDA(cudaStreamSynchronize(h->stream));
     API_END(h)
 }

@@ -1283,6 +1283,7 @@ struct fde_lu {
     double* arena = nullptr;
     struct H2Plan* plan = nullptr;
     double plan_ms = 0;   // host time of the leaf-ordered plan (structure, descriptors)
+    DBuf<double> pscr;    // paper partition: the vectors in the paper order (grow-only)
 };
 
 static bool hlu2_factor(fde_lu* L, fde_hm* hm);   // hlu2.cu
@@ -2015,6 +2016,8 @@ fde_lu* hlu_build(fde_ctx* h, fde_hm* hm, double tol)
         FDE_CUDA(cudaEventRecord(h->ev0, h->stream));
         L->B.resize(L->S.bl.size());
         if (!(g_hlu_mode == 0 && hlu2_factor(L, hm))) {
+        if (L->S.paper)   // (the recursive formatted H-LU assumes the element-interleaved tree)
+            fde_fail(FDE_EINVAL_PARAM, "hlu_factor: the paper partition is factorised by the leaf-ordered H-LU only");
         // recursive formatted H-LU (any partition): copy the H-matrix into working blocks
         for (size_t b = 0; b < L->S.bl.size(); ++b) {
             const HBlock& hb = L->S.bl[b];
@@ -2103,6 +2106,16 @@ void hlu_destroy(fde_lu* L)
 void precond_apply_internal(fde_ctx* h, fde_lu* lu, const double* r, int64_t ldr, double* z, int64_t ldz, int nrhs)
 {
     lu->h = h;
+    if (lu->S.paper) {   // the paper partition's H-LU works in the paper order
+        const int64_t n = lu->S.n;
+        if (lu->pscr.n < (size_t)(n * nrhs)) lu->pscr.alloc((size_t)(n * nrhs));
+        perm_internal_to_paper(h, lu->S.N, lu->S.P, r, ldr, lu->pscr.p, n, nrhs);
+        const int pi = prof_begin(h, PROF_PRECOND, 0.0);
+        apply_sched_run(h, lu, lu->pscr.p, n, nrhs);
+        prof_end(h, pi);
+        perm_paper_to_internal(h, lu->S.N, lu->S.P, lu->pscr.p, n, z, ldz, nrhs);
+        return;
+    }
     const int pi = prof_begin(h, PROF_PRECOND, 0.0);
     if (r != z) FDE_CUDA(cudaMemcpy2DAsync(z, ldz * sizeof(double), r, ldr * sizeof(double), lu->S.n * sizeof(double),
                                            nrhs, cudaMemcpyDeviceToDevice, h->stream));

@@ -35,12 +35,69 @@ static int build_cluster(HStruct& S, const std::vector<double>& x, int e0, int e
     c.child[0] = c.child[1] = -1;
     c.lo = x[e0];
     c.hi = x[std::min(e1 + 1, S.N)];
+    c.nlo = e0;
+    c.nhi = std::min(e1 + 1, S.N);
+    c.kind = HC_INTERLEAVED;
     int id = (int)S.cl.size();
     S.cl.push_back(c);
     if (e1 - e0 > n_min) {
         int mid = (e0 + e1) / 2;
         int a = build_cluster(S, x, e0, mid, n_min);
         int b = build_cluster(S, x, mid, e1, n_min);
+        S.cl[id].child[0] = a;
+        S.cl[id].child[1] = b;
+    }
+    return id;
+}
+
+// the paper's partition: a modal tree over elements (a cluster
+// [e0, e1) holds the dofs (e, p) in the paper order e (P-1) + p - 1, support
+// [x_e0, x_e1]) and a nodal tree over the interior nodes (a cluster [j0, j1) holds
+// the hats of nodes j0..j1-1, paper dofs N (P-1) + j - 1, support [x_{j0-1}, x_{j1}])
+static int build_modal(HStruct& S, const std::vector<double>& x, int e0, int e1, int n_min)
+{
+    HCluster c;
+    c.kind = HC_MODAL;
+    c.e0 = e0;
+    c.e1 = e1;
+    c.r0 = (int64_t)e0 * (S.P - 1);
+    c.r1 = (int64_t)e1 * (S.P - 1);
+    c.child[0] = c.child[1] = -1;
+    c.lo = x[e0];
+    c.hi = x[e1];
+    c.nlo = e0;
+    c.nhi = e1;
+    const int id = (int)S.cl.size();
+    S.cl.push_back(c);
+    if (e1 - e0 > n_min) {
+        const int mid = (e0 + e1) / 2;
+        const int a = build_modal(S, x, e0, mid, n_min);
+        const int b = build_modal(S, x, mid, e1, n_min);
+        S.cl[id].child[0] = a;
+        S.cl[id].child[1] = b;
+    }
+    return id;
+}
+static int build_nodal(HStruct& S, const std::vector<double>& x, int j0, int j1, int n_min)
+{
+    HCluster c;
+    c.kind = HC_NODAL;
+    c.e0 = j0;
+    c.e1 = j1;
+    const int64_t nm = (int64_t)S.N * (S.P - 1);
+    c.r0 = nm + j0 - 1;
+    c.r1 = nm + j1 - 1;
+    c.child[0] = c.child[1] = -1;
+    c.lo = x[j0 - 1];
+    c.hi = x[j1];
+    c.nlo = j0 - 1;
+    c.nhi = j1;
+    const int id = (int)S.cl.size();
+    S.cl.push_back(c);
+    if (j1 - j0 > n_min) {
+        const int mid = (j0 + j1) / 2;
+        const int a = build_nodal(S, x, j0, mid, n_min);
+        const int b = build_nodal(S, x, mid, j1, n_min);
         S.cl[id].child[0] = a;
         S.cl[id].child[1] = b;
     }
@@ -69,7 +126,7 @@ static int build_block(HStruct& S, int t, int s, double lam, int level)
     const HCluster &T = S.cl[t], &Sg = S.cl[s];
     if (admissible(T, Sg, lam)) {
         b.type = HB_LR;
-        b.lower = (T.e0 >= Sg.e1) ? 1 : 0;   // row cluster right of column cluster
+        b.lower = (T.lo >= Sg.hi) ? 1 : 0;   // row cluster right of column cluster
     } else if (T.child[0] < 0 || Sg.child[0] < 0) {
         b.type = HB_DENSE;
     } else {
@@ -88,7 +145,7 @@ static int build_block(HStruct& S, int t, int s, double lam, int level)
     return id;
 }
 
-void hstruct_build(HStruct& S, const std::vector<double>& nodes, int P, int n_min, double lam)
+void hstruct_build(HStruct& S, const std::vector<double>& nodes, int P, int n_min, double lam, int partition)
 {
     S.N = (int)nodes.size() - 1;
     S.P = P;
@@ -96,13 +153,44 @@ void hstruct_build(HStruct& S, const std::vector<double>& nodes, int P, int n_mi
     S.cl.clear();
     S.bl.clear();
     S.depth = 0;
-    int root = build_cluster(S, nodes, 0, S.N, std::max(1, n_min));
+    S.paper = partition;
+    int root;
+    if (!partition) {
+        root = build_cluster(S, nodes, 0, S.N, std::max(1, n_min));
+    } else {
+        // virtual root [modal | nodal] (never admissible: its supports overlap), so the
+        // block tree's first level is the 2 x 2 superblock [B F; E C] of PAPER.md:168-172
+        const bool has_modal = P > 1, has_nodal = S.N > 1;
+        if (has_modal && has_nodal) {
+            HCluster c;
+            c.kind = HC_ROOT;
+            c.e0 = 0;
+            c.e1 = S.N;
+            c.r0 = 0;
+            c.r1 = S.n;
+            c.lo = nodes[0];
+            c.hi = nodes[S.N];
+            c.nlo = 0;
+            c.nhi = S.N;
+            root = (int)S.cl.size();
+            S.cl.push_back(c);
+            const int a = build_modal(S, nodes, 0, S.N, std::max(1, n_min));
+            const int b = build_nodal(S, nodes, 1, S.N, std::max(1, n_min));
+            S.cl[root].child[0] = a;
+            S.cl[root].child[1] = b;
+        } else if (has_modal) {
+            root = build_modal(S, nodes, 0, S.N, std::max(1, n_min));
+        } else {
+            root = build_nodal(S, nodes, 1, S.N, std::max(1, n_min));
+        }
+    }
     S.root = build_block(S, root, root, lam, 0);
 }
 
 // ------------------------------------------------------------- device side
 struct FDesc {
-    int e0;            // first element of the cluster
+    int mode;          // cluster kind: HC_INTERLEAVED, HC_MODAL, HC_NODAL (dof of a row)
+    int e0;            // first element of the cluster (first node for HC_NODAL)
     int rows;          // dof rows
     int64_t out;       // arena offset of the factor (rows x kcap col-major, ld rows)
     int kind;          // 0: power  pref * alt^nu * c_nu * z^{1-alpha-nu},  1: polynomial pref * (x-x0)^nu
@@ -121,7 +209,18 @@ __global__ void k_factors(const FDesc* fd, const double* nodes, int N, int P, in
     const FDesc D = fd[blockIdx.y];
     const int row = blockIdx.x * 8 + wid;
     if (row >= D.rows) return;
-    const int e = D.e0 + row / P, q = row - (row / P) * P;
+    // the row's dof as (element e, q): q < P - 1 modal psi_{q+1} of e, q = P - 1 hat of node e + 1
+    int e, q;
+    if (D.mode == HC_MODAL) {
+        e = D.e0 + row / (P - 1);
+        q = row - (row / (P - 1)) * (P - 1);
+    } else if (D.mode == HC_NODAL) {
+        e = D.e0 + row - 1;
+        q = P - 1;
+    } else {
+        e = D.e0 + row / P;
+        q = row - (row / P) * P;
+    }
     double acc[32];
     for (int nu = 0; nu < R; ++nu) acc[nu] = 0.0;
     // 32-point Gauss-Legendre, one point per lane, over the 1 or 2 elements of the dof
@@ -241,7 +340,32 @@ __global__ void k_leaf_from_dense(const LeafTile* T, const double* __restrict__ 
         if (tx < d.m) arena[d.out + (int64_t)c * d.ldo + tx] = t[tx][c];
 }
 
-fde_hm* hm_build(fde_ctx* h, fde_op* op, int R, double lam, int n_min, bool recompute, bool from_band)
+// the same for leaves in the paper order (paper partition): dof i of the paper order
+// is internal dof e P + p - 1 (modal (e, p)) or (j - 1) P + P - 1 (hat of node j)
+__device__ __forceinline__ long long internal_of_paper_dof(long long i, int N, int P)
+{
+    const long long nm = (long long)N * (P - 1);
+    if (i < nm) {
+        const long long e = i / (P - 1);
+        return e * P + (i - e * (P - 1));
+    }
+    return (i - nm) * P + (P - 1);
+}
+__global__ void k_leaf_from_dense_paper(const LeafTile* T, const double* __restrict__ A, long long lda, double* arena,
+                                        int N, int P)
+{
+    __shared__ double t[32][33];
+    const LeafTile d = T[blockIdx.x];
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    const long long ci = tx < d.n ? internal_of_paper_dof(d.c + tx, N, P) : 0;
+    for (int r = ty; r < d.m; r += 8)
+        if (tx < d.n) t[r][tx] = A[internal_of_paper_dof(d.r + r, N, P) * lda + ci];
+    __syncthreads();
+    for (int c = ty; c < d.n; c += 8)
+        if (tx < d.m) arena[d.out + (int64_t)c * d.ldo + tx] = t[tx][c];
+}
+
+fde_hm* hm_build(fde_ctx* h, fde_op* op, int R, double lam, int n_min, bool recompute, bool from_band, int partition)
 {
     if (R < 1 || R > 32) fde_fail(FDE_EINVAL_PARAM, "hmatrix_build: R must be in [1, 32]");
     if (!(lam > 0)) fde_fail(FDE_EINVAL_PARAM, "hmatrix_build: lambda must be > 0");
@@ -262,7 +386,9 @@ fde_hm* hm_build(fde_ctx* h, fde_op* op, int R, double lam, int n_min, bool reco
         hm->lam = lam;
         hm->n_min = n_min;
         HStruct& S = hm->S;
-        hstruct_build(S, op->nodes_h, op->P, n_min, lam);
+        hstruct_build(S, op->nodes_h, op->P, n_min, lam, partition);
+        if (partition && !(op->A.p && op->r0 == 0 && op->r1 == op->n))
+            fde_fail(FDE_EINVAL_PARAM, "hmatrix_build: the paper partition needs the resident dense operator (world 1, FDE_OP_DENSE)");
         tick("structure");
         const int N = op->N, P = op->P;
         const std::vector<double>& x = op->nodes_h;
@@ -303,20 +429,22 @@ fde_hm* hm_build(fde_ctx* h, fde_op* op, int R, double lam, int n_min, bool reco
             const bool s_exp = (Sg.hi - Sg.lo) <= (T.hi - T.lo);
             FDesc q{}, w{};
             // Q on the test cluster, W on the trial cluster
+            q.mode = T.kind;
             q.e0 = T.e0;
             q.rows = (int)(T.r1 - T.r0);
+            w.mode = Sg.kind;
             w.e0 = Sg.e0;
             w.rows = (int)(Sg.r1 - Sg.r0);
             const double scale = B.lower ? theta : (1.0 - theta);
             if (s_exp) {
-                // s0 = mid(Sg): anchor at x_{Sg.e0}
-                const int ea = Sg.e0;
-                const double oa = 0.5 * (x[std::min(Sg.e1 + 1, N)] - x[Sg.e0]);
+                // s0 = mid(support of Sg): anchor at its left node
+                const int ea = Sg.nlo;
+                const double oa = 0.5 * (x[Sg.nhi] - x[Sg.nlo]);
                 q.kind = 0; q.sgn = 1; q.alt = 0; q.pref = g0; q.ea = ea; q.oa = oa;
                 w.kind = 1; w.sgn = 1; w.alt = 0; w.pref = 1.0; w.ea = ea; w.oa = oa;
             } else {
-                const int ea = T.e0;
-                const double oa = 0.5 * (x[std::min(T.e1 + 1, N)] - x[T.e0]);
+                const int ea = T.nlo;
+                const double oa = 0.5 * (x[T.nhi] - x[T.nlo]);
                 q.kind = 1; q.sgn = 1; q.alt = 0; q.pref = g0; q.ea = ea; q.oa = oa;
                 w.kind = 0; w.sgn = -1; w.alt = 1; w.pref = 1.0; w.ea = ea; w.oa = oa;
             }
@@ -374,7 +502,23 @@ fde_hm* hm_build(fde_ctx* h, fde_op* op, int R, double lam, int n_min, bool reco
             maxent = std::max(maxent, L.m * L.nc);
             ld.push_back(L);
         }
-        if (!ld.empty() && from_band) {
+        if (!ld.empty() && partition) {
+            // paper partition: leaves in the paper order, gathered from the internal-order A
+            std::vector<LeafTile> lt;
+            for (auto& L : ld)
+                for (int c0 = 0; c0 < L.nc; c0 += 32)
+                    for (int r0 = 0; r0 < L.m; r0 += 32)
+                        lt.push_back(LeafTile{L.ra + r0, L.ca + c0, L.out + (int64_t)c0 * L.m + r0, L.m,
+                                              std::min(32, L.m - r0), std::min(32, L.nc - c0)});
+            DBuf<LeafTile> dlt;
+            dlt.upload(lt.data(), lt.size(), h->stream);
+            for (size_t base = 0; base < lt.size(); base += 65535u * 8) {
+                const unsigned cnt = (unsigned)std::min<size_t>(65535u * 8, lt.size() - base);
+                k_leaf_from_dense_paper<<<cnt, dim3(32, 8), 0, h->stream>>>(dlt.p + base, op->A.p, op->lda, hm->dense.p,
+                                                                            N, P);
+                FDE_CHECK_LAUNCH();
+            }
+        } else if (!ld.empty() && from_band) {
             // the assembly's pair-moment band (all pairs j <= i, world 1) is complete:
             // the leaves are expanded from it while A's expansion still runs
             DBuf<LeafDesc> dld;

@@ -5,11 +5,19 @@
 
 enum { HB_DENSE = 0, HB_LR = 1, HB_HIER = 2 };
 
+// Cluster kinds: the element-interleaved tree (reading A9: a cluster holds the
+// modal dofs of its elements and the hats of their right nodes, dofs in the
+// internal order), or the paper's partition (Fig. fig200):
+// separate modal and nodal trees under a virtual root, dofs in the paper order.
+enum { HC_INTERLEAVED = 0, HC_MODAL = 1, HC_NODAL = 2, HC_ROOT = 3 };
+
 struct HCluster {
-    int e0, e1;          // element range [e0, e1)
-    int64_t r0, r1;      // dof range (internal order)
+    int e0, e1;          // element range [e0, e1) (interleaved / modal), interior node range [j0, j1) (nodal)
+    int64_t r0, r1;      // dof range (the H-matrix's order: internal, or paper for the paper partition)
     int child[2];        // -1 for leaves
-    double lo, hi;       // support [x_e0, x_min(e1+1,N)]
+    double lo, hi;       // support
+    int nlo = 0, nhi = 0;   // node indices of the support ends (expansion points: x_nlo + (x_nhi - x_nlo)/2)
+    int kind = HC_INTERLEAVED;
 };
 
 struct HBlock {
@@ -26,6 +34,7 @@ struct HBlock {
 struct HStruct {
     int N = 0, P = 0;
     int64_t n = 0;
+    int paper = 0;           // 1: the paper's modal / nodal partition, dofs in the paper order
     std::vector<HCluster> cl;
     std::vector<HBlock> bl;
     int root = 0;
@@ -63,9 +72,10 @@ void asm_expand_leaves(fde_ctx* h, fde_op* op, const double* Ktab, const LeafDes
                        double* arena);
 
 // build the cluster tree and block partition (host, structure only)
-void hstruct_build(HStruct& S, const std::vector<double>& nodes, int P, int n_min, double lam);
+void hstruct_build(HStruct& S, const std::vector<double>& nodes, int P, int n_min, double lam, int partition = 0);
 
 // recompute: build the inadmissible leaves from pair moments even when the dense
 // operator is resident (the build then does not wait for the dense assembly)
-fde_hm* hm_build(fde_ctx* h, fde_op* op, int R, double lam, int n_min, bool recompute = false, bool from_band = false);
+fde_hm* hm_build(fde_ctx* h, fde_op* op, int R, double lam, int n_min, bool recompute = false, bool from_band = false,
+                 int partition = 0);
 void hm_to_dense_internal(fde_ctx* h, fde_hm* hm, double* out, int64_t ldo);   // out col-major n x n

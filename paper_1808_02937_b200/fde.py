@@ -41,8 +41,9 @@ EXPORTED = [
     "fde_free_operator", "fde_free_hmatrix", "fde_free_hlu", "fde_profile", "fde_profile_collect",
     "fde_launch_count", "fde_shard_rows", "fde_debug_hlu_mode", "fde_debug_pool_bytes",
     "fde_operator_wait", "fde_hmatrix_wait", "fde_create_virtual_rank", "fde_operator_rows_internal",
-    "fde_shard_matvec", "fde_debug_compact_gather",
+    "fde_shard_matvec", "fde_debug_compact_gather", "hmatrix_build_partition",
 ]
+PARTITION_INTERLEAVED, PARTITION_PAPER = 0, 1
 
 
 class FdeError(RuntimeError):
@@ -127,6 +128,7 @@ def lib():
         L.sem_rhs.argtypes = [vp, vp, ctypes.POINTER(Forcing), i32, vp, i64]
         L.stiffness_matvec.argtypes = [vp, vp, vp, vp, i32, i64, i32]
         L.hmatrix_build.argtypes = [vp, vp, i32, dbl, i32, ctypes.POINTER(vp)]
+        L.hmatrix_build_partition.argtypes = [vp, vp, i32, dbl, i32, i32, ctypes.POINTER(vp)]
         L.fde_hmatrix_get_info.argtypes = [vp, ctypes.POINTER(HMatrixInfo)]
         L.fde_hmatrix_dense_paper.argtypes = [vp, vp, vp, i64]
         L.hlu_factor.argtypes = [vp, vp, dbl, ctypes.POINTER(vp)]
@@ -360,9 +362,15 @@ class HMatrix:
             pass
 
 
-def hmatrix_build(handle: Handle, op: Operator, R: int, lam: float = 1.0, n_min: int = 16) -> HMatrix:
+def hmatrix_build(handle: Handle, op: Operator, R: int, lam: float = 1.0, n_min: int = 16,
+                  partition: int = PARTITION_INTERLEAVED) -> HMatrix:
+    """partition: PARTITION_INTERLEAVED (default, reading A9) or PARTITION_PAPER
+    (separate modal / nodal trees)."""
     out = ctypes.c_void_p()
-    _check(lib().hmatrix_build(handle.h, op.ptr, R, lam, n_min, ctypes.byref(out)), handle.h)
+    if partition == PARTITION_INTERLEAVED:
+        _check(lib().hmatrix_build(handle.h, op.ptr, R, lam, n_min, ctypes.byref(out)), handle.h)
+    else:
+        _check(lib().hmatrix_build_partition(handle.h, op.ptr, R, lam, n_min, partition, ctypes.byref(out)), handle.h)
     return HMatrix(handle, out, op.n, op)
 
 

@@ -587,3 +587,71 @@ def test_mutation_power_side_is_caught(monkeypatch, tmp_path):
     monkeypatch.setattr(OO, "_lib", L)
     nodes = fi.graded_mesh(0.0, 10.0, 24, 5.0)
     assert _fails(check_power_load, nodes, 3, 0.0, 10.0, "R", 0.5)
+
+
+# ================================================ the paper's own partition
+def check_paper_partition_bounds(p, R, n_min=4, lam=1.0):
+    """The paper's partition (separate modal / nodal cluster trees):
+    the same entrywise Lemma 3.2 / Remark bound as check_admissible_block_bounds on
+    every admissible block, with the supports of the modal clusters (unions of
+    elements) and nodal clusters (unions of [x_{j-1}, x_{j+1}]); every block of
+    the partition is pure (modal x modal, modal x nodal, ...): the first block level
+    is S_l = [B F; E C]."""
+    sysm = _system(p)
+    At, part = O.hmatrix_dense(p, sysm, R=R, lam=lam, n_min=n_min, partition="paper")
+    nodes, P, N, alpha = p.nodes, p.P, p.N, p.alpha
+    g0 = 1 / math.gamma(2 - alpha)
+    nm = N * (P - 1)
+    covered = np.zeros((p.n, p.n), dtype=bool)
+    worst, nlr = 0.0, 0
+    for t, s, kind in part:
+        assert t.kind in ("modal", "nodal") and s.kind in ("modal", "nodal")
+        rows, cols = O.pcluster_dofs(N, P, t), O.pcluster_dofs(N, P, s)
+        assert not covered[np.ix_(rows, cols)].any()
+        covered[np.ix_(rows, cols)] = True
+        if kind != "lr":
+            assert np.array_equal(At[np.ix_(rows, cols)], sysm.A[np.ix_(rows, cols)])   # exact entries (PAPER.md:399)
+            continue
+        nlr += 1
+        ts, ss = O.pcluster_support(nodes, t), O.pcluster_support(nodes, s)
+        lower = ts[0] >= ss[1]
+        test, trial = (ts, ss) if lower else (ss, ts)
+        dist = test[0] - trial[1]
+        s_exp = (trial[1] - trial[0]) <= (test[1] - test[0])
+        dexp = (trial[1] - trial[0]) if s_exp else (test[1] - test[0])
+        r = 0.5 * dexp / (0.5 * dexp + dist)
+        kb = r ** R / (1 - r) / dist ** (alpha - 1)
+        w = p.theta if lower else 1 - p.theta
+        l1 = lambda I: 2.0 if I >= nm else _l1_deriv_bound(P, I % (P - 1) + 1)
+        for I in rows:
+            for J in cols:
+                bound = w * g0 * l1(I) * l1(J) * kb + 1e-12 * math.sqrt(abs(sysm.A[I, I] * sysm.A[J, J]))
+                worst = max(worst, abs(At[I, J] - sysm.A[I, J]) / bound)
+    assert covered.all()
+    assert nlr > 0
+    assert worst <= 1.0, worst
+    return worst
+
+
+@pytest.mark.parametrize("R", [3, 8])
+def test_paper_partition_blocks_within_taylor_bound(R):
+    check_paper_partition_bounds(_mirrored_problem(0.3), R)
+
+
+def test_paper_partition_error_decay_and_lambda0():
+    """||A - A~||_F decays geometrically in R on the paper's partition too, and
+    lambda -> 0 gives A~ = A."""
+    p = _mirrored_problem(0.3)
+    sysm = _system(p)
+    errs = [np.linalg.norm(sysm.A - O.hmatrix_dense(p, sysm, R=R, n_min=4, partition="paper")[0]) for R in (2, 4, 6, 8)]
+    assert all(errs[k + 1] < 0.5 * errs[k] for k in range(3)), errs
+    At, part = O.hmatrix_dense(p, sysm, R=3, lam=1e-9, n_min=4, partition="paper")
+    assert all(k == "dense" for _, _, k in part) and np.array_equal(At, sysm.A)
+
+
+def test_mutation_paper_nodal_support_is_caught(monkeypatch):
+    """A nodal cluster's support taken as [x_{j0}, x_{j1}] (dropping the hats' left
+    halves) admits blocks whose kernel is not smooth on the real supports."""
+    m = _mutant_py(OO.pcluster_support, "return nodes[c.a - 1], nodes[c.b]", "return nodes[c.a], nodes[c.b - 1]")
+    _patch(monkeypatch, "pcluster_support", m)
+    assert _fails(check_paper_partition_bounds, _mirrored_problem(0.3), 8)

@@ -3,7 +3,8 @@ P = 3) and Table 2 (p-refinement, N = 300) analogues (SURVEY 8
 NEXT-1).  BiCGSTAB on A~^{-1} A X = A~^{-1} G, tol 1e-13, Tol_HLU 1e-3, rho = 0,
 theta = 1, alpha = 1.6 (reading A16).  Each cell: iterations / operator
 applications (the paper's counts are even: two applications per iteration, A13).
-usage: python tools/table1.py [table1|table2|both]"""
+usage: python tools/table1.py [table1|table2|both] [interleaved|paper] [n_min]
+(paper: the paper's modal / nodal partition)"""
 import sys
 sys.path.insert(0, '.')
 import fde_inputs as fi  # noqa: E402
@@ -11,13 +12,17 @@ from paper_1808_02937_b200 import fde  # noqa: E402
 
 h = fde.Handle(0)
 which = sys.argv[1] if len(sys.argv) > 1 else "both"
+part = fde.PARTITION_PAPER if (len(sys.argv) > 2 and sys.argv[2] == "paper") else fde.PARTITION_INTERLEAVED
+nmin = int(sys.argv[3]) if len(sys.argv) > 3 else None
+print(f"# partition: {'paper (modal / nodal trees)' if part else 'interleaved (reading A9)'}, "
+      f"n_min {nmin or 'default (16)'}")
 
 
 def cell(N, P, R):
     p = fi.example51(N=N, P=P, R=R)
     op = fde.assemble_problem(h, p)
     G = fde.sem_rhs(h, op, p.forcings)
-    hm = fde.hmatrix_build(h, op, R, 1.0, p.n_min)
+    hm = fde.hmatrix_build(h, op, R, 1.0, nmin or p.n_min, partition=part)
     lu = fde.hlu_factor(h, hm, 1e-3)
     X, rep = fde.solve(h, op, lu, G, method=fde.BICGSTAB, tol=1e-13, maxiter=400)
     for o in (lu, hm, op):
