@@ -330,7 +330,6 @@ int sem_assemble(fde_handle h, const fde_problem* prob, const fde_mesh* mesh, in
     op->lda = round_up(op->n, 32);
 
     op->tm.start(h->stream);   // (the call returns without waiting: the next calls' host work overlaps it)
-    op->h = h;
     asm_prepare_tables(h, op);
     FDE_CUDA(cudaEventCreateWithFlags(&op->ev_tab, cudaEventDisableTiming));
     FDE_CUDA(cudaEventRecord(op->ev_tab, h->stream));
@@ -532,6 +531,9 @@ int hmatrix_build(fde_handle h, fde_operator op, int R, double lambda, int n_min
         (*out)->st = hb;
         h->stream = orig;
         fde_set_alloc_stream(orig);
+        // (the operator's buffers must not be released before this build read them)
+        if (!op->ev_side) FDE_CUDA(cudaEventCreateWithFlags(&op->ev_side, cudaEventDisableTiming));
+        FDE_CUDA(cudaEventRecord(op->ev_side, hb));
     } else {
         *out = hm_build(h, op, R, lambda, n_min);
         (*out)->st = h->stream;
@@ -686,14 +688,9 @@ int fde_solve(fde_handle h, fde_operator op, fde_hlu lu, const double* G, double
 
 void fde_free_operator(fde_operator op)
 {
-    // the operator's buffers are released stream-ordered on the caller's stream:
-    // behind any H-matrix build still reading its tables on the build stream
-    if (op && op->h && op->h->hb) {
-        try {
-            stream_after(op->h, op->h->stream, op->h->hb);
-        } catch (...) {
-        }
-    }
+    // the operator's buffers are released stream-ordered on the stream they were
+    // allocated on: behind any H-matrix build that read them on the build stream
+    if (op && op->ev_side && op->tab.nodes.s) cudaStreamWaitEvent(op->tab.nodes.s, op->ev_side, 0);
     delete op;
 }
 void fde_free_hmatrix(fde_hmatrix hm) { delete hm; }

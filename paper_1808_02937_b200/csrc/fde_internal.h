@@ -322,7 +322,7 @@ struct fde_op {
     size_t xw_cols = 0;
     double assemble_ms = 0;
     int world = 1;
-    fde_ctx* h = nullptr;           // creating handle (stream-ordered release behind its build stream)
+    cudaEvent_t ev_side = nullptr;  // recorded on the build stream after an H-matrix build read this operator
     cudaEvent_t ev_tab = nullptr;   // recorded after the quadrature / node tables: the H-matrix build may start
     cudaEvent_t ev_k = nullptr;     // recorded after the pair-moment band (world 1): leaves can be expanded from it
     const double* kb_row = nullptr; // the band (the handle's kt_row / kt_col: valid until the next assembly)
@@ -331,6 +331,7 @@ struct fde_op {
     {
         if (ev_tab) cudaEventDestroy(ev_tab);
         if (ev_k) cudaEventDestroy(ev_k);
+        if (ev_side) cudaEventDestroy(ev_side);
     }
 };
 
