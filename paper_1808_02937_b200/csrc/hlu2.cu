@@ -1591,12 +1591,16 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
     };
     auto put_panel = [&](const std::vector<VPanel>& v, H2Launch& ln) {
         ln.pan0 = (int)vpan.size();
+        static const int inv_strip = getenv("FDE_H2_INV_STRIP") ? std::max(8, std::min(H2_STRIP, atoi(getenv("FDE_H2_INV_STRIP")))) : 16;
         for (auto& p : v) {
-            for (int c0 = 0; c0 < p.nvec; c0 += H2_STRIP) {
+            // (the tile inverses -- substitutions on identity strips, X in the inverse
+            // arenas -- may use narrower strips: more CTAs, shorter trailing updates)
+            const int strip = (p.X.sp == 4 || p.X.sp == 5) && p.Ti.sp < 0 ? inv_strip : H2_STRIP;
+            for (int c0 = 0; c0 < p.nvec; c0 += strip) {
                 H2Panel d;
                 d.T = res(p.T);
                 d.ldt = p.ldt;
-                const int nv = std::min(H2_STRIP, p.nvec - c0);
+                const int nv = std::min(strip, p.nvec - c0);
                 d.X = res(p.X) + (p.mode == 2 ? c0 : c0 * p.ldx);
                 d.ldx = p.ldx;
                 d.m = p.m;
@@ -1673,8 +1677,8 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
             n_tc += (size_t)(ceil_div(S.bl[e.blk].m, TRUNC_CHUNK) + ceil_div(S.bl[e.blk].n, TRUNC_CHUNK));
         }
     };
-    auto cnt_pan = [&](const std::vector<VPanel>& v) {
-        for (auto& q : v) n_pan += (size_t)ceil_div(q.nvec, H2_STRIP);
+    auto cnt_pan = [&](const std::vector<VPanel>& v) {   // (8: the narrowest inverse strip, FDE_H2_INV_STRIP)
+        for (auto& q : v) n_pan += (size_t)ceil_div(q.nvec, (q.X.sp == 4 || q.X.sp == 5) && q.Ti.sp < 0 ? 8 : H2_STRIP);
     };
     auto cnt_cp = [&](const std::vector<VCopy>& v) {
         for (auto& c : v) {
