@@ -1592,10 +1592,11 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
     auto put_panel = [&](const std::vector<VPanel>& v, H2Launch& ln) {
         ln.pan0 = (int)vpan.size();
         static const int inv_strip = getenv("FDE_H2_INV_STRIP") ? std::max(8, std::min(H2_STRIP, atoi(getenv("FDE_H2_INV_STRIP")))) : 16;
+        static const bool sub_all = !(getenv("FDE_H2_SUB_STRIP_ALL") && atoi(getenv("FDE_H2_SUB_STRIP_ALL")) == 0);   // (also the neighbour panels)
         for (auto& p : v) {
             // (the tile inverses -- substitutions on identity strips, X in the inverse
             // arenas -- may use narrower strips: more CTAs, shorter trailing updates)
-            const int strip = (p.X.sp == 4 || p.X.sp == 5) && p.Ti.sp < 0 ? inv_strip : H2_STRIP;
+            const int strip = (sub_all || p.X.sp == 4 || p.X.sp == 5) && p.Ti.sp < 0 ? inv_strip : H2_STRIP;
             for (int c0 = 0; c0 < p.nvec; c0 += strip) {
                 H2Panel d;
                 d.T = res(p.T);
@@ -1678,7 +1679,7 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         }
     };
     auto cnt_pan = [&](const std::vector<VPanel>& v) {   // (8: the narrowest inverse strip, FDE_H2_INV_STRIP)
-        for (auto& q : v) n_pan += (size_t)ceil_div(q.nvec, (q.X.sp == 4 || q.X.sp == 5) && q.Ti.sp < 0 ? 8 : H2_STRIP);
+        for (auto& q : v) n_pan += (size_t)ceil_div(q.nvec, q.Ti.sp < 0 ? 8 : H2_STRIP);
     };
     auto cnt_cp = [&](const std::vector<VCopy>& v) {
         for (auto& c : v) {
