@@ -122,6 +122,24 @@ long long fde_launch_count(void);
  * compacted widths, sum of Jacobi sweeps, max width}; counted only when the
  * process runs with FDE_TRUNC_STATS=1 (no atomics on the hot path otherwise). */
 int fde_debug_trunc_stats(unsigned long long* out4);
+/* Diagnostics (FDE_TRUNC_STATS=1): out32[0..3] as above; out32[4 + i] = SM
+ * cycles of phase i of the truncation core k_bcore summed over its CTAs (0 column
+ * mask, 1 Gram reduction, 2 index / zeroing, 3 scaling, 4 pivoted Cholesky,
+ * 5 core product, 6 Jacobi, 7 ordering, 8 output); out32[16..19] = sum / max of
+ * the nonzero width and of the chunk count per entry; out32[20] = max cycles of
+ * one CTA.  The rest is zero. */
+int fde_debug_trunc_profile(unsigned long long* out32);
+/* Test entry: the H-LU's batched formatted truncation (the
+ * "prescribed tolerance" Tol_HLU of the H-LU, Boerm's truncation of a low-rank sum
+ * to the singular values sigma_i > tol * sigma_1) applied to nb independent sums
+ * U_q V_q^T, q < nb.  U: device, nb consecutive column-major m x k blocks; V: nb
+ * n x k blocks; Uo / Vo: device outputs, nb m x kc / n x kc blocks (columns >= the
+ * kept rank are zero; Uo_q Vo_q^T is the truncated sum).  1 <= k, kc <= 64,
+ * tol > 0.  *overflow = 1 when some sum kept more than kc singular values (then
+ * the first kc are kept).  Runs on the handle's stream and synchronises it.
+ * Errors: FDE_EINVAL_SIZE, FDE_EINVAL_PARAM, FDE_ECUDA. */
+int fde_debug_truncate(fde_handle h, const double* U, const double* V, int64_t m, int64_t n, int k, int nb, double tol,
+                       int kc, double* Uo, double* Vo, int* overflow);
 /* Diagnostics: H-LU algorithm selection for later hlu_factor calls (process
  * wide).  mode 0 (default): the leaf-ordered batched factorisation whenever the
  * partition allows it (leaves <= 128 dofs), else the recursive one; mode 1: the

@@ -21,6 +21,9 @@ void bnd_to_paper(fde_ctx* h, fde_op* op, double* out);
 void internal_dense_to_paper(fde_ctx* h, int N, int P, const double* in, int64_t ldi, double* out, int64_t ldo);
 void prof_collect(fde_ctx* h, double* out, int reset);
 void hlu_trunc_stats(unsigned long long* out4);
+void hlu_trunc_profile(unsigned long long* out32);
+int hlu_debug_truncate(fde_ctx* h, const double* U, const double* V, long long m, long long n, int k, int nb,
+                       double tol, int kc, double* Uo, double* Vo);
 
 static thread_local std::string g_noctx_err;
 static thread_local cudaStream_t g_alloc_stream = nullptr;
@@ -200,6 +203,23 @@ int fde_debug_trunc_stats(unsigned long long* out4)
     fde_ctx* h = nullptr;
     API_BEGIN
     hlu_trunc_stats(out4);
+    API_END(h)
+}
+
+int fde_debug_trunc_profile(unsigned long long* out32)
+{
+    fde_ctx* h = nullptr;
+    API_BEGIN
+    hlu_trunc_profile(out32);
+    API_END(h)
+}
+
+int fde_debug_truncate(fde_handle h, const double* U, const double* V, int64_t m, int64_t n, int k, int nb, double tol,
+                       int kc, double* Uo, double* Vo, int* overflow)
+{
+    API_BEGIN
+    if (!U || !V || !Uo || !Vo || !overflow) fde_fail(FDE_EINVAL_PARAM, "fde_debug_truncate: NULL pointer");
+    *overflow = hlu_debug_truncate(h, U, V, m, n, k, nb, tol, kc, Uo, Vo);
     API_END(h)
 }
 

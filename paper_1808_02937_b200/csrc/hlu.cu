@@ -752,10 +752,19 @@ __device__ __forceinline__ bool h2_chk(const void* p, long long nbytes, int tag,
     return false;
 }
 
-__device__ unsigned long long g_trunc_stats[4];
+__device__ unsigned long long g_trunc_stats[32];   // [0..3] calls, sum ke, sum sweeps, max; [4..12] k_bcore phase cycles; [16..20] shapes
 __constant__ int g_trunc_stats_on = 0;   // debug statistics only with FDE_TRUNC_STATS=1 (no atomics on the hot path)
 __device__ double g_trunc_jeps = 0.0;   // (debug FDE_TRUNC_JEPS)
 __device__ int g_trunc_check = 0;   // descriptor checks (FDE_DEBUG_SERIAL)   // calls, sum ke, sum sweeps, max ke
+// (debug FDE_TRUNC_STATS) cycles of k_bcore phase i, summed over CTAs (thread 0's clock)
+#define BC_MARK(i)                                                                              \
+    do {                                                                                        \
+        if (g_trunc_stats_on && threadIdx.x == 0) {                                             \
+            const long long t_ = clock64();                                                     \
+            atomicAdd(&g_trunc_stats[4 + (i)], (unsigned long long)(t_ - bc_t));                \
+            bc_t = t_;                                                                          \
+        }                                                                                       \
+    } while (0)
 
 // Truncation core (one CTA).  Input: Gram matrices Gu = U^T U, Gv = V^T V of a
 // low-rank sum U V^T with k columns (zero columns allowed: they are the unused
@@ -951,8 +960,9 @@ __global__ void __launch_bounds__(256) k_bgram(const TEntry* E, const TChunk* C,
 // (the common case: small footprint, the CTA fits beside the bulk GEMMs), else
 // in the entry's slot of the global scratch gscr (BCORE_GSCR doubles per entry).
 #define BCORE_KS 32
+#define BCORE_THREADS 256
 #define BCORE_GSCR (5 * TRUNC_KMAX * TRUNC_KMAX + TRUNC_KMAX)
-__global__ void __launch_bounds__(256) k_bcore(const TEntry* E, const TChunk* C, const double* part, double tol,
+__global__ void __launch_bounds__(BCORE_THREADS) k_bcore(const TEntry* E, const TChunk* C, const double* part, double tol,
                                               int kc, double* T, int* flag, double* gscr)
 {
     __shared__ double ssm[5 * BCORE_KS * BCORE_KS + BCORE_KS];
@@ -970,6 +980,8 @@ __global__ void __launch_bounds__(256) k_bcore(const TEntry* E, const TChunk* C,
     }
     __shared__ unsigned long long gmask;
     __shared__ int cm[TRUNC_KMAX];
+    long long bc_t = clock64();
+    const long long bc_t0 = bc_t;
     if (threadIdx.x == 0) gmask = 0ull;
     __syncthreads();
     // columns of U with a nonzero entry (the only ones with Gu_jj > 0; Gv is read
@@ -985,8 +997,15 @@ __global__ void __launch_bounds__(256) k_bcore(const TEntry* E, const TChunk* C,
         if ((threadIdx.x & 31) == 0 && lm) atomicOr(&gmask, lm);
     }
     __syncthreads();
+    BC_MARK(0);
     const unsigned long long gm = gmask;
     const int nm = __popcll(gm);
+    if (g_trunc_stats_on && threadIdx.x == 0) {
+        atomicAdd(&g_trunc_stats[16], (unsigned long long)nm);
+        atomicMax(&g_trunc_stats[17], (unsigned long long)nm);
+        atomicAdd(&g_trunc_stats[18], (unsigned long long)(e.c_hi - e.c_lo));
+        atomicMax(&g_trunc_stats[19], (unsigned long long)(e.c_hi - e.c_lo));
+    }
     if (threadIdx.x < k && ((gm >> threadIdx.x) & 1ull)) cm[__popcll(gm & ((1ull << threadIdx.x) - 1ull))] = threadIdx.x;
     double* W = (nm <= BCORE_KS) ? ssm : gscr + (long long)blockIdx.x * BCORE_GSCR;
     double* Gu = W;              // Gu[b * nm + a] = (U^T U)(cm[a], cm[b])
@@ -1012,8 +1031,17 @@ __global__ void __launch_bounds__(256) k_bcore(const TEntry* E, const TChunk* C,
         (side ? Gv : Gu)[q] = s;
     }
     __syncthreads();
+    BC_MARK(1);
     double* Tu = T + e.tofs;
     double* Tv = Tu + (long long)k * kc;
+    // rotation threshold: converged to 1e-12 relative when truncating to tol >= 1e-6
+    // (far below the truncation error), to rounding otherwise
+    // (and, then, off-diagonal entries below 1e-14 ||A||_F, the rounding noise
+    // the rotations themselves leave behind, are not rotated: with a wide
+    // eigenvalue range the relative test alone never stops)
+    // (FDE_TRUNC_JEPS: debug override of the relative rotation threshold)
+    const double jeps = g_trunc_jeps > 0.0 ? g_trunc_jeps : (tol >= 1e-6) ? 1e-12 : 1e-15,
+                 jarel = (tol >= 1e-6) ? 1e-14 : 1e-16;
     __shared__ int idx[TRUNC_KMAX];   // compact positions of the columns with Gu_jj > 0
     __shared__ int ke_sh;
     if (threadIdx.x == 0) {
@@ -1026,6 +1054,7 @@ __global__ void __launch_bounds__(256) k_bcore(const TEntry* E, const TChunk* C,
     const int ke = ke_sh;
     for (int t = threadIdx.x; t < k * kc; t += blockDim.x) { Tu[t] = 0.0; Tv[t] = 0.0; }
     __syncthreads();
+    BC_MARK(2);
     if (ke == 0) return;
     const int n = (ke + 1) & ~1;
     double* A = Gv + nm * nm;
@@ -1043,14 +1072,7 @@ __global__ void __launch_bounds__(256) k_bcore(const TEntry* E, const TChunk* C,
         A[t] = (i < ke && j < ke) ? Gu[idx[j] * nm + idx[i]] / (sc[i] * sc[j]) : 0.0;
     }
     __syncthreads();
-    // rotation threshold: converged to 1e-12 relative when truncating to tol >= 1e-6
-    // (far below the truncation error), to rounding otherwise
-    // (and, then, off-diagonal entries below 1e-14 ||A||_F, the rounding noise
-    // the rotations themselves leave behind, are not rotated: with a wide
-    // eigenvalue range the relative test alone never stops)
-    // (FDE_TRUNC_JEPS: debug override of the relative rotation threshold)
-    const double jeps = g_trunc_jeps > 0.0 ? g_trunc_jeps : (tol >= 1e-6) ? 1e-12 : 1e-15,
-                 jarel = (tol >= 1e-6) ? 1e-14 : 1e-16;
+    BC_MARK(3);
     // Factor of the scaled Gram by pivoted Cholesky, D Gu D = P R^T R P^T (R: ru x ke,
     // upper trapezoidal in pivoted order; pivots below 1e-14 of the unit diagonal --
     // nearly dependent columns -- end it), in place in A: ke sequential steps
@@ -1108,6 +1130,7 @@ __global__ void __launch_bounds__(256) k_bcore(const TEntry* E, const TChunk* C,
         }
         __syncthreads();
     }
+    BC_MARK(4);
     const int ru = ru_sh;
     const int n2 = (ru + 1) & ~1;
     // X_temp (ke x ru, in Eu): Gvp R^T, Gvp = pivoted scaled Gv;  M (ru x ru, in X): R X_temp
@@ -1130,8 +1153,10 @@ __global__ void __launch_bounds__(256) k_bcore(const TEntry* E, const TChunk* C,
         X[c * n2 + r] = s;
     }
     __syncthreads();
+    BC_MARK(5);
     const int sw2 = (n2 <= 32) ? warp_jacobi(X, Eu, n2, jeps, jarel) : cta_jacobi(X, Eu, n2, nullptr, jeps, jarel);
     __syncthreads();
+    BC_MARK(6);
     if (g_trunc_stats_on && threadIdx.x == 0) {   // (debug statistics: calls, sum ke, sum sweeps, max sweeps)
         atomicAdd(&g_trunc_stats[0], 1ull);
         atomicAdd(&g_trunc_stats[1], (unsigned long long)ke);
@@ -1162,6 +1187,7 @@ __global__ void __launch_bounds__(256) k_bcore(const TEntry* E, const TChunk* C,
         r_sh = r;
     }
     __syncthreads();
+    BC_MARK(7);
     const int r = r_sh;
     // T'v = R^T X_r S_r^{-1} (rows a = 0..ke-1, pivoted) and T'u = R11^{-1} X_r S_r
     // (back substitution, one thread per kept column); unpivot and unscale on store
@@ -1189,6 +1215,11 @@ __global__ void __launch_bounds__(256) k_bcore(const TEntry* E, const TChunk* C,
                 Tu[c * k + cm[idx[ia]]] = (a < ru ? y : 0.0) / sc[ia];
             }
         }
+        if (g_trunc_stats_on) {
+            __syncthreads();
+            BC_MARK(8);
+            if (threadIdx.x == 0) atomicMax(&g_trunc_stats[20], (unsigned long long)(clock64() - bc_t0));
+        }
         return;
     }
     for (int c = threadIdx.x; c < r; c += blockDim.x) {
@@ -1204,6 +1235,11 @@ __global__ void __launch_bounds__(256) k_bcore(const TEntry* E, const TChunk* C,
             const int ia = piv[a];
             Tu[c * k + cm[idx[ia]]] = (a < ru ? y[a] : 0.0) / sc[ia];
         }
+    }
+    if (g_trunc_stats_on) {
+        __syncthreads();
+        BC_MARK(8);
+        if (threadIdx.x == 0) atomicMax(&g_trunc_stats[20], (unsigned long long)(clock64() - bc_t0));
     }
 }
 
@@ -1662,7 +1698,7 @@ static void flush_dirty(fde_lu* L)
     k_bgram<<<(unsigned)C.size(), 256, 0, L->h->stream>>>(dE.p, dC.p, part);
     FDE_CHECK_LAUNCH();
     double* gscr = lu_alloc(L, E.size() * (size_t)BCORE_GSCR);
-    k_bcore<<<(unsigned)E.size(), 256, 0, L->h->stream>>>(dE.p, dC.p, part, L->tol, kc, T, L->dflag.p + 1, gscr);
+    k_bcore<<<(unsigned)E.size(), BCORE_THREADS, 0, L->h->stream>>>(dE.p, dC.p, part, L->tol, kc, T, L->dflag.p + 1, gscr);
     FDE_CHECK_LAUNCH();
     const size_t asmem = (size_t)(kmax * kc + TRUNC_CHUNK * kmax) * sizeof(double);
     set_smem_once((const void*)k_bapply, (int)asmem);
@@ -1992,7 +2028,7 @@ static void hlu_rec(fde_lu* L, int a)
 
 int g_hlu_mode = 0;   // 0: leaf-ordered batched H-LU when the partition allows it, 1: recursive only
 
-fde_lu* hlu_build(fde_ctx* h, fde_hm* hm, double tol)
+static void trunc_flags_once(fde_ctx* h)
 {
     static bool stats_set[64] = {};
     if (!stats_set[h->device & 63]) {   // (per device: __constant__ memory)
@@ -2000,6 +2036,11 @@ fde_lu* hlu_build(fde_ctx* h, fde_hm* hm, double tol)
         FDE_CUDA(cudaMemcpyToSymbol(g_trunc_stats_on, &on, sizeof(int)));
         stats_set[h->device & 63] = true;
     }
+}
+
+fde_lu* hlu_build(fde_ctx* h, fde_hm* hm, double tol)
+{
+    trunc_flags_once(h);
     fde_lu* L = new fde_lu();
     try {
         L->op = hm->op;
@@ -3430,4 +3471,70 @@ static void apply_sched_run(fde_ctx* h, fde_lu* L, double* x, int64_t ldx, int n
 void hlu_trunc_stats(unsigned long long* out4)
 {
     FDE_CUDA(cudaMemcpyFromSymbol(out4, g_trunc_stats, sizeof(unsigned long long) * 4));
+}
+// Debug / test entry: the batched truncation (k_bgram -> k_bcore -> k_bapply) of nb
+// independent sums U_q V_q^T (U_q: m x k, V_q: n x k, column-major, consecutive)
+// into Uo_q (m x kc), Vo_q (n x kc) on the handle's stream; returns the overflow flag.
+int hlu_debug_truncate(fde_ctx* h, const double* U, const double* V, long long m, long long n, int k, int nb,
+                       double tol, int kc, double* Uo, double* Vo)
+{
+    if (k < 1 || k > TRUNC_KMAX || kc < 1 || kc > TRUNC_KMAX || nb < 1 || m < 1 || n < 1 || !(tol > 0.0))
+        fde_fail(FDE_EINVAL_SIZE, "fde_debug_truncate: sizes");
+    trunc_flags_once(h);
+    cudaStream_t st = h->stream;
+    std::vector<TEntry> E;
+    std::vector<TChunk> C;
+    long long gofs = 0, tofs = 0;
+    for (int q = 0; q < nb; ++q) {
+        TEntry e;
+        e.U = U + (long long)q * m * k;
+        e.V = V + (long long)q * n * k;
+        e.Uo = Uo + (long long)q * m * kc;
+        e.Vo = Vo + (long long)q * n * kc;
+        e.m = m;
+        e.n = n;
+        e.k = k;
+        e.zero_tail = 0;
+        e.c_lo = (int)C.size();
+        for (int side = 0; side < 2; ++side) {
+            const long long rows = side ? n : m;
+            for (long long r0 = 0; r0 < rows; r0 += TRUNC_CHUNK)
+                C.push_back(TChunk{q, side, r0, (int)std::min<long long>(TRUNC_CHUNK, rows - r0)});
+        }
+        e.c_hi = (int)C.size();
+        e.gofs = gofs;
+        gofs += (long long)(e.c_hi - e.c_lo) * GRAM_SLOT(k);
+        e.tofs = tofs;
+        tofs += 2LL * k * kc;
+        E.push_back(e);
+    }
+    void *dE = nullptr, *dC = nullptr, *part = nullptr, *T = nullptr, *gscr = nullptr, *flag = nullptr;
+    FDE_CUDA(cudaMallocAsync(&dE, E.size() * sizeof(TEntry), st));
+    FDE_CUDA(cudaMallocAsync(&dC, C.size() * sizeof(TChunk), st));
+    FDE_CUDA(cudaMallocAsync(&part, gofs * sizeof(double), st));
+    FDE_CUDA(cudaMallocAsync(&T, tofs * sizeof(double), st));
+    FDE_CUDA(cudaMallocAsync(&gscr, E.size() * (size_t)BCORE_GSCR * sizeof(double), st));
+    FDE_CUDA(cudaMallocAsync(&flag, sizeof(int), st));
+    FDE_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), st));
+    FDE_CUDA(cudaMemcpyAsync(dE, E.data(), E.size() * sizeof(TEntry), cudaMemcpyHostToDevice, st));
+    FDE_CUDA(cudaMemcpyAsync(dC, C.data(), C.size() * sizeof(TChunk), cudaMemcpyHostToDevice, st));
+    k_bgram<<<(unsigned)C.size(), 256, 0, st>>>((const TEntry*)dE, (const TChunk*)dC, (double*)part);
+    FDE_CHECK_LAUNCH();
+    k_bcore<<<(unsigned)E.size(), BCORE_THREADS, 0, st>>>((const TEntry*)dE, (const TChunk*)dC, (const double*)part, tol,
+                                                        kc, (double*)T, (int*)flag, (double*)gscr);
+    FDE_CHECK_LAUNCH();
+    const size_t asmem = (size_t)(k * kc + TRUNC_CHUNK * k) * sizeof(double);
+    set_smem_once((const void*)k_bapply, (int)asmem);
+    k_bapply<<<(unsigned)C.size(), 256, asmem, st>>>((const TEntry*)dE, (const TChunk*)dC, (const double*)T, kc);
+    FDE_CHECK_LAUNCH();
+    int hf = 0;
+    FDE_CUDA(cudaMemcpyAsync(&hf, flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+    for (void* q : {dE, dC, part, T, gscr, flag}) FDE_CUDA(cudaFreeAsync(q, st));
+    FDE_CUDA(cudaStreamSynchronize(st));
+    return hf;
+}
+
+void hlu_trunc_profile(unsigned long long* out32)
+{
+    FDE_CUDA(cudaMemcpyFromSymbol(out32, g_trunc_stats, sizeof(unsigned long long) * 32));
 }

@@ -720,15 +720,23 @@ struct VTerm {
 struct VTermList {
     VTerm inl[1];
     int n = 0;
+    int off = 1;   // list index of more[0] (0 once a whole vector was adopted)
     std::vector<VTerm> more;
     void push_back(const VTerm& t)
     {
-        if (n < 1) inl[n] = t;
+        if (n < off) inl[n] = t;
         else more.push_back(t);
         ++n;
     }
+    // take over a vector of terms without copying them (on an empty list)
+    void adopt(std::vector<VTerm>&& v)
+    {
+        more = std::move(v);
+        n = (int)more.size();
+        off = 0;
+    }
     size_t size() const { return (size_t)n; }
-    const VTerm& operator[](int i) const { return i < 1 ? inl[i] : more[i - 1]; }
+    const VTerm& operator[](int i) const { return i < off ? inl[i] : more[i - off]; }
     struct It {
         const VTermList* l;
         int i;
@@ -1251,6 +1259,7 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
                                 if (dpend[key].empty()) {
                                     dfirst[key] = k;
                                     dstarted[k].push_back(key);
+                                    dpend[key].reserve(16);   // (~16 terms reach kflush)
                                 }
                                 dpend[key].push_back(term);
                                 if ((dpend_k[key] += term.k) >= kflush) dfull.push_back(key);
@@ -1281,11 +1290,11 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
                 const int t = own(i, j);
                 const HBlock& T = S.bl[t];
                 VTask tk{{0, t, (lr0[j] - col0(t)) * T.m + (lr0[i] - row0(t))}, T.m, lm(i), lm(j), 1.0, {}};
-                for (const VTerm& q : pv) tk.terms.push_back(q);
+                tk.terms.adopt(std::move(pv));   // (the pending vector moves into the task)
                 st.g3.push_back(std::move(tk));
                 // (k+2, k+2) on the critical stream: it is the input of LU(k+2) next step
                 st.g3crit.push_back(i == m2 && j == m2 ? 1 : 0);
-                std::vector<VTerm>().swap(pv);
+                pv = std::vector<VTerm>();
             };
             for (size_t key : dfull) flush((int)(key / nl), (int)(key % nl));
             dfull.clear();
@@ -1862,7 +1871,7 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         dbg("bgram");
         if (!ws) tmark(0);
         const int kmax = tr.kmax;
-        k_bcore<<<tr.ne, 256, 0, st>>>(E, C, part, L->tol, rmax, Tt, L->dflag.p + 1, ws ? P->tr_scr2 : P->tr_scr);
+        k_bcore<<<tr.ne, BCORE_THREADS, 0, st>>>(E, C, part, L->tol, rmax, Tt, L->dflag.p + 1, ws ? P->tr_scr2 : P->tr_scr);
         FDE_CHECK_LAUNCH();
         dbg("bcore");
         if (!ws) tmark(1);

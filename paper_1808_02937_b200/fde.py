@@ -41,7 +41,8 @@ EXPORTED = [
     "fde_free_operator", "fde_free_hmatrix", "fde_free_hlu", "fde_profile", "fde_profile_collect",
     "fde_launch_count", "fde_shard_rows", "fde_debug_hlu_mode", "fde_debug_pool_bytes",
     "fde_operator_wait", "fde_hmatrix_wait", "fde_create_virtual_rank", "fde_operator_rows_internal",
-    "fde_shard_matvec", "fde_debug_compact_gather", "hmatrix_build_partition",
+    "fde_shard_matvec", "fde_debug_compact_gather", "hmatrix_build_partition", "fde_debug_truncate",
+    "fde_debug_trunc_profile",
 ]
 PARTITION_INTERLEAVED, PARTITION_PAPER = 0, 1
 
@@ -115,6 +116,7 @@ def lib():
         L.fde_operator_rows_internal.argtypes = [vp, vp, vp, i64]
         L.fde_shard_matvec.argtypes = [vp, vp, vp, i64, vp, i64, i32]
         L.fde_debug_compact_gather.argtypes = [vp, vp, vp, vp, i64, i32]
+        L.fde_debug_truncate.argtypes = [vp, vp, vp, i64, i64, i32, i32, dbl, i32, vp, vp, ctypes.POINTER(i32)]
         L.fde_destroy.argtypes = [vp]
         L.fde_destroy.restype = None
         L.fde_last_error.argtypes = [vp]
@@ -324,6 +326,23 @@ def compact_gather(handle: Handle, op: Operator, gathered, nrhs: int):
     y = torch.empty((nrhs, op.n), dtype=torch.float64, device=g.device)
     _check(lib().fde_debug_compact_gather(handle.h, op.ptr, _ptr(g), _ptr(y), op.n, nrhs), handle.h)
     return y
+
+
+def truncate(handle: Handle, U, V, tol: float, kc: int):
+    """The H-LU's batched truncation of nb sums U_q V_q^T: U (nb, k, m), V (nb, k, n)
+    (rows of the torch tensors = columns of the column-major blocks) -> (Uo, Vo,
+    overflow) with Uo (nb, kc, m), Vo (nb, kc, n)."""
+    import torch
+    U = U.contiguous()
+    V = V.contiguous()
+    nb, k, m = U.shape
+    n = V.shape[2]
+    Uo = torch.empty((nb, kc, m), dtype=torch.float64, device=U.device)
+    Vo = torch.empty((nb, kc, n), dtype=torch.float64, device=U.device)
+    ov = ctypes.c_int32(0)
+    _check(lib().fde_debug_truncate(handle.h, _ptr(U), _ptr(V), m, n, k, nb, tol, kc, _ptr(Uo), _ptr(Vo),
+                                    ctypes.byref(ov)), handle.h)
+    return Uo, Vo, bool(ov.value)
 
 
 def operator_boundary_columns(handle: Handle, op: Operator):
