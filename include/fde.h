@@ -228,6 +228,16 @@ int fde_shard_matvec(fde_handle h, fde_operator op, const double* x, int64_t ldx
  * row r0(g) + r of column c from rank g.  Writes y (device, paper order, ld). */
 int fde_debug_compact_gather(fde_handle h, fde_operator op, const double* gathered, double* y, int64_t ld,
                              int nrhs);
+/* Test entry: the sharded matvec's communication path on one GPU.  On a world-1
+ * handle, creates a one-rank NCCL communicator (libnccl.so.2 resolved with
+ * dlopen, ncclGetUniqueId, ncclCommInitRank), computes the local rows of A x
+ * (x: nrhs paper-order columns, stride ld), passes them through ncclAllGather and
+ * the post-all-gather compaction exactly as every Krylov iteration of a world > 1
+ * run does, writes y (paper order, stride ld) and destroys the communicator.
+ * Synchronises the handle's stream.  Errors: FDE_EINVAL_PARAM (world != 1, a
+ * handle that already has a communicator, or no dense form), FDE_EINVAL_SIZE,
+ * FDE_ENCCL (library or call failure), FDE_ECUDA. */
+int fde_debug_comm_selftest(fde_handle h, fde_operator op, const double* x, double* y, int64_t ld, int nrhs);
 
 /* -------------------------------------------------------- hmatrix_build */
 /* H-matrix H ~ S_l on the element-cluster block tree with admissibility

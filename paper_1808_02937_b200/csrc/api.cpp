@@ -503,6 +503,36 @@ int fde_shard_matvec(fde_handle h, fde_operator op, const double* x, int64_t ldx
     API_END(h)
 }
 
+// The sharded matvec's communication path on ONE GPU: a one-rank NCCL communicator
+// (dlopen'ed libnccl, ncclGetUniqueId, ncclCommInitRank) carries the local GEMV's
+// rows through ncclAllGather and the post-all-gather compaction, exactly as a
+// world > 1 stiffness_matvec does per iteration; y must equal the world-1 A x.
+int fde_debug_comm_selftest(fde_handle h, fde_operator op, const double* x, double* y, int64_t ld, int nrhs)
+{
+    API_BEGIN
+    if (h->world != 1 || h->nccl || h->virt) fde_fail(FDE_EINVAL_PARAM, "fde_debug_comm_selftest: needs a world-1 handle");
+    if (!(op->flags & FDE_OP_DENSE)) fde_fail(FDE_EINVAL_PARAM, "operator has no dense form");
+    if (nrhs < 1 || ld < op->n) fde_fail(FDE_EINVAL_SIZE, "fde_debug_comm_selftest: sizes");
+    char uid[128];
+    comm_unique_id(uid);
+    comm_init(h, uid);
+    try {
+        ensure_work(op, nrhs);
+        perm_paper_to_internal(h, op->N, op->P, x, ld, op->xw.p, op->lda, nrhs);
+        const size_t need = (size_t)op->rows_max * nrhs;
+        if (h->mv_loc.n < need) h->mv_loc.alloc(need);
+        dense_gemv(h, op, op->xw.p, op->lda, h->mv_loc.p, op->rows_max, nrhs);
+        comm_allgather_rows(h, op, h->mv_loc.p, op->yw.p, op->lda, nrhs);
+        perm_internal_to_paper(h, op->N, op->P, op->yw.p, op->lda, y, ld, nrhs);
+        FDE_CUDA(cudaStreamSynchronize(h->stream));
+    } catch (...) {
+        comm_destroy(h);
+        throw;
+    }
+    comm_destroy(h);
+    API_END(h)
+}
+
 // the compaction + permutation step that follows the all-gather, on a buffer
 // in the all-gather layout (world x nrhs x rows_max) -> y paper order (ld)
 int fde_debug_compact_gather(fde_handle h, fde_operator op, const double* gathered, double* y, int64_t ld, int nrhs)

@@ -42,7 +42,7 @@ EXPORTED = [
     "fde_launch_count", "fde_shard_rows", "fde_debug_hlu_mode", "fde_debug_pool_bytes",
     "fde_operator_wait", "fde_hmatrix_wait", "fde_create_virtual_rank", "fde_operator_rows_internal",
     "fde_shard_matvec", "fde_debug_compact_gather", "hmatrix_build_partition", "fde_debug_truncate",
-    "fde_debug_trunc_profile",
+    "fde_debug_trunc_profile", "fde_debug_comm_selftest",
 ]
 PARTITION_INTERLEAVED, PARTITION_PAPER = 0, 1
 
@@ -116,6 +116,7 @@ def lib():
         L.fde_operator_rows_internal.argtypes = [vp, vp, vp, i64]
         L.fde_shard_matvec.argtypes = [vp, vp, vp, i64, vp, i64, i32]
         L.fde_debug_compact_gather.argtypes = [vp, vp, vp, vp, i64, i32]
+        L.fde_debug_comm_selftest.argtypes = [vp, vp, vp, vp, i64, i32]
         L.fde_debug_truncate.argtypes = [vp, vp, vp, i64, i64, i32, i32, dbl, i32, vp, vp, ctypes.POINTER(i32)]
         L.fde_destroy.argtypes = [vp]
         L.fde_destroy.restype = None
@@ -325,6 +326,15 @@ def compact_gather(handle: Handle, op: Operator, gathered, nrhs: int):
     g = gathered.contiguous()
     y = torch.empty((nrhs, op.n), dtype=torch.float64, device=g.device)
     _check(lib().fde_debug_compact_gather(handle.h, op.ptr, _ptr(g), _ptr(y), op.n, nrhs), handle.h)
+    return y
+
+
+def comm_selftest(handle: Handle, op: Operator, x):
+    """A x through a one-rank NCCL communicator (ncclAllGather + compaction), world-1 handle."""
+    import torch
+    x = x.contiguous()
+    y = torch.empty_like(x)
+    _check(lib().fde_debug_comm_selftest(handle.h, op.ptr, _ptr(x), _ptr(y), op.n, x.shape[0]), handle.h)
     return y
 
 

@@ -149,3 +149,18 @@ def test_compact_gather_synthetic(fde, h):
     assert np.array_equal(y, expect)
     op.free()
     hv.close()
+
+
+@pytest.mark.parametrize("nrhs", [1, 3])
+def test_nccl_one_rank_allgather_path(fde, h, nrhs):
+    """The world > 1 matvec's communication calls on real NCCL (one-rank
+    communicator: dlopen'ed libnccl, ncclGetUniqueId, ncclCommInitRank,
+    ncclAllGather of the padded local rows, k_compact_gather): bitwise the
+    world-1 A x."""
+    p = fi.config4(N=256, P=8)
+    op = fde.assemble_problem(h, p)
+    x = torch.tensor(np.random.default_rng(nrhs).standard_normal((nrhs, p.n)), device="cuda")
+    y1 = fde.stiffness_matvec(h, op, x, path=fde.PATH_DENSE)
+    y = fde.comm_selftest(h, op, x)
+    assert torch.equal(y, y1)
+    op.free()
