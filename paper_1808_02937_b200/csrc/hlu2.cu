@@ -27,7 +27,12 @@
 // Requirements (else hlu_build uses the recursive algorithm): leaves of at most
 // H2_MMAX dofs and dense diagonal leaf tiles.
 
+#include <atomic>
 #include <chrono>
+#include <memory>
+#include <exception>
+#include <mutex>
+#include <thread>
 #include <functional>
 #include <cstdlib>
 #include <set>
@@ -871,6 +876,61 @@ struct TKMap {
         head[t] = (int)kk.size() - 1;
     }
 };
+// Planner worker threads: run(f) calls f(0) here and f(1..n-1) on the workers and
+// returns when all are done (spin-wait handshake: one call per sweep step costs a
+// few microseconds; the workers exist only while a plan is built).
+struct PlanPool {
+    int n = 1;
+    std::vector<std::thread> th;
+    std::atomic<int> gen{0}, left{0};
+    std::atomic<bool> quit{false};
+    const std::function<void(int)>* fn = nullptr;
+    std::exception_ptr err;
+    std::mutex em;
+    explicit PlanPool(int nt) : n(std::max(1, nt))
+    {
+        for (int t = 1; t < n; ++t)
+            th.emplace_back([this, t]() {
+                int seen = 0;
+                for (;;) {
+                    int g;
+                    while ((g = gen.load(std::memory_order_acquire)) == seen) {
+                        if (quit.load(std::memory_order_acquire)) return;
+                        std::this_thread::yield();
+                    }
+                    seen = g;
+                    try {
+                        (*fn)(t);
+                    } catch (...) {
+                        std::lock_guard<std::mutex> l(em);
+                        if (!err) err = std::current_exception();
+                    }
+                    left.fetch_sub(1, std::memory_order_acq_rel);
+                }
+            });
+    }
+    void run(const std::function<void(int)>& f)
+    {
+        fn = &f;
+        left.store(n - 1, std::memory_order_release);
+        gen.fetch_add(1, std::memory_order_acq_rel);
+        std::exception_ptr mine;
+        try {
+            f(0);
+        } catch (...) {
+            mine = std::current_exception();
+        }
+        while (left.load(std::memory_order_acquire) > 0) std::this_thread::yield();
+        if (mine) std::rethrow_exception(mine);
+        if (err) std::rethrow_exception(err);
+    }
+    ~PlanPool()
+    {
+        quit.store(true, std::memory_order_release);
+        for (auto& t : th) t.join();
+    }
+};
+
 int g_hlu2_stop = -1;   // debug: run only the first g_hlu2_stop leaf steps
 
 static bool hlu2_factor(fde_lu* L, fde_hm* hm)
@@ -998,6 +1058,14 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
     std::vector<size_t> dfull;
     std::vector<int> dfirst(defer ? (size_t)nl * nl : 0, -1);            // step of a tile's oldest pending term
     std::vector<std::vector<size_t>> dstarted(defer ? nl : 0);           // tiles whose pending list started at step s
+    // the pending (deferred) dense terms of a step are built by planner threads, the
+    // tiles split by row (each tile's terms keep the serial order; c5: 680k terms)
+    const int plan_threads = getenv("FDE_H2_PLAN_THREADS")
+                                        ? std::max(1, atoi(getenv("FDE_H2_PLAN_THREADS")))
+                                        : (int)std::max(1u, std::min(8u, std::thread::hardware_concurrency() / 2));
+    const int npt = defer ? plan_threads : 1;
+    std::unique_ptr<PlanPool> ppool(new PlanPool(npt));
+    std::vector<std::vector<size_t>> tl_started(npt), tl_full(npt);
     // a tile whose pending terms reach this inner dimension is updated right away
     // (bounds the serial work of one GEMM tile; the tile is still read / written
     // once per KFLUSH of accumulated rank instead of once per step)
@@ -1223,8 +1291,14 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
                 if (!isLR(t) && !defer) {
                     st.dts.push_back({(int)st.dpairs.size() - 1, t});
                 } else if (!isLR(t)) {
-                    for (int i = std::max(std::max(t0[b], t0[t]), k + 1); i <= std::min(t1[b], t1[t]); ++i)
-                        for (int j = std::max(std::max(s0[c], s0[t]), k + 1); j <= std::min(s1[c], s1[t]); ++j) {
+                    const int jlo1 = std::max(std::max(s0[c], s0[t]), k + 1), jhi1 = std::min(s1[c], s1[t]);
+                    for (int i = std::max(std::max(t0[b], t0[t]), k + 1); i <= std::min(t1[b], t1[t]); ++i) {
+                        int jlo = jlo1, jhi = jhi1;
+                        if (npt > 1 && i != k + 1) {   // the pending tiles are the planner threads' share (below)
+                            if (jlo1 != k + 1) continue;
+                            jhi = k + 1;
+                        }
+                        for (int j = jlo; j <= jhi; ++j) {
                             const size_t key = (size_t)i * nl + j;
                             const bool to_pend = defer && i != k + 1 && j != k + 1;
                             int ti = -1;
@@ -1266,6 +1340,7 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
                             }
                             else st.g3[ti].terms.push_back(term);
                         }
+                    }
                 } else {
                     const int key = pr.bl ? b : (nb + c);
                     int gi;
@@ -1278,6 +1353,58 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
                     }
                     lterms.push_back({(int)pi, gi});
                 }
+            }
+        }
+        if (defer && npt > 1) {   // the pending tiles, rows i = tid mod npt per thread
+            std::vector<std::pair<int64_t, int64_t>> psnap(pairs.size());
+            for (size_t pi = 0; pi < pairs.size(); ++pi) {
+                const Pair& pr = pairs[pi];
+                psnap[pi] = {pr.bl ? snapU[pr.b] : 0, (!pr.bl && pr.cl) ? snapV[pr.c] : 0};
+            }
+            const std::function<void(int)> work = [&](int tid) {
+                std::vector<size_t>& started = tl_started[tid];
+                std::vector<size_t>& full = tl_full[tid];
+                started.clear();
+                full.clear();
+                for (size_t pi = 0; pi < pairs.size(); ++pi) {
+                    const Pair& pr = pairs[pi];
+                    const int b = pr.b, c = pr.c;
+                    const int64_t su_b = psnap[pi].first, sv_c = psnap[pi].second;
+                    const HBlock &B = S.bl[b], &C = S.bl[c];
+                    for (int t : ptg[pi]) {
+                        if (isLR(t)) continue;
+                        const int ilo = std::max(std::max(t0[b], t0[t]), k + 2), ihi = std::min(t1[b], t1[t]);
+                        const int jlo = std::max(std::max(s0[c], s0[t]), k + 2), jhi = std::min(s1[c], s1[t]);
+                        for (int i = ilo + (((tid - ilo) % npt) + npt) % npt; i <= ihi; i += npt)
+                            for (int j = jlo; j <= jhi; ++j) {
+                                const size_t key = (size_t)i * nl + j;
+                                VTerm term;
+                                if (!pr.bl && !pr.cl) {
+                                    term = {{0, b, (lr0[k] - col0(b)) * B.m + (lr0[i] - row0(b))},
+                                            {0, c, (lr0[j] - col0(c)) * C.m + (lr0[k] - row0(c))}, B.m, C.m, mk, 0, 0, -1.0};
+                                } else if (pr.bl) {
+                                    term = {{3, sid, su_b + (lr0[i] - row0(b))}, {3, sid, pr.w + (lr0[j] - col0(c))}, B.m,
+                                            C.n, kc[b], 0, 1, -1.0};
+                                } else {
+                                    term = {{3, sid, pr.w + (lr0[i] - row0(b))}, {3, sid, sv_c + (lr0[j] - col0(c))}, B.m,
+                                            C.n, kc[c], 0, 1, -1.0};
+                                }
+                                std::vector<VTerm>& pv = dpend[key];
+                                if (pv.empty()) {
+                                    dfirst[key] = k;
+                                    started.push_back(key);
+                                    pv.reserve(16);
+                                }
+                                pv.push_back(term);
+                                if ((dpend_k[key] += term.k) >= kflush) full.push_back(key);
+                            }
+                    }
+                }
+            };
+            ppool->run(work);
+            for (int q = 0; q < npt; ++q) {
+                dstarted[k].insert(dstarted[k].end(), tl_started[q].begin(), tl_started[q].end());
+                dfull.insert(dfull.end(), tl_full[q].begin(), tl_full[q].end());
             }
         }
         if (defer) {   // flush full tiles, and the pending terms of row / column k+2
@@ -1388,6 +1515,7 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t).count();
     };
     ptick(7);
+    ppool.reset();   // (the planner threads end with the simulation)
     const double ms_sim = ms_since(t_plan0);
     const auto t_alloc0 = std::chrono::steady_clock::now();
     // ---- arena layout

@@ -281,6 +281,28 @@ def test_hlu_deferred_updates_exact_mode(fde, h, case, monkeypatch):
         o.free()
 
 
+@pytest.mark.parametrize("tol", [0.0, 1e-3])
+def test_hlu_planner_threads_bitwise(fde, h, tol, monkeypatch):
+    """The deferred dense-update terms are built by planner threads (tiles split by
+    row, each tile's terms in the serial order): 1 and 4 threads give the same
+    factorisation bit for bit (precond_apply compared with torch.equal)."""
+    monkeypatch.setenv("FDE_H2_DEFER", "1")
+    monkeypatch.setenv("FDE_H2_KFLUSH", "32")
+    p = fi.config4(N=256, P=8)
+    op = fde.assemble_problem(h, p)
+    hm = fde.hmatrix_build(h, op, p.R, 1.0, 16)
+    r = torch.tensor(np.random.default_rng(5).standard_normal((3, p.n)), device="cuda")
+    z = {}
+    for nt in ("1", "4"):
+        monkeypatch.setenv("FDE_H2_PLAN_THREADS", nt)
+        lu = fde.hlu_factor(h, hm, tol)
+        z[nt] = fde.precond_apply(h, lu, r)
+        lu.free()
+    assert torch.equal(z["1"], z["4"])
+    hm.free()
+    op.free()
+
+
 @pytest.mark.parametrize("gemm_path", [False, True], ids=["tiles", "gemm-tasks"])
 @pytest.mark.parametrize("nrhs", [9, 19, 64])
 def test_hlu_apply_many_rhs_equals_dense_solve_of_Atilde(fde, h, nrhs, gemm_path, monkeypatch):
