@@ -163,6 +163,7 @@ struct fde_ctx {
     // concurrently on different streams / devices): the local GEMV shard, the
     // all-gather receive buffer and row starts, the Toeplitz spectra
     DBuf<double> mv_loc, g_recv;
+    DBuf<double> gemm_ws;   // split-K partial products of the multi-RHS DMMA GEMM
     DBuf<int64_t> g_rstart;
     DBuf<double2> t_Dhat, t_What;
     DBuf<double> t_wv;

@@ -291,7 +291,7 @@ void dense_gemv_raw(cudaStream_t s, const double* A, long long lda, long long ro
     }
 }
 
-void dense_gemm_dmma(cudaStream_t s, const double* A, long long lda, long long rows, long long ncol, const double* X,
+void dense_gemm_dmma(fde_ctx* h, const double* A, long long lda, long long rows, long long ncol, const double* X,
                      long long ldx, double* Y, long long ldy, int nrhs);
 
 // y = A x on the shard: GEMV (HBM-bound) for up to 4 RHS per pass, the DMMA
@@ -299,7 +299,7 @@ void dense_gemm_dmma(cudaStream_t s, const double* A, long long lda, long long r
 void dense_gemv(fde_ctx* h, fde_op* op, const double* x, int64_t ldx, double* y, int64_t ldy, int nrhs)
 {
     if (nrhs >= 8 && (op->lda % 2) == 0 && (ldx % 2) == 0)
-        dense_gemm_dmma(h->stream, op->A.p, op->lda, op->r1 - op->r0, op->lda, x, ldx, y, ldy, nrhs);
+        dense_gemm_dmma(h, op->A.p, op->lda, op->r1 - op->r0, op->lda, x, ldx, y, ldy, nrhs);
     else
         dense_gemv_raw(h->stream, op->A.p, op->lda, op->r1 - op->r0, x, ldx, y, ldy, nrhs);
 }
@@ -542,6 +542,10 @@ void prof_collect(fde_ctx* h, double* out, int reset)
 // FP64 tensor cores through mma.sync.m8n8k4.f64 (DMMA; tcgen05 has no f64 kind).
 // CTA tile 64 rows x 64 RHS x 32 (K), 8 warps of 16 x 32, 3-stage cp.async
 // pipeline; A is streamed once from HBM, X (L2-resident) once per row tile.
+// Split-K over gridDim.z: with 2 CTAs per SM, c5's 512 row tiles are 1.73 waves
+// (the last one 73 % full: 13.5 % of the time lost to the tail); S = 4 K-slices
+// make 2048 work units = 6.92 waves.  Each slice writes its partial product to a
+// workspace and k_sum_splits adds the S partials in a fixed order (deterministic).
 #define DG_BM 64
 #define DG_BN 64
 #define DG_BK 32
@@ -581,8 +585,12 @@ __global__ void __launch_bounds__(256) k_gemm_dmma(const double* __restrict__ A,
     for (int i = 0; i < 2; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-    const int nk = (int)((ncol + DG_BK - 1) / DG_BK);
-    auto load_stage = [&](int st, int kt) {
+    const int nkt = (int)((ncol + DG_BK - 1) / DG_BK);
+    const int kbeg = (int)((long long)nkt * blockIdx.z / gridDim.z), kend = (int)((long long)nkt * (blockIdx.z + 1) / gridDim.z);
+    const int nk = kend - kbeg;
+    if (gridDim.z > 1) Y += (long long)blockIdx.z * nrhs * ldy;   // this slice's partial (workspace, ld ldy = rows)
+    auto load_stage = [&](int st, int kt0) {
+        const int kt = kbeg + kt0;
         const long long k0 = (long long)kt * DG_BK;
         double* as = As + st * DG_BM * DG_LD;
         double* xs = Xs + st * DG_BN * DG_LD;
@@ -638,12 +646,56 @@ __global__ void __launch_bounds__(256) k_gemm_dmma(const double* __restrict__ A,
         }
 }
 
-void dense_gemm_dmma(cudaStream_t s, const double* A, long long lda, long long rows, long long ncol, const double* X,
+__global__ void k_sum_splits(const double* W, int S, long long rows, int nrhs, double* Y, long long ldy)
+{
+    const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const int c = blockIdx.y;
+    if (r >= rows) return;
+    double s = 0.0;
+    for (int z = 0; z < S; ++z) s += W[((long long)z * nrhs + c) * rows + r];
+    Y[(long long)c * ldy + r] = s;
+}
+
+void dense_gemm_dmma(fde_ctx* h, const double* A, long long lda, long long rows, long long ncol, const double* X,
                      long long ldx, double* Y, long long ldy, int nrhs)
 {
+    cudaStream_t s = h->stream;
     const size_t smem = (size_t)DG_STAGES * (DG_BM + DG_BN) * DG_LD * sizeof(double);
-    FDE_CUDA(cudaFuncSetAttribute(k_gemm_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    dim3 g((unsigned)ceil_div(rows, DG_BM), (unsigned)ceil_div(nrhs, DG_BN));
-    k_gemm_dmma<<<g, 256, smem, s>>>(A, lda, rows, ncol, X, ldx, nrhs, Y, ldy);
+    static int smem_set_dev[64] = {};
+    static int occ_dev[64] = {};
+    const int dv = h->device & 63;
+    if (!smem_set_dev[dv]) {   // (per device)
+        FDE_CUDA(cudaFuncSetAttribute(k_gemm_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int occ = 0;
+        FDE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gemm_dmma, 256, smem));
+        occ_dev[dv] = std::max(1, occ);
+        smem_set_dev[dv] = 1;
+    }
+    const long long tiles = ceil_div(rows, DG_BM) * ceil_div(nrhs, DG_BN);
+    const long long slots = (long long)occ_dev[dv] * h->num_sms;
+    const int nkt = (int)ceil_div(ncol, DG_BK);
+    // K slices: the fewest (<= 8, >= 16 K-tiles each) whose work units fill the
+    // last wave to >= 95 % (FDE_GEMM_SPLITK: fixed count)
+    int S = 1;
+    if (const char* e = getenv("FDE_GEMM_SPLITK")) {
+        S = std::max(1, std::min(8, atoi(e)));
+    } else {
+        for (int c = 1; c <= 8 && nkt / c >= 16; ++c) {
+            const long long u = tiles * c, waves = ceil_div(u, slots);
+            if ((double)u / (double)(waves * slots) >= 0.95) { S = c; break; }
+        }
+    }
+    if (nkt / S < 1) S = 1;
+    dim3 g((unsigned)ceil_div(rows, DG_BM), (unsigned)ceil_div(nrhs, DG_BN), (unsigned)S);
+    if (S == 1) {
+        k_gemm_dmma<<<g, 256, smem, s>>>(A, lda, rows, ncol, X, ldx, nrhs, Y, ldy);
+        FDE_CHECK_LAUNCH();
+        return;
+    }
+    const size_t need = (size_t)S * nrhs * rows;
+    if (h->gemm_ws.n < need) h->gemm_ws.alloc(need);
+    k_gemm_dmma<<<g, 256, smem, s>>>(A, lda, rows, ncol, X, ldx, nrhs, h->gemm_ws.p, rows);
+    FDE_CHECK_LAUNCH();
+    k_sum_splits<<<dim3((unsigned)ceil_div(rows, 256), (unsigned)nrhs), 256, 0, s>>>(h->gemm_ws.p, S, rows, nrhs, Y, ldy);
     FDE_CHECK_LAUNCH();
 }

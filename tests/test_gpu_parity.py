@@ -355,9 +355,14 @@ def test_hlu_preconditioned_gmres_matches_oracle(fde, h, case, hlu_mode):
         o.free()
 
 
+@pytest.mark.parametrize("splitk", [None, "3"], ids=["auto", "splitK3"])
 @pytest.mark.parametrize("nrhs", [8, 37, 64])
-def test_multi_rhs_dmma_matvec_matches_oracle(fde, h, nrhs):
-    """nrhs >= 8 routes the dense matvec to the FP64 tensor-core GEMM (DMMA)."""
+def test_multi_rhs_dmma_matvec_matches_oracle(fde, h, nrhs, splitk, monkeypatch):
+    """nrhs >= 8 routes the dense matvec to the FP64 tensor-core GEMM (DMMA); with
+    FDE_GEMM_SPLITK=3 the K dimension is cut into three slices whose partial
+    products are summed by k_sum_splits (the c5 launch uses 4)."""
+    if splitk:
+        monkeypatch.setenv("FDE_GEMM_SPLITK", splitk)
     p = fi.config4(N=40, P=6)
     op = fde.assemble_problem(h, p)
     so = oracle_system(p)
