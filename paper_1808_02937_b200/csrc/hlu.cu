@@ -753,6 +753,7 @@ __device__ __forceinline__ bool h2_chk(const void* p, long long nbytes, int tag,
 }
 
 __device__ unsigned long long g_trunc_stats[32];   // [0..3] calls, sum ke, sum sweeps, max; [4..12] k_bcore phase cycles; [16..20] shapes
+__constant__ int g_bcore_wj = 32;   // largest core solved by the one-warp Jacobi (FDE_BCORE_WJ)
 __constant__ int g_trunc_stats_on = 0;   // debug statistics only with FDE_TRUNC_STATS=1 (no atomics on the hot path)
 __device__ double g_trunc_jeps = 0.0;   // (debug FDE_TRUNC_JEPS)
 __device__ int g_trunc_check = 0;   // descriptor checks (FDE_DEBUG_SERIAL)   // calls, sum ke, sum sweeps, max ke
@@ -1154,7 +1155,7 @@ __global__ void __launch_bounds__(BCORE_THREADS) k_bcore(const TEntry* E, const 
     }
     __syncthreads();
     BC_MARK(5);
-    const int sw2 = (n2 <= 32) ? warp_jacobi(X, Eu, n2, jeps, jarel) : cta_jacobi(X, Eu, n2, nullptr, jeps, jarel);
+    const int sw2 = (n2 <= g_bcore_wj) ? warp_jacobi(X, Eu, n2, jeps, jarel) : cta_jacobi(X, Eu, n2, nullptr, jeps, jarel);
     __syncthreads();
     BC_MARK(6);
     if (g_trunc_stats_on && threadIdx.x == 0) {   // (debug statistics: calls, sum ke, sum sweeps, max sweeps)
@@ -1166,11 +1167,12 @@ __global__ void __launch_bounds__(BCORE_THREADS) k_bcore(const TEntry* E, const 
     __shared__ int ord[TRUNC_KMAX];
     __shared__ int r_sh;
     // eigenvalues in decreasing order (ties by index): thread i computes the rank of i
+    // (a NaN -- non-finite input -- sorts last: the ranks stay a permutation)
     for (int i = threadIdx.x; i < n2; i += blockDim.x) {
-        const double li = X[i * n2 + i];
+        const double xi = X[i * n2 + i], li = isnan(xi) ? -INFINITY : xi;
         int rk = 0;
         for (int j = 0; j < n2; ++j) {
-            const double lj = X[j * n2 + j];
+            const double xj = X[j * n2 + j], lj = isnan(xj) ? -INFINITY : xj;
             rk += (lj > li) || (lj == li && j < i);
         }
         ord[rk] = i;
@@ -2034,6 +2036,8 @@ static void trunc_flags_once(fde_ctx* h)
     if (!stats_set[h->device & 63]) {   // (per device: __constant__ memory)
         const int on = getenv("FDE_TRUNC_STATS") ? 1 : 0;
         FDE_CUDA(cudaMemcpyToSymbol(g_trunc_stats_on, &on, sizeof(int)));
+        const int wj = getenv("FDE_BCORE_WJ") ? atoi(getenv("FDE_BCORE_WJ")) : 32;
+        FDE_CUDA(cudaMemcpyToSymbol(g_bcore_wj, &wj, sizeof(int)));
         stats_set[h->device & 63] = true;
     }
 }

@@ -470,7 +470,9 @@ __global__ void __launch_bounds__(256) k_h2_panel(const H2Panel* P)
 // The (term, 16-deep slice) sequence of the tile runs through a 3-stage
 // asynchronous-copy pipeline in shared memory (8-byte cp.async: any operand
 // layout / transpose), so two slices are in flight while one is multiplied.
+#ifndef H2G_ST
 #define H2G_ST 3
+#endif
 #define H2G_TMAX 48
 #define H2G_SMEM(TM, TN) (H2G_ST * GK * ((TM) + (TN) + 2) * (int)sizeof(double))
 struct H2Cursor {   // position in the (term, slice) sequence of a tile
@@ -2011,9 +2013,16 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         nlaunch += 3;
     };
     static const bool lu_old = getenv("FDE_H2_LU_OLD") != nullptr;
+    // debug (critical-path analysis only: results are garbage): FDE_H2_SKIP lists launch
+    // classes to leave out -- l LU, i tile inverses, n neighbour panels, d diagonal-tile
+    // update, p panels, g products, s snapshots, x row/column k+1 update, r other
+    // updates, t operand truncations, o overflow truncations, c new columns
+    const std::string skipset = getenv("FDE_H2_SKIP") ? getenv("FDE_H2_SKIP") : "";
+    auto skip = [&](char c) { return skipset.find(c) != std::string::npos; };
     auto launch_lu = [&](int kk, cudaStream_t st) {   // LU of tile kk, then the inverses of its factors
         const H2Lu* t = P->lu.p + P->steps[kk].lu;
-        if (lu_old) k_h2_lu<<<1, 512, lu_smem, st>>>(t, L->dflag.p);
+        if (skip('l')) {
+        } else if (lu_old) k_h2_lu<<<1, 512, lu_smem, st>>>(t, L->dflag.p);
         else k_h2_lu_reg<<<1, 512, 0, st>>>(t, L->dflag.p);
         FDE_CHECK_LAUNCH();
         if (P->steps[kk].npi) {
@@ -2023,7 +2032,7 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
                 FDE_CUDA(cudaStreamWaitEvent(si, evLUo, 0));
                 sv = si;
             }
-            k_h2_panel<<<P->steps[kk].npi, 256, pan_smem, sv>>>(P->pan.p + P->steps[kk].pi0);
+            if (!skip('i')) k_h2_panel<<<P->steps[kk].npi, 256, pan_smem, sv>>>(P->pan.p + P->steps[kk].pi0);
             FDE_CHECK_LAUNCH();
             ++nlaunch;
             if (np_subst) FDE_CUDA(cudaEventRecord(evInv, si));
@@ -2225,12 +2234,12 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         FDE_CUDA(cudaEventRecord(evCp, sb));
         FDE_CUDA(cudaStreamWaitEvent(se, evCp, 0));
         FDE_CUDA(cudaStreamWaitEvent(se, evSnap, 0));   // snapshots of step k-1 taken
-        run_trunc(ln.tr_ov, se, 1);
+        if (!skip('o')) run_trunc(ln.tr_ov, se, 1);
         FDE_CUDA(cudaEventRecord(evOv, se));
         mark(k, T_OV, se);
         FDE_CUDA(cudaStreamWaitEvent(sb, evSnap, 0));
         if (tline) tmark = [&](int w) { mark(k, w ? T_CORE : T_GRAM, sb); };
-        run_trunc(ln.tr, sb, 0);
+        if (!skip('t')) run_trunc(ln.tr, sb, 0);
         tmark = [](int) {};
         FDE_CUDA(cudaEventRecord(evOp, sb));
         mark(k, T_OP, sb);
@@ -2247,7 +2256,7 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         if (np_subst) FDE_CUDA(cudaStreamWaitEvent(sa, evInv, 0));
         FDE_CUDA(cudaStreamWaitEvent(sa, evOp, 0));
         auto diag_lu = [&](cudaStream_t st) {   // tile (k+1, k+1), then LU(k+1) on sl
-            run_gemm(ln, 5, st);
+            if (!skip('d')) run_gemm(ln, 5, st);
             mark(k, T_DIAG, st);
             if (k + 1 < kstop) {
                 if (st != sl) {
@@ -2265,14 +2274,14 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         // (sa has captured evLU = LU(k) above; LU(k+1) may be recorded from here on)
         if (ln.nnp) {   // neighbour-tile panels, tile (k+1, k+1), LU(k+1): all on the LU stream
             FDE_CUDA(cudaStreamWaitEvent(sl, evCrit, 0));   // row / column k updated by step k-1
-            k_h2_panel<<<ln.nnp, 256, (pan_inv && !np_subst) ? pan_smem_inv : pan_smem, sl>>>(P->pan.p + ln.np0);
+            if (!skip('n')) k_h2_panel<<<ln.nnp, 256, (pan_inv && !np_subst) ? pan_smem_inv : pan_smem, sl>>>(P->pan.p + ln.np0);
             FDE_CHECK_LAUNCH();
             ++nlaunch;
             dbg("neighbour panels");
             FDE_CUDA(cudaEventRecord(evNP, sl));
             diag_lu(sl);
         }
-        run_panel(ln);
+        if (!skip('p')) run_panel(ln);
         mark(k, T_PAN, sa);
         if (ln.nnp) {
             FDE_CUDA(cudaStreamWaitEvent(sa, evNP, 0));   // the products read the neighbour tiles too
@@ -2281,17 +2290,17 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
             FDE_CUDA(cudaStreamWaitEvent(sl, evPan, 0));
             diag_lu(sl);
         }
-        run_gemm(ln, 0, sa);
+        if (!skip('g')) run_gemm(ln, 0, sa);
         mark(k, T_G1, sa);
-        run_gemm(ln, 1, sa);
+        if (!skip('g')) run_gemm(ln, 1, sa);
         mark(k, T_G2, sa);
-        run_gemm(ln, 3, sa);   // conversions to dense (after the products: a block may be
+        if (!skip('g')) run_gemm(ln, 3, sa);   // conversions to dense (after the products: a block may be
                                // an operand (row / column k) and a target (rows > k) at once)
         FDE_CUDA(cudaEventRecord(evP, sa));
         mark(k, T_PROD, sa);
         // snapshots of the operand factors for the dense updates (before the
         // truncations of step k+1 rewrite them: sb / se wait for evSnap)
-        if (ln.nsnap) {
+        if (ln.nsnap && !skip('s')) {
             k_h2_copy<<<ln.nsnap, 256, 0, sa>>>(P->cps.p + ln.snap0);
             FDE_CHECK_LAUNCH();
             ++nlaunch;
@@ -2301,14 +2310,14 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         mark(k, T_SNAP, sa);
         if (ln.diag_scr) diag_lu(sa);
         FDE_CUDA(cudaStreamWaitEvent(sa, evC, 0));   // remaining updates of step k-1
-        run_gemm(ln, 2, sa);                         // row / column k+1
+        if (!skip('x')) run_gemm(ln, 2, sa);         // row / column k+1
         FDE_CUDA(cudaEventRecord(evCrit, sa));
         mark(k, T_CRIT, sa);
         // sb: new low-rank columns of step k (after the overflow truncations)
         FDE_CUDA(cudaStreamWaitEvent(sb, evP, 0));
         FDE_CUDA(cudaStreamWaitEvent(sb, evOv, 0));
         for (size_t r = 0; r < ln.cpr.size(); ++r) {
-            if (ln.cpr[r].second) {
+            if (ln.cpr[r].second && !skip('c')) {
                 k_h2_copy<<<ln.cpr[r].second, 256, 0, sb>>>(P->cps.p + ln.cpr[r].first);
                 FDE_CHECK_LAUNCH();
                 ++nlaunch;
@@ -2318,7 +2327,7 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         mark(k, T_CP, sb);
         // sc: the other dense updates of step k
         FDE_CUDA(cudaStreamWaitEvent(sc, evSnap, 0));
-        if (!skip_rest) run_gemm(ln, 4, sc);   // (debug FDE_H2_SKIPREST: timing experiments only)
+        if (!skip_rest && !skip('r')) run_gemm(ln, 4, sc);   // (debug FDE_H2_SKIPREST: timing experiments only)
         FDE_CUDA(cudaEventRecord(evC, sc));
         mark(k, T_REST, sc);
         if (tline) thost.push_back(std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - th0).count());

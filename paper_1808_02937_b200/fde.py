@@ -107,9 +107,10 @@ def lib():
     """Load libfde.so (raises if it is missing: no CPU fallback exists)."""
     global _lib
     if _lib is None:
-        if not os.path.exists(_SO):
-            raise RuntimeError(f"libfde.so not built ({_SO}); run __graft_entry__.build()")
-        L = ctypes.CDLL(_SO)
+        so = os.environ.get("FDE_LIB_PATH", _SO)   # (dev A/B of compile-time variants)
+        if not os.path.exists(so):
+            raise RuntimeError(f"libfde.so not built ({so}); run __graft_entry__.build()")
+        L = ctypes.CDLL(so)
         vp, i32, i64, dbl = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_double
         L.fde_create.argtypes = [ctypes.POINTER(vp), i32, vp, vp, i32, i32]
         L.fde_create_virtual_rank.argtypes = [ctypes.POINTER(vp), i32, vp, i32, i32]
