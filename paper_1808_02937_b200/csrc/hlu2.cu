@@ -29,6 +29,7 @@
 
 #include <atomic>
 #include <chrono>
+#include <climits>
 #include <memory>
 #include <exception>
 #include <mutex>
@@ -1918,9 +1919,15 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
     FDE_CUDA(cudaEventRecord(evA, sa));   // (sa is ordered after the arena / descriptor allocations on s)
     FDE_CUDA(cudaStreamWaitEvent(sd, evA, 0));
     const bool sync_push = getenv("FDE_H2_SYNCPUSH") != nullptr;   // debug
-    auto push = [&]() {
-        const size_t now[8] = {vlu.size(), vpan.size(), vterm.size(), vtask.size(),
-                               vtile.size(), vcp.size(), vte.size(), vtc.size()};
+    auto sizes_now = [&](size_t* now) {
+        const size_t v[8] = {vlu.size(), vpan.size(), vterm.size(), vtask.size(),
+                             vtile.size(), vcp.size(), vte.size(), vtc.size()};
+        for (int a = 0; a < 8; ++a) now[a] = v[a];
+    };
+    auto push = [&](const size_t* given = nullptr) {
+        size_t now[8];
+        if (given) for (int a = 0; a < 8; ++a) now[a] = given[a];
+        else sizes_now(now);
         for (int a = 0; a < 8; ++a)
             if (now[a] > cap[a]) fde_fail(FDE_EINVAL_PARAM, "hlu_factor: descriptor count exceeds the plan (internal)");
         for (int a = 0; a < 8; ++a) {
@@ -2126,9 +2133,10 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
     auto mark = [&](int k, int w, cudaStream_t st) {
         if (tline) FDE_CUDA(cudaEventRecord(tev[(size_t)k * T_N + w], st));
     };
-    for (int k = 0; k < kstop; ++k) {
-        dbg_step = k;
-        const auto te0 = std::chrono::steady_clock::now();
+    // flatten of step k: the host descriptor lists of step k (writes only P->steps[k],
+    // the descriptor vectors -- capacity reserved, never reallocated -- and the
+    // flatten scratch)
+    auto flatten = [&](int k, std::chrono::steady_clock::time_point te0) {
         // flatten step k (the device is still busy with step k-1) and stage it
         H2Launch& ln = P->steps[k];
         VStep& st = steps[k];
@@ -2218,8 +2226,59 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
             put_gemm_sel(st.g3, &st.g3crit, 0, ln, 4, gemm_shape[4], &xg3, &xg3c);
             put_gemm_sel(st.g3, &st.g3crit, 2, ln, 5, gemm_shape[5], &xg3, &xg3c);
         }
+    };
+    // host pipeline (FDE_H2_PIPE, default on; the debug timeline turns it off): a
+    // worker thread flattens the steps ahead of this thread, which pushes step k's
+    // descriptors as soon as the worker has published their counts.  The vectors
+    // never reallocate (capacity = the plan's exact counts; checked), so [done,
+    // size_k) is final once published and the worker only appends past it.
+    const bool pipe = !(getenv("FDE_H2_PIPE") && atoi(getenv("FDE_H2_PIPE")) == 0) && !tline && kstop > 1;
+    std::vector<size_t> step_sz((size_t)std::max(kstop, 1) * 8);
+    std::atomic<int> flat_done{0};
+    std::exception_ptr flat_err;
+    std::thread flat_worker;
+    auto stg_src = [&](int a) -> const void* {
+        const void* d[8] = {vlu.data(), vpan.data(), vterm.data(), vtask.data(),
+                            vtile.data(), vcp.data(), vte.data(), vtc.data()};
+        return d[a];
+    };
+    struct Joiner {
+        std::thread& t;
+        ~Joiner() { if (t.joinable()) t.join(); }
+    } flat_join{flat_worker};
+    if (pipe) {
+        flat_worker = std::thread([&]() {
+            try {
+                for (int k = 0; k < kstop; ++k) {
+                    flatten(k, std::chrono::steady_clock::now());
+                    size_t* szk = &step_sz[(size_t)k * 8];
+                    sizes_now(szk);
+                    for (int a = 0; a < 8; ++a)
+                        if (szk[a] > cap[a] || (szk[a] && stg_src(a) != stg[a].src))
+                            fde_fail(FDE_EINVAL_PARAM, "hlu_factor: descriptor count exceeds the plan (internal)");
+                    flat_done.store(k + 1, std::memory_order_release);
+                }
+            } catch (...) {
+                flat_err = std::current_exception();
+                flat_done.store(INT_MAX, std::memory_order_release);
+            }
+        });
+    }
+    for (int k = 0; k < kstop; ++k) {
+        dbg_step = k;
+        const auto te0 = std::chrono::steady_clock::now();
+        size_t* szk = &step_sz[(size_t)k * 8];
+        if (pipe) {
+            int got;
+            while ((got = flat_done.load(std::memory_order_acquire)) <= k) std::this_thread::yield();
+            if (got == INT_MAX) break;   // the worker failed: rethrown below
+        } else {
+            flatten(k, te0);
+            sizes_now(szk);
+        }
+        H2Launch& ln = P->steps[k];
         const auto te1 = std::chrono::steady_clock::now();
-        push();
+        push(szk);
         const auto te2 = std::chrono::steady_clock::now();
         mark(k, T_PUSH, sd);
         dbg("push");
@@ -2338,6 +2397,8 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
             eq_us[2] += std::chrono::duration<double, std::micro>(te3 - te2).count();
         }
     }
+    if (flat_worker.joinable()) flat_worker.join();
+    if (flat_err) std::rethrow_exception(flat_err);
     if (tline) {
         FDE_CUDA(cudaDeviceSynchronize());
         const char* nm[T_N] = {"LU(k+1) end", "panel end", "products end", "crit end", "trunc_op end", "trunc_ov end",
