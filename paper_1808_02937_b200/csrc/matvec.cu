@@ -13,6 +13,8 @@
 #include <cstdlib>
 #include <cstring>
 
+#include <cuda.h>
+
 #include "fde_internal.h"
 
 // ------------------------------------------------------------- permutation
@@ -646,6 +648,160 @@ __global__ void __launch_bounds__(256) k_gemm_dmma(const double* __restrict__ A,
         }
 }
 
+// ---- the same contraction with TMA staging (cp.async.bulk.tensor) and mbarriers:
+// one producer warp streams 64 x 16 tiles of A and X (128-byte rows, SWIZZLE_128B,
+// out-of-range rows / columns zero-filled by the TMA unit) into a 6-stage ring; the
+// eight DMMA warps wait on the stage's full barrier and release it on its empty
+// barrier -- no CTA barrier and no per-thread copy instructions in the K loop.
+// Fragment reads undo the swizzle: element (r, c) of a tile sits at double
+// r*16 + (((c>>1) ^ (r&7)) << 1) + (c&1) (16-byte chunk XOR row mod 8: conflict free).
+#define DT_BK 16                  // doubles per swizzled 128-byte tile row
+#define DT_SUB 2                  // sub-tiles per stage (K = 32 per stage)
+#define DT_ST 3
+#define DT_TILE (DG_BM * DT_BK * DT_SUB)   // doubles per operand stage (16 KB)
+#define DT_SMEM (2 * DT_ST * DT_TILE * 8 + 2 * DT_ST * 8 + 1024)
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count)
+{
+    asm volatile("mbarrier.init.shared.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;\n" ::"r"(smem_u32(b)), "r"(bytes));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b)
+{
+    asm volatile("mbarrier.arrive.shared.b64 _, [%0];\n" ::"r"(smem_u32(b)));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity)
+{
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(b)),
+        "r"(parity));
+}
+__device__ __forceinline__ void tma_load_2d(double* dst, const CUtensorMap* tm, int c0, int c1, uint64_t* bar)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+            smem_u32(dst)),
+        "l"(tm), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ int dt_swz(int r, int c) { return r * DT_BK + ((((c >> 1) ^ (r & 7))) << 1) + (c & 1); }
+
+__global__ void __launch_bounds__(288) k_gemm_dmma_tma(const __grid_constant__ CUtensorMap tmA,
+                                                       const __grid_constant__ CUtensorMap tmX, long long rows,
+                                                       long long ncol, int nrhs, double* __restrict__ Y, long long ldy)
+{
+    extern __shared__ unsigned char dt_raw[];
+    double* As = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(dt_raw) + 1023) & ~(uintptr_t)1023);
+    double* Xs = As + DT_ST * DT_TILE;
+    uint64_t* full = reinterpret_cast<uint64_t*>(Xs + DT_ST * DT_TILE);
+    uint64_t* empty = full + DT_ST;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int m0 = blockIdx.x * DG_BM, n0 = blockIdx.y * DG_BN;
+    const int nkt = (int)((ncol + DT_BK * DT_SUB - 1) / (DT_BK * DT_SUB));
+    const int kbeg = (int)((long long)nkt * blockIdx.z / gridDim.z), kend = (int)((long long)nkt * (blockIdx.z + 1) / gridDim.z);
+    const int nk = kend - kbeg;
+    if (gridDim.z > 1) Y += (long long)blockIdx.z * nrhs * ldy;
+    if (tid == 0) {
+        for (int s = 0; s < DT_ST; ++s) {
+            mbar_init(full + s, 1);
+            mbar_init(empty + s, 8);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    if (warp == 8) {   // producer
+        if (lane == 0) {
+            for (int it = 0; it < nk; ++it) {
+                const int s = it % DT_ST;
+                if (it >= DT_ST) mbar_wait(empty + s, ((it / DT_ST) & 1) ^ 1);
+                mbar_expect_tx(full + s, 2 * DT_TILE * 8);
+                const int k0 = (kbeg + it) * DT_BK * DT_SUB;
+#pragma unroll
+                for (int u = 0; u < DT_SUB; ++u) {
+                    tma_load_2d(As + s * DT_TILE + u * DG_BM * DT_BK, &tmA, k0 + u * DT_BK, m0, full + s);
+                    tma_load_2d(Xs + s * DT_TILE + u * DG_BM * DT_BK, &tmX, k0 + u * DT_BK, n0, full + s);
+                }
+            }
+        }
+        return;
+    }
+    const int wm = (warp & 3) * 16, wn = (warp >> 2) * 32;
+    double acc[2][4][2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int it = 0; it < nk; ++it) {
+        const int s = it % DT_ST;
+        mbar_wait(full + s, (it / DT_ST) & 1);
+        const double* as = As + s * DT_TILE;
+        const double* xs = Xs + s * DT_TILE;
+#pragma unroll
+        for (int kk = 0; kk < DT_BK * DT_SUB; kk += 4) {
+            const int c = (kk % DT_BK) + (lane & 3), so = (kk / DT_BK) * DG_BM * DT_BK;
+            double a[2], b[4];
+#pragma unroll
+            for (int i = 0; i < 2; ++i) a[i] = as[so + dt_swz(wm + i * 8 + (lane >> 2), c)];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) b[j] = xs[so + dt_swz(wn + j * 8 + (lane >> 2), c)];
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + s);
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const long long r = m0 + wm + i * 8 + (lane >> 2);
+            const int c = n0 + wn + j * 8 + (lane & 3) * 2;
+            if (r < rows) {
+                if (c < nrhs) Y[(long long)c * ldy + r] = acc[i][j][0];
+                if (c + 1 < nrhs) Y[(long long)(c + 1) * ldy + r] = acc[i][j][1];
+            }
+        }
+}
+
+// row-major [d1][d0] double matrix (stride ld elements) -> 2-D tensor map with
+// 64 x 16 boxes, SWIZZLE_128B; false if the layout does not qualify (stride or base
+// not 16-byte aligned) or the driver entry point is missing
+typedef CUresult (*tmap_encode_fn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static bool make_tmap(CUtensorMap* tm, const double* base, long long d0, long long d1, long long ld)
+{
+    static tmap_encode_fn enc = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            enc = (tmap_encode_fn)fn;
+        (void)cudaGetLastError();
+    }
+    if (!enc || (ld % 2) != 0 || (reinterpret_cast<uintptr_t>(base) % 16) != 0 || d0 < 1 || d1 < 1) return false;
+    const cuuint64_t dims[2] = {(cuuint64_t)d0, (cuuint64_t)d1};
+    const cuuint64_t strides[1] = {(cuuint64_t)ld * sizeof(double)};
+    const cuuint32_t box[2] = {DT_BK, DG_BM};
+    const cuuint32_t es[2] = {1, 1};
+    return enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 __global__ void k_sum_splits(const double* W, int S, long long rows, int nrhs, double* Y, long long ldy)
 {
     const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -687,15 +843,27 @@ void dense_gemm_dmma(fde_ctx* h, const double* A, long long lda, long long rows,
     }
     if (nkt / S < 1) S = 1;
     dim3 g((unsigned)ceil_div(rows, DG_BM), (unsigned)ceil_div(nrhs, DG_BN), (unsigned)S);
-    if (S == 1) {
-        k_gemm_dmma<<<g, 256, smem, s>>>(A, lda, rows, ncol, X, ldx, nrhs, Y, ldy);
-        FDE_CHECK_LAUNCH();
-        return;
+    // TMA + mbarrier pipeline (opt-in FDE_GEMM_TMA=1, when both operands qualify)
+    const bool tma_on = getenv("FDE_GEMM_TMA") && atoi(getenv("FDE_GEMM_TMA")) == 1;
+    CUtensorMap tmA, tmX;
+    const bool tma = tma_on && make_tmap(&tmA, A, ncol, rows, lda) && make_tmap(&tmX, X, ncol, nrhs, ldx);
+    static int tma_smem_set[64] = {};
+    if (tma && !tma_smem_set[dv]) {
+        FDE_CUDA(cudaFuncSetAttribute(k_gemm_dmma_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, DT_SMEM));
+        tma_smem_set[dv] = 1;
     }
-    const size_t need = (size_t)S * nrhs * rows;
-    if (h->gemm_ws.n < need) h->gemm_ws.alloc(need);
-    k_gemm_dmma<<<g, 256, smem, s>>>(A, lda, rows, ncol, X, ldx, nrhs, h->gemm_ws.p, rows);
+    double* out = Y;
+    long long ldo = ldy;
+    if (S > 1) {
+        const size_t need = (size_t)S * nrhs * rows;
+        if (h->gemm_ws.n < need) h->gemm_ws.alloc(need);
+        out = h->gemm_ws.p;
+        ldo = rows;
+    }
+    if (tma) k_gemm_dmma_tma<<<g, 288, DT_SMEM, s>>>(tmA, tmX, rows, ncol, nrhs, out, ldo);
+    else k_gemm_dmma<<<g, 256, smem, s>>>(A, lda, rows, ncol, X, ldx, nrhs, out, ldo);
     FDE_CHECK_LAUNCH();
+    if (S == 1) return;
     k_sum_splits<<<dim3((unsigned)ceil_div(rows, 256), (unsigned)nrhs), 256, 0, s>>>(h->gemm_ws.p, S, rows, nrhs, Y, ldy);
     FDE_CHECK_LAUNCH();
 }

@@ -355,12 +355,15 @@ def test_hlu_preconditioned_gmres_matches_oracle(fde, h, case, hlu_mode):
         o.free()
 
 
+@pytest.mark.parametrize("tma", ["1", "0"], ids=["tma", "cpasync"])
 @pytest.mark.parametrize("splitk", [None, "3"], ids=["auto", "splitK3"])
 @pytest.mark.parametrize("nrhs", [8, 37, 64])
-def test_multi_rhs_dmma_matvec_matches_oracle(fde, h, nrhs, splitk, monkeypatch):
-    """nrhs >= 8 routes the dense matvec to the FP64 tensor-core GEMM (DMMA); with
-    FDE_GEMM_SPLITK=3 the K dimension is cut into three slices whose partial
-    products are summed by k_sum_splits (the c5 launch uses 4)."""
+def test_multi_rhs_dmma_matvec_matches_oracle(fde, h, nrhs, splitk, tma, monkeypatch):
+    """nrhs >= 8 routes the dense matvec to the FP64 tensor-core GEMM (DMMA): the TMA
+    kernel (64 x 16 swizzled tiles, mbarrier ring, zero-filled ragged edges) or the
+    cp.async one (FDE_GEMM_TMA=0); with FDE_GEMM_SPLITK=3 the K dimension is cut
+    into three slices whose partial products k_sum_splits adds (c5 uses 4)."""
+    monkeypatch.setenv("FDE_GEMM_TMA", tma)
     if splitk:
         monkeypatch.setenv("FDE_GEMM_SPLITK", splitk)
     p = fi.config4(N=40, P=6)
