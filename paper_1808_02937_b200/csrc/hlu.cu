@@ -34,7 +34,9 @@ static void set_smem_once(const void* fn, int bytes)
 
 // --------------------------------------------------------------- kernels
 #define GT 64   // GEMM tile
+#ifndef GK
 #define GK 16
+#endif
 
 // C[m x n] = alpha op(A) op(B) + beta C, column-major, op = N | T
 __global__ void __launch_bounds__(256) k_gemm(int m, int n, int k, double alpha, const double* __restrict__ A,
