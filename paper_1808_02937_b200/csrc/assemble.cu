@@ -81,7 +81,12 @@ struct WarpWS {
     double *acc, *Lu, *Lv, *T, *kv, *ua, *wa, *vb, *wb;
 };
 
-__host__ __device__ inline int ws_doubles(int P, int qm) { return P * P + 3 * qm * P + qm * qm + 4 * qm; }
+// kernel values of a cell are produced ASM_KVC columns at a time (qm x ASM_KVC
+// doubles instead of qm x qm: more warps per SM fit; same fma order, same bits)
+#ifndef ASM_KVC
+#define ASM_KVC 8
+#endif
+__host__ __device__ inline int ws_doubles(int P, int qm) { return P * P + 3 * qm * P + qm * ASM_KVC + 4 * qm; }
 
 __device__ inline WarpWS carve_ws(double* base, int P, int qm)
 {
@@ -91,7 +96,7 @@ __device__ inline WarpWS carve_ws(double* base, int P, int qm)
     w.Lv = w.Lu + qm * P;
     w.T = w.Lv + qm * P;
     w.kv = w.T + qm * P;
-    w.ua = w.kv + qm * qm;
+    w.ua = w.kv + qm * ASM_KVC;
     w.wa = w.ua + qm;
     w.vb = w.wa + qm;
     w.wb = w.vb + qm;
@@ -160,21 +165,23 @@ __device__ void warp_cell(const AsmDev& D, const WarpWS& ws, double d, double hi
     const double uc = 0.5 * (u0 + u1), vc = 0.5 * (v0 + v1);
     const double zc = d + uc + vc;
     const double kc = pow(zc, D.oma), izc = 1.0 / zc;
-    const float rQv = 1.0f / (float)Qv;
-    for (int idx = lane; idx < Qu * Qv; idx += 32) {
-        const int a = (int)(((float)idx + 0.5f) * rQv), b = idx - a * Qv;   // (exact: idx < 24^2)
-        double delta = ((ws.ua[a] - uc) + (ws.vb[b] - vc)) * izc;
-        ws.kv[idx] = ws.wa[a] * ws.wb[b] * kc * exp(D.oma * log1p(delta));
+    for (int b0 = 0; b0 < Qv; b0 += ASM_KVC) {
+        const int nb = min(ASM_KVC, Qv - b0);
+        for (int idx = lane; idx < Qu * nb; idx += 32) {
+            const int a = idx / nb, bb = idx - a * nb, b = b0 + bb;
+            double delta = ((ws.ua[a] - uc) + (ws.vb[b] - vc)) * izc;
+            ws.kv[a * ASM_KVC + bb] = ws.wa[a] * ws.wb[b] * kc * exp(D.oma * log1p(delta));
+        }
+        __syncwarp();
+        for (int idx = lane; idx < Qu * P; idx += 32) {
+            int a = idx / P, nn = idx - a * P;
+            const double* kr = ws.kv + a * ASM_KVC;
+            double s = (b0 == 0) ? 0.0 : ws.T[idx];   // (the same fma sequence as one pass over b)
+            for (int bb = 0; bb < nb; ++bb) s = fma(kr[bb], ws.Lv[(b0 + bb) * P + nn], s);
+            ws.T[idx] = s;
+        }
+        __syncwarp();
     }
-    __syncwarp();
-    for (int idx = lane; idx < Qu * P; idx += 32) {
-        int a = idx / P, nn = idx - a * P;
-        const double* kr = ws.kv + a * Qv;
-        double s = 0.0;
-        for (int b = 0; b < Qv; ++b) s = fma(kr[b], ws.Lv[b * P + nn], s);
-        ws.T[idx] = s;
-    }
-    __syncwarp();
     for (int idx = lane; idx < P * P; idx += 32) {
         int m = idx / P, nn = idx - m * P;
         double s = 0.0;
@@ -285,7 +292,9 @@ __device__ void warp_pair(const AsmDev& D, const WarpWS& ws, int i, int j, doubl
     __syncwarp();
 }
 
+#ifndef ASM_WARPS
 #define ASM_WARPS 4
+#endif
 
 // mode 0: triangle rows [i0,i1): pair p -> (i, j<=i), slot p - T(i0)
 // mode 1: rectangle i in [i0,i1) x j in [j0,j1)
