@@ -50,7 +50,7 @@ enum {
     FDE_EUNSUPPORTED_MESH = -6,  /* Toeplitz path requested on a non-uniform mesh    */
     FDE_EDIM = -7,               /* objects of different problems mixed              */
     FDE_ESINGULAR_PIVOT = -8,    /* zero/NaN pivot in an H-LU leaf                   */
-    FDE_EBREAKDOWN = -9,         /* Krylov breakdown                                 */
+    FDE_EBREAKDOWN = -9,         /* Krylov breakdown, or non-finite right-hand side  */
     FDE_EMAXITER = -10,          /* Krylov did not converge within maxiter           */
     FDE_ECUDA = -11,
     FDE_ENCCL = -12,

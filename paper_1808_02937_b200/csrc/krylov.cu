@@ -234,8 +234,11 @@ void krylov_gmres(fde_ctx* h, fde_op* op, fde_lu* lu, const double* G, double* X
     FDE_CHECK_LAUNCH();
     FDE_CUDA(cudaMemcpyAsync(bnorm.data(), W.nrm.p, sizeof(double) * nrhs, cudaMemcpyDeviceToHost, s));
     FDE_CUDA(cudaStreamSynchronize(s));
-    for (int c = 0; c < nrhs; ++c)
+    for (int c = 0; c < nrhs; ++c) {
+        if (!std::isfinite(bnorm[c]))   // (a NaN would otherwise read as a zero right-hand side)
+            fde_fail(FDE_EBREAKDOWN, "GMRES: non-finite (preconditioned) right-hand side");
         if (!(bnorm[c] > 0.0)) act[c] = 0;   // zero RHS: X = 0
+    }
     int it_total = 0, matvecs = 0;
     bool first = true;
     double worst = 0.0;
@@ -485,6 +488,7 @@ void krylov_bicgstab(fde_ctx* h, fde_op* op, fde_lu* lu, const double* G, double
     std::vector<int> act(nrhs);
     std::vector<double> sc_h((size_t)nrhs * BS);
     for (int c = 0; c < nrhs; ++c) {
+        if (!std::isfinite(bn[c])) fde_fail(FDE_EBREAKDOWN, "BiCGSTAB: non-finite (preconditioned) right-hand side");
         act[c] = bn[c] > 0.0;
         relres[c] = bn[c] > 0.0 ? 1.0 : 0.0;
         double* q = &sc_h[(size_t)c * BS];

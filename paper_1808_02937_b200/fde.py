@@ -165,6 +165,16 @@ def _check(rc: int, h=None):
 
 
 def _ptr(t) -> int:
+    """Device pointer of a tensor argument: the C-ABI takes float64 CUDA buffers with
+    the stated strides, so anything else is rejected here (a float32 or host
+    tensor would otherwise be read as garbage)."""
+    import torch
+    if t.dtype != torch.float64:
+        raise TypeError(f"fde: expected a float64 tensor, got {t.dtype}")
+    if not t.is_cuda:
+        raise ValueError("fde: expected a CUDA tensor (device buffers cross the C-ABI)")
+    if not t.is_contiguous():
+        raise ValueError("fde: expected a contiguous tensor")
     return t.data_ptr()
 
 

@@ -456,3 +456,58 @@ def test_condition_numbers_example51(fde, h):
     assert (s[0] / s[-1]).item() > 1e9
     assert (sp[0] / sp[-1]).item() < 10.0
     lu.free(); hm.free(); op.free()
+
+
+@pytest.mark.parametrize("NP", [(1, 2), (2, 1), (1, 4), (3, 1), (2, 2), (1, 9)], ids=lambda t: f"N{t[0]}P{t[1]}")
+def test_tiny_problems_full_path(fde, h, NP):
+    """The degenerate sizes of the method: one or two elements, P = 1 (n = N P - 1 =
+    1 .. 8 unknowns), through every call of the path (assembly, load, H-matrix with
+    a single leaf, H-LU, preconditioned GMRES) against the oracle's system and
+    Galerkin solution."""
+    N, P = NP
+    p = fi.Problem(f"tiny-N{N}-P{P}", 0.0, 1.0, 1.55, 0.4, 0.5, 0.25, -0.5, fi.uniform_mesh(0, 1, N), P, 3,
+                   n_min=1, forcings=[fi.random_legendre_forcing(11)])
+    op = fde.assemble_problem(h, p)
+    so = oracle_system(p)
+    Ag = fde.operator_dense_paper(h, op).cpu().numpy()
+    assert Ag.shape == (p.n, p.n)
+    assert metric_A(Ag, so.A) <= TOL
+    G = fde.sem_rhs(h, op, p.forcings)
+    Go = O.rhs(p, so, p.forcings[0])
+    assert np.max(np.abs(G.cpu().numpy()[0] - Go)) <= TOL * np.max(np.abs(Go))
+    hm = fde.hmatrix_build(h, op, p.R, 1.0, p.n_min)
+    lu = fde.hlu_factor(h, hm, 1e-3)
+    X, rep = fde.solve(h, op, lu, G, tol=1e-12)
+    Xo = np.linalg.solve(so.A, Go)
+    assert np.linalg.norm(X.cpu().numpy()[0] - Xo) <= 1e-10 * np.linalg.norm(Xo)
+    for o in (lu, hm, op):
+        o.free()
+
+
+def test_non_finite_inputs_fail_loudly(fde, h):
+    """Non-finite data never hangs or passes silently: a NaN in the load vector makes
+    GMRES and BiCGSTAB stop with FDE_EBREAKDOWN (before round 2's fix a NaN norm
+    read as a zero right-hand side: X = 0 returned as converged), precond_apply
+    propagates NaN, the binding rejects float32 and host tensors (they would be
+    read as garbage through the C-ABI), and the handle stays usable."""
+    p = fi.config4(N=32, P=4)
+    op = fde.assemble_problem(h, p)
+    hm = fde.hmatrix_build(h, op, p.R, 1.0, 4)
+    lu = fde.hlu_factor(h, hm, 1e-3)
+    G = fde.sem_rhs(h, op, p.forcings)
+    Gn = G.clone()
+    Gn[0, 5] = float("nan")
+    for method in (fde.GMRES, fde.BICGSTAB):
+        with pytest.raises(fde.FdeError) as e:
+            fde.solve(h, op, lu, Gn, tol=1e-12, method=method)
+        assert e.value.name == "FDE_EBREAKDOWN"
+    z = fde.precond_apply(h, lu, torch.full((1, p.n), float("nan"), device="cuda", dtype=torch.float64))
+    assert torch.isnan(z).all()                                                        # NaN in, NaN out
+    with pytest.raises(TypeError):                                                     # float32 is rejected
+        fde.precond_apply(h, lu, torch.zeros((1, p.n), device="cuda"))
+    with pytest.raises(ValueError):                                                    # so is host memory
+        fde.precond_apply(h, lu, torch.zeros((1, p.n), dtype=torch.float64))
+    X, rep = fde.solve(h, op, lu, G, tol=1e-12)                                        # still usable
+    assert torch.isfinite(X).all() and rep.iterations >= 1
+    for o in (lu, hm, op):
+        o.free()
