@@ -86,10 +86,18 @@ struct WarpWS {
 #ifndef ASM_KVC
 #define ASM_KVC 8
 #endif
-__host__ __device__ inline int ws_doubles(int P, int qm) { return P * P + 3 * qm * P + qm * ASM_KVC + 4 * qm; }
+// rows of the per-point arrays: the Gauss-Legendre cap qm, and the P + 1 radial
+// Gauss-Jacobi points of the Duffy corner (more than qm when P = FDE_MAX_P)
+__host__ __device__ inline int ws_rows(int P, int qm) { return qm > P + 1 ? qm : P + 1; }
+__host__ __device__ inline int ws_doubles(int P, int qm)
+{
+    const int q = ws_rows(P, qm);
+    return P * P + 3 * q * P + q * ASM_KVC + 4 * q;
+}
 
 __device__ inline WarpWS carve_ws(double* base, int P, int qm)
 {
+    qm = ws_rows(P, qm);
     WarpWS w;
     w.acc = base;
     w.Lu = w.acc + P * P;

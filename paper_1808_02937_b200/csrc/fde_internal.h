@@ -276,7 +276,7 @@ void gauss_jacobi(int n, double a, double b, std::vector<double>& x, std::vector
 }  // namespace fdeq
 
 // Maximum points of one tensor-rule direction on the device.
-#define FDE_QMAX 32
+#define FDE_QMAX 34   // (P + 2 points for the mass matrix at P = FDE_MAX_P = 32)
 // Packed Gauss-Legendre rules for Q = 1..FDE_QMAX: offset(Q) = Q(Q-1)/2.
 #define FDE_GL_TOTAL (FDE_QMAX * (FDE_QMAX + 1) / 2)
 

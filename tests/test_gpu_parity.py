@@ -511,3 +511,37 @@ def test_non_finite_inputs_fail_loudly(fde, h):
     assert torch.isfinite(X).all() and rep.iterations >= 1
     for o in (lu, hm, op):
         o.free()
+
+
+def _edge_problems():
+    out = []
+    rng = np.random.default_rng(21)
+    for alpha in (1.02, 1.98):        # near both ends of (1, 2): the kernel |x-s|^{1-alpha} almost flat / almost 1/|x-s|
+        out.append(fi.Problem(f"alpha{alpha}", 0.0, 1.0, alpha, 0.35, 0.5, 0.2, -0.1, fi.graded_mesh(0.0, 1.0, 20, 2.0),
+                              5, 6, n_min=2, forcings=[fi.random_legendre_forcing(5)]))
+    for theta in (0.0, 1.0):          # one-sided operators (right- / left-sided only)
+        out.append(fi.Problem(f"theta{theta}", -1.0, 2.0, 1.45, theta, 0.0, 0.0, 0.0, fi.uniform_mesh(-1.0, 2.0, 16),
+                              6, 6, n_min=2, forcings=[fi.random_legendre_forcing(6)]))
+    out.append(fi.Problem("Pmax", 0.0, 1.0, 1.6, 0.5, 1.0, 0.0, 0.0, fi.uniform_mesh(0.0, 1.0, 3), 32, 4, n_min=1,
+                          forcings=[fi.random_legendre_forcing(7)]))                 # P = FDE_MAX_P
+    nodes = np.concatenate([[0.0], np.sort(rng.uniform(0.0, 1.0, 9)) ** 4, [1.0]])   # clustered random mesh
+    out.append(fi.Problem("clustered", 0.0, 1.0, 1.7, 0.8, 3.0, 1.0, 2.0, nodes, 7, 6, n_min=2,
+                          forcings=[fi.random_legendre_forcing(8)]))
+    return out
+
+
+@pytest.mark.parametrize("p", _edge_problems(), ids=lambda p: p.name)
+def test_edge_parameters_full_path(fde, h, p):
+    """alpha near 1 and 2, theta = 0 and 1, P = FDE_MAX_P = 32, a clustered random
+    mesh with rho = 3 and nonzero boundary values: assembly (M-A), load, and the
+    preconditioned solve (M-D) against the oracle."""
+    op = fde.assemble_problem(h, p)
+    so = oracle_system(p)
+    assert metric_A(fde.operator_dense_paper(h, op).cpu().numpy(), so.A) <= TOL
+    G = fde.sem_rhs(h, op, p.forcings)
+    hm = fde.hmatrix_build(h, op, p.R, 1.0, p.n_min)
+    lu = fde.hlu_factor(h, hm, 1e-3)
+    X, rep = fde.solve(h, op, lu, G, tol=1e-13, maxiter=300)
+    md_check(p, X.cpu().numpy()[0], so, O.rhs(p, so, p.forcings[0]))
+    for o in (lu, hm, op):
+        o.free()
