@@ -545,3 +545,82 @@ def test_edge_parameters_full_path(fde, h, p):
     md_check(p, X.cpu().numpy()[0], so, O.rhs(p, so, p.forcings[0]))
     for o in (lu, hm, op):
         o.free()
+
+
+@pytest.mark.parametrize("tol", [0.0, 1e-3])
+def test_rank_limit_R32(fde, h, tol):
+    """R = 32 (the largest Taylor rank): A~ against the oracle's A~ (M-A), and the
+    H-LU (exact at tol = 0, truncated to capacity 32 at 1e-3) preconditioning a
+    GMRES solve that reaches the oracle's Galerkin solution."""
+    p = fi.config4(N=48, P=4)
+    op = fde.assemble_problem(h, p)
+    hm = fde.hmatrix_build(h, op, 32, 1.0, 2)
+    so = oracle_system(p)
+    At, _ = O.hmatrix_dense(p, so, R=32, lam=1.0, n_min=2)
+    assert metric_A(fde.hmatrix_dense_paper(h, hm).cpu().numpy(), At) <= TOL
+    lu = fde.hlu_factor(h, hm, tol)
+    G = fde.sem_rhs(h, op, p.forcings)
+    X, rep = fde.solve(h, op, lu, G, tol=1e-13)
+    md_check(p, X.cpu().numpy()[0], so, O.rhs(p, so, p.forcings[0]))
+    for o in (lu, hm, op):
+        o.free()
+
+
+def test_toeplitz_edge_sizes(fde, h):
+    """The FFT path at its edges: one element (n = P - 1), P = 32, and P = 1 (hats
+    only), against the dense operator of the same mesh."""
+    for N, P in [(1, 4), (2, 1), (4, 32), (3, 7)]:
+        p = fi.Problem(f"u{N}-{P}", 0.0, 2.0, 1.35, 0.3, 1.0, 0.0, 0.0, fi.uniform_mesh(0.0, 2.0, N), P, 3, n_min=1,
+                       forcings=[fi.random_legendre_forcing(2)])
+        if p.n < 1:
+            continue
+        opd = fde.assemble_problem(h, p)
+        opt = fde.assemble_problem(h, p, flags=fde.OP_TOEPLITZ)
+        x = torch.tensor(np.random.default_rng(N * 100 + P).standard_normal((2, p.n)), device="cuda")
+        yd = fde.stiffness_matvec(h, opd, x, path=fde.PATH_DENSE).cpu().numpy()
+        yt = fde.stiffness_matvec(h, opt, x, path=fde.PATH_TOEPLITZ).cpu().numpy()
+        so = oracle_system(p)
+        den = (np.abs(so.A) @ np.abs(x.cpu().numpy().T)).T
+        assert np.max(np.abs(yt - yd) / den) <= TOL, (N, P)
+        opd.free()
+        opt.free()
+
+
+def test_hundred_rhs_solve(fde, h):
+    """100 right-hand sides (two 64-wide DMMA column tiles, the many-RHS apply) give
+    the one-by-one solutions."""
+    p = fi.config4(N=64, P=4)
+    p.forcings = [fi.random_legendre_forcing(s) for s in range(100)]
+    op = fde.assemble_problem(h, p)
+    hm = fde.hmatrix_build(h, op, p.R, 1.0, 4)
+    lu = fde.hlu_factor(h, hm, 1e-3)
+    G = fde.sem_rhs(h, op, p.forcings)
+    X, rep = fde.solve(h, op, lu, G, tol=1e-13)
+    for c in (0, 63, 64, 99):
+        x1, _ = fde.solve(h, op, lu, G[c:c + 1].contiguous(), tol=1e-13)
+        assert np.linalg.norm(X[c].cpu().numpy() - x1[0].cpu().numpy()) <= 1e-10 * np.linalg.norm(x1[0].cpu().numpy())
+    for o in (lu, hm, op):
+        o.free()
+
+
+def test_many_handles_lifecycle(fde):
+    """Handles and objects created and released many times (streams, pools,
+    communicator-free contexts): no failure, no leak visible in the pool."""
+    import ctypes
+    p = fi.config1()
+    for _ in range(40):
+        hh = fde.Handle(0)
+        op = fde.assemble_problem(hh, p)
+        hm = fde.hmatrix_build(hh, op, p.R, p.lam, p.n_min)
+        lu = fde.hlu_factor(hh, hm, 1e-3)
+        G = fde.sem_rhs(hh, op, p.forcings)
+        fde.solve(hh, op, lu, G, tol=1e-12)
+        for o in (lu, hm, op):
+            o.free()
+        hh.close()
+    torch.cuda.synchronize()
+    r, u = ctypes.c_ulonglong(0), ctypes.c_ulonglong(0)
+    fde.lib().fde_debug_pool_bytes.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_ulonglong),
+                                               ctypes.POINTER(ctypes.c_ulonglong)]
+    fde.lib().fde_debug_pool_bytes(0, ctypes.byref(r), ctypes.byref(u))
+    assert u.value < (256 << 20), u.value
