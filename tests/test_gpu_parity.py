@@ -624,3 +624,25 @@ def test_many_handles_lifecycle(fde):
                                                ctypes.POINTER(ctypes.c_ulonglong)]
     fde.lib().fde_debug_pool_bytes(0, ctypes.byref(r), ctypes.byref(u))
     assert u.value < (256 << 20), u.value
+
+
+@pytest.mark.parametrize("lam,n_min", [(0.3, 2), (3.0, 2), (1.0, 64)], ids=["lam0.3", "lam3", "one-leaf"])
+def test_admissibility_and_leaf_extremes(fde, h, lam, n_min):
+    """The admissibility parameter lambda (Def. 3.1) far below and
+    above 1 (few / many admissible blocks) and a leaf size covering the whole mesh
+    (A~ = A: the H-LU is the dense LU): A~ against the oracle's A~, block counts,
+    exact-mode H-LU against the dense solve with A~."""
+    p = fi.config4(N=40, P=5)
+    op = fde.assemble_problem(h, p)
+    hm = fde.hmatrix_build(h, op, 6, lam, n_min)
+    so = oracle_system(p)
+    At, part = O.hmatrix_dense(p, so, R=6, lam=lam, n_min=n_min)
+    assert hm.info.nblocks_lr == sum(1 for _, _, k in part if k == "lr")
+    assert metric_A(fde.hmatrix_dense_paper(h, hm).cpu().numpy(), At) <= TOL
+    lu = fde.hlu_factor(h, hm, 0.0)
+    r = np.random.default_rng(1).standard_normal((2, p.n))
+    z = fde.precond_apply(h, lu, torch.tensor(r, device="cuda")).cpu().numpy()
+    zo = np.linalg.solve(At, r.T).T
+    assert np.linalg.norm(z - zo) <= TOL * np.linalg.norm(zo)
+    for o in (lu, hm, op):
+        o.free()
