@@ -300,6 +300,7 @@ void dense_gemm_dmma(fde_ctx* h, const double* A, long long lda, long long rows,
 // GEMM (FP64 tensor cores, one pass over A) from 8 RHS on
 void dense_gemv(fde_ctx* h, fde_op* op, const double* x, int64_t ldx, double* y, int64_t ldy, int nrhs)
 {
+    if (op->r1 <= op->r0) return;   // an empty shard (more ranks than elements): no local rows
     if (nrhs >= 8 && (op->lda % 2) == 0 && (ldx % 2) == 0)
         dense_gemm_dmma(h, op->A.p, op->lda, op->r1 - op->r0, op->lda, x, ldx, y, ldy, nrhs);
     else

@@ -164,3 +164,35 @@ def test_nccl_one_rank_allgather_path(fde, h, nrhs):
     y = fde.comm_selftest(h, op, x)
     assert torch.equal(y, y1)
     op.free()
+
+
+@pytest.mark.parametrize("NPG", [(8, 3, 8), (5, 2, 8), (3, 4, 4)], ids=lambda t: f"N{t[0]}P{t[1]}G{t[2]}")
+def test_more_ranks_than_elements(fde, h, NPG):
+    """One element per rank, and more ranks than elements (empty shards: a rank
+    with no rows must skip its GEMV instead of launching an empty grid -- found
+    and fixed in round 2): the gathered matvec is still bitwise the world-1 A x,
+    and every rank builds the H-matrix (recompute path)."""
+    N, P, G = NPG
+    p = fi.Problem(f"s{N}", 0.0, 1.0, 1.5, 0.5, 1.0, 0.0, 0.0, fi.uniform_mesh(0, 1, N), P, 3, n_min=1,
+                   forcings=[fi.random_legendre_forcing(1)])
+    op1 = fde.assemble_problem(h, p)
+    x = torch.tensor(np.random.default_rng(0).standard_normal((2, p.n)), device="cuda")
+    y1 = fde.stiffness_matvec(h, op1, x, path=fde.PATH_DENSE)
+    rm = fde.shard_rows(N, P, G, 0)[2]
+    locs, keep = [], None
+    for g in range(G):
+        hg = fde.Handle(0, virtual=True, rank=g, world=G)
+        opg = fde.assemble_problem(hg, p)
+        locs.append(fde.shard_matvec(hg, opg, x, rm))
+        hm = fde.hmatrix_build(hg, opg, 3, 1.0, 1)
+        hm.free()
+        if g == 0:
+            keep = (hg, opg)
+        else:
+            opg.free()
+            hg.close()
+    y = fde.compact_gather(keep[0], keep[1], torch.stack(locs), 2)
+    assert torch.equal(y, y1)
+    keep[1].free()
+    keep[0].close()
+    op1.free()
