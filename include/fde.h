@@ -41,7 +41,7 @@ extern "C" {
 /* ------------------------------------------------------------ error codes */
 enum {
     FDE_OK = 0,
-    FDE_EINVAL_DOMAIN = -1,      /* a >= b                                          */
+    FDE_EINVAL_DOMAIN = -1,      /* a >= b, or a / b not finite                      */
     FDE_EINVAL_SIZE = -2,        /* N < 1, nrhs < 1, ld < n                          */
     FDE_EINVAL_PARAM = -3,       /* alpha not in (1,2), theta not in [0,1], rho < 0,
                                     R < 1, lambda <= 0, n_min < 1, tol < 0           */

@@ -283,7 +283,10 @@ int fde_shard_rows(int N, int P, int world, int rank, int64_t* r0, int64_t* r1, 
 static void validate(const fde_problem* p, const fde_mesh* m)
 {
     if (!p || !m || !m->nodes) fde_fail(FDE_EINVAL_PARAM, "NULL problem/mesh");
-    if (!(p->a < p->b)) fde_fail(FDE_EINVAL_DOMAIN, "invalid domain: a >= b");
+    if (!(p->a < p->b) || !std::isfinite(p->a) || !std::isfinite(p->b))
+        fde_fail(FDE_EINVAL_DOMAIN, "invalid domain: need finite a < b");
+    if (!std::isfinite(p->rho) || !std::isfinite(p->c1) || !std::isfinite(p->c2))
+        fde_fail(FDE_EINVAL_PARAM, "rho, c1, c2 must be finite");
     if (m->N < 1) fde_fail(FDE_EINVAL_SIZE, "invalid size: N < 1");
     if (!(p->alpha > 1.0 && p->alpha < 2.0)) fde_fail(FDE_EINVAL_PARAM, "alpha must lie in (1,2)");
     if (!(p->theta >= 0.0 && p->theta <= 1.0)) fde_fail(FDE_EINVAL_PARAM, "theta must lie in [0,1]");

@@ -209,6 +209,20 @@ def test_invalid_inputs_raise(fde, h):
     with pytest.raises(fde.FdeError) as e:
         fde.sem_assemble(h, 0.0, 1.0, 1.5, 0.5, 1.0, 0, 0, p.nodes, 0)
     assert e.value.name == "FDE_EDEGREE"
+    nan, inf = float("nan"), float("inf")
+    for args, code in [((0.0, 1.0, nan, 0.5, 1.0, 0, 0), "FDE_EINVAL_PARAM"),      # non-finite parameters
+                       ((0.0, 1.0, 1.5, nan, 1.0, 0, 0), "FDE_EINVAL_PARAM"),
+                       ((0.0, 1.0, 1.5, 0.5, nan, 0, 0), "FDE_EINVAL_PARAM"),
+                       ((0.0, 1.0, 1.5, 0.5, inf, 0, 0), "FDE_EINVAL_PARAM"),
+                       ((0.0, 1.0, 1.5, 0.5, 1.0, nan, 0), "FDE_EINVAL_PARAM"),
+                       ((0.0, 1.0, 1.5, 0.5, 1.0, 0, inf), "FDE_EINVAL_PARAM")]:
+        with pytest.raises(fde.FdeError) as e:
+            fde.sem_assemble(h, *args, p.nodes, 4)
+        assert e.value.name == code, args
+    for nodes, a, b in [(np.concatenate([[-inf], p.nodes[1:]]), -inf, 1.0), (np.where(np.arange(p.nodes.size) == 3, nan, p.nodes), 0.0, 1.0)]:
+        with pytest.raises(fde.FdeError) as e:
+            fde.sem_assemble(h, a, b, 1.5, 0.5, 1.0, 0, 0, nodes, 4)
+        assert e.value.name in ("FDE_EINVAL_DOMAIN", "FDE_EINVAL_MESH")
 
 
 # ------------------------------------------------------------------ H-LU
