@@ -475,6 +475,15 @@ __global__ void __launch_bounds__(256) k_h2_panel(const H2Panel* P)
 #define H2G_ST 3
 #endif
 #define H2G_TMAX 48
+#ifndef H2G_EPI
+#define H2G_EPI 2     // C elements loaded before they are stored in the GEMM epilogue
+#endif
+#ifndef H2C_B
+#define H2C_B 8       // elements per thread loaded before they are stored in k_h2_copy
+#endif
+#ifndef H2G_MINB
+#define H2G_MINB 4    // __launch_bounds__ minimum CTAs per SM of k_h2_gemm
+#endif
 #define H2G_SMEM(TM, TN) (H2G_ST * GK * ((TM) + (TN) + 2) * (int)sizeof(double))
 struct H2Cursor {   // position in the (term, slice) sequence of a tile
     int q, k0;
@@ -643,37 +652,56 @@ __device__ __forceinline__ void h2_gemm_tile(const H2Tile* tiles, int tile, cons
         }
     }
     cp_async_wait_group<0>();
+    // epilogue C = acc + beta C: the C values of a fragment row are all loaded before
+    // any of them is stored (a load after a store to a possibly aliasing address
+    // cannot be hoisted by the compiler: one global round trip per element otherwise)
+    const bool rdc = tk.beta != 0.0;
     if (DM) {
+        // batches of H2G_EPI (j, h) elements of one fragment row
+        constexpr int NE = 2 * FN, EB = (H2G_EPI < NE) ? H2G_EPI : NE;
         if (wact)
 #pragma unroll
-            for (int i = 0; i < FM; ++i)
+            for (int i = 0; i < FM; ++i) {
+                const int gi = m0 + wm + i * 8 + (lane >> 2);
 #pragma unroll
-                for (int j = 0; j < FN; ++j)
+                for (int e0 = 0; e0 < NE; e0 += EB) {
+                    double cv[EB];
 #pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        const int gi = m0 + wm + i * 8 + (lane >> 2), gj = n0 + wn + j * 8 + 2 * (lane & 3) + h;
-                        if (gi < m && gj < n) {
-                            double* c = tk.C + (long long)gj * tk.ldc + gi;
-                            *c = dacc[i][j][h] + (tk.beta == 0.0 ? 0.0 : tk.beta * *c);
-                        }
+                    for (int e = 0; e < EB; ++e) {
+                        const int j = (e0 + e) >> 1, h = (e0 + e) & 1;
+                        const int gj = n0 + wn + j * 8 + 2 * (lane & 3) + h;
+                        cv[e] = (rdc && gi < m && gj < n) ? tk.C[(long long)gj * tk.ldc + gi] : 0.0;
                     }
+#pragma unroll
+                    for (int e = 0; e < EB; ++e) {
+                        const int j = (e0 + e) >> 1, h = (e0 + e) & 1;
+                        const int gj = n0 + wn + j * 8 + 2 * (lane & 3) + h;
+                        if (gi < m && gj < n) tk.C[(long long)gj * tk.ldc + gi] = dacc[i][j][h] + (rdc ? tk.beta * cv[e] : 0.0);
+                    }
+                }
+            }
         return;
     }
 #pragma unroll
-    for (int i = 0; i < RM; ++i)
+    for (int i = 0; i < RM; ++i) {
+        double cv[RN];
+        const int gi = m0 + tx + 16 * i;
 #pragma unroll
         for (int j = 0; j < RN; ++j) {
-            const int gi = m0 + tx + 16 * i, gj = n0 + ty + 16 * j;
-            if (gi < m && gj < n) {
-                double* c = tk.C + (long long)gj * tk.ldc + gi;
-                *c = acc[i][j] + (tk.beta == 0.0 ? 0.0 : tk.beta * *c);
-            }
+            const int gj = n0 + ty + 16 * j;
+            cv[j] = (rdc && gi < m && gj < n) ? tk.C[(long long)gj * tk.ldc + gi] : 0.0;
         }
+#pragma unroll
+        for (int j = 0; j < RN; ++j) {
+            const int gj = n0 + ty + 16 * j;
+            if (gi < m && gj < n) tk.C[(long long)gj * tk.ldc + gi] = acc[i][j] + (rdc ? tk.beta * cv[j] : 0.0);
+        }
+    }
 }
 
 // grid-stride over the tiles: a capped grid leaves SMs to the critical stream
 template <int TM, int TN, bool DM>
-__global__ void __launch_bounds__(256) k_h2_gemm(const H2Tile* tiles, const H2Task* tasks, const H2Term* terms, int ntile)
+__global__ void __launch_bounds__(256, H2G_MINB) k_h2_gemm(const H2Tile* tiles, const H2Task* tasks, const H2Term* terms, int ntile)
 {
     for (int t = blockIdx.x; t < ntile; t += gridDim.x) {
         h2_gemm_tile<TM, TN, DM>(tiles, t, tasks, terms);
@@ -690,13 +718,28 @@ __global__ void __launch_bounds__(256) k_h2_copy(const H2Copy* C)
         if (c.kind == 0) ok = ok && h2_chk(c.src, ((long long)(c.n - 1) * c.lds + c.m) * 8, 11, c.m, c.n);
         if (!ok) return;
     }
-    for (long long t = threadIdx.x; t < tot; t += blockDim.x) {
-        const int i = (int)(t % c.m), j = (int)(t / c.m);
-        double v;
-        if (c.kind == 0) v = c.alpha * c.src[(long long)j * c.lds + i];
-        else if (c.kind == 1) v = 0.0;
-        else v = (i == j) ? 1.0 : 0.0;
-        c.dst[(long long)j * c.ldd + i] = v;
+    // batches of 8 elements per thread: the 8 loads are issued before the 8 stores
+    // (one global round trip per batch instead of one per element)
+    constexpr int B = H2C_B;
+    for (long long t0 = threadIdx.x; t0 < tot; t0 += (long long)B * blockDim.x) {
+        double v[B];
+#pragma unroll
+        for (int u = 0; u < B; ++u) {
+            const long long t = t0 + (long long)u * blockDim.x;
+            const int i = (int)(t % c.m), j = (int)(t / c.m);
+            if (t >= tot) v[u] = 0.0;
+            else if (c.kind == 0) v[u] = c.src[(long long)j * c.lds + i];
+            else if (c.kind == 1) v[u] = 0.0;
+            else v[u] = (i == j) ? 1.0 : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < B; ++u) {
+            const long long t = t0 + (long long)u * blockDim.x;
+            if (t < tot) {
+                const int i = (int)(t % c.m), j = (int)(t / c.m);
+                c.dst[(long long)j * c.ldd + i] = c.kind == 0 ? c.alpha * v[u] : v[u];
+            }
+        }
     }
 }
 
@@ -2026,12 +2069,24 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
     // updates, t operand truncations, o overflow truncations, c new columns
     const std::string skipset = getenv("FDE_H2_SKIP") ? getenv("FDE_H2_SKIP") : "";
     auto skip = [&](char c) { return skipset.find(c) != std::string::npos; };
+    // debug (sensitivity analysis, results intact): FDE_H2_DELAY=c:us adds a us-long
+    // one-thread spin behind every launch of class c on its stream; the growth of the
+    // step period per added us says how far that class sits on the binding chain
+    const char* dly_e = getenv("FDE_H2_DELAY");
+    const char dly_c = (dly_e && dly_e[0] && dly_e[1] == ':') ? dly_e[0] : 0;
+    const long long dly_us = dly_c ? atoll(dly_e + 2) : 0;
+    auto delay = [&](char c, cudaStream_t st) {
+        if (c != dly_c || dly_us <= 0) return;
+        k_h2_spin<<<1, 1, 0, st>>>(dly_us);
+        FDE_CHECK_LAUNCH();
+    };
     auto launch_lu = [&](int kk, cudaStream_t st) {   // LU of tile kk, then the inverses of its factors
         const H2Lu* t = P->lu.p + P->steps[kk].lu;
         if (skip('l')) {
         } else if (lu_old) k_h2_lu<<<1, 512, lu_smem, st>>>(t, L->dflag.p);
         else k_h2_lu_reg<<<1, 512, 0, st>>>(t, L->dflag.p);
         FDE_CHECK_LAUNCH();
+        delay('l', st);
         if (P->steps[kk].npi) {
             cudaStream_t sv = st;
             if (np_subst) {
@@ -2041,6 +2096,7 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
             }
             if (!skip('i')) k_h2_panel<<<P->steps[kk].npi, 256, pan_smem, sv>>>(P->pan.p + P->steps[kk].pi0);
             FDE_CHECK_LAUNCH();
+            delay('i', sv);
             ++nlaunch;
             if (np_subst) FDE_CUDA(cudaEventRecord(evInv, si));
         }
@@ -2294,11 +2350,13 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         FDE_CUDA(cudaStreamWaitEvent(se, evCp, 0));
         FDE_CUDA(cudaStreamWaitEvent(se, evSnap, 0));   // snapshots of step k-1 taken
         if (!skip('o')) run_trunc(ln.tr_ov, se, 1);
+        delay('o', se);
         FDE_CUDA(cudaEventRecord(evOv, se));
         mark(k, T_OV, se);
         FDE_CUDA(cudaStreamWaitEvent(sb, evSnap, 0));
         if (tline) tmark = [&](int w) { mark(k, w ? T_CORE : T_GRAM, sb); };
         if (!skip('t')) run_trunc(ln.tr, sb, 0);
+        delay('t', sb);
         tmark = [](int) {};
         FDE_CUDA(cudaEventRecord(evOp, sb));
         mark(k, T_OP, sb);
@@ -2316,6 +2374,7 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         FDE_CUDA(cudaStreamWaitEvent(sa, evOp, 0));
         auto diag_lu = [&](cudaStream_t st) {   // tile (k+1, k+1), then LU(k+1) on sl
             if (!skip('d')) run_gemm(ln, 5, st);
+            delay('d', st);
             mark(k, T_DIAG, st);
             if (k + 1 < kstop) {
                 if (st != sl) {
@@ -2335,12 +2394,14 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
             FDE_CUDA(cudaStreamWaitEvent(sl, evCrit, 0));   // row / column k updated by step k-1
             if (!skip('n')) k_h2_panel<<<ln.nnp, 256, (pan_inv && !np_subst) ? pan_smem_inv : pan_smem, sl>>>(P->pan.p + ln.np0);
             FDE_CHECK_LAUNCH();
+            delay('n', sl);
             ++nlaunch;
             dbg("neighbour panels");
             FDE_CUDA(cudaEventRecord(evNP, sl));
             diag_lu(sl);
         }
         if (!skip('p')) run_panel(ln);
+        delay('p', sa);
         mark(k, T_PAN, sa);
         if (ln.nnp) {
             FDE_CUDA(cudaStreamWaitEvent(sa, evNP, 0));   // the products read the neighbour tiles too
@@ -2354,6 +2415,7 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         if (!skip('g')) run_gemm(ln, 1, sa);
         mark(k, T_G2, sa);
         if (!skip('g')) run_gemm(ln, 3, sa);   // conversions to dense (after the products: a block may be
+        delay('g', sa);
                                // an operand (row / column k) and a target (rows > k) at once)
         FDE_CUDA(cudaEventRecord(evP, sa));
         mark(k, T_PROD, sa);
@@ -2365,11 +2427,13 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
             ++nlaunch;
             dbg("snapshots");
         }
+        delay('s', sa);
         FDE_CUDA(cudaEventRecord(evSnap, sa));
         mark(k, T_SNAP, sa);
         if (ln.diag_scr) diag_lu(sa);
         FDE_CUDA(cudaStreamWaitEvent(sa, evC, 0));   // remaining updates of step k-1
         if (!skip('x')) run_gemm(ln, 2, sa);         // row / column k+1
+        delay('x', sa);
         FDE_CUDA(cudaEventRecord(evCrit, sa));
         mark(k, T_CRIT, sa);
         // sb: new low-rank columns of step k (after the overflow truncations)
@@ -2383,10 +2447,12 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
             }
             if (r < ln.trmid.size()) run_trunc(ln.trmid[r], sb, 0);
         }
+        delay('c', sb);
         mark(k, T_CP, sb);
         // sc: the other dense updates of step k
         FDE_CUDA(cudaStreamWaitEvent(sc, evSnap, 0));
         if (!skip_rest && !skip('r')) run_gemm(ln, 4, sc);   // (debug FDE_H2_SKIPREST: timing experiments only)
+        delay('r', sc);
         FDE_CUDA(cudaEventRecord(evC, sc));
         mark(k, T_REST, sc);
         if (tline) thost.push_back(std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - th0).count());
