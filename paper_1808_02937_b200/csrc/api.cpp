@@ -158,6 +158,8 @@ void fde_destroy(fde_handle h)
         cudaStreamDestroy(h->aux6);
         cudaStreamSynchronize(h->aux7);
         cudaStreamDestroy(h->aux7);
+        cudaStreamSynchronize(h->aux8);
+        cudaStreamDestroy(h->aux8);
         cudaStreamDestroy(h->aux);
         cudaStreamDestroy(h->aux2);
         cudaStreamDestroy(h->aux3);

@@ -36,6 +36,32 @@ extern long long g_fde_launches;
         FDE_CUDA(cudaGetLastError());             \
     } while (0)
 
+// Programmatic dependent launch (sm_90+): a kernel launched with launch_pdl right
+// behind another kernel of the same stream may start (its CTAs scheduled, its
+// descriptor prologue run) while that kernel drains; it calls pdl_wait() before
+// touching anything the previous kernel writes.  Every kernel that can be such a
+// predecessor calls pdl_trigger() first (both are no-ops without the attribute).
+#ifdef __CUDACC__
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+#endif
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args... args)
+{
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    FDE_CUDA(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...));
+}
+
 inline void fde_fail(int code, const std::string& m) { throw FdeError{code, m}; }
 
 // ----------------------------------------------------------- device buffer
@@ -151,7 +177,7 @@ struct fde_ctx {
     // (created on first use; ordered by events, never by implicit synchronisation)
     int* pinned = nullptr;   // small page-locked read-back buffer (allocated once per handle)
     cudaStream_t aux = nullptr, aux2 = nullptr, aux3 = nullptr, aux4 = nullptr, aux5 = nullptr, aux6 = nullptr,
-                 aux7 = nullptr;
+                 aux7 = nullptr, aux8 = nullptr;
     cudaEvent_t ev_aux[20] = {};
     void* stage = nullptr;   // page-locked staging of descriptor uploads (grow-only)
     size_t stage_bytes = 0;
@@ -211,6 +237,7 @@ inline cudaStream_t aux_stream(fde_ctx* h)
         FDE_CUDA(cudaStreamCreateWithPriority(&h->aux5, cudaStreamNonBlocking, hi));
         FDE_CUDA(cudaStreamCreateWithPriority(&h->aux6, cudaStreamNonBlocking, hi));
         FDE_CUDA(cudaStreamCreateWithPriority(&h->aux7, cudaStreamNonBlocking, hi));
+        FDE_CUDA(cudaStreamCreateWithPriority(&h->aux8, cudaStreamNonBlocking, hi));
         for (auto& e : h->ev_aux) FDE_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
     return h->aux;
@@ -263,6 +290,11 @@ inline cudaStream_t aux_stream7(fde_ctx* h)
 {
     aux_stream(h);
     return h->aux7;
+}
+inline cudaStream_t aux_stream8(fde_ctx* h)
+{
+    aux_stream(h);
+    return h->aux8;
 }
 
 // ------------------------------------------------------- quadrature tables

@@ -914,8 +914,10 @@ __global__ void __launch_bounds__(256) k_bgram(const TEntry* E, const TChunk* C,
     __shared__ double tile[TRUNC_CHUNK * (TRUNC_KMAX + 1)];
     __shared__ unsigned long long msk;
     __shared__ int cidx[TRUNC_KMAX];
+    pdl_trigger();
     const TChunk ch = C[blockIdx.x];
     const TEntry e = E[ch.e];
+    pdl_wait();
     const double* M = ch.side ? e.V : e.U;
     const long long ld = ch.side ? e.n : e.m;
     const int k = e.k;
@@ -968,8 +970,10 @@ __global__ void __launch_bounds__(256) k_bgram(const TEntry* E, const TChunk* C,
 __global__ void __launch_bounds__(BCORE_THREADS) k_bcore(const TEntry* E, const TChunk* C, const double* part, double tol,
                                               int kc, double* T, int* flag, double* gscr)
 {
+    pdl_trigger();
     __shared__ double ssm[5 * BCORE_KS * BCORE_KS + BCORE_KS];
     const TEntry e = E[blockIdx.x];
+    pdl_wait();
     const int k = e.k;
     if (g_h2_check && (!h2_chk(part + e.gofs, (long long)(e.c_hi - e.c_lo) * GRAM_SLOT(k) * 8, 60, k, e.c_hi - e.c_lo) ||
                        !h2_chk(T + e.tofs, 2LL * k * kc * 8, 61, k, kc)))
@@ -1252,9 +1256,11 @@ __global__ void __launch_bounds__(BCORE_THREADS) k_bcore(const TEntry* E, const 
 // (k * kc + TRUNC_CHUNK * k) doubles
 __global__ void __launch_bounds__(256) k_bapply(const TEntry* E, const TChunk* C, const double* T, int kc)
 {
+    pdl_trigger();
     extern __shared__ double bsm[];
     const TChunk ch = C[blockIdx.x];
     const TEntry e = E[ch.e];
+    pdl_wait();
     const int k = e.k;
     double* Ts = bsm;
     double* Ms = bsm + k * kc;

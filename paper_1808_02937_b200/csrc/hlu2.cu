@@ -266,16 +266,29 @@ __device__ void h2_panel_inv_body(const H2Panel& p, double* psm)
     double* Ts = psm + H2_STRIP * ldB;   // Ts[qq * ldT + i] = op(i, q0 + qq)
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const int nv = p.nvec;
+    const bool full = (m == H2_MMAX) && (nv == H2_STRIP);   // (shift / mask index forms)
     if (MODE == 2) {
-        for (int t = tid; t < nv * m; t += 256) {
-            const int c = t % nv, i = t / nv;
-            cp_async8(Bs + c * ldB + i, p.X + (long long)i * p.ldx + c);
-        }
+        if (full)
+            for (int t = tid; t < H2_STRIP * H2_MMAX; t += 256) {
+                const int c = t & (H2_STRIP - 1), i = t / H2_STRIP;
+                cp_async8(Bs + c * ldB + i, p.X + (long long)i * p.ldx + c);
+            }
+        else
+            for (int t = tid; t < nv * m; t += 256) {
+                const int c = t % nv, i = t / nv;
+                cp_async8(Bs + c * ldB + i, p.X + (long long)i * p.ldx + c);
+            }
     } else {
-        for (int t = tid; t < nv * m; t += 256) {
-            const int i = t % m, c = t / m;
-            cp_async8(Bs + c * ldB + i, p.X + (long long)c * p.ldx + i);
-        }
+        if (full)
+            for (int t = tid; t < H2_STRIP * H2_MMAX; t += 256) {
+                const int i = t & (H2_MMAX - 1), c = t / H2_MMAX;
+                cp_async8(Bs + c * ldB + i, p.X + (long long)c * p.ldx + i);
+            }
+        else
+            for (int t = tid; t < nv * m; t += 256) {
+                const int i = t % m, c = t / m;
+                cp_async8(Bs + c * ldB + i, p.X + (long long)c * p.ldx + i);
+            }
     }
     // FP64 tensor cores (mma.sync m8n8k4): warp w owns rows wm..wm+31 and vectors
     // wn..wn+15 of the 128 x 32 output (4 x 2 fragments of 8 x 8)
@@ -287,6 +300,20 @@ __device__ void h2_panel_inv_body(const H2Panel& p, double* psm)
         for (int j = 0; j < 2; ++j) dacc[i][j][0] = dacc[i][j][1] = 0.0;
     auto stage = [&](int q0, double* Tb) {
         const int nq = min(H2_PCH, m - q0);
+        if (m == H2_MMAX && nq == H2_PCH) {   // full chunk: compile-time index forms
+#pragma unroll
+            for (int u = 0; u < H2_PCH * H2_MMAX / 256; ++u) {
+                const int t = tid + 256 * u;
+                if (MODE == 0) {
+                    const int i = t & (H2_MMAX - 1), qq = t / H2_MMAX;
+                    cp_async8(Tb + qq * ldT + i, p.Ti + (long long)(q0 + qq) * p.ldi + i);
+                } else {
+                    const int qq = t & (H2_PCH - 1), i = t / H2_PCH;
+                    cp_async8(Tb + qq * ldT + i, p.Ti + (long long)i * p.ldi + q0 + qq);
+                }
+            }
+            return;
+        }
         if (MODE == 0) {   // op(i, q) = Ti(i, q): columns q0.. of Ti
             for (int t = tid; t < nq * m; t += 256) {
                 const int i = t % m, qq = t / m;
@@ -448,8 +475,10 @@ __device__ void h2_panel_body(const H2Panel& p, double* psm)
 
 __global__ void __launch_bounds__(256) k_h2_panel(const H2Panel* P)
 {
+    pdl_trigger();
     extern __shared__ double psm[];
     const H2Panel p = P[blockIdx.x];
+    pdl_wait();
     if (g_h2_check) {
         const long long ex = p.mode == 2 ? ((long long)(p.m - 1) * p.ldx + p.nvec) : ((long long)(p.nvec - 1) * p.ldx + p.m);
         if (!h2_chk(p.T, ((long long)(p.m - 1) * p.ldt + p.m) * 8, 20, p.m, p.mode) || !h2_chk(p.X, ex * 8, 21, p.nvec, p.mode))
@@ -480,6 +509,9 @@ __global__ void __launch_bounds__(256) k_h2_panel(const H2Panel* P)
 #endif
 #ifndef H2C_B
 #define H2C_B 8       // elements per thread loaded before they are stored in k_h2_copy
+#endif
+#ifndef H2G_PFC
+#define H2G_PFC 0     // prefetch the C tile into L2 at the start of a GEMM tile
 #endif
 #ifndef H2G_MINB
 #define H2G_MINB 4    // __launch_bounds__ minimum CTAs per SM of k_h2_gemm
@@ -551,6 +583,18 @@ __device__ __forceinline__ void h2_gemm_tile(const H2Tile* tiles, int tile, cons
         __syncthreads();
         tm = sT;
     }
+    pdl_wait();   // (descriptors above; operands and C below may come from the previous kernel)
+#if H2G_PFC
+    if (tk.beta != 0.0) {   // C tile lines into L2 now, read in the epilogue
+        const int mm = min(TM, tk.m - tl.m0), nn = min(TN, tk.n - tl.n0);
+        const int lines = (mm * 8 + 127) / 128;   // 128-byte lines per column
+        for (int t = threadIdx.x; t < lines * nn; t += blockDim.x) {
+            const int j = t / lines, l = t - j * lines;
+            const double* a = tk.C + (long long)(tl.n0 + j) * tk.ldc + tl.m0 + l * 16;
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
+        }
+    }
+#endif
     const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
     const int m0 = tl.m0, n0 = tl.n0, m = tk.m, n = tk.n;
     __shared__ int sbad;
@@ -703,6 +747,7 @@ __device__ __forceinline__ void h2_gemm_tile(const H2Tile* tiles, int tile, cons
 template <int TM, int TN, bool DM>
 __global__ void __launch_bounds__(256, H2G_MINB) k_h2_gemm(const H2Tile* tiles, const H2Task* tasks, const H2Term* terms, int ntile)
 {
+    pdl_trigger();
     for (int t = blockIdx.x; t < ntile; t += gridDim.x) {
         h2_gemm_tile<TM, TN, DM>(tiles, t, tasks, terms);
         __syncthreads();
@@ -711,7 +756,9 @@ __global__ void __launch_bounds__(256, H2G_MINB) k_h2_gemm(const H2Tile* tiles, 
 
 __global__ void __launch_bounds__(256) k_h2_copy(const H2Copy* C)
 {
+    pdl_trigger();
     const H2Copy c = C[blockIdx.x];
+    pdl_wait();
     const long long tot = (long long)c.m * c.n;
     if (g_h2_check) {
         bool ok = h2_chk(c.dst, ((long long)(c.n - 1) * c.ldd + c.m) * 8, 10, c.m, c.n);
@@ -1950,6 +1997,11 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
     cudaStream_t se = aux_stream6(L->h);   // overflow truncations
     cudaStream_t si = aux_stream7(L->h);   // tile inverses (np_subst)
     cudaEvent_t evLUo = L->h->ev_aux[16], evInv = L->h->ev_aux[17];
+    // operand snapshots on a stream of their own, right after the operand
+    // truncations (they read nothing the panels / products write), so they leave
+    // the t -> panels -> products -> t chain (FDE_H2_SNAP_EARLY=0: after the products)
+    const bool snap_early = !(getenv("FDE_H2_SNAP_EARLY") && atoi(getenv("FDE_H2_SNAP_EARLY")) == 0);
+    cudaStream_t ss = aux_stream8(L->h);
     // debug: fold auxiliary streams back onto the critical one (race bisection)
     if (const char* f = getenv("FDE_H2_FOLD")) {
         const std::string fs(f);
@@ -2040,6 +2092,10 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         dbg("copy");
     };
     std::function<void(int)> tmark = [](int) {};
+    // programmatic dependent launches (FDE_H2_PDL=0: off) for the kernels that follow
+    // another kernel of the same stream on the binding chain (truncation core and
+    // apply behind the Gram partials, the product groups behind the panels)
+    const bool use_pdl = !(getenv("FDE_H2_PDL") && atoi(getenv("FDE_H2_PDL")) == 0);
     auto run_trunc = [&](const H2Trunc& tr, cudaStream_t st, int ws) {
         if (!tr.ne) return;
         const TEntry* E = P->te.p + tr.e0;
@@ -2051,13 +2107,14 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         dbg("bgram");
         if (!ws) tmark(0);
         const int kmax = tr.kmax;
-        k_bcore<<<tr.ne, BCORE_THREADS, 0, st>>>(E, C, part, L->tol, rmax, Tt, L->dflag.p + 1, ws ? P->tr_scr2 : P->tr_scr);
+        launch_pdl(use_pdl, k_bcore, tr.ne, BCORE_THREADS, 0, st, E, C, part, L->tol, rmax, Tt, L->dflag.p + 1,
+                   ws ? P->tr_scr2 : P->tr_scr);
         FDE_CHECK_LAUNCH();
         dbg("bcore");
         if (!ws) tmark(1);
         const size_t asmem = (size_t)(kmax * rmax + TRUNC_CHUNK * kmax) * sizeof(double);
         set_smem_once((const void*)k_bapply, (int)asmem);
-        k_bapply<<<tr.nc, 256, asmem, st>>>(E, C, Tt, rmax);
+        launch_pdl(use_pdl, k_bapply, tr.nc, 256, asmem, st, E, C, (const double*)Tt, rmax);
         FDE_CHECK_LAUNCH();
         dbg("bapply");
         nlaunch += 3;
@@ -2107,14 +2164,26 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         const char* e = getenv("FDE_H2_REST_CTAS");
         gemm_cap[4] = e ? std::max(1, atoi(e)) : gemm_cap[4];
     }
-    auto run_gemm = [&](const H2Launch& ln, int w, cudaStream_t st) {
+    const int rest_smem = getenv("FDE_H2_REST_SMEM") ? std::max(H2G_SMEM(64, 64), atoi(getenv("FDE_H2_REST_SMEM"))) : 0;
+    if (rest_smem > 0) {
+        FDE_CUDA(cudaFuncSetAttribute(k_h2_gemm<64, 64, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, rest_smem));
+        FDE_CUDA(cudaFuncSetAttribute(k_h2_gemm<64, 64, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, rest_smem));
+    }
+    auto run_gemm = [&](const H2Launch& ln, int w, cudaStream_t st, bool pdl = false) {
+        pdl = pdl && use_pdl;
         if (!ln.g_ntile[w]) return;
         const int grid = std::min(ln.g_ntile[w], gemm_cap[w]);
         const H2Tile* tl = P->tiles.p + ln.g_tile0[w];
 #define H2G_LAUNCH(TM_, TN_)                                                                                   \
-    (use_dmma ? k_h2_gemm<TM_, TN_, true><<<grid, 256, H2G_SMEM(TM_, TN_), st>>>(tl, P->tasks.p, P->terms.p, ln.g_ntile[w]) \
-              : k_h2_gemm<TM_, TN_, false><<<grid, 256, H2G_SMEM(TM_, TN_), st>>>(tl, P->tasks.p, P->terms.p, ln.g_ntile[w]))
+    (use_dmma ? launch_pdl(pdl, k_h2_gemm<TM_, TN_, true>, grid, 256, H2G_SMEM(TM_, TN_), st, tl, P->tasks.p, P->terms.p, ln.g_ntile[w]) \
+              : launch_pdl(pdl, k_h2_gemm<TM_, TN_, false>, grid, 256, H2G_SMEM(TM_, TN_), st, tl, P->tasks.p, P->terms.p, ln.g_ntile[w]))
         switch (ln.g_shape[w]) {
+            case 0: if (w == 4 && rest_smem > 0) {   // (debug FDE_H2_REST_SMEM: fewer bulk-update CTAs per SM)
+                        launch_pdl(false, use_dmma ? k_h2_gemm<64, 64, true> : k_h2_gemm<64, 64, false>, grid, 256,
+                                   rest_smem, st, tl, P->tasks.p, P->terms.p, ln.g_ntile[w]);
+                        break;
+                    }
+                    H2G_LAUNCH(64, 64); break;
             case 1: H2G_LAUNCH(32, 32); break;
             case 2: H2G_LAUNCH(128, 16); break;
             case 3: H2G_LAUNCH(16, 16); break;
@@ -2349,6 +2418,7 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         FDE_CUDA(cudaEventRecord(evCp, sb));
         FDE_CUDA(cudaStreamWaitEvent(se, evCp, 0));
         FDE_CUDA(cudaStreamWaitEvent(se, evSnap, 0));   // snapshots of step k-1 taken
+        FDE_CUDA(cudaStreamWaitEvent(se, evP, 0));      // products of step k-1 done (their operands)
         if (!skip('o')) run_trunc(ln.tr_ov, se, 1);
         delay('o', se);
         FDE_CUDA(cudaEventRecord(evOv, se));
@@ -2360,6 +2430,22 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         tmark = [](int) {};
         FDE_CUDA(cudaEventRecord(evOp, sb));
         mark(k, T_OP, sb);
+        if (snap_early) {
+            // ss: snapshots of this step's operand factors once they are truncated; the
+            // ring scratch they fill was last read by the bulk updates of step k-2,
+            // which precede the row / column update of step k-1 (evCrit)
+            FDE_CUDA(cudaStreamWaitEvent(ss, evOp, 0));
+            FDE_CUDA(cudaStreamWaitEvent(ss, evCrit, 0));
+            FDE_CUDA(cudaStreamWaitEvent(ss, evD, 0));
+            if (ln.nsnap && !skip('s')) {
+                k_h2_copy<<<ln.nsnap, 256, 0, ss>>>(P->cps.p + ln.snap0);
+                FDE_CHECK_LAUNCH();
+                ++nlaunch;
+                dbg("snapshots");
+            }
+            delay('s', ss);
+            FDE_CUDA(cudaEventRecord(evSnap, ss));
+        }
         // sa: critical chain.  LU(k) ran on sl (k = 0: here), overlapping the
         // products and updates of step k-1; its only input from step k-1 is the
         // update of the diagonal tile, issued on sl right after the panels of step k-1.
@@ -2410,25 +2496,29 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
             FDE_CUDA(cudaStreamWaitEvent(sl, evPan, 0));
             diag_lu(sl);
         }
-        if (!skip('g')) run_gemm(ln, 0, sa);
+        if (!skip('g')) run_gemm(ln, 0, sa, !ln.nnp);   // (with neighbour panels an event wait precedes it)
         mark(k, T_G1, sa);
-        if (!skip('g')) run_gemm(ln, 1, sa);
+        if (!skip('g')) run_gemm(ln, 1, sa, ln.g_ntile[0] > 0);
         mark(k, T_G2, sa);
-        if (!skip('g')) run_gemm(ln, 3, sa);   // conversions to dense (after the products: a block may be
+        if (!skip('g')) run_gemm(ln, 3, sa, ln.g_ntile[0] + ln.g_ntile[1] > 0);   // conversions to dense (after the products: a block may be
         delay('g', sa);
                                // an operand (row / column k) and a target (rows > k) at once)
         FDE_CUDA(cudaEventRecord(evP, sa));
         mark(k, T_PROD, sa);
         // snapshots of the operand factors for the dense updates (before the
         // truncations of step k+1 rewrite them: sb / se wait for evSnap)
-        if (ln.nsnap && !skip('s')) {
-            k_h2_copy<<<ln.nsnap, 256, 0, sa>>>(P->cps.p + ln.snap0);
-            FDE_CHECK_LAUNCH();
-            ++nlaunch;
-            dbg("snapshots");
+        if (!snap_early) {
+            if (ln.nsnap && !skip('s')) {
+                k_h2_copy<<<ln.nsnap, 256, 0, sa>>>(P->cps.p + ln.snap0);
+                FDE_CHECK_LAUNCH();
+                ++nlaunch;
+                dbg("snapshots");
+            }
+            delay('s', sa);
+            FDE_CUDA(cudaEventRecord(evSnap, sa));
+        } else {
+            FDE_CUDA(cudaStreamWaitEvent(sa, evSnap, 0));   // (the updates below read the snapshots)
         }
-        delay('s', sa);
-        FDE_CUDA(cudaEventRecord(evSnap, sa));
         mark(k, T_SNAP, sa);
         if (ln.diag_scr) diag_lu(sa);
         FDE_CUDA(cudaStreamWaitEvent(sa, evC, 0));   // remaining updates of step k-1
@@ -2451,6 +2541,7 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
         mark(k, T_CP, sb);
         // sc: the other dense updates of step k
         FDE_CUDA(cudaStreamWaitEvent(sc, evSnap, 0));
+        FDE_CUDA(cudaStreamWaitEvent(sc, evP, 0));
         if (!skip_rest && !skip('r')) run_gemm(ln, 4, sc);   // (debug FDE_H2_SKIPREST: timing experiments only)
         delay('r', sc);
         FDE_CUDA(cudaEventRecord(evC, sc));
