@@ -530,7 +530,8 @@ __device__ __forceinline__ void h2_next(const H2Term* terms, int t_hi, H2Cursor&
     }
 }
 template <int TM, int TN>
-__device__ __forceinline__ void h2_stage(const H2Term& T, int m0, int n0, int m, int n, int k0, double* sA, double* sB)
+__device__ __forceinline__ void h2_stage(const H2Term& T, int m0, int n0, int m, int n, int k0, double* sA, double* sB,
+                                         bool stageB = true)
 {
     // sA[kk][mm] (ld TM + 1), sB[kk][nn] (ld TN + 1); zero outside the operands
 #pragma unroll
@@ -544,6 +545,7 @@ __device__ __forceinline__ void h2_stage(const H2Term& T, int m0, int n0, int m,
         if (gi < m && gk < T.k) cp_async8(da, T.ta ? T.A + (long long)gi * T.lda + gk : T.A + (long long)gk * T.lda + gi);
         else *da = 0.0;
     }
+    if (!stageB) return;
 #pragma unroll
     for (int u = 0; u < (TN * GK + 255) / 256; ++u) {
         const int t = threadIdx.x + 256 * u;
@@ -576,7 +578,7 @@ __device__ __forceinline__ void h2_gemm_tile(const H2Tile* tiles, int tile, cons
     __shared__ H2Term sT[H2G_TMAX];   // the task's term descriptors (one global read each)
     const H2Tile tl = tiles[tile];
     const H2Task tk = tasks[tl.task];
-    const int nt = tk.t_hi - tk.t_lo;
+    int nt = tk.t_hi - tk.t_lo;
     const H2Term* tm = terms + tk.t_lo;
     if (nt <= H2G_TMAX) {
         for (int q = threadIdx.x; q < nt; q += blockDim.x) sT[q] = terms[tk.t_lo + q];
@@ -584,6 +586,17 @@ __device__ __forceinline__ void h2_gemm_tile(const H2Tile* tiles, int tile, cons
         tm = sT;
     }
     pdl_wait();   // (descriptors above; operands and C below may come from the previous kernel)
+    // fused core (planner, rmax <= 16): the task W = V_c core carries the core
+    // definition core = U_c[k]^T V_b[k] as a leading term (ta == 3: A = U_c[k],
+    // B = V_b[k], k = rows of the sweep tile); the CTA forms the core itself in
+    // shared memory (one K slice, 16 x 16) instead of a separate launch
+    H2Term cdef;
+    const bool coremode = (TN == 16) && nt == 2 && tm[0].ta == 3;
+    if (coremode) {
+        cdef = tm[0];
+        ++tm;
+        nt = 1;
+    }
 #if H2G_PFC
     if (tk.beta != 0.0) {   // C tile lines into L2 now, read in the epilogue
         const int mm = min(TM, tk.m - tl.m0), nn = min(TN, tk.n - tl.n0);
@@ -605,7 +618,7 @@ __device__ __forceinline__ void h2_gemm_tile(const H2Tile* tiles, int tile, cons
         if (mm > 0 && nn > 0) h2_chk(tk.C + (long long)n0 * tk.ldc + m0, ((long long)(nn - 1) * tk.ldc + mm) * 8, 1, m, n);
         for (int q = 0; q < nt; ++q) {
             const H2Term T = terms[tk.t_lo + q];
-            if (T.k <= 0) continue;
+            if (T.k <= 0 || T.ta == 3) continue;
             // A: op(A) is m x k; stored (ta ? k x m : m x k) column-major with lda
             const long long ea = T.ta ? ((long long)(m0 + mm - 1) * T.lda + T.k) : ((long long)(T.k - 1) * T.lda + m0 + mm);
             const long long sa = T.ta ? (long long)m0 * T.lda : m0;
@@ -641,11 +654,37 @@ __device__ __forceinline__ void h2_gemm_tile(const H2Tile* tiles, int tile, cons
     for (int st = 0; st < H2G_ST - 1; ++st) {
         if (st < nslice) {
             const H2Term& T = tm[ld.q];
-            h2_stage<TM, TN>(T, m0, n0, m, n, ld.k0, sA[st], sB[st]);
+            h2_stage<TM, TN>(T, m0, n0, m, n, ld.k0, sA[st], sB[st], !coremode);
             if (threadIdx.x == 0) sAlpha[st] = T.alpha;
             h2_next(tm, nt, ld);
         }
         cp_async_commit_group();
+    }
+    if (TN == 16 && TM * GK >= 2048 && H2G_ST >= 3 && coremode) {
+        // U_c[k] (rows x kq) and V_b[k] (rows x n) -> sA[1], sA[2] as [col][row] (ld 129),
+        // then core[kk][nn] = sum_r U[r][kk] V[r][nn] (fixed order) -> the B stage of slice 0
+        const int rows = cdef.k, kq = tm[0].k;
+        double* sU = sA[1];
+        double* sV = sA[2];
+        for (int t = threadIdx.x; t < rows * kq; t += blockDim.x) {
+            const int r = t % rows, c = t / rows;
+            cp_async8(sU + c * 129 + r, cdef.A + (long long)c * cdef.lda + r);
+        }
+        for (int t = threadIdx.x; t < rows * n; t += blockDim.x) {
+            const int r = t % rows, c = t / rows;
+            cp_async8(sV + c * 129 + r, cdef.B + (long long)c * cdef.ldb + r);
+        }
+        cp_async_commit_group();
+        cp_async_wait_group<0>();
+        __syncthreads();
+        {
+            const int kk = threadIdx.x & 15, nn = threadIdx.x >> 4;
+            double v = 0.0;
+            if (kk < kq && nn < n)
+                for (int r = 0; r < rows; ++r) v = fma(sU[kk * 129 + r], sV[nn * 129 + r], v);
+            sB[0][kk * (TN + 1) + nn] = v;
+        }
+        __syncthreads();
     }
     for (int sl = 0; sl < nslice; ++sl) {
         cp_async_wait_group<H2G_ST - 2>();
@@ -1163,6 +1202,13 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
     // (bounds the serial work of one GEMM tile; the tile is still read / written
     // once per KFLUSH of accumulated rank instead of once per step)
     const int kflush = getenv("FDE_H2_KFLUSH") ? std::max(16, atoi(getenv("FDE_H2_KFLUSH"))) : 256;
+    // products W = V_c (U_c[k]^T V_b[k]) form their 16 x 16 core in-CTA (the 128 x 16 tile
+    // shape of rmax <= 16) instead of a separate launch on the binding chain.  Pays with
+    // few sweep tiles (c4, 64 tiles: factorisation 11.39 -> 11.28 ms); with many, every
+    // W tile re-forming its core costs more than the launch (c5, 256: 154.4 -> 156.7 ms).
+    // FDE_H2_FUSECORE=0/1 forces it.
+    const char* e_fc = getenv("FDE_H2_FUSECORE");
+    const bool fuse_core = rmax <= 16 && !getenv("FDE_H2_SHAPES") && (e_fc ? atoi(e_fc) != 0 : nl < 128);
     std::vector<int> stamp(nb, 0), tile_stamp((size_t)nl * nl, 0), tile_task((size_t)nl * nl, 0);
     int stamp_id = 0, tile_stamp_id = 0;
     for (int k = 0; k < nl; ++k) {
@@ -1273,17 +1319,22 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
                 const HBlock &B = S.bl[b], &C = S.bl[c];
                 if (isLR(b)) {
                     int64_t core = -1;
+                    const bool fuse = fuse_core && isLR(c) && kc[c] <= 16 && kc[b] <= 16;
                     if (isLR(c)) {   // core = U_c[k]^T V_b[k]  (kc_c x kc_b)
                         core = scr;
                         scr += (int64_t)kc[c] * kc[b];
-                        VTask t{{3, sid, core}, kc[c], kc[c], kc[b], 0.0, {}};
-                        t.terms.push_back({{1, c, lr0[k] - row0(c)}, {2, b, lr0[k] - col0(b)}, C.m, B.n, mk, 1, 0, 1.0});
-                        st.g1.push_back(t);
+                        if (!fuse) {
+                            VTask t{{3, sid, core}, kc[c], kc[c], kc[b], 0.0, {}};
+                            t.terms.push_back({{1, c, lr0[k] - row0(c)}, {2, b, lr0[k] - col0(b)}, C.m, B.n, mk, 1, 0, 1.0});
+                            st.g1.push_back(t);
+                        }
                     }
                     pr.w = scr;
                     pr.rw = kc[b];
                     scr += C.n * kc[b];
                     VTask t{{3, sid, pr.w}, C.n, (int)C.n, kc[b], 0.0, {}};
+                    if (fuse)      // the core definition rides with the product (formed in-CTA)
+                        t.terms.push_back({{1, c, lr0[k] - row0(c)}, {2, b, lr0[k] - col0(b)}, C.m, B.n, mk, 3, 0, 1.0});
                     if (isLR(c))   // W = V_c core
                         t.terms.push_back({{2, c, 0}, {3, sid, core}, C.n, kc[c], kc[c], 0, 0, 1.0});
                     else           // W = D_c[k rows, :]^T V_b[k]
