@@ -244,3 +244,39 @@ def test_config5_sampled_rows_and_fft_vs_dmma(fde, h):
     _record("c5_rows_fft_dmma", MA=mA, MB_dmma=mB, MB_fft_vs_dmma=mB_cross)
     del Ag, den
     op.free()
+
+
+def test_hlu_launch_variants(fde, h, monkeypatch):
+    """The H-LU sweep's launch-level options: programmatic dependent
+    launches and the operand snapshots on their own stream change only WHEN kernels
+    run, so the preconditioner is bitwise the default one with them off; the fused
+    16 x 16 cores (formed in-CTA by the product tiles, a different summation order)
+    give another tol = 1e-3 preconditioner, and every variant's solve reaches the
+    oracle's X (M-D).  Mirrored graded mesh N = 256, P = 8: 16 sweep tiles, so the
+    fused cores are on by default."""
+    p = fi.config4(N=256, P=8)
+    op = fde.assemble_problem(h, p)
+    G = fde.sem_rhs(h, op, p.forcings)
+    hm = fde.hmatrix_build(h, op, p.R, p.lam, p.n_min)
+    so = O.assemble_system(p)
+    Go = O.rhs(p, so, p.forcings[0])
+    Xo = O.solve_dense(so.A, Go).reshape(-1)
+    r = torch.tensor(np.random.default_rng(11).standard_normal((2, p.n)), device="cuda")
+    zs = {}
+    for name, env in [("default", {}), ("no-pdl", {"FDE_H2_PDL": "0"}), ("late-snap", {"FDE_H2_SNAP_EARLY": "0"}),
+                      ("no-fuse", {"FDE_H2_FUSECORE": "0"})]:
+        for k in ("FDE_H2_PDL", "FDE_H2_SNAP_EARLY", "FDE_H2_FUSECORE"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        lu = fde.hlu_factor(h, hm, 1e-3)
+        zs[name] = fde.precond_apply(h, lu, r).clone()
+        X, rep = fde.solve(h, op, lu, G, tol=1e-12)
+        md_check(p, X.cpu().numpy()[0], so, Go, Xo=Xo)
+        lu.free()
+    assert torch.equal(zs["no-pdl"], zs["default"])
+    assert torch.equal(zs["late-snap"], zs["default"])
+    q = (torch.linalg.norm(zs["no-fuse"] - zs["default"]) / torch.linalg.norm(zs["default"])).item()
+    assert q <= 1e-3, q
+    for o in (hm, op):
+        o.free()
