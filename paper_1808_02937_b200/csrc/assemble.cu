@@ -133,9 +133,11 @@ __device__ inline int q_select(double eta, int P, int qm)
     // (single precision suffices: the result is a point count; a count that differs
     // by one near a rounding boundary only moves the quadrature error around 1e-17)
     const float etaf = (float)fmin(eta, 1e30);
-    const float rho = etaf + sqrtf(fmaxf(etaf * etaf - 1.0f, 0.0f));
+    // (explicit fmaf: the same rounding wherever the function is inlined -- a contraction
+    // decided per call site moved counts at a rounding boundary between kernels)
+    const float rho = etaf + sqrtf(fmaxf(fmaf(etaf, etaf, -1.0f), 0.0f));
     const float lr = __log10f(fmaxf(0.8f * rho, 1.05f));
-    int q = (int)ceilf((__fdividef(c_qdigits, lr) + (float)P) * 0.5f);
+    int q = (int)ceilf(__fmul_rn(__fadd_rn(__fdividef(c_qdigits, lr), (float)P), 0.5f));
     int qmin = P / 2 + 2;
     if (q < qmin) q = qmin;
     if (q > qm) q = qm;
@@ -340,6 +342,129 @@ __global__ void __launch_bounds__(32 * ASM_WARPS) k_pairs_kernel(AsmDev D, int m
         slot = lslot[p];
     }
     warp_pair<PT>(D, ws, i, j, out + slot * (long long)D.P * D.P, lane);
+}
+
+// Lane-per-pair path for P <= 8: almost every pair of a mesh is "far" -- gap d > 0
+// and d >= 2 max(h_i, h_j), so warp_graded makes ONE cell of the whole rectangle --
+// and a warp spent on one such pair leaves most lanes idle (6 x 6 kernel values,
+// 6 + 6 Legendre rows, 64 moments over 32 lanes, warp barriers between the stages).
+// Here lane L of warp w owns pair 32 w + L and runs the same one-cell rule alone:
+// identical points, weights, kernel values and fma sequences (T[n] over b, then the
+// moments over a), so the moments are bit-identical to warp_cell's; the pairs that
+// are not single-cell far pairs (self, touching, near) are then done one by one by
+// the whole warp with warp_pair, as before.
+#ifndef ASM_LANE_UB
+#define ASM_LANE_UB 2     // (b loop by two: also the unrolling that reproduces warp_cell's bits)
+#endif
+#ifndef ASM_LANE_WARPS
+#define ASM_LANE_WARPS 2  // warps per CTA of the lane path
+#endif
+#ifndef ASM_LANE_UA
+#define ASM_LANE_UA 1
+#endif
+constexpr int kLaneUB = ASM_LANE_UB, kLaneUA = ASM_LANE_UA;   // (loop unrolling of the lane path)
+template <int PT>
+__global__ void __launch_bounds__(32 * ASM_LANE_WARPS) k_pairs_lane(AsmDev D, int mode, int i0, int i1, int j0, int j1,
+                                                              const int* li, const int* lj, const long long* lslot,
+                                                              long long count, double* out)
+{
+    static_assert(PT >= 1 && PT <= 8, "lane path: P <= 8 (moments in registers)");
+    constexpr int P = PT;
+    extern __shared__ double smem[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const long long p = ((long long)blockIdx.x * ASM_LANE_WARPS + wid) * 32 + lane;
+    const bool valid = p < count;
+    int i = 0, j = 0;
+    long long slot = 0;
+    if (valid) {
+        if (mode == 0) {
+            const long long T0 = (long long)i0 * (i0 + 1) / 2;
+            const long long g = T0 + p;
+            long long ii = (long long)((sqrt(8.0 * (double)g + 1.0) - 1.0) * 0.5);
+            while ((ii + 1) * (ii + 2) / 2 <= g) ++ii;
+            while (ii * (ii + 1) / 2 > g) --ii;
+            i = (int)ii;
+            j = (int)(g - ii * (ii + 1) / 2);
+            slot = p;
+        } else if (mode == 1) {
+            const int w = j1 - j0;
+            i = i0 + (int)(p / w);
+            j = j0 + (int)(p % w);
+            slot = p;
+        } else {
+            i = li[p];
+            j = lj[p];
+            slot = lslot[p];
+        }
+    }
+    bool far = false;
+    double hi = 0.0, hj = 0.0, d = 0.0;
+    if (valid && i != j) {
+        hi = D.nodes[i + 1] - D.nodes[i];
+        hj = D.nodes[j + 1] - D.nodes[j];
+        d = D.nodes[i] - D.nodes[j + 1];
+        if (d > 0.0) {   // warp_graded's first cell on (u0, v0) = (0, 0), c = 1/2
+            double ub = fmin(hi, 0.5 * d);
+            if (hi - ub < 1e-3 * ub) ub = hi;
+            double vb = fmin(hj, 0.5 * d);
+            if (hj - vb < 1e-3 * vb) vb = hj;
+            far = (ub == hi) && (vb == hj);
+        }
+    }
+    if (far) {   // warp_cell(d, hi, hj, 0, hi, 0, hj), one lane
+        const int Qu = q_select(1.0 + 2.0 * d / hi, P, D.qm);
+        const int Qv = q_select(1.0 + 2.0 * d / hj, P, D.qm);
+        const double* gxu = c_glx + Qu * (Qu - 1) / 2;
+        const double* gwu = c_glw + Qu * (Qu - 1) / 2;
+        const double* gxv = c_glx + Qv * (Qv - 1) / 2;
+        const double* gwv = c_glw + Qv * (Qv - 1) / 2;
+        const double uc = 0.5 * hi, vc = 0.5 * hj;
+        const double zc = d + uc + vc;
+        const double kc = pow(zc, D.oma), izc = 1.0 / zc;
+        double acc[P * P];
+#pragma unroll
+        for (int t = 0; t < P * P; ++t) acc[t] = 0.0;
+#pragma unroll kLaneUA
+        for (int a = 0; a < Qu; ++a) {
+            const double u = 0.5 * hi * (gxu[a] + 1.0);
+            const double wa = 0.5 * hi * gwu[a];
+            double Lu[P];
+            leg_all(P, 2.0 * u / hi - 1.0, Lu);
+            double T[P];
+#pragma unroll
+            for (int n = 0; n < P; ++n) T[n] = 0.0;
+#pragma unroll kLaneUB
+            for (int b = 0; b < Qv; ++b) {
+                const double v = 0.5 * hj * (gxv[b] + 1.0);
+                const double wb = 0.5 * hj * gwv[b];
+                double Lv[P];
+                leg_all(P, 1.0 - 2.0 * v / hj, Lv);
+                const double delta = ((u - uc) + (v - vc)) * izc;
+                const double kv = wa * wb * kc * exp(D.oma * log1p(delta));
+#pragma unroll
+                for (int n = 0; n < P; ++n) T[n] = fma(kv, Lv[n], T[n]);
+            }
+#pragma unroll
+            for (int m = 0; m < P; ++m)
+#pragma unroll
+                for (int n = 0; n < P; ++n) acc[m * P + n] = fma(Lu[m], T[n], acc[m * P + n]);
+        }
+        const double sc = D.g0 * (2.0 / hi) * (2.0 / hj);
+        double* o = out + slot * (long long)(P * P);
+#pragma unroll
+        for (int t = 0; t < P * P; ++t) o[t] = sc * (0.0 + acc[t]);
+    }
+    // the other pairs of this warp: one at a time with the whole warp
+    unsigned slow = __ballot_sync(0xffffffffu, valid && !far);
+    if (!slow) return;
+    WarpWS ws = carve_ws(smem + (size_t)wid * ws_doubles(P, D.qm), P, D.qm);
+    while (slow) {
+        const int L = __ffs(slow) - 1;
+        slow &= slow - 1;
+        const int ii = __shfl_sync(0xffffffffu, i, L), jj = __shfl_sync(0xffffffffu, j, L);
+        const long long sl = __shfl_sync(0xffffffffu, slot, L);
+        warp_pair<PT>(D, ws, ii, jj, out + sl * (long long)(P * P), lane);
+    }
 }
 
 // Kself[m][n] = gamma0 2^{alpha-2} sum_k sum_l wo_k wi_l L_m(xi_k) L_n(xi_k - (1+xi_k)(1+y_l)/2)
@@ -856,12 +981,27 @@ static void launch_pairs(fde_ctx* h, fde_op* op, int mode, int i0, int i1, int j
         k_pairs_kernel<PT_><<<(unsigned)blocks, 32 * ASM_WARPS, smem, h->stream>>>(D, mode, i0, i1, j0, j1, li, lj, ls, \
                                                                                   count, out);                   \
     } while (0)
-    switch (op->P) {
-        case 4: FDE_PAIRS(4); break;
-        case 8: FDE_PAIRS(8); break;
-        case 16: FDE_PAIRS(16); break;
-        default: FDE_PAIRS(0);
+    // lane-per-pair far-field path for P = 4, 8 (FDE_ASM_LANE=0: one warp per pair)
+    static const bool lane_path = !(getenv("FDE_ASM_LANE") && atoi(getenv("FDE_ASM_LANE")) == 0);
+    const size_t lsmem = (size_t)ASM_LANE_WARPS * ws_doubles(op->P, qm) * sizeof(double);
+#define FDE_PAIRS_LANE(PT_)                                                                                     \
+    do {                                                                                                        \
+        FDE_CUDA(cudaFuncSetAttribute(k_pairs_lane<PT_>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsmem)); \
+        k_pairs_lane<PT_><<<(unsigned)ceil_div(count, 32LL * ASM_LANE_WARPS), 32 * ASM_LANE_WARPS, lsmem, h->stream>>>( \
+            D, mode, i0, i1, j0, j1, li, lj, ls, count, out);                                                   \
+    } while (0)
+    if (lane_path && (op->P == 8 || op->P == 4)) {
+        if (op->P == 8) FDE_PAIRS_LANE(8);
+        else FDE_PAIRS_LANE(4);
+    } else {
+        switch (op->P) {
+            case 4: FDE_PAIRS(4); break;
+            case 8: FDE_PAIRS(8); break;
+            case 16: FDE_PAIRS(16); break;
+            default: FDE_PAIRS(0);
+        }
     }
+#undef FDE_PAIRS_LANE
 #undef FDE_PAIRS
     FDE_CHECK_LAUNCH();
 }
