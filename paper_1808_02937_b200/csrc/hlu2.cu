@@ -40,7 +40,9 @@
 
 #define H2_MMAX 128
 #define H2_STRIP 32
+#ifndef H2_PCH
 #define H2_PCH 16      // inverse-panel staging chunk (columns of op)
+#endif
 #define H2_CP_CHUNK 4096   // elements per copy CTA
 
 struct H2Lu {
