@@ -990,7 +990,10 @@ static void launch_pairs(fde_ctx* h, fde_op* op, int mode, int i0, int i1, int j
         k_pairs_lane<PT_><<<(unsigned)ceil_div(count, 32LL * ASM_LANE_WARPS), 32 * ASM_LANE_WARPS, lsmem, h->stream>>>( \
             D, mode, i0, i1, j0, j1, li, lj, ls, count, out);                                                   \
     } while (0)
-    if (lane_path && (op->P == 8 || op->P == 4)) {
+    // (only for large all-pairs launches -- the triangle or a rectangle of a dense assembly --
+    // where nearly every pair is far: near-field lists and the few lag pairs of a Toeplitz
+    // operator are mostly near pairs, which the lane path would serialise 32 to a warp)
+    if (lane_path && (op->P == 8 || op->P == 4) && mode != 2 && count >= 32LL * 1024) {
         if (op->P == 8) FDE_PAIRS_LANE(8);
         else FDE_PAIRS_LANE(4);
     } else {
