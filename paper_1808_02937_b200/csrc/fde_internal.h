@@ -179,6 +179,11 @@ struct fde_ctx {
     cudaStream_t aux = nullptr, aux2 = nullptr, aux3 = nullptr, aux4 = nullptr, aux5 = nullptr, aux6 = nullptr,
                  aux7 = nullptr, aux8 = nullptr;
     cudaEvent_t ev_aux[20] = {};
+    // SM partition of the H-LU sweep (FDE_H2_GREEN = SMs of the bulk dense updates):
+    // streams of two green contexts, made once per handle and partition size
+    int green_n = 0;
+    cudaStream_t g_bulk = nullptr;
+    cudaStream_t g_chain[6] = {};
     void* stage = nullptr;   // page-locked staging of descriptor uploads (grow-only)
     size_t stage_bytes = 0;
     // upload ring (fde_ring_upload): two halves; a half is reused after the event

@@ -37,6 +37,7 @@
 #include <functional>
 #include <cstdlib>
 #include <set>
+#include <cuda.h>   // (types of the green-context driver API; entry points via cudaGetDriverEntryPoint)
 
 #define H2_MMAX 128
 #define H2_STRIP 32
@@ -932,6 +933,57 @@ struct VStep {
     std::vector<std::vector<VTrunc>> trmid; // truncations between rounds
     int64_t scratch = 0;
 };
+
+// Green contexts (SM partitions) for the H-LU sweep: the bulk dense updates on
+// `nbulk` SMs, the binding chain (panels, products, truncations, new columns, LU)
+// on the others, so the latency-bound chain kernels never share an SM with the
+// long bulk-update CTAs.  Driver entry points through the runtime (no libcuda link).
+static bool h2_green_streams(fde_ctx* h, int nbulk)
+{
+    if (h->green_n == nbulk) return true;
+    if (h->green_n != 0) return false;   // (one partition per handle)
+    typedef CUresult (*FGet)(CUdevice*, int);
+    typedef CUresult (*FRes)(CUdevice, CUdevResource*, CUdevResourceType);
+    typedef CUresult (*FSplit)(CUdevResource*, unsigned*, const CUdevResource*, CUdevResource*, unsigned, unsigned);
+    typedef CUresult (*FDesc)(CUdevResourceDesc*, CUdevResource*, unsigned);
+    typedef CUresult (*FCreate)(CUgreenCtx*, CUdevResourceDesc, CUdevice, unsigned);
+    typedef CUresult (*FStream)(CUstream*, CUgreenCtx, unsigned, int);
+    void *pg = nullptr, *pr = nullptr, *ps = nullptr, *pd = nullptr, *pc = nullptr, *pt = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuDeviceGet", &pg, cudaEnableDefault, &q) != cudaSuccess || !pg ||
+        cudaGetDriverEntryPoint("cuDeviceGetDevResource", &pr, cudaEnableDefault, &q) != cudaSuccess || !pr ||
+        cudaGetDriverEntryPoint("cuDevSmResourceSplitByCount", &ps, cudaEnableDefault, &q) != cudaSuccess || !ps ||
+        cudaGetDriverEntryPoint("cuDevResourceGenerateDesc", &pd, cudaEnableDefault, &q) != cudaSuccess || !pd ||
+        cudaGetDriverEntryPoint("cuGreenCtxCreate", &pc, cudaEnableDefault, &q) != cudaSuccess || !pc ||
+        cudaGetDriverEntryPoint("cuGreenCtxStreamCreate", &pt, cudaEnableDefault, &q) != cudaSuccess || !pt)
+        return false;
+    int dev = 0;
+    FDE_CUDA(cudaGetDevice(&dev));
+    CUdevice cd;
+    if (((FGet)pg)(&cd, dev) != CUDA_SUCCESS) return false;
+    CUdevResource all, grp[1], rem;
+    unsigned ng = 1;
+    if (((FRes)pr)(cd, &all, CU_DEV_RESOURCE_TYPE_SM) != CUDA_SUCCESS) return false;
+    if (((FSplit)ps)(grp, &ng, &all, &rem, 0, (unsigned)nbulk) != CUDA_SUCCESS || ng != 1 || rem.sm.smCount < 8)
+        return false;
+    CUdevResourceDesc d1, d2;
+    CUgreenCtx g1, g2;
+    if (((FDesc)pd)(&d1, &grp[0], 1) != CUDA_SUCCESS || ((FDesc)pd)(&d2, &rem, 1) != CUDA_SUCCESS) return false;
+    if (((FCreate)pc)(&g1, d1, cd, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS ||
+        ((FCreate)pc)(&g2, d2, cd, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS)
+        return false;
+    int lo = 0, hi = 0;
+    FDE_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CUstream st;
+    if (((FStream)pt)(&st, g1, CU_STREAM_NON_BLOCKING, lo) != CUDA_SUCCESS) return false;
+    h->g_bulk = (cudaStream_t)st;
+    for (int i = 0; i < 6; ++i) {
+        if (((FStream)pt)(&st, g2, CU_STREAM_NON_BLOCKING, hi) != CUDA_SUCCESS) return false;
+        h->g_chain[i] = (cudaStream_t)st;
+    }
+    h->green_n = nbulk;   // (the green contexts live as long as the process: a handle keeps its streams)
+    return true;
+}
 
 struct H2Trunc {       // one batched truncation: ranges in the flat entry / chunk arrays
     int e0 = 0, ne = 0, c0 = 0, nc = 0, kmax = 0;
@@ -2055,6 +2107,21 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
     // the t -> panels -> products -> t chain (FDE_H2_SNAP_EARLY=0: after the products)
     const bool snap_early = !(getenv("FDE_H2_SNAP_EARLY") && atoi(getenv("FDE_H2_SNAP_EARLY")) == 0);
     cudaStream_t ss = aux_stream8(L->h);
+    // SM partition (FDE_H2_GREEN = SMs of the bulk dense updates, multiple of 8; 0: off)
+    if (const char* g = getenv("FDE_H2_GREEN")) {
+        const int nbulk = atoi(g);
+        if (nbulk > 0 && h2_green_streams(L->h, nbulk)) {
+            sc = L->h->g_bulk;
+            if (!(getenv("FDE_H2_GREEN_CHAIN") && atoi(getenv("FDE_H2_GREEN_CHAIN")) == 0)) {
+                sa = L->h->g_chain[0];
+                sb = L->h->g_chain[1];
+                sl = L->h->g_chain[2];
+                se = L->h->g_chain[3];
+                si = L->h->g_chain[4];
+                ss = L->h->g_chain[5];
+            }
+        }
+    }
     // debug: fold auxiliary streams back onto the critical one (race bisection)
     if (const char* f = getenv("FDE_H2_FOLD")) {
         const std::string fs(f);
