@@ -18,7 +18,7 @@ timeout 600 ncu --set full --clock-control none -k regex:k_apply_pf -s 2 -c 1 -o
 timeout 600 ncu --set full --clock-control none --kernel-name-base demangled -k "regex:k_h2_gemm<.int.64, .int.64" -s 41 -c 1 -o $O/${T}_h2gemm python tools/hlu_only.py 64 c4 > /dev/null 2>&1
 timeout 600 ncu --set full --clock-control none -k regex:k_h2_lu_reg -s 20 -c 1 -o $O/${T}_lureg python tools/hlu_only.py 64 c4 > /dev/null 2>&1
 timeout 600 ncu --set full --clock-control none -k regex:k_bcore -s 60 -c 1 -o $O/${T}_bcore python tools/hlu_only.py 64 c4 > /dev/null 2>&1
-timeout 600 ncu --set full --clock-control none -k regex:"k_pairs_kernel|k_expand_tiles" -s 0 -c 2 -o $O/${T}_asm python tools/gemv_only.py > /dev/null 2>&1
+timeout 600 ncu --set full --clock-control none -k regex:"k_pairs_kernel|k_pairs_lane|k_expand_tiles" -s 0 -c 2 -o $O/${T}_asm python tools/gemv_only.py > /dev/null 2>&1
 FDE_LAUNCH_CMD="python bench.py --steps 2 --warmup 1 --no-cpu-baseline" python tools/profile_summary.py $O/${T}_launches.csv $O/${T} $O/${T}_gemv.ncu-rep $O/${T}_gemm.ncu-rep $O/${T}_apply.ncu-rep $O/${T}_h2gemm.ncu-rep $O/${T}_lureg.ncu-rep $O/${T}_bcore.ncu-rep $O/${T}_asm.ncu-rep
 rm -f $O/*.ncu-rep $O/${T}_launches.csv   # (the summaries above are what is kept; gpurun_out is capped at 64 MiB)
 ls -la $O | tail -30
