@@ -787,7 +787,7 @@ __device__ __forceinline__ void h2_gemm_tile(const H2Tile* tiles, int tile, cons
 
 // grid-stride over the tiles: a capped grid leaves SMs to the critical stream
 template <int TM, int TN, bool DM>
-__global__ void __launch_bounds__(256, H2G_MINB) k_h2_gemm(const H2Tile* tiles, const H2Task* tasks, const H2Term* terms, int ntile)
+__global__ void __launch_bounds__(256, (TM * TN > 4096) ? 2 : H2G_MINB) k_h2_gemm(const H2Tile* tiles, const H2Task* tasks, const H2Term* terms, int ntile)
 {
     pdl_trigger();
     for (int t = blockIdx.x; t < ntile; t += gridDim.x) {
@@ -1867,7 +1867,7 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
     // 2 = 128 x 16 (products: outputs rmax wide), 3 = 16 x 16 (cores: rmax x rmax)
     int gemm_shape[6] = {rmax <= 16 ? 3 : 1, rmax <= 16 ? 2 : 0, 0, 0, 0, 1};
     if (const char* e = getenv("FDE_H2_SHAPES"))   // debug: six digits
-        for (int w = 0; w < 6 && e[w]; ++w) gemm_shape[w] = (e[w] - '0') & 3;
+        for (int w = 0; w < 6 && e[w]; ++w) gemm_shape[w] = std::min(5, std::max(0, e[w] - '0'));
     const bool plan_stats = getenv("FDE_DEBUG_PLAN") != nullptr;
     // tasks of v (then v2) with sel[q] == want (sel null: all), in order
     auto put_gemm_sel = [&](const std::vector<VTask>& v, const std::vector<char>* sel, char want, H2Launch& ln,
@@ -1875,7 +1875,7 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
                             const std::vector<char>* sel2 = nullptr) {
         ln.g_shape[which] = shape;
         ln.g_tile0[which] = (int)vtile.size();
-        static const int shm[4] = {64, 32, 128, 16}, shn[4] = {64, 32, 16, 16};
+        static const int shm[6] = {64, 32, 128, 16, 128, 64}, shn[6] = {64, 32, 16, 16, 64, 128};
         const int tm = shm[shape], tn = shn[shape];
         const size_t n1 = v.size(), n2 = v2 ? v2->size() : 0;
         for (size_t q = 0; q < n1 + n2; ++q) {
@@ -2000,7 +2000,7 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
     // ---- exact descriptor counts -> device arrays and the pinned staging buffer
     size_t n_pan = 0, n_task = 0, n_term = 0, n_tile = 0, n_cp = 0, n_te = 0, n_tc = 0;
     auto cnt_tasks = [&](const std::vector<VTask>& v, int shape) {
-        static const int shm[4] = {64, 32, 128, 16}, shn[4] = {64, 32, 16, 16};
+        static const int shm[6] = {64, 32, 128, 16, 128, 64}, shn[6] = {64, 32, 16, 16, 64, 128};
         for (auto& t : v) {
             ++n_task;
             n_term += t.terms.size();
@@ -2177,6 +2177,10 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
     set_smem_once((const void*)k_h2_gemm<128, 16, false>, H2G_SMEM(128, 16));
     set_smem_once((const void*)k_h2_gemm<32, 32, false>, H2G_SMEM(32, 32));
     set_smem_once((const void*)k_h2_gemm<16, 16, false>, H2G_SMEM(16, 16));
+    set_smem_once((const void*)k_h2_gemm<128, 64, true>, H2G_SMEM(128, 64));
+    set_smem_once((const void*)k_h2_gemm<64, 128, true>, H2G_SMEM(64, 128));
+    set_smem_once((const void*)k_h2_gemm<128, 64, false>, H2G_SMEM(128, 64));
+    set_smem_once((const void*)k_h2_gemm<64, 128, false>, H2G_SMEM(64, 128));
     int nlaunch = 0;
     // FDE_DEBUG_SERIAL: synchronise after every launch and name the first failing one
     const bool dbg_serial = getenv("FDE_DEBUG_SERIAL") != nullptr;
@@ -2307,6 +2311,8 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
             case 1: H2G_LAUNCH(32, 32); break;
             case 2: H2G_LAUNCH(128, 16); break;
             case 3: H2G_LAUNCH(16, 16); break;
+            case 4: H2G_LAUNCH(128, 64); break;   // (debug shapes: bulk tiles of 128 x 64 / 64 x 128)
+            case 5: H2G_LAUNCH(64, 128); break;
             default: H2G_LAUNCH(64, 64);
         }
 #undef H2G_LAUNCH
