@@ -474,28 +474,83 @@ __global__ void k_selfref_kernel(AsmDev D, double* kself, double* mref)
 {
     const int P = D.P;
     const int t = threadIdx.x;
+    // the Gauss-Jacobi rules in shared memory (read 81 times per entry: from global
+    // memory every inner step was a dependent L2 round trip)
+    __shared__ double sgx[FDE_MAX_P + 2], sgw[FDE_MAX_P + 2], six[FDE_MAX_P + 2], siw[FDE_MAX_P + 2];
+    for (int k = t; k < D.qr; k += blockDim.x) { sgx[k] = D.gjr_x[k]; sgw[k] = D.gjr_w[k]; }
+    for (int k = t; k < D.qi; k += blockDim.x) { six[k] = D.gji_x[k]; siw[k] = D.gji_w[k]; }
+    __syncthreads();
     double Lm[FDE_MAX_P + 2], Ln[FDE_MAX_P + 2];
     const double a2 = exp2(-1.0 - D.oma);   // 2^{alpha-2}
-    for (int idx = t; idx < P * P; idx += blockDim.x) {
-        int m = idx / P, nn = idx - m * P;
-        double s = 0.0;
-        for (int k = 0; k < D.qr; ++k) {
-            double xi = D.gjr_x[k];
-            leg_all(P, xi, Lm);
-            double inner = 0.0;
-            for (int l = 0; l < D.qi; ++l) {
-                double eta = xi - 0.5 * (1.0 + xi) * (1.0 + D.gji_x[l]);
-                leg_all(P, eta, Ln);
-                inner = fma(D.gji_w[l], Ln[nn], inner);
-            }
-            s = fma(D.gjr_w[k] * Lm[m], inner, s);
-        }
-        kself[idx] = D.g0 * a2 * s;
-    }
     const int M = P + 1;
     const int Q = (P + 2 < FDE_QMAX) ? P + 2 : FDE_QMAX;   // exact for degree 2P
     const double* gx = c_glx + Q * (Q - 1) / 2;
     const double* gw = c_glw + Q * (Q - 1) / 2;
+    // small degrees: the Legendre values of every point pair in shared memory, each
+    // computed once by its own thread, then the same fma sequences per entry from there
+    // (one thread per entry re-evaluated them serially in local memory: ~30 us)
+    constexpr int SR_CAP = 17 * 17 * 16;   // (P <= 16: qr, qi <= 17)
+    __shared__ double sLn[SR_CAP], sLm[17 * 16], sIn[17 * 16], sLq[18 * 18];
+    if (P <= 16 && D.qr <= 17 && D.qi <= 17 && D.qr * D.qi * P <= SR_CAP && Q <= 18) {
+        for (int kl = t; kl < D.qr * D.qi; kl += blockDim.x) {
+            const int k = kl / D.qi, l = kl - k * D.qi;
+            const double xi = sgx[k];
+            const double eta = xi - 0.5 * (1.0 + xi) * (1.0 + six[l]);
+            leg_all(P, eta, Ln);
+            for (int nn = 0; nn < P; ++nn) sLn[kl * P + nn] = Ln[nn];
+        }
+        for (int k = t; k < D.qr; k += blockDim.x) {
+            leg_all(P, sgx[k], Lm);
+            for (int m = 0; m < P; ++m) sLm[k * P + m] = Lm[m];
+        }
+        for (int k = t; k < Q; k += blockDim.x) {
+            leg_all(P + 2 > 2 ? P + 2 : 2, gx[k], Lm);
+            for (int a = 0; a < P + 2; ++a) sLq[k * (P + 2) + a] = Lm[a];
+        }
+        __syncthreads();
+        for (int kn = t; kn < D.qr * P; kn += blockDim.x) {   // inner[k][nn]
+            const int k = kn / P, nn = kn - k * P;
+            double inner = 0.0;
+            for (int l = 0; l < D.qi; ++l) inner = fma(siw[l], sLn[(k * D.qi + l) * P + nn], inner);
+            sIn[kn] = inner;
+        }
+        __syncthreads();
+        for (int idx = t; idx < P * P; idx += blockDim.x) {
+            const int m = idx / P, nn = idx - m * P;
+            double s = 0.0;
+            for (int k = 0; k < D.qr; ++k) s = fma(sgw[k] * sLm[k * P + m], sIn[k * P + nn], s);
+            kself[idx] = D.g0 * a2 * s;
+        }
+        for (int idx = t; idx < M * M; idx += blockDim.x) {
+            const int a = idx / M, b = idx - a * M;
+            double s = 0.0;
+            for (int k = 0; k < Q; ++k) {
+                const double xi = gx[k];
+                const double* Lq = sLq + k * (P + 2);
+                double fa = (a == 0) ? 0.5 * (1 - xi) : (a == P ? 0.5 * (1 + xi) : Lq[a - 1] - Lq[a + 1]);
+                double fb = (b == 0) ? 0.5 * (1 - xi) : (b == P ? 0.5 * (1 + xi) : Lq[b - 1] - Lq[b + 1]);
+                s = fma(gw[k], fa * fb, s);
+            }
+            mref[idx] = s;
+        }
+        return;
+    }
+    for (int idx = t; idx < P * P; idx += blockDim.x) {
+        int m = idx / P, nn = idx - m * P;
+        double s = 0.0;
+        for (int k = 0; k < D.qr; ++k) {
+            double xi = sgx[k];
+            leg_all(P, xi, Lm);
+            double inner = 0.0;
+            for (int l = 0; l < D.qi; ++l) {
+                double eta = xi - 0.5 * (1.0 + xi) * (1.0 + six[l]);
+                leg_all(P, eta, Ln);
+                inner = fma(siw[l], Ln[nn], inner);
+            }
+            s = fma(sgw[k] * Lm[m], inner, s);
+        }
+        kself[idx] = D.g0 * a2 * s;
+    }
     for (int idx = t; idx < M * M; idx += blockDim.x) {
         int a = idx / M, b = idx - a * M;
         double s = 0.0;
@@ -762,7 +817,8 @@ __global__ void __launch_bounds__(256) k_expand_dense(KBand K, long long r0, lon
     A[(r - r0) * lda + c] = v;
 }
 
-__global__ void k_boundary_cols(KBnd K, long long n, int N, int P, double theta, double rho,
+template <class KL>
+__global__ void k_boundary_cols(KL K, long long n, int N, int P, double theta, double rho,
                                 const double* nodes, const double* mref, double* bnd)
 {
     const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1092,6 +1148,22 @@ void asm_expand_dense(fde_ctx* h, fde_op* op, const double* Krow, const double* 
 void asm_boundary_columns(fde_ctx* h, fde_op* op)
 {
     const int N = op->N, P2 = op->P * op->P;
+    op->bnd.alloc((size_t)2 * op->n);
+    if (op->kb_row && op->e_lo == 0 && op->e_hi >= N) {
+        // one GPU, dense path: every pair (i, 0) and (N-1, i) is already in the band of
+        // pair moments the dense expansion read (same moments, same bits)
+        KBand K;
+        K.row = op->kb_row;
+        K.col = op->kb_col;
+        K.b0 = 0;
+        K.b1 = N - 1;
+        K.N = N;
+        K.P2 = P2;
+        k_boundary_cols<<<(unsigned)ceil_div(op->n, 256), 256, 0, h->stream>>>(
+            K, op->n, N, op->P, op->prob.theta, op->prob.rho, op->tab.nodes.p, op->tab.mref.p, op->bnd.p);
+        FDE_CHECK_LAUNCH();
+        return;
+    }
     // pair list: (i,0) -> slot i ; (N-1, i) -> slot N+i
     std::vector<int> li(2 * N), lj(2 * N);
     std::vector<long long> ls(2 * N);
@@ -1107,7 +1179,6 @@ void asm_boundary_columns(fde_ctx* h, fde_op* op)
     dsl.upload(ls.data(), ls.size(), h->stream);
     tab.alloc((size_t)2 * N * P2);
     asm_k_list(h, op, di.p, dj.p, dsl.p, 2 * N, tab.p);
-    op->bnd.alloc((size_t)2 * op->n);
     KBnd K{tab.p, N, P2};
     k_boundary_cols<<<(unsigned)ceil_div(op->n, 256), 256, 0, h->stream>>>(
         K, op->n, N, op->P, op->prob.theta, op->prob.rho, op->tab.nodes.p, op->tab.mref.p, op->bnd.p);

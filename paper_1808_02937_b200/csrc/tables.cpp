@@ -7,6 +7,10 @@
 // are the constants behind the Gauss-Legendre / Gauss-Jacobi rules the
 // assembly kernels use for the singular kernel |t-s|^{1-alpha}.
 #include <cmath>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <tuple>
 #include <vector>
 
 #include "fde_internal.h"
@@ -87,7 +91,28 @@ void gauss_legendre(int n, std::vector<double>& x, std::vector<double>& w)
 
 void gauss_jacobi(int n, double a, double b, std::vector<double>& x, std::vector<double>& w)
 {
+    // memoised per (n, a, b): a rule is a pure function of them, and the Sturm
+    // bisection of the Jacobi matrix in long double took ~40 us of host time per rule
+    // at the start of every assembly (the device waited for it)
+    typedef std::tuple<int, unsigned long long, unsigned long long> Key;
+    static std::mutex mu;
+    static std::map<Key, std::pair<std::vector<double>, std::vector<double>>> memo;
+    unsigned long long ua, ub;
+    std::memcpy(&ua, &a, sizeof ua);
+    std::memcpy(&ub, &b, sizeof ub);
+    const Key key(n, ua, ub);
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = memo.find(key);
+        if (it != memo.end()) {
+            x = it->second.first;
+            w = it->second.second;
+            return;
+        }
+    }
     gauss_from_jacobi(n, (ld)a, (ld)b, x, w);
+    std::lock_guard<std::mutex> lk(mu);
+    if (memo.size() < 4096) memo.emplace(key, std::make_pair(x, w));
 }
 
 }  // namespace fdeq
