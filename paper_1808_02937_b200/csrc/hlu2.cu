@@ -2184,20 +2184,31 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
     int nlaunch = 0;
     // FDE_DEBUG_SERIAL: synchronise after every launch and name the first failing one
     const bool dbg_serial = getenv("FDE_DEBUG_SERIAL") != nullptr;
+    // debug switches in __device__ variables: copied only when they change (a copy from
+    // pageable host memory waits for the stream to drain -- here, for the assembly and
+    // the H-matrix build -- so the host could not run ahead into the first steps)
     {
+        static int set_dev[64] = {};   // per device: 1 + (check << 1) + (serial << 2)
         const int on = getenv("FDE_H2_CHECK") ? 1 : 0;
-        const char* lo[4] = {(const char*)A, (const char*)hm->dense.p, (const char*)hm->lr.p, nullptr};
-        const char* hi[4] = {(const char*)(A + words), (const char*)(hm->dense.p + hm->dense.n),
-                             (const char*)(hm->lr.p + hm->lr.n), nullptr};
-        FDE_CUDA(cudaMemcpyToSymbolAsync(g_h2_check, &on, sizeof(int), 0, cudaMemcpyHostToDevice, sa));
-        FDE_CUDA(cudaMemcpyToSymbolAsync(g_h2_lo, lo, sizeof(lo), 0, cudaMemcpyHostToDevice, sa));
-        FDE_CUDA(cudaMemcpyToSymbolAsync(g_h2_hi, hi, sizeof(hi), 0, cudaMemcpyHostToDevice, sa));
-    }
-    {
         const int chk = dbg_serial ? 1 : 0;
-        FDE_CUDA(cudaMemcpyToSymbolAsync(g_trunc_check, &chk, sizeof(int), 0, cudaMemcpyHostToDevice, sa));
-        static const double jeps = getenv("FDE_TRUNC_JEPS") ? atof(getenv("FDE_TRUNC_JEPS")) : 0.0;
-        FDE_CUDA(cudaMemcpyToSymbolAsync(g_trunc_jeps, &jeps, sizeof(double), 0, cudaMemcpyHostToDevice, sa));
+        int dev = 0;
+        FDE_CUDA(cudaGetDevice(&dev));
+        const int state = 1 + (on << 1) + (chk << 2);
+        if (on) {   // (the bounds checks need this factorisation's arena: every time)
+            const char* lo[4] = {(const char*)A, (const char*)hm->dense.p, (const char*)hm->lr.p, nullptr};
+            const char* hi[4] = {(const char*)(A + words), (const char*)(hm->dense.p + hm->dense.n),
+                                 (const char*)(hm->lr.p + hm->lr.n), nullptr};
+            FDE_CUDA(cudaMemcpyToSymbolAsync(g_h2_lo, lo, sizeof(lo), 0, cudaMemcpyHostToDevice, sa));
+            FDE_CUDA(cudaMemcpyToSymbolAsync(g_h2_hi, hi, sizeof(hi), 0, cudaMemcpyHostToDevice, sa));
+        }
+        if (set_dev[dev & 63] != state) {
+            FDE_CUDA(cudaMemcpyToSymbolAsync(g_h2_check, &on, sizeof(int), 0, cudaMemcpyHostToDevice, sa));
+            FDE_CUDA(cudaMemcpyToSymbolAsync(g_trunc_check, &chk, sizeof(int), 0, cudaMemcpyHostToDevice, sa));
+            static const double jeps = getenv("FDE_TRUNC_JEPS") ? atof(getenv("FDE_TRUNC_JEPS")) : 0.0;
+            FDE_CUDA(cudaMemcpyToSymbolAsync(g_trunc_jeps, &jeps, sizeof(double), 0, cudaMemcpyHostToDevice, sa));
+            FDE_CUDA(cudaStreamSynchronize(sa));   // (the host values are stack / static: copied before use)
+            set_dev[dev & 63] = state;
+        }
     }
     int dbg_step = -1;
     auto dbg = [&](const char* what) {
