@@ -2818,6 +2818,17 @@ __device__ void pf_phase_A(const SweepDev& S, const SLeaf& L, const double* x, l
     const int W = L.wA;
     const int nseg = L.s_hi - L.s_lo;
     const bool ssm = W * nrhs <= PF_CAP_S;
+    // this thread's x entries for the z store at the end, loaded now (their L2 round
+    // trip overlaps the source gather instead of following the row sums)
+    double xr[RC];
+    {
+        int nrp0 = 1;
+        while (nrp0 < R.nr) nrp0 <<= 1;
+        const int T0 = PF_THREADS / nrp0, row0 = threadIdx.x / T0, li0 = threadIdx.x % T0;
+#pragma unroll
+        for (int c = 0; c < RC; ++c)
+            xr[c] = (c < nrhs && row0 < R.nr && li0 == 0) ? ldcg(x + (long long)c * ldx + L.r0 + R.r_lo + row0) : 0.0;
+    }
     if (ssm) {
         for (int e0 = threadIdx.x; e0 < W * nrhs; e0 += 4 * PF_THREADS) {
             double val[4];
@@ -2868,7 +2879,7 @@ __device__ void pf_phase_A(const SweepDev& S, const SLeaf& L, const double* x, l
         const double sum = pf_group_sum(acc[c], T, red);
         if (row < R.nr && li == 0) {
             const int grow = R.r_lo + row;
-            z[(long long)c * L.m + grow] = ldcg(x + (long long)c * ldx + L.r0 + grow) - sum;
+            z[(long long)c * L.m + grow] = xr[c] - sum;
         }
     }
 }
