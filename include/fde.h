@@ -17,8 +17,9 @@
  *  - Vector pointers are DEVICE pointers owned by the caller (e.g. torch
  *    tensors); the library never frees them.  Host pointers are marked (host).
  *  - Every call is ordered on the handle's CUDA stream; nothing synchronises
- *    the host except solve (returns after convergence) and calls that
- *    return host data.
+ *    the host except solve (returns after convergence), hlu_factor (returns
+ *    once the factorisation has finished, so that a zero pivot or a rank
+ *    overflow is its return value) and calls that return host data.
  *  - Opaque objects are created by the library and released with the
  *    matching fde_free_* call.  Mesh nodes are copied.  Lifetimes: an
  *    fde_hmatrix keeps a pointer to the fde_operator it was built from, and an
@@ -279,7 +280,10 @@ int fde_hmatrix_dense_paper(fde_handle h, fde_hmatrix hm, double* out, int64_t l
  * (Fig. fig:HLU); formatted arithmetic with per-block
  * truncation sigma_i <= tol sigma_1 (reading A12); tol = 0 keeps every rank
  * (exact up to rounding; rank capacity permitting).  No pivoting
- * (coercivity, Theorem 2.1).  Does not modify hm. */
+ * (coercivity, Theorem 2.1).  Does not modify hm.  Returns after the device
+ * work: FDE_ESINGULAR_PIVOT for a zero / non-finite pivot of a diagonal tile,
+ * FDE_ERANK when a truncated rank exceeds the block capacity (the host-side
+ * planning overlaps the device work queued before the call). */
 int hlu_factor(fde_handle h, fde_hmatrix hm, double tol, fde_hlu* out);
 
 typedef struct {
