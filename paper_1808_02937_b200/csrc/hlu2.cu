@@ -264,7 +264,9 @@ __device__ void h2_panel_inv_body(const H2Panel& p, double* psm)
     // op is staged in chunks of H2_PCH columns, double-buffered (the next chunk's
     // copies are in flight while one is multiplied; small shared footprint: the
     // CTA has to fit beside the bulk-update GEMMs of the previous step)
-    const int m = p.m, ldT = (m & 1) ? m + 2 : m + 1, ldB = ldT;
+    // strides = 4 (mod 16) doubles: the DMMA fragment loads (lane = 4 row + k, 16 lanes
+    // per 128-byte wavefront) hit 16 distinct bank pairs (m + 1 = 129: up to 4-way conflicts)
+    const int m = p.m, ldT = m + (20 - m % 16) % 16, ldB = ldT;
     double* Bs = psm;                 // vector c, element i at Bs[c * ldB + i]
     double* Ts = psm + H2_STRIP * ldB;   // Ts[qq * ldT + i] = op(i, q0 + qq)
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -2165,7 +2167,7 @@ static bool hlu2_factor(fde_lu* L, fde_hm* hm)
     // of step k, which overlap LU(k+1) and the panels of step k+1 (lookahead).
     const int pan_smem = (H2_STRIP + 64) * (H2_MMAX + 2) * (int)sizeof(double);   // (two 32-column block panels)
     set_smem_once((const void*)k_h2_panel, pan_smem);
-    const int pan_smem_inv = (H2_STRIP + 2 * H2_PCH) * (H2_MMAX + 2) * (int)sizeof(double);   // (double-buffered op)
+    const int pan_smem_inv = (H2_STRIP + 2 * H2_PCH) * (H2_MMAX + 16) * (int)sizeof(double);   // (double-buffered op)
     const int lu_smem = H2_MMAX * (H2_MMAX + 1) * (int)sizeof(double);   // padded 128 x 129
     set_smem_once((const void*)k_h2_lu, lu_smem);
     static const bool use_dmma = !getenv("FDE_H2_NODMMA");
