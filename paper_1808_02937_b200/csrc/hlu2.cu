@@ -521,7 +521,10 @@ __global__ void __launch_bounds__(256) k_h2_panel(const H2Panel* P)
 #ifndef H2G_MINB
 #define H2G_MINB 4    // __launch_bounds__ minimum CTAs per SM of k_h2_gemm
 #endif
-#define H2G_SMEM(TM, TN) (H2G_ST * GK * ((TM) + (TN) + 2) * (int)sizeof(double))
+#ifndef H2G_PAD
+#define H2G_PAD 4     // row padding of the staged operand slices: 4 (mod 16) doubles, conflict-free fragment loads
+#endif
+#define H2G_SMEM(TM, TN) (H2G_ST * GK * ((TM) + (TN) + 2 * H2G_PAD) * (int)sizeof(double))
 struct H2Cursor {   // position in the (term, slice) sequence of a tile
     int q, k0;
 };
@@ -546,7 +549,7 @@ __device__ __forceinline__ void h2_stage(const H2Term& T, int m0, int n0, int m,
         int kk, mm;
         if (T.ta) { mm = t / GK; kk = t % GK; } else { kk = t / TM; mm = t % TM; }
         const int gi = m0 + mm, gk = k0 + kk;
-        double* da = sA + kk * (TM + 1) + mm;
+        double* da = sA + kk * (TM + H2G_PAD) + mm;
         if (gi < m && gk < T.k) cp_async8(da, T.ta ? T.A + (long long)gi * T.lda + gk : T.A + (long long)gk * T.lda + gi);
         else *da = 0.0;
     }
@@ -558,7 +561,7 @@ __device__ __forceinline__ void h2_stage(const H2Term& T, int m0, int n0, int m,
         int kk, nn;
         if (T.tb) { kk = t / TN; nn = t % TN; } else { nn = t / GK; kk = t % GK; }
         const int gj = n0 + nn, gk2 = k0 + kk;
-        double* db = sB + kk * (TN + 1) + nn;
+        double* db = sB + kk * (TN + H2G_PAD) + nn;
         if (gj < n && gk2 < T.k) cp_async8(db, T.tb ? T.B + (long long)gk2 * T.ldb + gj : T.B + (long long)gj * T.ldb + gk2);
         else *db = 0.0;
     }
@@ -577,8 +580,8 @@ __device__ __forceinline__ void h2_gemm_tile(const H2Tile* tiles, int tile, cons
     constexpr int FM = TM / (8 * WM), FN = TN / (8 * WN);   // DMMA fragments per warp
     static_assert(FM >= 1 && FN >= 1 && WM * WN <= 8, "warp grid");
     extern __shared__ double gsm[];   // H2G_SMEM bytes: [stage] A slice, [stage] B slice
-    double (*sA)[GK * (TM + 1)] = reinterpret_cast<double (*)[GK * (TM + 1)]>(gsm);
-    double (*sB)[GK * (TN + 1)] = reinterpret_cast<double (*)[GK * (TN + 1)]>(gsm + H2G_ST * GK * (TM + 1));
+    double (*sA)[GK * (TM + H2G_PAD)] = reinterpret_cast<double (*)[GK * (TM + H2G_PAD)]>(gsm);
+    double (*sB)[GK * (TN + H2G_PAD)] = reinterpret_cast<double (*)[GK * (TN + H2G_PAD)]>(gsm + H2G_ST * GK * (TM + H2G_PAD));
     __shared__ double sAlpha[H2G_ST];
     __shared__ H2Term sT[H2G_TMAX];   // the task's term descriptors (one global read each)
     const H2Tile tl = tiles[tile];
@@ -687,7 +690,7 @@ __device__ __forceinline__ void h2_gemm_tile(const H2Tile* tiles, int tile, cons
             double v = 0.0;
             if (kk < kq && nn < n)
                 for (int r = 0; r < rows; ++r) v = fma(sU[kk * 129 + r], sV[nn * 129 + r], v);
-            sB[0][kk * (TN + 1) + nn] = v;
+            sB[0][kk * (TN + H2G_PAD) + nn] = v;
         }
         __syncthreads();
     }
@@ -715,9 +718,9 @@ __device__ __forceinline__ void h2_gemm_tile(const H2Tile* tiles, int tile, cons
                     double a[FM], b[FN];
                     const int kr = kk + (lane & 3);
 #pragma unroll
-                    for (int i = 0; i < FM; ++i) a[i] = al * a_s[kr * (TM + 1) + wm + i * 8 + (lane >> 2)];
+                    for (int i = 0; i < FM; ++i) a[i] = al * a_s[kr * (TM + H2G_PAD) + wm + i * 8 + (lane >> 2)];
 #pragma unroll
-                    for (int j = 0; j < FN; ++j) b[j] = b_s[kr * (TN + 1) + wn + j * 8 + (lane >> 2)];
+                    for (int j = 0; j < FN; ++j) b[j] = b_s[kr * (TN + H2G_PAD) + wn + j * 8 + (lane >> 2)];
 #pragma unroll
                     for (int i = 0; i < FM; ++i)
 #pragma unroll
@@ -729,9 +732,9 @@ __device__ __forceinline__ void h2_gemm_tile(const H2Tile* tiles, int tile, cons
             for (int kk = 0; kk < GK; ++kk) {
                 double a[RM], b[RN];
 #pragma unroll
-                for (int i = 0; i < RM; ++i) a[i] = al * a_s[kk * (TM + 1) + tx + 16 * i];
+                for (int i = 0; i < RM; ++i) a[i] = al * a_s[kk * (TM + H2G_PAD) + tx + 16 * i];
 #pragma unroll
-                for (int j = 0; j < RN; ++j) b[j] = b_s[kk * (TN + 1) + ty + 16 * j];
+                for (int j = 0; j < RN; ++j) b[j] = b_s[kk * (TN + H2G_PAD) + ty + 16 * j];
 #pragma unroll
                 for (int i = 0; i < RM; ++i)
 #pragma unroll
