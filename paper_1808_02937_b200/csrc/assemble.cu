@@ -745,7 +745,10 @@ template <int PT>
 __global__ void __launch_bounds__(256) k_expand_tiles(const double* Ktri, long long n, long long lda, int N, double theta,
                                                       double rho, const double* nodes, const double* mref_g, double* A)
 {
-    constexpr int P = PT, P2 = PT * PT, NB = EX_TE + 1;
+    // slot rows padded to P + 1 doubles: the S_l^T reads kb[n (P+1) + m] of 16 consecutive
+    // columns (two elements) then hit 16 distinct bank pairs (stride P: 8-way conflicts,
+    // half of all shared-memory wavefronts of the kernel were replays)
+    constexpr int P = PT, P2 = PT * PT, NB = EX_TE + 1, SP = PT + 1, PS = PT * SP;
     extern __shared__ __align__(16) double ksm[];   // [a][b] slots of P2 doubles
     __shared__ double mref[(PT + 1) * (PT + 1)];
     __shared__ double hh[2 * EX_TE + 2];
@@ -768,7 +771,10 @@ __global__ void __launch_bounds__(256) k_expand_tiles(const double* Ktri, long l
         const int hi = a > b ? a : b, lo = a > b ? b : a;
         double2 v = make_double2(0.0, 0.0);
         if (hi < N) v = reinterpret_cast<const double2*>(Ktri + ((long long)hi * (hi + 1) / 2 + lo) * P2)[w];
-        reinterpret_cast<double2*>(ksm + (long long)slot * P2)[w] = v;
+        const int m = (2 * w) / P, nn = 2 * w - m * P;   // (P even: a pair never straddles a row)
+        double* d = ksm + (long long)slot * PS + m * SP + nn;
+        d[0] = v.x;
+        d[1] = v.y;
     }
     __syncthreads();
     // the two blocks: (rows I, cols J) and, off the diagonal, (rows J, cols I)
@@ -792,9 +798,9 @@ __global__ void __launch_bounds__(256) k_expand_tiles(const double* Ktri, long l
                     const double cf = tr.c[x] * tc.c[y];
                     // slot of the pair (ei, ej): row index from I, column from J (or mirrored)
                     const int sa = blk ? ej - I0 : ei - I0, sb = blk ? ei - J0 : ej - J0;
-                    const double* kb = ksm + (sa * NB + sb) * P2;   // K(max(ei,ej), min(ei,ej))
-                    if (ej <= ei) sl = fma(cf, kb[tr.m[x] * P + tc.m[y]], sl);
-                    if (ei <= ej) slt = fma(cf, kb[tc.m[y] * P + tr.m[x]], slt);
+                    const double* kb = ksm + (sa * NB + sb) * PS;   // K(max(ei,ej), min(ei,ej))
+                    if (ej <= ei) sl = fma(cf, kb[tr.m[x] * SP + tc.m[y]], sl);
+                    if (ei <= ej) slt = fma(cf, kb[tc.m[y] * SP + tr.m[x]], slt);
                     if (ei == ej)
                         mass = fma(hh[blk ? NB + (ei - J0) : (ei - I0)], mref[tr.ml[x] * (P + 1) + tc.ml[y]], mass);
                 }
@@ -1108,7 +1114,7 @@ void asm_expand_dense(fde_ctx* h, fde_op* op, const double* Krow, const double* 
         if (op->lda > op->n)   // padding columns [n, lda) of every row
             FDE_CUDA(cudaMemset2DAsync(op->A.p + op->n, op->lda * sizeof(double), 0, (op->lda - op->n) * sizeof(double),
                                        op->n, h->stream));
-        const size_t smem = (size_t)(EX_TE + 1) * (EX_TE + 1) * op->P * op->P * sizeof(double);
+        const size_t smem = (size_t)(EX_TE + 1) * (EX_TE + 1) * op->P * (op->P + 1) * sizeof(double);
 #define FDE_EXPAND_T(PT_)                                                                                              do {                                                                                                                   FDE_CUDA(cudaFuncSetAttribute(k_expand_tiles<PT_>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));         k_expand_tiles<PT_><<<ntiles, 256, smem, h->stream>>>(Krow, op->n, op->lda, op->N, op->prob.theta,                                                                     op->prob.rho, op->tab.nodes.p, op->tab.mref.p, op->A.p);     } while (0)
         switch (op->P) {
             case 4: FDE_EXPAND_T(4); break;
